@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path — fine-propagator fp64 grid-point updates/s.
+
+Workload (BASELINE.json config 5, fine-propagator-only throughput sweep): periodic 2D
+grid, seeded random smooth medium c in [0.5, 1] (sum of 8 low-frequency sinusoids),
+seeded random Gaussian pulses as initial states, 64 velocity-Verlet steps per slice per
+step (= one coupling interval of K1).  A "step" is one batched K1 call over the
+per-GPU batch; slices are sharded across ranks (weak scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--grid 4096] [--batch 64]
+  python bench.py --impl reference      # the reference's propagate_coupling on host cores
+
+One JSON line (rank 0).  Timing: CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks.  Inputs (>= 1 GiB) exceed the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fine-propagator fp64 grid-pt updates/s"
+FLOPS_PER_UPDATE = 17  # Laplacian 9, x c^2 1, u-update 4, udot-update 3
+STEPS_PER_COUPLING = 64
+
+
+def medium(n: int, seed: int) -> np.ndarray:
+    """cfg5 medium: c = 0.75 + 0.25 S/max|S|, S = sum of 8 sinusoids, wavenumbers 1..4."""
+    rng = np.random.default_rng(seed)
+    y, x = np.meshgrid(np.arange(n) / n, np.arange(n) / n, indexing="ij")
+    s = np.zeros((n, n))
+    for _ in range(8):
+        ky, kx = rng.integers(1, 5, 2)
+        s += rng.uniform(0.2, 1.0) * np.sin(2 * np.pi * (ky * y + kx * x) + rng.uniform(0, 2 * np.pi))
+    return 0.75 + 0.25 * s / np.max(np.abs(s))
+
+
+def pulses(n: int, batch: int, seed: int) -> np.ndarray:
+    """cfg5 initial states: exp(-w |x - x0|^2), x0 ~ U[0,1)^2 (periodic distance), w ~ U[200, 2000]."""
+    rng = np.random.default_rng(seed)
+    ax = np.arange(n) / n
+    out = np.empty((batch, n, n))
+    for b in range(batch):
+        y0, x0 = rng.random(2)
+        w = rng.uniform(200, 2000)
+        dy = np.minimum(np.abs(ax - y0), 1 - np.abs(ax - y0))[:, None]
+        dx = np.minimum(np.abs(ax - x0), 1 - np.abs(ax - x0))[None, :]
+        out[b] = np.exp(-w * (dy * dy + dx * dx))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args, rank, world):
+    """The reference's propagate_coupling (propagator.cpp, compiled verbatim in oracle/_ref)
+    over a bounded sample of the same workload on all host cores."""
+    if rank != 0:
+        return
+    from oracle import refbind
+    from oracle.paratime_np import Grid
+
+    n = args.grid
+    cores = os.cpu_count() or 1
+    sample_slices = cores  # one slice per std::thread worker (parareal.cpp:25-47 partition)
+    g = Grid((n, n), (1.0 / n, 1.0 / n))
+    c = medium(n, 7)
+    dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
+    u0 = pulses(n, sample_slices, 11)
+    v0 = np.zeros_like(u0)
+    steps = max(1, args.ref_steps)
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        refbind.propagate(u0, v0, c, g, dt, steps, workers=cores)
+        t1 = time.perf_counter()
+        if k >= args.warmup:
+            times.append(t1 - t0)
+    per = float(np.mean(times))
+    value = sample_slices * n * n * steps / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "grid-pt updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg5 medium/pulses)",
+        "config": {"workload": f"cfg5 fine propagator {n}x{n}, {steps} Verlet steps per slice",
+                   "sample": f"{sample_slices} slices x {steps} steps per step (bounded CPU sample)"},
+        "cpu_baseline": {"value": value, "unit": "grid-pt updates/s", "cores": cores, "kind": "reference",
+                         "sample": f"{sample_slices} slices of {n}^2 x {steps} steps, propagate_coupling "
+                                   f"(propagator.cpp verbatim, -O3, std::thread x{cores})"},
+        "e2e": {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(n, steps=8):
+    """Same as the reference arm, small and quick, for the `cpu_baseline` key (rank 0, N=1)."""
+    try:
+        from oracle import refbind
+        from oracle.paratime_np import Grid
+
+        if not refbind.LIB_PATH.exists():
+            return None
+        cores = os.cpu_count() or 1
+        g = Grid((n, n), (1.0 / n, 1.0 / n))
+        c = medium(n, 7)
+        dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
+        u0 = pulses(n, cores, 11)
+        v0 = np.zeros_like(u0)
+        refbind.propagate(u0[:1], v0[:1], c, g, dt, 1, workers=1)  # warm
+        t0 = time.perf_counter()
+        refbind.propagate(u0, v0, c, g, dt, steps, workers=cores)
+        dt_s = time.perf_counter() - t0
+        return {"value": cores * n * n * steps / dt_s, "unit": "grid-pt updates/s", "cores": cores,
+                "kind": "reference",
+                "sample": f"{cores} slices of {n}^2 x {steps} steps through the reference's propagate_coupling "
+                          f"(oracle/_ref, propagator.cpp verbatim) on std::thread x{cores}"}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "error": str(e)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--grid", type=int, default=2048)
+    ap.add_argument("--batch", type=int, default=64, help="slices per GPU")
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--ref-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also time the cfg5 grid sweep")
+    args = ap.parse_args()
+
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    import paratime_b200 as B
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    n, batch = args.grid, args.batch
+    mode = B.FAST if args.mode == "fast" else B.EXACT
+    ctx = B.Context(local)
+    c = medium(n, 7)
+    dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
+    grid = B.Grid((n, n), (1.0 / n, 1.0 / n))
+    prop = B.Propagator(ctx, grid, c, dt, STEPS_PER_COUPLING)
+    # each rank owns its own contiguous block of slices (seeded by global slice index)
+    u_host = pulses(n, batch, 1000 + rank)
+    u = torch.as_tensor(u_host, device=f"cuda:{local}")
+    v = torch.zeros_like(u)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        prop.propagate(u, v, mode=mode)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    l0 = ctx.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches() - l0
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    updates = world * batch * n * n * STEPS_PER_COUPLING * args.steps
+    value = updates / (ms * 1e-3)
+    ms_per_step = ms / args.steps
+    finite = bool(torch.isfinite(u).all().item() and torch.isfinite(v).all().item())
+
+    # roofline: live fp64 FMA peak on this GPU; dominant kernel = the wavefront K1 pass
+    tflops_peak, _ = probe_fp64(ctx)
+    per_launch_ms = ms / max(launches, 1)
+    launches_per_step = launches / args.steps
+    steps_per_launch = STEPS_PER_COUPLING / launches_per_step
+    flops_per_launch = batch * n * n * steps_per_launch * FLOPS_PER_UPDATE
+    achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
+    hbm_bytes_per_launch = batch * n * n * 40.0  # read u, udot, coef; write u, udot (8 B each)
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(B, prop, u_host, mode, args.e2e_steps, local, dist, world)
+
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        except Exception:
+            pass
+        line = {
+            "metric": METRIC, "value": value, "unit": "grid-pt updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg5 medium and Gaussian pulses)",
+            "config": {"workload": f"cfg5 fine propagator {n}x{n} periodic, {batch} slices/GPU x "
+                                   f"{STEPS_PER_COUPLING} velocity-Verlet steps per step ({args.mode} mode)",
+                       "grid": n, "slices_per_gpu": batch, "steps_per_slice": STEPS_PER_COUPLING,
+                       "parallelism": f"slice-sharded x{world}", "l2": "inputs > L2 (no flush needed)",
+                       "finite": finite},
+            "gpu_launches": launches,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": tflops_peak, "unit": "TFLOP/s",
+                         "frac": achieved / tflops_peak if tflops_peak else None, "traffic": None,
+                         "peak_source": "measured live: DFMA probe (ptb_probe_fp64_peak)",
+                         "kernel": "k_wave<8,FAST>", "per_launch_ms": per_launch_ms,
+                         "flops_per_update": FLOPS_PER_UPDATE, "steps_per_launch": steps_per_launch,
+                         "hbm_algorithmic_GBps": hbm_bytes_per_launch / (per_launch_ms * 1e-3) / 1e9,
+                         "hbm_peak_GBps": peaks.get("hbm_gbs")},
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+        }
+        if world == 1:
+            line["cpu_baseline"] = cpu_baseline_sample(n)
+        if args.sweep:
+            line["sweep"] = sweep(B, ctx, mode)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def probe_fp64(ctx):
+    import ctypes
+
+    import paratime_b200 as B
+
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    B.api.check(B.lib().ptb_probe_fp64_peak(ctx.h, ctypes.byref(tf), ctypes.byref(ms)))
+    return tf.value, ms.value
+
+
+def measure_e2e(B, prop, u_host, mode, steps, local, dist, world):
+    """Same metric through the C-ABI host-buffer call: H2D inputs, K1, D2H results per step."""
+    import ctypes
+
+    import torch
+
+    batch = u_host.shape[0]
+    n = u_host.shape[1]
+    uh = torch.from_numpy(u_host).pin_memory()
+    vh = torch.zeros_like(uh).pin_memory()
+    ou = torch.empty_like(uh).pin_memory()
+    ov = torch.empty_like(uh).pin_memory()
+    flags = np.zeros(batch, dtype=np.int32)
+    dp = ctypes.POINTER(ctypes.c_double)
+
+    def call():
+        B.api.check(B.lib().ptb_propagate_batch_host(
+            prop.h, ctypes.c_size_t(batch), ctypes.cast(uh.data_ptr(), dp), ctypes.cast(vh.data_ptr(), dp),
+            ctypes.cast(ou.data_ptr(), dp), ctypes.cast(ov.data_ptr(), dp),
+            flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.c_int(mode)))
+
+    call()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    el = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([el], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    value = world * batch * n * n * STEPS_PER_COUPLING * steps / el
+    return {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": int(2 * uh.numel() * 8),
+            "d2h_bytes_per_step": int(2 * uh.numel() * 8 + batch * 4), "ms_per_step": el / steps * 1e3,
+            "api": "ptb_propagate_batch_host (pinned host buffers, 2-stream chunked copies)"}
+
+
+def sweep(B, ctx, mode):
+    """cfg5 grid sweep (128^2 .. 4096^2), device-resident, FAST mode."""
+    import torch
+
+    out = []
+    for n, batch in ((128, 512), (512, 256), (1024, 64), (4096, 16)):
+        c = medium(n, 7)
+        dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
+        prop = B.Propagator(ctx, B.Grid((n, n), (1.0 / n, 1.0 / n)), c, dt, STEPS_PER_COUPLING)
+        u = torch.as_tensor(pulses(n, batch, 5), device="cuda")
+        v = torch.zeros_like(u)
+        for _ in range(2):
+            prop.propagate(u, v, mode=mode)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        reps = 3
+        for _ in range(reps):
+            prop.propagate(u, v, mode=mode)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out.append({"grid": n, "batch": batch, "ms": ms, "updates_per_s": batch * n * n * STEPS_PER_COUPLING / (ms * 1e-3)})
+        del u, v, prop
+    return out
+
+
+if __name__ == "__main__":
+    main()

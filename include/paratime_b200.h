@@ -1,0 +1,130 @@
+/*
+ * paratime_b200 — C ABI of the B200 (sm_100a) hot path of data-driven theta-parareal
+ * for u_tt = c^2(x) Lap u on periodic 1D/2D boxes (arXiv 1905.00473).
+ *
+ * The reference ("paratime", /root/reference/proj) has no FFI; its boundary is the C++
+ * header API in proj/include/paratime/*.hpp.  This header is the thin extern "C" layer
+ * the C++ drop-in (include/paratime/*.hpp, same namespace and signatures) and any
+ * foreign binding (ctypes) call.  Plain pointers and sizes only.
+ *
+ * Conventions (mirroring proj/include/paratime/grid.hpp:8-13):
+ *   - fields are flat row-major fp64 arrays, 2D axis 0 = y (slow), axis 1 = x (fast);
+ *   - a batch of B states is slice-major SoA: u[b*N + i], udot[b*N + i], N = grid size;
+ *   - "_dev" pointers are device (HBM) addresses on the context's device, "_host"
+ *     pointers are host memory (pinned or pageable);
+ *   - every call is stream-ordered on the context stream; *_host calls synchronise.
+ * Errors: a ptb_status is returned and a thread-local message is kept
+ * (ptb_last_error).  The C++ layer rethrows the reference's exception types:
+ *   PTB_INVALID_ARGUMENT -> std::invalid_argument, PTB_DIVERGED -> PropagationDiverged,
+ *   PTB_DOMAIN -> std::domain_error, others -> std::runtime_error.
+ */
+#ifndef PARATIME_B200_H_
+#define PARATIME_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PTB_OK = 0,
+  PTB_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  PTB_DIVERGED = 2,         /* PropagationDiverged (errors.hpp:9-12)   */
+  PTB_DOMAIN = 3,           /* std::domain_error (energy_map.cpp:233)   */
+  PTB_CUDA = 4,             /* CUDA runtime / cuBLAS failure            */
+  PTB_NCCL = 5,             /* collective failure                       */
+  PTB_UNSUPPORTED = 6
+} ptb_status;
+
+/* Grid (grid.hpp:16-38): dim 1 or 2; n[0]/h[0] = axis 0 (y in 2D, the only axis in 1D). */
+typedef struct {
+  int dim;
+  size_t n[2];
+  double h[2];
+} ptb_grid;
+
+/* Propagator arithmetic.  EXACT reproduces propagator.cpp:31-73 operation by operation
+ * (no FMA contraction) and is bitwise equal to the reference; FAST is the same velocity
+ * Verlet in kick-drift-kick form with fused multiply-adds (parity <= 1e-12 rel. L2). */
+typedef enum { PTB_MODE_FAST = 0, PTB_MODE_EXACT = 1 } ptb_mode;
+
+typedef enum { PTB_INTERP_FOURIER = 0, PTB_INTERP_LINEAR = 1 } ptb_interp;     /* grid.hpp:54 */
+typedef enum { PTB_FD2 = 0, PTB_FD4 = 1, PTB_FD6 = 2, PTB_FD8 = 3, PTB_SPECTRAL = 4 } ptb_scheme; /* energy_map.hpp:12 */
+
+typedef struct ptb_context ptb_context;
+typedef struct ptb_propagator ptb_propagator;
+typedef struct ptb_transfer ptb_transfer;
+
+const char* ptb_last_error(void);
+const char* ptb_version(void);
+
+/* ---- context: device, stream, workspace --------------------------------------- */
+ptb_status ptb_context_create(int device, ptb_context** out);
+ptb_status ptb_context_destroy(ptb_context* ctx);
+ptb_status ptb_context_synchronize(ptb_context* ctx);
+/* cudaStream_t of the context (as void*); kernels of this context run on it */
+void* ptb_context_stream(ptb_context* ctx);
+/* run this context's work on an external stream (e.g. the caller's current stream);
+ * NULL restores the context's own stream */
+ptb_status ptb_context_set_stream(ptb_context* ctx, void* stream);
+int ptb_context_device(ptb_context* ctx);
+/* number of this library's kernels launched on the context so far */
+uint64_t ptb_context_launches(ptb_context* ctx);
+ptb_status ptb_device_alloc(ptb_context* ctx, size_t bytes, void** out);
+ptb_status ptb_device_free(ptb_context* ctx, void* p);
+ptb_status ptb_memcpy_h2d(ptb_context* ctx, void* dst_dev, const void* src_host, size_t bytes);
+ptb_status ptb_memcpy_d2h(ptb_context* ctx, void* dst_host, const void* src_dev, size_t bytes);
+
+/* ---- propagator (propagator.hpp:12-31) ----------------------------------------- */
+/* PropagatorConfig: validates exactly as propagator.cpp:11-27 (CFL, dt, steps) and
+ * uploads the speed field c (host, N values) plus derived coefficient arrays. */
+ptb_status ptb_propagator_create(ptb_context* ctx, const ptb_grid* grid, const double* c_host,
+                                 double dt, size_t steps_per_coupling, ptb_propagator** out);
+ptb_status ptb_propagator_destroy(ptb_propagator* p);
+/* device speed array (N doubles) owned by the propagator */
+const double* ptb_propagator_speed(ptb_propagator* p);
+
+/* K1: steps_per_coupling Verlet steps on `batch` states in place (device pointers).
+ * nonfinite_dev (nullable, int32[batch]) receives 1 where the result is not finite —
+ * the condition on which propagate_coupling throws (propagator.cpp:102-103). */
+ptb_status ptb_propagate_batch(ptb_propagator* p, size_t batch, double* u_dev, double* udot_dev,
+                               int32_t* nonfinite_dev, int mode);
+/* same with an explicit step count (used for `step`, propagator.cpp:85-93) */
+ptb_status ptb_propagate_steps_batch(ptb_propagator* p, size_t steps, size_t batch, double* u_dev,
+                                     double* udot_dev, int32_t* nonfinite_dev, int mode);
+/* propagate_coupling on host buffers (one state); PTB_DIVERGED when not finite. */
+ptb_status ptb_propagate_coupling_host(ptb_propagator* p, const double* u_in, const double* udot_in,
+                                       double* u_out, double* udot_out, int mode);
+/* batched propagate_coupling on HOST buffers: H2D copy, K1, D2H copy, all stream-ordered
+ * and chunked so copies of one chunk overlap the kernel of another.  nonfinite_host
+ * (nullable, int32[batch]) gets the per-slice divergence flags. */
+ptb_status ptb_propagate_batch_host(ptb_propagator* p, size_t batch, const double* u_in, const double* udot_in,
+                                    double* u_out, double* udot_out, int32_t* nonfinite_host, int mode);
+/* laplacian (propagator.cpp:31-58, reference operation order) */
+ptb_status ptb_laplacian_batch(ptb_context* ctx, const ptb_grid* grid, size_t batch,
+                               const double* f_dev, double* out_dev);
+
+/* ---- grid transfer (grid.hpp:56-89) ----------------------------------------------- */
+ptb_status ptb_transfer_create(ptb_context* ctx, const ptb_grid* coarse, const ptb_grid* fine,
+                               int kind, ptb_transfer** out);
+ptb_status ptb_transfer_destroy(ptb_transfer* t);
+/* restrict_field: out[j] = in[ratio*j]; `batch` fields, slice-major */
+ptb_status ptb_restrict_batch(ptb_transfer* t, size_t batch, const double* fine_dev, double* coarse_dev);
+/* interpolate_field (trigonometric with split Nyquist, or periodic linear) */
+ptb_status ptb_interpolate_batch(ptb_transfer* t, size_t batch, const double* coarse_dev, double* fine_dev);
+/* finite check of `batch` fields of n values each; flags_dev[b] |= 1 when any is non-finite */
+ptb_status ptb_nonfinite_batch(ptb_context* ctx, size_t n, size_t batch, const double* f_dev,
+                               int32_t* flags_dev);
+
+/* ---- measurement helpers (bench.py) ---------------------------------------------- */
+/* Peak fp64 FMA throughput of the device: independent DFMA chains on every SM, timed
+ * with CUDA events; returns TFLOP/s (2 flops per FMA) and the kernel time. */
+ptb_status ptb_probe_fp64_peak(ptb_context* ctx, double* tflops, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARATIME_B200_H_ */

@@ -1,0 +1,214 @@
+"""ctypes binding of libparatime_b200.so (include/paratime_b200.h).
+
+Device memory is owned by torch tensors (plumbing); the library only sees raw
+pointers.  The context runs on torch's current CUDA stream so library kernels and
+torch ops are stream-ordered.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+LIB = Path(__file__).resolve().parent / "libparatime_b200.so"
+
+OK, INVALID_ARGUMENT, DIVERGED, DOMAIN, CUDA_ERR, NCCL_ERR, UNSUPPORTED = range(7)
+FAST, EXACT = 0, 1
+FOURIER, LINEAR = 0, 1
+FD2, FD4, FD6, FD8, SPECTRAL = range(5)
+
+_lib = None
+
+
+class PtbError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[ptb status {status}] {msg}")
+        self.status = status
+
+
+class _Grid(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n", C.c_size_t * 2), ("h", C.c_double * 2)]
+
+
+def lib_path() -> Path:
+    return LIB
+
+
+def lib():
+    """Load the CUDA library; raises (no fallback) when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            raise ImportError(f"{LIB} is missing — build it with `python -m paratime_b200.build`")
+        _lib = C.CDLL(str(LIB))
+        _lib.ptb_last_error.restype = C.c_char_p
+        _lib.ptb_version.restype = C.c_char_p
+        _lib.ptb_context_stream.restype = C.c_void_p
+        _lib.ptb_context_launches.restype = C.c_uint64
+        _lib.ptb_propagator_speed.restype = C.c_void_p
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != OK:
+        raise PtbError(status, lib().ptb_last_error().decode())
+
+
+@dataclass(frozen=True)
+class Grid:
+    """grid.hpp:16-38 — n/h per axis, axis 0 = y in 2D."""
+
+    n: Tuple[int, ...]
+    h: Tuple[float, ...]
+
+    @property
+    def dim(self) -> int:
+        return len(self.n)
+
+    @property
+    def shape(self):
+        return tuple(self.n)
+
+    @property
+    def size(self) -> int:
+        return int(np.prod(self.n))
+
+    def c(self) -> _Grid:
+        g = _Grid()
+        g.dim = self.dim
+        g.n[0], g.n[1] = self.n[0], (self.n[1] if self.dim == 2 else 1)
+        g.h[0], g.h[1] = self.h[0], (self.h[1] if self.dim == 2 else 1.0)
+        return g
+
+    @staticmethod
+    def of(g) -> "Grid":
+        return Grid(tuple(int(x) for x in g.n), tuple(float(x) for x in g.h))
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(None)
+
+
+class Context:
+    """ptb_context: device + stream + scratch.  Follows torch's current stream."""
+
+    def __init__(self, device: int = 0):
+        import torch
+
+        self.torch = torch
+        self.device = device
+        h = C.c_void_p()
+        check(lib().ptb_context_create(C.c_int(device), C.byref(h)))
+        self.h = h
+        self.follow_torch_stream()
+
+    def follow_torch_stream(self):
+        s = self.torch.cuda.current_stream(self.device).cuda_stream
+        check(lib().ptb_context_set_stream(self.h, C.c_void_p(s)))
+
+    def launches(self) -> int:
+        return int(lib().ptb_context_launches(self.h))
+
+    def synchronize(self):
+        check(lib().ptb_context_synchronize(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ptb_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # helpers
+    def tensor(self, a, dtype=None):
+        t = self.torch.as_tensor(np.ascontiguousarray(a), dtype=dtype or self.torch.float64)
+        return t.to(f"cuda:{self.device}")
+
+    def laplacian(self, grid: Grid, f):
+        batch = f.numel() // grid.size
+        out = self.torch.empty_like(f)
+        check(lib().ptb_laplacian_batch(self.h, C.byref(grid.c()), C.c_size_t(batch), _ptr(f), _ptr(out)))
+        return out
+
+    def nonfinite(self, f, n: int):
+        batch = f.numel() // n
+        flags = self.torch.zeros(batch, dtype=self.torch.int32, device=f.device)
+        check(lib().ptb_nonfinite_batch(self.h, C.c_size_t(n), C.c_size_t(batch), _ptr(f), _ptr(flags)))
+        return flags
+
+
+class Propagator:
+    """PropagatorConfig (propagator.hpp:12-21) living on the device."""
+
+    def __init__(self, ctx: Context, grid: Grid, c, dt: float, steps: int):
+        self.ctx, self.grid, self.dt, self.steps = ctx, grid, float(dt), int(steps)
+        c = np.ascontiguousarray(c, dtype=np.float64).reshape(-1)
+        if c.size != grid.size:
+            raise PtbError(INVALID_ARGUMENT, "SpeedField: field size does not match grid")
+        h = C.c_void_p()
+        check(lib().ptb_propagator_create(ctx.h, C.byref(grid.c()), c.ctypes.data_as(C.POINTER(C.c_double)),
+                                          C.c_double(dt), C.c_size_t(steps), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ptb_propagator_destroy(self.h)
+        except Exception:
+            pass
+
+    def propagate(self, u, udot, mode: int = FAST, steps: Optional[int] = None, flags=None):
+        """In place on device tensors (batch, *grid.shape) or grid.shape."""
+        batch = u.numel() // self.grid.size
+        if steps is None:
+            check(lib().ptb_propagate_batch(self.h, C.c_size_t(batch), _ptr(u), _ptr(udot), _ptr(flags), C.c_int(mode)))
+        else:
+            check(lib().ptb_propagate_steps_batch(self.h, C.c_size_t(steps), C.c_size_t(batch), _ptr(u), _ptr(udot),
+                                                  _ptr(flags), C.c_int(mode)))
+        return u, udot
+
+    def propagate_host(self, u: np.ndarray, udot: np.ndarray, mode: int = FAST):
+        """propagate_coupling on host arrays; raises PtbError(DIVERGED) like the reference."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        udot = np.ascontiguousarray(udot, dtype=np.float64)
+        uo, vo = np.empty_like(u), np.empty_like(udot)
+        dp = C.POINTER(C.c_double)
+        check(lib().ptb_propagate_coupling_host(self.h, u.ctypes.data_as(dp), udot.ctypes.data_as(dp),
+                                                uo.ctypes.data_as(dp), vo.ctypes.data_as(dp), C.c_int(mode)))
+        return uo, vo
+
+
+class Transfer:
+    """GridTransfer (grid.hpp:56-67): restriction and interpolation on the device."""
+
+    def __init__(self, ctx: Context, coarse: Grid, fine: Grid, kind: int = FOURIER):
+        self.ctx, self.coarse, self.fine, self.kind = ctx, coarse, fine, kind
+        h = C.c_void_p()
+        check(lib().ptb_transfer_create(ctx.h, C.byref(coarse.c()), C.byref(fine.c()), C.c_int(kind), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ptb_transfer_destroy(self.h)
+        except Exception:
+            pass
+
+    def restrict(self, f):
+        batch = f.numel() // self.fine.size
+        out = self.ctx.torch.empty((batch,) + self.coarse.shape, dtype=f.dtype, device=f.device)
+        check(lib().ptb_restrict_batch(self.h, C.c_size_t(batch), _ptr(f), _ptr(out)))
+        return out
+
+    def interpolate(self, f):
+        batch = f.numel() // self.coarse.size
+        out = self.ctx.torch.empty((batch,) + self.fine.shape, dtype=f.dtype, device=f.device)
+        check(lib().ptb_interpolate_batch(self.h, C.c_size_t(batch), _ptr(f), _ptr(out)))
+        return out

@@ -1,0 +1,609 @@
+// K1 — batched fp64 velocity-Verlet propagator for u_tt = c^2 Lap u (periodic 5-point).
+//
+// Reference: /root/reference/proj/src/propagator.cpp
+//   laplacian_into        :31-58   (x term first, (f[x+1] - 2 f[x]) + f[x-1], times 1/h^2)
+//   verlet_step_inplace   :60-73   a0 = c^2 Lap u; u += dt*udot + dt^2/2 a0;
+//                                  a1 = Lap u; udot += dt/2 (a0 + c^2 a1)
+//   propagate_coupling    :95-105  m steps, finite check once at the end
+//
+// Two arithmetic modes share every kernel below:
+//   EXACT — the reference's operations in the reference's order with explicitly
+//           rounded intrinsics (__dadd_rn/__dmul_rn never contract to FMA), carrying
+//           (u, udot, a = c^2 Lap u).  Bitwise equal to the reference.  Reusing a from
+//           the previous step instead of recomputing Lap is bitwise neutral: the
+//           reference's a0 of step s+1 is Lap(u_s+1)*c^2, the very product used as
+//           c^2*a1 in step s.
+//   FAST  — the same Verlet step in kick-drift-kick form carrying (u, vh = udot + b),
+//           b = (dt/2) c^2 Lap u:  u' = u + dt vh;  b' = Kx*(cc*u' + ry*(uN+uS) + (uW+uE));
+//           vh' = vh + 2 b'  (final step: udot = vh + b').  Kx = (dt/2) c^2 / hx^2 is
+//           precomputed per point, so one update is 7 DP instructions (5 FMA/MUL/ADD
+//           for b, 1 FMA drift, 1 FMA kick).
+//
+// Kernel families:
+//   k_small   — one CTA owns a whole slice (N <= 4096: 1D fields, coarse 2D grids);
+//               u double-buffered in shared memory, all steps on chip, one barrier/step.
+//   k_wave    — 2D wavefront temporal blocking: a CTA owns a column strip (+ S+1 halo
+//               columns each side) of one slice and marches along y; S+1 time levels
+//               are in flight, level t one row behind level t-1.  Each thread owns one
+//               column: its u window (rows r-1, r) and carried velocity sit in registers,
+//               the current row of every level sits in shared memory (x-neighbours).
+//               S steps per HBM round trip (read u, udot, coef once; write u, udot once).
+//   k_stream  — generic fallback (large 1D): one kernel per half step, HBM streaming.
+//
+// Layout: slice-major SoA, u[b*N + iy*nx + ix], axis 0 = y (grid.hpp:8-13).
+
+#include <algorithm>
+#include <cmath>
+
+#include "ptb_internal.h"
+
+namespace ptb {
+
+void nonfinite_on(ptb_context* ctx, cudaStream_t st, size_t n, size_t batch, const double* f, int32_t* flags);
+
+namespace {
+
+using namespace std;
+
+// ------------------------------------------------------------------ arithmetic
+
+// propagator.cpp:44-56 in reference order.  1D: only the x term (propagator.cpp:32-40).
+template <bool HASY>
+__device__ __forceinline__ double lap_exact(double uc, double ul, double ur, double uu, double ud,
+                                            const StepParams& p) {
+  double x = __dadd_rn(__dsub_rn(ur, __dmul_rn(2.0, uc)), ul);
+  x = __dmul_rn(x, p.ihx2);
+  if (!HASY) return x;
+  double y = __dadd_rn(__dsub_rn(uu, __dmul_rn(2.0, uc)), ud);
+  return __dadd_rn(x, __dmul_rn(y, p.ihy2));
+}
+
+// FAST half-kick b = Kx * (cc*uc + ry*(uu+ud) + (ul+ur)).
+template <bool HASY>
+__device__ __forceinline__ double bfast(double uc, double ul, double ur, double uu, double ud, double kx,
+                                        const StepParams& p) {
+  const double s1 = ul + ur;
+  if (!HASY) return kx * fma(p.cc, uc, s1);
+  return kx * fma(p.cc, uc, fma(p.ry, uu + ud, s1));
+}
+
+__device__ __forceinline__ bool finite2(double a, double b) { return isfinite(a) && isfinite(b); }
+
+// periodic neighbour offsets of point p in an ny x nx slice
+struct Nb {
+  int l, r, u, d;
+};
+__device__ __forceinline__ Nb neighbours(int p, int ny, int nx) {
+  const int iy = p / nx, ix = p - iy * nx;
+  Nb n;
+  n.l = ix == 0 ? p + nx - 1 : p - 1;
+  n.r = ix == nx - 1 ? p - nx + 1 : p + 1;
+  n.u = iy == ny - 1 ? ix : p + nx;
+  n.d = iy == 0 ? p + (ny - 1) * nx : p - nx;
+  return n;
+}
+
+// ------------------------------------------------------------------ k_small
+
+struct SmallArgs {
+  StepParams p;
+  int n;  // points per slice
+  int steps;
+  double* u;
+  double* v;
+  const double* coef;  // EXACT: c2, FAST: kx
+  int32_t* flags;
+};
+
+template <int PPT, bool EXACT, bool HASY>
+__global__ void __launch_bounds__(1024) k_small(const SmallArgs a) {
+  extern __shared__ double buf[];  // [2][n]
+  const int n = a.n, T = blockDim.x, tid = threadIdx.x;
+  const size_t off = static_cast<size_t>(blockIdx.x) * n;
+  double* __restrict__ U = a.u + off;
+  double* __restrict__ V = a.v + off;
+  const StepParams& p = a.p;
+  double u[PPT], v[PPT], k[PPT], acc[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = tid + q * T;
+    u[q] = v[q] = k[q] = acc[q] = 0.0;
+    if (i < n) {
+      u[q] = U[i];
+      v[q] = V[i];
+      k[q] = a.coef[i];
+      buf[i] = u[q];
+    }
+  }
+  __syncthreads();
+  // initial acceleration (EXACT: a0 = Lap(u)*c^2) / half kick (FAST: vh = udot + b)
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = tid + q * T;
+    if (i < n) {
+      const Nb nb = neighbours(i, p.ny, p.nx);
+      if (EXACT) {
+        acc[q] = __dmul_rn(lap_exact<HASY>(u[q], buf[nb.l], buf[nb.r], buf[nb.u], buf[nb.d], p), k[q]);
+      } else {
+        const double b = bfast<HASY>(u[q], buf[nb.l], buf[nb.r], buf[nb.u], buf[nb.d], k[q], p);
+        v[q] = v[q] + b;
+      }
+    }
+  }
+  for (int s = 0; s < a.steps; ++s) {
+    double* dst = buf + ((s + 1) & 1) * n;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = tid + q * T;
+      if (i < n) {
+        if (EXACT)
+          u[q] = __dadd_rn(u[q], __dadd_rn(__dmul_rn(p.dt, v[q]), __dmul_rn(p.hdt2, acc[q])));
+        else
+          u[q] = fma(p.dt, v[q], u[q]);
+        dst[i] = u[q];
+      }
+    }
+    __syncthreads();
+    const bool last = s + 1 == a.steps;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = tid + q * T;
+      if (i < n) {
+        const Nb nb = neighbours(i, p.ny, p.nx);
+        if (EXACT) {
+          const double an = __dmul_rn(lap_exact<HASY>(u[q], dst[nb.l], dst[nb.r], dst[nb.u], dst[nb.d], p), k[q]);
+          v[q] = __dadd_rn(v[q], __dmul_rn(p.hd, __dadd_rn(acc[q], an)));
+          acc[q] = an;
+        } else {
+          const double b = bfast<HASY>(u[q], dst[nb.l], dst[nb.r], dst[nb.u], dst[nb.d], k[q], p);
+          v[q] = last ? v[q] + b : fma(2.0, b, v[q]);
+        }
+      }
+    }
+  }
+  bool ok = true;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = tid + q * T;
+    if (i < n) {
+      U[i] = u[q];
+      V[i] = v[q];
+      ok &= finite2(u[q], v[q]);
+    }
+  }
+  if (a.flags) {
+    const int bad = __syncthreads_or(!ok);
+    if (bad && tid == 0) atomicOr(&a.flags[blockIdx.x], 1);
+  }
+}
+
+// ------------------------------------------------------------------ k_stream
+
+struct StreamArgs {
+  StepParams p;
+  size_t n, total;  // points per slice, batch*n
+  double* u;
+  double* v;
+  double* acc;      // EXACT: a (N per slice) — FAST: unused
+  const double* coef;
+  int last;
+};
+
+template <bool EXACT, bool HASY>
+__global__ void k_stream_init(const StreamArgs a) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g < a.total; g += size_t(gridDim.x) * blockDim.x) {
+    const size_t s = g / a.n, i = g - s * a.n;
+    const double* U = a.u + s * a.n;
+    const Nb nb = neighbours(int(i), a.p.ny, a.p.nx);
+    if (EXACT)
+      a.acc[g] = __dmul_rn(lap_exact<HASY>(U[i], U[nb.l], U[nb.r], U[nb.u], U[nb.d], a.p), a.coef[i]);
+    else
+      a.v[g] = a.v[g] + bfast<HASY>(U[i], U[nb.l], U[nb.r], U[nb.u], U[nb.d], a.coef[i], a.p);
+  }
+}
+
+template <bool EXACT>
+__global__ void k_stream_drift(const StreamArgs a) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g < a.total; g += size_t(gridDim.x) * blockDim.x) {
+    if (EXACT)
+      a.u[g] = __dadd_rn(a.u[g], __dadd_rn(__dmul_rn(a.p.dt, a.v[g]), __dmul_rn(a.p.hdt2, a.acc[g])));
+    else
+      a.u[g] = fma(a.p.dt, a.v[g], a.u[g]);
+  }
+}
+
+template <bool EXACT, bool HASY>
+__global__ void k_stream_kick(const StreamArgs a) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g < a.total; g += size_t(gridDim.x) * blockDim.x) {
+    const size_t s = g / a.n, i = g - s * a.n;
+    const double* U = a.u + s * a.n;
+    const Nb nb = neighbours(int(i), a.p.ny, a.p.nx);
+    if (EXACT) {
+      const double an = __dmul_rn(lap_exact<HASY>(U[i], U[nb.l], U[nb.r], U[nb.u], U[nb.d], a.p), a.coef[i]);
+      a.v[g] = __dadd_rn(a.v[g], __dmul_rn(a.p.hd, __dadd_rn(a.acc[g], an)));
+      a.acc[g] = an;
+    } else {
+      const double b = bfast<HASY>(U[i], U[nb.l], U[nb.r], U[nb.u], U[nb.d], a.coef[i], a.p);
+      a.v[g] = a.last ? a.v[g] + b : fma(2.0, b, a.v[g]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ k_wave
+
+struct WaveArgs {
+  StepParams p;
+  const double* __restrict__ u_in;
+  const double* __restrict__ v_in;
+  double* __restrict__ u_out;
+  double* __restrict__ v_out;
+  const double* __restrict__ coef;  // EXACT: c2, FAST: kx
+  size_t stride;                    // points per slice
+  int wu;                           // useful (output) columns per strip
+  int rb;                           // output rows per row block
+  int32_t* flags;                   // nonfinite flags (nullable)
+};
+
+template <int S, bool EXACT>
+__global__ void __launch_bounds__(512) k_wave(const WaveArgs a) {
+  constexpr int HX = S + 1;  // halo columns each side: level 0 (a_0 stencil) + S levels
+  constexpr int NL = S + 1;  // time levels 0..S in flight
+  extern __shared__ double sm[];  // [NL][2][W] — u_t at the row level t processes, double-buffered
+  const int W = blockDim.x, j = threadIdx.x;
+  const int nx = a.p.nx, ny = a.p.ny;
+  const int x0 = blockIdx.x * a.wu;
+  int gx = (x0 - HX + j) % nx;
+  if (gx < 0) gx += nx;
+  const int Y0 = blockIdx.y * a.rb;
+  const int nrows = min(a.rb, ny - Y0);
+  const int ystart = Y0 - S;  // level S is valid from row ystart + S = Y0
+  const int n_iter = nrows + 2 * S;
+  const int oc = j - HX;
+  const bool col_out = oc >= 0 && j < W - HX && oc < a.wu && x0 + oc < nx;
+  const size_t off = static_cast<size_t>(blockIdx.z) * a.stride;
+  const double* __restrict__ U = a.u_in + off;
+  const double* __restrict__ V = a.v_in + off;
+  double* __restrict__ UO = a.u_out + off;
+  double* __restrict__ VO = a.v_out + off;
+  const double* __restrict__ K = a.coef;
+  const int jl = j > 0 ? j - 1 : 0, jr = j < W - 1 ? j + 1 : W - 1;
+  const StepParams& p = a.p;
+  auto rowp = [&](int y) -> int {
+    int r = y % ny;
+    if (r < 0) r += ny;
+    return r * nx + gx;
+  };
+  auto SM = [&](int t, int par) -> double* { return sm + (t * 2 + par) * W; };
+
+  double ulo[NL], uce[NL], vin[NL], kin[NL], ain[NL];
+#pragma unroll
+  for (int t = 0; t < NL; ++t) ulo[t] = uce[t] = vin[t] = kin[t] = ain[t] = 0.0;
+  ulo[0] = U[rowp(ystart - 1)];
+  uce[0] = U[rowp(ystart)];
+  SM(0, 0)[j] = uce[0];
+  // level-0 inputs, prefetched two iterations ahead: u_0[r0+1], udot_0[r0], coef[r0]
+  double pu0 = U[rowp(ystart + 1)], pv0 = V[rowp(ystart)], pk0 = K[rowp(ystart)];
+  double pu1 = U[rowp(ystart + 2)], pv1 = V[rowp(ystart + 1)], pk1 = K[rowp(ystart + 1)];
+  __syncthreads();
+  bool ok = true;
+  for (int i = 0; i < n_iter; ++i) {
+    const int par = i & 1, npar = par ^ 1;
+    const double uu0 = pu0, v0 = pv0, k0 = pk0;
+    pu0 = pu1;
+    pv0 = pv1;
+    pk0 = pk1;
+    if (i + 2 < n_iter) {
+      pu1 = U[rowp(ystart + i + 3)];
+      pv1 = V[rowp(ystart + i + 2)];
+      pk1 = K[rowp(ystart + i + 2)];
+    }
+    // ---- level 0: a_0 / b_0 at row ystart+i, produce u_1 at that row
+    double up, cv, ck, ca;  // carries to level 1: u_1[r], velocity, coef, (EXACT) a_0
+    {
+      const double uc = uce[0], ud = ulo[0], ul = SM(0, par)[jl], ur = SM(0, par)[jr];
+      SM(0, npar)[j] = uu0;
+      if (EXACT) {
+        const double a0 = __dmul_rn(lap_exact<true>(uc, ul, ur, uu0, ud, p), k0);
+        up = __dadd_rn(uc, __dadd_rn(__dmul_rn(p.dt, v0), __dmul_rn(p.hdt2, a0)));
+        cv = v0;
+        ca = a0;
+      } else {
+        const double vh = v0 + bfast<true>(uc, ul, ur, uu0, ud, k0, p);
+        up = fma(p.dt, vh, uc);
+        cv = vh;
+        ca = 0.0;
+      }
+      ck = k0;
+      SM(1, npar)[j] = up;
+      ulo[0] = uc;
+      uce[0] = uu0;
+    }
+    // ---- levels 1..S: level t finalises step t at row ystart+i-t
+#pragma unroll
+    for (int t = 1; t <= S; ++t) {
+      const double vprev = vin[t], kt = kin[t], aprev = ain[t];
+      vin[t] = cv;  // inputs of level t for the next iteration (row advances by one)
+      kin[t] = ck;
+      ain[t] = ca;
+      const double uu = up;
+      if (i >= 2 * t) {  // warp-uniform; before that the level's rows are warm-up only
+        const double uc = uce[t], ud = ulo[t], ul = SM(t, par)[jl], ur = SM(t, par)[jr];
+        if (EXACT) {
+          const double an = __dmul_rn(lap_exact<true>(uc, ul, ur, uu, ud, p), kt);
+          const double vn = __dadd_rn(vprev, __dmul_rn(p.hd, __dadd_rn(aprev, an)));
+          if (t < S) {
+            up = __dadd_rn(uc, __dadd_rn(__dmul_rn(p.dt, vn), __dmul_rn(p.hdt2, an)));
+            cv = vn;
+            ca = an;
+            ck = kt;
+            SM(t + 1, npar)[j] = up;
+          } else if (col_out) {
+            const int o = rowp(ystart + i - S);
+            UO[o] = uc;
+            VO[o] = vn;
+            ok &= finite2(uc, vn);
+          }
+        } else {
+          const double b = bfast<true>(uc, ul, ur, uu, ud, kt, p);
+          if (t < S) {
+            const double vh = fma(2.0, b, vprev);
+            up = fma(p.dt, vh, uc);
+            cv = vh;
+            ck = kt;
+            SM(t + 1, npar)[j] = up;
+          } else if (col_out) {
+            const double vS = vprev + b;
+            const int o = rowp(ystart + i - S);
+            UO[o] = uc;
+            VO[o] = vS;
+            ok &= finite2(uc, vS);
+          }
+        }
+      }
+      ulo[t] = uce[t];
+      uce[t] = uu;
+    }
+    __syncthreads();
+  }
+  if (a.flags) {
+    const int bad = __syncthreads_or(!ok);
+    if (bad && j == 0) atomicOr(&a.flags[blockIdx.z], 1);
+  }
+}
+
+// ------------------------------------------------------------------ misc kernels
+
+__global__ void k_laplacian(StepParams p, size_t n, size_t total, const double* f, double* out) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g < total; g += size_t(gridDim.x) * blockDim.x) {
+    const size_t s = g / n, i = g - s * n;
+    const double* F = f + s * n;
+    const Nb nb = neighbours(int(i), p.ny, p.nx);
+    out[g] = p.dim == 1 ? lap_exact<false>(F[i], F[nb.l], F[nb.r], 0, 0, p)
+                        : lap_exact<true>(F[i], F[nb.l], F[nb.r], F[nb.u], F[nb.d], p);
+  }
+}
+
+__global__ void k_nonfinite(size_t n, const double* f, int32_t* flags) {
+  const double* F = f + blockIdx.y * n;
+  bool ok = true;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    ok &= isfinite(F[i]);
+  const int bad = __syncthreads_or(!ok);
+  if (bad && threadIdx.x == 0) atomicOr(&flags[blockIdx.y], 1);
+}
+
+__global__ void k_copy2(size_t total, const double* a, const double* b, double* ao, double* bo) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g < total; g += size_t(gridDim.x) * blockDim.x) {
+    ao[g] = a[g];
+    bo[g] = b[g];
+  }
+}
+
+unsigned grid_for(ptb_context* ctx, size_t total, int block) {
+  const size_t want = (total + block - 1) / block;
+  return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(want, size_t(ctx->num_sms) * 16)));
+}
+
+// ------------------------------------------------------------------ dispatch
+
+template <int PPT, bool EXACT, bool HASY>
+void launch_small(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, int threads, size_t batch) {
+  const size_t smem = 2 * size_t(a.n) * sizeof(double);
+  auto kern = k_small<PPT, EXACT, HASY>;
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern<<<static_cast<unsigned>(batch), threads, smem, st>>>(a);
+  PTB_LAUNCH_CHECK(ctx);
+}
+
+template <bool EXACT, bool HASY>
+void small_dispatch(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, size_t batch) {
+  const int n = a.n;
+  int ppt = 1;
+  while (ppt < 4 && n > ppt * 1024) ppt *= 2;
+  int threads = (n + ppt - 1) / ppt;
+  threads = ((threads + 31) / 32) * 32;
+  switch (ppt) {
+    case 1: launch_small<1, EXACT, HASY>(ctx, st, a, threads, batch); break;
+    case 2: launch_small<2, EXACT, HASY>(ctx, st, a, threads, batch); break;
+    default: launch_small<4, EXACT, HASY>(ctx, st, a, threads, batch); break;
+  }
+}
+
+struct WavePlan {
+  int W, wu, strips, rb, nrb;
+};
+
+// Choose strip width W (threads) and row-block height rb.  Cost model: per-SM work in
+// warp-iterations = ceil(CTAs / SMs) * (W/32) * (rb + 2S) — halo columns and warm-up rows
+// are both paid for — with a latency penalty when fewer than 2 CTAs land on each SM.
+WavePlan plan_wave(ptb_context* ctx, int ny, int nx, int S, size_t batch) {
+  const int HX = S + 1;
+  WavePlan best{};
+  double best_cost = 1e300;
+  for (int W = 64; W <= 512; W += 32) {
+    const int wu_max = W - 2 * HX;
+    if (wu_max < 16) continue;
+    const int strips = (nx + wu_max - 1) / wu_max;
+    const int wu = (nx + strips - 1) / strips;
+    for (int div = 1;; div *= 2) {
+      const int rb = (ny + div - 1) / div;
+      if (div > 1 && rb < 2 * S) break;
+      const int nrb = (ny + rb - 1) / rb;
+      const size_t ctas = size_t(strips) * nrb * batch;
+      const double rounds = std::ceil(double(ctas) / ctx->num_sms);
+      const double lat = ctas < size_t(2 * ctx->num_sms) ? 1.5 : 1.0;
+      const double cost = rounds * (W / 32.0) * (rb + 2.0 * S) * lat;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = WavePlan{W, wu, strips, rb, nrb};
+      }
+      if (rb <= 1) break;
+    }
+  }
+  return best;
+}
+
+template <int S, bool EXACT>
+void launch_wave(ptb_context* ctx, cudaStream_t st, const WavePlan& pl, WaveArgs a, size_t batch) {
+  const size_t smem = size_t(S + 1) * 2 * pl.W * sizeof(double);
+  auto kern = k_wave<S, EXACT>;
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  a.wu = pl.wu;
+  a.rb = pl.rb;
+  dim3 grid(pl.strips, pl.nrb, static_cast<unsigned>(batch));
+  kern<<<grid, pl.W, smem, st>>>(a);
+  PTB_LAUNCH_CHECK(ctx);
+}
+
+template <bool EXACT>
+void wave_pass(ptb_context* ctx, cudaStream_t st, int S, const StepParams& p, size_t batch, const double* ui,
+               const double* vi, double* uo, double* vo, const double* coef, int32_t* flags) {
+  WaveArgs a{p, ui, vi, uo, vo, coef, size_t(p.ny) * p.nx, 0, 0, flags};
+  const WavePlan pl = plan_wave(ctx, p.ny, p.nx, S, batch);
+  switch (S) {
+    case 1: launch_wave<1, EXACT>(ctx, st, pl, a, batch); break;
+    case 2: launch_wave<2, EXACT>(ctx, st, pl, a, batch); break;
+    case 4: launch_wave<4, EXACT>(ctx, st, pl, a, batch); break;
+    case 8: launch_wave<8, EXACT>(ctx, st, pl, a, batch); break;
+    default: fail(PTB_UNSUPPORTED, "wavefront depth");
+  }
+}
+
+template <bool EXACT>
+void wave_propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double* v, int32_t* flags,
+                    const LaunchSlot& slot) {
+  ptb_context* ctx = pr->ctx;
+  const StepParams& p = pr->prm;
+  const size_t n = pr->n;
+  const double* coef = EXACT ? pr->c2 : pr->kx;
+  // decompose steps into passes of 8,4,2,1 levels; ping-pong between (u,v) and scratch
+  std::vector<int> passes;
+  size_t rem = steps;
+  while (rem >= 8) { passes.push_back(8); rem -= 8; }
+  for (int s : {4, 2, 1})
+    if (rem >= size_t(s)) { passes.push_back(s); rem -= size_t(s); }
+  double* su = slot.su ? slot.su : static_cast<double*>(ctx->scratch[0].get(batch * n * sizeof(double)));
+  double* sv = slot.sv ? slot.sv : static_cast<double*>(ctx->scratch[1].get(batch * n * sizeof(double)));
+  const double *ci = u, *cvi = v;
+  for (size_t k = 0; k < passes.size(); ++k) {
+    const bool to_scratch = (k % 2) == 0;
+    double* uo = to_scratch ? su : u;
+    double* vo = to_scratch ? sv : v;
+    wave_pass<EXACT>(ctx, slot.stream, passes[k], p, batch, ci, cvi, uo, vo, coef,
+                     k + 1 == passes.size() ? flags : nullptr);
+    ci = uo;
+    cvi = vo;
+  }
+  if (ci != u) {
+    const size_t total = batch * n;
+    k_copy2<<<grid_for(ctx, total, 256), 256, 0, slot.stream>>>(total, su, sv, u, v);
+    PTB_LAUNCH_CHECK(ctx);
+  }
+}
+
+template <bool EXACT, bool HASY>
+void stream_propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double* v, int32_t* flags,
+                      const LaunchSlot& slot) {
+  ptb_context* ctx = pr->ctx;
+  const size_t n = pr->n, total = batch * n;
+  double* acc = !EXACT ? nullptr
+                : slot.su ? slot.su
+                          : static_cast<double*>(ctx->scratch[2].get(total * sizeof(double)));
+  const cudaStream_t st = slot.stream;
+  StreamArgs a{pr->prm, n, total, u, v, acc, EXACT ? pr->c2 : pr->kx, 0};
+  const unsigned g = grid_for(ctx, total, 256);
+  k_stream_init<EXACT, HASY><<<g, 256, 0, st>>>(a);
+  PTB_LAUNCH_CHECK(ctx);
+  for (size_t s = 0; s < steps; ++s) {
+    a.last = s + 1 == steps;
+    k_stream_drift<EXACT><<<g, 256, 0, st>>>(a);
+    PTB_LAUNCH_CHECK(ctx);
+    k_stream_kick<EXACT, HASY><<<g, 256, 0, st>>>(a);
+    PTB_LAUNCH_CHECK(ctx);
+  }
+  if (flags) {
+    nonfinite_on(ctx, st, n, batch, u, flags);
+    nonfinite_on(ctx, st, n, batch, v, flags);
+  }
+}
+
+}  // namespace
+
+void propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double* v, int32_t* flags, int mode,
+               const LaunchSlot* slot_in) {
+  if (batch == 0 || steps == 0) return;
+  ptb_context* ctx = pr->ctx;
+  LaunchSlot slot;
+  if (slot_in) slot = *slot_in;
+  if (!slot.stream) slot.stream = ctx->stream;
+  const bool exact = mode == PTB_MODE_EXACT;
+  const StepParams& p = pr->prm;
+  const size_t n = pr->n;
+  if (n <= 4096) {
+    SmallArgs a{p, int(n), int(steps), u, v, exact ? pr->c2 : pr->kx, flags};
+    const cudaStream_t st = slot.stream;
+    if (p.dim == 1) {
+      exact ? small_dispatch<true, false>(ctx, st, a, batch) : small_dispatch<false, false>(ctx, st, a, batch);
+    } else {
+      exact ? small_dispatch<true, true>(ctx, st, a, batch) : small_dispatch<false, true>(ctx, st, a, batch);
+    }
+    return;
+  }
+  if (p.dim == 2) {
+    exact ? wave_propagate<true>(pr, steps, batch, u, v, flags, slot)
+          : wave_propagate<false>(pr, steps, batch, u, v, flags, slot);
+    return;
+  }
+  exact ? stream_propagate<true, false>(pr, steps, batch, u, v, flags, slot)
+        : stream_propagate<false, false>(pr, steps, batch, u, v, flags, slot);
+}
+
+void laplacian(ptb_context* ctx, const ptb_grid& g, size_t batch, const double* f, double* out) {
+  StepParams p{};
+  p.dim = g.dim;
+  p.ny = g.dim == 1 ? 1 : int(g.n[0]);
+  p.nx = g.dim == 1 ? int(g.n[0]) : int(g.n[1]);
+  if (g.dim == 1) {
+    p.ihx2 = 1.0 / (g.h[0] * g.h[0]);
+  } else {
+    p.ihy2 = 1.0 / (g.h[0] * g.h[0]);
+    p.ihx2 = 1.0 / (g.h[1] * g.h[1]);
+  }
+  const size_t n = grid_size(g), total = n * batch;
+  if (total == 0) return;
+  k_laplacian<<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(p, n, total, f, out);
+  PTB_LAUNCH_CHECK(ctx);
+}
+
+void nonfinite_on(ptb_context* ctx, cudaStream_t st, size_t n, size_t batch, const double* f, int32_t* flags) {
+  if (batch == 0 || n == 0) return;
+  const unsigned gx = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 64));
+  k_nonfinite<<<dim3(gx, static_cast<unsigned>(batch)), 256, 0, st>>>(n, f, flags);
+  PTB_LAUNCH_CHECK(ctx);
+}
+
+void nonfinite(ptb_context* ctx, size_t n, size_t batch, const double* f, int32_t* flags) {
+  nonfinite_on(ctx, ctx->stream, n, batch, f, flags);
+}
+
+}  // namespace ptb

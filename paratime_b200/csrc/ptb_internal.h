@@ -1,0 +1,143 @@
+// Internal declarations shared by the paratime_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "paratime_b200.h"
+
+namespace ptb {
+
+// Exception carrying a ptb_status; converted to a return code at the C ABI.
+struct Error : std::runtime_error {
+  ptb_status status;
+  Error(ptb_status s, const std::string& what) : std::runtime_error(what), status(s) {}
+};
+
+extern thread_local std::string g_last_error;
+
+[[noreturn]] inline void fail(ptb_status s, const std::string& what) { throw Error(s, what); }
+inline void require(bool ok, const std::string& what) {
+  if (!ok) fail(PTB_INVALID_ARGUMENT, what);
+}
+
+#define PTB_CUDA_CHECK(expr)                                                           \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      ::ptb::fail(PTB_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+  } while (0)
+
+#define PTB_LAUNCH_CHECK(ctx)                                                          \
+  do {                                                                                 \
+    cudaError_t _e = cudaGetLastError();                                               \
+    if (_e != cudaSuccess)                                                             \
+      ::ptb::fail(PTB_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                           \
+  } while (0)
+
+// Grow-only device scratch buffer.
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need);
+  void release();
+};
+
+}  // namespace ptb
+
+struct ptb_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;      // stream all work is issued on
+  cudaStream_t own_stream = nullptr;  // the context's own stream
+  int num_sms = 148;
+  std::atomic<uint64_t> launches{0};
+  std::recursive_mutex mutex;  // serialises host-API calls (reference runs stages concurrently)
+  ptb::DeviceBuffer scratch[4];
+  ptb::DeviceBuffer flags;
+  cudaStream_t aux[2] = {nullptr, nullptr};  // host-batch pipeline streams (lazy)
+  ptb::DeviceBuffer slotbuf[2][5];            // per pipeline slot: u, v, su, sv, flags
+  void* cublas = nullptr;  // lazily created cublasHandle_t
+};
+
+namespace ptb {
+
+// Arithmetic parameters of one propagator (host-computed exactly as propagator.cpp).
+struct StepParams {
+  int dim;              // 1 or 2
+  int ny, nx;           // 2D: points(0), points(1); 1D: ny = 1, nx = points(0)
+  double ihx2, ihy2;    // 1/(h*h) per axis, propagator.cpp:42-43 (1D: ihx2 = 1/(h0*h0))
+  double dt, hd, hdt2;  // dt, 0.5*dt, 0.5*dt*dt (propagator.cpp:64)
+  double ry, cc;        // FAST: ry = ihy2/ihx2 (0 in 1D), cc = -2*(1+ry)
+};
+
+}  // namespace ptb
+
+struct ptb_propagator {
+  ptb_context* ctx = nullptr;
+  ptb_grid grid{};
+  size_t n = 0;  // points
+  size_t steps = 0;
+  ptb::StepParams prm{};
+  double* c = nullptr;   // speed (N)
+  double* c2 = nullptr;  // c*c (N)                — EXACT coefficient
+  double* kx = nullptr;  // 0.5*dt*c*c/hx^2 (N)     — FAST coefficient
+};
+
+struct ptb_transfer {
+  ptb_context* ctx = nullptr;
+  ptb_grid coarse{}, fine{};
+  int kind = 0;
+  size_t ratio[2] = {1, 1};
+  // Fourier weights per axis: w[a][rem*nc + j] = weight of coarse node q-j..., see transfer.cu
+  double* wx = nullptr;
+  double* wy = nullptr;
+};
+
+namespace ptb {
+
+// Run `fn`, converting exceptions to a status + thread-local message (C ABI boundary).
+template <typename Fn>
+ptb_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return PTB_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PTB_CUDA;
+  }
+}
+
+// Where a propagation runs: stream + ping-pong scratch (2 x batch*N doubles, or null
+// to use the context scratch) + EXACT-mode acceleration scratch for the stream path.
+struct LaunchSlot {
+  cudaStream_t stream = nullptr;
+  double* su = nullptr;
+  double* sv = nullptr;
+};
+
+// propagate.cu
+void propagate(ptb_propagator* p, size_t steps, size_t batch, double* u, double* v, int32_t* flags,
+               int mode, const LaunchSlot* slot = nullptr);
+void laplacian(ptb_context* ctx, const ptb_grid& g, size_t batch, const double* f, double* out);
+void nonfinite(ptb_context* ctx, size_t n, size_t batch, const double* f, int32_t* flags);
+
+// transfer.cu
+void transfer_init(ptb_transfer* t);
+void restrict_fields(ptb_transfer* t, size_t batch, const double* fine, double* coarse);
+void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, double* fine);
+
+inline size_t grid_size(const ptb_grid& g) { return g.dim == 1 ? g.n[0] : g.n[0] * g.n[1]; }
+void validate_grid(const ptb_grid& g);
+
+}  // namespace ptb
