@@ -66,9 +66,11 @@ ptb_status ptb_context_destroy(ptb_context* ctx);
 ptb_status ptb_context_synchronize(ptb_context* ctx);
 /* cudaStream_t of the context (as void*); kernels of this context run on it */
 void* ptb_context_stream(ptb_context* ctx);
-/* run this context's work on an external stream (e.g. the caller's current stream);
- * NULL restores the context's own stream */
+/* run this context's work on an external cudaStream_t (e.g. the caller's current
+ * stream; 0 = the legacy default stream) ... */
 ptb_status ptb_context_set_stream(ptb_context* ctx, void* stream);
+/* ... or back on the context's own non-blocking stream */
+ptb_status ptb_context_use_own_stream(ptb_context* ctx);
 int ptb_context_device(ptb_context* ctx);
 /* number of this library's kernels launched on the context so far */
 uint64_t ptb_context_launches(ptb_context* ctx);

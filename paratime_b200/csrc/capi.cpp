@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -12,6 +13,14 @@
 namespace ptb {
 
 thread_local std::string g_last_error;
+
+bool sync_check_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PTB_SYNC_CHECK");
+    return e && *e == '1';
+  }();
+  return on;
+}
 
 void* DeviceBuffer::get(size_t need) {
   if (need == 0) need = 8;
@@ -106,7 +115,14 @@ void* ptb_context_stream(ptb_context* ctx) { return ctx ? static_cast<void*>(ctx
 ptb_status ptb_context_set_stream(ptb_context* ctx, void* stream) {
   return guarded([&] {
     require(ctx != nullptr, "context: null");
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+ptb_status ptb_context_use_own_stream(ptb_context* ctx) {
+  return guarded([&] {
+    require(ctx != nullptr, "context: null");
+    ctx->stream = ctx->own_stream;
   });
 }
 

@@ -35,11 +35,15 @@ inline void require(bool ok, const std::string& what) {
       ::ptb::fail(PTB_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
   } while (0)
 
+bool sync_check_enabled();  // PTB_SYNC_CHECK=1: synchronise after every launch (debug)
+
 #define PTB_LAUNCH_CHECK(ctx)                                                          \
   do {                                                                                 \
     cudaError_t _e = cudaGetLastError();                                               \
+    if (_e == cudaSuccess && ::ptb::sync_check_enabled()) _e = cudaDeviceSynchronize(); \
     if (_e != cudaSuccess)                                                             \
-      ::ptb::fail(PTB_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      ::ptb::fail(PTB_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e) +  \
+                                " at " + __FILE__ + ":" + std::to_string(__LINE__));   \
     (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                           \
   } while (0)
 
