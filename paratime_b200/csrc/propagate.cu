@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "ptb_internal.h"
 
@@ -68,6 +69,17 @@ __device__ __forceinline__ double bfast(double uc, double ul, double ur, double 
 }
 
 __device__ __forceinline__ bool finite2(double a, double b) { return isfinite(a) && isfinite(b); }
+
+// 8-byte global -> shared asynchronous copy (LDGSTS), grouped by commit/wait
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // periodic neighbour offsets of point p in an ny x nx slice
 struct Nb {
@@ -244,130 +256,187 @@ struct WaveArgs {
   int32_t* flags;                   // nonfinite flags (nullable)
 };
 
+// One iteration of the wavefront: level 0 loads row r0 = ystart+i (+ look-ahead row), levels
+// 1..S finalise step t at row ystart+i-t.  PAR (iteration parity) is a template parameter so
+// shared-memory addresses are base + immediate.  The per-level register "shifts" below are
+// SSA renames: the caller unrolls by 6 (lcm of the window period 3 and the carry period 2),
+// so they compile to no moves.
+template <int S, bool EXACT, int PAR>
+__device__ __forceinline__ void wave_iter(double* __restrict__ sbase, int sstride_par, const StepParams& p,
+                                          double (&ulo)[S + 1], double (&uce)[S + 1], double (&vin)[S + 1],
+                                          double (&kin)[S + 1], double (&ain)[S + 1], double uu0, double v0,
+                                          double k0, double& out_u, double& out_v) {
+  constexpr int NLP = (S + 1) | 1;  // odd stride per column: conflict-free 8-byte accesses
+  // reads of parity PAR, writes of parity PAR^1
+  const double* __restrict__ rd = sbase + PAR * sstride_par;
+  double* __restrict__ wr = sbase + (PAR ^ 1) * sstride_par;
+  // All x-neighbour loads first: they depend only on the previous iteration, so issuing
+  // them ahead of this iteration's stores keeps shared-memory latency off the level chain.
+  double ul[S + 1], ur[S + 1];
+#pragma unroll
+  for (int t = 0; t <= S; ++t) {
+    ul[t] = rd[t - NLP];
+    ur[t] = rd[t + NLP];
+  }
+  double up, cv, ck, ca;
+  {
+    const double uc = uce[0], ud = ulo[0];
+    if (EXACT) {
+      const double a0 = __dmul_rn(lap_exact<true>(uc, ul[0], ur[0], uu0, ud, p), k0);
+      up = __dadd_rn(uc, __dadd_rn(__dmul_rn(p.dt, v0), __dmul_rn(p.hdt2, a0)));
+      cv = v0;
+      ca = a0;
+    } else {
+      const double vh = v0 + bfast<true>(uc, ul[0], ur[0], uu0, ud, k0, p);
+      up = fma(p.dt, vh, uc);
+      cv = vh;
+      ca = 0.0;
+    }
+    ck = k0;
+    wr[0] = uu0;
+    wr[1] = up;
+    ulo[0] = uc;
+    uce[0] = uu0;
+  }
+  // FAST: the part of b independent of the level below, b = fma(Kx*ry, uu, q)
+  double q[S + 1], kr[S + 1];
+  if (!EXACT) {
+#pragma unroll
+    for (int t = 1; t <= S; ++t) {
+      q[t] = kin[t] * fma(p.cc, uce[t], fma(p.ry, ulo[t], ul[t] + ur[t]));
+      kr[t] = kin[t] * p.ry;
+    }
+  }
+#pragma unroll
+  for (int t = 1; t <= S; ++t) {
+    const double vprev = vin[t], kt = kin[t], aprev = ain[t];
+    vin[t] = cv;
+    kin[t] = ck;
+    ain[t] = ca;
+    const double uu = up;
+    const double uc = uce[t], ud = ulo[t];
+    if (EXACT) {
+      const double an = __dmul_rn(lap_exact<true>(uc, ul[t], ur[t], uu, ud, p), kt);
+      const double vn = __dadd_rn(vprev, __dmul_rn(p.hd, __dadd_rn(aprev, an)));
+      if (t < S) {
+        up = __dadd_rn(uc, __dadd_rn(__dmul_rn(p.dt, vn), __dmul_rn(p.hdt2, an)));
+        cv = vn;
+        ca = an;
+        ck = kt;
+        wr[t + 1] = up;
+      } else {
+        out_u = uc;
+        out_v = vn;
+      }
+    } else {
+      const double b = fma(kr[t], uu, q[t]);
+      if (t < S) {
+        const double vh = fma(2.0, b, vprev);
+        up = fma(p.dt, vh, uc);
+        cv = vh;
+        ck = kt;
+        wr[t + 1] = up;
+      } else {
+        out_u = uc;
+        out_v = vprev + b;
+      }
+    }
+    ulo[t] = uce[t];
+    uce[t] = uu;
+  }
+}
+
 template <int S, bool EXACT>
 __global__ void __launch_bounds__(512) k_wave(const WaveArgs a) {
   constexpr int HX = S + 1;  // halo columns each side: level 0 (a_0 stencil) + S levels
   constexpr int NL = S + 1;  // time levels 0..S in flight
-  extern __shared__ double sm[];  // [NL][2][W] — u_t at the row level t processes, double-buffered
+  constexpr int NLP = NL | 1;
+  constexpr int UNROLL = 6;
+  constexpr int RING = 6;  // must divide UNROLL so ring slots are compile-time
+  extern __shared__ double sm[];  // [2 parity][W + 2 pad columns][NLP] + [RING][3][W]
   const int W = blockDim.x, j = threadIdx.x;
   const int nx = a.p.nx, ny = a.p.ny;
-  const int x0 = blockIdx.x * a.wu;
+  const int npts = nx * ny;
+  // blockIdx.x = slice (fastest: concurrent CTAs share coef rows in L2), y = strip, z = row block
+  const int x0 = blockIdx.y * a.wu;
   int gx = (x0 - HX + j) % nx;
   if (gx < 0) gx += nx;
-  const int Y0 = blockIdx.y * a.rb;
+  const int Y0 = blockIdx.z * a.rb;
   const int nrows = min(a.rb, ny - Y0);
   const int ystart = Y0 - S;  // level S is valid from row ystart + S = Y0
-  const int n_iter = nrows + 2 * S;
+  const int n_iter = ((nrows + 2 * S + UNROLL - 1) / UNROLL) * UNROLL;
   const int oc = j - HX;
   const bool col_out = oc >= 0 && j < W - HX && oc < a.wu && x0 + oc < nx;
-  const size_t off = static_cast<size_t>(blockIdx.z) * a.stride;
+  const size_t off = static_cast<size_t>(blockIdx.x) * a.stride;
   const double* __restrict__ U = a.u_in + off;
   const double* __restrict__ V = a.v_in + off;
   double* __restrict__ UO = a.u_out + off;
   double* __restrict__ VO = a.v_out + off;
   const double* __restrict__ K = a.coef;
-  const int jl = j > 0 ? j - 1 : 0, jr = j < W - 1 ? j + 1 : W - 1;
-  const StepParams& p = a.p;
-  auto rowp = [&](int y) -> int {
+  const StepParams p = a.p;
+  // pad column on each side keeps j-1 / j+1 in bounds for the edge threads (values unused)
+  const int sstride_par = (W + 2) * NLP;
+  double* sbase = sm + (j + 1) * NLP;
+  auto wrap = [&](int y) -> int {  // flat offset of row y (any integer) at column gx
     int r = y % ny;
     if (r < 0) r += ny;
     return r * nx + gx;
   };
-  auto SM = [&](int t, int par) -> double* { return sm + (t * 2 + par) * W; };
-
   double ulo[NL], uce[NL], vin[NL], kin[NL], ain[NL];
 #pragma unroll
   for (int t = 0; t < NL; ++t) ulo[t] = uce[t] = vin[t] = kin[t] = ain[t] = 0.0;
-  ulo[0] = U[rowp(ystart - 1)];
-  uce[0] = U[rowp(ystart)];
-  SM(0, 0)[j] = uce[0];
-  // level-0 inputs, prefetched two iterations ahead: u_0[r0+1], udot_0[r0], coef[r0]
-  double pu0 = U[rowp(ystart + 1)], pv0 = V[rowp(ystart)], pk0 = K[rowp(ystart)];
-  double pu1 = U[rowp(ystart + 2)], pv1 = V[rowp(ystart + 1)], pk1 = K[rowp(ystart + 1)];
+  ulo[0] = U[wrap(ystart - 1)];
+  uce[0] = U[wrap(ystart)];
+  sbase[0] = uce[0];  // parity 0, level 0
+  // running offsets: look-ahead u row (ystart+i+1), v/k row (ystart+i), output row (ystart+i-S)
+  int ou = wrap(ystart + 1), ov = wrap(ystart), oo = wrap(ystart - S);
+  auto adv = [npts, nx](int& o) {
+    o += nx;
+    if (o >= npts) o -= npts;
+  };
+  // level-0 inputs stream through a cp.async ring of RING rows (prefetch distance RING-1):
+  // slot s holds {u_0[ystart+i+1], udot_0[ystart+i], coef[ystart+i]} for iteration i = s mod RING
+  double* ring = sm + 2 * sstride_par;  // [RING][3][W]
+  auto issue = [&](int slot) {
+    double* d = ring + (slot * 3) * W + j;
+    cp_async8(d, U + ou);
+    cp_async8(d + W, V + ov);
+    cp_async8(d + 2 * W, K + ov);
+    cp_async_commit();
+    adv(ou);
+    adv(ov);
+  };
+#pragma unroll
+  for (int s0 = 0; s0 < RING - 1; ++s0) issue(s0);
   __syncthreads();
   bool ok = true;
-  for (int i = 0; i < n_iter; ++i) {
-    const int par = i & 1, npar = par ^ 1;
-    const double uu0 = pu0, v0 = pv0, k0 = pk0;
-    pu0 = pu1;
-    pv0 = pv1;
-    pk0 = pk1;
-    if (i + 2 < n_iter) {
-      pu1 = U[rowp(ystart + i + 3)];
-      pv1 = V[rowp(ystart + i + 2)];
-      pk1 = K[rowp(ystart + i + 2)];
-    }
-    // ---- level 0: a_0 / b_0 at row ystart+i, produce u_1 at that row
-    double up, cv, ck, ca;  // carries to level 1: u_1[r], velocity, coef, (EXACT) a_0
-    {
-      const double uc = uce[0], ud = ulo[0], ul = SM(0, par)[jl], ur = SM(0, par)[jr];
-      SM(0, npar)[j] = uu0;
-      if (EXACT) {
-        const double a0 = __dmul_rn(lap_exact<true>(uc, ul, ur, uu0, ud, p), k0);
-        up = __dadd_rn(uc, __dadd_rn(__dmul_rn(p.dt, v0), __dmul_rn(p.hdt2, a0)));
-        cv = v0;
-        ca = a0;
-      } else {
-        const double vh = v0 + bfast<true>(uc, ul, ur, uu0, ud, k0, p);
-        up = fma(p.dt, vh, uc);
-        cv = vh;
-        ca = 0.0;
-      }
-      ck = k0;
-      SM(1, npar)[j] = up;
-      ulo[0] = uc;
-      uce[0] = uu0;
-    }
-    // ---- levels 1..S: level t finalises step t at row ystart+i-t
+  const int last_out = nrows + 2 * S;  // outputs are iterations [2S, nrows+2S)
+  for (int i0 = 0; i0 < n_iter; i0 += UNROLL) {
 #pragma unroll
-    for (int t = 1; t <= S; ++t) {
-      const double vprev = vin[t], kt = kin[t], aprev = ain[t];
-      vin[t] = cv;  // inputs of level t for the next iteration (row advances by one)
-      kin[t] = ck;
-      ain[t] = ca;
-      const double uu = up;
-      if (i >= 2 * t) {  // warp-uniform; before that the level's rows are warm-up only
-        const double uc = uce[t], ud = ulo[t], ul = SM(t, par)[jl], ur = SM(t, par)[jr];
-        if (EXACT) {
-          const double an = __dmul_rn(lap_exact<true>(uc, ul, ur, uu, ud, p), kt);
-          const double vn = __dadd_rn(vprev, __dmul_rn(p.hd, __dadd_rn(aprev, an)));
-          if (t < S) {
-            up = __dadd_rn(uc, __dadd_rn(__dmul_rn(p.dt, vn), __dmul_rn(p.hdt2, an)));
-            cv = vn;
-            ca = an;
-            ck = kt;
-            SM(t + 1, npar)[j] = up;
-          } else if (col_out) {
-            const int o = rowp(ystart + i - S);
-            UO[o] = uc;
-            VO[o] = vn;
-            ok &= finite2(uc, vn);
-          }
-        } else {
-          const double b = bfast<true>(uc, ul, ur, uu, ud, kt, p);
-          if (t < S) {
-            const double vh = fma(2.0, b, vprev);
-            up = fma(p.dt, vh, uc);
-            cv = vh;
-            ck = kt;
-            SM(t + 1, npar)[j] = up;
-          } else if (col_out) {
-            const double vS = vprev + b;
-            const int o = rowp(ystart + i - S);
-            UO[o] = uc;
-            VO[o] = vS;
-            ok &= finite2(uc, vS);
-          }
-        }
+    for (int k = 0; k < UNROLL; ++k) {
+      const int i = i0 + k;
+      cp_async_wait<RING - 2>();
+      const double* src = ring + ((k % RING) * 3) * W + j;
+      const double uu0 = src[0], v0 = src[W], k0 = src[2 * W];
+      issue((k + RING - 1) % RING);
+      double out_u, out_v;
+      if (k & 1)
+        wave_iter<S, EXACT, 1>(sbase, sstride_par, p, ulo, uce, vin, kin, ain, uu0, v0, k0, out_u, out_v);
+      else
+        wave_iter<S, EXACT, 0>(sbase, sstride_par, p, ulo, uce, vin, kin, ain, uu0, v0, k0, out_u, out_v);
+      if (col_out && i >= 2 * S && i < last_out) {
+        UO[oo] = out_u;
+        VO[oo] = out_v;
+        ok &= finite2(out_u, out_v);
       }
-      ulo[t] = uce[t];
-      uce[t] = uu;
+      adv(oo);
+      __syncthreads();
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
   if (a.flags) {
     const int bad = __syncthreads_or(!ok);
-    if (bad && j == 0) atomicOr(&a.flags[blockIdx.z], 1);
+    if (bad && j == 0) atomicOr(&a.flags[blockIdx.x], 1);
   }
 }
 
@@ -460,17 +529,32 @@ WavePlan plan_wave(ptb_context* ctx, int ny, int nx, int S, size_t batch) {
       if (rb <= 1) break;
     }
   }
+  // tuning overrides (measurement only): PTB_WAVE_W=<threads>, PTB_WAVE_DIV=<row blocks>
+  if (const char* e = std::getenv("PTB_WAVE_W"); e && std::atoi(e) > 0) {
+    const int W = std::atoi(e);
+    const int wu_max = W - 2 * HX;
+    if (W >= 64 && W <= 512 && wu_max >= 16) {
+      best.W = W;
+      best.strips = (nx + wu_max - 1) / wu_max;
+      best.wu = (nx + best.strips - 1) / best.strips;
+    }
+  }
+  if (const char* e = std::getenv("PTB_WAVE_DIV"); e && std::atoi(e) > 0) {
+    const int div = std::atoi(e);
+    best.rb = (ny + div - 1) / div;
+    best.nrb = (ny + best.rb - 1) / best.rb;
+  }
   return best;
 }
 
 template <int S, bool EXACT>
 void launch_wave(ptb_context* ctx, cudaStream_t st, const WavePlan& pl, WaveArgs a, size_t batch) {
-  const size_t smem = size_t(S + 1) * 2 * pl.W * sizeof(double);
+  const size_t smem = (size_t((S + 1) | 1) * 2 * (pl.W + 2) + size_t(6) * 3 * pl.W) * sizeof(double);
   auto kern = k_wave<S, EXACT>;
   PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   a.wu = pl.wu;
   a.rb = pl.rb;
-  dim3 grid(pl.strips, pl.nrb, static_cast<unsigned>(batch));
+  dim3 grid(static_cast<unsigned>(batch), pl.strips, pl.nrb);
   kern<<<grid, pl.W, smem, st>>>(a);
   PTB_LAUNCH_CHECK(ctx);
 }
