@@ -120,6 +120,93 @@ ptb_status ptb_interpolate_batch(ptb_transfer* t, size_t batch, const double* co
 ptb_status ptb_nonfinite_batch(ptb_context* ctx, size_t n, size_t batch, const double* f_dev,
                                int32_t* flags_dev);
 
+/* ---- energy map (energy_map.hpp:32-53) ----------------------------------------------- */
+/* Lambda: `batch` states -> stacked columns [grad axis 0; (grad axis 1;) udot/c] (column b at
+ * stacked_dev + b*ld) and mean_u[b] = sum(u) (nullable).  c_dev: speed on `grid`. */
+ptb_status ptb_energy_components_batch(ptb_context* ctx, const ptb_grid* grid, const double* c_dev, int scheme,
+                                       size_t batch, const double* u_dev, const double* udot_dev,
+                                       double* stacked_dev, size_t ld, double* mean_dev);
+/* Lambda-dagger (from_energy_components): stacked columns + mean_u -> states */
+ptb_status ptb_from_energy_components_batch(ptb_context* ctx, const ptb_grid* grid, const double* c_dev,
+                                            size_t batch, const double* stacked_dev, size_t ld,
+                                            const double* mean_dev, double* u_dev, double* udot_dev);
+/* per state pair b: sums4[4b..] = {|Lambda(a-b)|^2, |Lambda(b)|^2, |u_a-u_b|^2, |u_b|^2}; energy,
+ * energy_error and l2_error (energy_map.cpp:216-249) are closed forms of these sums */
+ptb_status ptb_energy_sums_batch(ptb_context* ctx, const ptb_grid* grid, const double* c_dev, int scheme,
+                                 size_t batch, const double* ua_dev, const double* udota_dev, const double* ub_dev,
+                                 const double* udotb_dev, double* sums4_dev);
+/* in-place complex DFT of `batch` fields (interleaved re/im), fft.hpp conventions */
+ptb_status ptb_dft_batch(ptb_context* ctx, const ptb_grid* grid, size_t batch, double* data_dev, int inverse);
+
+/* ---- Procrustes corrector (procrustes.hpp:22-81) ----------------------------------------- */
+typedef struct ptb_corrector ptb_corrector;
+/* an empty corrector (no accumulated data yet) */
+ptb_status ptb_corrector_create(ptb_context* ctx, ptb_corrector** out);
+ptb_status ptb_corrector_destroy(ptb_corrector* c);
+/* update_svd (procrustes.cpp:188-237) in place; F, G: rows x cols column-major device, ld = rows */
+ptb_status ptb_corrector_update(ptb_corrector* c, size_t rows, size_t cols, const double* F_dev, const double* G_dev,
+                                double tol);
+/* procrustes_solve (procrustes.cpp:177-186): validates shapes, then solves into c (reset) */
+ptb_status ptb_procrustes_solve(ptb_corrector* c, size_t rows, size_t cols, const double* F_dev, const double* G_dev,
+                                double tol);
+ptb_status ptb_corrector_shape(ptb_corrector* c, size_t* rows, size_t* rank);
+/* copy factors to host: X, Y rows x rank column-major, S rank */
+ptb_status ptb_corrector_factors(ptb_corrector* c, double* X_host, double* S_host, double* Y_host);
+/* out = copy with the first `count` triplets dropped (drop_leading) */
+ptb_status ptb_corrector_drop_leading(ptb_corrector* c, size_t count, ptb_corrector** out);
+/* out[:, b] = X (Y^T in[:, b]) for `batch` columns of length rows (apply, procrustes.cpp:82-86) */
+ptb_status ptb_corrector_apply_batch(ptb_corrector* c, size_t batch, const double* in_dev, double* out_dev);
+ptb_status ptb_relative_residual(ptb_corrector* c, size_t rows, size_t cols, const double* F_dev,
+                                 const double* G_dev, double* out);
+
+/* ---- parareal drivers (parareal.hpp:60-79) -------------------------------------------- */
+typedef enum { PTB_PLAIN = 0, PTB_THETA = 1, PTB_CORRECTED_COARSE_ONLY = 2, PTB_OMEGA_IDENTITY = 3 } ptb_variant;
+
+/* A CouplingSchedule + GridTransfer + options (parareal.hpp:17-57, experiment.hpp:20-44). */
+typedef struct {
+  int dim;
+  size_t fine_n[2];
+  double fine_h[2];
+  size_t coarse_n[2];
+  double coarse_h[2];
+  double dt_fine;
+  size_t m_fine;
+  double dt_coarse;
+  size_t m_coarse;
+  double T;
+  double dt_com;
+  size_t n_couplings;
+  int interp;         /* ptb_interp */
+  int iterations;     /* K correction passes */
+  int variant;        /* ptb_variant */
+  int scheme;         /* data-matrix gradient (ThetaOptions::scheme) */
+  int metric_scheme;  /* error seminorm (DriverOptions::metric_scheme) */
+  double tol;         /* truncation tolerance */
+  int remove_leading; /* singular triplets dropped before each sweep */
+  int mode;           /* ptb_mode of the fine and coarse propagators */
+} ptb_run_spec;
+
+#define PTB_MAX_TIMED_ITERS 64
+/* device-timed phases per iteration k = 1..K (CUDA events on the context stream) */
+typedef struct {
+  double reference_ms; /* serial fine reference (once per run) */
+  double parallel_ms[PTB_MAX_TIMED_ITERS];
+  double procrustes_ms[PTB_MAX_TIMED_ITERS];
+  double sweep_ms[PTB_MAX_TIMED_ITERS];
+  double finalize_ms[PTB_MAX_TIMED_ITERS];
+  double iteration_ms[PTB_MAX_TIMED_ITERS];
+} ptb_phase_times;
+
+/* plain_parareal / theta_parareal / corrected_coarse_only on one device.  Host inputs:
+ * c_fine (fine N), c_coarse (coarse N), init (u0, udot0 on the fine grid).  Outputs (host):
+ * energy_err, l2_err: (K+1)*(N+1) row-major [k][n]; residual, rank, diverged: K+1;
+ * states (nullable): (K+1)*(N+1)*2*Nf as [k][n][u|udot][pt]; reference (nullable): (N+1)*2*Nf;
+ * times (nullable). */
+ptb_status ptb_parareal_run(ptb_context* ctx, const ptb_run_spec* spec, const double* c_fine,
+                            const double* c_coarse, const double* u0, const double* udot0, double* energy_err,
+                            double* l2_err, double* residual, int* rank, int* diverged, double* states,
+                            double* reference, ptb_phase_times* times);
+
 /* ---- measurement helpers (bench.py) ---------------------------------------------- */
 /* Peak fp64 FMA throughput of the device: independent DFMA chains on every SM, timed
  * with CUDA events; returns TFLOP/s (2 flops per FMA) and the kernel time. */

@@ -212,3 +212,170 @@ class Transfer:
         out = self.ctx.torch.empty((batch,) + self.fine.shape, dtype=f.dtype, device=f.device)
         check(lib().ptb_interpolate_batch(self.h, C.c_size_t(batch), _ptr(f), _ptr(out)))
         return out
+
+
+# ---------------------------------------------------------------- energy map / DFT
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def energy_components(ctx: Context, grid: Grid, c_dev, scheme: int, u, udot):
+    """Lambda on `batch` device states -> (stacked (batch, (d+1)N), mean (batch,))."""
+    batch = u.numel() // grid.size
+    rows = (grid.dim + 1) * grid.size
+    out = ctx.torch.empty((batch, rows), dtype=ctx.torch.float64, device=u.device)
+    mean = ctx.torch.empty(batch, dtype=ctx.torch.float64, device=u.device)
+    check(lib().ptb_energy_components_batch(ctx.h, C.byref(grid.c()), _ptr(c_dev), C.c_int(scheme), C.c_size_t(batch),
+                                            _ptr(u), _ptr(udot), _ptr(out), C.c_size_t(rows), _ptr(mean)))
+    return out, mean
+
+
+def from_energy_components(ctx: Context, grid: Grid, c_dev, stacked, mean):
+    batch = stacked.shape[0]
+    rows = (grid.dim + 1) * grid.size
+    u = ctx.torch.empty((batch,) + grid.shape, dtype=ctx.torch.float64, device=stacked.device)
+    v = ctx.torch.empty_like(u)
+    check(lib().ptb_from_energy_components_batch(ctx.h, C.byref(grid.c()), _ptr(c_dev), C.c_size_t(batch),
+                                                 _ptr(stacked), C.c_size_t(rows), _ptr(mean), _ptr(u), _ptr(v)))
+    return u, v
+
+
+def energy_sums(ctx: Context, grid: Grid, c_dev, scheme: int, ua, va, ub, vb):
+    batch = ua.numel() // grid.size
+    out = ctx.torch.empty((batch, 4), dtype=ctx.torch.float64, device=ua.device)
+    check(lib().ptb_energy_sums_batch(ctx.h, C.byref(grid.c()), _ptr(c_dev), C.c_int(scheme), C.c_size_t(batch),
+                                      _ptr(ua), _ptr(va), _ptr(ub), _ptr(vb), _ptr(out)))
+    return out
+
+
+def dft(ctx: Context, grid: Grid, data_complex, inverse=False):
+    """In-place DFT of a complex128 device tensor (batch, *grid.shape)."""
+    batch = data_complex.numel() // grid.size
+    check(lib().ptb_dft_batch(ctx.h, C.byref(grid.c()), C.c_size_t(batch), _ptr(data_complex), C.c_int(int(inverse))))
+    return data_complex
+
+
+# ---------------------------------------------------------------- Procrustes corrector
+
+
+class Corrector:
+    """PhaseCorrector (procrustes.hpp:22-60) with device-resident factors."""
+
+    def __init__(self, ctx: Context, handle=None):
+        self.ctx = ctx
+        if handle is None:
+            handle = C.c_void_p()
+            check(lib().ptb_corrector_create(ctx.h, C.byref(handle)))
+        self.h = handle
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ptb_corrector_destroy(self.h)
+        except Exception:
+            pass
+
+    def update(self, F, G, tol: float):
+        """update_svd in place; F, G: device (cols, rows) tensors = column-major rows x cols."""
+        cols, rows = F.shape
+        check(lib().ptb_corrector_update(self.h, C.c_size_t(rows), C.c_size_t(cols), _ptr(F), _ptr(G), C.c_double(tol)))
+        return self
+
+    def solve(self, F, G, tol: float):
+        cols, rows = F.shape
+        check(lib().ptb_procrustes_solve(self.h, C.c_size_t(rows), C.c_size_t(cols), _ptr(F), _ptr(G), C.c_double(tol)))
+        return self
+
+    def shape(self):
+        r, k = C.c_size_t(), C.c_size_t()
+        check(lib().ptb_corrector_shape(self.h, C.byref(r), C.byref(k)))
+        return r.value, k.value
+
+    def factors(self):
+        rows, rank = self.shape()
+        X = np.empty((rank, rows))
+        Y = np.empty((rank, rows))
+        S = np.empty(rank)
+        check(lib().ptb_corrector_factors(self.h, _dp(X), _dp(S), _dp(Y)))
+        return X.T.copy(), S, Y.T.copy()
+
+    def drop_leading(self, count: int) -> "Corrector":
+        out = C.c_void_p()
+        check(lib().ptb_corrector_drop_leading(self.h, C.c_size_t(count), C.byref(out)))
+        return Corrector(self.ctx, out)
+
+    def apply(self, V):
+        """V: device (batch, rows) -> X (Y^T v) per row vector."""
+        out = self.ctx.torch.empty_like(V)
+        check(lib().ptb_corrector_apply_batch(self.h, C.c_size_t(V.shape[0]), _ptr(V), _ptr(out)))
+        return out
+
+    def residual(self, F, G) -> float:
+        cols, rows = F.shape
+        out = C.c_double()
+        check(lib().ptb_relative_residual(self.h, C.c_size_t(rows), C.c_size_t(cols), _ptr(F), _ptr(G), C.byref(out)))
+        return out.value
+
+
+# ---------------------------------------------------------------- drivers
+
+PLAIN, THETA, CORRECTED_COARSE_ONLY, OMEGA_IDENTITY = range(4)
+MAX_TIMED = 64
+
+
+class RunSpec(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("fine_n", C.c_size_t * 2), ("fine_h", C.c_double * 2), ("coarse_n", C.c_size_t * 2),
+        ("coarse_h", C.c_double * 2), ("dt_fine", C.c_double), ("m_fine", C.c_size_t), ("dt_coarse", C.c_double),
+        ("m_coarse", C.c_size_t), ("T", C.c_double), ("dt_com", C.c_double), ("n_couplings", C.c_size_t),
+        ("interp", C.c_int), ("iterations", C.c_int), ("variant", C.c_int), ("scheme", C.c_int),
+        ("metric_scheme", C.c_int), ("tol", C.c_double), ("remove_leading", C.c_int), ("mode", C.c_int),
+    ]
+
+
+class PhaseTimes(C.Structure):
+    _fields_ = [("reference_ms", C.c_double), ("parallel_ms", C.c_double * MAX_TIMED),
+                ("procrustes_ms", C.c_double * MAX_TIMED), ("sweep_ms", C.c_double * MAX_TIMED),
+                ("finalize_ms", C.c_double * MAX_TIMED), ("iteration_ms", C.c_double * MAX_TIMED)]
+
+
+def run_spec(**kw) -> RunSpec:
+    s = RunSpec()
+    for k, v in kw.items():
+        if k in ("fine_n", "coarse_n", "fine_h", "coarse_h"):
+            arr = getattr(s, k)
+            arr[0] = v[0]
+            arr[1] = v[1] if len(v) > 1 else (1 if "n" in k else 1.0)
+        else:
+            setattr(s, k, v)
+    return s
+
+
+def parareal_run(ctx: Context, spec: RunSpec, c_fine, c_coarse, u0, udot0, keep_states=False,
+                 keep_reference=False):
+    """plain / theta / corrected-coarse-only parareal on the device (parareal.cpp)."""
+    K, N = spec.iterations, spec.n_couplings
+    fine_shape = (spec.fine_n[0],) if spec.dim == 1 else (spec.fine_n[0], spec.fine_n[1])
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+    cf, cc, u0, v0 = f(c_fine), f(c_coarse), f(u0), f(udot0)
+    ee = np.empty((K + 1, N + 1))
+    l2 = np.empty((K + 1, N + 1))
+    res = np.empty(K + 1)
+    rank = np.empty(K + 1, dtype=np.int32)
+    div = np.empty(K + 1, dtype=np.int32)
+    states = np.empty((K + 1, N + 1, 2) + fine_shape) if keep_states else None
+    ref = np.empty((N + 1, 2) + fine_shape) if keep_reference else None
+    times = PhaseTimes()
+    ip = C.POINTER(C.c_int)
+    check(lib().ptb_parareal_run(ctx.h, C.byref(spec), _dp(cf), _dp(cc), _dp(u0), _dp(v0), _dp(ee), _dp(l2), _dp(res),
+                                 rank.ctypes.data_as(ip), div.ctypes.data_as(ip),
+                                 _dp(states) if states is not None else None, _dp(ref) if ref is not None else None,
+                                 C.byref(times)))
+    k = min(K, MAX_TIMED)
+    t = {"reference_ms": times.reference_ms}
+    for name in ("parallel_ms", "procrustes_ms", "sweep_ms", "finalize_ms", "iteration_ms"):
+        t[name] = list(getattr(times, name))[:k]
+    return dict(energy_err=ee, l2_err=l2, residual=res, rank=rank, diverged=div, states=states, reference=ref,
+                times=t)

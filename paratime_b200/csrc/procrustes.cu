@@ -1,0 +1,748 @@
+// Energy-norm Procrustes corrector on the device (K5/K6).
+//
+// Reference: /root/reference/proj/src/procrustes.cpp
+//   check_tol            :14-17    tol in (0, 1)
+//   fix_signs            :21-30    largest-|.| entry of each left column positive (first max)
+//   truncated_qr         :34-46    column-pivoted thin QR, R un-pivoted, keep leading |R_ii| > guard
+//   solve_from_scratch   :48-69    SVD(R_F R_G^T), keep sigma_i/sigma_1 > tol, X = Q_F U, Y = Q_G V
+//   apply / drop_leading :82-93
+//   update_svd           :188-237  Algorithm 1
+//   relative_residual    :245-253
+//
+// Kernels written here (sm_100a):
+//   k_qrcp      cooperative column-pivoted Householder QR of a tall m x n block: every CTA
+//               owns a row range; per column one grid barrier reduces the remaining column
+//               norms (fused into the previous update), picks the pivot (max remaining
+//               norm, first index on ties — the dgeqp3 rule with exact instead of downdated
+//               norms), forms the reflector (dlarfg), and a second barrier reduces v^T A.
+//               Stops at the first |R_jj| <= guard (the reference's keep rule).
+//   k_qr_formq  cooperative backward accumulation Q = H_0 ... H_{keep-1} [I; 0].
+//   k_jacobi    one-sided (Hestenes) Jacobi SVD in a single CTA, round-robin pair
+//               ordering, rotations until every pair is orthogonal to ~eps; singular
+//               values sorted descending.
+//   k_fix_signs one CTA per column.
+// Large products (U^T F, U UF, [U Q_F] Xh, X(Y^T v)) are plain cuBLAS DGEMMs.
+
+#include <cooperative_groups.h>
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ptb_procrustes.h"
+
+namespace cg = cooperative_groups;
+
+namespace ptb {
+namespace {
+
+constexpr int QR_THREADS = 256;
+
+struct QrArgs {
+  double* A;  // m x n column-major, lda = m
+  int m, n;
+  double drop_tol;
+  double* tau;     // n
+  int* perm;       // n (pivoted column j = original column perm[j])
+  double* part;    // [2][grid][n+1] partial sums
+  int* keep_out;   // 1
+  double* beta_out;  // n (|R_jj| sequence, for diagnostics)
+};
+
+__device__ double cta_reduce(double x, double* red) {
+  // fixed-order tree over QR_THREADS values
+  red[threadIdx.x] = x;
+  __syncthreads();
+  for (int s = QR_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sh[];  // red[QR_THREADS] | w[n] | nrm[n]
+  double* red = sh;
+  double* w = red + QR_THREADS;
+  double* nrm = w + a.n;
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int m = a.m, n = a.n;
+  const int rows_per = (m + G - 1) / G;
+  const int r0 = min(m, g * rows_per), r1 = min(m, r0 + rows_per);
+  double* A = a.A;
+  auto col = [&](int k) { return A + size_t(k) * m; };
+  // initial column norms (squared), partial per CTA
+  double* part0 = a.part;  // parity 0
+  for (int k = 0; k < n; ++k) {
+    double s = 0.0;
+    for (int i = r0 + tid; i < r1; i += QR_THREADS) s += col(k)[i] * col(k)[i];
+    s = cta_reduce(s, red);
+    if (tid == 0) part0[size_t(g) * (n + 1) + k] = s;
+  }
+  if (g == 0)
+    for (int k = tid; k < n; k += QR_THREADS) a.perm[k] = k;
+  int keep = 0;
+  bool stopped = false;
+  for (int j = 0; j < n && j < m; ++j) {
+    double* part = a.part + size_t(j & 1) * G * (n + 1);
+    double* partn = a.part + size_t((j + 1) & 1) * G * (n + 1);
+    grid.sync();
+    // remaining squared norms of columns k >= j (rows >= j), fixed-order reduction
+    for (int k = j + tid; k < n; k += QR_THREADS) {
+      double s = 0.0;
+      for (int c = 0; c < G; ++c) s += part[size_t(c) * (n + 1) + k];
+      nrm[k] = s;
+    }
+    __syncthreads();
+    // pivot: max remaining norm, first index on ties (idamax)
+    int p = j;
+    double best = nrm[j];
+    for (int k = j + 1; k < n; ++k)
+      if (nrm[k] > best) {
+        best = nrm[k];
+        p = k;
+      }
+    // swap columns j and p (own rows), and the permutation
+    if (p != j) {
+      for (int i = r0 + tid; i < r1; i += QR_THREADS) {
+        const double t = col(j)[i];
+        col(j)[i] = col(p)[i];
+        col(p)[i] = t;
+      }
+      if (g == 0 && tid == 0) {
+        const int t = a.perm[j];
+        a.perm[j] = a.perm[p];
+        a.perm[p] = t;
+      }
+    }
+    // reflector for column j rows j..m-1 (dlarfg): alpha = A[j][j], xnorm^2 = nrm - alpha^2
+    // is cancellation-prone, so the below-diagonal norm comes from its own partial.
+    __syncthreads();
+    double xs = 0.0;
+    for (int i = max(r0, j + 1) + tid; i < r1; i += QR_THREADS) xs += col(j)[i] * col(j)[i];
+    xs = cta_reduce(xs, red);
+    if (tid == 0) partn[size_t(g) * (n + 1) + n] = xs;
+    grid.sync();
+    double xnorm2 = 0.0;
+    for (int c = 0; c < G; ++c) xnorm2 += partn[size_t(c) * (n + 1) + n];
+    const double alpha = col(j)[j];
+    const double xnorm = sqrt(xnorm2);
+    double beta, tau, scal;
+    if (xnorm == 0.0) {
+      beta = alpha;
+      tau = 0.0;
+      scal = 0.0;
+    } else {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (fabs(beta) <= a.drop_tol) {  // first pivot at or below the guard: stop (keep = j)
+      stopped = true;
+      if (g == 0 && tid == 0) a.beta_out[j] = fabs(beta);
+      break;
+    }
+    keep = j + 1;
+    if (g == 0 && tid == 0) {
+      a.tau[j] = tau;
+      a.beta_out[j] = fabs(beta);
+    }
+    // v (stored below the diagonal) and R_jj
+    for (int i = max(r0, j + 1) + tid; i < r1; i += QR_THREADS) col(j)[i] *= scal;
+    // w_k = A[j][k] + sum_{i>j} v_i A[i][k], k > j  (own-row partials)
+    for (int k = j + 1; k < n; ++k) {
+      double s = 0.0;
+      for (int i = max(r0, j) + tid; i < r1; i += QR_THREADS) s += (i == j ? 1.0 : col(j)[i]) * col(k)[i];
+      s = cta_reduce(s, red);
+      if (tid == 0) part[size_t(g) * (n + 1) + k] = s;
+    }
+    grid.sync();
+    for (int k = j + 1 + tid; k < n; k += QR_THREADS) {
+      double s = 0.0;
+      for (int c = 0; c < G; ++c) s += part[size_t(c) * (n + 1) + k];
+      w[k] = s;
+    }
+    __syncthreads();
+    if (j >= r0 && j < r1 && tid == 0) col(j)[j] = beta;
+    // update A[i][k] -= tau v_i w_k (i >= j), and fuse the remaining norms (rows >= j+1)
+    for (int k = j + 1; k < n; ++k) {
+      const double tw = tau * w[k];
+      double s = 0.0;
+      for (int i = max(r0, j) + tid; i < r1; i += QR_THREADS) {
+        const double v = (i == j) ? 1.0 : col(j)[i];
+        const double x = col(k)[i] - tw * v;
+        col(k)[i] = x;
+        if (i > j) s += x * x;
+      }
+      s = cta_reduce(s, red);
+      if (tid == 0) partn[size_t(g) * (n + 1) + k] = s;
+    }
+  }
+  (void)stopped;
+  if (g == 0 && tid == 0) *a.keep_out = keep;
+}
+
+struct FormQArgs {
+  const double* A;  // reflectors below the diagonal (m x n, lda m)
+  const double* tau;
+  int m, keep;
+  double* Q;       // m x keep
+  double* part;    // [2][grid][keep]
+};
+
+__global__ void __launch_bounds__(QR_THREADS) k_qr_formq(FormQArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sh[];
+  double* red = sh;
+  double* w = red + QR_THREADS;
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int m = a.m, K = a.keep;
+  const int rows_per = (m + G - 1) / G;
+  const int r0 = min(m, g * rows_per), r1 = min(m, r0 + rows_per);
+  for (int c = 0; c < K; ++c)
+    for (int i = r0 + tid; i < r1; i += QR_THREADS) a.Q[size_t(c) * m + i] = (i == c) ? 1.0 : 0.0;
+  for (int j = K - 1; j >= 0; --j) {
+    const double* v = a.A + size_t(j) * m;
+    double* part = a.part + size_t(j & 1) * G * K;
+    for (int c = j; c < K; ++c) {
+      double s = 0.0;
+      for (int i = max(r0, j) + tid; i < r1; i += QR_THREADS) s += (i == j ? 1.0 : v[i]) * a.Q[size_t(c) * m + i];
+      s = cta_reduce(s, red);
+      if (tid == 0) part[size_t(g) * K + c] = s;
+    }
+    grid.sync();
+    for (int c = j + tid; c < K; c += QR_THREADS) {
+      double s = 0.0;
+      for (int q = 0; q < G; ++q) s += part[size_t(q) * K + c];
+      w[c] = s;
+    }
+    __syncthreads();
+    const double tau = a.tau[j];
+    for (int c = j; c < K; ++c) {
+      const double tw = tau * w[c];
+      for (int i = max(r0, j) + tid; i < r1; i += QR_THREADS) a.Q[size_t(c) * m + i] -= tw * (i == j ? 1.0 : v[i]);
+    }
+  }
+}
+
+// R (keep x n) = upper rows of the pivoted factor, un-pivoted: R[:, perm[k]] = Rp[:, k]
+__global__ void k_unpivot_r(const double* A, int m, int n, int keep, const int* perm, double* R) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < keep * n; e += gridDim.x * blockDim.x) {
+    const int k = e / keep, i = e - k * keep;  // pivoted column k, row i
+    R[size_t(perm[k]) * keep + i] = (i <= k) ? A[size_t(k) * m + i] : 0.0;
+  }
+}
+
+// ---- one-sided Jacobi SVD, single CTA ------------------------------------------------
+
+struct JacobiArgs {
+  double* A;  // r x c column-major (r >= c), overwritten by U*Sigma then U
+  double* V;  // c x c
+  int r, c;
+  double* sigma;  // c (sorted desc)
+  int* order;     // c scratch
+  double* tmp;    // r*c + c*c scratch for the sorted copies
+  int max_sweeps;
+};
+
+__device__ __forceinline__ double warp_sum(double x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
+  const int r = a.r, c = a.c;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  __shared__ int rotated;
+  // V = I
+  for (int e = threadIdx.x; e < c * c; e += blockDim.x) a.V[e] = (e % (c + 1) == 0) ? 1.0 : 0.0;
+  const int cc = (c % 2 == 0) ? c : c + 1;  // tournament size (dummy column when odd)
+  const double eps = 2.220446049250313e-16;
+  const double tol = eps * sqrt(double(r));
+  __syncthreads();
+  for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < cc - 1; ++round) {
+      for (int pr = warp; pr < cc / 2; pr += nwarps) {
+        // round-robin pairing: position 0 fixed, others rotate
+        auto pos = [&](int q) { return q == 0 ? 0 : 1 + (q - 1 + round) % (cc - 1); };
+        int i = pos(pr), j = pos(cc - 1 - pr);
+        if (i > j) {
+          const int t = i;
+          i = j;
+          j = t;
+        }
+        if (j >= c) continue;  // dummy
+        double* ai = a.A + size_t(i) * r;
+        double* aj = a.A + size_t(j) * r;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int k = lane; k < r; k += 32) {
+          const double x = ai[k], y = aj[k];
+          al += x * x;
+          be += y * y;
+          ga += x * y;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (fabs(ga) > tol * sqrt(al) * sqrt(be) && ga != 0.0) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          for (int k = lane; k < r; k += 32) {
+            const double x = ai[k], y = aj[k];
+            ai[k] = cs * x - sn * y;
+            aj[k] = sn * x + cs * y;
+          }
+          double* vi = a.V + size_t(i) * c;
+          double* vj = a.V + size_t(j) * c;
+          for (int k = lane; k < c; k += 32) {
+            const double x = vi[k], y = vj[k];
+            vi[k] = cs * x - sn * y;
+            vj[k] = sn * x + cs * y;
+          }
+          if (lane == 0) rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // singular values and descending order (stable: ties keep the lower index first)
+  for (int k = warp; k < c; k += nwarps) {
+    double s = 0.0;
+    for (int q = lane; q < r; q += 32) s += a.A[size_t(k) * r + q] * a.A[size_t(k) * r + q];
+    s = warp_sum(s);
+    if (lane == 0) a.tmp[size_t(r) * c + size_t(c) * c + k] = sqrt(s);
+  }
+  __syncthreads();
+  const double* sv = a.tmp + size_t(r) * c + size_t(c) * c;
+  for (int k = threadIdx.x; k < c; k += blockDim.x) {
+    int rank = 0;
+    for (int q = 0; q < c; ++q)
+      if (sv[q] > sv[k] || (sv[q] == sv[k] && q < k)) ++rank;
+    a.order[rank] = k;
+  }
+  __syncthreads();
+  // sorted copies: U columns normalised (zero column when sigma = 0)
+  for (int e = threadIdx.x; e < r * c; e += blockDim.x) {
+    const int k = e / r, q = e - k * r;
+    const int src = a.order[k];
+    const double s = sv[src];
+    a.tmp[e] = s > 0.0 ? a.A[size_t(src) * r + q] / s : 0.0;
+  }
+  for (int e = threadIdx.x; e < c * c; e += blockDim.x) {
+    const int k = e / c, q = e - k * c;
+    a.tmp[size_t(r) * c + e] = a.V[size_t(a.order[k]) * c + q];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * c; e += blockDim.x) a.A[e] = a.tmp[e];
+  for (int e = threadIdx.x; e < c * c; e += blockDim.x) a.V[e] = a.tmp[size_t(r) * c + e];
+  for (int k = threadIdx.x; k < c; k += blockDim.x) a.sigma[k] = sv[a.order[k]];
+}
+
+__global__ void k_transpose(const double* in, int rows, int cols, double* out) {
+  // in: rows x cols (col-major) -> out: cols x rows
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int j = e / rows, i = e - j * rows;
+    out[size_t(i) * cols + j] = in[e];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fix_signs(double* X, double* Y, int rows) {
+  const int j = blockIdx.x;
+  double* x = X + size_t(j) * rows;
+  double* y = Y + size_t(j) * rows;
+  __shared__ double bv[256];
+  __shared__ int bi[256];
+  double best = -1.0;
+  int idx = 0;
+  for (int i = threadIdx.x; i < rows; i += 256) {
+    const double a = fabs(x[i]);
+    if (a > best) {  // strictly greater: first maximum within the thread's stride
+      best = a;
+      idx = i;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = idx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double o = bv[threadIdx.x + s];
+      const int oi = bi[threadIdx.x + s];
+      if (o > bv[threadIdx.x] || (o == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+        bv[threadIdx.x] = o;
+        bi[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  const bool flip = rows > 0 && x[bi[0]] < 0.0;
+  __syncthreads();
+  if (flip)
+    for (int i = threadIdx.x; i < rows; i += 256) {
+      x[i] = -x[i];
+      y[i] = -y[i];
+    }
+}
+
+// H = [UF; RF] [VG; RG]^T + diag(S, 0): assembled blocks (col-major)
+__global__ void k_stack_rows(const double* top, int rt, const double* bot, int rb, int cols, double* out) {
+  const int rows = rt + rb;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int j = e / rows, i = e - j * rows;
+    out[e] = i < rt ? top[size_t(j) * rt + i] : bot[size_t(j) * rb + (i - rt)];
+  }
+}
+
+__global__ void k_add_diag(double* H, int ld, const double* s, int r) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x)
+    H[size_t(i) * ld + i] += s[i];
+}
+
+__global__ void __launch_bounds__(256) k_sumsq(const double* x, size_t n, double* out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += 256) s += x[i] * x[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+cublasHandle_t blas(ptb_context* ctx) {
+  if (!ctx->cublas) {
+    cublasHandle_t h = nullptr;
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(PTB_CUDA, "cublasCreate failed");
+    ctx->cublas = h;
+  }
+  cublasHandle_t h = static_cast<cublasHandle_t>(ctx->cublas);
+  cublasSetStream(h, ctx->stream);
+  cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
+  return h;
+}
+
+void check_blas(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS) fail(PTB_CUDA, std::string("cuBLAS ") + what + " failed");
+}
+
+double dev_sumsq(ptb_context* ctx, const double* x, size_t n, DeviceBuffer& scratch) {
+  double* d = static_cast<double*>(scratch.get(sizeof(double)));
+  k_sumsq<<<1, 256, 0, ctx->stream>>>(x, n, d);
+  PTB_LAUNCH_CHECK(ctx);
+  double h = 0.0;
+  PTB_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  return h;
+}
+
+int qr_grid(ptb_context* ctx, int m, size_t smem, const void* kern) {
+  int per_sm = 0;
+  PTB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, QR_THREADS, smem));
+  const int cap = std::max(1, per_sm) * ctx->num_sms;
+  const int want = std::max(1, (m + 511) / 512);
+  return std::min({cap, want, ctx->num_sms});
+}
+
+}  // namespace
+
+// C (m x n) = alpha op(A) op(B) + beta C, all column-major
+void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
+          const double* B, int ldb, double beta, double* C, int ldc) {
+  if (m == 0 || n == 0) return;
+  if (k == 0) {
+    if (beta == 0.0) PTB_CUDA_CHECK(cudaMemsetAsync(C, 0, size_t(ldc) * n * sizeof(double), ctx->stream));
+    return;
+  }
+  check_blas(cublasDgemm(blas(ctx), ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k, &alpha, A,
+                         std::max(1, lda), B, std::max(1, ldb), &beta, C, std::max(1, ldc)),
+             "dgemm");
+  ctx->launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+ProcWork::ProcWork(ptb_context* c) : ctx(c) {}
+ProcWork::~ProcWork() {
+  for (auto& b : buf) b.release();
+}
+
+DevCorrector::~DevCorrector() {
+  X.release();
+  Y.release();
+  Sd.release();
+}
+
+void DevCorrector::assign(int rows_, int rank_, const std::vector<double>& s, double tol_) {
+  rows = rows_;
+  rank = rank_;
+  S = s;
+  tol = tol_;
+  double* d = static_cast<double*>(Sd.get(std::max<size_t>(1, S.size()) * sizeof(double)));
+  if (!S.empty())
+    PTB_CUDA_CHECK(cudaMemcpy(d, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+// truncated_qr (procrustes.cpp:34-46): Q (m x keep) and R (keep x n, un-pivoted) in
+// caller buffers; A is copied (the input is not modified).  Returns keep.
+int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb, DeviceBuffer& Rb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  const int k = std::min(m, n);
+  if (k == 0) {
+    Qb.get(8);
+    Rb.get(8);
+    return 0;
+  }
+  double* A = static_cast<double*>(w.buf[0].get(size_t(m) * n * sizeof(double)));
+  PTB_CUDA_CHECK(cudaMemcpyAsync(A, A_in, size_t(m) * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  double* tau = static_cast<double*>(w.buf[1].get(size_t(n) * sizeof(double)));
+  int* perm = static_cast<int*>(w.buf[2].get(size_t(n) * sizeof(int)));
+  int* keep_d = static_cast<int*>(w.buf[3].get(sizeof(int)));
+  double* betas = static_cast<double*>(w.buf[5].get(size_t(n) * sizeof(double)));
+  const size_t smem = (QR_THREADS + 2 * size_t(n)) * sizeof(double);
+  const int G = qr_grid(ctx, m, smem, reinterpret_cast<const void*>(k_qrcp));
+  double* part = static_cast<double*>(w.buf[4].get(size_t(2) * G * (n + 1) * sizeof(double)));
+  QrArgs qa{A, m, n, drop_tol, tau, perm, part, keep_d, betas};
+  void* args[] = {&qa};
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qrcp), G, QR_THREADS, args, smem, st));
+  PTB_LAUNCH_CHECK(ctx);
+  int keep = 0;
+  PTB_CUDA_CHECK(cudaMemcpyAsync(&keep, keep_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+  double* Q = static_cast<double*>(Qb.get(std::max<size_t>(1, size_t(m) * keep) * sizeof(double)));
+  double* R = static_cast<double*>(Rb.get(std::max<size_t>(1, size_t(keep) * n) * sizeof(double)));
+  if (keep > 0) {
+    const size_t smem2 = (QR_THREADS + size_t(keep)) * sizeof(double);
+    const int G2 = qr_grid(ctx, m, smem2, reinterpret_cast<const void*>(k_qr_formq));
+    double* part2 = static_cast<double*>(w.buf[4].get(std::max(size_t(2) * G * (n + 1), size_t(2) * G2 * keep) *
+                                                        sizeof(double)));
+    FormQArgs fa{A, tau, m, keep, Q, part2};
+    void* args2[] = {&fa};
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qr_formq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+    PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qr_formq), G2, QR_THREADS, args2, smem2, st));
+    PTB_LAUNCH_CHECK(ctx);
+    k_unpivot_r<<<std::max(1, std::min(256, (keep * n + 255) / 256)), 256, 0, st>>>(A, m, n, keep, perm, R);
+    PTB_LAUNCH_CHECK(ctx);
+  }
+  return keep;
+}
+
+// thin SVD of M (p x q): U (p x k), sigma (k, host), V (q x k), k = min(p, q)
+void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std::vector<double>& sigma,
+              DeviceBuffer& Vb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  const int k = std::min(p, q);
+  sigma.assign(size_t(k), 0.0);
+  if (k == 0) {
+    Ub.get(8);
+    Vb.get(8);
+    return;
+  }
+  const bool trans = p < q;
+  const int r = trans ? q : p, c = k;
+  double* A = static_cast<double*>(w.buf[6].get(size_t(r) * c * sizeof(double)));
+  if (trans) {
+    k_transpose<<<std::max(1, std::min(1024, (p * q + 255) / 256)), 256, 0, st>>>(M, p, q, A);
+    PTB_LAUNCH_CHECK(ctx);
+  } else {
+    PTB_CUDA_CHECK(cudaMemcpyAsync(A, M, size_t(p) * q * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  double* V = static_cast<double*>(w.buf[7].get(size_t(c) * c * sizeof(double)));
+  double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
+  int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
+  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c) * sizeof(double)));
+  JacobiArgs ja{A, V, r, c, sg, order, tmp, 60};
+  k_jacobi<<<1, 1024, 0, st>>>(ja);
+  PTB_LAUNCH_CHECK(ctx);
+  PTB_CUDA_CHECK(cudaMemcpyAsync(sigma.data(), sg, size_t(c) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // M = A_sorted diag(s) V^T  (A is r x c = U when !trans; when trans, M^T = A S V^T -> M = V S A^T)
+  double* U = static_cast<double*>(Ub.get(size_t(p) * k * sizeof(double)));
+  double* Vo = static_cast<double*>(Vb.get(size_t(q) * k * sizeof(double)));
+  if (!trans) {
+    PTB_CUDA_CHECK(cudaMemcpyAsync(U, A, size_t(p) * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(Vo, V, size_t(q) * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    PTB_CUDA_CHECK(cudaMemcpyAsync(U, V, size_t(p) * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(Vo, A, size_t(q) * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+static int truncate_count(const std::vector<double>& sigma, double tol) {
+  const double smax = sigma.empty() ? 0.0 : sigma[0];
+  int keep = 0;
+  while (keep < int(sigma.size()) && smax > 0.0 && sigma[size_t(keep)] / smax > tol) ++keep;
+  return keep;
+}
+
+void fix_signs(ptb_context* ctx, double* X, double* Y, int rows, int cols) {
+  if (cols == 0 || rows == 0) return;
+  k_fix_signs<<<cols, 256, 0, ctx->stream>>>(X, Y, rows);
+  PTB_LAUNCH_CHECK(ctx);
+}
+
+void check_tol(double tol) {
+  if (!(tol > 0.0) || !(tol < 1.0)) fail(PTB_INVALID_ARGUMENT, "truncation tolerance must lie in (0, 1)");
+}
+
+// procrustes.cpp:48-69
+void solve_from_scratch(ProcWork& w, DevCorrector& out, const double* F, const double* G, int rows, int cols,
+                        double tol) {
+  ptb_context* ctx = w.ctx;
+  const double qr_guard = 1e-14;
+  const double fn = std::sqrt(dev_sumsq(ctx, F, size_t(rows) * cols, w.buf[11]));
+  const double gn = std::sqrt(dev_sumsq(ctx, G, size_t(rows) * cols, w.buf[11]));
+  const int qf = truncated_qr(w, F, rows, cols, qr_guard * fn, w.QF, w.RF);
+  const int qg = truncated_qr(w, G, rows, cols, qr_guard * gn, w.QG, w.RG);
+  if (qf == 0 || qg == 0) {
+    out.X.get(8);
+    out.Y.get(8);
+    out.assign(rows, 0, {}, tol);
+    return;
+  }
+  double* M = static_cast<double*>(w.buf[12].get(size_t(qf) * qg * sizeof(double)));
+  gemm(ctx, false, true, qf, qg, cols, 1.0, static_cast<double*>(w.RF.ptr), qf, static_cast<double*>(w.RG.ptr), qg,
+       0.0, M, qf);
+  std::vector<double> sigma;
+  thin_svd(w, M, qf, qg, w.Uh, sigma, w.Vh);
+  const int s = truncate_count(sigma, tol);
+  double* X = static_cast<double*>(out.X.get(std::max<size_t>(1, size_t(rows) * s) * sizeof(double)));
+  double* Y = static_cast<double*>(out.Y.get(std::max<size_t>(1, size_t(rows) * s) * sizeof(double)));
+  gemm(ctx, false, false, rows, s, qf, 1.0, static_cast<double*>(w.QF.ptr), rows, static_cast<double*>(w.Uh.ptr), qf,
+       0.0, X, rows);
+  gemm(ctx, false, false, rows, s, qg, 1.0, static_cast<double*>(w.QG.ptr), rows, static_cast<double*>(w.Vh.ptr), qg,
+       0.0, Y, rows);
+  fix_signs(ctx, X, Y, rows, s);
+  sigma.resize(size_t(s));
+  out.assign(rows, s, sigma, tol);
+}
+
+// procrustes.cpp:188-237; `c` is updated in place.
+void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, int rows, int cols, double tol) {
+  check_tol(tol);
+  ptb_context* ctx = w.ctx;
+  if (c.empty()) {
+    DevCorrector fresh;
+    solve_from_scratch(w, fresh, F, G, rows, cols, tol);
+    std::swap(c.X, fresh.X);
+    std::swap(c.Y, fresh.Y);
+    c.assign(fresh.rows, fresh.rank, fresh.S, fresh.tol);
+    return;
+  }
+  require(rows == c.rows, "update_svd: block rows do not match corrector");
+  const int r = c.rank;
+  const double* U = c.Xp();
+  const double* V = c.Yp();
+  double* UF = static_cast<double*>(w.buf[13].get(std::max<size_t>(1, size_t(r) * cols) * sizeof(double)));
+  double* VG = static_cast<double*>(w.buf[14].get(std::max<size_t>(1, size_t(r) * cols) * sizeof(double)));
+  gemm(ctx, true, false, r, cols, rows, 1.0, U, rows, F, rows, 0.0, UF, r);
+  gemm(ctx, true, false, r, cols, rows, 1.0, V, rows, G, rows, 0.0, VG, r);
+  double* Fr = static_cast<double*>(w.buf[15].get(size_t(rows) * cols * sizeof(double)));
+  double* Gr = static_cast<double*>(w.buf[16].get(size_t(rows) * cols * sizeof(double)));
+  PTB_CUDA_CHECK(cudaMemcpyAsync(Fr, F, size_t(rows) * cols * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  PTB_CUDA_CHECK(cudaMemcpyAsync(Gr, G, size_t(rows) * cols * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  gemm(ctx, false, false, rows, cols, r, -1.0, U, rows, UF, r, 1.0, Fr, rows);
+  gemm(ctx, false, false, rows, cols, r, -1.0, V, rows, VG, r, 1.0, Gr, rows);
+  const double qr_guard = 1e-14;
+  const double fn = std::sqrt(dev_sumsq(ctx, F, size_t(rows) * cols, w.buf[11]));
+  const double gn = std::sqrt(dev_sumsq(ctx, G, size_t(rows) * cols, w.buf[11]));
+  const int qf = truncated_qr(w, Fr, rows, cols, qr_guard * fn, w.QF, w.RF);
+  const int qg = truncated_qr(w, Gr, rows, cols, qr_guard * gn, w.QG, w.RG);
+  double* LB = static_cast<double*>(w.buf[17].get(std::max<size_t>(1, size_t(r + qf) * cols) * sizeof(double)));
+  double* RB = static_cast<double*>(w.buf[18].get(std::max<size_t>(1, size_t(r + qg) * cols) * sizeof(double)));
+  const unsigned nb = unsigned(std::max(1, std::min(1024, ((r + std::max(qf, qg)) * cols + 255) / 256)));
+  k_stack_rows<<<nb, 256, 0, ctx->stream>>>(UF, r, static_cast<double*>(w.RF.ptr), qf, cols, LB);
+  PTB_LAUNCH_CHECK(ctx);
+  k_stack_rows<<<nb, 256, 0, ctx->stream>>>(VG, r, static_cast<double*>(w.RG.ptr), qg, cols, RB);
+  PTB_LAUNCH_CHECK(ctx);
+  const int hp = r + qf, hq = r + qg;
+  double* H = static_cast<double*>(w.buf[12].get(size_t(hp) * hq * sizeof(double)));
+  gemm(ctx, false, true, hp, hq, cols, 1.0, LB, hp, RB, hq, 0.0, H, hp);
+  k_add_diag<<<1, 256, 0, ctx->stream>>>(H, hp, static_cast<const double*>(c.Sd.ptr), r);
+  PTB_LAUNCH_CHECK(ctx);
+  std::vector<double> sigma;
+  thin_svd(w, H, hp, hq, w.Uh, sigma, w.Vh);
+  const int keep = truncate_count(sigma, tol);
+  // Uext = [U QF], Vext = [V QG]; X = Uext Uh[:, :keep], Y = Vext Vh[:, :keep]
+  DevCorrector nc;
+  double* X = static_cast<double*>(nc.X.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
+  double* Y = static_cast<double*>(nc.Y.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
+  const double* Uh = static_cast<double*>(w.Uh.ptr);
+  const double* Vh = static_cast<double*>(w.Vh.ptr);
+  gemm(ctx, false, false, rows, keep, r, 1.0, U, rows, Uh, hp, 0.0, X, rows);
+  gemm(ctx, false, false, rows, keep, qf, 1.0, static_cast<double*>(w.QF.ptr), rows, Uh + r, hp, 1.0, X, rows);
+  gemm(ctx, false, false, rows, keep, r, 1.0, V, rows, Vh, hq, 0.0, Y, rows);
+  gemm(ctx, false, false, rows, keep, qg, 1.0, static_cast<double*>(w.QG.ptr), rows, Vh + r, hq, 1.0, Y, rows);
+  fix_signs(ctx, X, Y, rows, keep);
+  sigma.resize(size_t(keep));
+  PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  std::swap(c.X, nc.X);
+  std::swap(c.Y, nc.Y);
+  c.assign(rows, keep, sigma, tol);
+}
+
+// out (rows x batch) = X (Y^T in)   (procrustes.cpp:82-86)
+void apply_corrector(ProcWork& w, const DevCorrector& c, size_t batch, const double* in, size_t ld_in, double* out,
+                     size_t ld_out) {
+  ptb_context* ctx = w.ctx;
+  if (batch == 0) return;
+  if (c.rank == 0) {
+    PTB_CUDA_CHECK(cudaMemset2DAsync(out, ld_out * sizeof(double), 0, size_t(c.rows) * sizeof(double), batch,
+                                     ctx->stream));
+    return;
+  }
+  double* z = static_cast<double*>(w.buf[19].get(size_t(c.rank) * batch * sizeof(double)));
+  gemm(ctx, true, false, c.rank, int(batch), c.rows, 1.0, c.Yp(), c.rows, in, int(ld_in), 0.0, z, c.rank);
+  gemm(ctx, false, false, c.rows, int(batch), c.rank, 1.0, c.Xp(), c.rows, z, c.rank, 0.0, out, int(ld_out));
+}
+
+// procrustes.cpp:245-253
+double relative_residual(ProcWork& w, const DevCorrector& c, const double* F, const double* G, int rows, int cols) {
+  ptb_context* ctx = w.ctx;
+  const double fnorm = std::sqrt(dev_sumsq(ctx, F, size_t(rows) * cols, w.buf[11]));
+  if (fnorm == 0.0) return 0.0;
+  if (c.rank == 0) return 1.0;
+  double* D = static_cast<double*>(w.buf[20].get(size_t(rows) * cols * sizeof(double)));
+  apply_corrector(w, c, size_t(cols), G, size_t(rows), D, size_t(rows));
+  // D = F - X Y^T G
+  const double minus1 = -1.0, one = 1.0;
+  check_blas(cublasDgeam(blas(ctx), CUBLAS_OP_N, CUBLAS_OP_N, rows, cols, &one, F, rows, &minus1, D, rows, D, rows),
+             "dgeam");
+  return std::sqrt(dev_sumsq(ctx, D, size_t(rows) * cols, w.buf[11])) / fnorm;
+}
+
+void drop_leading(const DevCorrector& c, size_t count, DevCorrector& out, ptb_context* ctx) {
+  const int keep = std::max(0, c.rank - int(std::min<size_t>(count, size_t(c.rank))));
+  const int first = c.rank - keep;
+  double* X = static_cast<double*>(out.X.get(std::max<size_t>(1, size_t(c.rows) * keep) * sizeof(double)));
+  double* Y = static_cast<double*>(out.Y.get(std::max<size_t>(1, size_t(c.rows) * keep) * sizeof(double)));
+  if (keep > 0) {
+    PTB_CUDA_CHECK(cudaMemcpyAsync(X, c.Xp() + size_t(first) * c.rows, size_t(c.rows) * keep * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(Y, c.Yp() + size_t(first) * c.rows, size_t(c.rows) * keep * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  out.assign(c.rows, keep, std::vector<double>(c.S.begin() + first, c.S.end()), c.tol);
+}
+
+}  // namespace ptb
+
+extern "C" void ptb_release_blas(ptb_context* ctx) {
+  if (ctx && ctx->cublas) {
+    cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
+    ctx->cublas = nullptr;
+  }
+}

@@ -1,0 +1,49 @@
+#pragma once
+#include <vector>
+
+#include "ptb_internal.h"
+
+namespace ptb {
+
+// Device-resident truncated factors (X, S, Y) of the accumulated correlation matrix
+// (procrustes.hpp:22-60): X, Y are rows x rank column-major in HBM, S on host + device.
+struct DevCorrector {
+  int rows = 0, rank = 0;
+  double tol = 0.0;
+  std::vector<double> S;
+  DeviceBuffer X, Y, Sd;
+  bool empty() const { return rows == 0; }
+  const double* Xp() const { return static_cast<const double*>(X.ptr); }
+  const double* Yp() const { return static_cast<const double*>(Y.ptr); }
+  double* Xp() { return static_cast<double*>(X.ptr); }
+  double* Yp() { return static_cast<double*>(Y.ptr); }
+  void assign(int rows_, int rank_, const std::vector<double>& s, double tol_);
+  DevCorrector() = default;
+  DevCorrector(const DevCorrector&) = delete;
+  DevCorrector& operator=(const DevCorrector&) = delete;
+  ~DevCorrector();
+};
+
+struct ProcWork {
+  ptb_context* ctx;
+  DeviceBuffer buf[24];
+  DeviceBuffer QF, RF, QG, RG, Uh, Vh;
+  explicit ProcWork(ptb_context* c);
+  ~ProcWork();
+};
+
+void check_tol(double tol);
+int truncated_qr(ProcWork& w, const double* A, int m, int n, double drop_tol, DeviceBuffer& Q, DeviceBuffer& R);
+void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& U, std::vector<double>& sigma, DeviceBuffer& V);
+void solve_from_scratch(ProcWork& w, DevCorrector& out, const double* F, const double* G, int rows, int cols,
+                        double tol);
+void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, int rows, int cols, double tol);
+void apply_corrector(ProcWork& w, const DevCorrector& c, size_t batch, const double* in, size_t ld_in, double* out,
+                     size_t ld_out);
+double relative_residual(ProcWork& w, const DevCorrector& c, const double* F, const double* G, int rows, int cols);
+void drop_leading(const DevCorrector& c, size_t count, DevCorrector& out, ptb_context* ctx);
+void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
+          const double* B, int ldb, double beta, double* C, int ldc);
+void fix_signs(ptb_context* ctx, double* X, double* Y, int rows, int cols);
+
+}  // namespace ptb

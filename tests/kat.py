@@ -304,3 +304,280 @@ PROPAGATOR_KATS = [config_enforces_cfl, laplacian_known_answers, laplacian_2d_su
                    divergence_reported]
 TRANSFER_KATS = [grid_invariants, transfer_rejects_non_nested, restriction_pointwise, fourier_band_limited,
                  linear_constants_monotone, restrict_interpolate_identity, fourier_preserves_mean]
+
+
+# ------------------------------------------------------------ test_energy_map.cpp
+
+FD_SCHEMES = (0, 1, 2, 3)
+SPECTRAL = 4
+
+
+def components_constant_displacement(impl):
+    """test_energy_map.cpp:50-64"""
+    g = impl.grid((40,), (0.025,))
+    c = np.full(40, 2.0)
+    for scheme in (0, SPECTRAL):
+        st, mean = impl.components(np.full(40, 5.0), c.copy(), c, g, scheme)
+        assert np.max(np.abs(st[:40])) <= 1e-12
+        assert np.max(np.abs(st[40:] - 1.0)) <= 1e-15
+        assert mean == pytest.approx(200.0)
+
+
+def spectral_gradient_exact(impl):
+    """test_energy_map.cpp:66-76 (through the gradient block of Lambda)"""
+    g = impl.grid((50,), (0.02,))
+    x = np.arange(50) * 0.02
+    u = np.sin(2 * math.pi * x)
+    du = 2 * math.pi * np.cos(2 * math.pi * x)
+    st, _ = impl.components(u, np.zeros(50), np.ones(50), g, SPECTRAL)
+    assert np.max(np.abs(st[:50] - du)) <= 1e-12 * np.max(np.abs(du))
+
+
+def fd_gradients_match_stencil(impl):
+    """test_energy_map.cpp:78-92"""
+    from oracle.paratime_np import STENCILS
+
+    g = impl.grid((36,), (1.0 / 36,))
+    u = np.random.default_rng(21).uniform(-1, 1, 36)
+    for scheme in FD_SCHEMES:
+        beta = STENCILS[scheme]
+        st, _ = impl.components(u, np.zeros(36), np.ones(36), g, scheme)
+        for i in range(36):
+            acc = sum(b * (u[(i + j) % 36] - u[(i - j) % 36]) for j, b in enumerate(beta, start=1))
+            assert st[i] == pytest.approx(acc * 36.0, rel=1e-12, abs=1e-12)
+
+
+def reconstruction_inverts_spectral(impl):
+    """test_energy_map.cpp:94-107 (1D 64 and 2D 12x20)"""
+    rng = np.random.default_rng(33)
+    for g in (impl.grid((64,), (1.0 / 64,)), impl.grid((12, 20), (1.0 / 12, 1.0 / 20))):
+        c = np.ones(g.shape)
+        for _ in range(5):
+            u, v = smooth_field(g, rng), smooth_field(g, rng)
+            st, mean = impl.components(u, v, c, g, SPECTRAL)
+            bu, bv = impl.reconstruct(st, mean, c, g)
+            assert rel_l2(bu, u) <= 1e-12 and rel_l2(bv, v) <= 1e-12
+
+
+def fd2_reconstruction_sinc(impl):
+    """test_energy_map.cpp:109-127"""
+    g = impl.grid((32,), (1.0 / 32,))
+    c = np.ones(32)
+    h = 1.0 / 32
+    for k in range(1, 16):
+        xi = 2 * math.pi * k
+        sinc = math.sin(xi * h) / (xi * h)
+        u = np.cos(xi * np.arange(32) * h) + 0.5 * np.sin(xi * np.arange(32) * h)
+        st, mean = impl.components(u, np.zeros(32), c, g, 0)
+        bu, _ = impl.reconstruct(st, mean, c, g)
+        np.testing.assert_allclose(bu, sinc * u, rtol=1e-12, atol=1e-12)
+
+
+def zero_gradients_reconstruct_mean(impl):
+    """test_energy_map.cpp:129-137"""
+    g = impl.grid((25,), (0.04,))
+    st = np.zeros(50)
+    bu, bv = impl.reconstruct(st, 5.0, np.ones(25), g)
+    assert np.max(np.abs(bu - 0.2)) <= 1e-14
+    assert np.max(np.abs(bv)) == 0.0
+
+
+def energy_closed_forms(impl):
+    """test_energy_map.cpp:139-152"""
+    g = impl.grid((80,), (0.0125,))
+    c = np.full(80, 3.0)
+    assert impl.energy(np.zeros(80), np.zeros(80), c, g, 0) == 0.0
+    assert impl.energy(np.zeros(80), c.copy(), c, g, 0) == pytest.approx(0.5 * 80 * 0.0125)
+    g2 = impl.grid((8, 10), (0.5, 0.2))
+    c2 = np.full((8, 10), 1.7)
+    assert impl.energy(np.zeros((8, 10)), c2.copy(), c2, g2, 1) == pytest.approx(0.5 * 80 * 0.1)
+
+
+def energy_error_direct(impl):
+    """test_energy_map.cpp:176-199"""
+    rng = np.random.default_rng(55)
+    g = impl.grid((44,), (1.0 / 44,))
+    c = np.ones(44)
+    a = (rng.uniform(-1, 1, 44), rng.uniform(-1, 1, 44))
+    b = (rng.uniform(-1, 1, 44), rng.uniform(-1, 1, 44))
+    assert impl.energy_error(b, b, c, g, 1) == 0.0
+    assert impl.energy_error((2 * b[0], 2 * b[1]), b, c, g, 1) == pytest.approx(1.0)
+    expect = math.sqrt(impl.energy(a[0] - b[0], a[1] - b[1], c, g, 1) / impl.energy(b[0], b[1], c, g, 1))
+    assert impl.energy_error(a, b, c, g, 1) == pytest.approx(expect)
+    with pytest.raises(ZeroDivisionError):
+        impl.energy_error(a, (np.zeros(44), np.zeros(44)), c, g, 1)
+
+
+def reconstruction_never_amplifies(impl):
+    """test_energy_map.cpp:201-219"""
+    rng = np.random.default_rng(61)
+    for g in (impl.grid((40,), (0.025,)), impl.grid((10, 14), (0.1, 1.0 / 14))):
+        c = np.ones(g.shape)
+        for _ in range(3):
+            u, v = rng.uniform(-1, 1, g.shape), rng.uniform(-1, 1, g.shape)
+            for scheme in FD_SCHEMES + (SPECTRAL,):
+                st, mean = impl.components(u, v, c, g, scheme)
+                bu, bv = impl.reconstruct(st, mean, c, g)
+                e_comp = 0.5 * float(np.sum(st * st)) * float(np.prod(g.h))
+                assert impl.energy(bu, bv, c, g, scheme) <= e_comp * (1.0 + 1e-12)
+
+
+ENERGY_KATS = [components_constant_displacement, spectral_gradient_exact, fd_gradients_match_stencil,
+               reconstruction_inverts_spectral, fd2_reconstruction_sinc, zero_gradients_reconstruct_mean,
+               energy_closed_forms, energy_error_direct, reconstruction_never_amplifies]
+
+
+# ------------------------------------------------------------ test_procrustes.cpp / acceptance.cpp
+
+
+def _haar(n, rng):
+    q, r = np.linalg.qr(rng.standard_normal((n, n)))
+    return q * np.sign(np.diag(r))
+
+
+def _defect(m):
+    return float(np.max(np.abs(m.T @ m - np.eye(m.shape[1])))) if m.shape[1] else 0.0
+
+
+def solve_aligned_identity(impl):
+    """test_procrustes.cpp:46-53"""
+    G = np.random.default_rng(101).standard_normal((12, 4))
+    c = impl.procrustes_solve(G, G, 1e-14)
+    assert np.linalg.norm(G - c.X @ (c.Y.T @ G)) <= 1e-10 * np.linalg.norm(G)
+    assert _defect(c.X) <= 1e-12 and _defect(c.Y) <= 1e-12
+
+
+def solve_planted_rotation(impl):
+    """test_procrustes.cpp:55-68 (wide block through the update path)"""
+    rng = np.random.default_rng(103)
+    al = 0.41
+    rot = np.array([[math.cos(al), -math.sin(al)], [math.sin(al), math.cos(al)]])
+    G = rng.standard_normal((2, 3))
+    F = rot @ G
+    c = impl.update_svd(None, F, G, 1e-14)
+    assert c.rank == 2
+    omega = c.X @ c.Y.T
+    assert np.max(np.abs(omega - rot)) <= 1e-12
+    assert np.linalg.norm(F - omega @ G) <= 1e-12 * np.linalg.norm(F)
+
+
+def solve_matches_dense_oracle(impl):
+    """test_procrustes.cpp:70-94 and acceptance criterion 2"""
+    rng = np.random.default_rng(107)
+    for _ in range(10):
+        F = rng.standard_normal((8, 3))
+        G = rng.standard_normal((8, 3))
+        c = impl.procrustes_solve(F, G, 1e-15)
+        res = np.linalg.norm(F - c.X @ (c.Y.T @ G))
+        U, s, Vt = np.linalg.svd(F @ G.T)
+        res_full = np.linalg.norm(F - (U @ Vt) @ G)
+        assert res == pytest.approx(res_full, rel=1e-10)
+        ident = np.sum(F * F) + np.sum(G * G) - 2.0 * np.sum(c.S)
+        assert res * res == pytest.approx(ident, rel=1e-10)
+        for _ in range(20):
+            assert res <= np.linalg.norm(F - _haar(8, rng) @ G) + 1e-10
+
+
+def zero_data_annihilates(impl):
+    """test_procrustes.cpp:96-103"""
+    Z = np.zeros((10, 3))
+    c = impl.procrustes_solve(Z, Z, 1e-12)
+    assert c.rank == 0
+    out = impl.apply(c, np.ones(10))
+    assert np.linalg.norm(out) == 0.0
+
+
+def solve_validates(impl):
+    """test_procrustes.cpp:105-115"""
+    rng = np.random.default_rng(109)
+    F = rng.standard_normal((6, 2))
+    for args in ((F, rng.standard_normal((6, 3)), 1e-12), (rng.standard_normal((2, 6)), rng.standard_normal((2, 6)), 1e-12),
+                 (F, F, 0.0), (F, F, 1.0)):
+        with pytest.raises(InvalidArgument):
+            impl.procrustes_solve(*args)
+    with pytest.raises(InvalidArgument):
+        impl.update_svd(None, F, F, -1.0)
+
+
+def update_on_empty_equals_solve(impl):
+    """test_procrustes.cpp:117-126"""
+    rng = np.random.default_rng(113)
+    F, G = rng.standard_normal((10, 4)), rng.standard_normal((10, 4))
+    a = impl.procrustes_solve(F, G, 1e-13)
+    b = impl.update_svd(None, F, G, 1e-13)
+    assert np.max(np.abs(a.S - b.S)) <= 1e-12
+    ra = a.X @ np.diag(a.S) @ a.Y.T
+    rb = b.X @ np.diag(b.S) @ b.Y.T
+    assert np.linalg.norm(ra - rb) <= 1e-10 * np.linalg.norm(ra)
+    assert np.max(np.abs(a.X - b.X)) <= 1e-10
+
+
+def chained_updates_match_dense(impl):
+    """test_procrustes.cpp:128-143 and acceptance criterion 3"""
+    rng = np.random.default_rng(127)
+    for _ in range(5):
+        c = None
+        direct = np.zeros((16, 16))
+        for _ in range(4):
+            F, G = rng.standard_normal((16, 3)), rng.standard_normal((16, 3))
+            direct += F @ G.T
+            c = impl.update_svd(c, F, G, 1e-15)
+            assert _defect(c.X) <= 1e-12 and _defect(c.Y) <= 1e-12
+        rec = c.X @ np.diag(c.S) @ c.Y.T
+        assert np.linalg.norm(rec - direct) <= 1e-10 * np.linalg.norm(direct)
+
+
+def zero_block_update_unchanged(impl):
+    """test_procrustes.cpp:145-153"""
+    rng = np.random.default_rng(131)
+    F, G = rng.standard_normal((9, 3)), rng.standard_normal((9, 3))
+    c = impl.procrustes_solve(F, G, 1e-13)
+    after = impl.update_svd(c, np.zeros((9, 2)), np.zeros((9, 2)), 1e-13)
+    rc = c.X @ np.diag(c.S) @ c.Y.T
+    ra = after.X @ np.diag(after.S) @ after.Y.T
+    assert np.linalg.norm(ra - rc) <= 1e-12 * np.linalg.norm(rc)
+
+
+def rank_monotone_in_tol(impl):
+    """test_procrustes.cpp:155-165"""
+    rng = np.random.default_rng(137)
+    F, G = rng.standard_normal((20, 6)), rng.standard_normal((20, 6))
+    last = 7
+    for tol in (1e-15, 1e-6, 1e-2, 0.2, 0.9):
+        c = impl.procrustes_solve(F, G, tol)
+        assert c.rank <= last
+        last = c.rank
+
+
+def apply_partial_isometry(impl):
+    """test_procrustes.cpp:167-193"""
+    rng = np.random.default_rng(139)
+    zero = impl.procrustes_solve(np.zeros((24, 2)), np.zeros((24, 2)), 1e-12)
+    v = rng.uniform(-1, 1, 24)
+    assert np.max(np.abs(impl.apply(zero, v))) == 0.0
+    F, G = rng.standard_normal((24, 5)), rng.standard_normal((24, 5))
+    pc = impl.procrustes_solve(F, G, 1e-13)
+    for _ in range(10):
+        v = rng.standard_normal(24)
+        assert np.linalg.norm(impl.apply(pc, v)) <= np.linalg.norm(v) * (1 + 1e-12)
+    aligned = impl.procrustes_solve(G, G, 1e-14)
+    inr = G @ rng.standard_normal(5)
+    assert np.linalg.norm(impl.apply(aligned, inr) - inr) <= 1e-10 * np.linalg.norm(inr)
+
+
+def drop_leading_removes_largest(impl):
+    """test_procrustes.cpp:195-207"""
+    rng = np.random.default_rng(149)
+    F, G = rng.standard_normal((15, 5)), rng.standard_normal((15, 5))
+    c = impl.procrustes_solve(F, G, 1e-15)
+    d = impl.drop_leading(c, 2)
+    assert d.rank == c.rank - 2
+    assert d.S[0] == c.S[2]
+    assert impl.relative_residual(d, F, G) > impl.relative_residual(c, F, G)
+    assert impl.drop_leading(c, c.rank + 3).rank == 0
+
+
+PROCRUSTES_KATS = [solve_aligned_identity, solve_planted_rotation, solve_matches_dense_oracle, zero_data_annihilates,
+                   solve_validates, update_on_empty_equals_solve, chained_updates_match_dense,
+                   zero_block_update_unchanged, rank_monotone_in_tol, apply_partial_isometry,
+                   drop_leading_removes_largest]

@@ -8,7 +8,7 @@ from tests.impls import OracleImpl
 IMPL = OracleImpl()
 
 
-@pytest.mark.parametrize("check", kat.PROPAGATOR_KATS + kat.TRANSFER_KATS, ids=lambda f: f.__name__)
+@pytest.mark.parametrize("check", kat.PROPAGATOR_KATS + kat.TRANSFER_KATS + kat.ENERGY_KATS + kat.PROCRUSTES_KATS, ids=lambda f: f.__name__)
 def test_oracle_known_answers(check):
     check(IMPL)
 
