@@ -159,6 +159,15 @@ ptb_status ptb_corrector_apply_batch(ptb_corrector* c, size_t batch, const doubl
 ptb_status ptb_relative_residual(ptb_corrector* c, size_t rows, size_t cols, const double* F_dev,
                                  const double* G_dev, double* out);
 
+/* building blocks of update_svd, exposed for parity tests:
+ * truncated_qr (procrustes.cpp:34-46): A m x n (device, col-major) -> Q m x keep, R keep x n
+ * (un-pivoted), keep = leading pivoted |R_ii| > drop_tol.  Q_dev/R_dev sized m*n / n*n. */
+ptb_status ptb_truncated_qr(ptb_context* ctx, size_t m, size_t n, const double* A_dev, double drop_tol,
+                            double* Q_dev, double* R_dev, size_t* keep);
+/* thin SVD M (p x q) = U diag(S) V^T, k = min(p, q), S descending (S_host k values) */
+ptb_status ptb_thin_svd(ptb_context* ctx, size_t p, size_t q, const double* M_dev, double* U_dev, double* S_host,
+                        double* V_dev);
+
 /* ---- parareal drivers (parareal.hpp:60-79) -------------------------------------------- */
 typedef enum { PTB_PLAIN = 0, PTB_THETA = 1, PTB_CORRECTED_COARSE_ONLY = 2, PTB_OMEGA_IDENTITY = 3 } ptb_variant;
 

@@ -279,11 +279,15 @@ class Corrector:
 
     def update(self, F, G, tol: float):
         """update_svd in place; F, G: device (cols, rows) tensors = column-major rows x cols."""
+        if tuple(F.shape) != tuple(G.shape):
+            raise PtbError(INVALID_ARGUMENT, "update_svd: F and G must have the same shape")
         cols, rows = F.shape
         check(lib().ptb_corrector_update(self.h, C.c_size_t(rows), C.c_size_t(cols), _ptr(F), _ptr(G), C.c_double(tol)))
         return self
 
     def solve(self, F, G, tol: float):
+        if tuple(F.shape) != tuple(G.shape):
+            raise PtbError(INVALID_ARGUMENT, "procrustes_solve: F and G must have the same shape")
         cols, rows = F.shape
         check(lib().ptb_procrustes_solve(self.h, C.c_size_t(rows), C.c_size_t(cols), _ptr(F), _ptr(G), C.c_double(tol)))
         return self

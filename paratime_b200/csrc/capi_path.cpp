@@ -179,6 +179,46 @@ ptb_status ptb_relative_residual(ptb_corrector* c, size_t rows, size_t cols, con
   });
 }
 
+ptb_status ptb_truncated_qr(ptb_context* ctx, size_t m, size_t n, const double* A, double drop_tol, double* Q,
+                            double* R, size_t* keep) {
+  return guarded([&] {
+    require(ctx && keep, "truncated_qr: null argument");
+    Dev d(ctx->device);
+    std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
+    ProcWork w(ctx);
+    DeviceBuffer qb, rb;
+    const int k = truncated_qr(w, A, int(m), int(n), drop_tol, qb, rb);
+    if (k > 0) {
+      PTB_CUDA_CHECK(cudaMemcpyAsync(Q, qb.ptr, m * size_t(k) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+      PTB_CUDA_CHECK(cudaMemcpyAsync(R, rb.ptr, size_t(k) * n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    qb.release();
+    rb.release();
+    *keep = size_t(k);
+  });
+}
+
+ptb_status ptb_thin_svd(ptb_context* ctx, size_t p, size_t q, const double* M, double* U, double* S, double* V) {
+  return guarded([&] {
+    require(ctx && S, "thin_svd: null argument");
+    Dev d(ctx->device);
+    std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
+    ProcWork w(ctx);
+    DeviceBuffer ub, vb;
+    std::vector<double> sigma;
+    thin_svd(w, M, int(p), int(q), ub, sigma, vb);
+    const size_t k = std::min(p, q);
+    if (k) {
+      PTB_CUDA_CHECK(cudaMemcpy(U, ub.ptr, p * k * sizeof(double), cudaMemcpyDeviceToDevice));
+      PTB_CUDA_CHECK(cudaMemcpy(V, vb.ptr, q * k * sizeof(double), cudaMemcpyDeviceToDevice));
+    }
+    for (size_t i = 0; i < k; ++i) S[i] = sigma[i];
+    ub.release();
+    vb.release();
+  });
+}
+
 ptb_status ptb_parareal_run(ptb_context* ctx, const ptb_run_spec* spec, const double* cf, const double* cc,
                             const double* u0, const double* v0, double* ee, double* l2, double* residual, int* rank,
                             int* diverged, double* states, double* reference, ptb_phase_times* times) {

@@ -63,6 +63,9 @@ __device__ double cta_reduce(double x, double* red) {
   return r;
 }
 
+// Values written by other CTAs (partial sums, the pivot row) are read with __ldcg: the
+// grid barrier orders the writes but does not invalidate this SM's L1, so a plain load
+// could return a line cached two steps earlier.
 __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sh[];  // red[QR_THREADS] | w[n] | nrm[n]
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     // remaining squared norms of columns k >= j (rows >= j), fixed-order reduction
     for (int k = j + tid; k < n; k += QR_THREADS) {
       double s = 0.0;
-      for (int c = 0; c < G; ++c) s += part[size_t(c) * (n + 1) + k];
+      for (int c = 0; c < G; ++c) s += __ldcg(&part[size_t(c) * (n + 1) + k]);
       nrm[k] = s;
     }
     __syncthreads();
@@ -128,8 +131,8 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     if (tid == 0) partn[size_t(g) * (n + 1) + n] = xs;
     grid.sync();
     double xnorm2 = 0.0;
-    for (int c = 0; c < G; ++c) xnorm2 += partn[size_t(c) * (n + 1) + n];
-    const double alpha = col(j)[j];
+    for (int c = 0; c < G; ++c) xnorm2 += __ldcg(&partn[size_t(c) * (n + 1) + n]);
+    const double alpha = __ldcg(&col(j)[j]);
     const double xnorm = sqrt(xnorm2);
     double beta, tau, scal;
     if (xnorm == 0.0) {
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     }
     // v (stored below the diagonal) and R_jj
     for (int i = max(r0, j + 1) + tid; i < r1; i += QR_THREADS) col(j)[i] *= scal;
+    __syncthreads();  // the partials below read rows scaled by neighbouring threads
     // w_k = A[j][k] + sum_{i>j} v_i A[i][k], k > j  (own-row partials)
     for (int k = j + 1; k < n; ++k) {
       double s = 0.0;
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     grid.sync();
     for (int k = j + 1 + tid; k < n; k += QR_THREADS) {
       double s = 0.0;
-      for (int c = 0; c < G; ++c) s += part[size_t(c) * (n + 1) + k];
+      for (int c = 0; c < G; ++c) s += __ldcg(&part[size_t(c) * (n + 1) + k]);
       w[k] = s;
     }
     __syncthreads();
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_formq(FormQArgs a) {
     grid.sync();
     for (int c = j + tid; c < K; c += QR_THREADS) {
       double s = 0.0;
-      for (int q = 0; q < G; ++q) s += part[size_t(q) * K + c];
+      for (int q = 0; q < G; ++q) s += __ldcg(&part[size_t(q) * K + c]);
       w[c] = s;
     }
     __syncthreads();
