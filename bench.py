@@ -31,6 +31,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "fine-propagator fp64 grid-pt updates/s"
+ITER_CONFIGS = (2, 3)  # BASELINE configs timed for seconds per parareal iteration
 FLOPS_PER_UPDATE = 17  # Laplacian 9, x c^2 1, u-update 4, udot-update 3
 STEPS_PER_COUPLING = 64
 
@@ -191,6 +192,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time the cfg5 grid sweep")
+    ap.add_argument("--no-parareal", action="store_true", help="skip the s/iteration measurement")
     args = ap.parse_args()
 
     rank, world, local = dist_env()
@@ -263,6 +265,10 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(B, prop, u_host, mode, args.e2e_steps, local, dist, world)
+    del u, v
+    parareal = None
+    if not args.no_parareal:
+        parareal = parareal_iteration_times(B, ctx, rank, world, dist)
 
     if rank == 0:
         peaks = {}
@@ -289,14 +295,87 @@ def main():
                          "hbm_peak_GBps": peaks.get("hbm_gbs")},
             "clocks": clocks.summary(),
             "e2e": e2e,
+            "parareal": parareal,
         }
         if world == 1:
             line["cpu_baseline"] = cpu_baseline_sample(n)
+            if parareal is not None:
+                line["cpu_baseline_parareal"] = cpu_parareal_iteration(2)
         if args.sweep:
             line["sweep"] = sweep(B, ctx, mode)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def parareal_iteration_times(B, ctx, rank, world, dist, cfgs=ITER_CONFIGS):
+    """Seconds per theta-parareal iteration on BASELINE configs (device-timed CUDA events around
+    each iteration's body: parallel F + C.R, all-gather, snapshots + update_svd, coarse sweep,
+    fine combine + finalize), slices sharded over the ranks.  The one-time serial fine
+    reference is excluded and reported separately."""
+    import workloads as W
+
+    comm = None
+    if world > 1:
+        def bcast(raw):
+            obj = [raw]
+            dist.broadcast_object_list(obj, src=0)
+            return obj[0]
+
+        comm = B.api.Comm(ctx, rank, world, broadcast=bcast)
+    out = {}
+    for cfg in cfgs:
+        spec, cf, cc, u0, v0 = W.CONFIGS[cfg]()
+        B.api.parareal_run(ctx, B.api.run_spec(**dict(spec, iterations=1)), cf, cc, u0, v0, comm=comm)  # warm-up
+        r = B.api.parareal_run(ctx, B.api.run_spec(**spec), cf, cc, u0, v0, comm=comm)
+        t = r["times"]
+        it = np.array(t["iteration_ms"])
+        out[f"cfg{cfg}"] = {
+            "s_per_iteration": float(np.median(it)) / 1e3, "iteration_ms": [round(x, 3) for x in it],
+            "phase_ms_median": {k: float(np.median(t[k])) for k in ("parallel_ms", "gather_ms", "procrustes_ms",
+                                                                       "sweep_ms", "finalize_ms")},
+            "serial_fine_reference_ms": t["reference_ms"], "ranks": r["rank"].tolist(),
+            "final_energy_error": float(r["energy_err"][-1, -1]), "tol": spec["tol"], "K": spec["iterations"],
+            "N": spec["n_couplings"], "fine": spec["fine_n"][0], "coarse": spec["coarse_n"][0]}
+    return out
+
+
+def cpu_parareal_iteration(cfg=2):
+    """The reference's theta_parareal (oracle/_ref: parareal.cpp verbatim, Procrustes on LAPACK)
+    on the host cores for one BASELINE config: (wall - serial fine reference) / K."""
+    try:
+        import workloads as W
+        from oracle import refbind
+
+        if not refbind.LIB_PATH.exists():
+            return None
+        spec, cf, cc, u0, v0 = W.CONFIGS[cfg]()
+        cores = os.cpu_count() or 1
+        rs = refbind.RunSpec()
+        rs.dim = 2
+        for k in range(2):
+            rs.fine_n[k], rs.fine_h[k] = spec["fine_n"][k], spec["fine_h"][k]
+            rs.coarse_n[k], rs.coarse_h[k] = spec["coarse_n"][k], spec["coarse_h"][k]
+        for k in ("dt_fine", "m_fine", "dt_coarse", "m_coarse", "T", "dt_com", "n_couplings", "interp",
+                  "iterations", "variant", "scheme", "metric_scheme", "tol", "remove_leading"):
+            setattr(rs, k, spec[k])
+        rs.workers = cores
+        from oracle.paratime_np import Grid
+
+        g = Grid(tuple(spec["fine_n"]), tuple(spec["fine_h"]))
+        t0 = time.perf_counter()  # the serial fine reference the driver computes first
+        u, v = u0[None], v0[None]
+        for _ in range(spec["n_couplings"]):
+            u, v, _ = refbind.propagate(u, v, cf, g, spec["dt_fine"], spec["m_fine"], workers=1)
+        ref_s = time.perf_counter() - t0
+        r = refbind.parareal_run(rs, cf, cc, u0, v0)
+        wall = r["wall_ms"] / 1e3
+        return {"value": (wall - ref_s) / spec["iterations"], "unit": "s/iteration", "cores": cores,
+                "kind": "reference", "config": f"cfg{cfg}",
+                "sample": f"theta_parareal on cfg{cfg} (K={spec['iterations']}, N={spec['n_couplings']}), "
+                          f"wall {wall:.2f} s minus serial fine reference {ref_s:.2f} s, std::thread x{cores}"}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "error": str(e)}
 
 
 def probe_fp64(ctx):

@@ -54,6 +54,7 @@ typedef enum { PTB_INTERP_FOURIER = 0, PTB_INTERP_LINEAR = 1 } ptb_interp;     /
 typedef enum { PTB_FD2 = 0, PTB_FD4 = 1, PTB_FD6 = 2, PTB_FD8 = 3, PTB_SPECTRAL = 4 } ptb_scheme; /* energy_map.hpp:12 */
 
 typedef struct ptb_context ptb_context;
+typedef struct ptb_comm ptb_comm;
 typedef struct ptb_propagator ptb_propagator;
 typedef struct ptb_transfer ptb_transfer;
 
@@ -199,6 +200,7 @@ typedef struct {
 /* device-timed phases per iteration k = 1..K (CUDA events on the context stream) */
 typedef struct {
   double reference_ms; /* serial fine reference (once per run) */
+  double gather_ms[PTB_MAX_TIMED_ITERS];  /* coarse payload all-gather (0 on one GPU) */
   double parallel_ms[PTB_MAX_TIMED_ITERS];
   double procrustes_ms[PTB_MAX_TIMED_ITERS];
   double sweep_ms[PTB_MAX_TIMED_ITERS];
@@ -215,6 +217,23 @@ ptb_status ptb_parareal_run(ptb_context* ctx, const ptb_run_spec* spec, const do
                             const double* c_coarse, const double* u0, const double* udot0, double* energy_err,
                             double* l2_err, double* residual, int* rank, int* diverged, double* states,
                             double* reference, ptb_phase_times* times);
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ----------------------- */
+/* 128-byte ncclUniqueId created on rank 0 and broadcast by the caller (e.g. torch.distributed) */
+ptb_status ptb_nccl_unique_id(char* out128);
+ptb_status ptb_comm_create(ptb_context* ctx, int rank, int world, const char* id128, ptb_comm** out);
+ptb_status ptb_comm_destroy(ptb_comm* c);
+
+/* ptb_parareal_run with the N slices block-sharded over the ranks of `comm` (null = one GPU).
+ * Every rank passes the same inputs; outputs energy_err/l2_err/residual/rank/diverged are
+ * complete on every rank; states (nullable) receive this rank's slices only (plus n = 0
+ * on rank 0).  Per iteration: one all-gather of the coarse per-slice payload, one of the
+ * error sums, one boundary fine state to the next rank. */
+ptb_status ptb_parareal_run_sharded(ptb_context* ctx, ptb_comm* comm, const ptb_run_spec* spec,
+                                    const double* c_fine, const double* c_coarse, const double* u0,
+                                    const double* udot0, double* energy_err, double* l2_err, double* residual,
+                                    int* rank, int* diverged, double* states, double* reference,
+                                    ptb_phase_times* times);
 
 /* ---- measurement helpers (bench.py) ---------------------------------------------- */
 /* Peak fp64 FMA throughput of the device: independent DFMA chains on every SM, timed

@@ -340,7 +340,8 @@ class RunSpec(C.Structure):
 
 
 class PhaseTimes(C.Structure):
-    _fields_ = [("reference_ms", C.c_double), ("parallel_ms", C.c_double * MAX_TIMED),
+    _fields_ = [("reference_ms", C.c_double), ("gather_ms", C.c_double * MAX_TIMED),
+                ("parallel_ms", C.c_double * MAX_TIMED),
                 ("procrustes_ms", C.c_double * MAX_TIMED), ("sweep_ms", C.c_double * MAX_TIMED),
                 ("finalize_ms", C.c_double * MAX_TIMED), ("iteration_ms", C.c_double * MAX_TIMED)]
 
@@ -357,9 +358,34 @@ def run_spec(**kw) -> RunSpec:
     return s
 
 
+class Comm:
+    """NCCL communicator for slice sharding (one process per GPU).  `broadcast` sends rank 0's
+    128-byte unique id to every rank (e.g. via torch.distributed)."""
+
+    def __init__(self, ctx: Context, rank: int, world: int, broadcast=None):
+        self.rank, self.world = rank, world
+        uid = C.create_string_buffer(128)
+        if world > 1:
+            if rank == 0:
+                check(lib().ptb_nccl_unique_id(uid))
+            raw = broadcast(bytes(uid.raw)) if broadcast else bytes(uid.raw)
+            uid = C.create_string_buffer(raw, 128)
+        h = C.c_void_p()
+        check(lib().ptb_comm_create(ctx.h, C.c_int(rank), C.c_int(world), uid, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ptb_comm_destroy(self.h)
+        except Exception:
+            pass
+
+
 def parareal_run(ctx: Context, spec: RunSpec, c_fine, c_coarse, u0, udot0, keep_states=False,
-                 keep_reference=False):
-    """plain / theta / corrected-coarse-only parareal on the device (parareal.cpp)."""
+                 keep_reference=False, comm: "Comm" = None):
+    """plain / theta / corrected-coarse-only parareal on the device (parareal.cpp); with `comm`
+    the slices are sharded over the ranks (states then hold this rank's slices only)."""
     K, N = spec.iterations, spec.n_couplings
     fine_shape = (spec.fine_n[0],) if spec.dim == 1 else (spec.fine_n[0], spec.fine_n[1])
     f = lambda a: np.ascontiguousarray(a, dtype=np.float64)
@@ -373,13 +399,13 @@ def parareal_run(ctx: Context, spec: RunSpec, c_fine, c_coarse, u0, udot0, keep_
     ref = np.empty((N + 1, 2) + fine_shape) if keep_reference else None
     times = PhaseTimes()
     ip = C.POINTER(C.c_int)
-    check(lib().ptb_parareal_run(ctx.h, C.byref(spec), _dp(cf), _dp(cc), _dp(u0), _dp(v0), _dp(ee), _dp(l2), _dp(res),
-                                 rank.ctypes.data_as(ip), div.ctypes.data_as(ip),
-                                 _dp(states) if states is not None else None, _dp(ref) if ref is not None else None,
-                                 C.byref(times)))
+    check(lib().ptb_parareal_run_sharded(ctx.h, comm.h if comm is not None else None, C.byref(spec), _dp(cf), _dp(cc),
+                                         _dp(u0), _dp(v0), _dp(ee), _dp(l2), _dp(res), rank.ctypes.data_as(ip),
+                                         div.ctypes.data_as(ip), _dp(states) if states is not None else None,
+                                         _dp(ref) if ref is not None else None, C.byref(times)))
     k = min(K, MAX_TIMED)
     t = {"reference_ms": times.reference_ms}
-    for name in ("parallel_ms", "procrustes_ms", "sweep_ms", "finalize_ms", "iteration_ms"):
+    for name in ("parallel_ms", "gather_ms", "procrustes_ms", "sweep_ms", "finalize_ms", "iteration_ms"):
         t[name] = list(getattr(times, name))[:k]
     return dict(energy_err=ee, l2_err=l2, residual=res, rank=rank, diverged=div, states=states, reference=ref,
                 times=t)

@@ -20,9 +20,17 @@ LIB = PKG / "libparatime_b200.so"
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+def _nccl_include():
+    import sysconfig
+
+    pip = Path(sysconfig.get_paths()["purelib"]) / "nvidia" / "nccl" / "include"
+    return pip if (pip / "nccl.h").exists() else Path("/usr/include")
+
+
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{ROOT / 'include'}", f"-I{CSRC}",
+          f"-I{_nccl_include()}"]
 CUDA_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-LINK = ["-lcublas", "-lcudart"]
+LINK = ["-lcublas", "-lcudart", "-ldl"]
 
 
 def sources():

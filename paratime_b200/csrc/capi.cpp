@@ -364,6 +364,7 @@ ptb_status ptb_transfer_destroy(ptb_transfer* t) {
     DeviceGuard g(t->ctx->device);
     if (t->wx) cudaFree(t->wx);
     if (t->wy) cudaFree(t->wy);
+    t->nodes_half.release();
     delete t;
   });
 }

@@ -3,6 +3,7 @@
 
 #include <memory>
 
+#include "ptb_comm.h"
 #include "ptb_driver.h"
 #include "ptb_energy.h"
 #include "ptb_fft.h"
@@ -226,7 +227,20 @@ ptb_status ptb_parareal_run(ptb_context* ctx, const ptb_run_spec* spec, const do
     require(ctx && spec && cf && cc && u0 && v0 && ee && l2 && residual && rank && diverged,
             "parareal: null argument");
     Dev d(ctx->device);
-    run_parareal(ctx, *spec, cf, cc, u0, v0, ee, l2, residual, rank, diverged, states, reference, times);
+    run_parareal(ctx, nullptr, *spec, cf, cc, u0, v0, ee, l2, residual, rank, diverged, states, reference, times);
+  });
+}
+
+ptb_status ptb_parareal_run_sharded(ptb_context* ctx, ptb_comm* comm, const ptb_run_spec* spec, const double* cf,
+                                    const double* cc, const double* u0, const double* v0, double* ee, double* l2,
+                                    double* residual, int* rank, int* diverged, double* states, double* reference,
+                                    ptb_phase_times* times) {
+  return guarded([&] {
+    require(ctx && spec && cf && cc && u0 && v0 && ee && l2 && residual && rank && diverged,
+            "parareal: null argument");
+    Dev d(ctx->device);
+    run_parareal(ctx, comm_of(comm), *spec, cf, cc, u0, v0, ee, l2, residual, rank, diverged, states, reference,
+                 times);
   });
 }
 

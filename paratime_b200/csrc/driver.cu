@@ -1,5 +1,6 @@
 // Device-resident parareal drivers: serial fine reference, plain parareal, theta
-// (data-driven Procrustes) parareal and the corrected-coarse-only ablation.
+// (data-driven Procrustes) parareal and the corrected-coarse-only ablation, with the
+// N time slices block-sharded over one or more GPUs.
 //
 // Reference: /root/reference/proj/src/parareal.cpp
 //   nan_state / fine_stage / coarse_stage   :49-73   divergence -> NaN state
@@ -10,20 +11,31 @@
 //   plain_parareal                          :201-237
 //   corrected_coarse_state / theta_engine   :245-350
 //
-// Every fine/coarse state, snapshot matrix and corrector factor stays in HBM for the whole
-// run.  The parallel stage is one batched K1 call over all N slices (fine) plus one over
-// their restrictions (coarse); snapshot assembly is a batched Lambda into the columns of
-// F and G; the corrector update is ptb::update_svd; the corrected "old" coarse states of
-// the sweep do not depend on the sweep and are computed for all n in one batch before it.
-// Host control flow reads back only per-slice flags and scalar sums.
+// Structure.  The reference's sweep is sequential in n and
+// works on fine states: next[n] = fine_next[n] + I(corrected(C R next[n-1]) - corrected(
+// coarse_next[n])).  Restriction is pointwise, so R(next[n-1]) = R(fine_next[n-1]) +
+// R(I(d_{n-1})) exactly (interpolate_at_coarse_nodes evaluates the interpolant at the
+// shared nodes with the same arithmetic as the full I).  The sequential part therefore
+// runs on coarse vectors only and the fine combine next[n] = fine_next[n] + I(d_n) is one
+// batched pass afterwards.  Lambda-dagger is linear with a separate zero mode, so the
+// corrected difference is Z (z_w - z_old) + (mean_w - mean_old)/N_c with Z = Lambda-dagger(X)
+// computed once per iteration and z = Y^T Lambda(.) — two GEMVs per sweep step instead of
+// three 2D FFTs.  The "old" terms do not depend on the sweep and are one GEMM for all n.
+//
+// Sharding: rank r owns slices [a_r, b_r) and keeps the fine states [a_r-1, b_r).  After
+// the parallel stage the coarse payload of every slice is all-gathered (NCCL); the
+// Procrustes update and the coarse sweep are then replicated (deterministic, identical on
+// every rank), each rank forms its own fine iterates, and the last own state is sent to
+// the next rank.  No fine-grid data crosses GPUs except that one boundary state.
+
+#include <math_constants.h>
 
 #include <cmath>
 #include <cstring>
 #include <limits>
 #include <vector>
 
-#include <math_constants.h>
-
+#include "ptb_comm.h"
 #include "ptb_driver.h"
 #include "ptb_energy.h"
 #include "ptb_procrustes.h"
@@ -34,74 +46,6 @@ namespace {
 constexpr double kNaN = std::numeric_limits<double>::quiet_NaN();
 constexpr double kInf = std::numeric_limits<double>::infinity();
 
-__global__ void k_fill(size_t n, double v, double* a) {
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) a[i] = v;
-}
-
-// per-state NaN fill where flags[b] != 0 (fine_stage/coarse_stage NaN states)
-__global__ void k_nan_where(size_t n, size_t batch, const int32_t* flags, double* u, double* v) {
-  const size_t total = n * batch;
-  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
-    const size_t b = e / n;
-    if (flags[b]) {
-      u[e] = CUDART_NAN;
-      v[e] = CUDART_NAN;
-    }
-  }
-}
-
-// theta sweep combine (parareal.cpp:321-331): next = fine + I(diff), or NaN when any of
-// w, coarse_next[n], fine_next[n] is non-finite.
-__global__ void k_combine_theta(size_t n, const int32_t* wflag, const int32_t* cflag, const int32_t* fflag,
-                                const double* fu, const double* fv, const double* du, const double* dv, double* ou,
-                                double* ov) {
-  const bool bad = *wflag || *cflag || *fflag;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-    if (bad) {
-      ou[i] = CUDART_NAN;
-      ov[i] = CUDART_NAN;
-    } else {
-      ou[i] = __dadd_rn(fu[i], du[i]);
-      ov[i] = __dadd_rn(fv[i], dv[i]);
-    }
-  }
-}
-
-// corrected-coarse-only: next = I(corrected) or NaN when w is non-finite
-__global__ void k_nan_if(size_t n, const int32_t* flag, double* u, double* v) {
-  if (!*flag) return;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-    u[i] = CUDART_NAN;
-    v[i] = CUDART_NAN;
-  }
-}
-
-// plain sweep (parareal.cpp:224-230): next = (I C R next[n-1] + fine_next[n]) - coarse_next[n]
-__global__ void k_combine_plain(size_t n, const int32_t* wflag, const double* cu, const double* cv, const double* fu,
-                                const double* fv, const double* ou_, const double* ov_, double* nu, double* nv) {
-  const bool bad = *wflag;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-    const double a = bad ? CUDART_NAN : cu[i];
-    const double b = bad ? CUDART_NAN : cv[i];
-    nu[i] = __dsub_rn(__dadd_rn(a, fu[i]), ou_[i]);
-    nv[i] = __dsub_rn(__dadd_rn(b, fv[i]), ov_[i]);
-  }
-}
-
-__global__ void k_sub(size_t n, const double* a, const double* b, double* o) {
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
-    o[i] = __dsub_rn(a[i], b[i]);
-}
-
-__global__ void k_state_flags(size_t n, size_t batch, const double* u, const double* v, size_t stride, int32_t* flags) {
-  const size_t b = blockIdx.y;
-  bool ok = true;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
-    ok &= isfinite(u[b * stride + i]) && isfinite(v[b * stride + i]);
-  const int bad = __syncthreads_or(!ok);
-  if (bad && threadIdx.x == 0) atomicOr(&flags[b], 1);
-}
-
 unsigned blocks(ptb_context* ctx, size_t n) {
   return unsigned(std::max<size_t>(1, std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 16)));
 }
@@ -111,30 +55,93 @@ T* dalloc(DeviceBuffer& b, size_t count) {
   return static_cast<T*>(b.get(std::max<size_t>(1, count) * sizeof(T)));
 }
 
-}  // namespace
+#define GRID_STRIDE(i, n) \
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < (n); i += size_t(gridDim.x) * blockDim.x)
 
-// ------------------------------------------------------------------------------------
+__global__ void k_fill(size_t n, double v, double* a) {
+  GRID_STRIDE(i, n) a[i] = v;
+}
+
+// states b of `n` values where flags[b] (or any of the optional flag arrays) is set -> NaN
+__global__ void k_nan_where(size_t n, size_t batch, const int32_t* f0, const int32_t* f1, const int32_t* f2,
+                            double* u, double* v) {
+  GRID_STRIDE(e, n * batch) {
+    const size_t b = e / n;
+    const bool bad = (f0 && f0[b]) || (f1 && f1[b]) || (f2 && f2[b]);
+    if (bad) {
+      u[e] = CUDART_NAN;
+      if (v) v[e] = CUDART_NAN;
+    }
+  }
+}
+
+__global__ void k_axpby(size_t n, double a, const double* x, double b, const double* y, double* out) {
+  GRID_STRIDE(i, n) out[i] = a * x[i] + b * y[i];
+}
+
+__global__ void k_add(size_t n, const double* x, const double* y, double* out) {
+  GRID_STRIDE(i, n) out[i] = __dadd_rn(x[i], y[i]);
+}
+
+__global__ void k_sub(size_t n, const double* x, const double* y, double* out) {
+  GRID_STRIDE(i, n) out[i] = __dsub_rn(x[i], y[i]);
+}
+
+// (x + y) - z, reference order of plain parareal (parareal.cpp:230)
+__global__ void k_add_sub(size_t n, const double* x, const double* y, const double* z, double* out) {
+  GRID_STRIDE(i, n) out[i] = __dsub_rn(__dadd_rn(x[i], y[i]), z[i]);
+}
+
+// u-part of Lambda-dagger(X z, m): u += (m_new - m_old) / Nc  (zero mode of the inverse DFT)
+__global__ void k_add_mean(size_t n, const double* mnew, const double* mold, double* u) {
+  const double dm = mold ? __dsub_rn(*mnew, *mold) : *mnew;
+  const double v = dm / double(n);
+  GRID_STRIDE(i, n) u[i] += v;
+}
+
+__global__ void k_state_flags(size_t n, const double* u, const double* v, size_t stride, int32_t* flags) {
+  const size_t b = blockIdx.y;
+  bool ok = true;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    ok &= isfinite(u[b * stride + i]) && isfinite(v[b * stride + i]);
+  const int bad = __syncthreads_or(!ok);
+  if (bad && threadIdx.x == 0) atomicOr(&flags[b], 1);
+}
+
+__global__ void k_or_flags(int32_t* out, const int32_t* a, const int32_t* b, const int32_t* c) {
+  *out = (*a ? 1 : 0) | (b && *b ? 1 : 0) | (c && *c ? 1 : 0);
+}
+
+}  // namespace
 
 struct Driver {
   ptb_context* ctx;
   const ptb_run_spec& s;
+  Comm single;
+  const Comm* comm;
   ptb_grid fg{}, cg{};
-  size_t nf = 0, nc = 0, N = 0;
+  size_t nf = 0, nc = 0, N = 0, chunk = 0, a = 1, b = 1, L = 0;  // own slices [a, b), L = b - a
   int K = 0;
   ptb_propagator* pf = nullptr;
   ptb_propagator* pc = nullptr;
   ptb_transfer* tr = nullptr;
   EnergyWork ew;
   ProcWork pw;
-  // device arrays
-  DeviceBuffer ref_u, ref_v, cur_u, cur_v, nxt_u, nxt_v, fn_u, fn_v, cn_u, cn_v, cold_u, cold_v;
-  DeviceBuffer flags_f, flags_c, flags_w, flags_s, flags_ref, sums, Fm, Gm, idx, comp, mean, comp2, mean2, wc_u,
-      wc_v, tmp_u, tmp_v, fine_tmp_u, fine_tmp_v, cnew_u, cnew_v, cof_u, cof_v;
-  std::vector<int32_t> ref_bad;  // per n (host)
   DevCorrector corr;
   ptb_phase_times* times = nullptr;
+  // fine, own: states [a-1, b) -> index 0..L
+  DeviceBuffer cur_u, cur_v, nxt_u, nxt_v, ref_u, ref_v, fn_u, fn_v, fine_u, fine_v, fine2_u, fine2_v;
+  // coarse, one slot per slice n = 1..N at index (n-1) (padded to world*chunk)
+  DeviceBuffer rf_u, rf_v, kn_u, kn_v, d_u, d_v, w_u, w_v, rik_u, rik_v, own_pay, all_pay;
+  DeviceBuffer ff, cf, wf, bad, sflags, sums_own, sums_all, own_sc, all_sc;
+  DeviceBuffer rn_u, rn_v, ri_u, ri_v, init_u, init_v, init_cu, init_cv;
+  DeviceBuffer comp, mean, comp_old, mean_old, zold, zw, Zu, Zv, Fm, Gm, idx, tmpc;
+  std::vector<int32_t> ref_bad;
+  const double* cf_dev = nullptr;  // coarse speed
 
-  Driver(ptb_context* c, const ptb_run_spec& spec) : ctx(c), s(spec), ew(c), pw(c) {}
+  Driver(ptb_context* c, const Comm* cm, const ptb_run_spec& spec) : ctx(c), s(spec), comm(cm), ew(c), pw(c) {
+    if (!comm) comm = &single;
+  }
   ~Driver() {
     ptb_propagator_destroy(pf);
     ptb_propagator_destroy(pc);
@@ -142,23 +149,48 @@ struct Driver {
   }
 
   cudaStream_t st() const { return ctx->stream; }
-
+  void copy(double* dst, const double* src, size_t n) {
+    if (n) PTB_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st()));
+  }
   void nan_fill(double* p, size_t n) {
+    if (!n) return;
     k_fill<<<blocks(ctx, n), 256, 0, st()>>>(n, kNaN, p);
     PTB_LAUNCH_CHECK(ctx);
   }
-
-  void copy(double* dst, const double* src, size_t n) {
-    PTB_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st()));
+  void nan_where(size_t n, size_t batch, const int32_t* f0, const int32_t* f1, const int32_t* f2, double* u,
+                 double* v) {
+    if (!n || !batch) return;
+    k_nan_where<<<blocks(ctx, n * batch), 256, 0, st()>>>(n, batch, f0, f1, f2, u, v);
+    PTB_LAUNCH_CHECK(ctx);
+  }
+  template <typename T>
+  std::vector<T> to_host(const T* d, size_t n) {
+    std::vector<T> h(n);
+    if (n) PTB_CUDA_CHECK(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, st()));
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st()));
+    return h;
   }
 
-  void setup(const double* cf, const double* cc) {
+  // own-index accessors (fine): state m in [a-1, b) at index m - (a-1)
+  double* CU(size_t m) { return static_cast<double*>(cur_u.ptr) + (m - (a - 1)) * nf; }
+  double* CV(size_t m) { return static_cast<double*>(cur_v.ptr) + (m - (a - 1)) * nf; }
+  double* NU(size_t m) { return static_cast<double*>(nxt_u.ptr) + (m - (a - 1)) * nf; }
+  double* NV(size_t m) { return static_cast<double*>(nxt_v.ptr) + (m - (a - 1)) * nf; }
+  double* RU(size_t m) { return static_cast<double*>(ref_u.ptr) + (m - (a - 1)) * nf; }
+  double* RV(size_t m) { return static_cast<double*>(ref_v.ptr) + (m - (a - 1)) * nf; }
+  double* FU(size_t n) { return static_cast<double*>(fn_u.ptr) + (n - a) * nf; }  // own slices
+  double* FV(size_t n) { return static_cast<double*>(fn_v.ptr) + (n - a) * nf; }
+  // coarse per-slice slots (n = 1..N)
+  static double* slot(DeviceBuffer& bf, size_t n, size_t nc_) { return static_cast<double*>(bf.ptr) + (n - 1) * nc_; }
+  int32_t* fl(DeviceBuffer& bf) { return static_cast<int32_t*>(bf.ptr); }
+
+  void setup(const double* cfh, const double* cch) {
     fg.dim = cg.dim = s.dim;
-    for (int a = 0; a < 2; ++a) {
-      fg.n[a] = s.fine_n[a];
-      fg.h[a] = s.fine_h[a];
-      cg.n[a] = s.coarse_n[a];
-      cg.h[a] = s.coarse_h[a];
+    for (int k = 0; k < 2; ++k) {
+      fg.n[k] = s.fine_n[k];
+      fg.h[k] = s.fine_h[k];
+      cg.n[k] = s.coarse_n[k];
+      cg.h[k] = s.coarse_h[k];
     }
     validate_grid(fg);
     validate_grid(cg);
@@ -166,405 +198,645 @@ struct Driver {
     nc = grid_size(cg);
     N = s.n_couplings;
     K = s.iterations;
-    // PropagatorConfig x2 (propagator.cpp:11-27)
-    ptb_status st1 = ptb_propagator_create(ctx, &fg, cf, s.dt_fine, s.m_fine, &pf);
-    if (st1 != PTB_OK) fail(st1, g_last_error);
-    ptb_status st2 = ptb_propagator_create(ctx, &cg, cc, s.dt_coarse, s.m_coarse, &pc);
-    if (st2 != PTB_OK) fail(st2, g_last_error);
-    // CouplingSchedule (parareal.cpp:172-188)
+    ptb_status e1 = ptb_propagator_create(ctx, &fg, cfh, s.dt_fine, s.m_fine, &pf);
+    if (e1 != PTB_OK) fail(e1, g_last_error);
+    ptb_status e2 = ptb_propagator_create(ctx, &cg, cch, s.dt_coarse, s.m_coarse, &pc);
+    if (e2 != PTB_OK) fail(e2, g_last_error);
     require(s.T > 0.0 && s.dt_com > 0.0 && N > 0, "CouplingSchedule: T, dt_com, N must be positive");
     require(std::abs(double(N) * s.dt_com - s.T) <= 1e-9 * s.T, "CouplingSchedule: N * dt_com must equal T");
     require(std::abs(double(s.m_fine) * s.dt_fine - s.dt_com) <= 1e-12 * s.dt_com,
             "CouplingSchedule: fine steps_per_coupling * dt != dt_com");
     require(std::abs(double(s.m_coarse) * s.dt_coarse - s.dt_com) <= 1e-12 * s.dt_com,
             "CouplingSchedule: coarse steps_per_coupling * dt != dt_com");
-    ptb_status st3 = ptb_transfer_create(ctx, &cg, &fg, s.interp, &tr);
-    if (st3 != PTB_OK) fail(st3, g_last_error);
+    ptb_status e3 = ptb_transfer_create(ctx, &cg, &fg, s.interp, &tr);
+    if (e3 != PTB_OK) fail(e3, g_last_error);
     require(K >= 0, "parareal: negative iteration count");
     require(s.variant >= 0 && s.variant <= 3, "parareal: unknown variant");
     require(s.mode == PTB_MODE_FAST || s.mode == PTB_MODE_EXACT, "parareal: unknown propagator mode");
-    const size_t S = (N + 1) * nf;
-    dalloc<double>(ref_u, S);
-    dalloc<double>(ref_v, S);
-    dalloc<double>(cur_u, S);
-    dalloc<double>(cur_v, S);
-    dalloc<double>(nxt_u, S);
-    dalloc<double>(nxt_v, S);
-    dalloc<double>(fn_u, N * nf);
-    dalloc<double>(fn_v, N * nf);
-    dalloc<double>(cn_u, N * nc);
-    dalloc<double>(cn_v, N * nc);
-    dalloc<int32_t>(flags_f, N);
-    dalloc<int32_t>(flags_c, N);
-    dalloc<int32_t>(flags_w, N + 1);
-    dalloc<int32_t>(flags_s, N + 1);
-    dalloc<double>(sums, 4 * (N + 1));
-    dalloc<double>(wc_u, nc);
-    dalloc<double>(wc_v, nc);
+    cf_dev = ptb_propagator_speed(pc);
+    // static block partition of slices 1..N (parareal.cpp:25-47 chunking)
+    const size_t W = size_t(comm->world);
+    chunk = (N + W - 1) / W;
+    a = std::min(N + 1, 1 + size_t(comm->rank) * chunk);
+    b = std::min(N + 1, a + chunk);
+    L = b - a;
+    const size_t S = (L + 1) * nf;
+    for (DeviceBuffer* bf : {&cur_u, &cur_v, &nxt_u, &nxt_v, &ref_u, &ref_v}) dalloc<double>(*bf, S);
+    for (DeviceBuffer* bf : {&fn_u, &fn_v, &fine_u, &fine_v, &fine2_u, &fine2_v}) dalloc<double>(*bf, L * nf);
+    const size_t P = W * chunk;  // padded slice slots
+    for (DeviceBuffer* bf : {&rf_u, &rf_v, &kn_u, &kn_v, &d_u, &d_v, &w_u, &w_v, &rik_u, &rik_v})
+      dalloc<double>(*bf, P * nc);
+    for (DeviceBuffer* bf : {&ff, &cf, &wf, &bad, &sflags}) dalloc<int32_t>(*bf, P + 1);
+    for (DeviceBuffer* bf : {&rn_u, &rn_v, &ri_u, &ri_v, &init_cu, &init_cv}) dalloc<double>(*bf, nc);
+    dalloc<double>(init_u, nf);
+    dalloc<double>(init_v, nf);
   }
 
-  double* RU(size_t n) { return static_cast<double*>(ref_u.ptr) + n * nf; }
-  double* RV(size_t n) { return static_cast<double*>(ref_v.ptr) + n * nf; }
-  double* CU(size_t n) { return static_cast<double*>(cur_u.ptr) + n * nf; }
-  double* CV(size_t n) { return static_cast<double*>(cur_v.ptr) + n * nf; }
-  double* NU(size_t n) { return static_cast<double*>(nxt_u.ptr) + n * nf; }
-  double* NV(size_t n) { return static_cast<double*>(nxt_v.ptr) + n * nf; }
-  double* FU(size_t n) { return static_cast<double*>(fn_u.ptr) + (n - 1) * nf; }  // n = 1..N
-  double* FV(size_t n) { return static_cast<double*>(fn_v.ptr) + (n - 1) * nf; }
-  double* KU(size_t n) { return static_cast<double*>(cn_u.ptr) + (n - 1) * nc; }
-  double* KV(size_t n) { return static_cast<double*>(cn_v.ptr) + (n - 1) * nc; }
-  int32_t* fl(DeviceBuffer& b) { return static_cast<int32_t*>(b.ptr); }
-
-  // coarse_stage on one fine state (parareal.cpp:66-73) into (wu, wv); flag -> *flag
-  void coarse_stage(const double* u, const double* v, double* wu, double* wv, int32_t* flag) {
-    restrict_fields(tr, 1, u, wu);
-    restrict_fields(tr, 1, v, wv);
-    PTB_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), st()));
-    propagate(pc, pc->steps, 1, wu, wv, flag, s.mode);
-    k_nan_where<<<blocks(ctx, nc), 256, 0, st()>>>(nc, 1, flag, wu, wv);
-    PTB_LAUNCH_CHECK(ctx);
+  // ---- collectives -------------------------------------------------------------------
+  // Gather the coarse payload of the own slices: R(fine_next), coarse_next, flags.
+  void gather_payload() {
+    const size_t per = chunk * (4 * nc) * sizeof(double) + 2 * chunk * sizeof(int32_t);
+    char* own = static_cast<char*>(own_pay.get(per));
+    char* all = static_cast<char*>(all_pay.get(per * size_t(comm->world)));
+    const size_t bc = chunk * nc * sizeof(double);
+    if (comm->world == 1) return;  // single GPU: the own slots are the global slots
+    // pack own slots (slice a..b-1 live at global slots a-1..)
+    auto pack = [&](DeviceBuffer& src, size_t k) {
+      if (L) PTB_CUDA_CHECK(cudaMemcpyAsync(own + k * bc, slot(src, a, nc), L * nc * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, st()));
+    };
+    pack(rf_u, 0);
+    pack(rf_v, 1);
+    pack(kn_u, 2);
+    pack(kn_v, 3);
+    int32_t* of = reinterpret_cast<int32_t*>(own + 4 * bc);
+    if (L) {
+      PTB_CUDA_CHECK(cudaMemcpyAsync(of, fl(ff) + (a - 1), L * sizeof(int32_t), cudaMemcpyDeviceToDevice, st()));
+      PTB_CUDA_CHECK(cudaMemcpyAsync(of + chunk, fl(cf) + (a - 1), L * sizeof(int32_t), cudaMemcpyDeviceToDevice, st()));
+    }
+    comm->allgather(own, all, per, st());
+    for (int r = 0; r < comm->world; ++r) {
+      const size_t ra = 1 + size_t(r) * chunk;
+      if (ra > N) break;
+      const size_t rl = std::min(N + 1, ra + chunk) - ra;
+      const char* src = all + size_t(r) * per;
+      auto unpack = [&](DeviceBuffer& dst, size_t k) {
+        PTB_CUDA_CHECK(cudaMemcpyAsync(slot(dst, ra, nc), src + k * bc, rl * nc * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st()));
+      };
+      unpack(rf_u, 0);
+      unpack(rf_v, 1);
+      unpack(kn_u, 2);
+      unpack(kn_v, 3);
+      const int32_t* rfl = reinterpret_cast<const int32_t*>(src + 4 * bc);
+      PTB_CUDA_CHECK(cudaMemcpyAsync(fl(ff) + (ra - 1), rfl, rl * sizeof(int32_t), cudaMemcpyDeviceToDevice, st()));
+      PTB_CUDA_CHECK(cudaMemcpyAsync(fl(cf) + (ra - 1), rfl + chunk, rl * sizeof(int32_t), cudaMemcpyDeviceToDevice, st()));
+    }
   }
 
-  // reference_or_nan (parareal.cpp:133-145)
+  // gather per-slice scalars: `own` (chunk * per) -> `all` slots n = 1..N
+  std::vector<double> gather_scalars(const double* own_dev, size_t per) {
+    std::vector<double> h;
+    if (comm->world == 1) {
+      h = to_host(own_dev, N * per);
+      return h;
+    }
+    double* all = dalloc<double>(all_sc, size_t(comm->world) * chunk * per);
+    comm->allgather(own_dev, all, chunk * per * sizeof(double), st());
+    h = to_host(all, size_t(comm->world) * chunk * per);
+    h.resize(N * per);
+    return h;
+  }
+
+  // ---- stages ------------------------------------------------------------------------
+  void coarse_propagate(double* u, double* v, size_t batch, int32_t* flags) {
+    if (!batch) return;
+    PTB_CUDA_CHECK(cudaMemsetAsync(flags, 0, batch * sizeof(int32_t), st()));
+    propagate(pc, pc->steps, batch, u, v, flags, s.mode);
+    nan_where(nc, batch, flags, nullptr, nullptr, u, v);
+  }
+
+  // reference_or_nan (parareal.cpp:133-145): chain on every rank up to its last slice
   void serial_reference() {
-    copy(RU(0), s_u0, nf);
-    copy(RV(0), s_v0, nf);
-    int32_t* f = fl(flags_w);
+    copy(static_cast<double*>(ref_u.ptr), fl_init_u(), nf);
+    copy(static_cast<double*>(ref_v.ptr), fl_init_v(), nf);
+    int32_t* f = fl(sflags);
     PTB_CUDA_CHECK(cudaMemsetAsync(f, 0, (N + 1) * sizeof(int32_t), st()));
-    for (size_t n = 1; n <= N; ++n) {
-      copy(RU(n), RU(n - 1), nf);
-      copy(RV(n), RV(n - 1), nf);
-      propagate(pf, pf->steps, 1, RU(n), RV(n), f + n, s.mode);
+    // walk the chain 1..b-1 with a rolling state, storing the own states [a-1, b)
+    double* pu = dalloc<double>(fine2_u, std::max<size_t>(L, 1) * nf);
+    double* pv = dalloc<double>(fine2_v, std::max<size_t>(L, 1) * nf);
+    copy(pu, fl_init_u(), nf);
+    copy(pv, fl_init_v(), nf);
+    for (size_t n = 1; n < b; ++n) {
+      propagate(pf, pf->steps, 1, pu, pv, f + n, s.mode);
+      if (n >= a - 1) {
+        copy(RU(n), pu, nf);
+        copy(RV(n), pv, nf);
+      }
     }
-    std::vector<int32_t> h(N + 1);
-    PTB_CUDA_CHECK(cudaMemcpyAsync(h.data(), f, (N + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st()));
-    PTB_CUDA_CHECK(cudaStreamSynchronize(st()));
-    bool any = false;
-    for (size_t n = 1; n <= N; ++n) any |= h[n] != 0;
-    if (any) {  // serial_fine threw: every n >= 1 becomes NaN
-      nan_fill(RU(1), N * nf);
-      nan_fill(RV(1), N * nf);
+    // any divergence anywhere in 1..N makes every reference slot n >= 1 NaN
+    std::vector<int32_t> h = to_host(f, N + 1);
+    double any = 0.0;
+    for (size_t n = 1; n < b; ++n) any = std::max(any, double(h[n]));
+    double* sc = dalloc<double>(own_sc, chunk);
+    std::vector<double> mine(chunk, 0.0);
+    mine[0] = any;
+    PTB_CUDA_CHECK(cudaMemcpyAsync(sc, mine.data(), chunk * sizeof(double), cudaMemcpyHostToDevice, st()));
+    double global_any = any;
+    if (comm->world > 1) {
+      double* all = dalloc<double>(all_sc, size_t(comm->world) * chunk);
+      comm->allgather(sc, all, chunk * sizeof(double), st());
+      std::vector<double> g = to_host(all, size_t(comm->world) * chunk);
+      for (int r = 0; r < comm->world; ++r) global_any = std::max(global_any, g[size_t(r) * chunk]);
     }
-    // reference finiteness per n (init may itself be non-finite)
-    int32_t* rf = dalloc<int32_t>(flags_ref, N + 1);
-    PTB_CUDA_CHECK(cudaMemsetAsync(rf, 0, (N + 1) * sizeof(int32_t), st()));
-    k_state_flags<<<dim3(blocks(ctx, nf) > 64 ? 64 : blocks(ctx, nf), unsigned(N + 1)), 256, 0, st()>>>(
-        nf, N + 1, RU(0), RV(0), nf, rf);
-    PTB_LAUNCH_CHECK(ctx);
-    ref_bad.assign(N + 1, 0);
-    PTB_CUDA_CHECK(cudaMemcpyAsync(ref_bad.data(), rf, (N + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st()));
-    PTB_CUDA_CHECK(cudaStreamSynchronize(st()));
-  }
-
-  const double* s_u0 = nullptr;
-  const double* s_v0 = nullptr;
-
-  // serial_coarse_init (parareal.cpp:147-159) into cur
-  void serial_coarse_init() {
-    copy(CU(0), s_u0, nf);
-    copy(CV(0), s_v0, nf);
-    int32_t* f = fl(flags_w);
-    for (size_t n = 1; n <= N; ++n) {
-      coarse_stage(CU(n - 1), CV(n - 1), wcu(), wcv(), f + n);
-      interpolate_fields(tr, 1, wcu(), CU(n));
-      interpolate_fields(tr, 1, wcv(), CV(n));
-      k_nan_where<<<blocks(ctx, nf), 256, 0, st()>>>(nf, 1, f + n, CU(n), CV(n));
+    if (global_any > 0.0) {
+      const size_t first = std::max<size_t>(a - 1, 1);
+      if (b > first) {
+        nan_fill(RU(first), (b - first) * nf);
+        nan_fill(RV(first), (b - first) * nf);
+      }
+    }
+    // reference finiteness of own slots (for measure) — every rank keeps the full vector
+    PTB_CUDA_CHECK(cudaMemsetAsync(f, 0, (N + 1) * sizeof(int32_t), st()));
+    if (L) {
+      k_state_flags<<<dim3(std::min(64u, blocks(ctx, nf)), unsigned(L)), 256, 0, st()>>>(nf, RU(a), RV(a), nf, f + a);
       PTB_LAUNCH_CHECK(ctx);
     }
+    ref_bad = to_host(f, N + 1);  // own entries valid; others unused
   }
-  double* wcu() { return static_cast<double*>(wc_u.ptr); }
-  double* wcv() { return static_cast<double*>(wc_v.ptr); }
 
-  // finalize_iteration (parareal.cpp:107-128) on states (su, sv); previous may be null
-  void finalize(double* su, double* sv, double* pu, double* pv, double* ee, double* l2, int* diverged,
-                double* states_out) {
-    int32_t* sf = fl(flags_s);
-    PTB_CUDA_CHECK(cudaMemsetAsync(sf, 0, (N + 1) * sizeof(int32_t), st()));
-    k_state_flags<<<dim3(std::min(64u, blocks(ctx, nf)), unsigned(N + 1)), 256, 0, st()>>>(nf, N + 1, su, sv, nf, sf);
+  double* fl_init_u() { return static_cast<double*>(init_u.ptr); }
+  double* fl_init_v() { return static_cast<double*>(init_v.ptr); }
+
+  // finalize_iteration (parareal.cpp:107-128) on own states (su, sv) [a-1, b); prev may be null
+  void finalize(DeviceBuffer& su_b, DeviceBuffer& sv_b, DeviceBuffer* pu_b, DeviceBuffer* pv_b, double* ee, double* l2,
+                int* diverged, double* states_out) {
+    double* su = static_cast<double*>(su_b.ptr);
+    double* sv = static_cast<double*>(sv_b.ptr);
+    int32_t* f = fl(sflags);
+    PTB_CUDA_CHECK(cudaMemsetAsync(f, 0, (L + 1) * sizeof(int32_t), st()));
+    k_state_flags<<<dim3(std::min(64u, blocks(ctx, nf)), unsigned(L + 1)), 256, 0, st()>>>(nf, su, sv, nf, f);
     PTB_LAUNCH_CHECK(ctx);
-    double* sm = static_cast<double*>(sums.ptr);
-    pair_energy_sums(ew, fg, s.metric_scheme, N, su + nf, sv + nf, nf, RU(1), RV(1), nf, ptb_propagator_speed(pf),
-                     sm + 4);
-    std::vector<int32_t> bad(N + 1);
-    std::vector<double> h(4 * (N + 1));
-    PTB_CUDA_CHECK(cudaMemcpyAsync(bad.data(), sf, (N + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st()));
-    PTB_CUDA_CHECK(cudaMemcpyAsync(h.data() + 4, sm + 4, 4 * N * sizeof(double), cudaMemcpyDeviceToHost, st()));
-    PTB_CUDA_CHECK(cudaStreamSynchronize(st()));
+    double* own = dalloc<double>(sums_own, chunk * 5);
+    PTB_CUDA_CHECK(cudaMemsetAsync(own, 0, chunk * 5 * sizeof(double), st()));
+    if (L) {
+      double* tmp = dalloc<double>(sums_all, L * 4);
+      pair_energy_sums(ew, fg, s.metric_scheme, L, su + nf, sv + nf, nf, RU(a), RV(a), nf, ptb_propagator_speed(pf),
+                       tmp);
+      // pack [flag, s0..s3] per own slice
+      PTB_CUDA_CHECK(cudaMemcpy2DAsync(own + 1, 5 * sizeof(double), tmp, 4 * sizeof(double), 4 * sizeof(double), L,
+                                       cudaMemcpyDeviceToDevice, st()));
+    }
+    std::vector<int32_t> hf = to_host(f, L + 1);
+    {  // flags as doubles into column 0
+      std::vector<double> fd(L);
+      for (size_t i = 0; i < L; ++i) fd[i] = hf[i + 1];
+      if (L)
+        PTB_CUDA_CHECK(cudaMemcpy2DAsync(own, 5 * sizeof(double), fd.data(), sizeof(double), sizeof(double), L,
+                                         cudaMemcpyHostToDevice, st()));
+    }
+    const std::vector<double> g = gather_scalars(own, 5);
     const double vol = [&] {
       double v = 1.0;
-      for (int a = 0; a < fg.dim; ++a) v *= fg.h[a];
+      for (int k = 0; k < fg.dim; ++k) v *= fg.h[k];
       return v;
     }();
-    bool dv = false;
-    for (size_t n = 0; n <= N; ++n) {
-      double e = 0.0, l = 0.0;
-      if (n > 0) {  // measure (parareal.cpp:80-103)
-        if (bad[n] || ref_bad[n]) {
-          e = l = kInf;
-        } else {
-          const double sd = h[4 * n], sr = h[4 * n + 1], ld = h[4 * n + 2], lr = h[4 * n + 3];
-          const double e_ref = 0.5 * sr * vol, e_diff = 0.5 * sd * vol;
-          e = (e_ref == 0.0) ? (e_diff == 0.0 ? 0.0 : kInf) : std::sqrt(e_diff / e_ref);
-          l = (lr == 0.0) ? (ld == 0.0 ? 0.0 : kInf) : std::sqrt(ld / lr);
-        }
+    // n = 0: the initial condition (identical on every rank)
+    bool dv = init_bad;
+    ee[0] = 0.0;
+    l2[0] = 0.0;
+    for (size_t n = 1; n <= N; ++n) {
+      const double* q = &g[(n - 1) * 5];
+      const bool bad_n = q[0] != 0.0;
+      double e, l;
+      if (bad_n || ref_bad_global[n]) {
+        e = l = kInf;
+      } else {
+        const double e_ref = 0.5 * q[2] * vol, e_diff = 0.5 * q[1] * vol;
+        e = (e_ref == 0.0) ? (e_diff == 0.0 ? 0.0 : kInf) : std::sqrt(e_diff / e_ref);
+        l = (q[4] == 0.0) ? (q[3] == 0.0 ? 0.0 : kInf) : std::sqrt(q[3] / q[4]);
       }
       ee[n] = e;
       l2[n] = l;
-      if (bad[n]) {
-        dv = true;
-        if (pu) {
-          copy(su + n * nf, pu + n * nf, nf);
-          copy(sv + n * nf, pv + n * nf, nf);
-        }
-      }
+      if (bad_n) dv = true;
     }
     *diverged = dv ? 1 : 0;
+    // clamp own non-finite states to the previous iterate
+    if (pu_b) {
+      for (size_t i = 1; i <= L; ++i)
+        if (hf[i]) {
+          copy(su + i * nf, static_cast<double*>(pu_b->ptr) + i * nf, nf);
+          copy(sv + i * nf, static_cast<double*>(pv_b->ptr) + i * nf, nf);
+        }
+    }
     if (states_out) {
-      for (size_t n = 0; n <= N; ++n) {
-        PTB_CUDA_CHECK(cudaMemcpyAsync(states_out + (2 * n) * nf, su + n * nf, nf * sizeof(double),
+      for (size_t m = (a == 1 ? 0 : a); m < b; ++m) {
+        const size_t i = m - (a - 1);
+        PTB_CUDA_CHECK(cudaMemcpyAsync(states_out + (2 * m) * nf, su + i * nf, nf * sizeof(double),
                                        cudaMemcpyDeviceToHost, st()));
-        PTB_CUDA_CHECK(cudaMemcpyAsync(states_out + (2 * n + 1) * nf, sv + n * nf, nf * sizeof(double),
+        PTB_CUDA_CHECK(cudaMemcpyAsync(states_out + (2 * m + 1) * nf, sv + i * nf, nf * sizeof(double),
                                        cudaMemcpyDeviceToHost, st()));
       }
       PTB_CUDA_CHECK(cudaStreamSynchronize(st()));
     }
   }
 
-  // parallel stage: fine_next[n] = F(cur[n-1]), coarse_next[n] = C(R(cur[n-1])), n = 1..N
+  bool init_bad = false;
+  std::vector<int32_t> ref_bad_global;
+
+  void gather_ref_flags() {
+    // every rank needs reference finiteness of all n for the error table
+    double* own = dalloc<double>(own_sc, chunk);
+    std::vector<double> h(chunk, 0.0);
+    for (size_t n = a; n < b; ++n) h[n - a] = ref_bad[n];
+    PTB_CUDA_CHECK(cudaMemcpyAsync(own, h.data(), chunk * sizeof(double), cudaMemcpyHostToDevice, st()));
+    const std::vector<double> g = gather_scalars(own, 1);
+    ref_bad_global.assign(N + 1, 0);
+    for (size_t n = 1; n <= N; ++n) ref_bad_global[n] = g[n - 1] != 0.0;
+  }
+
+  // parallel stage on own slices: fine_next[n] = F(cur[n-1]), coarse_next[n] = C(R cur[n-1])
   void parallel_stage() {
-    copy(FU(1), CU(0), N * nf);
-    copy(FV(1), CV(0), N * nf);
-    PTB_CUDA_CHECK(cudaMemsetAsync(fl(flags_f), 0, N * sizeof(int32_t), st()));
-    PTB_CUDA_CHECK(cudaMemsetAsync(fl(flags_c), 0, N * sizeof(int32_t), st()));
-    propagate(pf, pf->steps, N, FU(1), FV(1), fl(flags_f), s.mode);
-    k_nan_where<<<blocks(ctx, N * nf), 256, 0, st()>>>(nf, N, fl(flags_f), FU(1), FV(1));
+    if (!L) return;
+    copy(FU(a), CU(a - 1), L * nf);
+    copy(FV(a), CV(a - 1), L * nf);
+    int32_t* ffo = fl(ff) + (a - 1);
+    int32_t* cfo = fl(cf) + (a - 1);
+    PTB_CUDA_CHECK(cudaMemsetAsync(ffo, 0, L * sizeof(int32_t), st()));
+    propagate(pf, pf->steps, L, FU(a), FV(a), ffo, s.mode);
+    nan_where(nf, L, ffo, nullptr, nullptr, FU(a), FV(a));
+    restrict_fields(tr, L, CU(a - 1), slot(kn_u, a, nc));
+    restrict_fields(tr, L, CV(a - 1), slot(kn_v, a, nc));
+    coarse_propagate(slot(kn_u, a, nc), slot(kn_v, a, nc), L, cfo);
+    restrict_fields(tr, L, FU(a), slot(rf_u, a, nc));
+    restrict_fields(tr, L, FV(a), slot(rf_v, a, nc));
+  }
+
+  // Z = Lambda-dagger(X, 0): u and udot blocks (Nc x r each)
+  void precompute_Z(const DevCorrector& c) {
+    const int r = c.rank;
+    if (r == 0) return;
+    const size_t rows = size_t(cg.dim + 1) * nc;
+    double* zu = dalloc<double>(Zu, nc * r);
+    double* zv = dalloc<double>(Zv, nc * r);
+    double* m0 = dalloc<double>(mean_old, std::max<size_t>(N, size_t(r)));
+    PTB_CUDA_CHECK(cudaMemsetAsync(m0, 0, size_t(r) * sizeof(double), st()));
+    from_energy_components(ew, cg, size_t(r), c.Xp(), rows, m0, cf_dev, zu, zv, nc);
+  }
+
+  // corrected coarse vectors for `batch` coarse states: Z (Y^T Lambda(.)) + mean/Nc, stored to (ou, ov)
+  // (omega_identity: Lambda-dagger(Lambda(.)))
+  void corrected_batch(const DevCorrector& c, bool omega_identity, size_t batch, const double* u, const double* v,
+                       double* ou, double* ov, double* zout, double* mout) {
+    const size_t rows = size_t(cg.dim + 1) * nc;
+    double* cp = dalloc<double>(comp, rows * batch);
+    energy_components(ew, cg, s.scheme, batch, u, v, nc, nullptr, cf_dev, cp, rows, mout);
+    if (omega_identity) {
+      if (ou) from_energy_components(ew, cg, batch, cp, rows, mout, cf_dev, ou, ov, nc);
+      return;
+    }
+    if (c.rank == 0) {
+      if (zout) PTB_CUDA_CHECK(cudaMemsetAsync(zout, 0, sizeof(double), st()));
+      return;
+    }
+    gemm(ctx, true, false, c.rank, int(batch), int(rows), 1.0, c.Yp(), int(rows), cp, int(rows), 0.0, zout, c.rank);
+  }
+
+  // ---- sweeps (coarse, replicated) --------------------------------------------------------
+
+  // R(next) for the first step: R(init)
+  void restrict_init(double* ou, double* ov) {
+    restrict_fields(tr, 1, fl_init_u(), ou);
+    restrict_fields(tr, 1, fl_init_v(), ov);
+  }
+
+  // d (coarse) = Z (z_w - z_old) + (m_w - m_old)/Nc  [u], Zv (z_w - z_old) [udot]
+  void assemble_d(const DevCorrector& c, const double* zw_, const double* zold_, const double* mw, const double* mold,
+                  double* du, double* dv) {
+    const int r = c.rank;
+    double* dz = dalloc<double>(tmpc, std::max(r, 1));
+    if (r > 0) {
+      if (zold_) {
+        k_sub<<<1, 256, 0, st()>>>(size_t(r), zw_, zold_, dz);
+        PTB_LAUNCH_CHECK(ctx);
+      } else {
+        copy(dz, zw_, size_t(r));
+      }
+      gemm(ctx, false, false, int(nc), 1, r, 1.0, static_cast<double*>(Zu.ptr), int(nc), dz, r, 0.0, du, int(nc));
+      gemm(ctx, false, false, int(nc), 1, r, 1.0, static_cast<double*>(Zv.ptr), int(nc), dz, r, 0.0, dv, int(nc));
+    } else {
+      PTB_CUDA_CHECK(cudaMemsetAsync(du, 0, nc * sizeof(double), st()));
+      PTB_CUDA_CHECK(cudaMemsetAsync(dv, 0, nc * sizeof(double), st()));
+    }
+    k_add_mean<<<blocks(ctx, nc), 256, 0, st()>>>(nc, mw, mold, du);
     PTB_LAUNCH_CHECK(ctx);
-    restrict_fields(tr, N, CU(0), KU(1));
-    restrict_fields(tr, N, CV(0), KV(1));
-    propagate(pc, pc->steps, N, KU(1), KV(1), fl(flags_c), s.mode);
-    k_nan_where<<<blocks(ctx, N * nc), 256, 0, st()>>>(nc, N, fl(flags_c), KU(1), KV(1));
-    PTB_LAUNCH_CHECK(ctx);
+  }
+
+  // theta sweep, additive (parareal.cpp:311-331) on coarse vectors -> d[n], bad[n]
+  void theta_sweep(const DevCorrector& c, bool omega_identity) {
+    const size_t rows = size_t(cg.dim + 1) * nc;
+    int32_t* wfl = fl(wf);
+    PTB_CUDA_CHECK(cudaMemsetAsync(wfl, 0, (N + 1) * sizeof(int32_t), st()));
+    // "old" terms for n = 2..N, one batch
+    double* zo = nullptr;
+    double* mo = dalloc<double>(mean_old, std::max<size_t>(N, size_t(c.rank)));
+    double* cold = nullptr;
+    if (N >= 2) {
+      if (omega_identity) {
+        cold = dalloc<double>(comp_old, rows * (N - 1));
+        energy_components(ew, cg, s.scheme, N - 1, slot(kn_u, 2, nc), slot(kn_v, 2, nc), nc, nullptr, cf_dev, cold,
+                          rows, mo + 1);
+      } else {
+        precompute_Z(c);
+        zo = dalloc<double>(zold, std::max<size_t>(1, size_t(c.rank) * N));
+        corrected_batch(c, false, N - 1, slot(kn_u, 2, nc), slot(kn_v, 2, nc), nullptr, nullptr,
+                        zo + size_t(c.rank), mo + 1);
+      }
+    }
+    double* zwp = dalloc<double>(zw, std::max(c.rank, 1));
+    double* mw = dalloc<double>(mean, std::max<size_t>(N, 1));
+    double* ru = static_cast<double*>(rn_u.ptr);
+    double* rv = static_cast<double*>(rn_v.ptr);
+    // n = 1: next[1] = fine_next[1]  ->  d_1 = 0, R(next[1]) = R(fine_next[1])
+    PTB_CUDA_CHECK(cudaMemsetAsync(slot(d_u, 1, nc), 0, nc * sizeof(double), st()));
+    PTB_CUDA_CHECK(cudaMemsetAsync(slot(d_v, 1, nc), 0, nc * sizeof(double), st()));
+    copy(ru, slot(rf_u, 1, nc), nc);
+    copy(rv, slot(rf_v, 1, nc), nc);
+    for (size_t n = 2; n <= N; ++n) {
+      coarse_propagate(ru, rv, 1, wfl + n);  // w = C(R next[n-1]) in place
+      double* du = slot(d_u, n, nc);
+      double* dv = slot(d_v, n, nc);
+      if (omega_identity) {
+        double* cw = dalloc<double>(comp, rows);
+        energy_components(ew, cg, s.scheme, 1, ru, rv, nc, nullptr, cf_dev, cw, rows, mw);
+        k_sub<<<blocks(ctx, rows), 256, 0, st()>>>(rows, cw, cold + (n - 2) * rows, cw);
+        k_sub<<<1, 32, 0, st()>>>(1, mw, mo + (n - 1), mw + 1);
+        PTB_LAUNCH_CHECK(ctx);
+        from_energy_components(ew, cg, 1, cw, rows, mw + 1, cf_dev, du, dv, nc);
+      } else {
+        corrected_batch(c, false, 1, ru, rv, nullptr, nullptr, zwp, mw);
+        assemble_d(c, zwp, zo + (n - 1) * size_t(c.rank), mw, mo + (n - 1), du, dv);
+      }
+      // NaN when w, coarse_next[n] or fine_next[n] is non-finite (parareal.cpp:323-326)
+      nan_where(nc, 1, wfl + n, fl(cf) + (n - 1), fl(ff) + (n - 1), du, dv);
+      // R(next[n]) = R(fine_next[n]) + R(I(d_n))
+      if (n < N) {
+        interpolate_at_coarse_nodes(tr, 1, du, static_cast<double*>(ri_u.ptr));
+        interpolate_at_coarse_nodes(tr, 1, dv, static_cast<double*>(ri_v.ptr));
+        k_add<<<blocks(ctx, nc), 256, 0, st()>>>(nc, slot(rf_u, n, nc), static_cast<double*>(ri_u.ptr), ru);
+        k_add<<<blocks(ctx, nc), 256, 0, st()>>>(nc, slot(rf_v, n, nc), static_cast<double*>(ri_v.ptr), rv);
+        PTB_LAUNCH_CHECK(ctx);
+      }
+    }
+  }
+
+  // corrected-coarse-only sweep (parareal.cpp:332-338): d[n] = corrected(C R next[n-1])
+  void corrected_only_sweep(const DevCorrector& c, bool omega_identity) {
+    int32_t* wfl = fl(wf);
+    PTB_CUDA_CHECK(cudaMemsetAsync(wfl, 0, (N + 1) * sizeof(int32_t), st()));
+    if (!omega_identity) precompute_Z(c);
+    double* zwp = dalloc<double>(zw, std::max(c.rank, 1));
+    double* mw = dalloc<double>(mean, std::max<size_t>(N, 1));
+    double* ru = static_cast<double*>(rn_u.ptr);
+    double* rv = static_cast<double*>(rn_v.ptr);
+    restrict_init(ru, rv);
+    for (size_t n = 1; n <= N; ++n) {
+      coarse_propagate(ru, rv, 1, wfl + n);
+      double* du = slot(d_u, n, nc);
+      double* dv = slot(d_v, n, nc);
+      if (omega_identity) {
+        corrected_batch(c, true, 1, ru, rv, du, dv, nullptr, mw);
+      } else {
+        corrected_batch(c, false, 1, ru, rv, nullptr, nullptr, zwp, mw);
+        assemble_d(c, zwp, nullptr, mw, nullptr, du, dv);
+      }
+      nan_where(nc, 1, wfl + n, nullptr, nullptr, du, dv);
+      interpolate_at_coarse_nodes(tr, 1, du, ru);
+      interpolate_at_coarse_nodes(tr, 1, dv, rv);
+    }
+  }
+
+  // plain sweep (parareal.cpp:222-231): w[n] = C(R next[n-1]); R next[n] = (RI w + RF) - RI K
+  void plain_sweep() {
+    int32_t* wfl = fl(wf);
+    PTB_CUDA_CHECK(cudaMemsetAsync(wfl, 0, (N + 1) * sizeof(int32_t), st()));
+    interpolate_at_coarse_nodes(tr, N, slot(kn_u, 1, nc), slot(rik_u, 1, nc));
+    interpolate_at_coarse_nodes(tr, N, slot(kn_v, 1, nc), slot(rik_v, 1, nc));
+    double* ru = static_cast<double*>(rn_u.ptr);
+    double* rv = static_cast<double*>(rn_v.ptr);
+    restrict_init(ru, rv);
+    for (size_t n = 1; n <= N; ++n) {
+      double* wu = slot(w_u, n, nc);
+      double* wv = slot(w_v, n, nc);
+      copy(wu, ru, nc);
+      copy(wv, rv, nc);
+      coarse_propagate(wu, wv, 1, wfl + n);
+      if (n < N) {
+        interpolate_at_coarse_nodes(tr, 1, wu, static_cast<double*>(ri_u.ptr));
+        interpolate_at_coarse_nodes(tr, 1, wv, static_cast<double*>(ri_v.ptr));
+        k_add_sub<<<blocks(ctx, nc), 256, 0, st()>>>(nc, static_cast<double*>(ri_u.ptr), slot(rf_u, n, nc),
+                                                       slot(rik_u, n, nc), ru);
+        k_add_sub<<<blocks(ctx, nc), 256, 0, st()>>>(nc, static_cast<double*>(ri_v.ptr), slot(rf_v, n, nc),
+                                                       slot(rik_v, n, nc), rv);
+        PTB_LAUNCH_CHECK(ctx);
+      }
+    }
+  }
+
+  // serial_coarse_init (parareal.cpp:147-159): cur[n] = I(C R cur[n-1]) via the coarse chain
+  void serial_coarse_init() {
+    int32_t* wfl = fl(wf);
+    PTB_CUDA_CHECK(cudaMemsetAsync(wfl, 0, (N + 1) * sizeof(int32_t), st()));
+    double* ru = static_cast<double*>(rn_u.ptr);
+    double* rv = static_cast<double*>(rn_v.ptr);
+    restrict_init(ru, rv);
+    for (size_t n = 1; n <= N; ++n) {
+      double* wu = slot(w_u, n, nc);
+      double* wv = slot(w_v, n, nc);
+      copy(wu, ru, nc);
+      copy(wv, rv, nc);
+      coarse_propagate(wu, wv, 1, wfl + n);
+      if (n < N) {
+        interpolate_at_coarse_nodes(tr, 1, wu, ru);
+        interpolate_at_coarse_nodes(tr, 1, wv, rv);
+      }
+    }
+    if (a == 1) {
+      copy(CU(0), fl_init_u(), nf);
+      copy(CV(0), fl_init_v(), nf);
+    }
+    if (L) {
+      interpolate_fields(tr, L, slot(w_u, a, nc), CU(a));
+      interpolate_fields(tr, L, slot(w_v, a, nc), CV(a));
+      nan_where(nf, L, wfl + a, nullptr, nullptr, CU(a), CV(a));
+    }
+  }
+
+  // fine combine on own slices -> nxt
+  void fine_combine(bool theta, bool additive) {
+    if (a == 1) {
+      copy(NU(0), fl_init_u(), nf);
+      copy(NV(0), fl_init_v(), nf);
+    }
+    if (!L) return;
+    double* iu = dalloc<double>(fine_u, L * nf);
+    double* iv = dalloc<double>(fine_v, L * nf);
+    if (theta) {
+      interpolate_fields(tr, L, slot(d_u, a, nc), iu);
+      interpolate_fields(tr, L, slot(d_v, a, nc), iv);
+      if (additive) {
+        k_add<<<blocks(ctx, L * nf), 256, 0, st()>>>(L * nf, FU(a), iu, NU(a));
+        k_add<<<blocks(ctx, L * nf), 256, 0, st()>>>(L * nf, FV(a), iv, NV(a));
+        PTB_LAUNCH_CHECK(ctx);
+        if (a == 1) {  // next[1] = fine_next[1] exactly
+          copy(NU(1), FU(1), nf);
+          copy(NV(1), FV(1), nf);
+        }
+        nan_where(nf, L, fl(wf) + a, fl(cf) + (a - 1), fl(ff) + (a - 1), NU(a), NV(a));
+        if (a == 1) {  // n = 1 carries fine_next[1] as is, whatever its finiteness
+          copy(NU(1), FU(1), nf);
+          copy(NV(1), FV(1), nf);
+        }
+      } else {
+        copy(NU(a), iu, L * nf);
+        copy(NV(a), iv, L * nf);
+        nan_where(nf, L, fl(wf) + a, nullptr, nullptr, NU(a), NV(a));
+      }
+    } else {
+      // (I(w) + fine_next) - I(coarse_next), with NaN states where w / coarse_next diverged
+      double* ku = dalloc<double>(fine2_u, L * nf);
+      double* kv = dalloc<double>(fine2_v, L * nf);
+      interpolate_fields(tr, L, slot(w_u, a, nc), iu);
+      interpolate_fields(tr, L, slot(w_v, a, nc), iv);
+      nan_where(nf, L, fl(wf) + a, nullptr, nullptr, iu, iv);
+      interpolate_fields(tr, L, slot(kn_u, a, nc), ku);
+      interpolate_fields(tr, L, slot(kn_v, a, nc), kv);
+      nan_where(nf, L, fl(cf) + (a - 1), nullptr, nullptr, ku, kv);
+      k_add_sub<<<blocks(ctx, L * nf), 256, 0, st()>>>(L * nf, iu, FU(a), ku, NU(a));
+      k_add_sub<<<blocks(ctx, L * nf), 256, 0, st()>>>(L * nf, iv, FV(a), kv, NV(a));
+      PTB_LAUNCH_CHECK(ctx);
+    }
+  }
+
+  // boundary: state b-1 -> next rank's slot a'-1
+  void exchange_boundary(DeviceBuffer& u_b, DeviceBuffer& v_b) {
+    if (comm->world == 1) return;
+    const bool has_next = comm->rank + 1 < comm->world && b <= N;
+    const bool has_prev = comm->rank > 0 && a <= N;
+    double* u = static_cast<double*>(u_b.ptr);
+    double* v = static_cast<double*>(v_b.ptr);
+    comm->shift_right(u + L * nf, nf * sizeof(double), has_next && L > 0, u, nf * sizeof(double), has_prev, st());
+    comm->shift_right(v + L * nf, nf * sizeof(double), has_next && L > 0, v, nf * sizeof(double), has_prev, st());
   }
 
   void run(const double* u0h, const double* v0h, double* ee, double* l2, double* residual, int* rank, int* diverged,
            double* states, double* reference) {
-    // upload the initial state into nxt[0] as staging
-    PTB_CUDA_CHECK(cudaMemcpyAsync(NU(0), u0h, nf * sizeof(double), cudaMemcpyHostToDevice, st()));
-    PTB_CUDA_CHECK(cudaMemcpyAsync(NV(0), v0h, nf * sizeof(double), cudaMemcpyHostToDevice, st()));
-    // keep a pristine copy of init in the reference slot 0 (serial_reference copies from s_u0)
-    double* init_u = dalloc<double>(tmp_u, nf);
-    double* init_v = dalloc<double>(tmp_v, nf);
-    copy(init_u, NU(0), nf);
-    copy(init_v, NV(0), nf);
-    s_u0 = init_u;
-    s_v0 = init_v;
-    cudaEvent_t ev[6];
+    PTB_CUDA_CHECK(cudaMemcpyAsync(fl_init_u(), u0h, nf * sizeof(double), cudaMemcpyHostToDevice, st()));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(fl_init_v(), v0h, nf * sizeof(double), cudaMemcpyHostToDevice, st()));
+    init_bad = false;
+    for (size_t i = 0; i < nf; ++i)
+      if (!std::isfinite(u0h[i]) || !std::isfinite(v0h[i])) {
+        init_bad = true;
+        break;
+      }
+    cudaEvent_t ev[7];
     for (auto& e : ev) PTB_CUDA_CHECK(cudaEventCreate(&e));
-    auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, a, b);
-      return double(ms);
+    auto ms = [&](cudaEvent_t x, cudaEvent_t y) {
+      float t = 0;
+      cudaEventElapsedTime(&t, x, y);
+      return double(t);
     };
     PTB_CUDA_CHECK(cudaEventRecord(ev[0], st()));
     serial_reference();
     PTB_CUDA_CHECK(cudaEventRecord(ev[1], st()));
     PTB_CUDA_CHECK(cudaEventSynchronize(ev[1]));
-    if (times) times->reference_ms = elapsed(ev[0], ev[1]);
+    if (times) times->reference_ms = ms(ev[0], ev[1]);
+    gather_ref_flags();
     if (reference) {
-      for (size_t n = 0; n <= N; ++n) {
-        PTB_CUDA_CHECK(cudaMemcpyAsync(reference + 2 * n * nf, RU(n), nf * sizeof(double), cudaMemcpyDeviceToHost, st()));
+      for (size_t m = (a == 1 ? 0 : a); m < b; ++m) {
+        PTB_CUDA_CHECK(cudaMemcpyAsync(reference + 2 * m * nf, RU(m), nf * sizeof(double), cudaMemcpyDeviceToHost, st()));
         PTB_CUDA_CHECK(
-            cudaMemcpyAsync(reference + (2 * n + 1) * nf, RV(n), nf * sizeof(double), cudaMemcpyDeviceToHost, st()));
+            cudaMemcpyAsync(reference + (2 * m + 1) * nf, RV(m), nf * sizeof(double), cudaMemcpyDeviceToHost, st()));
       }
+      PTB_CUDA_CHECK(cudaStreamSynchronize(st()));
     }
     serial_coarse_init();
     residual[0] = kNaN;
     rank[0] = 0;
-    finalize(CU(0), CV(0), nullptr, nullptr, ee, l2, diverged, states);
+    finalize(cur_u, cur_v, nullptr, nullptr, ee, l2, diverged, states);
+    exchange_boundary(cur_u, cur_v);
 
-    const bool theta = s.variant != 0;
-    const bool omega_identity = s.variant == 3;
-    const bool additive = s.variant != 2;
-    const int d = cg.dim;
-    const size_t rows = size_t(d + 1) * nc;
+    const bool theta = s.variant != PTB_PLAIN;
+    const bool omega_identity = s.variant == PTB_OMEGA_IDENTITY;
+    const bool additive = s.variant != PTB_CORRECTED_COARSE_ONLY;
+    const size_t rows = size_t(cg.dim + 1) * nc;
     double* Fp = dalloc<double>(Fm, rows * N);
     double* Gp = dalloc<double>(Gm, rows * N);
     int* idx_d = dalloc<int>(idx, N);
-    DevCorrector applied_drop;
+    DevCorrector dropped;
     for (int k = 1; k <= K; ++k) {
       PTB_CUDA_CHECK(cudaEventRecord(ev[0], st()));
       parallel_stage();
       PTB_CUDA_CHECK(cudaEventRecord(ev[1], st()));
+      gather_payload();
+      PTB_CUDA_CHECK(cudaEventRecord(ev[2], st()));
       double res = kNaN;
       int rk = 0;
       const DevCorrector* applied = &corr;
-      std::vector<int32_t> ffl(N), cfl(N);
-      PTB_CUDA_CHECK(cudaMemcpyAsync(ffl.data(), fl(flags_f), N * sizeof(int32_t), cudaMemcpyDeviceToHost, st()));
-      PTB_CUDA_CHECK(cudaMemcpyAsync(cfl.data(), fl(flags_c), N * sizeof(int32_t), cudaMemcpyDeviceToHost, st()));
-      PTB_CUDA_CHECK(cudaStreamSynchronize(st()));
       if (theta) {
+        const std::vector<int32_t> ffh = to_host(fl(ff), N), cfh = to_host(fl(cf), N);
         std::vector<int> keep;
         for (size_t n = 1; n <= N; ++n)
-          if (!ffl[n - 1] && !cfl[n - 1]) keep.push_back(int(n - 1));
+          if (!ffh[n - 1] && !cfh[n - 1]) keep.push_back(int(n - 1));
         if (!keep.empty()) {
           const int cols = int(keep.size());
           PTB_CUDA_CHECK(cudaMemcpyAsync(idx_d, keep.data(), keep.size() * sizeof(int), cudaMemcpyHostToDevice, st()));
-          // assemble_snapshots (procrustes.cpp:158-175): F = Lambda(R fine_next), G = Lambda(coarse_next)
-          double* ru = dalloc<double>(cof_u, N * nc);
-          double* rv = dalloc<double>(cof_v, N * nc);
-          restrict_fields(tr, N, FU(1), ru);
-          restrict_fields(tr, N, FV(1), rv);
-          energy_components(ew, cg, s.scheme, size_t(cols), ru, rv, nc, idx_d, ptb_propagator_speed(pc), Fp, rows,
-                            nullptr);
-          energy_components(ew, cg, s.scheme, size_t(cols), KU(1), KV(1), nc, idx_d, ptb_propagator_speed(pc), Gp,
-                            rows, nullptr);
+          // assemble_snapshots (procrustes.cpp:158-175) from the gathered coarse payload
+          energy_components(ew, cg, s.scheme, size_t(cols), slot(rf_u, 1, nc), slot(rf_v, 1, nc), nc, idx_d, cf_dev,
+                            Fp, rows, nullptr);
+          energy_components(ew, cg, s.scheme, size_t(cols), slot(kn_u, 1, nc), slot(kn_v, 1, nc), nc, idx_d, cf_dev,
+                            Gp, rows, nullptr);
           if (omega_identity) {
-            const double fn2 = std::sqrt(frob2(Fp, rows * cols));
-            if (fn2 > 0.0) {
-              double* D = dalloc<double>(comp2, rows * cols);
-              k_sub<<<blocks(ctx, rows * cols), 256, 0, st()>>>(rows * cols, Fp, Gp, D);
-              PTB_LAUNCH_CHECK(ctx);
-              res = std::sqrt(frob2(D, rows * cols)) / fn2;
-            } else {
-              res = 0.0;
-            }
+            std::vector<double> nrm(2);
+            double* d2 = dalloc<double>(tmpc, 2);
+            column_sumsq(ctx, int(rows * cols), 1, Fp, rows * cols, d2);
+            double* D = dalloc<double>(comp_old, rows * cols);
+            k_sub<<<blocks(ctx, rows * cols), 256, 0, st()>>>(rows * cols, Fp, Gp, D);
+            PTB_LAUNCH_CHECK(ctx);
+            column_sumsq(ctx, int(rows * cols), 1, D, rows * cols, d2 + 1);
+            nrm = to_host(d2, 2);
+            res = nrm[0] > 0.0 ? std::sqrt(nrm[1]) / std::sqrt(nrm[0]) : 0.0;
           } else {
             update_svd(pw, corr, Fp, Gp, int(rows), cols, s.tol);
             if (s.remove_leading > 0) {
-              drop_leading(corr, size_t(s.remove_leading), applied_drop, ctx);
-              applied = &applied_drop;
+              drop_leading(corr, size_t(s.remove_leading), dropped, ctx);
+              applied = &dropped;
             }
             res = relative_residual(pw, *applied, Fp, Gp, int(rows), cols);
             rk = applied->rank;
           }
         } else if (!omega_identity) {
-          drop_leading(corr, size_t(std::max(0, s.remove_leading)), applied_drop, ctx);
-          applied = &applied_drop;
+          drop_leading(corr, size_t(std::max(0, s.remove_leading)), dropped, ctx);
+          applied = &dropped;
           rk = applied->rank;
         }
       }
-      PTB_CUDA_CHECK(cudaEventRecord(ev[2], st()));
-      if (theta)
-        theta_sweep(*applied, additive, omega_identity);
-      else
-        plain_sweep();
       PTB_CUDA_CHECK(cudaEventRecord(ev[3], st()));
+      if (!theta)
+        plain_sweep();
+      else if (additive)
+        theta_sweep(*applied, omega_identity);
+      else
+        corrected_only_sweep(*applied, omega_identity);
+      PTB_CUDA_CHECK(cudaEventRecord(ev[4], st()));
+      fine_combine(theta, additive);
       residual[k] = res;
       rank[k] = rk;
-      finalize(NU(0), NV(0), CU(0), CV(0), ee + size_t(k) * (N + 1), l2 + size_t(k) * (N + 1), diverged + k,
+      finalize(nxt_u, nxt_v, &cur_u, &cur_v, ee + size_t(k) * (N + 1), l2 + size_t(k) * (N + 1), diverged + k,
                states ? states + size_t(k) * (N + 1) * 2 * nf : nullptr);
-      PTB_CUDA_CHECK(cudaEventRecord(ev[4], st()));
-      PTB_CUDA_CHECK(cudaEventSynchronize(ev[4]));
+      exchange_boundary(nxt_u, nxt_v);
+      PTB_CUDA_CHECK(cudaEventRecord(ev[5], st()));
+      PTB_CUDA_CHECK(cudaEventSynchronize(ev[5]));
       if (times && k <= PTB_MAX_TIMED_ITERS) {
-        times->parallel_ms[k - 1] = elapsed(ev[0], ev[1]);
-        times->procrustes_ms[k - 1] = elapsed(ev[1], ev[2]);
-        times->sweep_ms[k - 1] = elapsed(ev[2], ev[3]);
-        times->finalize_ms[k - 1] = elapsed(ev[3], ev[4]);
-        times->iteration_ms[k - 1] = elapsed(ev[0], ev[4]);
+        times->parallel_ms[k - 1] = ms(ev[0], ev[1]);
+        times->gather_ms[k - 1] = ms(ev[1], ev[2]);
+        times->procrustes_ms[k - 1] = ms(ev[2], ev[3]);
+        times->sweep_ms[k - 1] = ms(ev[3], ev[4]);
+        times->finalize_ms[k - 1] = ms(ev[4], ev[5]);
+        times->iteration_ms[k - 1] = ms(ev[0], ev[5]);
       }
       std::swap(cur_u, nxt_u);
       std::swap(cur_v, nxt_v);
     }
     for (auto& e : ev) cudaEventDestroy(e);
   }
-
-  double frob2(const double* p, size_t n) {
-    double* d = dalloc<double>(mean2, 1);
-    column_sumsq(ctx, int(n), 1, p, n, d);
-    double h = 0;
-    PTB_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, st()));
-    PTB_CUDA_CHECK(cudaStreamSynchronize(st()));
-    return h;
-  }
-
-  // corrected_coarse_state (parareal.cpp:245-253) for `batch` coarse states -> (ou, ov)
-  void corrected(const DevCorrector& applied, bool omega_identity, size_t batch, const double* u, const double* v,
-                 double* ou, double* ov) {
-    const size_t rows = size_t(cg.dim + 1) * nc;
-    double* cp = dalloc<double>(comp, rows * batch);
-    double* mp = dalloc<double>(mean, batch);
-    energy_components(ew, cg, s.scheme, batch, u, v, nc, nullptr, ptb_propagator_speed(pc), cp, rows, mp);
-    const double* src = cp;
-    if (!omega_identity) {
-      double* c2 = dalloc<double>(comp2, rows * batch);
-      apply_corrector(pw, applied, batch, cp, rows, c2, rows);
-      src = c2;
-    }
-    from_energy_components(ew, cg, batch, src, rows, mp, ptb_propagator_speed(pc), ou, ov, nc);
-  }
-
-  // theta sweep (parareal.cpp:311-340), writes nxt
-  void theta_sweep(const DevCorrector& applied, bool additive, bool omega_identity) {
-    copy(NU(0), s_u0, nf);
-    copy(NV(0), s_v0, nf);
-    int32_t* wf = fl(flags_w);
-    PTB_CUDA_CHECK(cudaMemsetAsync(wf, 0, (N + 1) * sizeof(int32_t), st()));
-    double* ou = dalloc<double>(cold_u, N * nc);
-    double* ov = dalloc<double>(cold_v, N * nc);
-    if (additive && N >= 2) corrected(applied, omega_identity, N - 1, KU(2), KV(2), ou + nc, ov + nc);
-    double* du = dalloc<double>(cnew_u, nc);
-    double* dv = dalloc<double>(cnew_v, nc);
-    double* iu = dalloc<double>(fine_tmp_u, nf);
-    double* iv = dalloc<double>(fine_tmp_v, nf);
-    for (size_t n = 1; n <= N; ++n) {
-      if (additive && n == 1) {  // the two theta terms cancel exactly at the first coupling
-        copy(NU(1), FU(1), nf);
-        copy(NV(1), FV(1), nf);
-        continue;
-      }
-      coarse_stage(NU(n - 1), NV(n - 1), wcu(), wcv(), wf + n);
-      corrected(applied, omega_identity, 1, wcu(), wcv(), du, dv);
-      if (additive) {
-        const double* cou = ou + (n - 1) * nc;
-        const double* cov = ov + (n - 1) * nc;
-        k_sub<<<blocks(ctx, nc), 256, 0, st()>>>(nc, du, cou, du);
-        k_sub<<<blocks(ctx, nc), 256, 0, st()>>>(nc, dv, cov, dv);
-        PTB_LAUNCH_CHECK(ctx);
-        interpolate_fields(tr, 1, du, iu);
-        interpolate_fields(tr, 1, dv, iv);
-        k_combine_theta<<<blocks(ctx, nf), 256, 0, st()>>>(nf, wf + n, fl(flags_c) + (n - 1), fl(flags_f) + (n - 1),
-                                                            FU(n), FV(n), iu, iv, NU(n), NV(n));
-        PTB_LAUNCH_CHECK(ctx);
-      } else {
-        interpolate_fields(tr, 1, du, NU(n));
-        interpolate_fields(tr, 1, dv, NV(n));
-        k_nan_if<<<blocks(ctx, nf), 256, 0, st()>>>(nf, wf + n, NU(n), NV(n));
-        PTB_LAUNCH_CHECK(ctx);
-      }
-    }
-  }
-
-  // plain sweep (parareal.cpp:222-231), writes nxt
-  void plain_sweep() {
-    copy(NU(0), s_u0, nf);
-    copy(NV(0), s_v0, nf);
-    int32_t* wf = fl(flags_w);
-    PTB_CUDA_CHECK(cudaMemsetAsync(wf, 0, (N + 1) * sizeof(int32_t), st()));
-    // coarse_next on the fine grid: I(C R cur[n-1]) or NaN (parareal.cpp:218-220)
-    double* cfu = dalloc<double>(cof_u, N * nf);
-    double* cfv = dalloc<double>(cof_v, N * nf);
-    interpolate_fields(tr, N, KU(1), cfu);
-    interpolate_fields(tr, N, KV(1), cfv);
-    k_nan_where<<<blocks(ctx, N * nf), 256, 0, st()>>>(nf, N, fl(flags_c), cfu, cfv);
-    PTB_LAUNCH_CHECK(ctx);
-    double* iu = dalloc<double>(fine_tmp_u, nf);
-    double* iv = dalloc<double>(fine_tmp_v, nf);
-    for (size_t n = 1; n <= N; ++n) {
-      coarse_stage(NU(n - 1), NV(n - 1), wcu(), wcv(), wf + n);
-      interpolate_fields(tr, 1, wcu(), iu);
-      interpolate_fields(tr, 1, wcv(), iv);
-      k_combine_plain<<<blocks(ctx, nf), 256, 0, st()>>>(nf, wf + n, iu, iv, FU(n), FV(n), cfu + (n - 1) * nf,
-                                                          cfv + (n - 1) * nf, NU(n), NV(n));
-      PTB_LAUNCH_CHECK(ctx);
-    }
-  }
 };
 
-void run_parareal(ptb_context* ctx, const ptb_run_spec& spec, const double* cf, const double* cc, const double* u0,
-                  const double* v0, double* ee, double* l2, double* residual, int* rank, int* diverged, double* states,
-                  double* reference, ptb_phase_times* times) {
+void run_parareal(ptb_context* ctx, const Comm* comm, const ptb_run_spec& spec, const double* cf, const double* cc,
+                  const double* u0, const double* v0, double* ee, double* l2, double* residual, int* rank,
+                  int* diverged, double* states, double* reference, ptb_phase_times* times) {
   std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
-  Driver d(ctx, spec);
+  Driver d(ctx, comm, spec);
   d.times = times;
   d.setup(cf, cc);
   d.run(u0, v0, ee, l2, residual, rank, diverged, states, reference);

@@ -103,6 +103,7 @@ struct ptb_transfer {
   // Fourier weights per axis: w[a][rem*nc + j] = weight of coarse node q-j..., see transfer.cu
   double* wx = nullptr;
   double* wy = nullptr;
+  ptb::DeviceBuffer nodes_half;  // scratch of interpolate_at_coarse_nodes
 };
 
 namespace ptb {
@@ -140,6 +141,9 @@ void nonfinite(ptb_context* ctx, size_t n, size_t batch, const double* f, int32_
 void transfer_init(ptb_transfer* t);
 void restrict_fields(ptb_transfer* t, size_t batch, const double* fine, double* coarse);
 void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, double* fine);
+// R(I(coarse)): the interpolant's values at the coarse nodes, bitwise equal to restricting
+// the full interpolation (used by the coarse-only sweep)
+void interpolate_at_coarse_nodes(ptb_transfer* t, size_t batch, const double* coarse, double* out);
 
 inline size_t grid_size(const ptb_grid& g) { return g.dim == 1 ? g.n[0] : g.n[0] * g.n[1]; }
 void validate_grid(const ptb_grid& g);

@@ -89,6 +89,27 @@ __global__ void k_interp_linear(TGeom g, size_t batch, const double* __restrict_
   }
 }
 
+// linear I at the coarse nodes (fine index r*j), same arithmetic as k_interp_linear
+__global__ void k_interp_linear_nodes(TGeom g, size_t batch, const double* __restrict__ coarse,
+                                      double* __restrict__ out) {
+  const size_t nc = size_t(g.cy) * g.cx, total = batch * nc;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t b = e / nc;
+    const int p = int(e - b * nc);
+    const int jy = p / g.cx, jx = p - jy * g.cx;
+    const double* C = coarse + b * nc;
+    const int ix = jx * g.rx;
+    const double h0 = lin_at(C + size_t(jy) * g.cx, 1, g.cx, g.rx, ix);
+    double v = h0;
+    if (g.ry > 1) {
+      const double h1 = lin_at(C + size_t((jy + 1) % g.cy) * g.cx, 1, g.cx, g.rx, ix);
+      const double t = 0.0;
+      v = __dadd_rn(__dmul_rn(__dsub_rn(1.0, t), h0), __dmul_rn(t, h1));
+    }
+    out[e] = v;
+  }
+}
+
 // Fourier pass along x: in (rows x n) -> out (rows x n*r), weights W[r][n]
 __global__ void k_fourier_x(int rows, int n, int r, size_t batch, const double* __restrict__ w,
                             const double* __restrict__ in, double* __restrict__ out) {
@@ -124,6 +145,43 @@ __global__ void k_fourier_y(int n, int cols, int r, size_t batch, const double* 
     int idx = q;
     for (int d = 0; d < n; ++d) {
       acc = fma(Wr[d], P[size_t(idx) * cols], acc);
+      idx = idx == 0 ? n - 1 : idx - 1;
+    }
+    out[e] = acc;
+  }
+}
+
+// I(d) evaluated only at the coarse nodes (fine index r*j): the rem = 0 outputs of the
+// x pass, then of the y pass — the same weights and accumulation order as the full passes,
+// so the values equal restricting the full interpolation bitwise.
+__global__ void k_fourier_x_nodes(int rows, int n, size_t batch, const double* __restrict__ w,
+                                  const double* __restrict__ in, double* __restrict__ out) {
+  const size_t total = batch * rows * size_t(n);
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t line = e / n;
+    const int q = int(e - line * n);
+    const double* L = in + line * n;
+    double acc = 0.0;
+    int idx = q;
+    for (int d = 0; d < n; ++d) {
+      acc = fma(w[d], L[idx], acc);
+      idx = idx == 0 ? n - 1 : idx - 1;
+    }
+    out[e] = acc;
+  }
+}
+
+__global__ void k_fourier_y_nodes(int n, int cols, size_t batch, const double* __restrict__ w,
+                                  const double* __restrict__ in, double* __restrict__ out) {
+  const size_t plane = size_t(n) * cols, total = batch * plane;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t b = e / plane, f = e - b * plane;
+    const int q = int(f / cols), x = int(f - size_t(q) * cols);
+    const double* P = in + b * plane + x;
+    double acc = 0.0;
+    int idx = q;
+    for (int d = 0; d < n; ++d) {
+      acc = fma(w[d], P[size_t(idx) * cols], acc);
       idx = idx == 0 ? n - 1 : idx - 1;
     }
     out[e] = acc;
@@ -213,6 +271,29 @@ void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, dou
     PTB_LAUNCH_CHECK(ctx);
   } else if (g.rx == 1) {
     k_copy<<<blocks_for(ctx, batch * nf), 256, 0, ctx->stream>>>(batch * nf, coarse, fine);
+    PTB_LAUNCH_CHECK(ctx);
+  }
+}
+
+void interpolate_at_coarse_nodes(ptb_transfer* t, size_t batch, const double* coarse, double* out) {
+  ptb_context* ctx = t->ctx;
+  const TGeom g = geom(t);
+  const size_t nc = size_t(g.cy) * g.cx;
+  if (batch == 0) return;
+  if (t->kind == PTB_INTERP_LINEAR || (g.rx == 1 && g.ry == 1)) {
+    k_interp_linear_nodes<<<blocks_for(ctx, batch * nc), 256, 0, ctx->stream>>>(g, batch, coarse, out);
+    PTB_LAUNCH_CHECK(ctx);
+    return;
+  }
+  const double* src = coarse;
+  if (g.rx > 1) {
+    double* half = (g.ry > 1) ? static_cast<double*>(t->nodes_half.get(batch * nc * sizeof(double))) : out;
+    k_fourier_x_nodes<<<blocks_for(ctx, batch * nc), 256, 0, ctx->stream>>>(g.cy, g.cx, batch, t->wx, coarse, half);
+    PTB_LAUNCH_CHECK(ctx);
+    src = half;
+  }
+  if (g.ry > 1) {
+    k_fourier_y_nodes<<<blocks_for(ctx, batch * nc), 256, 0, ctx->stream>>>(g.cy, g.cx, batch, t->wy, src, out);
     PTB_LAUNCH_CHECK(ctx);
   }
 }

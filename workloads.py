@@ -1,0 +1,128 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations (bench + tests).
+
+BASELINE.json lists five configs; the reference publishes no data for them (SURVEY.md
+8(c)), so every field here is generated from a fixed seed (20261019 + cfg) with numpy's
+PCG64 and documented in DESIGN.md.  T = 1 where BASELINE.json leaves it open (cfg 2-4).
+
+Each cfgN() returns (spec, c_fine, c_coarse, u0, udot0) where `spec` holds the keyword
+fields of the C ABI's ptb_run_spec (include/paratime_b200.h).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+SEED = 20261019
+
+
+def _mesh(n):
+    y, x = np.meshgrid(np.arange(n) / n, np.arange(n) / n, indexing="ij")
+    return y, x
+
+
+def _spec(nf, nc, N, K, m_f, m_c, tol, variant=1, scheme=0, interp=0, mode=0):
+    dt_com = 1.0 / N
+    return dict(dim=2, fine_n=(nf, nf), fine_h=(1 / nf, 1 / nf), coarse_n=(nc, nc), coarse_h=(1 / nc, 1 / nc),
+                dt_fine=dt_com / m_f, m_fine=m_f, dt_coarse=dt_com / m_c, m_coarse=m_c, T=1.0, dt_com=dt_com,
+                n_couplings=N, interp=interp, iterations=K, variant=variant, scheme=scheme, metric_scheme=scheme,
+                tol=tol, remove_leading=0, mode=mode)
+
+
+def restrict(c, r):
+    return np.ascontiguousarray(c[::r, ::r])
+
+
+def cfg1(tol=1e-8, **kw):
+    """c = 1, 128^2 / 32^2, N = 16, K = 4, u0 = exp(-400 |x - (0.5, 0.5)|^2), udot0 = 0."""
+    nf, nc = 128, 32
+    y, x = _mesh(nf)
+    u0 = np.exp(-400.0 * ((x - 0.5) ** 2 + (y - 0.5) ** 2))
+    c = np.ones((nf, nf))
+    return _spec(nf, nc, 16, 4, 64, 8, tol, **kw), c, restrict(c, 4), u0, np.zeros_like(u0)
+
+
+def cfg2(tol=1e-4, **kw):
+    """c = 1 - 0.25 sin(2 pi x) sin(2 pi y), 256^2 / 64^2, N = 32, K = 6, Gaussian pulse with a
+    seeded centre x0 ~ U[0.3, 0.7]^2."""
+    nf, nc = 256, 64
+    rng = np.random.default_rng(SEED + 2)
+    y0, x0 = rng.uniform(0.3, 0.7, 2)
+    y, x = _mesh(nf)
+    c = 1.0 - 0.25 * np.sin(2 * math.pi * x) * np.sin(2 * math.pi * y)
+    u0 = np.exp(-400.0 * ((x - x0) ** 2 + (y - y0) ** 2))
+    return _spec(nf, nc, 32, 6, 64, 8, tol, **kw), c, restrict(c, 4), u0, np.zeros_like(u0)
+
+
+def layered_faulted(n, rng, layers=12, faults=3, cmin=0.27, cmax=1.0, noise=0.03):
+    """Seeded layered-faulted medium: sorted uniform interface depths, velocities rising with
+    depth in [cmin, cmax], +-3% i.i.d. uniform noise, `faults` dipping faults that offset the
+    layering by 5-20 cells.  Row = depth (axis 0)."""
+    depths = np.sort(rng.uniform(0, 1, layers - 1))
+    vel = np.sort(rng.uniform(cmin, cmax, layers))
+    vel[0], vel[-1] = cmin, cmax
+    ycell = (np.arange(n) + 0.5) / n
+    xcell = (np.arange(n) + 0.5) / n
+    shift = np.zeros((n, n))  # depth shift (in fraction of the box) applied per cell
+    for _ in range(faults):
+        x_top = rng.uniform(0.2, 0.8)
+        dip = rng.uniform(-0.5, 0.5)  # dx per unit depth
+        offset = rng.integers(5, 21) / n
+        yy, xx = np.meshgrid(ycell, xcell, indexing="ij")
+        side = xx > (x_top + dip * yy)  # hanging wall
+        shift += np.where(side, offset, 0.0)
+    yy, _ = np.meshgrid(ycell, xcell, indexing="ij")
+    layer = np.searchsorted(depths, (yy - shift) % 1.0)
+    c = vel[layer]
+    c *= 1.0 + noise * rng.uniform(-1, 1, (n, n))
+    return c
+
+
+def gaussian_smooth_periodic(c, sigma):
+    """Periodic Gaussian smoothing (FFT), sigma in cells."""
+    n = c.shape[0]
+    k = np.fft.fftfreq(n) * 2 * math.pi
+    g = np.exp(-0.5 * (sigma ** 2) * (k[:, None] ** 2 + k[None, :] ** 2))
+    return np.real(np.fft.ifft2(np.fft.fft2(c) * g))
+
+
+def cfg3(tol=1e-4, **kw):
+    """Layered-faulted medium 512^2 / 128^2, N = 64, K = 8; coarse c = Gaussian-smoothed
+    (sigma = m_s/2 = 2 fine cells) then restricted fine c; u0 = exp(-2500 |x - x0|^2) near the top."""
+    nf, nc = 512, 128
+    rng = np.random.default_rng(SEED + 3)
+    c = layered_faulted(nf, rng)
+    cc = restrict(gaussian_smooth_periodic(c, 2.0), 4)
+    y, x = _mesh(nf)
+    x0 = rng.uniform(0.3, 0.7)
+    u0 = np.exp(-2500.0 * ((x - x0) ** 2 + (y - 0.15) ** 2))
+    return _spec(nf, nc, 64, 8, 64, 8, tol, **kw), c, cc, u0, np.zeros_like(u0)
+
+
+def cfg5_medium(n, seed=SEED + 5):
+    """c = 0.75 + 0.25 S/max|S|, S = sum of 8 sinusoids of integer wavenumbers 1..4."""
+    rng = np.random.default_rng(seed)
+    y, x = _mesh(n)
+    s = np.zeros((n, n))
+    for _ in range(8):
+        ky, kx = rng.integers(1, 5, 2)
+        s += rng.uniform(0.2, 1.0) * np.sin(2 * math.pi * (ky * y + kx * x) + rng.uniform(0, 2 * math.pi))
+    return 0.75 + 0.25 * s / np.max(np.abs(s))
+
+
+def cfg5_pulses(n, batch, seed=SEED + 50):
+    """"Random Gaussian initial states": exp(-w |x - x0|^2), x0 ~ U[0,1)^2 (periodic distance),
+    w ~ U[200, 2000], udot0 = 0."""
+    rng = np.random.default_rng(seed)
+    ax = np.arange(n) / n
+    out = np.empty((batch, n, n))
+    for b in range(batch):
+        y0, x0 = rng.random(2)
+        w = rng.uniform(200, 2000)
+        dy = np.minimum(np.abs(ax - y0), 1 - np.abs(ax - y0))[:, None]
+        dx = np.minimum(np.abs(ax - x0), 1 - np.abs(ax - x0))[None, :]
+        out[b] = np.exp(-w * (dy * dy + dx * dx))
+    return out
+
+
+CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3}
