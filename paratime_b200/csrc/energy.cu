@@ -241,16 +241,20 @@ __global__ void k_finish_inverse(size_t total, int n, int d, const double2* uhat
 }
 
 // fused fd energy sums of a state pair: S_diff = |Lambda(a-b)|^2, S_ref = |Lambda(b)|^2,
-// L_diff = sum (ua-ub)^2, L_ref = sum ub^2 (energy_map.cpp:216-249); one CTA per pair
+// L_diff = sum (ua-ub)^2, L_ref = sum ub^2 (energy_map.cpp:216-249).  grid = (PB, pairs):
+// fixed per-block partials, then k_pair_final sums them in block order (deterministic).
+constexpr int PAIR_BLOCKS = 32;
+
 __global__ void __launch_bounds__(256) k_pair_sums(Geo G, Beta B, int n, const double* ua, const double* va,
                                                    size_t sa, const double* ub, const double* vb, size_t sb,
-                                                   const double* c, double* out) {
-  const double* UA = ua + blockIdx.x * sa;
-  const double* VA = va + blockIdx.x * sa;
-  const double* UB = ub + blockIdx.x * sb;
-  const double* VB = vb + blockIdx.x * sb;
+                                                   const double* c, double* part) {
+  const size_t pr = blockIdx.y;
+  const double* UA = ua + pr * sa;
+  const double* VA = va + pr * sa;
+  const double* UB = ub + pr * sb;
+  const double* VB = vb + pr * sb;
   double sd = 0.0, sr = 0.0, ld = 0.0, lr = 0.0;
-  for (int p = threadIdx.x; p < n; p += 256) {
+  for (int p = blockIdx.x * 256 + threadIdx.x; p < n; p += gridDim.x * 256) {
     for (int ax = 0; ax < G.dim; ++ax) {
       const double gd = fd_grad<true>(UA, UB, G, B, ax, p);
       const double gr = fd_grad<false>(UB, nullptr, G, B, ax, p);
@@ -270,10 +274,20 @@ __global__ void __launch_bounds__(256) k_pair_sums(Geo G, Beta B, int n, const d
   ld = block_sum<256>(ld);
   lr = block_sum<256>(lr);
   if (threadIdx.x == 0) {
-    out[blockIdx.x * 4 + 0] = sd;
-    out[blockIdx.x * 4 + 1] = sr;
-    out[blockIdx.x * 4 + 2] = ld;
-    out[blockIdx.x * 4 + 3] = lr;
+    double* o = part + (pr * gridDim.x + blockIdx.x) * 4;
+    o[0] = sd;
+    o[1] = sr;
+    o[2] = ld;
+    o[3] = lr;
+  }
+}
+
+__global__ void k_pair_final(size_t pairs, int nb, const double* part, double* out) {
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < pairs * 4; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t pr = e / 4, q = e % 4;
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) acc += part[(pr * nb + b) * 4 + q];
+    out[e] = acc;
   }
 }
 
@@ -419,7 +433,11 @@ void pair_energy_sums(EnergyWork& w, const ptb_grid& g, int scheme, size_t batch
   const Geo G = geo_of(g);
   const int n = G.ny * G.nx;
   if (scheme != PTB_SPECTRAL) {
-    k_pair_sums<<<unsigned(batch), 256, 0, st>>>(G, beta_of(scheme), n, ua, va, sa, ub, vb, sb, c, out4);
+    const int nb = std::max(1, std::min(PAIR_BLOCKS, (n + 255) / 256));
+    double* part = static_cast<double*>(w.buf[7].get(batch * nb * 4 * sizeof(double)));
+    k_pair_sums<<<dim3(nb, unsigned(batch)), 256, 0, st>>>(G, beta_of(scheme), n, ua, va, sa, ub, vb, sb, c, part);
+    PTB_LAUNCH_CHECK(ctx);
+    k_pair_final<<<nblk(ctx, batch * 4), 256, 0, st>>>(batch, nb, part, out4);
     PTB_LAUNCH_CHECK(ctx);
     return;
   }

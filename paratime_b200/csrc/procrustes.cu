@@ -63,9 +63,16 @@ __device__ double cta_reduce(double x, double* red) {
   return r;
 }
 
+__device__ __forceinline__ double warp_sum(double x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
 // Values written by other CTAs (partial sums, the pivot row) are read with __ldcg: the
 // grid barrier orders the writes but does not invalidate this SM's L1, so a plain load
-// could return a line cached two steps earlier.
+// could return a line cached two steps earlier.  Per column step: one warp per trailing
+// column computes its dot product / update over the CTA's rows and reduces with shuffles,
+// so the only block-wide barriers are the three grid barriers.
 __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sh[];  // red[QR_THREADS] | w[n] | nrm[n]
@@ -73,43 +80,38 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
   double* w = red + QR_THREADS;
   double* nrm = w + a.n;
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = QR_THREADS / 32;
   const int m = a.m, n = a.n;
   const int rows_per = (m + G - 1) / G;
   const int r0 = min(m, g * rows_per), r1 = min(m, r0 + rows_per);
   double* A = a.A;
   auto col = [&](int k) { return A + size_t(k) * m; };
-  // initial column norms (squared), partial per CTA
-  double* part0 = a.part;  // parity 0
-  for (int k = 0; k < n; ++k) {
-    double s = 0.0;
-    for (int i = r0 + tid; i < r1; i += QR_THREADS) s += col(k)[i] * col(k)[i];
-    s = cta_reduce(s, red);
-    if (tid == 0) part0[size_t(g) * (n + 1) + k] = s;
+  for (int k = warp; k < n; k += nwarps) {  // initial squared column norms, per CTA
+    double sacc = 0.0;
+    for (int i = r0 + lane; i < r1; i += 32) sacc += col(k)[i] * col(k)[i];
+    sacc = warp_sum(sacc);
+    if (lane == 0) a.part[size_t(g) * (n + 1) + k] = sacc;
   }
   if (g == 0)
     for (int k = tid; k < n; k += QR_THREADS) a.perm[k] = k;
   int keep = 0;
-  bool stopped = false;
   for (int j = 0; j < n && j < m; ++j) {
     double* part = a.part + size_t(j & 1) * G * (n + 1);
     double* partn = a.part + size_t((j + 1) & 1) * G * (n + 1);
     grid.sync();
-    // remaining squared norms of columns k >= j (rows >= j), fixed-order reduction
     for (int k = j + tid; k < n; k += QR_THREADS) {
-      double s = 0.0;
-      for (int c = 0; c < G; ++c) s += __ldcg(&part[size_t(c) * (n + 1) + k]);
-      nrm[k] = s;
+      double sacc = 0.0;
+      for (int c = 0; c < G; ++c) sacc += __ldcg(&part[size_t(c) * (n + 1) + k]);
+      nrm[k] = sacc;
     }
     __syncthreads();
-    // pivot: max remaining norm, first index on ties (idamax)
-    int p = j;
+    int p = j;  // max remaining norm, first index on ties (idamax)
     double best = nrm[j];
     for (int k = j + 1; k < n; ++k)
       if (nrm[k] > best) {
         best = nrm[k];
         p = k;
       }
-    // swap columns j and p (own rows), and the permutation
     if (p != j) {
       for (int i = r0 + tid; i < r1; i += QR_THREADS) {
         const double t = col(j)[i];
@@ -122,9 +124,8 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
         a.perm[p] = t;
       }
     }
-    // reflector for column j rows j..m-1 (dlarfg): alpha = A[j][j], xnorm^2 = nrm - alpha^2
-    // is cancellation-prone, so the below-diagonal norm comes from its own partial.
     __syncthreads();
+    // below-diagonal norm of the pivot column (dlarfg's xnorm) from its own partial
     double xs = 0.0;
     for (int i = max(r0, j + 1) + tid; i < r1; i += QR_THREADS) xs += col(j)[i] * col(j)[i];
     xs = cta_reduce(xs, red);
@@ -144,8 +145,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    if (fabs(beta) <= a.drop_tol) {  // first pivot at or below the guard: stop (keep = j)
-      stopped = true;
+    if (fabs(beta) <= a.drop_tol) {  // first pivot at or below the guard: keep = j
       if (g == 0 && tid == 0) a.beta_out[j] = fabs(beta);
       break;
     }
@@ -154,39 +154,36 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
       a.tau[j] = tau;
       a.beta_out[j] = fabs(beta);
     }
-    // v (stored below the diagonal) and R_jj
     for (int i = max(r0, j + 1) + tid; i < r1; i += QR_THREADS) col(j)[i] *= scal;
-    __syncthreads();  // the partials below read rows scaled by neighbouring threads
-    // w_k = A[j][k] + sum_{i>j} v_i A[i][k], k > j  (own-row partials)
-    for (int k = j + 1; k < n; ++k) {
-      double s = 0.0;
-      for (int i = max(r0, j) + tid; i < r1; i += QR_THREADS) s += (i == j ? 1.0 : col(j)[i]) * col(k)[i];
-      s = cta_reduce(s, red);
-      if (tid == 0) part[size_t(g) * (n + 1) + k] = s;
+    __syncthreads();  // the dot products below read rows scaled by other threads
+    const double* v = col(j);
+    for (int k = j + 1 + warp; k < n; k += nwarps) {  // w_k = v^T A[j:, k], own rows
+      double sacc = 0.0;
+      for (int i = max(r0, j) + lane; i < r1; i += 32) sacc += (i == j ? 1.0 : v[i]) * col(k)[i];
+      sacc = warp_sum(sacc);
+      if (lane == 0) part[size_t(g) * (n + 1) + k] = sacc;
     }
     grid.sync();
     for (int k = j + 1 + tid; k < n; k += QR_THREADS) {
-      double s = 0.0;
-      for (int c = 0; c < G; ++c) s += __ldcg(&part[size_t(c) * (n + 1) + k]);
-      w[k] = s;
+      double sacc = 0.0;
+      for (int c = 0; c < G; ++c) sacc += __ldcg(&part[size_t(c) * (n + 1) + k]);
+      w[k] = sacc;
+    }
+    __syncthreads();
+    for (int k = j + 1 + warp; k < n; k += nwarps) {  // A[:, k] -= tau v w_k; fused next norms
+      const double tw = tau * w[k];
+      double sacc = 0.0;
+      for (int i = max(r0, j) + lane; i < r1; i += 32) {
+        const double x = col(k)[i] - tw * (i == j ? 1.0 : v[i]);
+        col(k)[i] = x;
+        if (i > j) sacc += x * x;
+      }
+      sacc = warp_sum(sacc);
+      if (lane == 0) partn[size_t(g) * (n + 1) + k] = sacc;
     }
     __syncthreads();
     if (j >= r0 && j < r1 && tid == 0) col(j)[j] = beta;
-    // update A[i][k] -= tau v_i w_k (i >= j), and fuse the remaining norms (rows >= j+1)
-    for (int k = j + 1; k < n; ++k) {
-      const double tw = tau * w[k];
-      double s = 0.0;
-      for (int i = max(r0, j) + tid; i < r1; i += QR_THREADS) {
-        const double v = (i == j) ? 1.0 : col(j)[i];
-        const double x = col(k)[i] - tw * v;
-        col(k)[i] = x;
-        if (i > j) s += x * x;
-      }
-      s = cta_reduce(s, red);
-      if (tid == 0) partn[size_t(g) * (n + 1) + k] = s;
-    }
   }
-  (void)stopped;
   if (g == 0 && tid == 0) *a.keep_out = keep;
 }
 
@@ -201,9 +198,9 @@ struct FormQArgs {
 __global__ void __launch_bounds__(QR_THREADS) k_qr_formq(FormQArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sh[];
-  double* red = sh;
-  double* w = red + QR_THREADS;
+  double* w = sh;
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = QR_THREADS / 32;
   const int m = a.m, K = a.keep;
   const int rows_per = (m + G - 1) / G;
   const int r0 = min(m, g * rows_per), r1 = min(m, r0 + rows_per);
@@ -212,24 +209,25 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_formq(FormQArgs a) {
   for (int j = K - 1; j >= 0; --j) {
     const double* v = a.A + size_t(j) * m;
     double* part = a.part + size_t(j & 1) * G * K;
-    for (int c = j; c < K; ++c) {
-      double s = 0.0;
-      for (int i = max(r0, j) + tid; i < r1; i += QR_THREADS) s += (i == j ? 1.0 : v[i]) * a.Q[size_t(c) * m + i];
-      s = cta_reduce(s, red);
-      if (tid == 0) part[size_t(g) * K + c] = s;
+    for (int c = j + warp; c < K; c += nwarps) {
+      double sacc = 0.0;
+      for (int i = max(r0, j) + lane; i < r1; i += 32) sacc += (i == j ? 1.0 : v[i]) * a.Q[size_t(c) * m + i];
+      sacc = warp_sum(sacc);
+      if (lane == 0) part[size_t(g) * K + c] = sacc;
     }
     grid.sync();
     for (int c = j + tid; c < K; c += QR_THREADS) {
-      double s = 0.0;
-      for (int q = 0; q < G; ++q) s += __ldcg(&part[size_t(q) * K + c]);
-      w[c] = s;
+      double sacc = 0.0;
+      for (int q = 0; q < G; ++q) sacc += __ldcg(&part[size_t(q) * K + c]);
+      w[c] = sacc;
     }
     __syncthreads();
     const double tau = a.tau[j];
-    for (int c = j; c < K; ++c) {
+    for (int c = j + warp; c < K; c += nwarps) {
       const double tw = tau * w[c];
-      for (int i = max(r0, j) + tid; i < r1; i += QR_THREADS) a.Q[size_t(c) * m + i] -= tw * (i == j ? 1.0 : v[i]);
+      for (int i = max(r0, j) + lane; i < r1; i += 32) a.Q[size_t(c) * m + i] -= tw * (i == j ? 1.0 : v[i]);
     }
+    __syncthreads();
   }
 }
 
@@ -253,27 +251,43 @@ struct JacobiArgs {
   int max_sweeps;
 };
 
-__device__ __forceinline__ double warp_sum(double x) {
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-
+// SMEM: A (r x c) and V (c x c) are staged in shared memory when they fit.  A pair is
+// rotated when |a_i . a_j| > sqrt(r) eps |a_i||a_j| (relative orthogonality, as dgesvj) and
+// the pair is not negligible against the largest column (|a_i||a_j| > eps^2 max|a_k|^2),
+// which keeps round-off-level columns from spinning forever.
+template <bool SMEM>
 __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
+  extern __shared__ double js[];
   const int r = a.r, c = a.c;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   __shared__ int rotated;
-  // V = I
-  for (int e = threadIdx.x; e < c * c; e += blockDim.x) a.V[e] = (e % (c + 1) == 0) ? 1.0 : 0.0;
+  __shared__ double colmax;
+  double* A = SMEM ? js : a.A;
+  double* V = SMEM ? js + size_t(r) * c : a.V;
+  if (SMEM)
+    for (int e = threadIdx.x; e < r * c; e += blockDim.x) A[e] = a.A[e];
+  for (int e = threadIdx.x; e < c * c; e += blockDim.x) V[e] = (e % (c + 1) == 0) ? 1.0 : 0.0;
   const int cc = (c % 2 == 0) ? c : c + 1;  // tournament size (dummy column when odd)
   const double eps = 2.220446049250313e-16;
   const double tol = eps * sqrt(double(r));
   __syncthreads();
-  for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
-    if (threadIdx.x == 0) rotated = 0;
+  int sweep = 0;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) {
+      rotated = 0;
+      colmax = 0.0;
+    }
     __syncthreads();
+    for (int k = warp; k < c; k += nwarps) {
+      double sacc = 0.0;
+      for (int q = lane; q < r; q += 32) sacc += A[size_t(k) * r + q] * A[size_t(k) * r + q];
+      sacc = warp_sum(sacc);
+      if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&colmax), __double_as_longlong(sacc));
+    }
+    __syncthreads();
+    const double floor2 = eps * eps * colmax;
     for (int round = 0; round < cc - 1; ++round) {
       for (int pr = warp; pr < cc / 2; pr += nwarps) {
-        // round-robin pairing: position 0 fixed, others rotate
         auto pos = [&](int q) { return q == 0 ? 0 : 1 + (q - 1 + round) % (cc - 1); };
         int i = pos(pr), j = pos(cc - 1 - pr);
         if (i > j) {
@@ -281,9 +295,9 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
           i = j;
           j = t;
         }
-        if (j >= c) continue;  // dummy
-        double* ai = a.A + size_t(i) * r;
-        double* aj = a.A + size_t(j) * r;
+        if (j >= c) continue;
+        double* ai = A + size_t(i) * r;
+        double* aj = A + size_t(j) * r;
         double al = 0.0, be = 0.0, ga = 0.0;
         for (int k = lane; k < r; k += 32) {
           const double x = ai[k], y = aj[k];
@@ -294,7 +308,8 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
         al = warp_sum(al);
         be = warp_sum(be);
         ga = warp_sum(ga);
-        if (fabs(ga) > tol * sqrt(al) * sqrt(be) && ga != 0.0) {
+        const double nab = sqrt(al) * sqrt(be);
+        if (ga != 0.0 && fabs(ga) > tol * nab && nab > floor2) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
@@ -303,8 +318,8 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
             ai[k] = cs * x - sn * y;
             aj[k] = sn * x + cs * y;
           }
-          double* vi = a.V + size_t(i) * c;
-          double* vj = a.V + size_t(j) * c;
+          double* vi = V + size_t(i) * c;
+          double* vj = V + size_t(j) * c;
           for (int k = lane; k < c; k += 32) {
             const double x = vi[k], y = vj[k];
             vi[k] = cs * x - sn * y;
@@ -315,19 +330,18 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
       }
       __syncthreads();
     }
-    __syncthreads();
     if (!rotated) break;
     __syncthreads();
   }
-  // singular values and descending order (stable: ties keep the lower index first)
+  double* sv = a.tmp + size_t(r) * c + size_t(c) * c;
   for (int k = warp; k < c; k += nwarps) {
-    double s = 0.0;
-    for (int q = lane; q < r; q += 32) s += a.A[size_t(k) * r + q] * a.A[size_t(k) * r + q];
-    s = warp_sum(s);
-    if (lane == 0) a.tmp[size_t(r) * c + size_t(c) * c + k] = sqrt(s);
+    double sacc = 0.0;
+    for (int q = lane; q < r; q += 32) sacc += A[size_t(k) * r + q] * A[size_t(k) * r + q];
+    sacc = warp_sum(sacc);
+    if (lane == 0) sv[k] = sqrt(sacc);
   }
+  if (threadIdx.x == 0) sv[c] = double(sweep);  // diagnostics: sweeps used
   __syncthreads();
-  const double* sv = a.tmp + size_t(r) * c + size_t(c) * c;
   for (int k = threadIdx.x; k < c; k += blockDim.x) {
     int rank = 0;
     for (int q = 0; q < c; ++q)
@@ -335,20 +349,25 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
     a.order[rank] = k;
   }
   __syncthreads();
-  // sorted copies: U columns normalised (zero column when sigma = 0)
+  const double* SA = A;
+  const double* SV = V;
+  if (!SMEM) {  // in-place permutation needs a staging copy
+    for (int e = threadIdx.x; e < r * c; e += blockDim.x) a.tmp[e] = A[e];
+    for (int e = threadIdx.x; e < c * c; e += blockDim.x) a.tmp[size_t(r) * c + e] = V[e];
+    SA = a.tmp;
+    SV = a.tmp + size_t(r) * c;
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < r * c; e += blockDim.x) {
     const int k = e / r, q = e - k * r;
     const int src = a.order[k];
-    const double s = sv[src];
-    a.tmp[e] = s > 0.0 ? a.A[size_t(src) * r + q] / s : 0.0;
+    const double sg = sv[src];
+    a.A[e] = sg > 0.0 ? SA[size_t(src) * r + q] / sg : 0.0;
   }
   for (int e = threadIdx.x; e < c * c; e += blockDim.x) {
     const int k = e / c, q = e - k * c;
-    a.tmp[size_t(r) * c + e] = a.V[size_t(a.order[k]) * c + q];
+    a.V[e] = SV[size_t(a.order[k]) * c + q];
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < r * c; e += blockDim.x) a.A[e] = a.tmp[e];
-  for (int e = threadIdx.x; e < c * c; e += blockDim.x) a.V[e] = a.tmp[size_t(r) * c + e];
   for (int k = threadIdx.x; k < c; k += blockDim.x) a.sigma[k] = sv[a.order[k]];
 }
 
@@ -412,10 +431,24 @@ __global__ void k_add_diag(double* H, int ld, const double* s, int r) {
     H[size_t(i) * ld + i] += s[i];
 }
 
-__global__ void __launch_bounds__(256) k_sumsq(const double* x, size_t n, double* out) {
+// deterministic two-stage sum of squares: fixed grid, per-block partials, one final block
+__global__ void __launch_bounds__(256) k_sumsq_part(const double* x, size_t n, double* part) {
   __shared__ double red[256];
   double s = 0.0;
-  for (size_t i = threadIdx.x; i < n; i += 256) s += x[i] * x[i];
+  for (size_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += size_t(gridDim.x) * 256) s += x[i] * x[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(256) k_sum_final(const double* part, int np, double* out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += 256) s += part[i];
   red[threadIdx.x] = s;
   __syncthreads();
   for (int k = 128; k > 0; k >>= 1) {
@@ -442,8 +475,11 @@ void check_blas(cublasStatus_t s, const char* what) {
 }
 
 double dev_sumsq(ptb_context* ctx, const double* x, size_t n, DeviceBuffer& scratch) {
-  double* d = static_cast<double*>(scratch.get(sizeof(double)));
-  k_sumsq<<<1, 256, 0, ctx->stream>>>(x, n, d);
+  constexpr int NP = 296;  // fixed partial count (2 x 148 SMs): deterministic for a given n
+  double* d = static_cast<double*>(scratch.get((NP + 1) * sizeof(double)));
+  k_sumsq_part<<<NP, 256, 0, ctx->stream>>>(x, n, d + 1);
+  PTB_LAUNCH_CHECK(ctx);
+  k_sum_final<<<1, 256, 0, ctx->stream>>>(d + 1, NP, d);
   PTB_LAUNCH_CHECK(ctx);
   double h = 0.0;
   PTB_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -527,7 +563,7 @@ int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol,
   double* Q = static_cast<double*>(Qb.get(std::max<size_t>(1, size_t(m) * keep) * sizeof(double)));
   double* R = static_cast<double*>(Rb.get(std::max<size_t>(1, size_t(keep) * n) * sizeof(double)));
   if (keep > 0) {
-    const size_t smem2 = (QR_THREADS + size_t(keep)) * sizeof(double);
+    const size_t smem2 = std::max<size_t>(1, size_t(keep)) * sizeof(double);
     const int G2 = qr_grid(ctx, m, smem2, reinterpret_cast<const void*>(k_qr_formq));
     double* part2 = static_cast<double*>(w.buf[4].get(std::max(size_t(2) * G * (n + 1), size_t(2) * G2 * keep) *
                                                         sizeof(double)));
@@ -566,9 +602,15 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
   double* V = static_cast<double*>(w.buf[7].get(size_t(c) * c * sizeof(double)));
   double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
   int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
-  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c) * sizeof(double)));
-  JacobiArgs ja{A, V, r, c, sg, order, tmp, 60};
-  k_jacobi<<<1, 1024, 0, st>>>(ja);
+  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 1) * sizeof(double)));
+  JacobiArgs ja{A, V, r, c, sg, order, tmp, 40};
+  const size_t smem = (size_t(r) * c + size_t(c) * c) * sizeof(double);
+  if (smem <= 200 * 1024) {
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_jacobi<true><<<1, 1024, smem, st>>>(ja);
+  } else {
+    k_jacobi<false><<<1, 1024, 0, st>>>(ja);
+  }
   PTB_LAUNCH_CHECK(ctx);
   PTB_CUDA_CHECK(cudaMemcpyAsync(sigma.data(), sg, size_t(c) * sizeof(double), cudaMemcpyDeviceToHost, st));
   // M = A_sorted diag(s) V^T  (A is r x c = U when !trans; when trans, M^T = A S V^T -> M = V S A^T)
