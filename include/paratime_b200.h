@@ -223,6 +223,12 @@ ptb_status ptb_parareal_run(ptb_context* ctx, const ptb_run_spec* spec, const do
 ptb_status ptb_nccl_unique_id(char* out128);
 ptb_status ptb_comm_create(ptb_context* ctx, int rank, int world, const char* id128, ptb_comm** out);
 ptb_status ptb_comm_destroy(ptb_comm* c);
+/* in-process ranks (one host thread per rank, contexts on the same or peer GPUs): the
+ * collectives rendezvous on the host and copy with cudaMemcpy — for tests and single-node
+ * debugging of the sharded driver */
+ptb_status ptb_loopback_group_create(int world, void** out);
+ptb_status ptb_loopback_group_destroy(void* group);
+ptb_status ptb_comm_create_loopback(ptb_context* ctx, void* group, int rank, ptb_comm** out);
 
 /* ptb_parareal_run with the N slices block-sharded over the ranks of `comm` (null = one GPU).
  * Every rank passes the same inputs; outputs energy_err/l2_err/residual/rank/diverged are

@@ -382,6 +382,30 @@ class Comm:
             pass
 
 
+class LoopbackGroup:
+    """In-process ranks for the sharded driver (one thread per rank)."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(lib().ptb_loopback_group_create(C.c_int(world), C.byref(h)))
+        self.h, self.world = h, world
+
+    def comm(self, ctx: Context, rank: int) -> "Comm":
+        c = Comm.__new__(Comm)
+        c.rank, c.world = rank, self.world
+        h = C.c_void_p()
+        check(lib().ptb_comm_create_loopback(ctx.h, self.h, C.c_int(rank), C.byref(h)))
+        c.h = h
+        return c
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ptb_loopback_group_destroy(self.h)
+        except Exception:
+            pass
+
+
 def parareal_run(ctx: Context, spec: RunSpec, c_fine, c_coarse, u0, udot0, keep_states=False,
                  keep_reference=False, comm: "Comm" = None):
     """plain / theta / corrected-coarse-only parareal on the device (parareal.cpp); with `comm`

@@ -10,8 +10,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "ptb_comm.h"
 
@@ -63,7 +65,43 @@ void check_nccl(ncclResult_t r, const char* what) {
 
 }  // namespace
 
+// In-process communicator: W host threads, each driving its own context (same or peer
+// GPUs).  A collective synchronises the caller's stream, publishes its send buffer, meets
+// the other ranks at a host barrier, copies what it needs with cudaMemcpy (peer-capable)
+// and meets them again before anyone may reuse a buffer.  No device code waits on
+// another rank, so several ranks can share one GPU safely.
+struct LoopbackGroup {
+  int world;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long generation = 0;
+  std::vector<const void*> sends;
+  explicit LoopbackGroup(int w) : world(w), sends(size_t(w), nullptr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lock(m);
+    const long gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lock, [&] { return generation != gen; });
+    }
+  }
+};
+
 void Comm::allgather(const void* send, void* recv, size_t bytes_per_rank, cudaStream_t st) const {
+  if (loopback) {
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+    loopback->sends[size_t(rank)] = send;
+    loopback->barrier();
+    for (int r = 0; r < world; ++r)
+      PTB_CUDA_CHECK(cudaMemcpy(static_cast<char*>(recv) + size_t(r) * bytes_per_rank, loopback->sends[size_t(r)],
+                                bytes_per_rank, cudaMemcpyDefault));
+    loopback->barrier();
+    return;
+  }
   if (world == 1) {
     if (send != recv)
       PTB_CUDA_CHECK(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, st));
@@ -76,6 +114,16 @@ void Comm::allgather(const void* send, void* recv, size_t bytes_per_rank, cudaSt
 void Comm::shift_right(const void* send, size_t send_bytes, bool do_send, void* recv, size_t recv_bytes,
                        bool do_recv, cudaStream_t st) const {
   if (world == 1) return;
+  if (loopback) {
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+    loopback->sends[size_t(rank)] = send;
+    loopback->barrier();
+    if (do_recv) PTB_CUDA_CHECK(cudaMemcpy(recv, loopback->sends[size_t(rank - 1)], recv_bytes, cudaMemcpyDefault));
+    loopback->barrier();
+    (void)send_bytes;
+    (void)do_send;
+    return;
+  }
   auto& a = nccl();
   check_nccl(a.groupStart(), "ncclGroupStart");
   if (do_send) check_nccl(a.send(send, send_bytes, ncclChar, rank + 1, static_cast<ncclComm_t>(handle), st), "ncclSend");
@@ -118,6 +166,30 @@ ptb_status ptb_comm_create(ptb_context* ctx, int rank, int world, const char* id
       check_nccl(nccl().commInitRank(&comm, world, id, rank), "ncclCommInitRank");
       c->c.handle = comm;
     }
+    *out = c;
+  });
+}
+
+ptb_status ptb_loopback_group_create(int world, void** out) {
+  return guarded([&] {
+    require(world >= 1 && out, "loopback: bad arguments");
+    *out = new LoopbackGroup(world);
+  });
+}
+
+ptb_status ptb_loopback_group_destroy(void* group) {
+  return guarded([&] { delete static_cast<LoopbackGroup*>(group); });
+}
+
+ptb_status ptb_comm_create_loopback(ptb_context* ctx, void* group, int rank, ptb_comm** out) {
+  return guarded([&] {
+    require(ctx && group && out, "loopback comm: null argument");
+    auto* g = static_cast<LoopbackGroup*>(group);
+    require(rank >= 0 && rank < g->world, "loopback comm: bad rank");
+    auto* c = new ptb_comm();
+    c->c.rank = rank;
+    c->c.world = g->world;
+    c->c.loopback = g;
     *out = c;
   });
 }

@@ -1,0 +1,110 @@
+"""Test infrastructure: the sharded parareal decomposition restated on the numpy oracle.
+
+Rank r owns slices [a_r, b_r).  Per iteration: fine/coarse stages for own slices, an
+all-gather of the coarse payload (R(fine_next), coarse_next, flags), a replicated coarse
+sweep that tracks R(next[n]) = R(fine_next[n]) + R(I(d_n)) instead of fine states, the
+fine combine next[n] = fine_next[n] + I(d_n) on own slices and the boundary state sent to
+rank r+1 — the algorithm of paratime_b200/csrc/driver.cu.  Used by the gloo CPU test to
+check that the decomposition reproduces the reference's theta_engine (oracle)."""
+from __future__ import annotations
+
+import numpy as np
+import torch.distributed as dist
+
+from oracle import paratime_np as P
+
+
+def partition(N, world, rank):
+    chunk = -(-N // world)
+    a = min(N + 1, 1 + rank * chunk)
+    b = min(N + 1, a + chunk)
+    return a, b
+
+
+def _allgather(obj):
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def theta_sharded(init, sch: P.Schedule, t: P.Transfer, K, scheme, tol):
+    rank, world = dist.get_rank(), dist.get_world_size()
+    N = sch.n
+    a, b = partition(N, world, rank)
+    cc = sch.c_coarse
+    RI = lambda s: (P.restrict_field(P.interpolate_field(s[0], t), t), P.restrict_field(P.interpolate_field(s[1], t), t))
+    R = lambda s: (P.restrict_field(s[0], t), P.restrict_field(s[1], t))
+    # iteration 0: coarse chain, replicated
+    w0 = {}
+    rn = R(init)
+    for n in range(1, N + 1):
+        try:
+            w = P.propagate_coupling(rn[0], rn[1], cc, t.coarse, sch.dt_coarse, sch.m_coarse)
+        except P.PropagationDiverged:
+            w = P._nan_state(t.coarse)
+        w0[n] = w
+        rn = RI(w)
+    cur = {0: init} if a == 1 else {}
+    for n in range(a, b):
+        cur[n] = P._interp_state(w0[n], t) if P.finite(*w0[n]) else P._nan_state(t.fine)
+    # boundary: state a-1 from the previous rank
+    cur = _shift(cur, a, b, init)
+    corrector = P.empty_corrector()
+    history = []
+    for _ in range(K):
+        fine_next, coarse_next = {}, {}
+        for n in range(a, b):
+            fine_next[n] = P.fine_stage(cur[n - 1], sch)
+            coarse_next[n] = P.coarse_stage(cur[n - 1], sch, t)
+        pay = {n: (R(fine_next[n]), coarse_next[n], P.finite(*fine_next[n]), P.finite(*coarse_next[n]))
+               for n in range(a, b)}
+        allpay = {}
+        for d in _allgather(pay):
+            allpay.update(d)
+        keep = [n for n in range(1, N + 1) if allpay[n][2] and allpay[n][3]]
+        if keep:
+            F = np.stack([P.to_energy_components(*allpay[n][0], cc, t.coarse, scheme)[0] for n in keep], 1)
+            G = np.stack([P.to_energy_components(*allpay[n][1], cc, t.coarse, scheme)[0] for n in keep], 1)
+            corrector = P.update_svd(corrector, F, G, tol)
+        applied = corrector
+        d = {1: None}
+        rn = allpay[1][0]
+        for n in range(2, N + 1):
+            try:
+                w = P.propagate_coupling(rn[0], rn[1], cc, t.coarse, sch.dt_coarse, sch.m_coarse)
+            except P.PropagationDiverged:
+                w = P._nan_state(t.coarse)
+            if not P.finite(*w) or not allpay[n][3] or not allpay[n][2]:
+                d[n] = P._nan_state(t.coarse)
+            else:
+                cn = P._corrected_coarse_state(w, applied, cc, t.coarse, scheme, False)
+                co = P._corrected_coarse_state(allpay[n][1], applied, cc, t.coarse, scheme, False)
+                d[n] = (cn[0] - co[0], cn[1] - co[1])
+            ri = RI(d[n])
+            rn = (allpay[n][0][0] + ri[0], allpay[n][0][1] + ri[1])
+        nxt = {0: init} if a == 1 else {}
+        for n in range(a, b):
+            if n == 1:
+                nxt[n] = fine_next[1]
+            else:
+                i = P._interp_state(d[n], t)
+                nxt[n] = (fine_next[n][0] + i[0], fine_next[n][1] + i[1])
+            if not P.finite(*nxt[n]):
+                nxt[n] = cur[n]
+        nxt = _shift(nxt, a, b, init)
+        history.append({n: nxt[n] for n in range(a, b)})
+        cur = nxt
+    return history
+
+
+def _shift(states, a, b, init):
+    """Send state b-1 to rank+1; receive state a-1 from rank-1 (object p2p over gloo)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    objs = _allgather((b - 1, states.get(b - 1)) if b - 1 >= a else (None, None))
+    if a > 1:
+        for m, s in objs:
+            if m == a - 1:
+                states[a - 1] = s
+    else:
+        states[0] = init
+    return states
