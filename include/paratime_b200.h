@@ -151,6 +151,10 @@ ptb_status ptb_corrector_update(ptb_corrector* c, size_t rows, size_t cols, cons
 ptb_status ptb_procrustes_solve(ptb_corrector* c, size_t rows, size_t cols, const double* F_dev, const double* G_dev,
                                 double tol);
 ptb_status ptb_corrector_shape(ptb_corrector* c, size_t* rows, size_t* rank);
+/* load factors from host (X, Y rows x rank column-major, S rank) — the value-type C++ API
+ * keeps PhaseCorrector on the host and uploads it for each device operation */
+ptb_status ptb_corrector_set(ptb_corrector* c, size_t rows, size_t rank, const double* X_host, const double* S_host,
+                             const double* Y_host, double tol);
 /* copy factors to host: X, Y rows x rank column-major, S rank */
 ptb_status ptb_corrector_factors(ptb_corrector* c, double* X_host, double* S_host, double* Y_host);
 /* out = copy with the first `count` triplets dropped (drop_leading) */

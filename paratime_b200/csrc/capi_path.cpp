@@ -127,6 +127,23 @@ ptb_status ptb_procrustes_solve(ptb_corrector* c, size_t rows, size_t cols, cons
   });
 }
 
+ptb_status ptb_corrector_set(ptb_corrector* c, size_t rows, size_t rank, const double* X, const double* S,
+                             const double* Y, double tol) {
+  return guarded([&] {
+    require(c != nullptr, "corrector: null");
+    require(rank == 0 || (X && S && Y), "corrector: null factors");
+    Dev d(c->ctx->device);
+    const size_t n = rows * rank;
+    double* dx = static_cast<double*>(c->c.X.get(std::max<size_t>(1, n) * sizeof(double)));
+    double* dy = static_cast<double*>(c->c.Y.get(std::max<size_t>(1, n) * sizeof(double)));
+    if (n) {
+      PTB_CUDA_CHECK(cudaMemcpy(dx, X, n * sizeof(double), cudaMemcpyHostToDevice));
+      PTB_CUDA_CHECK(cudaMemcpy(dy, Y, n * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    c->c.assign(int(rows), int(rank), std::vector<double>(S, S + rank), tol);
+  });
+}
+
 ptb_status ptb_corrector_shape(ptb_corrector* c, size_t* rows, size_t* rank) {
   return guarded([&] {
     require(c && rows && rank, "corrector: null argument");

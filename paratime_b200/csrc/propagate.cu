@@ -15,9 +15,9 @@
 //           c^2*a1 in step s.
 //   FAST  — the same Verlet step in kick-drift-kick form carrying (u, vh = udot + b),
 //           b = (dt/2) c^2 Lap u:  u' = u + dt vh;  b' = Kx*(cc*u' + ry*(uN+uS) + (uW+uE));
-//           vh' = vh + 2 b'  (final step: udot = vh + b').  Kx = (dt/2) c^2 / hx^2 is
-//           precomputed per point, so one update is 7 DP instructions (5 FMA/MUL/ADD
-//           for b, 1 FMA drift, 1 FMA kick).
+//           udot' = vh + b';  vh' = udot' + b'.  Kx = (dt/2) c^2 / hx^2 is precomputed per
+//           point.  Keeping the two half kicks as separate adds makes a fused coupling
+//           bitwise equal to repeated single steps, as in the reference.
 //
 // Kernel families:
 //   k_small   — one CTA owns a whole slice (N <= 4096: 1D fields, coarse 2D grids);
@@ -59,13 +59,16 @@ __device__ __forceinline__ double lap_exact(double uc, double ul, double ur, dou
   return __dadd_rn(x, __dmul_rn(y, p.ihy2));
 }
 
-// FAST half-kick b = Kx * (cc*uc + ry*(uu+ud) + (ul+ur)).
+// FAST half-kick b = Kx*ry*uu + Kx*(cc*uc + ry*ud + (ul+ur)).  One canonical association is
+// used by every kernel and every time level, so b depends on its inputs only: a fused
+// coupling then equals the same number of single steps bitwise (test_propagator.cpp:135-149),
+// and only the last fma waits on uu (the level below in the wavefront kernel).
 template <bool HASY>
 __device__ __forceinline__ double bfast(double uc, double ul, double ur, double uu, double ud, double kx,
                                         const StepParams& p) {
   const double s1 = ul + ur;
   if (!HASY) return kx * fma(p.cc, uc, s1);
-  return kx * fma(p.cc, uc, fma(p.ry, uu + ud, s1));
+  return fma(kx * p.ry, uu, kx * fma(p.cc, uc, fma(p.ry, ud, s1)));
 }
 
 __device__ __forceinline__ bool finite2(double a, double b) { return isfinite(a) && isfinite(b); }
@@ -168,7 +171,8 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs a) {
           acc[q] = an;
         } else {
           const double b = bfast<HASY>(u[q], dst[nb.l], dst[nb.r], dst[nb.u], dst[nb.d], k[q], p);
-          v[q] = last ? v[q] + b : fma(2.0, b, v[q]);
+          v[q] = v[q] + b;
+          if (!last) v[q] = v[q] + b;
         }
       }
     }
@@ -236,7 +240,8 @@ __global__ void k_stream_kick(const StreamArgs a) {
       a.acc[g] = an;
     } else {
       const double b = bfast<HASY>(U[i], U[nb.l], U[nb.r], U[nb.u], U[nb.d], a.coef[i], a.p);
-      a.v[g] = a.last ? a.v[g] + b : fma(2.0, b, a.v[g]);
+      const double vt = a.v[g] + b;
+      a.v[g] = a.last ? vt : vt + b;
     }
   }
 }
@@ -331,7 +336,7 @@ __device__ __forceinline__ void wave_iter(double* __restrict__ sbase, int sstrid
     } else {
       const double b = fma(kr[t], uu, q[t]);
       if (t < S) {
-        const double vh = fma(2.0, b, vprev);
+        const double vh = (vprev + b) + b;
         up = fma(p.dt, vh, uc);
         cv = vh;
         ck = kt;

@@ -1,0 +1,29 @@
+"""The reference's own doctest suites, run unmodified against the B200 library.
+
+tests/refsuite/Makefile compiles /root/reference/proj/tests/test_{propagator,field_core,
+parareal}.cpp against include/paratime/*.hpp (the drop-in API) and libparatime_b200.so;
+the binaries are built in the development container (where /root/reference exists) and
+ship with the repo snapshot.  Each suite must pass in both propagator modes."""
+import os
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BIN = Path(__file__).resolve().parent / "refsuite" / "_bin"
+SUITES = ["test_field_core", "test_propagator", "test_parareal"]
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_passes_on_b200(suite, mode):
+    exe = BIN / suite
+    if not exe.exists():
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    env = dict(os.environ, PTB_MODE=mode)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600, env=env)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "failed checks: 0" in r.stdout
