@@ -445,6 +445,196 @@ __global__ void __launch_bounds__(512) k_wave(const WaveArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ k_wave2 (FAST, 2 columns/thread)
+//
+// Same wavefront as k_wave, but every thread owns the column PAIR (2j, 2j+1): the x-neighbours
+// inside the pair stay in registers and only the pair's edge values go through shared memory
+// (separate left-edge / right-edge rows, conflict-free 8-byte accesses), halving crossbar
+// traffic per update.  Level-0 inputs stream as 16-byte cp.async pairs, outputs are 16-byte
+// stores.  Requires even nx (pairs never straddle the periodic wrap); the strip halo is the
+// even HXE = S + 2 columns per side.  Arithmetic identical to k_wave/k_small FAST.
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+
+template <int S, int W, int PAR>
+__device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __restrict__ eR,
+                                           const StepParams& p, double (&ulo)[S + 1][2], double (&uce)[S + 1][2],
+                                           double (&vin)[S + 1][2], double (&kin)[S + 1][2], const double2 uu0,
+                                           const double2 v0, const double2 k0, double2& out_u, double2& out_v) {
+  // edge rows: eL/eR + parity*pstride + level*lstride + j (+1 padding)
+  constexpr int lstride = W + 2, pstride = (S + 1) * lstride;
+  const double* __restrict__ rL = eL + PAR * pstride;
+  const double* __restrict__ rR = eR + PAR * pstride;
+  double* __restrict__ wL = eL + (PAR ^ 1) * pstride;
+  double* __restrict__ wR = eR + (PAR ^ 1) * pstride;
+  double nl[S + 1], nr[S + 1];  // left neighbour of col 0, right neighbour of col 1, per level
+#pragma unroll
+  for (int t = 0; t <= S; ++t) {
+    nl[t] = rR[t * lstride - 1];
+    nr[t] = rL[t * lstride + 1];
+  }
+  double up0, up1, cv0, cv1, ck0, ck1;
+  {
+    const double uc0 = uce[0][0], uc1 = uce[0][1];
+    wL[0] = uu0.x;
+    wR[0] = uu0.y;
+    const double vh0 = v0.x + bfast<true>(uc0, nl[0], uc1, uu0.x, ulo[0][0], k0.x, p);
+    const double vh1 = v0.y + bfast<true>(uc1, uc0, nr[0], uu0.y, ulo[0][1], k0.y, p);
+    up0 = fma(p.dt, vh0, uc0);
+    up1 = fma(p.dt, vh1, uc1);
+    cv0 = vh0;
+    cv1 = vh1;
+    ck0 = k0.x;
+    ck1 = k0.y;
+    wL[lstride] = up0;
+    wR[lstride] = up1;
+    ulo[0][0] = uc0;
+    ulo[0][1] = uc1;
+    uce[0][0] = uu0.x;
+    uce[0][1] = uu0.y;
+  }
+  // parts of b independent of the level below: b = fma(K ry, uu, K (cc uc + ry ud + (ul + ur)))
+  double q0[S + 1], q1[S + 1];
+#pragma unroll
+  for (int t = 1; t <= S; ++t) {
+    q0[t] = kin[t][0] * fma(p.cc, uce[t][0], fma(p.ry, ulo[t][0], nl[t] + uce[t][1]));
+    q1[t] = kin[t][1] * fma(p.cc, uce[t][1], fma(p.ry, ulo[t][1], uce[t][0] + nr[t]));
+  }
+#pragma unroll
+  for (int t = 1; t <= S; ++t) {
+    const double vp0 = vin[t][0], vp1 = vin[t][1], k0t = kin[t][0], k1t = kin[t][1];
+    vin[t][0] = cv0;
+    vin[t][1] = cv1;
+    kin[t][0] = ck0;
+    kin[t][1] = ck1;
+    const double uu_0 = up0, uu_1 = up1;
+    const double uc0 = uce[t][0], uc1 = uce[t][1];
+    const double b0 = fma(k0t * p.ry, uu_0, q0[t]);
+    const double b1 = fma(k1t * p.ry, uu_1, q1[t]);
+    if (t < S) {
+      const double vh0 = (vp0 + b0) + b0;
+      const double vh1 = (vp1 + b1) + b1;
+      up0 = fma(p.dt, vh0, uc0);
+      up1 = fma(p.dt, vh1, uc1);
+      cv0 = vh0;
+      cv1 = vh1;
+      ck0 = k0t;
+      ck1 = k1t;
+      wL[(t + 1) * lstride] = up0;
+      wR[(t + 1) * lstride] = up1;
+    } else {
+      out_u = make_double2(uc0, uc1);
+      out_v = make_double2(vp0 + b0, vp1 + b1);
+    }
+    ulo[t][0] = uc0;
+    ulo[t][1] = uc1;
+    uce[t][0] = uu_0;
+    uce[t][1] = uu_1;
+  }
+}
+
+template <int S, int W>
+__global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
+  constexpr int HXE = (S + 3) & ~1;  // even halo >= S + 1 (16-byte aligned pairs)
+  constexpr int NL = S + 1;
+  constexpr int UNROLL = 6, RING = 6;
+  extern __shared__ double sm[];
+  constexpr int T = W;
+  const int j = threadIdx.x;
+  const int nx = a.p.nx, ny = a.p.ny;
+  const int npts = nx * ny;
+  const int x0 = blockIdx.y * a.wu;  // even
+  int gx = (x0 - HXE + 2 * j) % nx;
+  if (gx < 0) gx += nx;
+  const int Y0 = blockIdx.z * a.rb;
+  const int nrows = min(a.rb, ny - Y0);
+  const int ystart = Y0 - S;
+  const int n_iter = ((nrows + 2 * S + UNROLL - 1) / UNROLL) * UNROLL;
+  const int oc = 2 * j - HXE;  // output column offset of col 0 within the strip
+  const bool col_out = oc >= 0 && 2 * j + 1 < 2 * T - HXE && oc < a.wu && x0 + oc < nx;
+  const size_t off = static_cast<size_t>(blockIdx.x) * a.stride;
+  const double* __restrict__ U = a.u_in + off;
+  const double* __restrict__ V = a.v_in + off;
+  double* __restrict__ UO = a.u_out + off;
+  double* __restrict__ VO = a.v_out + off;
+  const double* __restrict__ K = a.coef;
+  const StepParams p = a.p;
+  // shared: edges [2 parity][NL][T+2] for L and R, then ring [RING][3][T] double2
+  constexpr int pstride = NL * (T + 2);
+  double* eL = sm + 1 + j;  // +1: pad so j-1 >= 0
+  double* eR = sm + 2 * pstride + 1 + j;
+  double2* ring = reinterpret_cast<double2*>(sm + 4 * pstride);
+  auto wrap = [&](int y) -> int {
+    int r = y % ny;
+    if (r < 0) r += ny;
+    return r * nx + gx;
+  };
+  double ulo[NL][2], uce[NL][2], vin[NL][2], kin[NL][2];
+#pragma unroll
+  for (int t = 0; t < NL; ++t)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) ulo[t][c] = uce[t][c] = vin[t][c] = kin[t][c] = 0.0;
+  {
+    const double2 lo = *reinterpret_cast<const double2*>(U + wrap(ystart - 1));
+    const double2 ce = *reinterpret_cast<const double2*>(U + wrap(ystart));
+    ulo[0][0] = lo.x;
+    ulo[0][1] = lo.y;
+    uce[0][0] = ce.x;
+    uce[0][1] = ce.y;
+    eL[0] = ce.x;  // parity 0, level 0
+    eR[0] = ce.y;
+  }
+  int ou = wrap(ystart + 1), ov = wrap(ystart), oo = wrap(ystart - S);
+  auto adv = [npts, nx](int& o) {
+    o += nx;
+    if (o >= npts) o -= npts;
+  };
+  auto issue = [&](int slot) {
+    double2* d = ring + (slot * 3) * T + j;
+    cp_async16(d, U + ou);
+    cp_async16(d + T, V + ov);
+    cp_async16(d + 2 * T, K + ov);
+    cp_async_commit();
+    adv(ou);
+    adv(ov);
+  };
+#pragma unroll
+  for (int s0 = 0; s0 < RING - 1; ++s0) issue(s0);
+  __syncthreads();
+  bool ok = true;
+  const int last_out = nrows + 2 * S;
+  for (int i0 = 0; i0 < n_iter; i0 += UNROLL) {
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      const int i = i0 + k;
+      cp_async_wait<RING - 2>();
+      const double2* src = ring + ((k % RING) * 3) * T + j;
+      const double2 uu0 = src[0], v0 = src[T], k0 = src[2 * T];
+      issue((k + RING - 1) % RING);
+      double2 out_u, out_v;
+      if (k & 1)
+        wave2_iter<S, W, 1>(eL, eR, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
+      else
+        wave2_iter<S, W, 0>(eL, eR, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
+      if (col_out && i >= 2 * S && i < last_out) {
+        *reinterpret_cast<double2*>(UO + oo) = out_u;
+        *reinterpret_cast<double2*>(VO + oo) = out_v;
+        ok &= finite2(out_u.x, out_v.x) && finite2(out_u.y, out_v.y);
+      }
+      adv(oo);
+      __syncthreads();
+    }
+  }
+  cp_async_wait<0>();
+  if (a.flags) {
+    const int bad = __syncthreads_or(!ok);
+    if (bad && j == 0) atomicOr(&a.flags[blockIdx.x], 1);
+  }
+}
+
 // ------------------------------------------------------------------ misc kernels
 
 __global__ void k_laplacian(StepParams p, size_t n, size_t total, const double* f, double* out) {
@@ -564,10 +754,111 @@ void launch_wave(ptb_context* ctx, cudaStream_t st, const WavePlan& pl, WaveArgs
   PTB_LAUNCH_CHECK(ctx);
 }
 
+// k_wave2: W threads cover 2W columns; useful width even; occupancy from the runtime.
+size_t wave2_smem(int S, int W) {
+  return (size_t(4) * (S + 1) * (W + 2) + size_t(6) * 3 * 2 * W) * sizeof(double);
+}
+
+// strip widths (threads) k_wave2 is instantiated for; each thread covers 2 columns
+constexpr int kWave2Widths[] = {64, 96, 128, 160, 192, 256};
+
+template <int S, int W>
+const void* wave2_fn() {
+  return reinterpret_cast<const void*>(k_wave2<S, W>);
+}
+template <int S>
+const void* wave2_kernel(int W) {
+  switch (W) {
+    case 64: return wave2_fn<S, 64>();
+    case 96: return wave2_fn<S, 96>();
+    case 128: return wave2_fn<S, 128>();
+    case 160: return wave2_fn<S, 160>();
+    case 192: return wave2_fn<S, 192>();
+    case 256: return wave2_fn<S, 256>();
+  }
+  fail(PTB_UNSUPPORTED, "k_wave2 width");
+}
+
+template <int S>
+WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
+  const int HXE = (S + 3) & ~1;
+  WavePlan best{};
+  double best_cost = 1e300;
+  int forceW = 0;
+  if (const char* e = std::getenv("PTB_WAVE_W"); e && std::atoi(e) > 0) forceW = std::atoi(e);
+  for (int W : kWave2Widths) {
+    if (forceW && W != forceW) continue;
+    const int wu_max = (2 * W - 2 * HXE) & ~1;
+    if (wu_max < 16) continue;
+    int occ = 0;
+    const size_t smem = wave2_smem(S, W);
+    const void* kern = wave2_kernel<S>(W);
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    PTB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W, smem));
+    if (occ < 1) continue;
+    const int strips = (nx + wu_max - 1) / wu_max;
+    const int wu = (((nx + strips - 1) / strips) + 1) & ~1;
+    for (int div = 1;; div *= 2) {
+      const int rb = (ny + div - 1) / div;
+      if (div > 1 && rb < 2 * S) break;
+      const int nrb = (ny + rb - 1) / rb;
+      const size_t ctas = size_t(strips) * nrb * batch;
+      const size_t slots = size_t(ctx->num_sms) * occ;
+      const double rounds = std::ceil(double(ctas) / slots);
+      const double resident = double(std::min(ctas, slots)) / ctx->num_sms * (W / 32.0);  // warps per SM
+      const double lat = resident < 8 ? 8.0 / resident : 1.0;
+      const double cost = rounds * occ * (W / 32.0) * (rb + 2.0 * S) * std::max(1.0, lat * 0.5);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = WavePlan{W, wu, strips, rb, nrb};
+      }
+      if (rb <= 1) break;
+    }
+  }
+  if (best.W == 0) fail(PTB_UNSUPPORTED, "k_wave2: no feasible strip width");
+  if (const char* e = std::getenv("PTB_WAVE_DIV"); e && std::atoi(e) > 0) {
+    const int div = std::atoi(e);
+    best.rb = (ny + div - 1) / div;
+    best.nrb = (ny + best.rb - 1) / best.rb;
+  }
+  return best;
+}
+
+template <int S>
+void launch_wave2(ptb_context* ctx, cudaStream_t st, WaveArgs a, size_t batch) {
+  const WavePlan pl = plan_wave2<S>(ctx, a.p.ny, a.p.nx, batch);
+  const size_t smem = wave2_smem(S, pl.W);
+  a.wu = pl.wu;
+  a.rb = pl.rb;
+  dim3 grid(static_cast<unsigned>(batch), pl.strips, pl.nrb);
+  void* args[] = {&a};
+  PTB_CUDA_CHECK(cudaLaunchKernel(wave2_kernel<S>(pl.W), grid, dim3(pl.W), args, smem, st));
+  PTB_LAUNCH_CHECK(ctx);
+}
+
+bool use_wave2(const StepParams& p) {
+  static const int env = [] {
+    const char* e = std::getenv("PTB_WAVE2");
+    return e ? std::atoi(e) : 1;
+  }();
+  return env != 0 && p.nx % 2 == 0 && p.nx >= 32;
+}
+
 template <bool EXACT>
 void wave_pass(ptb_context* ctx, cudaStream_t st, int S, const StepParams& p, size_t batch, const double* ui,
                const double* vi, double* uo, double* vo, const double* coef, int32_t* flags) {
   WaveArgs a{p, ui, vi, uo, vo, coef, size_t(p.ny) * p.nx, 0, 0, flags};
+  if constexpr (!EXACT) {
+    if (use_wave2(p)) {
+      switch (S) {
+        case 1: launch_wave2<1>(ctx, st, a, batch); return;
+        case 2: launch_wave2<2>(ctx, st, a, batch); return;
+        case 4: launch_wave2<4>(ctx, st, a, batch); return;
+        case 8: launch_wave2<8>(ctx, st, a, batch); return;
+        default: fail(PTB_UNSUPPORTED, "wavefront depth");
+      }
+    }
+  }
   const WavePlan pl = plan_wave(ctx, p.ny, p.nx, S, batch);
   switch (S) {
     case 1: launch_wave<1, EXACT>(ctx, st, pl, a, batch); break;
