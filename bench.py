@@ -261,6 +261,8 @@ def main():
     flops_per_launch = batch * n * n * steps_per_launch * FLOPS_PER_UPDATE
     achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
     hbm_bytes_per_launch = batch * n * n * 40.0  # read u, udot, coef; write u, udot (8 B each)
+    plan = prop.plan(batch, mode)
+    traffic = ncu_traffic(n, batch, args.mode, plan)
 
     e2e = None
     if not args.no_e2e:
@@ -287,9 +289,11 @@ def main():
                        "finite": finite},
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": tflops_peak, "unit": "TFLOP/s",
-                         "frac": achieved / tflops_peak if tflops_peak else None, "traffic": None,
+                         "frac": achieved / tflops_peak if tflops_peak else None,
+                         "traffic": traffic and traffic["dram_bytes_per_launch"],
+                         "traffic_source": traffic and traffic["source"],
                          "peak_source": "measured live: DFMA probe (ptb_probe_fp64_peak)",
-                         "kernel": "k_wave<8,FAST>", "per_launch_ms": per_launch_ms,
+                         "kernel": plan, "per_launch_ms": per_launch_ms,
                          "flops_per_update": FLOPS_PER_UPDATE, "steps_per_launch": steps_per_launch,
                          "hbm_algorithmic_GBps": hbm_bytes_per_launch / (per_launch_ms * 1e-3) / 1e9,
                          "hbm_peak_GBps": peaks.get("hbm_gbs")},
@@ -306,6 +310,18 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def ncu_traffic(n, batch, mode, plan):
+    """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` summary
+    (profiles/k1_ncu.json), used only when it was captured on this exact grid/batch/mode/plan."""
+    try:
+        d = json.loads((ROOT / "profiles" / "k1_ncu.json").read_text())
+    except Exception:
+        return None
+    if (d.get("grid"), d.get("batch"), d.get("mode"), d.get("plan")) != (n, batch, mode, plan):
+        return None
+    return {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "source": d["source"]}
 
 
 def parareal_iteration_times(B, ctx, rank, world, dist, cfgs=ITER_CONFIGS):
@@ -326,7 +342,7 @@ def parareal_iteration_times(B, ctx, rank, world, dist, cfgs=ITER_CONFIGS):
     out = {}
     for cfg in cfgs:
         spec, cf, cc, u0, v0 = W.CONFIGS[cfg]()
-        B.api.parareal_run(ctx, B.api.run_spec(**dict(spec, iterations=1)), cf, cc, u0, v0, comm=comm)  # warm-up
+        B.api.parareal_run(ctx, B.api.run_spec(**spec), cf, cc, u0, v0, comm=comm)  # warm-up (all K: module loads)
         r = B.api.parareal_run(ctx, B.api.run_spec(**spec), cf, cc, u0, v0, comm=comm)
         t = r["times"]
         it = np.array(t["iteration_ms"])

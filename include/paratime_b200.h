@@ -95,6 +95,10 @@ const double* ptb_propagator_speed(ptb_propagator* p);
 ptb_status ptb_propagate_batch(ptb_propagator* p, size_t batch, double* u_dev, double* udot_dev,
                                int32_t* nonfinite_dev, int mode);
 /* same with an explicit step count (used for `step`, propagator.cpp:85-93) */
+/* Describe the launch plan propagate would use for (steps, batch, mode): kernel names, strip
+ * widths and grids, NUL-terminated into buf (truncated to len).  Diagnostics only (new). */
+ptb_status ptb_propagate_plan(ptb_propagator* p, size_t steps, size_t batch, int mode, char* buf, size_t len);
+
 ptb_status ptb_propagate_steps_batch(ptb_propagator* p, size_t steps, size_t batch, double* u_dev,
                                      double* udot_dev, int32_t* nonfinite_dev, int mode);
 /* propagate_coupling on host buffers (one state); PTB_DIVERGED when not finite. */

@@ -174,6 +174,14 @@ class Propagator:
                                                   _ptr(flags), C.c_int(mode)))
         return u, udot
 
+    def plan(self, batch: int, mode: int = FAST, steps: Optional[int] = None) -> str:
+        """Launch plan propagate() would use (kernel names, strip widths, grids)."""
+        buf = C.create_string_buffer(512)
+        nsteps = self.steps if steps is None else steps
+        check(lib().ptb_propagate_plan(self.h, C.c_size_t(nsteps), C.c_size_t(batch), C.c_int(mode), buf,
+                                       C.c_size_t(len(buf))))
+        return buf.value.decode()
+
     def propagate_host(self, u: np.ndarray, udot: np.ndarray, mode: int = FAST):
         """propagate_coupling on host arrays; raises PtbError(DIVERGED) like the reference."""
         u = np.ascontiguousarray(u, dtype=np.float64)

@@ -243,6 +243,18 @@ ptb_status ptb_propagate_steps_batch(ptb_propagator* p, size_t steps, size_t bat
   });
 }
 
+ptb_status ptb_propagate_plan(ptb_propagator* p, size_t steps, size_t batch, int mode, char* buf, size_t len) {
+  return guarded([&] {
+    require(p && buf && len > 0, "propagate_plan: null argument");
+    DeviceGuard g(p->ctx->device);
+    std::lock_guard<std::recursive_mutex> lock(p->ctx->mutex);
+    const std::string d = describe_plan(p, steps, batch, mode);
+    const size_t k = std::min(len - 1, d.size());
+    std::memcpy(buf, d.data(), k);
+    buf[k] = 0;
+  });
+}
+
 ptb_status ptb_propagate_batch(ptb_propagator* p, size_t batch, double* u, double* v, int32_t* flags, int mode) {
   if (!p) return PTB_INVALID_ARGUMENT;
   return ptb_propagate_steps_batch(p, p->steps, batch, u, v, flags, mode);

@@ -958,6 +958,43 @@ void propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double
         : stream_propagate<false, false>(pr, steps, batch, u, v, flags, slot);
 }
 
+std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mode) {
+  const bool exact = mode == PTB_MODE_EXACT;
+  const StepParams& p = pr->prm;
+  const char* m = exact ? "EXACT" : "FAST";
+  if (batch == 0 || steps == 0) return "none";
+  if (pr->n <= 4096) return std::string("k_small<") + m + "> x1 launch, one CTA per slice";
+  if (p.dim != 2) return std::string("k_stream_drift/kick<") + m + "> 2 launches per step";
+  std::string out;
+  size_t rem = steps;
+  int passes = 0;
+  for (int S : {8, 4, 2, 1}) {
+    const size_t k = S == 8 ? rem / 8 : (rem >= size_t(S) ? 1 : 0);
+    if (!k) continue;
+    rem -= k * S;
+    passes += int(k);
+    std::string d;
+    if (!exact && use_wave2(p)) {
+      WavePlan pl;
+      switch (S) {
+        case 8: pl = plan_wave2<8>(pr->ctx, p.ny, p.nx, batch); break;
+        case 4: pl = plan_wave2<4>(pr->ctx, p.ny, p.nx, batch); break;
+        case 2: pl = plan_wave2<2>(pr->ctx, p.ny, p.nx, batch); break;
+        default: pl = plan_wave2<1>(pr->ctx, p.ny, p.nx, batch); break;
+      }
+      d = "k_wave2<" + std::to_string(S) + "," + std::to_string(pl.W) + ">";
+      d += " grid " + std::to_string(batch) + "x" + std::to_string(pl.strips) + "x" + std::to_string(pl.nrb);
+    } else {
+      const WavePlan pl = plan_wave(pr->ctx, p.ny, p.nx, S, batch);
+      d = "k_wave<" + std::to_string(S) + "," + m + "> W " + std::to_string(pl.W);
+      d += " grid " + std::to_string(batch) + "x" + std::to_string(pl.strips) + "x" + std::to_string(pl.nrb);
+    }
+    out += (out.empty() ? "" : " + ") + std::to_string(k) + " x " + d;
+  }
+  if (passes % 2) out += " + k_copy2";
+  return out;
+}
+
 void laplacian(ptb_context* ctx, const ptb_grid& g, size_t batch, const double* f, double* out) {
   StepParams p{};
   p.dim = g.dim;

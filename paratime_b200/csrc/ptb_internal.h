@@ -132,6 +132,8 @@ struct LaunchSlot {
 };
 
 // propagate.cu
+// Human-readable launch plan of propagate() (kernels, strip widths, grids).
+std::string describe_plan(ptb_propagator* p, size_t steps, size_t batch, int mode);
 void propagate(ptb_propagator* p, size_t steps, size_t batch, double* u, double* v, int32_t* flags,
                int mode, const LaunchSlot* slot = nullptr);
 void laplacian(ptb_context* ctx, const ptb_grid& g, size_t batch, const double* f, double* out);
