@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstddef>
+#include <iosfwd>
 #include <span>
 #include <utility>
 #include <vector>
@@ -59,6 +60,10 @@ class PhaseCorrector {
 
   std::vector<double> apply(const std::vector<double>& stacked) const;
   PhaseCorrector drop_leading(Index count) const;
+
+  /// Text checkpoint: "rows r" header then X, S, Y blocks (procrustes.hpp:41-43).
+  void save(std::ostream& os) const;
+  static PhaseCorrector load(std::istream& is);
 
  private:
   Matrix left_;

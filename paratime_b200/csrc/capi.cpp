@@ -376,6 +376,8 @@ ptb_status ptb_transfer_destroy(ptb_transfer* t) {
     DeviceGuard g(t->ctx->device);
     if (t->wx) cudaFree(t->wx);
     if (t->wy) cudaFree(t->wy);
+    if (t->mx) cudaFree(t->mx);
+    if (t->my) cudaFree(t->my);
     t->nodes_half.release();
     delete t;
   });

@@ -11,6 +11,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <functional>
+#include <istream>
+#include <ostream>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -545,6 +547,41 @@ PhaseCorrector PhaseCorrector::drop_leading(Index count) const {
   std::copy(left_.col(first), left_.col(first) + rows() * keep, l.data());
   std::copy(right_.col(first), right_.col(first) + rows() * keep, r.data());
   return PhaseCorrector(std::move(l), std::vector<double>(sv_.begin() + first, sv_.end()), std::move(r), tol_);
+}
+
+// Checkpoint text format of procrustes.cpp:95-127: "rows rank" line, then X row by row, the
+// singular values on one line, Y row by row; 17 significant digits, single-space separated.
+void PhaseCorrector::save(std::ostream& os) const {
+  os << rows() << " " << rank() << "\n";
+  os.precision(17);
+  const auto dump = [&os](const Matrix& m) {
+    for (Index i = 0; i < m.rows(); ++i) {
+      for (Index j = 0; j < m.cols(); ++j) os << (j ? " " : "") << m(i, j);
+      os << "\n";
+    }
+  };
+  dump(left_);
+  for (size_t i = 0; i < sv_.size(); ++i) os << (i ? " " : "") << sv_[i];
+  os << "\n";
+  dump(right_);
+}
+
+PhaseCorrector PhaseCorrector::load(std::istream& is) {
+  Index rows = 0, r = 0;
+  if (!(is >> rows >> r) || rows < 0 || r < 0) throw std::runtime_error("corrector checkpoint: bad header");
+  const auto block = [&is, rows, r]() {
+    Matrix m(rows, r);
+    for (Index i = 0; i < rows; ++i)
+      for (Index j = 0; j < r; ++j)
+        if (!(is >> m(i, j))) throw std::runtime_error("corrector checkpoint: truncated matrix block");
+    return m;
+  };
+  Matrix X = block();
+  std::vector<double> sv(static_cast<size_t>(r));
+  for (Index i = 0; i < r; ++i)
+    if (!(is >> sv[size_t(i)])) throw std::runtime_error("corrector checkpoint: truncated values");
+  Matrix Y = block();
+  return PhaseCorrector(std::move(X), std::move(sv), std::move(Y), 0.0);
 }
 
 std::vector<double> stack_components(const EnergyComponents& comp) {

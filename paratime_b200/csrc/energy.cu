@@ -282,6 +282,85 @@ __global__ void __launch_bounds__(256) k_pair_sums(Geo G, Beta B, int n, const d
   }
 }
 
+// 2D variant: block rows r = blockIdx.x (+ k * gridDim.x), threads along x; periodic neighbour
+// offsets resolved once per row instead of integer div/mod per access.  Per-point arithmetic is
+// that of fd_grad / k_pair_sums (same rounding), only the grouping of the partial sums differs.
+__device__ __forceinline__ double grad_x(const double* ra, const double* rb, int x, int nx, const Beta& B, double ih,
+                                         bool diff) {
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 1; j <= 4; ++j) {
+    if (j > B.m) break;
+    const int xp = x + j >= nx ? x + j - nx : x + j;
+    const int xm = x - j < 0 ? x - j + nx : x - j;
+    const double a = diff ? __dsub_rn(ra[xp], rb[xp]) : ra[xp];
+    const double b = diff ? __dsub_rn(ra[xm], rb[xm]) : ra[xm];
+    acc = __dadd_rn(acc, __dmul_rn(B.b[j - 1], __dsub_rn(a, b)));
+  }
+  return __dmul_rn(acc, ih);
+}
+
+__global__ void __launch_bounds__(256) k_pair_sums2d(Geo G, Beta B, const double* ua, const double* va, size_t sa,
+                                                     const double* ub, const double* vb, size_t sb, const double* c,
+                                                     double* part) {
+  const size_t pr = blockIdx.y;
+  const double* UA = ua + pr * sa;
+  const double* VA = va + pr * sa;
+  const double* UB = ub + pr * sb;
+  const double* VB = vb + pr * sb;
+  const int nx = G.nx, ny = G.ny;
+  double sd = 0.0, sr = 0.0, ld = 0.0, lr = 0.0;
+  for (int r = blockIdx.x; r < ny; r += gridDim.x) {
+    int rp[4], rm[4];
+#pragma unroll
+    for (int j = 1; j <= 4; ++j) {
+      rp[j - 1] = ((r + j) % ny) * nx;
+      rm[j - 1] = ((r + ny * 4 - j) % ny) * nx;
+    }
+    const size_t row = size_t(r) * nx;
+    for (int x = threadIdx.x; x < nx; x += 256) {
+      const size_t p = row + x;
+      // axis 0 (y)
+      double ady = 0.0, ary = 0.0;
+#pragma unroll
+      for (int j = 1; j <= 4; ++j) {
+        if (j > B.m) break;
+        const size_t pp = size_t(rp[j - 1]) + x, pm = size_t(rm[j - 1]) + x;
+        const double bp = UB[pp], bm = UB[pm];
+        ady = __dadd_rn(ady, __dmul_rn(B.b[j - 1], __dsub_rn(__dsub_rn(UA[pp], bp), __dsub_rn(UA[pm], bm))));
+        ary = __dadd_rn(ary, __dmul_rn(B.b[j - 1], __dsub_rn(bp, bm)));
+      }
+      const double gdy = __dmul_rn(ady, G.ih[0]), gry = __dmul_rn(ary, G.ih[0]);
+      sd += gdy * gdy;
+      sr += gry * gry;
+      // axis 1 (x)
+      const double gdx = grad_x(UA + row, UB + row, x, nx, B, G.ih[1], true);
+      const double grx = grad_x(UB + row, nullptr, x, nx, B, G.ih[1], false);
+      sd += gdx * gdx;
+      sr += grx * grx;
+      const double cp = c[p], vbp = VB[p], ubp = UB[p];
+      const double md = __ddiv_rn(__dsub_rn(VA[p], vbp), cp);
+      const double mr = __ddiv_rn(vbp, cp);
+      sd += md * md;
+      sr += mr * mr;
+      const double du = __dsub_rn(UA[p], ubp);
+      ld += du * du;
+      lr += ubp * ubp;
+    }
+  }
+  sd = block_sum<256>(sd);
+  sr = block_sum<256>(sr);
+  ld = block_sum<256>(ld);
+  lr = block_sum<256>(lr);
+  if (threadIdx.x == 0) {
+    double* o = part + (pr * gridDim.x + blockIdx.x) * 4;
+    o[0] = sd;
+    o[1] = sr;
+    o[2] = ld;
+    o[3] = lr;
+  }
+}
+
 __global__ void k_pair_final(size_t pairs, int nb, const double* part, double* out) {
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < pairs * 4; e += size_t(gridDim.x) * blockDim.x) {
     const size_t pr = e / 4, q = e % 4;
@@ -435,7 +514,10 @@ void pair_energy_sums(EnergyWork& w, const ptb_grid& g, int scheme, size_t batch
   if (scheme != PTB_SPECTRAL) {
     const int nb = std::max(1, std::min(PAIR_BLOCKS, (n + 255) / 256));
     double* part = static_cast<double*>(w.buf[7].get(batch * nb * 4 * sizeof(double)));
-    k_pair_sums<<<dim3(nb, unsigned(batch)), 256, 0, st>>>(G, beta_of(scheme), n, ua, va, sa, ub, vb, sb, c, part);
+    if (G.dim == 2 && G.nx >= 256)
+      k_pair_sums2d<<<dim3(nb, unsigned(batch)), 256, 0, st>>>(G, beta_of(scheme), ua, va, sa, ub, vb, sb, c, part);
+    else
+      k_pair_sums<<<dim3(nb, unsigned(batch)), 256, 0, st>>>(G, beta_of(scheme), n, ua, va, sa, ub, vb, sb, c, part);
     PTB_LAUNCH_CHECK(ctx);
     k_pair_final<<<nblk(ctx, batch * 4), 256, 0, st>>>(batch, nb, part, out4);
     PTB_LAUNCH_CHECK(ctx);

@@ -103,6 +103,9 @@ struct ptb_transfer {
   // Fourier weights per axis: w[a][rem*nc + j] = weight of coarse node q-j..., see transfer.cu
   double* wx = nullptr;
   double* wy = nullptr;
+  // dense forms of the same maps for the GEMM path (2D, large grids): mx = cx x fx, my = fy x cy
+  double* mx = nullptr;
+  double* my = nullptr;
   ptb::DeviceBuffer nodes_half;  // scratch of interpolate_at_coarse_nodes
 };
 

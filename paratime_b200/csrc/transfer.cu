@@ -18,11 +18,18 @@
 // bin contributes cos(pi delta)).  W is tabulated on the host with exact integer
 // argument reduction, so the device path is a two-pass (x then y) dense stencil with
 // no FFT; R(I(U)) = U holds to round-off like the reference's FFT route.
+// On large 2D grids the two passes are matrix products with the dense forms
+//   Mx[j][q*r + rem] = W[rem][(q - j) mod n]   (x: half = in . Mx)
+//   My[q*r + rem][j] = W[rem][(q - j) mod n]   (y: out = My . half)
+// issued as cuBLAS DGEMMs of one fixed shape per field, so each slice's result does not
+// depend on how many slices a call (or a rank) carries.
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "ptb_internal.h"
+#include "ptb_procrustes.h"  // gemm (cuBLAS DGEMM on the context stream)
 
 namespace ptb {
 namespace {
@@ -246,6 +253,55 @@ void restrict_fields(ptb_transfer* t, size_t batch, const double* fine, double* 
   PTB_LAUNCH_CHECK(ctx);
 }
 
+namespace {
+// dense circulant matrix of one axis: rows x cols row-major, TRANSPOSED selects the x form
+std::vector<double> dense_axis(int n, int r, bool x_form) {
+  const std::vector<double> w = fourier_weights(n, r);
+  const size_t m = size_t(n) * r;
+  std::vector<double> d(m * n);
+  for (size_t i = 0; i < m; ++i) {
+    const int q = int(i / r), rem = int(i % r);
+    for (int j = 0; j < n; ++j) {
+      const double v = w[size_t(rem) * n + size_t(((q - j) % n + n) % n)];
+      if (x_form)
+        d[size_t(j) * m + i] = v;  // Mx[j][i]
+      else
+        d[i * n + size_t(j)] = v;  // My[i][j]
+    }
+  }
+  return d;
+}
+
+bool use_gemm(const TGeom& g) {
+  static const int env = [] {
+    const char* e = std::getenv("PTB_INTERP_GEMM");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (env == 0) return false;
+  const bool ok = g.cy > 1 && g.rx > 1 && g.ry > 1;
+  return ok && (env == 1 || size_t(g.fy) * g.fx >= size_t(512) * 512);
+}
+
+void interpolate_gemm(ptb_transfer* t, const TGeom& g, size_t batch, const double* coarse, double* fine) {
+  ptb_context* ctx = t->ctx;
+  if (!t->mx) {
+    const std::vector<double> mx = dense_axis(g.cx, g.rx, true), my = dense_axis(g.cy, g.ry, false);
+    PTB_CUDA_CHECK(cudaMalloc(&t->mx, mx.size() * sizeof(double)));
+    PTB_CUDA_CHECK(cudaMalloc(&t->my, my.size() * sizeof(double)));
+    PTB_CUDA_CHECK(cudaMemcpy(t->mx, mx.data(), mx.size() * sizeof(double), cudaMemcpyHostToDevice));
+    PTB_CUDA_CHECK(cudaMemcpy(t->my, my.data(), my.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  const size_t nc = size_t(g.cy) * g.cx, nh = size_t(g.cy) * g.fx, nf = size_t(g.fy) * g.fx;
+  double* half = static_cast<double*>(ctx->scratch[3].get(batch * nh * sizeof(double)));
+  // row-major products as column-major GEMMs: half_b^T (fx x cy) = Mx^T (fx x cx) . in_b^T (cx x cy)
+  for (size_t b = 0; b < batch; ++b)
+    gemm(ctx, false, false, g.fx, g.cy, g.cx, 1.0, t->mx, g.fx, coarse + b * nc, g.cx, 0.0, half + b * nh, g.fx);
+  // out_b^T (fx x fy) = half_b^T (fx x cy) . My^T (cy x fy)
+  for (size_t b = 0; b < batch; ++b)
+    gemm(ctx, false, false, g.fx, g.fy, g.cy, 1.0, half + b * nh, g.fx, t->my, g.cy, 0.0, fine + b * nf, g.fx);
+}
+}  // namespace
+
 void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, double* fine) {
   ptb_context* ctx = t->ctx;
   const TGeom g = geom(t);
@@ -254,6 +310,10 @@ void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, dou
   if (t->kind == PTB_INTERP_LINEAR || (g.rx == 1 && g.ry == 1)) {
     k_interp_linear<<<blocks_for(ctx, batch * nf), 256, 0, ctx->stream>>>(g, batch, coarse, fine);
     PTB_LAUNCH_CHECK(ctx);
+    return;
+  }
+  if (use_gemm(g)) {
+    interpolate_gemm(t, g, batch, coarse, fine);
     return;
   }
   // Fourier: x pass into scratch (cy x fx), then y pass (fy x fx)

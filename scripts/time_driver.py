@@ -1,12 +1,16 @@
-"""Time the device theta-parareal on BASELINE configs 1-3 (and optionally compare with the oracle/_ref)."""
+"""Time the device theta-parareal on BASELINE configs 1-4 (args "cfg[:K]") (and optionally compare with the oracle/_ref)."""
 import os, sys, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paratime_b200 as B
 import workloads as W
 ctx = B.Context(0)
-for cfg in [int(a) for a in (sys.argv[1:] or ["1", "2", "3"])]:
+for arg in (sys.argv[1:] or ["1", "2", "3"]):
+    cfg, _, kk = arg.partition(":")  # "cfg[:K]"
+    cfg = int(cfg)
     spec, cf, cc, u0, v0 = W.CONFIGS[cfg]()
+    if kk:
+        spec["iterations"] = int(kk)
     t0 = time.time()
     r = B.api.parareal_run(ctx, B.api.run_spec(**spec), cf, cc, u0, v0)
     wall = time.time() - t0

@@ -99,6 +99,22 @@ def cfg3(tol=1e-4, **kw):
     return _spec(nf, nc, 64, 8, 64, 8, tol, **kw), c, cc, u0, np.zeros_like(u0)
 
 
+def cfg4(tol=1e-4, **kw):
+    """The cfg3 generator at 2048^2 / 256^2, N = 128, K = 8, m_F = 128, m_C = 8 (m_s = 8, m_t = 16);
+    coarse c = Gaussian-smoothed (sigma = m_s/2 = 4 fine cells) then restricted fine c;
+    u0 = exp(-40000 |x - x0|^2) near the top.  PERIODIC: BASELINE's 32-cell absorbing layer is not
+    part of the reference (no oracle), so the periodic problem is the
+    parity-checkable stand-in."""
+    nf, nc = 2048, 256
+    rng = np.random.default_rng(SEED + 4)
+    c = layered_faulted(nf, rng)
+    cc = restrict(gaussian_smooth_periodic(c, 4.0), 8)
+    y, x = _mesh(nf)
+    x0 = rng.uniform(0.3, 0.7)
+    u0 = np.exp(-40000.0 * ((x - x0) ** 2 + (y - 0.15) ** 2))
+    return _spec(nf, nc, 128, 8, 128, 8, tol, **kw), c, cc, u0, np.zeros_like(u0)
+
+
 def cfg5_medium(n, seed=SEED + 5):
     """c = 0.75 + 0.25 S/max|S|, S = sum of 8 sinusoids of integer wavenumbers 1..4."""
     rng = np.random.default_rng(seed)
@@ -125,4 +141,4 @@ def cfg5_pulses(n, batch, seed=SEED + 50):
     return out
 
 
-CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3}
+CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4}
