@@ -16,7 +16,7 @@
 //               norm, first index on ties — the dgeqp3 rule with exact instead of downdated
 //               norms), forms the reflector (dlarfg), and a second barrier reduces v^T A.
 //               Stops at the first |R_jj| <= guard (the reference's keep rule).
-//   k_qr_formq  cooperative backward accumulation Q = H_0 ... H_{keep-1} [I; 0].
+//   k_wy_prep/k_wy_larft + DGEMMs  cooperative backward accumulation Q = H_0 ... H_{keep-1} [I; 0].
 //   k_jacobi    one-sided (Hestenes) Jacobi SVD in a single CTA, round-robin pair
 //               ordering, rotations until every pair is orthogonal to ~eps; singular
 //               values sorted descending.
@@ -75,10 +75,11 @@ __device__ __forceinline__ double warp_sum(double x) {
 // so the only block-wide barriers are the three grid barriers.
 __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double sh[];  // red[QR_THREADS] | w[n] | nrm[n]
+  extern __shared__ double sh[];  // red[QR_THREADS] | w[n] | nrm[n] | vs[rows_per]
   double* red = sh;
   double* w = red + QR_THREADS;
   double* nrm = w + a.n;
+  double* vs = nrm + a.n;  // this CTA's rows of the current reflector (1 at row j, 0 above)
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = QR_THREADS / 32;
   const int m = a.m, n = a.n;
@@ -154,13 +155,31 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
       a.tau[j] = tau;
       a.beta_out[j] = fabs(beta);
     }
-    for (int i = max(r0, j + 1) + tid; i < r1; i += QR_THREADS) col(j)[i] *= scal;
+    for (int i = r0 + tid; i < r1; i += QR_THREADS) {
+      double x = 0.0;
+      if (i > j) {
+        x = col(j)[i] * scal;
+        col(j)[i] = x;
+      } else if (i == j) {
+        x = 1.0;
+      }
+      vs[i - r0] = x;
+    }
     __syncthreads();  // the dot products below read rows scaled by other threads
-    const double* v = col(j);
-    for (int k = j + 1 + warp; k < n; k += nwarps) {  // w_k = v^T A[j:, k], own rows
-      double sacc = 0.0;
-      for (int i = max(r0, j) + lane; i < r1; i += 32) sacc += (i == j ? 1.0 : v[i]) * col(k)[i];
-      sacc = warp_sum(sacc);
+    const int i0 = max(r0, j);
+    // w_k = v^T A[j:, k] over own rows; 4 independent accumulators keep 4 loads in flight per lane
+    for (int k = j + 1 + warp; k < n; k += nwarps) {
+      const double* ck = col(k);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int i = i0 + lane;
+      for (; i + 96 < r1; i += 128) {
+        s0 += vs[i - r0] * ck[i];
+        s1 += vs[i + 32 - r0] * ck[i + 32];
+        s2 += vs[i + 64 - r0] * ck[i + 64];
+        s3 += vs[i + 96 - r0] * ck[i + 96];
+      }
+      for (; i < r1; i += 32) s0 += vs[i - r0] * ck[i];
+      const double sacc = warp_sum((s0 + s1) + (s2 + s3));
       if (lane == 0) part[size_t(g) * (n + 1) + k] = sacc;
     }
     grid.sync();
@@ -172,13 +191,27 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     __syncthreads();
     for (int k = j + 1 + warp; k < n; k += nwarps) {  // A[:, k] -= tau v w_k; fused next norms
       const double tw = tau * w[k];
-      double sacc = 0.0;
-      for (int i = max(r0, j) + lane; i < r1; i += 32) {
-        const double x = col(k)[i] - tw * (i == j ? 1.0 : v[i]);
-        col(k)[i] = x;
-        if (i > j) sacc += x * x;
+      double* ck = col(k);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int i = i0 + lane;
+      for (; i + 96 < r1; i += 128) {
+        const double x0 = ck[i] - tw * vs[i - r0], x1 = ck[i + 32] - tw * vs[i + 32 - r0];
+        const double x2 = ck[i + 64] - tw * vs[i + 64 - r0], x3 = ck[i + 96] - tw * vs[i + 96 - r0];
+        ck[i] = x0;
+        ck[i + 32] = x1;
+        ck[i + 64] = x2;
+        ck[i + 96] = x3;
+        s0 += i != j ? x0 * x0 : 0.0;  // row j becomes R's row: not part of the trailing norms
+        s1 += x1 * x1;
+        s2 += x2 * x2;
+        s3 += x3 * x3;
       }
-      sacc = warp_sum(sacc);
+      for (; i < r1; i += 32) {
+        const double x = ck[i] - tw * vs[i - r0];
+        ck[i] = x;
+        if (i != j) s0 += x * x;
+      }
+      const double sacc = warp_sum((s0 + s1) + (s2 + s3));
       if (lane == 0) partn[size_t(g) * (n + 1) + k] = sacc;
     }
     __syncthreads();
@@ -187,46 +220,34 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
   if (g == 0 && tid == 0) *a.keep_out = keep;
 }
 
-struct FormQArgs {
-  const double* A;  // reflectors below the diagonal (m x n, lda m)
-  const double* tau;
-  int m, keep;
-  double* Q;       // m x keep
-  double* part;    // [2][grid][keep]
-};
+// Blocked Q (compact WY, LAPACK dlarft/dorg2r order): H_1...H_k = I - V T V^T with V the unit
+// lower-trapezoidal reflector block and T upper triangular, so Q = E - V (T V1^T) with
+// E = [I_k; 0] and V1 the top k x k block of V.  Two DGEMMs replace k BLAS-2 sweeps.
+__global__ void k_wy_prep(const double* A, int m, int k, double* V, double* Q) {
+  const size_t total = size_t(m) * k;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const int c = int(e / m), i = int(e - size_t(c) * m);
+    V[e] = i < c ? 0.0 : (i == c ? 1.0 : A[e]);
+    Q[e] = i == c ? 1.0 : 0.0;
+  }
+}
 
-__global__ void __launch_bounds__(QR_THREADS) k_qr_formq(FormQArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ double sh[];
-  double* w = sh;
-  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = QR_THREADS / 32;
-  const int m = a.m, K = a.keep;
-  const int rows_per = (m + G - 1) / G;
-  const int r0 = min(m, g * rows_per), r1 = min(m, r0 + rows_per);
-  for (int c = 0; c < K; ++c)
-    for (int i = r0 + tid; i < r1; i += QR_THREADS) a.Q[size_t(c) * m + i] = (i == c) ? 1.0 : 0.0;
-  for (int j = K - 1; j >= 0; --j) {
-    const double* v = a.A + size_t(j) * m;
-    double* part = a.part + size_t(j & 1) * G * K;
-    for (int c = j + warp; c < K; c += nwarps) {
-      double sacc = 0.0;
-      for (int i = max(r0, j) + lane; i < r1; i += 32) sacc += (i == j ? 1.0 : v[i]) * a.Q[size_t(c) * m + i];
-      sacc = warp_sum(sacc);
-      if (lane == 0) part[size_t(g) * K + c] = sacc;
-    }
-    grid.sync();
-    for (int c = j + tid; c < K; c += QR_THREADS) {
-      double sacc = 0.0;
-      for (int q = 0; q < G; ++q) sacc += __ldcg(&part[size_t(q) * K + c]);
-      w[c] = sacc;
-    }
+// T from S = V^T V (k x k, column-major) and tau: T_jj = tau_j,
+// T[0:j, j] = T[0:j, 0:j] (-tau_j S[0:j, j])   (dlarft, direct = F, storev = C)
+__global__ void __launch_bounds__(256) k_wy_larft(const double* S, const double* tau, int k, double* T) {
+  extern __shared__ double z[];
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) T[e] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    const double tj = tau[j];
+    for (int l = threadIdx.x; l < j; l += blockDim.x) z[l] = -tj * S[size_t(j) * k + l];
     __syncthreads();
-    const double tau = a.tau[j];
-    for (int c = j + warp; c < K; c += nwarps) {
-      const double tw = tau * w[c];
-      for (int i = max(r0, j) + lane; i < r1; i += 32) a.Q[size_t(c) * m + i] -= tw * (i == j ? 1.0 : v[i]);
+    for (int i = threadIdx.x; i < j; i += blockDim.x) {
+      double acc = 0.0;
+      for (int l = i; l < j; ++l) acc += T[size_t(l) * k + i] * z[l];
+      T[size_t(j) * k + i] = acc;
     }
+    if (threadIdx.x == 0) T[size_t(j) * k + j] = tj;
     __syncthreads();
   }
 }
@@ -549,8 +570,11 @@ int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol,
   int* perm = static_cast<int*>(w.buf[2].get(size_t(n) * sizeof(int)));
   int* keep_d = static_cast<int*>(w.buf[3].get(sizeof(int)));
   double* betas = static_cast<double*>(w.buf[5].get(size_t(n) * sizeof(double)));
-  const size_t smem = (QR_THREADS + 2 * size_t(n)) * sizeof(double);
-  const int G = qr_grid(ctx, m, smem, reinterpret_cast<const void*>(k_qrcp));
+  size_t smem = (QR_THREADS + 2 * size_t(n)) * sizeof(double);
+  const int G = qr_grid(ctx, m, smem + 16384 * sizeof(double), reinterpret_cast<const void*>(k_qrcp));
+  const size_t rows_per = (size_t(m) + G - 1) / G;
+  if (rows_per > 16384) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
+  smem += rows_per * sizeof(double);
   double* part = static_cast<double*>(w.buf[4].get(size_t(2) * G * (n + 1) * sizeof(double)));
   QrArgs qa{A, m, n, drop_tol, tau, perm, part, keep_d, betas};
   void* args[] = {&qa};
@@ -563,15 +587,19 @@ int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol,
   double* Q = static_cast<double*>(Qb.get(std::max<size_t>(1, size_t(m) * keep) * sizeof(double)));
   double* R = static_cast<double*>(Rb.get(std::max<size_t>(1, size_t(keep) * n) * sizeof(double)));
   if (keep > 0) {
-    const size_t smem2 = std::max<size_t>(1, size_t(keep)) * sizeof(double);
-    const int G2 = qr_grid(ctx, m, smem2, reinterpret_cast<const void*>(k_qr_formq));
-    double* part2 = static_cast<double*>(w.buf[4].get(std::max(size_t(2) * G * (n + 1), size_t(2) * G2 * keep) *
-                                                        sizeof(double)));
-    FormQArgs fa{A, tau, m, keep, Q, part2};
-    void* args2[] = {&fa};
-    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qr_formq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
-    PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qr_formq), G2, QR_THREADS, args2, smem2, st));
+    const size_t mk = size_t(m) * keep, kk = size_t(keep) * keep;
+    double* V = static_cast<double*>(w.buf[19].get(mk * sizeof(double)));
+    double* S = static_cast<double*>(w.buf[20].get(3 * kk * sizeof(double)));
+    double* T = S + kk;
+    double* W = T + kk;
+    k_wy_prep<<<unsigned(std::min<size_t>((mk + 255) / 256, size_t(ctx->num_sms) * 16)), 256, 0, st>>>(A, m, keep,
+                                                                                                      V, Q);
     PTB_LAUNCH_CHECK(ctx);
+    gemm(ctx, true, false, keep, keep, m, 1.0, V, m, V, m, 0.0, S, keep);  // S = V^T V
+    k_wy_larft<<<1, 256, size_t(keep) * sizeof(double), st>>>(S, tau, keep, T);
+    PTB_LAUNCH_CHECK(ctx);
+    gemm(ctx, false, true, keep, keep, keep, 1.0, T, keep, V, m, 0.0, W, keep);  // W = T V1^T
+    gemm(ctx, false, false, m, keep, keep, -1.0, V, m, W, keep, 1.0, Q, m);     // Q = E - V W
     k_unpivot_r<<<std::max(1, std::min(256, (keep * n + 255) / 256)), 256, 0, st>>>(A, m, n, keep, perm, R);
     PTB_LAUNCH_CHECK(ctx);
   }
