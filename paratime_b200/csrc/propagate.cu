@@ -22,6 +22,10 @@
 // Kernel families:
 //   k_small   — one CTA owns a whole slice (N <= 4096: 1D fields, coarse 2D grids);
 //               u double-buffered in shared memory, all steps on chip, one barrier/step.
+//   k_cluster — a thread-block cluster owns a slice (2D, 4096 < N <= 32768, nx % 128 == 0):
+//               rows split over the CTAs, halo rows exchanged through DSMEM (st.async +
+//               mbarrier transaction counts), all steps on chip.
+//   k_wave2   — FAST-mode wavefront (below) with two columns per thread (even nx).
 //   k_wave    — 2D wavefront temporal blocking: a CTA owns a column strip (+ S+1 halo
 //               columns each side) of one slice and marches along y; S+1 time levels
 //               are in flight, level t one row behind level t-1.  Each thread owns one
@@ -36,9 +40,13 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "ptb_internal.h"
 
 namespace ptb {
+
+namespace cg = cooperative_groups;
 
 void nonfinite_on(ptb_context* ctx, cudaStream_t st, size_t n, size_t batch, const double* f, int32_t* flags);
 
@@ -191,6 +199,223 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs a) {
     const int bad = __syncthreads_or(!ok);
     if (bad && tid == 0) atomicOr(&a.flags[blockIdx.x], 1);
   }
+}
+
+// ------------------------------------------------------------------ k_cluster
+//
+// On-chip path for 2D slices of 4096 < N <= 32768 points (cfg1 / cfg5 128^2 fine slices):
+// one thread-block cluster of CS <= 8 CTAs owns a slice for all its steps.  CTA c holds
+// rows [c R, (c+1) R) (R = ny / CS); every thread keeps a 4-point row segment's u, vh and
+// coefficient (EXACT: also a) in registers.  u is double-buffered in shared memory with one
+// halo row above and below.  Per step: drift, publish the segment to shared memory, and the
+// CTA's first / last row go straight into the neighbouring CTAs' halo rows with st.async,
+// which completes bytes on the receiver's mbarrier (periodic ring, DSMEM).  A CTA barrier
+// covers its own rows; only the boundary-row threads wait on the mbarrier phase.  x
+// neighbours inside a warp come by shuffle.  No HBM traffic between the first load and the
+// last store.  Arithmetic identical to k_small / k_wave(2).
+//
+// Buffer reuse: halo rows of buffer P are rewritten two steps later, by a neighbour that
+// first had to receive this CTA's next-step rows, which it sends only after finishing the
+// reads of this step, so one mbarrier per buffer and no cluster-wide barrier per step.
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned cluster_map(unsigned addr, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async2(unsigned remote, double a, double b, unsigned remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(remote),
+               "d"(a), "d"(b), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// Thread mapping: the CTA's rows are cut into 128-point chunks (nx % 128 == 0, so a chunk
+// lies in one row); warp w owns chunks RW w .. RW w + RW - 1 and in each chunk lane l owns the
+// pairs A = chunk + 2l and B = chunk + 64 + 2l, so every 16-byte shared/global access of a
+// warp is contiguous (4 wavefronts).  x neighbours come by shuffle; only the chunk's outer
+// neighbours (lane 0 left, lane 31 right) are read from shared memory.
+constexpr int CL_RW = 2;        // chunks per warp
+constexpr int CL_THREADS = 512;  // 4096 points per CTA
+
+template <bool EXACT>
+__global__ void __launch_bounds__(CL_THREADS, 1) k_cluster(const SmallArgs a) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double cbuf[];  // [2][R + 2][nx]
+  __shared__ alignas(8) unsigned long long bars[2];
+  const int CS = int(cluster.num_blocks()), c = int(cluster.block_rank());
+  const int nx = a.p.nx, ny = a.p.ny, R = ny / CS;
+  const int plane = (R + 2) * nx;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t slice = blockIdx.x / CS;
+  const StepParams& p = a.p;
+  int lr[CL_RW], xa[CL_RW], xl[CL_RW], xr[CL_RW];
+#pragma unroll
+  for (int i = 0; i < CL_RW; ++i) {
+    const int g = 128 * (CL_RW * warp + i);  // first point of the chunk in the CTA's block
+    lr[i] = g / nx;
+    const int xc = g - lr[i] * nx;
+    xa[i] = xc + 2 * lane;
+    xl[i] = xc == 0 ? nx - 1 : xc - 1;
+    xr[i] = xc + 128 == nx ? 0 : xc + 128;
+  }
+  auto gidx = [&](int i, int half) {  // offset of pair (i, half) within the slice
+    return size_t(c * R + lr[i]) * nx + xa[i] + 64 * half;
+  };
+  double* __restrict__ U = a.u + slice * size_t(a.n);
+  double* __restrict__ V = a.v + slice * size_t(a.n);
+  // u, v, k, acc per point: index 4 i + {A0, A1, B0, B1}
+  double u[4 * CL_RW], v[4 * CL_RW], k[4 * CL_RW], acc[4 * CL_RW];
+#pragma unroll
+  for (int i = 0; i < CL_RW; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const size_t o = gidx(i, h);
+      const double2 uu = *reinterpret_cast<const double2*>(U + o);
+      const double2 vv = *reinterpret_cast<const double2*>(V + o);
+      const double2 kk = *reinterpret_cast<const double2*>(a.coef + o);
+      u[4 * i + 2 * h] = uu.x, u[4 * i + 2 * h + 1] = uu.y;
+      v[4 * i + 2 * h] = vv.x, v[4 * i + 2 * h + 1] = vv.y;
+      k[4 * i + 2 * h] = kk.x, k[4 * i + 2 * h + 1] = kk.y;
+      acc[4 * i + 2 * h] = acc[4 * i + 2 * h + 1] = 0.0;
+    }
+  // ranks owning the rows above (c+1: larger y) and below (c-1)
+  const int up_rank = c + 1 == CS ? 0 : c + 1, dn_rank = c == 0 ? CS - 1 : c - 1;
+  const unsigned bar0 = smem_addr(&bars[0]);
+  const unsigned halo_bytes = 2u * unsigned(nx) * sizeof(double);
+  bool waiter = false;
+#pragma unroll
+  for (int i = 0; i < CL_RW; ++i) waiter |= lr[i] == 0 || lr[i] == R - 1;
+  if (tid == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  cluster.sync();  // barriers initialised before any neighbour sends
+  // use index q: buffer q & 1, mbarrier phase (q >> 1) & 1
+  auto publish = [&](int q) {
+    double* buf = cbuf + (q & 1) * plane;
+    const unsigned bar = bar0 + 8u * unsigned(q & 1);
+#pragma unroll
+    for (int i = 0; i < CL_RW; ++i) {
+      double* row = buf + (lr[i] + 1) * nx;
+      *reinterpret_cast<double2*>(row + xa[i]) = make_double2(u[4 * i], u[4 * i + 1]);
+      *reinterpret_cast<double2*>(row + xa[i] + 64) = make_double2(u[4 * i + 2], u[4 * i + 3]);
+      if (lr[i] == 0) {  // first own row = top halo (row R+1) of the CTA below
+        const unsigned dst = cluster_map(smem_addr(buf + (R + 1) * nx), dn_rank);
+        const unsigned rb = cluster_map(bar, dn_rank);
+        st_async2(dst + 8u * unsigned(xa[i]), u[4 * i], u[4 * i + 1], rb);
+        st_async2(dst + 8u * unsigned(xa[i] + 64), u[4 * i + 2], u[4 * i + 3], rb);
+      }
+      if (lr[i] == R - 1) {  // last own row = bottom halo (row 0) of the CTA above
+        const unsigned dst = cluster_map(smem_addr(buf), up_rank);
+        const unsigned rb = cluster_map(bar, up_rank);
+        st_async2(dst + 8u * unsigned(xa[i]), u[4 * i], u[4 * i + 1], rb);
+        st_async2(dst + 8u * unsigned(xa[i] + 64), u[4 * i + 2], u[4 * i + 3], rb);
+      }
+    }
+    if (tid == 0) mbar_expect(bar, halo_bytes);
+    __syncthreads();  // own rows of buf complete
+    if (waiter) mbar_wait(bar, unsigned(q >> 1) & 1u);
+  };
+  // b (FAST) or c^2 Lap u (EXACT) for the points from buffer q & 1
+  auto kick = [&](int q, double (&out)[4 * CL_RW]) {
+#pragma unroll
+    for (int i = 0; i < CL_RW; ++i) {
+      const double* row = cbuf + (q & 1) * plane + (lr[i] + 1) * nx;
+      const double* w = u + 4 * i;
+      const double2 upa = *reinterpret_cast<const double2*>(row + nx + xa[i]);
+      const double2 upb = *reinterpret_cast<const double2*>(row + nx + xa[i] + 64);
+      const double2 dna = *reinterpret_cast<const double2*>(row - nx + xa[i]);
+      const double2 dnb = *reinterpret_cast<const double2*>(row - nx + xa[i] + 64);
+      // right of A1: lane+1's A0 (lane 31: lane 0's B0); right of B1: lane+1's B0 (lane 31: next chunk)
+      const double ra = __shfl_sync(0xffffffffu, lane == 0 ? w[2] : w[0], (lane + 1) & 31);
+      const double rbv = __shfl_down_sync(0xffffffffu, w[2], 1);
+      // left of A0: lane-1's A1 (lane 0: previous chunk); left of B0: lane-1's B1 (lane 0: lane 31's A1)
+      const double la = __shfl_up_sync(0xffffffffu, w[1], 1);
+      const double lbv = __shfl_sync(0xffffffffu, lane == 31 ? w[1] : w[3], (lane + 31) & 31);
+      const double left_a = lane == 0 ? row[xl[i]] : la;
+      const double right_b = lane == 31 ? row[xr[i]] : rbv;
+      const double ul[4] = {left_a, w[0], lbv, w[2]}, ur[4] = {w[1], ra, w[3], right_b};
+      const double ups[4] = {upa.x, upa.y, upb.x, upb.y}, dns[4] = {dna.x, dna.y, dnb.x, dnb.y};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (EXACT)
+          out[4 * i + j] = __dmul_rn(lap_exact<true>(w[j], ul[j], ur[j], ups[j], dns[j], p), k[4 * i + j]);
+        else
+          out[4 * i + j] = bfast<true>(w[j], ul[j], ur[j], ups[j], dns[j], k[4 * i + j], p);
+      }
+    }
+  };
+  publish(0);
+  {
+    double b[4 * CL_RW];
+    kick(0, b);
+#pragma unroll
+    for (int j = 0; j < 4 * CL_RW; ++j) {
+      if (EXACT)
+        acc[j] = b[j];
+      else
+        v[j] = v[j] + b[j];
+    }
+  }
+  for (int s = 0; s < a.steps; ++s) {
+#pragma unroll
+    for (int j = 0; j < 4 * CL_RW; ++j) {
+      if (EXACT)
+        u[j] = __dadd_rn(u[j], __dadd_rn(__dmul_rn(p.dt, v[j]), __dmul_rn(p.hdt2, acc[j])));
+      else
+        u[j] = fma(p.dt, v[j], u[j]);
+    }
+    publish(s + 1);
+    const bool last = s + 1 == a.steps;
+    double b[4 * CL_RW];
+    kick(s + 1, b);
+#pragma unroll
+    for (int j = 0; j < 4 * CL_RW; ++j) {
+      if (EXACT) {
+        v[j] = __dadd_rn(v[j], __dmul_rn(p.hd, __dadd_rn(acc[j], b[j])));
+        acc[j] = b[j];
+      } else {
+        v[j] = v[j] + b[j];
+        if (!last) v[j] = v[j] + b[j];
+      }
+    }
+  }
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < CL_RW; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const size_t o = gidx(i, h);
+      *reinterpret_cast<double2*>(U + o) = make_double2(u[4 * i + 2 * h], u[4 * i + 2 * h + 1]);
+      *reinterpret_cast<double2*>(V + o) = make_double2(v[4 * i + 2 * h], v[4 * i + 2 * h + 1]);
+      ok &= finite2(u[4 * i + 2 * h], v[4 * i + 2 * h]) && finite2(u[4 * i + 2 * h + 1], v[4 * i + 2 * h + 1]);
+    }
+  if (a.flags) {
+    const int bad = __syncthreads_or(!ok);
+    if (bad && tid == 0) atomicOr(&a.flags[slice], 1);
+  }
+  cluster.sync();  // no CTA exits while a neighbour may still address its shared memory
 }
 
 // ------------------------------------------------------------------ k_stream
@@ -679,6 +904,47 @@ void launch_small(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, int thr
   PTB_LAUNCH_CHECK(ctx);
 }
 
+// cluster size for k_cluster (0 = not applicable): smallest CS with ny % CS == 0 and at most
+// 4096 points (1024 threads x 4) per CTA
+int cluster_size(const StepParams& p, size_t n) {
+  static const int env = [] {
+    const char* e = std::getenv("PTB_CLUSTER");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (env == 0 || p.dim != 2 || n <= 4096 || n > 32768 || p.nx % 128 != 0) return 0;
+  // measured (scripts/sweep_w.py): ahead of k_wave2 up to clusters of 8 (128^2: 0.41-0.45e12
+  // vs 0.27-0.42e12 upd/s); at 16 CTAs (256^2) the wavefront kernel is as fast or faster
+  for (int cs : {2, 4, 8}) {
+    if (p.ny % cs) continue;
+    const size_t per = size_t(p.ny / cs) * p.nx;
+    if (per == size_t(128) * CL_RW * (CL_THREADS / 32)) return cs;  // exactly one full CTA
+  }
+  return 0;
+}
+
+template <bool EXACT>
+void launch_cluster(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, int cs, size_t batch) {
+  const int R = a.p.ny / cs, threads = CL_THREADS;
+  const size_t smem = size_t(2) * (R + 2) * a.p.nx * sizeof(double);
+  auto kern = k_cluster<EXACT>;
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (cs > 8) PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(batch * cs));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PTB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
+  PTB_LAUNCH_CHECK(ctx);
+}
+
 template <bool EXACT, bool HASY>
 void small_dispatch(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, size_t batch) {
   const int n = a.n;
@@ -805,9 +1071,13 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
       const size_t ctas = size_t(strips) * nrb * batch;
       const size_t slots = size_t(ctx->num_sms) * occ;
       const double rounds = std::ceil(double(ctas) / slots);
-      const double resident = double(std::min(ctas, slots)) / ctx->num_sms * (W / 32.0);  // warps per SM
-      const double lat = resident < 8 ? 8.0 / resident : 1.0;
-      const double cost = rounds * occ * (W / 32.0) * (rb + 2.0 * S) * std::max(1.0, lat * 0.5);
+      // per-SM time of one round ~ resident warps x rows / throughput; the kernel is
+      // latency-bound below 8 warps per SM (ncu: W=160, 5 warps/SM, runs ~1.6x slower per
+      // warp-row than 2 x W=128), so throughput scales with min(1, warps / 8)
+      const double warps = double(occ) * (W / 32.0);
+      const double resident = double(std::min(ctas, slots)) / ctx->num_sms * (W / 32.0);
+      const double eff = std::min(1.0, std::min(warps, resident) / 8.0);
+      const double cost = rounds * warps * (rb + 2.0 * S) / eff;
       if (cost < best_cost) {
         best_cost = cost;
         best = WavePlan{W, wu, strips, rb, nrb};
@@ -949,6 +1219,11 @@ void propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double
     }
     return;
   }
+  if (const int cs = cluster_size(p, n)) {
+    SmallArgs a{p, int(n), int(steps), u, v, exact ? pr->c2 : pr->kx, flags};
+    exact ? launch_cluster<true>(ctx, slot.stream, a, cs, batch) : launch_cluster<false>(ctx, slot.stream, a, cs, batch);
+    return;
+  }
   if (p.dim == 2) {
     exact ? wave_propagate<true>(pr, steps, batch, u, v, flags, slot)
           : wave_propagate<false>(pr, steps, batch, u, v, flags, slot);
@@ -964,6 +1239,9 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
   const char* m = exact ? "EXACT" : "FAST";
   if (batch == 0 || steps == 0) return "none";
   if (pr->n <= 4096) return std::string("k_small<") + m + "> x1 launch, one CTA per slice";
+  if (const int cs = cluster_size(p, pr->n))
+    return std::string("k_cluster<") + m + "> x1 launch, cluster of " + std::to_string(cs) + " CTAs x " +
+           std::to_string(CL_THREADS) + " threads per slice";
   if (p.dim != 2) return std::string("k_stream_drift/kick<") + m + "> 2 launches per step";
   std::string out;
   size_t rem = steps;

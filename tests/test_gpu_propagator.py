@@ -38,6 +38,9 @@ CASES = [
     (((37, 1030), (1 / 37, 1 / 1030)), 11, 2),  # several strips, tiny ny
     (((256, 256), (1 / 256, 1 / 256)), 64, 2),  # cfg2 fine grid
     (((200, 96), (1 / 200, 1 / 96)), 3, 1),
+    (((64, 128), (1 / 64, 1 / 128)), 21, 3),    # k_cluster, cluster of 2
+    (((256, 128), (1 / 256, 1 / 128)), 10, 2),  # k_cluster, cluster of 8
+    (((32, 512), (1 / 32, 1 / 512)), 9, 2),     # k_cluster, cluster of 4, 4 chunks per row
 ]
 
 
