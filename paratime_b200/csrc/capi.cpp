@@ -25,10 +25,19 @@ bool sync_check_enabled() {
 void* DeviceBuffer::get(size_t need) {
   if (need == 0) need = 8;
   if (need > bytes) {
+    // geometric growth (1.5x, 2 MiB granules): buffers sized by the corrector rank grow every
+    // parareal iteration, and each cudaFree/cudaMalloc pair synchronises the device
+    size_t want = need;
+    if (bytes) want = std::max(need, bytes + bytes / 2);
+    want = (want + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
     if (ptr) PTB_CUDA_CHECK(cudaFree(ptr));
     ptr = nullptr;
-    PTB_CUDA_CHECK(cudaMalloc(&ptr, need));
-    bytes = need;
+    if (cudaMalloc(&ptr, want) != cudaSuccess) {  // fall back to the exact size under pressure
+      (void)cudaGetLastError();
+      want = need;
+      PTB_CUDA_CHECK(cudaMalloc(&ptr, want));
+    }
+    bytes = want;
   }
   return ptr;
 }

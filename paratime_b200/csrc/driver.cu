@@ -787,12 +787,15 @@ struct Driver {
             nrm = to_host(d2, 2);
             res = nrm[0] > 0.0 ? std::sqrt(nrm[1]) / std::sqrt(nrm[0]) : 0.0;
           } else {
+            HostProf hp_(st());
             update_svd(pw, corr, Fp, Gp, int(rows), cols, s.tol);
+            hp_.mark("driver: update_svd total");
             if (s.remove_leading > 0) {
               drop_leading(corr, size_t(s.remove_leading), dropped, ctx);
               applied = &dropped;
             }
             res = relative_residual(pw, *applied, Fp, Gp, int(rows), cols);
+            hp_.mark("driver: residual");
             rk = applied->rank;
           }
         } else if (!omega_identity) {

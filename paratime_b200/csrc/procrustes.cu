@@ -392,6 +392,158 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
   for (int k = threadIdx.x; k < c; k += blockDim.x) a.sigma[k] = sv[a.order[k]];
 }
 
+// Multi-CTA one-sided Jacobi for matrices that do not fit one CTA's shared memory: the same
+// tournament schedule and per-pair arithmetic as k_jacobi (warp-strided sums, xor-shuffle
+// reduction, same rotation and stopping rules), so the result is bitwise the one k_jacobi<false>
+// computes; the c/2 pairs of a round are spread over all warps of the grid and a grid barrier
+// separates rounds.  A and V live in global memory (L2) and are read with __ldcg: another SM
+// may have rotated a column since this SM last cached it.  `ctl` (global): [0..1] colmax bits,
+// [2..3] rotated flags (double-buffered by sweep parity), [4] sweeps used.
+__global__ void __launch_bounds__(256) k_jacobi_coop(JacobiArgs a, unsigned long long* ctl) {
+  cg::grid_group grid = cg::this_grid();
+  const int r = a.r, c = a.c;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int gw = blockIdx.x * nw + (threadIdx.x >> 5), tw = gridDim.x * nw;
+  double* A = a.A;
+  double* V = a.V;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < size_t(c) * c; e += size_t(gridDim.x) * blockDim.x)
+    V[e] = (e % (c + 1) == 0) ? 1.0 : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl[0] = ctl[1] = ctl[2] = ctl[3] = 0ull;
+  const int cc = (c % 2 == 0) ? c : c + 1;
+  const double eps = 2.220446049250313e-16;
+  const double tol = eps * sqrt(double(r));
+  grid.sync();
+  int sweep = 0;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    const int par = sweep & 1;
+    for (int k = gw; k < c; k += tw) {
+      double sacc = 0.0;
+      for (int q = lane; q < r; q += 32) {
+        const double x = __ldcg(&A[size_t(k) * r + q]);
+        sacc += x * x;
+      }
+      sacc = warp_sum(sacc);
+      if (lane == 0) atomicMax(&ctl[par], static_cast<unsigned long long>(__double_as_longlong(sacc)));
+    }
+    grid.sync();
+    // every block has finished sweep - 1 (incl. reading its rotated flag): clear its slots,
+    // which sweep + 1 reuses
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl[par ^ 1] = ctl[2 + (par ^ 1)] = 0ull;
+    const double floor2 = eps * eps * __longlong_as_double(static_cast<long long>(__ldcg(&ctl[par])));
+    for (int round = 0; round < cc - 1; ++round) {
+      for (int pr = gw; pr < cc / 2; pr += tw) {
+        auto pos = [&](int q) { return q == 0 ? 0 : 1 + (q - 1 + round) % (cc - 1); };
+        int i = pos(pr), j = pos(cc - 1 - pr);
+        if (i > j) {
+          const int t = i;
+          i = j;
+          j = t;
+        }
+        if (j >= c) continue;
+        double* ai = A + size_t(i) * r;
+        double* aj = A + size_t(j) * r;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        // loads 4 rows ahead (L2 latency), accumulation in k order as k_jacobi (bitwise equal)
+        int k = lane;
+        for (; k + 96 < r; k += 128) {
+          double x[4], y[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            x[u] = __ldcg(&ai[k + 32 * u]);
+            y[u] = __ldcg(&aj[k + 32 * u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            al += x[u] * x[u];
+            be += y[u] * y[u];
+            ga += x[u] * y[u];
+          }
+        }
+        for (; k < r; k += 32) {
+          const double x = __ldcg(&ai[k]), y = __ldcg(&aj[k]);
+          al += x * x;
+          be += y * y;
+          ga += x * y;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        const double nab = sqrt(al) * sqrt(be);
+        if (ga != 0.0 && fabs(ga) > tol * nab && nab > floor2) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          auto rotate = [&](double* pi, double* pj, int len) {
+            int q = lane;
+            for (; q + 96 < len; q += 128) {
+              double x[4], y[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                x[u] = __ldcg(&pi[q + 32 * u]);
+                y[u] = __ldcg(&pj[q + 32 * u]);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                __stcg(&pi[q + 32 * u], cs * x[u] - sn * y[u]);
+                __stcg(&pj[q + 32 * u], sn * x[u] + cs * y[u]);
+              }
+            }
+            for (; q < len; q += 32) {
+              const double x = __ldcg(&pi[q]), y = __ldcg(&pj[q]);
+              __stcg(&pi[q], cs * x - sn * y);
+              __stcg(&pj[q], sn * x + cs * y);
+            }
+          };
+          rotate(ai, aj, r);
+          rotate(V + size_t(i) * c, V + size_t(j) * c, c);
+          if (lane == 0) ctl[2 + par] = 1ull;
+        }
+      }
+      grid.sync();
+    }
+    if (__ldcg(&ctl[2 + par]) == 0ull) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl[4] = static_cast<unsigned long long>(sweep);
+}
+
+// Epilogue of the multi-CTA path (single CTA): singular values = column norms, descending
+// order with index tie-break, U = A P / sigma, V P — as k_jacobi's tail.
+__global__ void __launch_bounds__(1024) k_jacobi_finish(JacobiArgs a, const unsigned long long* ctl) {
+  const int r = a.r, c = a.c;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  double* sv = a.tmp + size_t(r) * c + size_t(c) * c;
+  for (int k = warp; k < c; k += nwarps) {
+    double sacc = 0.0;
+    for (int q = lane; q < r; q += 32) sacc += a.A[size_t(k) * r + q] * a.A[size_t(k) * r + q];
+    sacc = warp_sum(sacc);
+    if (lane == 0) sv[k] = sqrt(sacc);
+  }
+  if (threadIdx.x == 0) sv[c] = double(ctl[4]);
+  __syncthreads();
+  for (int k = threadIdx.x; k < c; k += blockDim.x) {
+    int rank = 0;
+    for (int q = 0; q < c; ++q)
+      if (sv[q] > sv[k] || (sv[q] == sv[k] && q < k)) ++rank;
+    a.order[rank] = k;
+  }
+  for (int e = threadIdx.x; e < r * c; e += blockDim.x) a.tmp[e] = a.A[e];
+  for (int e = threadIdx.x; e < c * c; e += blockDim.x) a.tmp[size_t(r) * c + e] = a.V[e];
+  __syncthreads();
+  const double* SA = a.tmp;
+  const double* SV = a.tmp + size_t(r) * c;
+  for (int e = threadIdx.x; e < r * c; e += blockDim.x) {
+    const int k = e / r, q = e - k * r;
+    const int src = a.order[k];
+    const double sg = sv[src];
+    a.A[e] = sg > 0.0 ? SA[size_t(src) * r + q] / sg : 0.0;
+  }
+  for (int e = threadIdx.x; e < c * c; e += blockDim.x) {
+    const int k = e / c, q = e - k * c;
+    a.V[e] = SV[size_t(a.order[k]) * c + q];
+  }
+  for (int k = threadIdx.x; k < c; k += blockDim.x) a.sigma[k] = sv[a.order[k]];
+}
+
 __global__ void k_transpose(const double* in, int rows, int cols, double* out) {
   // in: rows x cols (col-major) -> out: cols x rows
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
@@ -633,13 +785,29 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
   double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 1) * sizeof(double)));
   JacobiArgs ja{A, V, r, c, sg, order, tmp, 40};
   const size_t smem = (size_t(r) * c + size_t(c) * c) * sizeof(double);
+  static const int jacobi_env = [] {  // PTB_JACOBI=single forces the one-CTA global-memory kernel
+    const char* e = std::getenv("PTB_JACOBI");
+    return e && std::string(e) == "single" ? 1 : 0;
+  }();
   if (smem <= 200 * 1024) {
     PTB_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k_jacobi<true><<<1, 1024, smem, st>>>(ja);
-  } else {
+    PTB_LAUNCH_CHECK(ctx);
+  } else if (jacobi_env == 1) {
     k_jacobi<false><<<1, 1024, 0, st>>>(ja);
+    PTB_LAUNCH_CHECK(ctx);
+  } else {
+    unsigned long long* ctl = static_cast<unsigned long long*>(w.buf[21].get(8 * sizeof(unsigned long long)));
+    const int pairs = ((c % 2 == 0) ? c : c + 1) / 2;
+    int per_sm = 0;
+    PTB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_coop, 256, 0));
+    const int G = std::max(1, std::min({(pairs + 7) / 8, ctx->num_sms * std::max(1, per_sm), ctx->num_sms}));
+    void* args[] = {&ja, &ctl};
+    PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_jacobi_coop), G, 256, args, 0, st));
+    PTB_LAUNCH_CHECK(ctx);
+    k_jacobi_finish<<<1, 1024, 0, st>>>(ja, ctl);
+    PTB_LAUNCH_CHECK(ctx);
   }
-  PTB_LAUNCH_CHECK(ctx);
   PTB_CUDA_CHECK(cudaMemcpyAsync(sigma.data(), sg, size_t(c) * sizeof(double), cudaMemcpyDeviceToHost, st));
   // M = A_sorted diag(s) V^T  (A is r x c = U when !trans; when trans, M^T = A S V^T -> M = V S A^T)
   double* U = static_cast<double*>(Ub.get(size_t(p) * k * sizeof(double)));
@@ -716,6 +884,7 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
     return;
   }
   require(rows == c.rows, "update_svd: block rows do not match corrector");
+  HostProf hp_(ctx->stream);
   const int r = c.rank;
   const double* U = c.Xp();
   const double* V = c.Yp();
@@ -729,11 +898,15 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
   PTB_CUDA_CHECK(cudaMemcpyAsync(Gr, G, size_t(rows) * cols * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   gemm(ctx, false, false, rows, cols, r, -1.0, U, rows, UF, r, 1.0, Fr, rows);
   gemm(ctx, false, false, rows, cols, r, -1.0, V, rows, VG, r, 1.0, Gr, rows);
+  hp_.mark("update: projections");
   const double qr_guard = 1e-14;
   const double fn = std::sqrt(dev_sumsq(ctx, F, size_t(rows) * cols, w.buf[11]));
   const double gn = std::sqrt(dev_sumsq(ctx, G, size_t(rows) * cols, w.buf[11]));
+  hp_.mark("update: norms");
   const int qf = truncated_qr(w, Fr, rows, cols, qr_guard * fn, w.QF, w.RF);
+  hp_.mark("update: qr F");
   const int qg = truncated_qr(w, Gr, rows, cols, qr_guard * gn, w.QG, w.RG);
+  hp_.mark("update: qr G");
   double* LB = static_cast<double*>(w.buf[17].get(std::max<size_t>(1, size_t(r + qf) * cols) * sizeof(double)));
   double* RB = static_cast<double*>(w.buf[18].get(std::max<size_t>(1, size_t(r + qg) * cols) * sizeof(double)));
   const unsigned nb = unsigned(std::max(1, std::min(1024, ((r + std::max(qf, qg)) * cols + 255) / 256)));
@@ -746,8 +919,10 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
   gemm(ctx, false, true, hp, hq, cols, 1.0, LB, hp, RB, hq, 0.0, H, hp);
   k_add_diag<<<1, 256, 0, ctx->stream>>>(H, hp, static_cast<const double*>(c.Sd.ptr), r);
   PTB_LAUNCH_CHECK(ctx);
+  hp_.mark("update: H");
   std::vector<double> sigma;
   thin_svd(w, H, hp, hq, w.Uh, sigma, w.Vh);
+  hp_.mark("update: svd");
   const int keep = truncate_count(sigma, tol);
   // Uext = [U QF], Vext = [V QG]; X = Uext Uh[:, :keep], Y = Vext Vh[:, :keep]
   DevCorrector nc;
@@ -762,9 +937,11 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
   fix_signs(ctx, X, Y, rows, keep);
   sigma.resize(size_t(keep));
   PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  hp_.mark("update: rotate");
   std::swap(c.X, nc.X);
   std::swap(c.Y, nc.Y);
   c.assign(rows, keep, sigma, tol);
+  hp_.mark("update: assign/free");
 }
 
 // out (rows x batch) = X (Y^T in)   (procrustes.cpp:82-86)

@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <mutex>
 #include <stdexcept>
+#include <chrono>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -46,6 +48,30 @@ bool sync_check_enabled();  // PTB_SYNC_CHECK=1: synchronise after every launch 
                                 " at " + __FILE__ + ":" + std::to_string(__LINE__));   \
     (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                           \
   } while (0)
+
+// Opt-in host timeline (PTB_PROF=1): mark(label) synchronises the stream and prints the time
+// since the previous mark to stderr.  Diagnostics only; off by default (no synchronisation).
+struct HostProf {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::chrono::steady_clock::time_point t;
+  explicit HostProf(cudaStream_t s) : st(s) {
+    static const bool env = std::getenv("PTB_PROF") != nullptr;
+    on = env;
+    if (on) {
+      cudaStreamSynchronize(st);
+      t = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(const char* label) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ptb prof] %-28s %9.3f ms\n", label,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // Grow-only device scratch buffer.
 struct DeviceBuffer {
