@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -102,7 +103,7 @@ void Comm::allgather(const void* send, void* recv, size_t bytes_per_rank, cudaSt
     loopback->barrier();
     return;
   }
-  if (world == 1) {
+  if (world == 1 && !handle) {
     if (send != recv)
       PTB_CUDA_CHECK(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, st));
     return;
@@ -157,10 +158,20 @@ ptb_status ptb_comm_create(ptb_context* ctx, int rank, int world, const char* id
     auto* c = new ptb_comm();
     c->c.rank = rank;
     c->c.world = world;
-    if (world > 1) {
-      require(id128 != nullptr, "comm: null unique id");
+    // PTB_NCCL_FORCE=1 (tests): a one-rank NCCL communicator, so world 1 exercises the
+    // NCCL runtime path (dlopen, init, all-gather) on a single GPU
+    static const bool force = [] {
+      const char* e = std::getenv("PTB_NCCL_FORCE");
+      return e && std::atoi(e) != 0;
+    }();
+    if (world > 1 || force) {
       ncclUniqueId id;
-      std::memcpy(&id, id128, sizeof(id));
+      if (world == 1) {  // nobody to share an id with
+        check_nccl(nccl().getUniqueId(&id), "ncclGetUniqueId");
+      } else {
+        require(id128 != nullptr, "comm: null unique id");
+        std::memcpy(&id, id128, sizeof(id));
+      }
       cudaSetDevice(ctx->device);
       ncclComm_t comm = nullptr;
       check_nccl(nccl().commInitRank(&comm, world, id, rank), "ncclCommInitRank");

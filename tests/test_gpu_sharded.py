@@ -58,3 +58,28 @@ def test_sharded_equals_single_gpu(world, variant):
         b = min(N + 1, a + chunk)
         lo = 0 if r == 0 else a
         assert np.array_equal(o["states"][:, lo:b], single["states"][:, lo:b])
+
+
+def test_nccl_communicator_world1_equals_no_comm(tmp_path):
+    """The NCCL runtime path (dlopen of libnccl.so.2, ncclCommInitRank, ncclAllGather of the
+    coarse payload) on one GPU: a one-rank NCCL communicator must give bitwise the result of
+    the communicator-free run.  Multi-rank NCCL needs several GPUs (bench.py under torchrun)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    import paratime_b200 as B
+
+    root = Path(__file__).resolve().parent.parent
+    out = tmp_path / "nccl.npz"
+    env = dict(os.environ, PTB_NCCL_FORCE="1", PYTHONPATH=str(root))
+    subprocess.run([sys.executable, str(root / "tests" / "nccl_probe.py"), str(out)], check=True, env=env,
+                   timeout=600)
+    got = np.load(out)
+    spec, cf, cc, u0, v0 = W.cfg1()
+    ctx = B.Context(0)
+    ref = B.api.parareal_run(ctx, B.api.run_spec(**spec), cf, cc, u0, v0, keep_states=True)
+    assert np.array_equal(got["states"], ref["states"])
+    assert np.array_equal(got["energy_err"], ref["energy_err"])
+    assert np.array_equal(got["rank"], ref["rank"])
