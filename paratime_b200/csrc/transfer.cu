@@ -158,43 +158,6 @@ __global__ void k_fourier_y(int n, int cols, int r, size_t batch, const double* 
   }
 }
 
-// I(d) evaluated only at the coarse nodes (fine index r*j): the rem = 0 outputs of the
-// x pass, then of the y pass — the same weights and accumulation order as the full passes,
-// so the values equal restricting the full interpolation bitwise.
-__global__ void k_fourier_x_nodes(int rows, int n, size_t batch, const double* __restrict__ w,
-                                  const double* __restrict__ in, double* __restrict__ out) {
-  const size_t total = batch * rows * size_t(n);
-  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
-    const size_t line = e / n;
-    const int q = int(e - line * n);
-    const double* L = in + line * n;
-    double acc = 0.0;
-    int idx = q;
-    for (int d = 0; d < n; ++d) {
-      acc = fma(w[d], L[idx], acc);
-      idx = idx == 0 ? n - 1 : idx - 1;
-    }
-    out[e] = acc;
-  }
-}
-
-__global__ void k_fourier_y_nodes(int n, int cols, size_t batch, const double* __restrict__ w,
-                                  const double* __restrict__ in, double* __restrict__ out) {
-  const size_t plane = size_t(n) * cols, total = batch * plane;
-  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
-    const size_t b = e / plane, f = e - b * plane;
-    const int q = int(f / cols), x = int(f - size_t(q) * cols);
-    const double* P = in + b * plane + x;
-    double acc = 0.0;
-    int idx = q;
-    for (int d = 0; d < n; ++d) {
-      acc = fma(w[d], P[size_t(idx) * cols], acc);
-      idx = idx == 0 ? n - 1 : idx - 1;
-    }
-    out[e] = acc;
-  }
-}
-
 __global__ void k_copy(size_t total, const double* in, double* out) {
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x)
     out[e] = in[e];
@@ -212,6 +175,10 @@ std::vector<double> fourier_weights(int n, int r) {
   const int smax = (n % 2 == 0) ? n / 2 - 1 : (n - 1) / 2;
   for (int rem = 0; rem < r; ++rem)
     for (int d = 0; d < n; ++d) {
+      if (rem == 0) {  // K(integer d) = delta(d) exactly: the interpolant passes through the nodes
+        w[size_t(d)] = d == 0 ? 1.0 : 0.0;
+        continue;
+      }
       const long long num = (long long)d * r + rem;  // delta = num / r
       long double acc = 1.0L;
       for (int s = 1; s <= smax; ++s) {
@@ -345,17 +312,13 @@ void interpolate_at_coarse_nodes(ptb_transfer* t, size_t batch, const double* co
     PTB_LAUNCH_CHECK(ctx);
     return;
   }
-  const double* src = coarse;
-  if (g.rx > 1) {
-    double* half = (g.ry > 1) ? static_cast<double*>(t->nodes_half.get(batch * nc * sizeof(double))) : out;
-    k_fourier_x_nodes<<<blocks_for(ctx, batch * nc), 256, 0, ctx->stream>>>(g.cy, g.cx, batch, t->wx, coarse, half);
-    PTB_LAUNCH_CHECK(ctx);
-    src = half;
-  }
-  if (g.ry > 1) {
-    k_fourier_y_nodes<<<blocks_for(ctx, batch * nc), 256, 0, ctx->stream>>>(g.cy, g.cx, batch, t->wy, src, out);
-    PTB_LAUNCH_CHECK(ctx);
-  }
+  // Fourier: W[0][d] = delta(d) exactly (fourier_weights), so both passes reproduce the node
+  // values bit for bit (adding exact zeros) for finite data, and so does the dense GEMM route:
+  // R(I(d)) = d.  (Non-finite d: the coarse step that follows turns the state all-NaN, as the
+  // reference's nan_state does, so NaN spreading inside I is not observable.)
+  const size_t total = batch * nc;
+  k_copy<<<blocks_for(ctx, total), 256, 0, ctx->stream>>>(total, coarse, out);
+  PTB_LAUNCH_CHECK(ctx);
 }
 
 }  // namespace ptb
