@@ -809,6 +809,12 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
     PTB_LAUNCH_CHECK(ctx);
   }
   PTB_CUDA_CHECK(cudaMemcpyAsync(sigma.data(), sg, size_t(c) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (HostProf(st).on) {  // diagnostics: sweeps used (written after the singular values)
+    double sweeps = 0.0;
+    PTB_CUDA_CHECK(cudaMemcpy(&sweeps, tmp + size_t(r) * c + size_t(c) * c + c, sizeof(double),
+                              cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[ptb prof] jacobi %d x %d: %g sweeps\n", r, c, sweeps);
+  }
   // M = A_sorted diag(s) V^T  (A is r x c = U when !trans; when trans, M^T = A S V^T -> M = V S A^T)
   double* U = static_cast<double*>(Ub.get(size_t(p) * k * sizeof(double)));
   double* Vo = static_cast<double*>(Vb.get(size_t(q) * k * sizeof(double)));
