@@ -687,6 +687,7 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
 ProcWork::ProcWork(ptb_context* c) : ctx(c) {}
 ProcWork::~ProcWork() {
   for (auto& b : buf) b.release();
+  for (DeviceBuffer* b : {&QF, &RF, &QG, &RG, &Uh, &Vh, &PQ, &PR, &PU}) b->release();
 }
 
 DevCorrector::~DevCorrector() {
@@ -759,30 +760,11 @@ int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol,
 }
 
 // thin SVD of M (p x q): U (p x k), sigma (k, host), V (q x k), k = min(p, q)
-void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std::vector<double>& sigma,
-              DeviceBuffer& Vb) {
+// One-sided Jacobi of A (r x c, r >= c, column-major, overwritten): A := U (sorted, unit
+// columns), V (c x c), sigma (c, descending) -- the device buffers of JacobiArgs.
+void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, double* tmp, int* order) {
   ptb_context* ctx = w.ctx;
   cudaStream_t st = ctx->stream;
-  const int k = std::min(p, q);
-  sigma.assign(size_t(k), 0.0);
-  if (k == 0) {
-    Ub.get(8);
-    Vb.get(8);
-    return;
-  }
-  const bool trans = p < q;
-  const int r = trans ? q : p, c = k;
-  double* A = static_cast<double*>(w.buf[6].get(size_t(r) * c * sizeof(double)));
-  if (trans) {
-    k_transpose<<<std::max(1, std::min(1024, (p * q + 255) / 256)), 256, 0, st>>>(M, p, q, A);
-    PTB_LAUNCH_CHECK(ctx);
-  } else {
-    PTB_CUDA_CHECK(cudaMemcpyAsync(A, M, size_t(p) * q * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  }
-  double* V = static_cast<double*>(w.buf[7].get(size_t(c) * c * sizeof(double)));
-  double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
-  int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
-  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 1) * sizeof(double)));
   JacobiArgs ja{A, V, r, c, sg, order, tmp, 40};
   const size_t smem = (size_t(r) * c + size_t(c) * c) * sizeof(double);
   static const int jacobi_env = [] {  // PTB_JACOBI=single forces the one-CTA global-memory kernel
@@ -808,16 +790,85 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
     k_jacobi_finish<<<1, 1024, 0, st>>>(ja, ctl);
     PTB_LAUNCH_CHECK(ctx);
   }
-  PTB_CUDA_CHECK(cudaMemcpyAsync(sigma.data(), sg, size_t(c) * sizeof(double), cudaMemcpyDeviceToHost, st));
   if (HostProf(st).on) {  // diagnostics: sweeps used (written after the singular values)
     double sweeps = 0.0;
-    PTB_CUDA_CHECK(cudaMemcpy(&sweeps, tmp + size_t(r) * c + size_t(c) * c + c, sizeof(double),
-                              cudaMemcpyDeviceToHost));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(&sweeps, tmp + size_t(r) * c + size_t(c) * c + c, sizeof(double),
+                                   cudaMemcpyDeviceToHost, st));
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st));
     std::fprintf(stderr, "[ptb prof] jacobi %d x %d: %g sweeps\n", r, c, sweeps);
   }
-  // M = A_sorted diag(s) V^T  (A is r x c = U when !trans; when trans, M^T = A S V^T -> M = V S A^T)
+}
+
+// thin SVD of M (p x q): U (p x k), sigma (k, host), V (q x k), k = min(p, q).
+// A = M (or M^T) is r x c with r >= c.  For c >= 32 it is preconditioned as in dgesvj: a
+// column-pivoted QR A = Q R first, then one-sided Jacobi on R^T (c x kq), whose columns are
+// already close to orthogonal for graded matrices, so far fewer sweeps are needed (the
+// corrector's H spans ~13 decades: 16-24 sweeps unpreconditioned).  R^T = U' S V'^T gives
+// A = (Q V') S U'^T.  Row order does not change column inner products, so the un-pivoted R
+// truncated_qr returns serves as well as the pivoted one.
+void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std::vector<double>& sigma,
+              DeviceBuffer& Vb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  const int k = std::min(p, q);
+  sigma.assign(size_t(k), 0.0);
+  if (k == 0) {
+    Ub.get(8);
+    Vb.get(8);
+    return;
+  }
+  const bool trans = p < q;
+  const int r = trans ? q : p, c = k;
+  double* A = static_cast<double*>(w.buf[6].get(size_t(r) * c * sizeof(double)));
+  if (trans) {
+    k_transpose<<<std::max(1, std::min(1024, (p * q + 255) / 256)), 256, 0, st>>>(M, p, q, A);
+    PTB_LAUNCH_CHECK(ctx);
+  } else {
+    PTB_CUDA_CHECK(cudaMemcpyAsync(A, M, size_t(p) * q * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  static const bool precond_env = [] {
+    const char* e = std::getenv("PTB_SVD_PRECOND");
+    return !(e && std::atoi(e) == 0);
+  }();
   double* U = static_cast<double*>(Ub.get(size_t(p) * k * sizeof(double)));
   double* Vo = static_cast<double*>(Vb.get(size_t(q) * k * sizeof(double)));
+  if (precond_env && c >= 32) {
+    const int kq = truncated_qr(w, A, r, c, 0.0, w.PQ, w.PR);  // A = Q R, Q r x kq, R kq x c
+    double* Bt = static_cast<double*>(w.buf[6].get(size_t(r) * c * sizeof(double)));  // A no longer needed
+    double* V = static_cast<double*>(w.buf[7].get(std::max<size_t>(1, size_t(kq) * kq) * sizeof(double)));
+    double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
+    int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
+    double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 1) * sizeof(double)));
+    std::vector<double> s_k(size_t(kq), 0.0);
+    if (kq > 0) {
+      // Bt = R^T (c x kq): R is kq x c column-major
+      k_transpose<<<std::max(1, std::min(1024, (kq * c + 255) / 256)), 256, 0, st>>>(static_cast<double*>(w.PR.ptr),
+                                                                                   kq, c, Bt);
+      PTB_LAUNCH_CHECK(ctx);
+      jacobi_core(w, Bt, c, kq, V, sg, tmp, order);  // Bt := U' (c x kq), V' (kq x kq)
+      PTB_CUDA_CHECK(cudaMemcpyAsync(s_k.data(), sg, size_t(kq) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    // left factor of A: Q V' (r x kq); right factor: U' (c x kq); columns kq..k-1 (sigma 0): zero
+    double* QV = static_cast<double*>(w.PU.get(size_t(r) * k * sizeof(double)));
+    PTB_CUDA_CHECK(cudaMemsetAsync(QV, 0, size_t(r) * k * sizeof(double), st));
+    if (kq > 0) gemm(ctx, false, false, r, kq, kq, 1.0, static_cast<double*>(w.PQ.ptr), r, V, kq, 0.0, QV, r);
+    double* UL = trans ? U : Vo;  // destination of U' (c rows)
+    double* AL = trans ? Vo : U;  // destination of Q V' (r rows)
+    PTB_CUDA_CHECK(cudaMemsetAsync(UL, 0, size_t(c) * k * sizeof(double), st));
+    if (kq > 0)
+      PTB_CUDA_CHECK(cudaMemcpyAsync(UL, Bt, size_t(c) * kq * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(AL, QV, size_t(r) * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (int i = 0; i < kq; ++i) sigma[size_t(i)] = s_k[size_t(i)];
+    return;
+  }
+  double* V = static_cast<double*>(w.buf[7].get(size_t(c) * c * sizeof(double)));
+  double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
+  int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
+  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 1) * sizeof(double)));
+  jacobi_core(w, A, r, c, V, sg, tmp, order);
+  PTB_CUDA_CHECK(cudaMemcpyAsync(sigma.data(), sg, size_t(c) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // M = A_sorted diag(s) V^T  (A is r x c = U when !trans; when trans, M^T = A S V^T -> M = V S A^T)
   if (!trans) {
     PTB_CUDA_CHECK(cudaMemcpyAsync(U, A, size_t(p) * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
     PTB_CUDA_CHECK(cudaMemcpyAsync(Vo, V, size_t(q) * k * sizeof(double), cudaMemcpyDeviceToDevice, st));

@@ -28,6 +28,7 @@ struct ProcWork {
   ptb_context* ctx;
   DeviceBuffer buf[24];
   DeviceBuffer QF, RF, QG, RG, Uh, Vh;
+  DeviceBuffer PQ, PR, PU;  // thin_svd preconditioning: Q, R of the QR and U of R^T
   explicit ProcWork(ptb_context* c);
   ~ProcWork();
 };
