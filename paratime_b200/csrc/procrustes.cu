@@ -37,7 +37,7 @@ namespace cg = cooperative_groups;
 namespace ptb {
 namespace {
 
-constexpr int QR_THREADS = 256;
+constexpr int QR_THREADS = 1024;
 
 struct QrArgs {
   double* A;  // m x n column-major, lda = m
@@ -100,10 +100,12 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     double* part = a.part + size_t(j & 1) * G * (n + 1);
     double* partn = a.part + size_t((j + 1) & 1) * G * (n + 1);
     grid.sync();
-    for (int k = j + tid; k < n; k += QR_THREADS) {
+    // cross-CTA partials: one warp per column, lanes over CTAs (fixed order for a given grid)
+    for (int k = j + warp; k < n; k += nwarps) {
       double sacc = 0.0;
-      for (int c = 0; c < G; ++c) sacc += __ldcg(&part[size_t(c) * (n + 1) + k]);
-      nrm[k] = sacc;
+      for (int c = lane; c < G; c += 32) sacc += __ldcg(&part[size_t(c) * (n + 1) + k]);
+      sacc = warp_sum(sacc);
+      if (lane == 0) nrm[k] = sacc;
     }
     __syncthreads();
     int p = j;  // max remaining norm, first index on ties (idamax)
@@ -132,8 +134,15 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     xs = cta_reduce(xs, red);
     if (tid == 0) partn[size_t(g) * (n + 1) + n] = xs;
     grid.sync();
-    double xnorm2 = 0.0;
-    for (int c = 0; c < G; ++c) xnorm2 += __ldcg(&partn[size_t(c) * (n + 1) + n]);
+    if (warp == 0) {
+      double sacc = 0.0;
+      for (int c = lane; c < G; c += 32) sacc += __ldcg(&partn[size_t(c) * (n + 1) + n]);
+      sacc = warp_sum(sacc);
+      if (lane == 0) red[0] = sacc;
+    }
+    __syncthreads();
+    const double xnorm2 = red[0];
+    __syncthreads();  // red is reused by cta_reduce in the next column
     const double alpha = __ldcg(&col(j)[j]);
     const double xnorm = sqrt(xnorm2);
     double beta, tau, scal;
@@ -170,48 +179,51 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     // w_k = v^T A[j:, k] over own rows; 4 independent accumulators keep 4 loads in flight per lane
     for (int k = j + 1 + warp; k < n; k += nwarps) {
       const double* ck = col(k);
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       int i = i0 + lane;
-      for (; i + 96 < r1; i += 128) {
-        s0 += vs[i - r0] * ck[i];
-        s1 += vs[i + 32 - r0] * ck[i + 32];
-        s2 += vs[i + 64 - r0] * ck[i + 64];
-        s3 += vs[i + 96 - r0] * ck[i + 96];
+      for (; i + 224 < r1; i += 256) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = ck[i + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] += vs[i + 32 * u - r0] * x[u];
       }
-      for (; i < r1; i += 32) s0 += vs[i - r0] * ck[i];
-      const double sacc = warp_sum((s0 + s1) + (s2 + s3));
+      for (; i < r1; i += 32) s[0] += vs[i - r0] * ck[i];
+      const double sacc = warp_sum(((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7])));
       if (lane == 0) part[size_t(g) * (n + 1) + k] = sacc;
     }
     grid.sync();
-    for (int k = j + 1 + tid; k < n; k += QR_THREADS) {
+    for (int k = j + 1 + warp; k < n; k += nwarps) {
       double sacc = 0.0;
-      for (int c = 0; c < G; ++c) sacc += __ldcg(&part[size_t(c) * (n + 1) + k]);
-      w[k] = sacc;
+      for (int c = lane; c < G; c += 32) sacc += __ldcg(&part[size_t(c) * (n + 1) + k]);
+      sacc = warp_sum(sacc);
+      if (lane == 0) w[k] = sacc;
     }
     __syncthreads();
     for (int k = j + 1 + warp; k < n; k += nwarps) {  // A[:, k] -= tau v w_k; fused next norms
       const double tw = tau * w[k];
       double* ck = col(k);
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       int i = i0 + lane;
-      for (; i + 96 < r1; i += 128) {
-        const double x0 = ck[i] - tw * vs[i - r0], x1 = ck[i + 32] - tw * vs[i + 32 - r0];
-        const double x2 = ck[i + 64] - tw * vs[i + 64 - r0], x3 = ck[i + 96] - tw * vs[i + 96 - r0];
-        ck[i] = x0;
-        ck[i + 32] = x1;
-        ck[i + 64] = x2;
-        ck[i + 96] = x3;
-        s0 += i != j ? x0 * x0 : 0.0;  // row j becomes R's row: not part of the trailing norms
-        s1 += x1 * x1;
-        s2 += x2 * x2;
-        s3 += x3 * x3;
+      for (; i + 224 < r1; i += 256) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = ck[i + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          x[u] -= tw * vs[i + 32 * u - r0];
+          ck[i + 32 * u] = x[u];
+        }
+        s[0] += i != j ? x[0] * x[0] : 0.0;  // row j becomes R's row: not part of the trailing norms
+#pragma unroll
+        for (int u = 1; u < 8; ++u) s[u] += x[u] * x[u];
       }
       for (; i < r1; i += 32) {
         const double x = ck[i] - tw * vs[i - r0];
         ck[i] = x;
-        if (i != j) s0 += x * x;
+        if (i != j) s[0] += x * x;
       }
-      const double sacc = warp_sum((s0 + s1) + (s2 + s3));
+      const double sacc = warp_sum(((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7])));
       if (lane == 0) partn[size_t(g) * (n + 1) + k] = sacc;
     }
     __syncthreads();
