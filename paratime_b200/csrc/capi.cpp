@@ -110,6 +110,7 @@ ptb_status ptb_context_destroy(ptb_context* ctx) {
     for (auto& st : ctx->aux)
       if (st) cudaStreamDestroy(st);
     ctx->flags.release();
+    ctx->driver_cache.reset();  // parareal work buffers
     ptb_release_blas(ctx);
     cudaStreamDestroy(ctx->own_stream);
     delete ctx;

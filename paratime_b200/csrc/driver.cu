@@ -114,6 +114,21 @@ __global__ void k_or_flags(int32_t* out, const int32_t* a, const int32_t* b, con
 
 }  // namespace
 
+// Work buffers reused by successive runs on one context (ptb_context::driver_cache).
+constexpr int kDriverBuffers = 56;
+struct DriverCache {
+  EnergyWork ew;
+  ProcWork pw;
+  DeviceBuffer bufs[kDriverBuffers];
+  DeviceBuffer corr_x, corr_y;
+  explicit DriverCache(ptb_context* c) : ew(c), pw(c) {}
+};
+
+DriverCache& driver_cache(ptb_context* ctx) {
+  if (!ctx->driver_cache) ctx->driver_cache = std::make_shared<DriverCache>(ctx);
+  return *static_cast<DriverCache*>(ctx->driver_cache.get());
+}
+
 struct Driver {
   ptb_context* ctx;
   const ptb_run_spec& s;
@@ -125,8 +140,9 @@ struct Driver {
   ptb_propagator* pf = nullptr;
   ptb_propagator* pc = nullptr;
   ptb_transfer* tr = nullptr;
-  EnergyWork ew;
-  ProcWork pw;
+  DriverCache& cache;
+  EnergyWork& ew;
+  ProcWork& pw;
   DevCorrector corr;
   ptb_phase_times* times = nullptr;
   // fine, own: states [a-1, b) -> index 0..L
@@ -139,10 +155,28 @@ struct Driver {
   std::vector<int32_t> ref_bad;
   const double* cf_dev = nullptr;  // coarse speed
 
-  Driver(ptb_context* c, const Comm* cm, const ptb_run_spec& spec) : ctx(c), s(spec), comm(cm), ew(c), pw(c) {
+  std::vector<DeviceBuffer*> owned() {
+    return {&cur_u, &cur_v, &nxt_u, &nxt_v, &ref_u, &ref_v, &fn_u, &fn_v, &fine_u, &fine_v, &fine2_u, &fine2_v,
+            &rf_u, &rf_v, &kn_u, &kn_v, &d_u, &d_v, &w_u, &w_v, &rik_u, &rik_v, &own_pay, &all_pay,
+            &ff, &cf, &wf, &bad, &sflags, &sums_own, &sums_all, &own_sc, &all_sc,
+            &rn_u, &rn_v, &ri_u, &ri_v, &init_u, &init_v, &init_cu, &init_cv,
+            &comp, &mean, &comp_old, &mean_old, &zold, &zw, &Zu, &Zv, &Fm, &Gm, &idx, &tmpc};
+  }
+
+  Driver(ptb_context* c, const Comm* cm, const ptb_run_spec& spec)
+      : ctx(c), s(spec), comm(cm), cache(driver_cache(c)), ew(cache.ew), pw(cache.pw) {
     if (!comm) comm = &single;
+    const std::vector<DeviceBuffer*> b = owned();
+    if (b.size() > size_t(kDriverBuffers)) fail(PTB_UNSUPPORTED, "driver cache too small");
+    for (size_t i = 0; i < b.size(); ++i) *b[i] = std::move(cache.bufs[i]);
+    corr.X = std::move(cache.corr_x);
+    corr.Y = std::move(cache.corr_y);
   }
   ~Driver() {
+    const std::vector<DeviceBuffer*> b = owned();
+    for (size_t i = 0; i < b.size(); ++i) cache.bufs[i] = std::move(*b[i]);
+    cache.corr_x = std::move(corr.X);
+    cache.corr_y = std::move(corr.Y);
     ptb_propagator_destroy(pf);
     ptb_propagator_destroy(pc);
     ptb_transfer_destroy(tr);

@@ -699,7 +699,7 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
 ProcWork::ProcWork(ptb_context* c) : ctx(c) {}
 ProcWork::~ProcWork() {
   for (auto& b : buf) b.release();
-  for (DeviceBuffer* b : {&QF, &RF, &QG, &RG, &Uh, &Vh, &PQ, &PR, &PU}) b->release();
+  for (DeviceBuffer* b : {&QF, &RF, &QG, &RG, &Uh, &Vh, &PQ, &PR, &PU, &SX, &SY}) b->release();
 }
 
 DevCorrector::~DevCorrector() {
@@ -944,12 +944,8 @@ void solve_from_scratch(ProcWork& w, DevCorrector& out, const double* F, const d
 void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, int rows, int cols, double tol) {
   check_tol(tol);
   ptb_context* ctx = w.ctx;
-  if (c.empty()) {
-    DevCorrector fresh;
-    solve_from_scratch(w, fresh, F, G, rows, cols, tol);
-    std::swap(c.X, fresh.X);
-    std::swap(c.Y, fresh.Y);
-    c.assign(fresh.rows, fresh.rank, fresh.S, fresh.tol);
+  if (c.empty()) {  // F, G are not read from c: solve straight into its buffers
+    solve_from_scratch(w, c, F, G, rows, cols, tol);
     return;
   }
   require(rows == c.rows, "update_svd: block rows do not match corrector");
@@ -994,9 +990,9 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
   hp_.mark("update: svd");
   const int keep = truncate_count(sigma, tol);
   // Uext = [U QF], Vext = [V QG]; X = Uext Uh[:, :keep], Y = Vext Vh[:, :keep]
-  DevCorrector nc;
-  double* X = static_cast<double*>(nc.X.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
-  double* Y = static_cast<double*>(nc.Y.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
+  // new factors into the spare buffers (U, V = c's factors are still read below), then swap
+  double* X = static_cast<double*>(w.SX.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
+  double* Y = static_cast<double*>(w.SY.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
   const double* Uh = static_cast<double*>(w.Uh.ptr);
   const double* Vh = static_cast<double*>(w.Vh.ptr);
   gemm(ctx, false, false, rows, keep, r, 1.0, U, rows, Uh, hp, 0.0, X, rows);
@@ -1007,10 +1003,10 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
   sigma.resize(size_t(keep));
   PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   hp_.mark("update: rotate");
-  std::swap(c.X, nc.X);
-  std::swap(c.Y, nc.Y);
+  std::swap(c.X, w.SX);
+  std::swap(c.Y, w.SY);
   c.assign(rows, keep, sigma, tol);
-  hp_.mark("update: assign/free");
+  hp_.mark("update: assign");
 }
 
 // out (rows x batch) = X (Y^T in)   (procrustes.cpp:82-86)

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <chrono>
@@ -73,10 +74,28 @@ struct HostProf {
   }
 };
 
-// Grow-only device scratch buffer.
+// Grow-only device scratch buffer; owns its allocation (move-only, freed on destruction).
 struct DeviceBuffer {
   void* ptr = nullptr;
   size_t bytes = 0;
+  DeviceBuffer() = default;
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : ptr(o.ptr), bytes(o.bytes) {
+    o.ptr = nullptr;
+    o.bytes = 0;
+  }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      release();
+      ptr = o.ptr;
+      bytes = o.bytes;
+      o.ptr = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DeviceBuffer() { release(); }
   void* get(size_t need);
   void release();
 };
@@ -95,6 +114,9 @@ struct ptb_context {
   cudaStream_t aux[2] = {nullptr, nullptr};  // host-batch pipeline streams (lazy)
   ptb::DeviceBuffer slotbuf[2][5];            // per pipeline slot: u, v, su, sv, flags
   void* cublas = nullptr;  // lazily created cublasHandle_t
+  // parareal driver work buffers kept between runs (driver.cu), so a repeated run neither
+  // reallocates nor synchronises on cudaMalloc/cudaFree; freed with the context
+  std::shared_ptr<void> driver_cache;
 };
 
 namespace ptb {

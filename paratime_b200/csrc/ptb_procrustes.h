@@ -29,6 +29,7 @@ struct ProcWork {
   DeviceBuffer buf[24];
   DeviceBuffer QF, RF, QG, RG, Uh, Vh;
   DeviceBuffer PQ, PR, PU;  // thin_svd preconditioning: Q, R of the QR and U of R^T
+  DeviceBuffer SX, SY;      // spare corrector factors: update_svd writes here, then swaps
   explicit ProcWork(ptb_context* c);
   ~ProcWork();
 };

@@ -1,0 +1,15 @@
+"""time_driver after torch has reserved (and cached) large device buffers, as in bench.py."""
+import os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paratime_b200 as B
+import workloads as W
+x = torch.empty(int(sys.argv[1]) * (1 << 27), dtype=torch.float64, device="cuda")  # GiB
+x.fill_(1.0)
+del x
+ctx = B.Context(0)
+for cfg in (1, 2):
+    spec, cf, cc, u0, v0 = W.CONFIGS[cfg]()
+    B.api.parareal_run(ctx, B.api.run_spec(**spec), cf, cc, u0, v0)
+    r = B.api.parareal_run(ctx, B.api.run_spec(**spec), cf, cc, u0, v0)
+    print(cfg, [round(v, 2) for v in r["times"]["iteration_ms"]], [round(v, 2) for v in r["times"]["procrustes_ms"]])
