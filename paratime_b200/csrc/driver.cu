@@ -63,6 +63,27 @@ __global__ void k_fill(size_t n, double v, double* a) {
 }
 
 // states b of `n` values where flags[b] (or any of the optional flag arrays) is set -> NaN
+// theta sweep step tail: d_n := NaN where w, coarse_next[n] or fine_next[n] is non-finite
+// (parareal.cpp:323-326), then R(next[n]) = R(fine_next[n]) + R(I(d_n)) = R(fine_next[n]) + d_n:
+// the interpolant passes through the coarse nodes (Fourier: W[0] = delta exactly; linear: t = 0),
+// bitwise for finite d, and a NaN d gives a NaN R(next) as in the reference.
+__global__ void k_sweep_tail(size_t n, const int32_t* f0, const int32_t* f1, const int32_t* f2, double* du,
+                             double* dv, const double* rfu, const double* rfv, double* ru, double* rv) {
+  const bool bad = (*f0) || (*f1) || (*f2);
+  GRID_STRIDE(e, n) {
+    double a = du[e], b = dv[e];
+    if (bad) {
+      a = b = CUDART_NAN;
+      du[e] = a;
+      dv[e] = b;
+    }
+    if (ru) {
+      ru[e] = rfu[e] + a;
+      rv[e] = rfv[e] + b;
+    }
+  }
+}
+
 __global__ void k_nan_where(size_t n, size_t batch, const int32_t* f0, const int32_t* f1, const int32_t* f2,
                             double* u, double* v) {
   GRID_STRIDE(e, n * batch) {
@@ -591,16 +612,13 @@ struct Driver {
         corrected_batch(c, false, 1, ru, rv, nullptr, nullptr, zwp, mw);
         assemble_d(c, zwp, zo + (n - 1) * size_t(c.rank), mw, mo + (n - 1), du, dv);
       }
-      // NaN when w, coarse_next[n] or fine_next[n] is non-finite (parareal.cpp:323-326)
-      nan_where(nc, 1, wfl + n, fl(cf) + (n - 1), fl(ff) + (n - 1), du, dv);
-      // R(next[n]) = R(fine_next[n]) + R(I(d_n))
-      if (n < N) {
-        interpolate_at_coarse_nodes(tr, 1, du, static_cast<double*>(ri_u.ptr));
-        interpolate_at_coarse_nodes(tr, 1, dv, static_cast<double*>(ri_v.ptr));
-        k_add<<<blocks(ctx, nc), 256, 0, st()>>>(nc, slot(rf_u, n, nc), static_cast<double*>(ri_u.ptr), ru);
-        k_add<<<blocks(ctx, nc), 256, 0, st()>>>(nc, slot(rf_v, n, nc), static_cast<double*>(ri_v.ptr), rv);
-        PTB_LAUNCH_CHECK(ctx);
-      }
+      // NaN flags (parareal.cpp:323-326) and R(next[n]) = R(fine_next[n]) + d_n, one launch
+      const bool more = n < N;
+      k_sweep_tail<<<blocks(ctx, nc), 256, 0, st()>>>(nc, wfl + n, fl(cf) + (n - 1), fl(ff) + (n - 1), du, dv,
+                                                      more ? slot(rf_u, n, nc) : nullptr,
+                                                      more ? slot(rf_v, n, nc) : nullptr, more ? ru : nullptr,
+                                                      more ? rv : nullptr);
+      PTB_LAUNCH_CHECK(ctx);
     }
   }
 

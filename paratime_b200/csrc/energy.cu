@@ -137,15 +137,28 @@ __device__ double block_sum(double x) {
   return r;
 }
 
+// mean_u partials: grid (P, batch); block p sums the points p, p + P*256, ... of its state, so
+// the partial layout (and the result) depends only on n and P = state_sum_parts(n)
 __global__ void __launch_bounds__(256) k_state_sum(int n, const double* f, size_t sstride, const int* index,
-                                                   double* out) {
-  const size_t src = index ? size_t(index[blockIdx.x]) : blockIdx.x;
+                                                   double* part) {
+  const size_t b = blockIdx.y;
+  const size_t src = index ? size_t(index[b]) : b;
   const double* F = f + src * sstride;
   double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += 256) acc += F[i];
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) acc += F[i];
   const double s = block_sum<256>(acc);
-  if (threadIdx.x == 0) out[blockIdx.x] = s;
+  if (threadIdx.x == 0) part[b * gridDim.x + blockIdx.x] = s;
 }
+
+__global__ void k_state_sum_final(size_t batch, int P, const double* part, double* out) {
+  for (size_t b = blockIdx.x * size_t(blockDim.x) + threadIdx.x; b < batch; b += size_t(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < P; ++q) acc += part[b * P + q];
+    out[b] = acc;
+  }
+}
+
+int state_sum_parts(int n) { return std::max(1, std::min(64, n / 4096)); }
 
 // complex staging for spectral maps
 __global__ void k_real_to_complex(size_t total, int n, const double* src, size_t sstride, const int* index,
@@ -470,7 +483,11 @@ void energy_components(EnergyWork& w, const ptb_grid& g, int scheme, size_t batc
     PTB_LAUNCH_CHECK(ctx);
   }
   if (mean) {
-    k_state_sum<<<unsigned(batch), 256, 0, st>>>(n, u, sstride, index, mean);
+    const int P = state_sum_parts(n);
+    double* part = static_cast<double*>(w.buf[8].get(batch * P * sizeof(double)));
+    k_state_sum<<<dim3(unsigned(P), unsigned(batch)), 256, 0, st>>>(n, u, sstride, index, part);
+    PTB_LAUNCH_CHECK(ctx);
+    k_state_sum_final<<<unsigned(std::min<size_t>((batch + 255) / 256, 1024)), 256, 0, st>>>(batch, P, part, mean);
     PTB_LAUNCH_CHECK(ctx);
   }
 }

@@ -6,7 +6,7 @@ namespace ptb {
 // Scratch owned by whoever runs energy-map work (driver, C ABI calls).
 struct EnergyWork {
   ptb_context* ctx = nullptr;
-  DeviceBuffer buf[8];
+  DeviceBuffer buf[9];  // [8]: mean_u partials
   explicit EnergyWork(ptb_context* c) : ctx(c) {}
   ~EnergyWork();
 };
