@@ -40,8 +40,10 @@ namespace {
 constexpr int QR_THREADS = 1024;
 
 struct QrArgs {
-  double* A;  // m x n column-major, lda = m
+  double* A;  // m x n column-major, leading dimension lda (>= m)
   int m, n;
+  int lda;
+  int pivot;  // 0: no column pivoting (panels of the blocked QR)
   double drop_tol;
   double* tau;     // n
   int* perm;       // n (pivoted column j = original column perm[j])
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
   const int rows_per = (m + G - 1) / G;
   const int r0 = min(m, g * rows_per), r1 = min(m, r0 + rows_per);
   double* A = a.A;
-  auto col = [&](int k) { return A + size_t(k) * m; };
+  auto col = [&](int k) { return A + size_t(k) * a.lda; };
   for (int k = warp; k < n; k += nwarps) {  // initial squared column norms, per CTA
     double sacc = 0.0;
     for (int i = r0 + lane; i < r1; i += 32) sacc += col(k)[i] * col(k)[i];
@@ -109,12 +111,14 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
     }
     __syncthreads();
     int p = j;  // max remaining norm, first index on ties (idamax)
-    double best = nrm[j];
-    for (int k = j + 1; k < n; ++k)
-      if (nrm[k] > best) {
-        best = nrm[k];
-        p = k;
-      }
+    if (a.pivot) {
+      double best = nrm[j];
+      for (int k = j + 1; k < n; ++k)
+        if (nrm[k] > best) {
+          best = nrm[k];
+          p = k;
+        }
+    }
     if (p != j) {
       for (int i = r0 + tid; i < r1; i += QR_THREADS) {
         const double t = col(j)[i];
@@ -261,6 +265,23 @@ __global__ void __launch_bounds__(256) k_wy_larft(const double* S, const double*
     }
     if (threadIdx.x == 0) T[size_t(j) * k + j] = tj;
     __syncthreads();
+  }
+}
+
+// blocked QR helpers: a panel's unit lower-trapezoidal reflectors (rows c0.., ld lda) into V
+// (same offsets, ld lda), and the upper triangle of the leading n x n block.
+__global__ void k_panel_v(const double* A, int lda, int mp, int w, double* V) {
+  const size_t total = size_t(mp) * w;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const int c = int(e / mp), i = int(e - size_t(c) * mp);
+    V[size_t(c) * lda + i] = i < c ? 0.0 : (i == c ? 1.0 : A[size_t(c) * lda + i]);
+  }
+}
+
+__global__ void k_triu(const double* A, int lda, int n, double* R) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int c = e / n, i = e - c * n;
+    R[e] = i <= c ? A[size_t(c) * lda + i] : 0.0;
   }
 }
 
@@ -699,7 +720,8 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
 ProcWork::ProcWork(ptb_context* c) : ctx(c) {}
 ProcWork::~ProcWork() {
   for (auto& b : buf) b.release();
-  for (DeviceBuffer* b : {&QF, &RF, &QG, &RG, &Uh, &Vh, &PQ, &PR, &PU, &SX, &SY}) b->release();
+  for (DeviceBuffer* b : {&QF, &RF, &QG, &RG, &Uh, &Vh, &PQ, &PR, &PU, &SX, &SY, &BA, &BV, &BT, &BR, &BQ2})
+    b->release();
 }
 
 DevCorrector::~DevCorrector() {
@@ -720,7 +742,8 @@ void DevCorrector::assign(int rows_, int rank_, const std::vector<double>& s, do
 
 // truncated_qr (procrustes.cpp:34-46): Q (m x keep) and R (keep x n, un-pivoted) in
 // caller buffers; A is copied (the input is not modified).  Returns keep.
-int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb, DeviceBuffer& Rb) {
+int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb,
+                        DeviceBuffer& Rb) {
   ptb_context* ctx = w.ctx;
   cudaStream_t st = ctx->stream;
   const int k = std::min(m, n);
@@ -741,7 +764,7 @@ int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol,
   if (rows_per > 16384) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
   smem += rows_per * sizeof(double);
   double* part = static_cast<double*>(w.buf[4].get(size_t(2) * G * (n + 1) * sizeof(double)));
-  QrArgs qa{A, m, n, drop_tol, tau, perm, part, keep_d, betas};
+  QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, part, keep_d, betas};
   void* args[] = {&qa};
   PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qrcp), G, QR_THREADS, args, smem, st));
@@ -809,6 +832,94 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
     PTB_CUDA_CHECK(cudaStreamSynchronize(st));
     std::fprintf(stderr, "[ptb prof] jacobi %d x %d: %g sweeps\n", r, c, sweeps);
   }
+}
+
+// Tall blocked variant of truncated_qr (m >= 8n): (1) unpivoted Householder QR A = Q1 R1 in
+// panels of QB columns -- each panel factored by k_qrcp without pivoting on L2-resident data,
+// the trailing matrix updated with compact WY (three DGEMMs); (2) the pivoted QR of the small
+// R1 (n x n) by truncated_qr_direct: R1 P = Q2 R2 with the reference's keep rule -- column norms
+// are invariant under Q1, so the pivot order and |R_jj| are those of A's own column-pivoted QR
+// (procrustes.cpp:37) up to rounding; (3) Q = Q1 [Q2; 0], applying the panels in reverse.
+constexpr int QB = 32;
+
+int truncated_qr_blocked(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb,
+                         DeviceBuffer& Rb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  double* A = static_cast<double*>(w.BA.get(size_t(m) * n * sizeof(double)));
+  double* V = static_cast<double*>(w.BV.get(size_t(m) * n * sizeof(double)));
+  PTB_CUDA_CHECK(cudaMemcpyAsync(A, A_in, size_t(m) * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  const int P = (n + QB - 1) / QB;
+  double* tau = static_cast<double*>(w.BT.get((size_t(n) + size_t(P) * QB * QB + 3 * size_t(QB) * n) *
+                                              sizeof(double)));
+  double* Tall = tau + n;               // P x (QB x QB)
+  double* W1 = Tall + size_t(P) * QB * QB;  // QB x n
+  double* W2 = W1 + size_t(QB) * n;         // QB x n
+  double* S = W2 + size_t(QB) * n;          // QB x QB (<= QB x n)
+  int* perm = static_cast<int*>(w.buf[2].get(size_t(n) * sizeof(int)));
+  int* keep_d = static_cast<int*>(w.buf[3].get(sizeof(int)));
+  double* betas = static_cast<double*>(w.buf[5].get(size_t(n) * sizeof(double)));
+  for (int p = 0; p < P; ++p) {
+    const int c0 = p * QB, wd = std::min(QB, n - c0), mp = m - c0, nr = n - c0 - wd;
+    double* Ap = A + size_t(c0) * m + c0;
+    size_t smem = (QR_THREADS + 2 * size_t(wd)) * sizeof(double);
+    const int G = qr_grid(ctx, mp, smem + 16384 * sizeof(double), reinterpret_cast<const void*>(k_qrcp));
+    const size_t rows_per = (size_t(mp) + G - 1) / G;
+    if (rows_per > 16384) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
+    smem += rows_per * sizeof(double);
+    double* part = static_cast<double*>(w.buf[4].get(size_t(2) * G * (wd + 1) * sizeof(double)));
+    QrArgs qa{Ap, mp, wd, m, 0, -1.0, tau + c0, perm, part, keep_d, betas};
+    void* args[] = {&qa};
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qrcp), G, QR_THREADS, args, smem, st));
+    PTB_LAUNCH_CHECK(ctx);
+    double* Vp = V + size_t(c0) * m + c0;
+    k_panel_v<<<unsigned(std::min<size_t>((size_t(mp) * wd + 255) / 256, size_t(ctx->num_sms) * 16)), 256, 0, st>>>(
+        Ap, m, mp, wd, Vp);
+    PTB_LAUNCH_CHECK(ctx);
+    double* Tp = Tall + size_t(p) * QB * QB;
+    gemm(ctx, true, false, wd, wd, mp, 1.0, Vp, m, Vp, m, 0.0, S, wd);  // S = Vp^T Vp
+    k_wy_larft<<<1, 256, size_t(wd) * sizeof(double), st>>>(S, tau + c0, wd, Tp);
+    PTB_LAUNCH_CHECK(ctx);
+    if (nr > 0) {  // A_trail -= Vp (Tp^T (Vp^T A_trail))
+      double* At = A + size_t(c0 + wd) * m + c0;
+      gemm(ctx, true, false, wd, nr, mp, 1.0, Vp, m, At, m, 0.0, W1, wd);
+      gemm(ctx, true, false, wd, nr, wd, 1.0, Tp, wd, W1, wd, 0.0, W2, wd);
+      gemm(ctx, false, false, mp, nr, wd, -1.0, Vp, m, W2, wd, 1.0, At, m);
+    }
+  }
+  // R1 and its pivoted QR
+  double* R1 = static_cast<double*>(w.BR.get(size_t(n) * n * sizeof(double)));
+  k_triu<<<unsigned(std::max(1, std::min(1024, (n * n + 255) / 256))), 256, 0, st>>>(A, m, n, R1);
+  PTB_LAUNCH_CHECK(ctx);
+  const int kq = truncated_qr_direct(w, R1, n, n, drop_tol, w.BQ2, Rb);
+  double* Q = static_cast<double*>(Qb.get(std::max<size_t>(1, size_t(m) * kq) * sizeof(double)));
+  if (kq == 0) return 0;
+  // Q = Q1 [Q2; 0]
+  PTB_CUDA_CHECK(cudaMemsetAsync(Q, 0, size_t(m) * kq * sizeof(double), st));
+  PTB_CUDA_CHECK(cudaMemcpy2DAsync(Q, size_t(m) * sizeof(double), w.BQ2.ptr, size_t(n) * sizeof(double),
+                                   size_t(n) * sizeof(double), kq, cudaMemcpyDeviceToDevice, st));
+  double* Y1 = W1;  // QB x kq (kq <= n)
+  double* Y2 = W2;
+  for (int p = P - 1; p >= 0; --p) {
+    const int c0 = p * QB, wd = std::min(QB, n - c0), mp = m - c0;
+    const double* Vp = V + size_t(c0) * m + c0;
+    const double* Tp = Tall + size_t(p) * QB * QB;
+    double* Xp = Q + c0;  // rows c0.., ld m
+    gemm(ctx, true, false, wd, kq, mp, 1.0, Vp, m, Xp, m, 0.0, Y1, wd);
+    gemm(ctx, false, false, wd, kq, wd, 1.0, Tp, wd, Y1, wd, 0.0, Y2, wd);
+    gemm(ctx, false, false, mp, kq, wd, -1.0, Vp, m, Y2, wd, 1.0, Xp, m);
+  }
+  return kq;
+}
+
+int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb, DeviceBuffer& Rb) {
+  static const int env = [] {  // PTB_QR=direct forces the unblocked pivoted kernel
+    const char* e = std::getenv("PTB_QR");
+    return e && std::string(e) == "direct" ? 1 : 0;
+  }();
+  if (env == 0 && n > QB && m >= 8 * n) return truncated_qr_blocked(w, A_in, m, n, drop_tol, Qb, Rb);
+  return truncated_qr_direct(w, A_in, m, n, drop_tol, Qb, Rb);
 }
 
 // thin SVD of M (p x q): U (p x k), sigma (k, host), V (q x k), k = min(p, q).

@@ -30,6 +30,7 @@ struct ProcWork {
   DeviceBuffer QF, RF, QG, RG, Uh, Vh;
   DeviceBuffer PQ, PR, PU;  // thin_svd preconditioning: Q, R of the QR and U of R^T
   DeviceBuffer SX, SY;      // spare corrector factors: update_svd writes here, then swaps
+  DeviceBuffer BA, BV, BT, BR, BQ2;  // blocked tall QR: work copy, reflectors, tau/T/W, R1, Q2
   explicit ProcWork(ptb_context* c);
   ~ProcWork();
 };
