@@ -388,6 +388,7 @@ ptb_status ptb_transfer_destroy(ptb_transfer* t) {
     if (t->wy) cudaFree(t->wy);
     if (t->mx) cudaFree(t->mx);
     if (t->my) cudaFree(t->my);
+    transfer_release(t);
     t->nodes_half.release();
     delete t;
   });

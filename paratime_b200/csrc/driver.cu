@@ -408,6 +408,7 @@ struct Driver {
                 int* diverged, double* states_out) {
     double* su = static_cast<double*>(su_b.ptr);
     double* sv = static_cast<double*>(sv_b.ptr);
+    HostProf hp_(st());
     int32_t* f = fl(sflags);
     PTB_CUDA_CHECK(cudaMemsetAsync(f, 0, (L + 1) * sizeof(int32_t), st()));
     k_state_flags<<<dim3(std::min(64u, blocks(ctx, nf)), unsigned(L + 1)), 256, 0, st()>>>(nf, su, sv, nf, f);
@@ -416,8 +417,10 @@ struct Driver {
     PTB_CUDA_CHECK(cudaMemsetAsync(own, 0, chunk * 5 * sizeof(double), st()));
     if (L) {
       double* tmp = dalloc<double>(sums_all, L * 4);
+      hp_.mark("finalize: flags");
       pair_energy_sums(ew, fg, s.metric_scheme, L, su + nf, sv + nf, nf, RU(a), RV(a), nf, ptb_propagator_speed(pf),
                        tmp);
+      hp_.mark("finalize: error sums");
       // pack [flag, s0..s3] per own slice
       PTB_CUDA_CHECK(cudaMemcpy2DAsync(own + 1, 5 * sizeof(double), tmp, 4 * sizeof(double), 4 * sizeof(double), L,
                                        cudaMemcpyDeviceToDevice, st()));
@@ -711,15 +714,18 @@ struct Driver {
       copy(NV(0), fl_init_v(), nf);
     }
     if (!L) return;
+    HostProf hp_(st());
     double* iu = dalloc<double>(fine_u, L * nf);
     double* iv = dalloc<double>(fine_v, L * nf);
     if (theta) {
       interpolate_fields(tr, L, slot(d_u, a, nc), iu);
       interpolate_fields(tr, L, slot(d_v, a, nc), iv);
+      hp_.mark("combine: interpolate");
       if (additive) {
         k_add<<<blocks(ctx, L * nf), 256, 0, st()>>>(L * nf, FU(a), iu, NU(a));
         k_add<<<blocks(ctx, L * nf), 256, 0, st()>>>(L * nf, FV(a), iv, NV(a));
         PTB_LAUNCH_CHECK(ctx);
+        hp_.mark("combine: add");
         if (a == 1) {  // next[1] = fine_next[1] exactly
           copy(NU(1), FU(1), nf);
           copy(NV(1), FV(1), nf);

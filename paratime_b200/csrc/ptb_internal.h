@@ -154,6 +154,10 @@ struct ptb_transfer {
   // dense forms of the same maps for the GEMM path (2D, large grids): mx = cx x fx, my = fy x cy
   double* mx = nullptr;
   double* my = nullptr;
+  // FFT route (2D Fourier, large grids): cuFFT plans for one field (coarse D2Z, fine Z2D) and
+  // the two spectra; plans are created lazily (int handles, 0 = none)
+  int fft_fwd = 0, fft_inv = 0;
+  ptb::DeviceBuffer spec_c, spec_f;
   ptb::DeviceBuffer nodes_half;  // scratch of interpolate_at_coarse_nodes
 };
 
@@ -192,6 +196,7 @@ void nonfinite(ptb_context* ctx, size_t n, size_t batch, const double* f, int32_
 
 // transfer.cu
 void transfer_init(ptb_transfer* t);
+void transfer_release(ptb_transfer* t);  // cuFFT plans
 void restrict_fields(ptb_transfer* t, size_t batch, const double* fine, double* coarse);
 void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, double* fine);
 // R(I(coarse)): the interpolant's values at the coarse nodes, bitwise equal to restricting

@@ -23,10 +23,18 @@
 //   My[q*r + rem][j] = W[rem][(q - j) mod n]   (y: out = My . half)
 // issued as cuBLAS DGEMMs of one fixed shape per field, so each slice's result does not
 // depend on how many slices a call (or a rank) carries.
+// Default on large 2D grids is the reference's own construction done with cuFFT (fft.cpp wraps
+// FFTW): 2D D2Z of the coarse field, the zero-padded spectrum (Nyquist bins split 1/2-1/2 per
+// axis as grid.cpp:161-166; the x split comes from the implicit Hermitian mirror of the
+// half-spectrum), 2D Z2D on the fine grid.  The 2D DFT is separable, so this equals the
+// reference's x-then-y line interpolation; plans are for one field, executed per field (same
+// determinism argument as the DGEMMs).  Memory-bound instead of 2 n_c flops per output point.
 
 #include <cmath>
 #include <cstdlib>
 #include <vector>
+
+#include <cufft.h>
 
 #include "ptb_internal.h"
 #include "ptb_procrustes.h"  // gemm (cuBLAS DGEMM on the context stream)
@@ -211,6 +219,12 @@ void transfer_init(ptb_transfer* t) {
   if (t->coarse.dim == 2) t->wy = upload(g.cy, g.ry);
 }
 
+void transfer_release(ptb_transfer* t) {
+  if (t->fft_fwd) cufftDestroy(cufftHandle(t->fft_fwd));
+  if (t->fft_inv) cufftDestroy(cufftHandle(t->fft_inv));
+  t->fft_fwd = t->fft_inv = 0;
+}
+
 void restrict_fields(ptb_transfer* t, size_t batch, const double* fine, double* coarse) {
   ptb_context* ctx = t->ctx;
   const TGeom g = geom(t);
@@ -249,6 +263,99 @@ bool use_gemm(const TGeom& g) {
   return ok && (env == 1 || size_t(g.fy) * g.fx >= size_t(512) * 512);
 }
 
+__global__ void k_pad_spectrum(int cy, int cx, int fy, int fx, double scale, const double2* __restrict__ in_all,
+                               double2* __restrict__ out_all) {
+  const int hc = cx / 2 + 1, hf = fx / 2 + 1;
+  const size_t total = size_t(fy) * hf;
+  const double2* __restrict__ in = in_all + size_t(blockIdx.y) * cy * hc;
+  double2* __restrict__ out = out_all + size_t(blockIdx.y) * total;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const int ky = int(e / hf), kx = int(e - size_t(ky) * hf);
+    double2 v = make_double2(0.0, 0.0);
+    // source row: fine row ky <-> signed frequency sy (coarse row sy mod cy)
+    int sy;
+    double wgt = scale;
+    if (ky < (cy + 1) / 2) {
+      sy = ky;
+    } else if (ky > fy - (cy + 1) / 2) {
+      sy = ky - fy + cy;
+    } else if (cy % 2 == 0 && (ky == cy / 2 || ky == fy - cy / 2)) {
+      sy = cy / 2;  // Nyquist row split between +cy/2 and -cy/2
+      wgt *= 0.5;
+    } else {
+      sy = -1;
+    }
+    if (sy >= 0 && kx <= cx / 2) {
+      if (cx % 2 == 0 && kx == cx / 2) wgt *= 0.5;  // mirror (implicit) carries the other half
+      const double2 f = in[size_t(sy) * hc + kx];
+      v = make_double2(f.x * wgt, f.y * wgt);
+    }
+    out[e] = v;
+  }
+}
+
+void check_fft(cufftResult r, const char* what) {
+  if (r != CUFFT_SUCCESS) fail(PTB_CUDA, std::string("cuFFT ") + what + " failed (" + std::to_string(int(r)) + ")");
+}
+
+bool use_fft(const TGeom& g) {
+  static const int env = [] {
+    const char* e = std::getenv("PTB_INTERP_FFT");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (env == 0) return false;
+  const bool ok = g.cy > 1 && g.rx > 1 && g.ry > 1;
+  return ok && (env == 1 || size_t(g.fy) * g.fx >= size_t(1024) * 1024);
+}
+
+constexpr int FFT_CHUNK = 8;  // fields per cuFFT execution (fixed: a partial chunk is padded)
+
+void interpolate_fft(ptb_transfer* t, const TGeom& g, size_t batch, const double* coarse, double* fine) {
+  ptb_context* ctx = t->ctx;
+  cudaStream_t st = ctx->stream;
+  const int hc = g.cx / 2 + 1, hf = g.fx / 2 + 1;
+  const size_t nc = size_t(g.cy) * g.cx, nf = size_t(g.fy) * g.fx;
+  const size_t sc_n = size_t(g.cy) * hc, sf_n = size_t(g.fy) * hf;
+  if (!t->fft_fwd) {
+    cufftHandle f = 0, b = 0;
+    int nC[2] = {g.cy, g.cx}, nF[2] = {g.fy, g.fx};
+    check_fft(cufftPlanMany(&f, 2, nC, nullptr, 1, int(nc), nullptr, 1, int(sc_n), CUFFT_D2Z, FFT_CHUNK),
+              "plan D2Z");
+    check_fft(cufftPlanMany(&b, 2, nF, nullptr, 1, int(sf_n), nullptr, 1, int(nf), CUFFT_Z2D, FFT_CHUNK),
+              "plan Z2D");
+    t->fft_fwd = int(f);
+    t->fft_inv = int(b);
+  }
+  const cufftHandle f = cufftHandle(t->fft_fwd), b = cufftHandle(t->fft_inv);
+  check_fft(cufftSetStream(f, st), "set stream");
+  check_fft(cufftSetStream(b, st), "set stream");
+  double2* sc = static_cast<double2*>(t->spec_c.get(FFT_CHUNK * sc_n * sizeof(double2)));
+  double2* sf = static_cast<double2*>(t->spec_f.get(FFT_CHUNK * sf_n * sizeof(double2)));
+  const double scale = 1.0 / double(nc);
+  for (size_t i0 = 0; i0 < batch; i0 += FFT_CHUNK) {
+    const size_t cnt = std::min<size_t>(FFT_CHUNK, batch - i0);
+    const double* in = coarse + i0 * nc;
+    double* out = fine + i0 * nf;
+    double* stage_in = nullptr;
+    double* stage_out = nullptr;
+    if (cnt < FFT_CHUNK) {  // partial chunk: same plan on a zero-padded staging copy
+      stage_in = static_cast<double*>(ctx->scratch[2].get(FFT_CHUNK * nc * sizeof(double)));
+      stage_out = static_cast<double*>(ctx->scratch[3].get(FFT_CHUNK * nf * sizeof(double)));
+      PTB_CUDA_CHECK(cudaMemsetAsync(stage_in, 0, FFT_CHUNK * nc * sizeof(double), st));
+      PTB_CUDA_CHECK(cudaMemcpyAsync(stage_in, in, cnt * nc * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      in = stage_in;
+    }
+    // cuFFT's D2Z takes its input as non-const
+    check_fft(cufftExecD2Z(f, const_cast<double*>(in), reinterpret_cast<cufftDoubleComplex*>(sc)), "exec D2Z");
+    k_pad_spectrum<<<dim3(blocks_for(ctx, sf_n), FFT_CHUNK), 256, 0, st>>>(g.cy, g.cx, g.fy, g.fx, scale, sc, sf);
+    PTB_LAUNCH_CHECK(ctx);
+    check_fft(cufftExecZ2D(b, reinterpret_cast<cufftDoubleComplex*>(sf), stage_out ? stage_out : out), "exec Z2D");
+    ctx->launches.fetch_add(2, std::memory_order_relaxed);
+    if (stage_out)
+      PTB_CUDA_CHECK(cudaMemcpyAsync(out, stage_out, cnt * nf * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+}
+
 void interpolate_gemm(ptb_transfer* t, const TGeom& g, size_t batch, const double* coarse, double* fine) {
   ptb_context* ctx = t->ctx;
   if (!t->mx) {
@@ -277,6 +384,10 @@ void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, dou
   if (t->kind == PTB_INTERP_LINEAR || (g.rx == 1 && g.ry == 1)) {
     k_interp_linear<<<blocks_for(ctx, batch * nf), 256, 0, ctx->stream>>>(g, batch, coarse, fine);
     PTB_LAUNCH_CHECK(ctx);
+    return;
+  }
+  if (use_fft(g)) {
+    interpolate_fft(t, g, batch, coarse, fine);
     return;
   }
   if (use_gemm(g)) {
