@@ -1,7 +1,8 @@
 """The reference's own doctest suites, run unmodified against the B200 library.
 
 tests/refsuite/Makefile compiles /root/reference/proj/tests/test_{propagator,field_core,
-parareal}.cpp against include/paratime/*.hpp (the drop-in API) and libparatime_b200.so;
+parareal,energy_map}.cpp against include/paratime/*.hpp (the drop-in API) and libparatime_b200.so
+(test_energy_map's one Eigen use — a MatrixXd of stacked columns — through a test-only shim);
 the binaries are built in the development container (where /root/reference exists) and
 ship with the repo snapshot.  Each suite must pass in both propagator modes."""
 import os
@@ -13,7 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 BIN = Path(__file__).resolve().parent / "refsuite" / "_bin"
-SUITES = ["test_field_core", "test_propagator", "test_parareal"]
+SUITES = ["test_field_core", "test_propagator", "test_parareal", "test_energy_map"]
 
 
 @pytest.mark.parametrize("mode", ["fast", "exact"])
