@@ -54,7 +54,28 @@ def num(m, k):
     return x * scale
 
 
+def launches_only(argv):
+    """python scripts/ncu_summary.py launches NAME LAUNCH_CSV "command" -> profiles/NAME.md"""
+    name, path, command = argv[0], Path(argv[1]), argv[2]
+    agg, total, unit, n = launches(path)
+    lines = [f"# {name}: ncu launch list", "", f"Command: `{command}`", "",
+             f"`ncu --metrics gpu__time_duration.sum --clock-control none` — {n} launches, "
+             f"{total / 1e6:.1f} ms of kernel time (serialised, cold-cache: compare shares).", "",
+             f"| kernel | launches | total ({unit}) | mean ({unit}) | share |", "|---|---:|---:|---:|---:|"]
+    for kname, (cnt, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:40]:
+        short = kname if len(kname) < 90 else kname[:87] + "..."
+        lines.append(f"| `{short}` | {cnt} | {t:.1f} | {t / cnt:.1f} | {100 * t / total:.1f}% |")
+    out = ROOT / "profiles" / f"{name}.md"
+    out.write_text("\n".join(lines) + "\n")
+    print(out.read_text())
+
+
 def main():
+    import sys
+
+    if len(sys.argv) > 1 and sys.argv[1] == "launches":
+        launches_only(sys.argv[2:])
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("round", type=int)
     ap.add_argument("launch_csv", type=Path)
