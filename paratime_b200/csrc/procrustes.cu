@@ -236,6 +236,127 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
   if (g == 0 && tid == 0) *a.keep_out = keep;
 }
 
+// Unpivoted Householder QR of a tall panel (the blocked QR's panels) with ONE grid barrier per
+// column: column j+1's squared norm and its raw dot products with the trailing columns are
+// accumulated during column j's update pass (w_k = A_jk + scal * sum_{i>j} x_i A_ik needs only the
+// unscaled column), so the reduction, the reflector and the update of a column need no further
+// barrier.  Within a CTA, column j+1 is updated first, then (after a CTA barrier) every other
+// trailing column is updated and dotted with it in the same sweep.  Partials are double-buffered
+// by column parity.  Outputs as k_qrcp (LAPACK layout: R above, v below the diagonal, tau).
+struct PanelArgs {
+  double* A;
+  int m, n, lda;
+  double* tau;
+  double* part;  // [2][grid][n + 1]: dots (k), squared norm (n)
+};
+
+__global__ void __launch_bounds__(QR_THREADS) k_qr_panel(PanelArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sh[];  // wv[n] | vs[rows_per] | xs[rows_per]
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = QR_THREADS / 32;
+  const int m = a.m, n = a.n;
+  const int rows_per = (m + G - 1) / G;
+  const int r0 = min(m, g * rows_per), r1 = min(m, r0 + rows_per);
+  double* wv = sh;
+  double* vs = wv + n;
+  double* xs = vs + rows_per;
+  auto col = [&](int k) { return a.A + size_t(k) * a.lda; };
+  auto slot = [&](int j) { return a.part + size_t(j & 1) * G * (n + 1) + size_t(g) * (n + 1); };
+  // partials of column 0
+  {
+    double* P = slot(0);
+    const double* x = col(0);
+    for (int k = warp; k <= n; k += nwarps) {
+      double acc = 0.0;
+      if (k == n) {
+        for (int i = max(r0, 1) + lane; i < r1; i += 32) acc += x[i] * x[i];
+      } else if (k > 0) {
+        const double* ck = col(k);
+        for (int i = max(r0, 1) + lane; i < r1; i += 32) acc += x[i] * ck[i];
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) P[k] = acc;
+    }
+  }
+  for (int j = 0; j < n && j < m; ++j) {
+    grid.sync();
+    const double* Pj = a.part + size_t(j & 1) * G * (n + 1);
+    // reduce: squared norm below the diagonal (into wv[j]) and raw dots d_k (into wv[k], k > j)
+    for (int k = j + warp; k <= n; k += nwarps) {
+      if (k == j) continue;
+      double acc = 0.0;
+      for (int c = lane; c < G; c += 32) acc += __ldcg(&Pj[size_t(c) * (n + 1) + k]);
+      acc = warp_sum(acc);
+      if (lane == 0) wv[k == n ? j : k] = acc;
+    }
+    __syncthreads();
+    const double xnorm2 = wv[j];
+    const double alpha = __ldcg(&col(j)[j]);
+    const double xnorm = sqrt(xnorm2);
+    double beta, tau, scal;
+    if (xnorm == 0.0) {
+      beta = alpha;
+      tau = 0.0;
+      scal = 0.0;
+    } else {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (g == 0 && tid == 0) a.tau[j] = tau;
+    __syncthreads();  // every thread has read wv[j] before wv[k] are overwritten below
+    // w_k = A_jk + scal d_k (row j of column k, unchanged since the last pass)
+    for (int k = j + 1 + tid; k < n; k += QR_THREADS) wv[k] = __ldcg(&col(k)[j]) + scal * wv[k];
+    // v over own rows: 0 above j, 1 at j, scaled x below
+    for (int i = r0 + tid; i < r1; i += QR_THREADS) {
+      double x = 0.0;
+      if (i > j) {
+        x = col(j)[i] * scal;
+        col(j)[i] = x;
+      } else if (i == j) {
+        x = 1.0;
+      }
+      vs[i - r0] = x;
+    }
+    __syncthreads();
+    const int i0 = max(r0, j);
+    if (j + 1 < n) {
+      // column j+1 first: update, keep own rows in xs, squared norm below row j+1
+      double* c1 = col(j + 1);
+      const double tw1 = tau * wv[j + 1];
+      double nacc = 0.0;
+      for (int i = r0 + tid; i < r1; i += QR_THREADS) {
+        double x = c1[i];
+        if (i >= j) {
+          x -= tw1 * vs[i - r0];
+          c1[i] = x;
+        }
+        xs[i - r0] = x;
+        if (i > j + 1) nacc += x * x;
+      }
+      nacc = cta_reduce(nacc, sh + n + 2 * rows_per);  // red scratch after xs
+      __syncthreads();
+      double* Pn = slot(j + 1);
+      if (tid == 0) Pn[n] = nacc;
+      // other trailing columns: update and dot with the new column j+1 (rows > j+1)
+      for (int k = j + 2 + warp; k < n; k += nwarps) {
+        double* ck = col(k);
+        const double tw = tau * wv[k];
+        double acc = 0.0;
+        for (int i = i0 + lane; i < r1; i += 32) {
+          const double x = ck[i] - tw * vs[i - r0];
+          ck[i] = x;
+          if (i > j + 1) acc += xs[i - r0] * x;
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) Pn[k] = acc;
+      }
+    }
+    if (j >= r0 && j < r1 && tid == 0) col(j)[j] = beta;
+  }
+}
+
 // Blocked Q (compact WY, LAPACK dlarft/dorg2r order): H_1...H_k = I - V T V^T with V the unit
 // lower-trapezoidal reflector block and T upper triangular, so Q = E - V (T V1^T) with
 // E = [I_k; 0] and V1 the top k x k block of V.  Two DGEMMs replace k BLAS-2 sweeps.
@@ -862,16 +983,16 @@ int truncated_qr_blocked(ProcWork& w, const double* A_in, int m, int n, double d
   for (int p = 0; p < P; ++p) {
     const int c0 = p * QB, wd = std::min(QB, n - c0), mp = m - c0, nr = n - c0 - wd;
     double* Ap = A + size_t(c0) * m + c0;
-    size_t smem = (QR_THREADS + 2 * size_t(wd)) * sizeof(double);
-    const int G = qr_grid(ctx, mp, smem + 16384 * sizeof(double), reinterpret_cast<const void*>(k_qrcp));
+    const size_t smem0 = (size_t(wd) + QR_THREADS) * sizeof(double);
+    const int G = qr_grid(ctx, mp, smem0 + 2 * 8192 * sizeof(double), reinterpret_cast<const void*>(k_qr_panel));
     const size_t rows_per = (size_t(mp) + G - 1) / G;
-    if (rows_per > 16384) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
-    smem += rows_per * sizeof(double);
+    if (rows_per > 8192) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
+    const size_t smem = smem0 + 2 * rows_per * sizeof(double);
     double* part = static_cast<double*>(w.buf[4].get(size_t(2) * G * (wd + 1) * sizeof(double)));
-    QrArgs qa{Ap, mp, wd, m, 0, -1.0, tau + c0, perm, part, keep_d, betas};
-    void* args[] = {&qa};
-    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qrcp), G, QR_THREADS, args, smem, st));
+    PanelArgs pa{Ap, mp, wd, m, tau + c0, part};
+    void* args[] = {&pa};
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qr_panel), G, QR_THREADS, args, smem, st));
     PTB_LAUNCH_CHECK(ctx);
     double* Vp = V + size_t(c0) * m + c0;
     k_panel_v<<<unsigned(std::min<size_t>((size_t(mp) * wd + 255) / 256, size_t(ctx->num_sms) * 16)), 256, 0, st>>>(

@@ -1,0 +1,44 @@
+"""Subprocess helper for tests/test_gpu_qr.py: ptb_truncated_qr on seeded tall matrices (the
+QR path is chosen by PTB_QR, read once per process)."""
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
+import paratime_b200 as B
+
+
+def mats():
+    rng = np.random.default_rng(77)
+    out = []
+    for m, n, rank in [(4096, 40, 40), (6000, 64, 50), (20000, 100, 100), (3000, 33, 20), (8192, 96, 96)]:
+        a = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n))
+        a *= np.logspace(0, -6, n)[None, :]  # graded columns: pivoting matters
+        out.append(a)
+    return out
+
+
+def main(path):
+    ctx = B.Context(0)
+    lib = B.lib()
+    res = {}
+    for t, a in enumerate(mats()):
+        m, n = a.shape
+        A = torch.tensor(np.asfortranarray(a).ravel(order="F"), device="cuda")
+        Q = torch.zeros(m * n, dtype=torch.float64, device="cuda")
+        R = torch.zeros(n * n, dtype=torch.float64, device="cuda")
+        keep = C.c_size_t()
+        tol = 1e-14 * np.linalg.norm(a)
+        B.api.check(lib.ptb_truncated_qr(ctx.h, C.c_size_t(m), C.c_size_t(n), C.c_void_p(A.data_ptr()), C.c_double(tol),
+                                         C.c_void_p(Q.data_ptr()), C.c_void_p(R.data_ptr()), C.byref(keep)))
+        k = keep.value
+        res[f"A{t}"] = a
+        res[f"Q{t}"] = Q.cpu().numpy()[: m * k].reshape(k, m).T
+        res[f"R{t}"] = R.cpu().numpy()[: k * n].reshape(n, k).T
+        res[f"tol{t}"] = tol
+    np.savez(path, **res)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
