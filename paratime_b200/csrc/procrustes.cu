@@ -248,6 +248,7 @@ struct PanelArgs {
   int m, n, lda;
   double* tau;
   double* part;  // [2][grid][n + 1]: dots (k), squared norm (n)
+  double* rowb;  // [2][n]: row j of the panel as of the start of column j (A_jj = alpha, A_jk)
 };
 
 __global__ void __launch_bounds__(QR_THREADS) k_qr_panel(PanelArgs a) {
@@ -263,6 +264,11 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_panel(PanelArgs a) {
   double* xs = vs + rows_per;
   auto col = [&](int k) { return a.A + size_t(k) * a.lda; };
   auto slot = [&](int j) { return a.part + size_t(j & 1) * G * (n + 1) + size_t(g) * (n + 1); };
+  // row j is rewritten by its owner during column j's pass while other CTAs still need its
+  // values, so the owner publishes a copy (parity j & 1) before the barrier that precedes use
+  auto rowcopy = [&](int j) { return a.rowb + size_t(j & 1) * n; };
+  if (r0 == 0 && r1 > 0)
+    for (int k = tid; k < n; k += QR_THREADS) rowcopy(0)[k] = col(k)[0];
   // partials of column 0
   {
     double* P = slot(0);
@@ -292,7 +298,8 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_panel(PanelArgs a) {
     }
     __syncthreads();
     const double xnorm2 = wv[j];
-    const double alpha = __ldcg(&col(j)[j]);
+    const double* rowj = rowcopy(j);
+    const double alpha = __ldcg(&rowj[j]);
     const double xnorm = sqrt(xnorm2);
     double beta, tau, scal;
     if (xnorm == 0.0) {
@@ -306,8 +313,8 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_panel(PanelArgs a) {
     }
     if (g == 0 && tid == 0) a.tau[j] = tau;
     __syncthreads();  // every thread has read wv[j] before wv[k] are overwritten below
-    // w_k = A_jk + scal d_k (row j of column k, unchanged since the last pass)
-    for (int k = j + 1 + tid; k < n; k += QR_THREADS) wv[k] = __ldcg(&col(k)[j]) + scal * wv[k];
+    // w_k = A_jk + scal d_k
+    for (int k = j + 1 + tid; k < n; k += QR_THREADS) wv[k] = __ldcg(&rowj[k]) + scal * wv[k];
     // v over own rows: 0 above j, 1 at j, scaled x below
     for (int i = r0 + tid; i < r1; i += QR_THREADS) {
       double x = 0.0;
@@ -326,6 +333,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_panel(PanelArgs a) {
       double* c1 = col(j + 1);
       const double tw1 = tau * wv[j + 1];
       double nacc = 0.0;
+      double* rown = rowcopy(j + 1);
       for (int i = r0 + tid; i < r1; i += QR_THREADS) {
         double x = c1[i];
         if (i >= j) {
@@ -334,6 +342,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_panel(PanelArgs a) {
         }
         xs[i - r0] = x;
         if (i > j + 1) nacc += x * x;
+        if (i == j + 1) rown[j + 1] = x;
       }
       nacc = cta_reduce(nacc, sh + n + 2 * rows_per);  // red scratch after xs
       __syncthreads();
@@ -348,6 +357,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_panel(PanelArgs a) {
           const double x = ck[i] - tw * vs[i - r0];
           ck[i] = x;
           if (i > j + 1) acc += xs[i - r0] * x;
+          if (i == j + 1) rown[k] = x;
         }
         acc = warp_sum(acc);
         if (lane == 0) Pn[k] = acc;
@@ -989,7 +999,8 @@ int truncated_qr_blocked(ProcWork& w, const double* A_in, int m, int n, double d
     if (rows_per > 8192) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
     const size_t smem = smem0 + 2 * rows_per * sizeof(double);
     double* part = static_cast<double*>(w.buf[4].get(size_t(2) * G * (wd + 1) * sizeof(double)));
-    PanelArgs pa{Ap, mp, wd, m, tau + c0, part};
+    double* rowb = static_cast<double*>(w.buf[22].get(size_t(2) * wd * sizeof(double)));
+    PanelArgs pa{Ap, mp, wd, m, tau + c0, part, rowb};
     void* args[] = {&pa};
     PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qr_panel), G, QR_THREADS, args, smem, st));
@@ -1077,7 +1088,9 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
   double* U = static_cast<double*>(Ub.get(size_t(p) * k * sizeof(double)));
   double* Vo = static_cast<double*>(Vb.get(size_t(q) * k * sizeof(double)));
   if (precond_env && c >= 32) {
+    HostProf hp_(st);
     const int kq = truncated_qr(w, A, r, c, 0.0, w.PQ, w.PR);  // A = Q R, Q r x kq, R kq x c
+    hp_.mark("svd: precondition qr");
     double* Bt = static_cast<double*>(w.buf[6].get(size_t(r) * c * sizeof(double)));  // A no longer needed
     double* V = static_cast<double*>(w.buf[7].get(std::max<size_t>(1, size_t(kq) * kq) * sizeof(double)));
     double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
@@ -1090,6 +1103,7 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
                                                                                    kq, c, Bt);
       PTB_LAUNCH_CHECK(ctx);
       jacobi_core(w, Bt, c, kq, V, sg, tmp, order);  // Bt := U' (c x kq), V' (kq x kq)
+      hp_.mark("svd: jacobi");
       PTB_CUDA_CHECK(cudaMemcpyAsync(s_k.data(), sg, size_t(kq) * sizeof(double), cudaMemcpyDeviceToHost, st));
     }
     // left factor of A: Q V' (r x kq); right factor: U' (c x kq); columns kq..k-1 (sigma 0): zero
