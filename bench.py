@@ -27,6 +27,8 @@ from pathlib import Path
 
 import numpy as np
 
+from workloads import cfg5_medium, cfg5_pulses
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -191,7 +193,7 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also time the cfg5 grid sweep")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the cfg5 grid sweep")
     ap.add_argument("--no-parareal", action="store_true", help="skip the s/iteration measurement")
     args = ap.parse_args()
 
@@ -325,8 +327,8 @@ def main():
             line["cpu_baseline"] = cpu_baseline_sample(n)
             if parareal is not None:
                 line["cpu_baseline_parareal"] = cpu_parareal_iteration(2)
-        if args.sweep:
-            line["sweep"] = sweep(B, ctx, mode)
+        if not args.no_sweep:
+            line["cfg5_sweep"] = sweep(B, ctx, mode, tflops_peak, hbm_peak)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -463,32 +465,41 @@ def measure_e2e(B, prop, u_host, mode, steps, local, dist, world):
             "api": "ptb_propagate_batch_host (pinned host buffers, 2-stream chunked copies)"}
 
 
-def sweep(B, ctx, mode):
-    """cfg5 grid sweep (128^2 .. 4096^2), device-resident, FAST mode."""
+def sweep(B, ctx, mode, tflops_peak, hbm_peak):
+    """cfg5 grid sweep (the >= 60 % target is judged on every cfg5 grid at batch >= 64):
+    device-resident, FAST, 64 steps per slice, batch 64.  Per grid: updates/s, the launch plan,
+    and the binding-roofline fraction max(upd/s*17/FP64, upd/s*(40/s_f)/HBM) with s_f the steps
+    fused per HBM round trip of the plan (64 for the on-chip k_cluster, 8 per wavefront pass)."""
     import torch
 
     out = []
-    for n, batch in ((128, 512), (512, 256), (1024, 64), (4096, 16)):
-        c = medium(n, 7)
+    for n, batch in ((128, 64), (128, 512), (256, 64), (512, 64), (1024, 64), (2048, 64), (4096, 64)):
+        c = cfg5_medium(n)
         dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
         prop = B.Propagator(ctx, B.Grid((n, n), (1.0 / n, 1.0 / n)), c, dt, STEPS_PER_COUPLING)
-        u = torch.as_tensor(pulses(n, batch, 5), device="cuda")
+        u = torch.as_tensor(cfg5_pulses(n, batch), device="cuda")
         v = torch.zeros_like(u)
-        for _ in range(2):
+        for _ in range(3):
             prop.propagate(u, v, mode=mode)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        reps = 5
         e0.record()
-        reps = 3
         for _ in range(reps):
             prop.propagate(u, v, mode=mode)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        out.append({"grid": n, "batch": batch, "ms": ms, "updates_per_s": batch * n * n * STEPS_PER_COUPLING / (ms * 1e-3)})
+        ups = batch * n * n * STEPS_PER_COUPLING / (ms * 1e-3)
+        plan = prop.plan(batch, mode)
+        s_f = STEPS_PER_COUPLING if plan.startswith("k_cluster") or plan.startswith("k_small") else 8
+        f_fp64 = ups * FLOPS_PER_UPDATE / (tflops_peak * 1e12) if tflops_peak else None
+        f_hbm = ups * (40.0 / s_f) / (hbm_peak * 1e9)
+        out.append({"grid": n, "batch": batch, "ms": round(ms, 3), "updates_per_s": ups, "plan": plan,
+                    "fused_steps": s_f, "frac_fp64": f_fp64, "frac_hbm": f_hbm,
+                    "frac_binding": max(f_fp64 or 0.0, f_hbm)})
         del u, v, prop
     return out
-
 
 if __name__ == "__main__":
     main()

@@ -484,6 +484,7 @@ struct WaveArgs {
   int wu;                           // useful (output) columns per strip
   int rb;                           // output rows per row block
   int32_t* flags;                   // nonfinite flags (nullable)
+  int full = 0;                     // k_wave2: the strip is the whole periodic row (2W == nx)
 };
 
 // One iteration of the wavefront: level 0 loads row r0 = ystart+i (+ look-ahead row), levels
@@ -685,7 +686,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 }
 
 template <int S, int W, int PAR>
-__device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __restrict__ eR,
+__device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __restrict__ eR, const int mirror,
                                            const StepParams& p, double (&ulo)[S + 1][2], double (&uce)[S + 1][2],
                                            double (&vin)[S + 1][2], double (&kin)[S + 1][2], const double2 uu0,
                                            const double2 v0, const double2 k0, double2& out_u, double2& out_v) {
@@ -706,6 +707,8 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
     const double uc0 = uce[0][0], uc1 = uce[0][1];
     wL[0] = uu0.x;
     wR[0] = uu0.y;
+    if (mirror < 0) wR[-W] = uu0.y;  // full-width strip: periodic pads (thread W-1 / thread 0)
+    if (mirror > 0) wL[W] = uu0.x;
     const double vh0 = v0.x + bfast<true>(uc0, nl[0], uc1, uu0.x, ulo[0][0], k0.x, p);
     const double vh1 = v0.y + bfast<true>(uc1, uc0, nr[0], uu0.y, ulo[0][1], k0.y, p);
     up0 = fma(p.dt, vh0, uc0);
@@ -716,6 +719,8 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
     ck1 = k0.y;
     wL[lstride] = up0;
     wR[lstride] = up1;
+    if (mirror < 0) wR[lstride - W] = up1;
+    if (mirror > 0) wL[lstride + W] = up0;
     ulo[0][0] = uc0;
     ulo[0][1] = uc1;
     uce[0][0] = uu0.x;
@@ -750,6 +755,8 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
       ck1 = k1t;
       wL[(t + 1) * lstride] = up0;
       wR[(t + 1) * lstride] = up1;
+      if (mirror < 0) wR[(t + 1) * lstride - W] = up1;
+      if (mirror > 0) wL[(t + 1) * lstride + W] = up0;
     } else {
       out_u = make_double2(uc0, uc1);
       out_v = make_double2(vp0 + b0, vp1 + b1);
@@ -763,12 +770,16 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
 
 template <int S, int W>
 __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
-  constexpr int HXE = (S + 3) & ~1;  // even halo >= S + 1 (16-byte aligned pairs)
+  // even halo >= S + 1 (16-byte aligned pairs); none when the strip is the whole periodic row
+  const int HXE = a.full ? 0 : (S + 3) & ~1;
   constexpr int NL = S + 1;
   constexpr int UNROLL = 6, RING = 6;
   extern __shared__ double sm[];
   constexpr int T = W;
   const int j = threadIdx.x;
+  // full-width strip: thread W-1's right edge and thread 0's left edge are also stored in the
+  // pads of the opposite end, so x-neighbours wrap inside the CTA
+  const int mirror = !a.full ? 0 : (j == W - 1 ? -1 : (j == 0 ? 1 : 0));
   const int nx = a.p.nx, ny = a.p.ny;
   const int npts = nx * ny;
   const int x0 = blockIdx.y * a.wu;  // even
@@ -811,6 +822,8 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     uce[0][1] = ce.y;
     eL[0] = ce.x;  // parity 0, level 0
     eR[0] = ce.y;
+    if (mirror < 0) eR[-W] = ce.y;
+    if (mirror > 0) eL[W] = ce.x;
   }
   int ou = wrap(ystart + 1), ov = wrap(ystart), oo = wrap(ystart - S);
   auto adv = [npts, nx](int& o) {
@@ -841,9 +854,9 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
       issue((k + RING - 1) % RING);
       double2 out_u, out_v;
       if (k & 1)
-        wave2_iter<S, W, 1>(eL, eR, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
+        wave2_iter<S, W, 1>(eL, eR, mirror, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
       else
-        wave2_iter<S, W, 0>(eL, eR, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
+        wave2_iter<S, W, 0>(eL, eR, mirror, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
       if (col_out && i >= 2 * S && i < last_out) {
         *reinterpret_cast<double2*>(UO + oo) = out_u;
         *reinterpret_cast<double2*>(VO + oo) = out_v;
@@ -961,6 +974,7 @@ void small_dispatch(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, size_
 
 struct WavePlan {
   int W, wu, strips, rb, nrb;
+  int full = 0;  // k_wave2: one strip spanning the periodic row, no halo columns
 };
 
 // Choose strip width W (threads) and row-block height rb.  Cost model: per-SM work in
@@ -1052,9 +1066,15 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
   double best_cost = 1e300;
   int forceW = 0;
   if (const char* e = std::getenv("PTB_WAVE_W"); e && std::atoi(e) > 0) forceW = std::atoi(e);
-  for (int W : kWave2Widths) {
+  static const int full_env = [] {
+    const char* e = std::getenv("PTB_WAVE_FULL");
+    return e ? std::atoi(e) : 1;
+  }();
+  for (int W : kWave2Widths)
+   for (int full = 0; full < 2; ++full) {
     if (forceW && W != forceW) continue;
-    const int wu_max = (2 * W - 2 * HXE) & ~1;
+    if (full && (nx != 2 * W || !full_env)) continue;
+    const int wu_max = full ? nx : (2 * W - 2 * HXE) & ~1;
     if (wu_max < 16) continue;
     int occ = 0;
     const size_t smem = wave2_smem(S, W);
@@ -1062,8 +1082,8 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
     PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     PTB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W, smem));
     if (occ < 1) continue;
-    const int strips = (nx + wu_max - 1) / wu_max;
-    const int wu = (((nx + strips - 1) / strips) + 1) & ~1;
+    const int strips = full ? 1 : (nx + wu_max - 1) / wu_max;
+    const int wu = full ? nx : (((nx + strips - 1) / strips) + 1) & ~1;
     for (int div = 1;; div *= 2) {
       const int rb = (ny + div - 1) / div;
       if (div > 1 && rb < 2 * S) break;
@@ -1077,10 +1097,11 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
       const double warps = double(occ) * (W / 32.0);
       const double resident = double(std::min(ctas, slots)) / ctx->num_sms * (W / 32.0);
       const double eff = std::min(1.0, std::min(warps, resident) / 8.0);
-      const double cost = rounds * warps * (rb + 2.0 * S) / eff;
+      double cost = rounds * warps * (rb + 2.0 * S) / eff;
+      if (full && full_env == 2) cost *= 1e-6;  // PTB_WAVE_FULL=2 (tests): prefer full-row strips
       if (cost < best_cost) {
         best_cost = cost;
-        best = WavePlan{W, wu, strips, rb, nrb};
+        best = WavePlan{W, wu, strips, rb, nrb, full};
       }
       if (rb <= 1) break;
     }
@@ -1100,6 +1121,7 @@ void launch_wave2(ptb_context* ctx, cudaStream_t st, WaveArgs a, size_t batch) {
   const size_t smem = wave2_smem(S, pl.W);
   a.wu = pl.wu;
   a.rb = pl.rb;
+  a.full = pl.full;
   dim3 grid(static_cast<unsigned>(batch), pl.strips, pl.nrb);
   void* args[] = {&a};
   PTB_CUDA_CHECK(cudaLaunchKernel(wave2_kernel<S>(pl.W), grid, dim3(pl.W), args, smem, st));
@@ -1260,7 +1282,7 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
         case 2: pl = plan_wave2<2>(pr->ctx, p.ny, p.nx, batch); break;
         default: pl = plan_wave2<1>(pr->ctx, p.ny, p.nx, batch); break;
       }
-      d = "k_wave2<" + std::to_string(S) + "," + std::to_string(pl.W) + ">";
+      d = "k_wave2<" + std::to_string(S) + "," + std::to_string(pl.W) + ">" + (pl.full ? " full-row" : "");
       d += " grid " + std::to_string(batch) + "x" + std::to_string(pl.strips) + "x" + std::to_string(pl.nrb);
     } else {
       const WavePlan pl = plan_wave(pr->ctx, p.ny, p.nx, S, batch);

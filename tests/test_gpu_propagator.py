@@ -41,6 +41,8 @@ CASES = [
     (((64, 128), (1 / 64, 1 / 128)), 21, 3),    # k_cluster, cluster of 2
     (((256, 128), (1 / 256, 1 / 128)), 10, 2),  # k_cluster, cluster of 8
     (((32, 512), (1 / 32, 1 / 512)), 9, 2),     # k_cluster, cluster of 4, 4 chunks per row
+    (((64, 192), (1 / 64, 1 / 192)), 19, 2),    # k_wave2 full-row strip (W = 96), passes 8+8+2+1
+    (((40, 384), (1 / 40, 1 / 384)), 8, 3),     # k_wave2 full-row strip (W = 192)
 ]
 
 
