@@ -919,12 +919,16 @@ void launch_small(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, int thr
 
 // cluster size for k_cluster (0 = not applicable): smallest CS with ny % CS == 0 and at most
 // 4096 points (1024 threads x 4) per CTA
-int cluster_size(const StepParams& p, size_t n) {
+int cluster_size(const StepParams& p, size_t n, size_t batch) {
   static const int env = [] {
     const char* e = std::getenv("PTB_CLUSTER");
     return e ? std::atoi(e) : 1;
   }();
   if (env == 0 || p.dim != 2 || n <= 4096 || n > 32768 || p.nx % 128 != 0) return 0;
+  // measured crossover (128^2, scripts/sweep_w.py): the cluster kernel wins below ~128 slices
+  // (0.44e12 vs 0.31e12 at 64); with more slices the full-row wavefront fills the GPU without
+  // row splitting and wins (0.48e12 at 128, 0.61e12 at 512, 0.73e12 at 2048)
+  if (env == 1 && batch >= 128) return 0;
   // measured (scripts/sweep_w.py): ahead of k_wave2 up to clusters of 8 (128^2: 0.41-0.45e12
   // vs 0.27-0.42e12 upd/s); at 16 CTAs (256^2) the wavefront kernel is as fast or faster
   for (int cs : {2, 4, 8}) {
@@ -1241,7 +1245,7 @@ void propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double
     }
     return;
   }
-  if (const int cs = cluster_size(p, n)) {
+  if (const int cs = cluster_size(p, n, batch)) {
     SmallArgs a{p, int(n), int(steps), u, v, exact ? pr->c2 : pr->kx, flags};
     exact ? launch_cluster<true>(ctx, slot.stream, a, cs, batch) : launch_cluster<false>(ctx, slot.stream, a, cs, batch);
     return;
@@ -1261,7 +1265,7 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
   const char* m = exact ? "EXACT" : "FAST";
   if (batch == 0 || steps == 0) return "none";
   if (pr->n <= 4096) return std::string("k_small<") + m + "> x1 launch, one CTA per slice";
-  if (const int cs = cluster_size(p, pr->n))
+  if (const int cs = cluster_size(p, pr->n, batch))
     return std::string("k_cluster<") + m + "> x1 launch, cluster of " + std::to_string(cs) + " CTAs x " +
            std::to_string(CL_THREADS) + " threads per slice";
   if (p.dim != 2) return std::string("k_stream_drift/kick<") + m + "> 2 launches per step";
