@@ -35,7 +35,8 @@ typedef enum {
   PTB_DOMAIN = 3,           /* std::domain_error (energy_map.cpp:233)   */
   PTB_CUDA = 4,             /* CUDA runtime / cuBLAS failure            */
   PTB_NCCL = 5,             /* collective failure                       */
-  PTB_UNSUPPORTED = 6
+  PTB_UNSUPPORTED = 6,
+  PTB_CONFIG = 7            /* ConfigError (errors.hpp): malformed input file */
 } ptb_status;
 
 /* Grid (grid.hpp:16-38): dim 1 or 2; n[0]/h[0] = axis 0 (y in 2D, the only axis in 1D). */
@@ -176,6 +177,14 @@ ptb_status ptb_truncated_qr(ptb_context* ctx, size_t m, size_t n, const double* 
 /* thin SVD M (p x q) = U diag(S) V^T, k = min(p, q), S descending (S_host k values) */
 ptb_status ptb_thin_svd(ptb_context* ctx, size_t p, size_t q, const double* M_dev, double* U_dev, double* S_host,
                         double* V_dev);
+
+/* ---- speed-model text format (experiment.hpp:84-90, experiment.cpp:711-784) — host only ---- */
+/* Writes "ny nx dy dx" then ny rows of nx values (%.17g).  needed = bytes required incl. NUL;
+ * writes nothing when len < needed. */
+ptb_status ptb_speed_model_write(const ptb_grid* grid, const double* c, char* buf, size_t len, size_t* needed);
+/* Parses text; grid and (when cap >= points) c are filled; npoints = ny*nx.  PTB_CONFIG on
+ * malformed input (the reference's ConfigError, message in ptb_last_error()). */
+ptb_status ptb_speed_model_read(const char* text, ptb_grid* grid, double* c, size_t cap, size_t* npoints);
 
 /* ---- parareal drivers (parareal.hpp:60-79) -------------------------------------------- */
 typedef enum { PTB_PLAIN = 0, PTB_THETA = 1, PTB_CORRECTED_COARSE_ONLY = 2, PTB_OMEGA_IDENTITY = 3 } ptb_variant;

@@ -110,6 +110,7 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+
 int ref_laplacian(int dim, std::size_t n0, std::size_t n1, double h0, double h1, const double* f,
                   double* out) {
   return guarded([&] {

@@ -301,3 +301,4 @@ def parareal_run(spec: RunSpec, c_fine, c_coarse, u0, udot0, keep_states=False, 
                                   _p(ref) if ref is not None else None, C.byref(wall)))
     return dict(energy_err=ee, l2_err=l2, residual=res, rank=rank, diverged=div, states=states,
                 reference=ref, wall_ms=wall.value)
+

@@ -15,7 +15,7 @@ import numpy as np
 
 LIB = Path(__file__).resolve().parent / "libparatime_b200.so"
 
-OK, INVALID_ARGUMENT, DIVERGED, DOMAIN, CUDA_ERR, NCCL_ERR, UNSUPPORTED = range(7)
+OK, INVALID_ARGUMENT, DIVERGED, DOMAIN, CUDA_ERR, NCCL_ERR, UNSUPPORTED, CONFIG = range(8)
 FAST, EXACT = 0, 1
 FOURIER, LINEAR = 0, 1
 FD2, FD4, FD6, FD8, SPECTRAL = range(5)
@@ -227,6 +227,30 @@ class Transfer:
 
 def _dp(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def write_speed_model(grid: Grid, c) -> str:
+    """Speed-model text (experiment.hpp:90): "ny nx dy dx" header, ny rows of nx values (%.17g)."""
+    c = np.ascontiguousarray(c, dtype=np.float64).ravel()
+    need = C.c_size_t()
+    check(lib().ptb_speed_model_write(C.byref(grid.c()), _dp(c), None, C.c_size_t(0), C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(lib().ptb_speed_model_write(C.byref(grid.c()), _dp(c), buf, C.c_size_t(need.value), C.byref(need)))
+    return buf.value.decode()
+
+
+def read_speed_model(text: str):
+    """read_speed_model (experiment.hpp:86): (Grid, c as grid.shape); PtbError(CONFIG) on malformed
+    input, as the reference's ConfigError."""
+    g = _Grid()
+    npts = C.c_size_t()
+    raw = text.encode()
+    check(lib().ptb_speed_model_read(raw, C.byref(g), None, C.c_size_t(0), C.byref(npts)))
+    c = np.empty(npts.value)
+    check(lib().ptb_speed_model_read(raw, C.byref(g), _dp(c), C.c_size_t(npts.value), C.byref(npts)))
+    grid = Grid((int(g.n[0]),), (float(g.h[0]),)) if g.dim == 1 else Grid((int(g.n[0]), int(g.n[1])),
+                                                                           (float(g.h[0]), float(g.h[1])))
+    return grid, c.reshape(grid.shape)
 
 
 def energy_components(ctx: Context, grid: Grid, c_dev, scheme: int, u, udot):

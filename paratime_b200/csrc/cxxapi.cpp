@@ -11,6 +11,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <functional>
+#include <cstring>
+#include <sstream>
+#include <fstream>
+#include <cstdio>
 #include <istream>
 #include <ostream>
 #include <map>
@@ -21,6 +25,7 @@
 
 #include "paratime/energy_map.hpp"
 #include "paratime/errors.hpp"
+#include "paratime/speed_model.hpp"
 #include "paratime/grid.hpp"
 #include "paratime/parareal.hpp"
 #include "paratime/procrustes.hpp"
@@ -784,3 +789,136 @@ double speedup_full(double n_cpu, double iterations, double dt_fine, double dt_c
 }
 
 }  // namespace paratime
+
+// ---- speed-model text format (experiment.hpp:84-90; behaviour of experiment.cpp:711-784) ----
+namespace paratime {
+namespace {
+
+struct SpeedText {
+  std::size_t ny = 0, nx = 0;
+  double dy = 0.0, dx = 0.0;
+  std::vector<double> values;
+};
+
+std::string fmt17(double v) {  // experiment.cpp:19-23
+  char buf[40];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+
+SpeedText parse_speed(std::istream& is) {
+  SpeedText t;
+  long ny = 0, nx = 0;
+  if (!(is >> ny >> nx >> t.dy >> t.dx)) throw ConfigError("speed model: bad header (want: ny nx dy dx)");
+  if (ny < 1 || nx < 1) throw ConfigError("speed model: nonpositive shape");
+  if (!(t.dx > 0.0) || (ny > 1 && !(t.dy > 0.0))) throw ConfigError("speed model: nonpositive spacing");
+  t.ny = std::size_t(ny);
+  t.nx = std::size_t(nx);
+  t.values.resize(t.ny * t.nx);
+  for (double& v : t.values) {
+    if (!(is >> v)) throw ConfigError("speed model: truncated value table");
+    if (!(v > 0.0) || !std::isfinite(v))
+      throw ConfigError("speed model: wave speed entries must be positive and finite");
+  }
+  double extra;
+  if (is >> extra) throw ConfigError("speed model: trailing values beyond ny*nx");
+  return t;
+}
+
+SpeedField to_field(SpeedText t) {
+  if (t.nx < 4 || (t.ny > 1 && t.ny < 4))
+    throw ConfigError("speed model: too few points for a grid; resample to a target size");
+  if (t.ny == 1) return SpeedField(Grid({t.nx}, {t.dx}), std::move(t.values));
+  return SpeedField(Grid({t.ny, t.nx}, {t.dy, t.dx}), std::move(t.values));
+}
+
+}  // namespace
+
+SpeedField read_speed_model(std::istream& is) { return to_field(parse_speed(is)); }
+
+SpeedField ingest_speed_model(const std::string& path) {
+  std::ifstream is(path);
+  if (!is) throw ConfigError("cannot open speed model: " + path);
+  return read_speed_model(is);
+}
+
+SpeedField ingest_speed_model(const std::string& path, const Grid& target) {
+  std::ifstream is(path);
+  if (!is) throw ConfigError("cannot open speed model: " + path);
+  SpeedText t = parse_speed(is);
+  const std::size_t ty = target.dim() == 1 ? 1 : target.points(0);
+  const std::size_t tx = target.dim() == 1 ? target.points(0) : target.points(1);
+  if (target.dim() == 2 && t.ny == 1) throw ConfigError("speed model: 1D file cannot fill a 2D grid");
+  return SpeedField(target, bilinear_resample(t.values, t.ny, t.nx, ty, tx));
+}
+
+void write_speed_model(const SpeedField& field, std::ostream& os) {
+  const Grid& g = field.grid;
+  const std::size_t ny = g.dim() == 1 ? 1 : g.points(0);
+  const std::size_t nx = g.dim() == 1 ? g.points(0) : g.points(1);
+  const double dy = g.dim() == 1 ? 1.0 : g.spacing(0);
+  const double dx = g.dim() == 1 ? g.spacing(0) : g.spacing(1);
+  os << ny << " " << nx << " " << fmt17(dy) << " " << fmt17(dx) << "\n";
+  for (std::size_t iy = 0; iy < ny; ++iy) {
+    for (std::size_t ix = 0; ix < nx; ++ix) os << (ix ? " " : "") << fmt17(field.c[iy * nx + ix]);
+    os << "\n";
+  }
+}
+
+}  // namespace paratime
+
+namespace ptb {
+extern thread_local std::string g_last_error;  // capi.cpp (ptb_last_error)
+}
+
+namespace {
+// C ABI wrappers: ConfigError -> PTB_CONFIG, std::invalid_argument -> PTB_INVALID_ARGUMENT
+template <typename Fn>
+ptb_status host_guarded(Fn&& fn) {
+  try {
+    fn();
+    return PTB_OK;
+  } catch (const paratime::ConfigError& e) {
+    ptb::g_last_error = e.what();
+    return PTB_CONFIG;
+  } catch (const std::invalid_argument& e) {
+    ptb::g_last_error = e.what();
+    return PTB_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    ptb::g_last_error = e.what();
+    return PTB_UNSUPPORTED;
+  }
+}
+}  // namespace
+
+extern "C" ptb_status ptb_speed_model_write(const ptb_grid* grid, const double* c, char* buf, size_t len,
+                                            size_t* needed) {
+  return host_guarded([&] {
+    if (!grid || !c || !needed) throw std::invalid_argument("speed_model_write: null argument");
+    std::vector<std::size_t> n(grid->n, grid->n + grid->dim);
+    std::vector<double> h(grid->h, grid->h + grid->dim);
+    const paratime::Grid g(n, h);
+    const paratime::SpeedField f(g, std::vector<double>(c, c + g.size()));
+    std::ostringstream os;
+    paratime::write_speed_model(f, os);
+    const std::string t = os.str();
+    *needed = t.size() + 1;
+    if (buf && len >= t.size() + 1) std::memcpy(buf, t.c_str(), t.size() + 1);
+  });
+}
+
+extern "C" ptb_status ptb_speed_model_read(const char* text, ptb_grid* grid, double* c, size_t cap,
+                                           size_t* npoints) {
+  return host_guarded([&] {
+    if (!text || !grid || !npoints) throw std::invalid_argument("speed_model_read: null argument");
+    std::istringstream is(text);
+    const paratime::SpeedField f = paratime::read_speed_model(is);
+    grid->dim = f.grid.dim();
+    for (int a = 0; a < 2; ++a) {
+      grid->n[a] = a < f.grid.dim() ? f.grid.points(a) : 0;
+      grid->h[a] = a < f.grid.dim() ? f.grid.spacing(a) : 0.0;
+    }
+    *npoints = f.c.size();
+    if (c && cap >= f.c.size()) std::copy(f.c.begin(), f.c.end(), c);
+  });
+}
