@@ -933,11 +933,13 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
   cudaStream_t st = ctx->stream;
   JacobiArgs ja{A, V, r, c, sg, order, tmp, 40};
   const size_t smem = (size_t(r) * c + size_t(c) * c) * sizeof(double);
-  static const int jacobi_env = [] {  // PTB_JACOBI=single forces the one-CTA global-memory kernel
+  static const int jacobi_env = [] {  // PTB_JACOBI=single: one-CTA global-memory kernel; =coop: grid
     const char* e = std::getenv("PTB_JACOBI");
-    return e && std::string(e) == "single" ? 1 : 0;
+    if (e && std::string(e) == "single") return 1;
+    if (e && std::string(e) == "coop") return 2;
+    return 0;
   }();
-  if (smem <= 200 * 1024) {
+  if (smem <= 200 * 1024 && jacobi_env != 2) {
     PTB_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k_jacobi<true><<<1, 1024, smem, st>>>(ja);
     PTB_LAUNCH_CHECK(ctx);
