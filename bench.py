@@ -462,7 +462,7 @@ def measure_e2e(B, prop, u_host, mode, steps, local, dist, world):
     value = world * batch * n * n * STEPS_PER_COUPLING * steps / el
     return {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": int(2 * uh.numel() * 8),
             "d2h_bytes_per_step": int(2 * uh.numel() * 8 + batch * 4), "ms_per_step": el / steps * 1e3,
-            "api": "ptb_propagate_batch_host (pinned host buffers, 2-stream chunked copies)"}
+            "api": "ptb_propagate_batch_host (pinned host buffers, 3-stream chunked copies)"}
 
 
 def sweep(B, ctx, mode, tflops_peak, hbm_peak):

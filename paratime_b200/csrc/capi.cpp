@@ -111,6 +111,7 @@ ptb_status ptb_context_destroy(ptb_context* ctx) {
       if (st) cudaStreamDestroy(st);
     ctx->flags.release();
     ctx->driver_cache.reset();  // parareal work buffers
+    if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
     ptb_release_blas(ctx);
     cudaStreamDestroy(ctx->own_stream);
     delete ctx;
@@ -310,12 +311,20 @@ ptb_status ptb_propagate_batch_host(ptb_propagator* p, size_t batch, const doubl
     const size_t n = p->n, slice_bytes = n * sizeof(double);
     const size_t target = size_t(128) << 20;  // ~128 MiB of u per chunk
     size_t chunk = std::max<size_t>(1, target / slice_bytes);
-    if (batch > 1) chunk = std::min(chunk, (batch + 1) / 2);  // at least two chunks to overlap
+    if (batch > 1) chunk = std::min(chunk, (batch + 2) / 3);  // at least three chunks to overlap
     for (auto& st : ctx->aux)
       if (!st) PTB_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (flags_host && ctx->pinned_flags_n < batch) {
+      if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
+      ctx->pinned_flags = nullptr;
+      ctx->pinned_flags_n = 0;
+      PTB_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->pinned_flags), batch * sizeof(int32_t),
+                                   cudaHostAllocDefault));
+      ctx->pinned_flags_n = batch;
+    }
     for (size_t b0 = 0, c = 0; b0 < batch; b0 += chunk, ++c) {
       const size_t nb = std::min(chunk, batch - b0);
-      const int k = int(c % 2);
+      const int k = int(c % 3);
       cudaStream_t st = ctx->aux[k];
       auto& sb = ctx->slotbuf[k];
       double* du = static_cast<double*>(sb[0].get(chunk * slice_bytes));
@@ -332,9 +341,11 @@ ptb_status ptb_propagate_batch_host(ptb_propagator* p, size_t batch, const doubl
       PTB_CUDA_CHECK(cudaMemcpyAsync(u_out + b0 * n, du, nb * slice_bytes, cudaMemcpyDeviceToHost, st));
       PTB_CUDA_CHECK(cudaMemcpyAsync(v_out + b0 * n, dv, nb * slice_bytes, cudaMemcpyDeviceToHost, st));
       if (flags_host)
-        PTB_CUDA_CHECK(cudaMemcpyAsync(flags_host + b0, df, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        PTB_CUDA_CHECK(
+            cudaMemcpyAsync(ctx->pinned_flags + b0, df, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     }
     for (auto& st : ctx->aux) PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (flags_host) std::memcpy(flags_host, ctx->pinned_flags, batch * sizeof(int32_t));
   });
 }
 

@@ -111,8 +111,14 @@ struct ptb_context {
   std::recursive_mutex mutex;  // serialises host-API calls (reference runs stages concurrently)
   ptb::DeviceBuffer scratch[4];
   ptb::DeviceBuffer flags;
-  cudaStream_t aux[2] = {nullptr, nullptr};  // host-batch pipeline streams (lazy)
-  ptb::DeviceBuffer slotbuf[2][5];            // per pipeline slot: u, v, su, sv, flags
+  // host-batch pipeline: three streams/slots so the H2D of chunk i+1, the propagation of chunk i
+  // and the D2H of chunk i-1 overlap (separate copy engines for the two directions)
+  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+  ptb::DeviceBuffer slotbuf[3][5];  // per pipeline slot: u, v, su, sv, flags
+  // pinned staging for the per-slice flags of the host-batch call: a D2H copy into pageable
+  // memory is synchronous and would serialise the pipeline
+  int32_t* pinned_flags = nullptr;
+  size_t pinned_flags_n = 0;
   void* cublas = nullptr;  // lazily created cublasHandle_t
   // parareal driver work buffers kept between runs (driver.cu), so a repeated run neither
   // reallocates nor synchronises on cudaMalloc/cudaFree; freed with the context
