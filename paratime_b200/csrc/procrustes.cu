@@ -236,6 +236,134 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
   if (g == 0 && tid == 0) *a.keep_out = keep;
 }
 
+// Column-pivoted Householder QR of a small matrix held entirely in one CTA's shared memory
+// (the corrector's H and the blocked QR's R1: up to ~160 x 160).  Same algorithm, keep rule and
+// output layout as k_qrcp (R above the diagonal with beta on it, scaled reflectors below, tau,
+// perm, keep, |R_jj| sequence) without grid barriers or global-memory sweeps.
+__global__ void __launch_bounds__(1024) k_qrcp_small(QrArgs a) {
+  extern __shared__ double qs[];  // A[m*n] | nrm[n] | w[n] | red[32]
+  const int m = a.m, n = a.n, tid = threadIdx.x, T = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
+  double* A = qs;
+  double* nrm = A + size_t(m) * n;
+  double* wv = nrm + n;
+  double* red = wv + n;
+  __shared__ int piv;
+  __shared__ double s_xn2;
+  for (int e = tid; e < m * n; e += T) {
+    const int c = e / m, i = e - c * m;
+    A[e] = a.A[size_t(c) * a.lda + i];
+  }
+  for (int k = tid; k < n; k += T) a.perm[k] = k;
+  __syncthreads();
+  for (int k = warp; k < n; k += nwarps) {  // initial squared column norms
+    double acc = 0.0;
+    for (int i = lane; i < m; i += 32) acc += A[size_t(k) * m + i] * A[size_t(k) * m + i];
+    acc = warp_sum(acc);
+    if (lane == 0) nrm[k] = acc;
+  }
+  __syncthreads();
+  int keep = 0;
+  for (int j = 0; j < n && j < m; ++j) {
+    if (warp == 0) {  // pivot: max remaining norm, first index on ties (idamax)
+      double best = -1.0;
+      int bi = n;
+      for (int k = j + lane; k < n; k += 32)
+        if (nrm[k] > best) {
+          best = nrm[k];
+          bi = k;
+        }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == 0) piv = bi;
+    }
+    __syncthreads();
+    const int p = piv;
+    if (p != j) {
+      for (int i = tid; i < m; i += T) {
+        const double t = A[size_t(j) * m + i];
+        A[size_t(j) * m + i] = A[size_t(p) * m + i];
+        A[size_t(p) * m + i] = t;
+      }
+      if (tid == 0) {
+        const int t = a.perm[j];
+        a.perm[j] = a.perm[p];
+        a.perm[p] = t;
+        const double tn = nrm[j];
+        nrm[j] = nrm[p];
+        nrm[p] = tn;
+      }
+      __syncthreads();
+    }
+    double* cj = A + size_t(j) * m;
+    if (warp == 0) {  // below-diagonal norm of the pivot column (dlarfg's xnorm)
+      double acc = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) acc += cj[i] * cj[i];
+      acc = warp_sum(acc);
+      if (lane == 0) s_xn2 = acc;
+    }
+    __syncthreads();
+    const double alpha = cj[j];
+    const double xnorm = sqrt(s_xn2);
+    double beta, tau, scal;
+    if (xnorm == 0.0) {
+      beta = alpha;
+      tau = 0.0;
+      scal = 0.0;
+    } else {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (fabs(beta) <= a.drop_tol) {
+      if (tid == 0) a.beta_out[j] = fabs(beta);
+      break;
+    }
+    keep = j + 1;
+    if (tid == 0) {
+      a.tau[j] = tau;
+      a.beta_out[j] = fabs(beta);
+    }
+    for (int i = j + 1 + tid; i < m; i += T) cj[i] *= scal;
+    __syncthreads();
+    for (int k = j + 1 + warp; k < n; k += nwarps) {  // w_k = v^T A[j:, k]
+      const double* ck = A + size_t(k) * m;
+      double acc = lane == 0 ? ck[j] : 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) acc += cj[i] * ck[i];
+      acc = warp_sum(acc);
+      if (lane == 0) wv[k] = acc;
+    }
+    __syncthreads();
+    for (int k = j + 1 + warp; k < n; k += nwarps) {  // A[:, k] -= tau v w_k; next norms below row j
+      double* ck = A + size_t(k) * m;
+      const double tw = tau * wv[k];
+      if (lane == 0) ck[j] -= tw;
+      double acc = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) {
+        const double x = ck[i] - tw * cj[i];
+        ck[i] = x;
+        acc += x * x;
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) nrm[k] = acc;
+    }
+    if (tid == 0) cj[j] = beta;
+    __syncthreads();
+  }
+  for (int e = tid; e < m * n; e += T) {
+    const int c = e / m, i = e - c * m;
+    a.A[size_t(c) * a.lda + i] = A[e];
+  }
+  if (tid == 0) *a.keep_out = keep;
+  (void)red;
+}
+
 // Unpivoted Householder QR of a tall panel (the blocked QR's panels) with ONE grid barrier per
 // column: column j+1's squared norm and its raw dot products with the trailing columns are
 // accumulated during column j's update pass (w_k = A_jk + scal * sum_{i>j} x_i A_ik needs only the
@@ -889,17 +1017,29 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
   int* perm = static_cast<int*>(w.buf[2].get(size_t(n) * sizeof(int)));
   int* keep_d = static_cast<int*>(w.buf[3].get(sizeof(int)));
   double* betas = static_cast<double*>(w.buf[5].get(size_t(n) * sizeof(double)));
-  size_t smem = (QR_THREADS + 2 * size_t(n)) * sizeof(double);
-  const int G = qr_grid(ctx, m, smem + 16384 * sizeof(double), reinterpret_cast<const void*>(k_qrcp));
-  const size_t rows_per = (size_t(m) + G - 1) / G;
-  if (rows_per > 16384) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
-  smem += rows_per * sizeof(double);
-  double* part = static_cast<double*>(w.buf[4].get(size_t(2) * G * (n + 1) * sizeof(double)));
-  QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, part, keep_d, betas};
-  void* args[] = {&qa};
-  PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qrcp), G, QR_THREADS, args, smem, st));
-  PTB_LAUNCH_CHECK(ctx);
+  const size_t small_smem = (size_t(m) * n + 2 * size_t(n) + 32) * sizeof(double);
+  static const bool small_env = [] {  // PTB_QR_SMALL=0 keeps small matrices on the cooperative kernel
+    const char* e = std::getenv("PTB_QR_SMALL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (small_env && small_smem <= 200 * 1024) {
+    QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, nullptr, keep_d, betas};
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp_small, cudaFuncAttributeMaxDynamicSharedMemorySize, int(small_smem)));
+    k_qrcp_small<<<1, 1024, small_smem, st>>>(qa);
+    PTB_LAUNCH_CHECK(ctx);
+  } else {
+    size_t smem = (QR_THREADS + 2 * size_t(n)) * sizeof(double);
+    const int G = qr_grid(ctx, m, smem + 16384 * sizeof(double), reinterpret_cast<const void*>(k_qrcp));
+    const size_t rows_per = (size_t(m) + G - 1) / G;
+    if (rows_per > 16384) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
+    smem += rows_per * sizeof(double);
+    double* part = static_cast<double*>(w.buf[4].get(size_t(2) * G * (n + 1) * sizeof(double)));
+    QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, part, keep_d, betas};
+    void* args[] = {&qa};
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    PTB_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qrcp), G, QR_THREADS, args, smem, st));
+    PTB_LAUNCH_CHECK(ctx);
+  }
   int keep = 0;
   PTB_CUDA_CHECK(cudaMemcpyAsync(&keep, keep_d, sizeof(int), cudaMemcpyDeviceToHost, st));
   PTB_CUDA_CHECK(cudaStreamSynchronize(st));
