@@ -10,17 +10,20 @@
 //   relative_residual    :245-253
 //
 // Kernels written here (sm_100a):
-//   k_qrcp      cooperative column-pivoted Householder QR of a tall m x n block: every CTA
-//               owns a row range; per column one grid barrier reduces the remaining column
-//               norms (fused into the previous update), picks the pivot (max remaining
-//               norm, first index on ties — the dgeqp3 rule with exact instead of downdated
-//               norms), forms the reflector (dlarfg), and a second barrier reduces v^T A.
-//               Stops at the first |R_jj| <= guard (the reference's keep rule).
-//   k_wy_prep/k_wy_larft + DGEMMs  cooperative backward accumulation Q = H_0 ... H_{keep-1} [I; 0].
-//   k_jacobi    one-sided (Hestenes) Jacobi SVD in a single CTA, round-robin pair
-//               ordering, rotations until every pair is orthogonal to ~eps; singular
-//               values sorted descending.
-//   k_fix_signs one CTA per column.
+//   truncated_qr   tall blocks (m >= 8n, n > 32): blocked Householder QR -- k_qr_panel (one
+//                  panel of 32 columns, unpivoted, ONE grid barrier per column: the next
+//                  column's norm and raw dot products are reduced during the current update)
+//                  with compact-WY trailing updates (cuBLAS DGEMMs), then the column-pivoted
+//                  QR of the small R1 (pivots and |R_jj| of A, since norms are invariant under
+//                  Q1), Q = Q1 [Q2; 0].  Other shapes: k_qrcp (cooperative, rows split over
+//                  CTAs, dgeqp3 pivot rule with exact norms) or k_qrcp_small (whole matrix in
+//                  one CTA's shared memory).  Both stop at the first |R_jj| <= guard.
+//   k_wy_prep / k_wy_larft + DGEMMs   thin Q in compact WY form (dlarft / dorg2r order).
+//   k_jacobi       one-sided (Hestenes) Jacobi SVD in a single CTA (shared memory when it fits),
+//                  round-robin pairs, relative-orthogonality stop; k_jacobi_coop spreads the same
+//                  schedule over a cooperative grid (bitwise equal) for larger matrices.  thin_svd
+//                  preconditions with a pivoted QR (Jacobi on R^T, as dgesvj).
+//   k_fix_signs    one CTA per column.
 // Large products (U^T F, U UF, [U Q_F] Xh, X(Y^T v)) are plain cuBLAS DGEMMs.
 
 #include <cooperative_groups.h>
