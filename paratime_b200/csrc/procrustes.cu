@@ -243,20 +243,25 @@ __global__ void __launch_bounds__(QR_THREADS) k_qrcp(QrArgs a) {
 // (the corrector's H and the blocked QR's R1: up to ~160 x 160).  Same algorithm, keep rule and
 // output layout as k_qrcp (R above the diagonal with beta on it, scaled reflectors below, tau,
 // perm, keep, |R_jj| sequence) without grid barriers or global-memory sweeps.
+// SMEM = false: the same single-CTA kernel working in place on global memory (lda == m; the
+// matrix stays L2-resident), for matrices too large for shared memory but small enough that one
+// CTA without grid barriers beats the cooperative kernel (the corrector's H at cfg4, ~270^2).
+template <bool SMEM>
 __global__ void __launch_bounds__(1024) k_qrcp_small(QrArgs a) {
-  extern __shared__ double qs[];  // A[m*n] | nrm[n] | w[n] | red[32]
+  extern __shared__ double qs[];  // SMEM: A[m*n] | nrm[n] | w[n] | red[32];  else nrm | w | red
   const int m = a.m, n = a.n, tid = threadIdx.x, T = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
-  double* A = qs;
-  double* nrm = A + size_t(m) * n;
+  double* A = SMEM ? qs : a.A;
+  double* nrm = SMEM ? A + size_t(m) * n : qs;
   double* wv = nrm + n;
   double* red = wv + n;
   __shared__ int piv;
   __shared__ double s_xn2;
-  for (int e = tid; e < m * n; e += T) {
-    const int c = e / m, i = e - c * m;
-    A[e] = a.A[size_t(c) * a.lda + i];
-  }
+  if (SMEM)
+    for (int e = tid; e < m * n; e += T) {
+      const int c = e / m, i = e - c * m;
+      A[e] = a.A[size_t(c) * a.lda + i];
+    }
   for (int k = tid; k < n; k += T) a.perm[k] = k;
   __syncthreads();
   for (int k = warp; k < n; k += nwarps) {  // initial squared column norms
@@ -359,10 +364,11 @@ __global__ void __launch_bounds__(1024) k_qrcp_small(QrArgs a) {
     if (tid == 0) cj[j] = beta;
     __syncthreads();
   }
-  for (int e = tid; e < m * n; e += T) {
-    const int c = e / m, i = e - c * m;
-    a.A[size_t(c) * a.lda + i] = A[e];
-  }
+  if (SMEM)
+    for (int e = tid; e < m * n; e += T) {
+      const int c = e / m, i = e - c * m;
+      a.A[size_t(c) * a.lda + i] = A[e];
+    }
   if (tid == 0) *a.keep_out = keep;
   (void)red;
 }
@@ -955,11 +961,11 @@ double dev_sumsq(ptb_context* ctx, const double* x, size_t n, DeviceBuffer& scra
   return h;
 }
 
-int qr_grid(ptb_context* ctx, int m, size_t smem, const void* kern) {
+int qr_grid(ptb_context* ctx, int m, size_t smem, const void* kern, int rows_per_cta = 512) {
   int per_sm = 0;
   PTB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, QR_THREADS, smem));
   const int cap = std::max(1, per_sm) * ctx->num_sms;
-  const int want = std::max(1, (m + 511) / 512);
+  const int want = std::max(1, (m + rows_per_cta - 1) / rows_per_cta);
   return std::min({cap, want, ctx->num_sms});
 }
 
@@ -1027,12 +1033,22 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
   }();
   if (small_env && small_smem <= 200 * 1024) {
     QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, nullptr, keep_d, betas};
-    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp_small, cudaFuncAttributeMaxDynamicSharedMemorySize, int(small_smem)));
-    k_qrcp_small<<<1, 1024, small_smem, st>>>(qa);
+    PTB_CUDA_CHECK(
+        cudaFuncSetAttribute(k_qrcp_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(small_smem)));
+    k_qrcp_small<true><<<1, 1024, small_smem, st>>>(qa);
+    PTB_LAUNCH_CHECK(ctx);
+  } else if (small_env && m <= 1024 && n <= 4096) {
+    QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, nullptr, keep_d, betas};
+    const size_t gsmem = (2 * size_t(n) + 32) * sizeof(double);
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_qrcp_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsmem)));
+    k_qrcp_small<false><<<1, 1024, gsmem, st>>>(qa);
     PTB_LAUNCH_CHECK(ctx);
   } else {
     size_t smem = (QR_THREADS + 2 * size_t(n)) * sizeof(double);
-    const int G = qr_grid(ctx, m, smem + 16384 * sizeof(double), reinterpret_cast<const void*>(k_qrcp));
+    // matrices too big for k_qrcp_small but with few rows (the corrector's H at cfg4 is ~270^2):
+    // spread the rows thinner, the per-column latency rather than bandwidth is what matters
+    const int G = qr_grid(ctx, m, smem + 16384 * sizeof(double), reinterpret_cast<const void*>(k_qrcp),
+                          m < 8192 ? 64 : 512);
     const size_t rows_per = (size_t(m) + G - 1) / G;
     if (rows_per > 16384) fail(PTB_UNSUPPORTED, "truncated_qr: too many rows per CTA");
     smem += rows_per * sizeof(double);
