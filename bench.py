@@ -115,6 +115,14 @@ def dist_env():
     return rank, world, local
 
 
+def arm_config(n, batch, mode, world):
+    """The workload both arms report (bench.py's own arm and --impl reference)."""
+    return {"workload": f"cfg5 fine propagator {n}x{n} periodic, {batch} slices/GPU x "
+                        f"{STEPS_PER_COUPLING} velocity-Verlet steps per step ({mode} mode)",
+            "grid": n, "slices_per_gpu": batch, "steps_per_slice": STEPS_PER_COUPLING,
+            "parallelism": f"slice-sharded x{world}", "l2": "inputs > L2 (no flush needed)"}
+
+
 def run_reference(args, rank, world):
     """The reference's propagate_coupling (propagator.cpp, compiled verbatim in oracle/_ref)
     over a bounded sample of the same workload on all host cores."""
@@ -145,8 +153,9 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "grid-pt updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg5 medium/pulses)",
-        "config": {"workload": f"cfg5 fine propagator {n}x{n}, {steps} Verlet steps per slice",
-                   "sample": f"{sample_slices} slices x {steps} steps per step (bounded CPU sample)"},
+        "config": dict(arm_config(n, args.batch, args.mode, world),
+                       sample=f"each step: {sample_slices} slices x {steps} steps of this workload on the host "
+                              f"(bounded CPU sample; the metric is per grid-point update)"),
         "cpu_baseline": {"value": value, "unit": "grid-pt updates/s", "cores": cores, "kind": "reference",
                          "sample": f"{sample_slices} slices of {n}^2 x {steps} steps, propagate_coupling "
                                    f"(propagator.cpp verbatim, -O3, std::thread x{cores})"},
@@ -312,11 +321,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "grid-pt updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg5 medium and Gaussian pulses)",
-            "config": {"workload": f"cfg5 fine propagator {n}x{n} periodic, {batch} slices/GPU x "
-                                   f"{STEPS_PER_COUPLING} velocity-Verlet steps per step ({args.mode} mode)",
-                       "grid": n, "slices_per_gpu": batch, "steps_per_slice": STEPS_PER_COUPLING,
-                       "parallelism": f"slice-sharded x{world}", "l2": "inputs > L2 (no flush needed)",
-                       "finite": finite},
+            "config": dict(arm_config(n, batch, args.mode, world), finite=finite),
             "gpu_launches": launches,
             "roofline": roofline,
             "clocks": clocks.summary(),
