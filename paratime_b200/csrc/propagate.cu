@@ -127,15 +127,18 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs a) {
   double* __restrict__ V = a.v + off;
   const StepParams& p = a.p;
   double u[PPT], v[PPT], k[PPT], acc[PPT];
+  Nb nbq[PPT];  // periodic neighbour offsets, computed once (integer div/mod off the step loop)
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     const int i = tid + q * T;
     u[q] = v[q] = k[q] = acc[q] = 0.0;
+    nbq[q] = Nb{0, 0, 0, 0};
     if (i < n) {
       u[q] = U[i];
       v[q] = V[i];
       k[q] = a.coef[i];
       buf[i] = u[q];
+      nbq[q] = neighbours(i, p.ny, p.nx);
     }
   }
   __syncthreads();
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs a) {
   for (int q = 0; q < PPT; ++q) {
     const int i = tid + q * T;
     if (i < n) {
-      const Nb nb = neighbours(i, p.ny, p.nx);
+      const Nb nb = nbq[q];
       if (EXACT) {
         acc[q] = __dmul_rn(lap_exact<HASY>(u[q], buf[nb.l], buf[nb.r], buf[nb.u], buf[nb.d], p), k[q]);
       } else {
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs a) {
     for (int q = 0; q < PPT; ++q) {
       const int i = tid + q * T;
       if (i < n) {
-        const Nb nb = neighbours(i, p.ny, p.nx);
+        const Nb nb = nbq[q];
         if (EXACT) {
           const double an = __dmul_rn(lap_exact<HASY>(u[q], dst[nb.l], dst[nb.r], dst[nb.u], dst[nb.d], p), k[q]);
           v[q] = __dadd_rn(v[q], __dmul_rn(p.hd, __dadd_rn(acc[q], an)));
