@@ -114,6 +114,76 @@ __global__ void k_add_sub(size_t n, const double* x, const double* y, const doub
 }
 
 // u-part of Lambda-dagger(X z, m): u += (m_new - m_old) / Nc  (zero mode of the inverse DFT)
+__device__ __forceinline__ double drv_block_sum256(double x) {
+  __shared__ double red[256];
+  red[threadIdx.x] = x;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// z = Y^T x for ONE vector (the sweep's z_w = Y^T Lambda(w)): block j reduces column j in a
+// fixed order (four accumulators, tree), one launch instead of cuBLAS's gemv + reductions
+// grid (r, P): block (j, p) reduces rows [p*chunk, (p+1)*chunk) of column j -> z[j*P + p]; the P
+// partials are summed in order by k_assemble_d (fixed layout for a given row count)
+__global__ void __launch_bounds__(256) k_gemv_t1(size_t rows, size_t chunk, const double* Y, size_t ld,
+                                                 const double* x, double* z) {
+  const double* Yj = Y + size_t(blockIdx.x) * ld;
+  const size_t r0 = size_t(blockIdx.y) * chunk, r1 = min(rows, r0 + chunk);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  size_t i = r0 + threadIdx.x;
+  for (; i + 768 < r1; i += 1024) {
+    a0 += Yj[i] * x[i];
+    a1 += Yj[i + 256] * x[i + 256];
+    a2 += Yj[i + 512] * x[i + 512];
+    a3 += Yj[i + 768] * x[i + 768];
+  }
+  for (; i < r1; i += 256) a0 += Yj[i] * x[i];
+  const double s = drv_block_sum256((a0 + a1) + (a2 + a3));
+  if (threadIdx.x == 0) z[size_t(blockIdx.x) * gridDim.y + blockIdx.y] = s;
+}
+
+int gemv_parts(size_t rows) { return int(std::max<size_t>(1, std::min<size_t>(64, rows / 4096))); }
+
+// corrected difference on the coarse grid (one launch): dz = z_w - z_old (z_old nullable),
+// du = Zu dz + (m_w - m_old)/N_c, dv = Zv dz  (Zu, Zv: N_c x r column-major)
+__global__ void __launch_bounds__(256) k_assemble_d(size_t nc, int r, const double* Zu, const double* Zv,
+                                                    const double* zw, int zparts, const double* zold,
+                                                    const double* mw, const double* mold, double* du, double* dv) {
+  extern __shared__ double dz[];
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    double zj = 0.0;  // z_w[j] = sum of its partials, in order
+    for (int q = 0; q < zparts; ++q) zj += zw[size_t(j) * zparts + q];
+    dz[j] = zold ? __dsub_rn(zj, zold[j]) : zj;
+  }
+  __syncthreads();
+  const double dm = mold ? __dsub_rn(*mw, *mold) : *mw;
+  const double add = dm / double(nc);
+  GRID_STRIDE(i, nc) {
+    // four independent accumulators per output (loads of four columns in flight), fixed order
+    double su[4] = {0.0, 0.0, 0.0, 0.0}, sv[4] = {0.0, 0.0, 0.0, 0.0};
+    int j = 0;
+    for (; j + 3 < r; j += 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        su[q] = fma(Zu[size_t(j + q) * nc + i], dz[j + q], su[q]);
+        sv[q] = fma(Zv[size_t(j + q) * nc + i], dz[j + q], sv[q]);
+      }
+    }
+    for (; j < r; ++j) {
+      su[0] = fma(Zu[size_t(j) * nc + i], dz[j], su[0]);
+      sv[0] = fma(Zv[size_t(j) * nc + i], dz[j], sv[0]);
+    }
+    du[i] = ((su[0] + su[1]) + (su[2] + su[3])) + add;
+    dv[i] = (sv[0] + sv[1]) + (sv[2] + sv[3]);
+  }
+}
+
 __global__ void k_add_mean(size_t n, const double* mnew, const double* mold, double* u) {
   const double dm = mold ? __dsub_rn(*mnew, *mold) : *mnew;
   const double v = dm / double(n);
@@ -174,6 +244,13 @@ struct Driver {
   DeviceBuffer rn_u, rn_v, ri_u, ri_v, init_u, init_v, init_cu, init_cv;
   DeviceBuffer comp, mean, comp_old, mean_old, zold, zw, Zu, Zv, Fm, Gm, idx, tmpc;
   std::vector<int32_t> ref_bad;
+  int zw_parts = 1;  // partials per z_w entry written by corrected_batch (batch 1)
+
+  // per-step sweep products as single fused launches (k_gemv_t1 + k_assemble_d) for small and mid
+  // correctors (latency-bound: cfg1-3); cuBLAS GEMVs for large ones (HBM-bound: cfg4)
+  bool fused_sweep(const DevCorrector& c) const {
+    return size_t(cg.dim + 1) * nc * size_t(std::max(c.rank, 1)) <= (size_t(4) << 20);
+  }
   const double* cf_dev = nullptr;  // coarse speed
 
   std::vector<DeviceBuffer*> owned() {
@@ -537,7 +614,17 @@ struct Driver {
       if (zout) PTB_CUDA_CHECK(cudaMemsetAsync(zout, 0, sizeof(double), st()));
       return;
     }
-    gemm(ctx, true, false, c.rank, int(batch), int(rows), 1.0, c.Yp(), int(rows), cp, int(rows), 0.0, zout, c.rank);
+    if (batch == 1 && fused_sweep(c)) {  // the sweep's per-step product: one launch, fixed order, P partials
+      const int P = gemv_parts(rows);
+      zw_parts = P;
+      k_gemv_t1<<<dim3(unsigned(c.rank), unsigned(P)), 256, 0, st()>>>(rows, (rows + P - 1) / P, c.Yp(), rows, cp,
+                                                                       zout);
+      PTB_LAUNCH_CHECK(ctx);
+    } else {
+      if (batch == 1) zw_parts = 1;
+      gemm(ctx, true, false, c.rank, int(batch), int(rows), 1.0, c.Yp(), int(rows), cp, int(rows), 0.0, zout,
+           c.rank);
+    }
   }
 
   // ---- sweeps (coarse, replicated) --------------------------------------------------------
@@ -552,6 +639,14 @@ struct Driver {
   void assemble_d(const DevCorrector& c, const double* zw_, const double* zold_, const double* mw, const double* mold,
                   double* du, double* dv) {
     const int r = c.rank;
+    if (fused_sweep(c)) {
+      k_assemble_d<<<blocks(ctx, nc), 256, size_t(std::max(r, 1)) * sizeof(double), st()>>>(
+          nc, r, static_cast<double*>(Zu.ptr), static_cast<double*>(Zv.ptr), zw_, zw_parts, zold_, mw, mold, du,
+          dv);
+      PTB_LAUNCH_CHECK(ctx);
+      return;
+    }
+    // large corrector (cfg4: 3 N_c x r = 30 M entries): cuBLAS GEMVs stream Zu, Zv faster
     double* dz = dalloc<double>(tmpc, std::max(r, 1));
     if (r > 0) {
       if (zold_) {
@@ -591,7 +686,7 @@ struct Driver {
                         zo + size_t(c.rank), mo + 1);
       }
     }
-    double* zwp = dalloc<double>(zw, std::max(c.rank, 1));
+    double* zwp = dalloc<double>(zw, size_t(std::max(c.rank, 1)) * 64);  // r x P partials
     double* mw = dalloc<double>(mean, std::max<size_t>(N, 1));
     double* ru = static_cast<double*>(rn_u.ptr);
     double* rv = static_cast<double*>(rn_v.ptr);
@@ -630,7 +725,7 @@ struct Driver {
     int32_t* wfl = fl(wf);
     PTB_CUDA_CHECK(cudaMemsetAsync(wfl, 0, (N + 1) * sizeof(int32_t), st()));
     if (!omega_identity) precompute_Z(c);
-    double* zwp = dalloc<double>(zw, std::max(c.rank, 1));
+    double* zwp = dalloc<double>(zw, size_t(std::max(c.rank, 1)) * 64);  // r x P partials
     double* mw = dalloc<double>(mean, std::max<size_t>(N, 1));
     double* ru = static_cast<double*>(rn_u.ptr);
     double* rv = static_cast<double*>(rn_v.ptr);

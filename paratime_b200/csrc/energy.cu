@@ -144,9 +144,18 @@ __global__ void __launch_bounds__(256) k_state_sum(int n, const double* f, size_
   const size_t b = blockIdx.y;
   const size_t src = index ? size_t(index[b]) : b;
   const double* F = f + src * sstride;
-  double acc = 0.0;
-  for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) acc += F[i];
-  const double s = block_sum<256>(acc);
+  // four independent accumulators (four loads in flight per thread), combined in fixed order
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int step = gridDim.x * 256;
+  int i = blockIdx.x * 256 + threadIdx.x;
+  for (; i + 3 * step < n; i += 4 * step) {
+    a0 += F[i];
+    a1 += F[i + step];
+    a2 += F[i + 2 * step];
+    a3 += F[i + 3 * step];
+  }
+  for (; i < n; i += step) a0 += F[i];
+  const double s = block_sum<256>((a0 + a1) + (a2 + a3));
   if (threadIdx.x == 0) part[b * gridDim.x + blockIdx.x] = s;
 }
 
@@ -485,10 +494,14 @@ void energy_components(EnergyWork& w, const ptb_grid& g, int scheme, size_t batc
   if (mean) {
     const int P = state_sum_parts(n);
     double* part = static_cast<double*>(w.buf[8].get(batch * P * sizeof(double)));
-    k_state_sum<<<dim3(unsigned(P), unsigned(batch)), 256, 0, st>>>(n, u, sstride, index, part);
+    // one partial per state: the block writes the sum directly (0 + x == x, same bits)
+    k_state_sum<<<dim3(unsigned(P), unsigned(batch)), 256, 0, st>>>(n, u, sstride, index, P == 1 ? mean : part);
     PTB_LAUNCH_CHECK(ctx);
-    k_state_sum_final<<<unsigned(std::min<size_t>((batch + 255) / 256, 1024)), 256, 0, st>>>(batch, P, part, mean);
-    PTB_LAUNCH_CHECK(ctx);
+    if (P > 1) {
+      k_state_sum_final<<<unsigned(std::min<size_t>((batch + 255) / 256, 1024)), 256, 0, st>>>(batch, P, part,
+                                                                                              mean);
+      PTB_LAUNCH_CHECK(ctx);
+    }
   }
 }
 
