@@ -609,7 +609,16 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
     __syncthreads();
     const double floor2 = eps * eps * colmax;
     for (int round = 0; round < cc - 1; ++round) {
-      for (int pr = warp; pr < cc / 2; pr += nwarps) {
+      // pairs per lane group: 16-lane groups in the shared-memory variant (two pairs per warp at
+      // once, half the sequential steps per round), whole warps otherwise (k_jacobi_coop's order)
+      constexpr int GS = SMEM ? 16 : 32;
+      const int glane = threadIdx.x & (GS - 1), grp = threadIdx.x / GS, ngrp = blockDim.x / GS;
+      const unsigned gmask = GS == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+      auto gsum = [&](double x) {
+        for (int o = GS / 2; o > 0; o >>= 1) x += __shfl_xor_sync(gmask, x, o);
+        return x;
+      };
+      for (int pr = grp; pr < cc / 2; pr += ngrp) {
         auto pos = [&](int q) { return q == 0 ? 0 : 1 + (q - 1 + round) % (cc - 1); };
         int i = pos(pr), j = pos(cc - 1 - pr);
         if (i > j) {
@@ -621,33 +630,33 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
         double* ai = A + size_t(i) * r;
         double* aj = A + size_t(j) * r;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int k = lane; k < r; k += 32) {
+        for (int k = glane; k < r; k += GS) {
           const double x = ai[k], y = aj[k];
           al += x * x;
           be += y * y;
           ga += x * y;
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
+        al = gsum(al);
+        be = gsum(be);
+        ga = gsum(ga);
         const double nab = sqrt(al) * sqrt(be);
         if (ga != 0.0 && fabs(ga) > tol * nab && nab > floor2) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          for (int k = lane; k < r; k += 32) {
+          for (int k = glane; k < r; k += GS) {
             const double x = ai[k], y = aj[k];
             ai[k] = cs * x - sn * y;
             aj[k] = sn * x + cs * y;
           }
           double* vi = V + size_t(i) * c;
           double* vj = V + size_t(j) * c;
-          for (int k = lane; k < c; k += 32) {
+          for (int k = glane; k < c; k += GS) {
             const double x = vi[k], y = vj[k];
             vi[k] = cs * x - sn * y;
             vj[k] = sn * x + cs * y;
           }
-          if (lane == 0) rotated = 1;
+          if (glane == 0) rotated = 1;
         }
       }
       __syncthreads();
