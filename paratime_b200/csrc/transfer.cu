@@ -23,7 +23,8 @@
 //   My[q*r + rem][j] = W[rem][(q - j) mod n]   (y: out = My . half)
 // issued as cuBLAS DGEMMs of one fixed shape per field, so each slice's result does not
 // depend on how many slices a call (or a rank) carries.
-// Default on large 2D grids is the reference's own construction done with cuFFT (fft.cpp wraps
+// Default on 2D fine grids >= 256^2 (measured: faster than the DGEMMs from 256^2 up; the
+// DGEMM route stays for PTB_INTERP_FFT=0) is the reference's own construction done with cuFFT (fft.cpp wraps
 // FFTW): 2D D2Z of the coarse field, the zero-padded spectrum (Nyquist bins split 1/2-1/2 per
 // axis as grid.cpp:161-166; the x split comes from the implicit Hermitian mirror of the
 // half-spectrum), 2D Z2D on the fine grid.  The 2D DFT is separable, so this equals the
@@ -305,7 +306,7 @@ bool use_fft(const TGeom& g) {
   }();
   if (env == 0) return false;
   const bool ok = g.cy > 1 && g.rx > 1 && g.ry > 1;
-  return ok && (env == 1 || size_t(g.fy) * g.fx >= size_t(1024) * 1024);
+  return ok && (env == 1 || size_t(g.fy) * g.fx >= size_t(256) * 256);
 }
 
 constexpr int FFT_CHUNK = 8;  // fields per cuFFT execution (fixed: a partial chunk is padded)
