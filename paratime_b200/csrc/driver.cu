@@ -421,11 +421,14 @@ struct Driver {
   }
 
   // ---- stages ------------------------------------------------------------------------
-  void coarse_propagate(double* u, double* v, size_t batch, int32_t* flags) {
+  // C on `batch` coarse states with the NaN-state rule (coarse_stage, parareal.cpp:64-73).
+  // sweep_step: flags pre-zeroed by the caller and the state consumed only through the theta
+  // sweep's tail, which turns d_n into NaN on this same flag -> no memset, no NaN fill here.
+  void coarse_propagate(double* u, double* v, size_t batch, int32_t* flags, bool sweep_step = false) {
     if (!batch) return;
-    PTB_CUDA_CHECK(cudaMemsetAsync(flags, 0, batch * sizeof(int32_t), st()));
+    if (!sweep_step) PTB_CUDA_CHECK(cudaMemsetAsync(flags, 0, batch * sizeof(int32_t), st()));
     propagate(pc, pc->steps, batch, u, v, flags, s.mode);
-    nan_where(nc, batch, flags, nullptr, nullptr, u, v);
+    if (!sweep_step) nan_where(nc, batch, flags, nullptr, nullptr, u, v);
   }
 
   // reference_or_nan (parareal.cpp:133-145): chain on every rank up to its last slice
@@ -696,7 +699,7 @@ struct Driver {
     copy(ru, slot(rf_u, 1, nc), nc);
     copy(rv, slot(rf_v, 1, nc), nc);
     for (size_t n = 2; n <= N; ++n) {
-      coarse_propagate(ru, rv, 1, wfl + n);  // w = C(R next[n-1]) in place
+      coarse_propagate(ru, rv, 1, wfl + n, /*sweep_step=*/true);  // w = C(R next[n-1]) in place
       double* du = slot(d_u, n, nc);
       double* dv = slot(d_v, n, nc);
       if (omega_identity) {
