@@ -491,7 +491,8 @@ struct Driver {
     HostProf hp_(st());
     int32_t* f = fl(sflags);
     PTB_CUDA_CHECK(cudaMemsetAsync(f, 0, (L + 1) * sizeof(int32_t), st()));
-    k_state_flags<<<dim3(std::min(64u, blocks(ctx, nf)), unsigned(L + 1)), 256, 0, st()>>>(nf, su, sv, nf, f);
+    // state 0 (index a-1) here; states 1..L are checked by the error sums, which read them anyway
+    k_state_flags<<<dim3(std::min(64u, blocks(ctx, nf)), 1u), 256, 0, st()>>>(nf, su, sv, nf, f);
     PTB_LAUNCH_CHECK(ctx);
     double* own = dalloc<double>(sums_own, chunk * 5);
     PTB_CUDA_CHECK(cudaMemsetAsync(own, 0, chunk * 5 * sizeof(double), st()));
@@ -499,7 +500,7 @@ struct Driver {
       double* tmp = dalloc<double>(sums_all, L * 4);
       hp_.mark("finalize: flags");
       pair_energy_sums(ew, fg, s.metric_scheme, L, su + nf, sv + nf, nf, RU(a), RV(a), nf, ptb_propagator_speed(pf),
-                       tmp);
+                       tmp, f + 1);
       hp_.mark("finalize: error sums");
       // pack [flag, s0..s3] per own slice
       PTB_CUDA_CHECK(cudaMemcpy2DAsync(own + 1, 5 * sizeof(double), tmp, 4 * sizeof(double), 4 * sizeof(double), L,

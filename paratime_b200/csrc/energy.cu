@@ -269,7 +269,8 @@ constexpr int PAIR_BLOCKS = 32;
 
 __global__ void __launch_bounds__(256) k_pair_sums(Geo G, Beta B, int n, const double* ua, const double* va,
                                                    size_t sa, const double* ub, const double* vb, size_t sb,
-                                                   const double* c, double* part) {
+                                                   const double* c, double* part, int32_t* nonfinite) {
+  bool ok = true;
   const size_t pr = blockIdx.y;
   const double* UA = ua + pr * sa;
   const double* VA = va + pr * sa;
@@ -290,7 +291,9 @@ __global__ void __launch_bounds__(256) k_pair_sums(Geo G, Beta B, int n, const d
     const double du = __dsub_rn(UA[p], UB[p]);
     ld += du * du;
     lr += UB[p] * UB[p];
+    ok &= isfinite(UA[p]) && isfinite(VA[p]);
   }
+  if (nonfinite && __syncthreads_or(!ok) && threadIdx.x == 0) atomicOr(&nonfinite[pr], 1);
   sd = block_sum<256>(sd);
   sr = block_sum<256>(sr);
   ld = block_sum<256>(ld);
@@ -324,7 +327,8 @@ __device__ __forceinline__ double grad_x(const double* ra, const double* rb, int
 
 __global__ void __launch_bounds__(256) k_pair_sums2d(Geo G, Beta B, const double* ua, const double* va, size_t sa,
                                                      const double* ub, const double* vb, size_t sb, const double* c,
-                                                     double* part) {
+                                                     double* part, int32_t* nonfinite) {
+  bool ok = true;
   const size_t pr = blockIdx.y;
   const double* UA = ua + pr * sa;
   const double* VA = va + pr * sa;
@@ -360,8 +364,9 @@ __global__ void __launch_bounds__(256) k_pair_sums2d(Geo G, Beta B, const double
       const double grx = grad_x(UB + row, nullptr, x, nx, B, G.ih[1], false);
       sd += gdx * gdx;
       sr += grx * grx;
-      const double cp = c[p], vbp = VB[p], ubp = UB[p];
-      const double md = __ddiv_rn(__dsub_rn(VA[p], vbp), cp);
+      const double cp = c[p], vbp = VB[p], ubp = UB[p], vap = VA[p];
+      ok &= isfinite(UA[p]) && isfinite(vap);
+      const double md = __ddiv_rn(__dsub_rn(vap, vbp), cp);
       const double mr = __ddiv_rn(vbp, cp);
       sd += md * md;
       sr += mr * mr;
@@ -370,6 +375,7 @@ __global__ void __launch_bounds__(256) k_pair_sums2d(Geo G, Beta B, const double
       lr += ubp * ubp;
     }
   }
+  if (nonfinite && __syncthreads_or(!ok) && threadIdx.x == 0) atomicOr(&nonfinite[pr], 1);
   sd = block_sum<256>(sd);
   sr = block_sum<256>(sr);
   ld = block_sum<256>(ld);
@@ -534,8 +540,17 @@ void from_energy_components(EnergyWork& w, const ptb_grid& g, size_t batch, cons
   PTB_LAUNCH_CHECK(ctx);
 }
 
+__global__ void k_nonfinite_states(int n, const double* u, const double* v, size_t stride, int32_t* flags) {
+  const size_t b = blockIdx.y;
+  bool ok = true;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    ok &= isfinite(u[b * stride + i]) && isfinite(v[b * stride + i]);
+  if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicOr(&flags[b], 1);
+}
+
 void pair_energy_sums(EnergyWork& w, const ptb_grid& g, int scheme, size_t batch, const double* ua, const double* va,
-                      size_t sa, const double* ub, const double* vb, size_t sb, const double* c, double* out4) {
+                      size_t sa, const double* ub, const double* vb, size_t sb, const double* c, double* out4,
+                      int32_t* nonfinite_a) {
   ptb_context* ctx = w.ctx;
   cudaStream_t st = ctx->stream;
   if (batch == 0) return;
@@ -545,13 +560,20 @@ void pair_energy_sums(EnergyWork& w, const ptb_grid& g, int scheme, size_t batch
     const int nb = std::max(1, std::min(PAIR_BLOCKS, (n + 255) / 256));
     double* part = static_cast<double*>(w.buf[7].get(batch * nb * 4 * sizeof(double)));
     if (G.dim == 2 && G.nx >= 256)
-      k_pair_sums2d<<<dim3(nb, unsigned(batch)), 256, 0, st>>>(G, beta_of(scheme), ua, va, sa, ub, vb, sb, c, part);
+      k_pair_sums2d<<<dim3(nb, unsigned(batch)), 256, 0, st>>>(G, beta_of(scheme), ua, va, sa, ub, vb, sb, c, part,
+                                                                 nonfinite_a);
     else
-      k_pair_sums<<<dim3(nb, unsigned(batch)), 256, 0, st>>>(G, beta_of(scheme), n, ua, va, sa, ub, vb, sb, c, part);
+      k_pair_sums<<<dim3(nb, unsigned(batch)), 256, 0, st>>>(G, beta_of(scheme), n, ua, va, sa, ub, vb, sb, c, part,
+                                                               nonfinite_a);
     PTB_LAUNCH_CHECK(ctx);
     k_pair_final<<<nblk(ctx, batch * 4), 256, 0, st>>>(batch, nb, part, out4);
     PTB_LAUNCH_CHECK(ctx);
     return;
+  }
+  if (nonfinite_a) {
+    k_nonfinite_states<<<dim3(unsigned(std::max(1, std::min(64, (n + 255) / 256))), unsigned(batch)), 256, 0, st>>>(
+        n, ua, va, sa, nonfinite_a);
+    PTB_LAUNCH_CHECK(ctx);
   }
   // spectral: components of (a - b) and b, then sums of squares (chunked over states)
   const size_t rows = size_t(G.dim + 1) * n;

@@ -22,7 +22,8 @@ void from_energy_components(EnergyWork& w, const ptb_grid& g, size_t batch, cons
 
 // Per state pair b: out4[4b..4b+3] = { |Lambda(a-b)|^2, |Lambda(b)|^2, |u_a-u_b|^2, |u_b|^2 }.
 void pair_energy_sums(EnergyWork& w, const ptb_grid& g, int scheme, size_t batch, const double* ua, const double* va,
-                      size_t sa, const double* ub, const double* vb, size_t sb, const double* c, double* out4);
+                      size_t sa, const double* ub, const double* vb, size_t sb, const double* c, double* out4,
+                      int32_t* nonfinite_a = nullptr);  // optional: OR 1 into [b] if state a_b is non-finite
 
 // out[j] = sum_i m[j*ld + i]^2, i < rows (deterministic).
 void column_sumsq(ptb_context* ctx, int rows, size_t cols, const double* m, size_t ld, double* out);

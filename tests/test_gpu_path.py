@@ -200,6 +200,32 @@ def test_nonfinite_initial_state_flags_divergence():
     assert np.all(np.isinf(gpu["energy_err"][:, -1]))
 
 
+@pytest.mark.parametrize("variant", [0, 1])
+def test_overflowing_iterates_flag_divergence(variant):
+    """A finite initial state whose propagation overflows (amplitude 1e305): every state after
+    the first is non-finite, so the per-iteration divergence flags come from the finalize error
+    sums of states 1..N (parareal.cpp:107-128), not from the state-0 check."""
+    spec, cf, cc, u0, v0 = config1(iterations=2, variant=variant)
+    u0 = u0 * 1e305
+    gpu = run_gpu(spec, cf, cc, u0, v0)
+    with np.errstate(over="ignore", invalid="ignore"):
+        run, _ = run_oracle(spec, cf, cc, u0, v0)
+    assert list(gpu["diverged"]) == [int(r.diverged) for r in run.iterations] == [1, 1, 1]
+    for k, rec in enumerate(run.iterations):
+        np.testing.assert_array_equal(gpu["energy_err"][k], rec.energy_err)
+
+
+def test_overflowing_iterates_flag_divergence_wide_grid():
+    """Same on config 2's 256^2 fine grid (the 2-D error-sum kernel)."""
+    import workloads as W
+
+    spec, cf, cc, u0, v0 = W.cfg2(iterations=2)
+    gpu = run_gpu(spec, cf, cc, u0 * 1e305, v0)
+    assert list(gpu["diverged"]) == [1, 1, 1]
+    assert np.all(gpu["energy_err"][:, 0] == 0.0)
+    assert np.all(np.isinf(gpu["energy_err"][:, 1:]))
+
+
 def test_one_dimensional_preset_matches_reference(ref):
     """The reference's own rank-tolerance preset (experiment.cpp:279-284), shortened."""
     spec_r, cf, cc, u0, v0 = ref.build_setup("rank-tolerance", overrides="iterations=4\nT=2")
