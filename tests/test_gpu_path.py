@@ -204,8 +204,10 @@ def test_nonfinite_initial_state_flags_divergence():
 def test_overflowing_iterates_flag_divergence(variant):
     """A finite initial state whose propagation overflows (amplitude 1e305): every state after
     the first is non-finite, so the per-iteration divergence flags come from the finalize error
-    sums of states 1..N (parareal.cpp:107-128), not from the state-0 check."""
-    spec, cf, cc, u0, v0 = config1(iterations=2, variant=variant)
+    sums of states 1..N (parareal.cpp:107-128), not from the state-0 check.  EXACT mode: it
+    follows the reference's operation order, so it overflows where the reference does (FAST
+    mode's premultiplied kick coefficient keeps these states finite)."""
+    spec, cf, cc, u0, v0 = config1(iterations=2, variant=variant, mode=1)
     u0 = u0 * 1e305
     gpu = run_gpu(spec, cf, cc, u0, v0)
     with np.errstate(over="ignore", invalid="ignore"):
@@ -219,7 +221,8 @@ def test_overflowing_iterates_flag_divergence_wide_grid():
     """Same on config 2's 256^2 fine grid (the 2-D error-sum kernel)."""
     import workloads as W
 
-    spec, cf, cc, u0, v0 = W.cfg2(iterations=2)
+    spec, cf, cc, u0, v0 = W.cfg2(mode=1)
+    spec["iterations"] = 2
     gpu = run_gpu(spec, cf, cc, u0 * 1e305, v0)
     assert list(gpu["diverged"]) == [1, 1, 1]
     assert np.all(gpu["energy_err"][:, 0] == 0.0)
