@@ -1409,12 +1409,14 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
   // new factors into the spare buffers (U, V = c's factors are still read below), then swap
   double* X = static_cast<double*>(w.SX.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
   double* Y = static_cast<double*>(w.SY.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
+  hp_.mark("update: alloc X/Y");
   const double* Uh = static_cast<double*>(w.Uh.ptr);
   const double* Vh = static_cast<double*>(w.Vh.ptr);
   gemm(ctx, false, false, rows, keep, r, 1.0, U, rows, Uh, hp, 0.0, X, rows);
   gemm(ctx, false, false, rows, keep, qf, 1.0, static_cast<double*>(w.QF.ptr), rows, Uh + r, hp, 1.0, X, rows);
   gemm(ctx, false, false, rows, keep, r, 1.0, V, rows, Vh, hq, 0.0, Y, rows);
   gemm(ctx, false, false, rows, keep, qg, 1.0, static_cast<double*>(w.QG.ptr), rows, Vh + r, hq, 1.0, Y, rows);
+  hp_.mark("update: rotate gemms");
   fix_signs(ctx, X, Y, rows, keep);
   sigma.resize(size_t(keep));
   PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));

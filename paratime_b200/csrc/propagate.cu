@@ -79,6 +79,15 @@ __device__ __forceinline__ double bfast(double uc, double ul, double ur, double 
   return fma(kx * p.ry, uu, kx * fma(p.cc, uc, fma(p.ry, ud, s1)));
 }
 
+// bfast<true> when ry == 1 (square cells): fma(1, ud, s1) == ud + s1 and kx * 1 == kx exactly,
+// so this is the same value with one multiply fewer
+template <bool RY1>
+__device__ __forceinline__ double bfast2(double uc, double ul, double ur, double uu, double ud, double kx,
+                                         const StepParams& p) {
+  if (!RY1) return bfast<true>(uc, ul, ur, uu, ud, kx, p);
+  return fma(kx, uu, kx * fma(p.cc, uc, ud + (ul + ur)));
+}
+
 __device__ __forceinline__ bool finite2(double a, double b) { return isfinite(a) && isfinite(b); }
 
 // 8-byte global -> shared asynchronous copy (LDGSTS), grouped by commit/wait
@@ -688,8 +697,9 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
 
-template <int S, int W, int PAR>
-__device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __restrict__ eR, const int mirror,
+template <int S, int W, int PAR, bool RY1>
+__device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __restrict__ eR, const int offl,
+                                           const int offr,
                                            const StepParams& p, double (&ulo)[S + 1][2], double (&uce)[S + 1][2],
                                            double (&vin)[S + 1][2], double (&kin)[S + 1][2], const double2 uu0,
                                            const double2 v0, const double2 k0, double2& out_u, double2& out_v) {
@@ -702,18 +712,16 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
   double nl[S + 1], nr[S + 1];  // left neighbour of col 0, right neighbour of col 1, per level
 #pragma unroll
   for (int t = 0; t <= S; ++t) {
-    nl[t] = rR[t * lstride - 1];
-    nr[t] = rL[t * lstride + 1];
+    nl[t] = rR[t * lstride + offl];
+    nr[t] = rL[t * lstride + offr];
   }
   double up0, up1, cv0, cv1, ck0, ck1;
   {
     const double uc0 = uce[0][0], uc1 = uce[0][1];
     wL[0] = uu0.x;
     wR[0] = uu0.y;
-    if (mirror < 0) wR[-W] = uu0.y;  // full-width strip: periodic pads (thread W-1 / thread 0)
-    if (mirror > 0) wL[W] = uu0.x;
-    const double vh0 = v0.x + bfast<true>(uc0, nl[0], uc1, uu0.x, ulo[0][0], k0.x, p);
-    const double vh1 = v0.y + bfast<true>(uc1, uc0, nr[0], uu0.y, ulo[0][1], k0.y, p);
+    const double vh0 = v0.x + bfast2<RY1>(uc0, nl[0], uc1, uu0.x, ulo[0][0], k0.x, p);
+    const double vh1 = v0.y + bfast2<RY1>(uc1, uc0, nr[0], uu0.y, ulo[0][1], k0.y, p);
     up0 = fma(p.dt, vh0, uc0);
     up1 = fma(p.dt, vh1, uc1);
     cv0 = vh0;
@@ -722,8 +730,6 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
     ck1 = k0.y;
     wL[lstride] = up0;
     wR[lstride] = up1;
-    if (mirror < 0) wR[lstride - W] = up1;
-    if (mirror > 0) wL[lstride + W] = up0;
     ulo[0][0] = uc0;
     ulo[0][1] = uc1;
     uce[0][0] = uu0.x;
@@ -733,8 +739,13 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
   double q0[S + 1], q1[S + 1];
 #pragma unroll
   for (int t = 1; t <= S; ++t) {
-    q0[t] = kin[t][0] * fma(p.cc, uce[t][0], fma(p.ry, ulo[t][0], nl[t] + uce[t][1]));
-    q1[t] = kin[t][1] * fma(p.cc, uce[t][1], fma(p.ry, ulo[t][1], uce[t][0] + nr[t]));
+    if (RY1) {
+      q0[t] = kin[t][0] * fma(p.cc, uce[t][0], ulo[t][0] + (nl[t] + uce[t][1]));
+      q1[t] = kin[t][1] * fma(p.cc, uce[t][1], ulo[t][1] + (uce[t][0] + nr[t]));
+    } else {
+      q0[t] = kin[t][0] * fma(p.cc, uce[t][0], fma(p.ry, ulo[t][0], nl[t] + uce[t][1]));
+      q1[t] = kin[t][1] * fma(p.cc, uce[t][1], fma(p.ry, ulo[t][1], uce[t][0] + nr[t]));
+    }
   }
 #pragma unroll
   for (int t = 1; t <= S; ++t) {
@@ -745,8 +756,8 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
     kin[t][1] = ck1;
     const double uu_0 = up0, uu_1 = up1;
     const double uc0 = uce[t][0], uc1 = uce[t][1];
-    const double b0 = fma(k0t * p.ry, uu_0, q0[t]);
-    const double b1 = fma(k1t * p.ry, uu_1, q1[t]);
+    const double b0 = fma(RY1 ? k0t : k0t * p.ry, uu_0, q0[t]);
+    const double b1 = fma(RY1 ? k1t : k1t * p.ry, uu_1, q1[t]);
     if (t < S) {
       const double vh0 = (vp0 + b0) + b0;
       const double vh1 = (vp1 + b1) + b1;
@@ -758,8 +769,6 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
       ck1 = k1t;
       wL[(t + 1) * lstride] = up0;
       wR[(t + 1) * lstride] = up1;
-      if (mirror < 0) wR[(t + 1) * lstride - W] = up1;
-      if (mirror > 0) wL[(t + 1) * lstride + W] = up0;
     } else {
       out_u = make_double2(uc0, uc1);
       out_v = make_double2(vp0 + b0, vp1 + b1);
@@ -771,18 +780,22 @@ __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __re
   }
 }
 
-template <int S, int W>
+// VAR: bit 0 = FULL (one strip spans the periodic row), bit 1 = RY1 (hy == hx)
+template <int S, int W, int VAR>
 __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
+  constexpr bool FULL = VAR & 1, RY1 = (VAR & 2) != 0;
   // even halo >= S + 1 (16-byte aligned pairs); none when the strip is the whole periodic row
-  const int HXE = a.full ? 0 : (S + 3) & ~1;
+  constexpr int HXE = FULL ? 0 : (S + 3) & ~1;
   constexpr int NL = S + 1;
   constexpr int UNROLL = 6, RING = 6;
   extern __shared__ double sm[];
   constexpr int T = W;
   const int j = threadIdx.x;
-  // full-width strip: thread W-1's right edge and thread 0's left edge are also stored in the
-  // pads of the opposite end, so x-neighbours wrap inside the CTA
-  const int mirror = !a.full ? 0 : (j == W - 1 ? -1 : (j == 0 ? 1 : 0));
+  // x-neighbour offsets into the edge rows: the left neighbour of column 2j is thread j-1's
+  // right edge, the right neighbour of column 2j+1 thread j+1's left edge; a full-width strip
+  // wraps them inside the CTA (thread 0 <-> thread W-1) instead of through halo columns
+  const int offl = FULL && j == 0 ? W - 1 : -1;
+  const int offr = FULL && j == W - 1 ? -(W - 1) : 1;
   const int nx = a.p.nx, ny = a.p.ny;
   const int npts = nx * ny;
   const int x0 = blockIdx.y * a.wu;  // even
@@ -825,8 +838,6 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     uce[0][1] = ce.y;
     eL[0] = ce.x;  // parity 0, level 0
     eR[0] = ce.y;
-    if (mirror < 0) eR[-W] = ce.y;
-    if (mirror > 0) eL[W] = ce.x;
   }
   int ou = wrap(ystart + 1), ov = wrap(ystart), oo = wrap(ystart - S);
   auto adv = [npts, nx](int& o) {
@@ -857,9 +868,9 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
       issue((k + RING - 1) % RING);
       double2 out_u, out_v;
       if (k & 1)
-        wave2_iter<S, W, 1>(eL, eR, mirror, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
+        wave2_iter<S, W, 1, RY1>(eL, eR, offl, offr, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
       else
-        wave2_iter<S, W, 0>(eL, eR, mirror, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
+        wave2_iter<S, W, 0, RY1>(eL, eR, offl, offr, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
       if (col_out && i >= 2 * S && i < last_out) {
         *reinterpret_cast<double2*>(UO + oo) = out_u;
         *reinterpret_cast<double2*>(VO + oo) = out_v;
@@ -1050,20 +1061,33 @@ size_t wave2_smem(int S, int W) {
 constexpr int kWave2Widths[] = {64, 96, 128, 160, 192, 256};
 
 template <int S, int W>
-const void* wave2_fn() {
-  return reinterpret_cast<const void*>(k_wave2<S, W>);
+const void* wave2_fn(int v) {
+  switch (v) {
+    case 0: return reinterpret_cast<const void*>(k_wave2<S, W, 0>);
+    case 1: return reinterpret_cast<const void*>(k_wave2<S, W, 1>);
+    case 2: return reinterpret_cast<const void*>(k_wave2<S, W, 2>);
+    default: return reinterpret_cast<const void*>(k_wave2<S, W, 3>);
+  }
 }
+// variant bits: FULL | RY1 << 1 (see k_wave2)
 template <int S>
-const void* wave2_kernel(int W) {
+const void* wave2_kernel(int W, int v) {
   switch (W) {
-    case 64: return wave2_fn<S, 64>();
-    case 96: return wave2_fn<S, 96>();
-    case 128: return wave2_fn<S, 128>();
-    case 160: return wave2_fn<S, 160>();
-    case 192: return wave2_fn<S, 192>();
-    case 256: return wave2_fn<S, 256>();
+    case 64: return wave2_fn<S, 64>(v);
+    case 96: return wave2_fn<S, 96>(v);
+    case 128: return wave2_fn<S, 128>(v);
+    case 160: return wave2_fn<S, 160>(v);
+    case 192: return wave2_fn<S, 192>(v);
+    case 256: return wave2_fn<S, 256>(v);
   }
   fail(PTB_UNSUPPORTED, "k_wave2 width");
+}
+inline int wave2_variant(const StepParams& p, int full) {
+  static const bool ry1_env = [] {  // PTB_WAVE_RY1=0: general-ry kernels only (diagnostics)
+    const char* e = std::getenv("PTB_WAVE_RY1");
+    return !e || std::atoi(e) != 0;
+  }();
+  return (full ? 1 : 0) | (ry1_env && p.ry == 1.0 ? 2 : 0);
 }
 
 template <int S>
@@ -1085,7 +1109,7 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
     if (wu_max < 16) continue;
     int occ = 0;
     const size_t smem = wave2_smem(S, W);
-    const void* kern = wave2_kernel<S>(W);
+    const void* kern = wave2_kernel<S>(W, full);  // occupancy: same registers for both RY variants
     PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     PTB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W, smem));
     if (occ < 1) continue;
@@ -1131,7 +1155,9 @@ void launch_wave2(ptb_context* ctx, cudaStream_t st, WaveArgs a, size_t batch) {
   a.full = pl.full;
   dim3 grid(static_cast<unsigned>(batch), pl.strips, pl.nrb);
   void* args[] = {&a};
-  PTB_CUDA_CHECK(cudaLaunchKernel(wave2_kernel<S>(pl.W), grid, dim3(pl.W), args, smem, st));
+  const void* kern = wave2_kernel<S>(pl.W, wave2_variant(a.p, pl.full));
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  PTB_CUDA_CHECK(cudaLaunchKernel(kern, grid, dim3(pl.W), args, smem, st));
   PTB_LAUNCH_CHECK(ctx);
 }
 

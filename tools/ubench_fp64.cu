@@ -1,97 +1,84 @@
-// Microbenchmark: fp64 pipe latency/throughput, shared-memory latency, barrier cost.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench_fp64 tools/ubench_fp64.cu
+// FP64 latency / throughput micro-benchmark (B200): dependent DFMA / DADD chains timed with
+// clock64 in one warp, and the per-SM DFMA rate with ILP chains x warps.
 #include <cstdio>
 #include <cuda_runtime.h>
 
-__global__ void dfma_latency(double* out, long long* cyc, int n) {
-  double a = out[0], m = 0.9999, c = 1e-9;
+template <int OP>
+__global__ void k_lat(double* out, double a, double b, int n, long long* cyc) {
+  double x = a + threadIdx.x;
   long long t0 = clock64();
   for (int i = 0; i < n; ++i) {
 #pragma unroll
-    for (int k = 0; k < 32; ++k) a = fma(a, m, c);
+    for (int k = 0; k < 16; ++k) {
+      if (OP == 0) x = fma(x, a, b);
+      else if (OP == 1) x = x + b;
+      else x = x * a;
+    }
   }
   long long t1 = clock64();
-  out[1] = a;
-  cyc[0] = t1 - t0;
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
 }
 
-__global__ void dadd_latency(double* out, long long* cyc, int n) {
-  double a = out[0], c = 1e-9;
-  long long t0 = clock64();
+template <int ILP>
+__global__ void k_tput(double* out, double a, double b, int n) {
+  double x[ILP];
+#pragma unroll
+  for (int k = 0; k < ILP; ++k) x[k] = a + threadIdx.x + k;
   for (int i = 0; i < n; ++i) {
 #pragma unroll
-    for (int k = 0; k < 32; ++k) a = a + c;
+    for (int k = 0; k < ILP; ++k) x[k] = fma(x[k], a, b);
   }
-  long long t1 = clock64();
-  out[1] = a;
-  cyc[0] = t1 - t0;
-}
-
-__global__ void lds_latency(double* out, long long* cyc, int n) {
-  __shared__ int idx[1024];
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) idx[i] = (i + 1) % 1024;
-  __syncthreads();
-  int p = 0;
-  long long t0 = clock64();
-  for (int i = 0; i < n; ++i) {
-#pragma unroll
-    for (int k = 0; k < 32; ++k) p = idx[p];
-  }
-  long long t1 = clock64();
-  out[1] = p;
-  cyc[0] = t1 - t0;
-}
-
-// per-warp chain of `chains` independent dfma sequences: throughput vs ILP
-template <int CH>
-__global__ void dfma_ilp(double* out, long long* cyc, int n) {
-  double a[CH];
-#pragma unroll
-  for (int k = 0; k < CH; ++k) a[k] = out[0] + k;
-  long long t0 = clock64();
-  for (int i = 0; i < n; ++i) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int k = 0; k < CH; ++k) a[k] = fma(a[k], 0.9999, 1e-9);
-  }
-  long long t1 = clock64();
   double s = 0;
 #pragma unroll
-  for (int k = 0; k < CH; ++k) s += a[k];
-  if (threadIdx.x == 0 && blockIdx.x == 0) { out[1] = s; cyc[0] = t1 - t0; }
-}
-
-__global__ void bar_cost(double* out, long long* cyc, int n) {
-  long long t0 = clock64();
-  for (int i = 0; i < n; ++i) __syncthreads();
-  long long t1 = clock64();
-  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+  for (int k = 0; k < ILP; ++k) s += x[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
 int main() {
-  double* d; long long* c; long long h;
-  cudaMalloc(&d, 64); cudaMalloc(&c, 64);
-  cudaMemset(d, 0, 64);
-  const int n = 1000;
-  dfma_latency<<<1, 1>>>(d, c, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-  printf("DFMA dependent latency: %.2f cycles\n", double(h) / (n * 32));
-  dadd_latency<<<1, 1>>>(d, c, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-  printf("DADD dependent latency: %.2f cycles\n", double(h) / (n * 32));
-  lds_latency<<<1, 32>>>(d, c, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-  printf("LDS dependent latency: %.2f cycles\n", double(h) / (n * 32));
-  for (int w : {1, 2, 4, 8, 16}) {
-    dfma_ilp<1><<<1, 32 * w>>>(d, c, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-    double per = double(h) / (n * 8);
-    dfma_ilp<4><<<1, 32 * w>>>(d, c, n); long long h4; cudaMemcpy(&h4, c, 8, cudaMemcpyDeviceToHost);
-    dfma_ilp<8><<<1, 32 * w>>>(d, c, n); long long h8; cudaMemcpy(&h8, c, 8, cudaMemcpyDeviceToHost);
-    printf("warps/SM %2d: ILP1 %.2f cyc/dfma-round, ILP4 %.2f, ILP8 %.2f  (per warp-instr: %.2f %.2f %.2f)\n", w, per,
-           double(h4) / (n * 8), double(h8) / (n * 8), per / w, double(h4) / (n * 8) / (4 * w), double(h8) / (n * 8) / (8 * w));
+  double* out;
+  long long* cyc;
+  cudaMalloc(&out, 1 << 26);
+  cudaMalloc(&cyc, 8);
+  const int n = 4096;
+  const char* names[3] = {"DFMA", "DADD", "DMUL"};
+  for (int op = 0; op < 3; ++op) {
+    for (int rep = 0; rep < 2; ++rep) {
+      if (op == 0) k_lat<0><<<1, 32>>>(out, 0.999, 1e-3, n, cyc);
+      if (op == 1) k_lat<1><<<1, 32>>>(out, 0.999, 1e-3, n, cyc);
+      if (op == 2) k_lat<2><<<1, 32>>>(out, 0.999, 1e-3, n, cyc);
+    }
+    long long c;
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%s dependent latency: %.2f cycles\n", names[op], double(c) / (16.0 * n));
   }
-  for (int w : {4, 8, 16}) {
-    bar_cost<<<1, 32 * w>>>(d, c, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-    printf("__syncthreads with %d warps: %.1f cycles\n", w, double(h) / n);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int clk;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 1 << 14;
+  for (int warps : {1, 2, 4, 8, 16, 32}) {
+    for (int ilp : {1, 2, 4, 8}) {
+      auto launch = [&] {
+        if (ilp == 1) k_tput<1><<<sms, 32 * warps>>>(out, 0.999, 1e-3, iters);
+        if (ilp == 2) k_tput<2><<<sms, 32 * warps>>>(out, 0.999, 1e-3, iters);
+        if (ilp == 4) k_tput<4><<<sms, 32 * warps>>>(out, 0.999, 1e-3, iters);
+        if (ilp == 8) k_tput<8><<<sms, 32 * warps>>>(out, 0.999, 1e-3, iters);
+      };
+      launch();
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double fmas = double(sms) * 32 * warps * ilp * iters;
+      printf("warps/SM %2d ilp %d: %.2f TFLOP/s  (%.2f DFMA warp-instr/clk/SM at %d MHz)\n", warps, ilp,
+             2 * fmas / (ms * 1e-3) / 1e12, fmas / 32 / (ms * 1e-3) / sms / (clk * 1e3), clk / 1000);
+    }
   }
-  cudaError_t e = cudaDeviceSynchronize();
-  printf("status %s\n", cudaGetErrorString(e));
+  return 0;
 }
