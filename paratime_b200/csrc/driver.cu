@@ -148,39 +148,63 @@ __global__ void __launch_bounds__(256) k_gemv_t1(size_t rows, size_t chunk, cons
   if (threadIdx.x == 0) z[size_t(blockIdx.x) * gridDim.y + blockIdx.y] = s;
 }
 
-int gemv_parts(size_t rows) { return int(std::max<size_t>(1, std::min<size_t>(64, rows / 4096))); }
+int gemv_parts(size_t rows) { return int(std::max<size_t>(1, std::min<size_t>(64, rows / 2048))); }
 
 // corrected difference on the coarse grid (one launch): dz = z_w - z_old (z_old nullable),
-// du = Zu dz + (m_w - m_old)/N_c, dv = Zv dz  (Zu, Zv: N_c x r column-major)
-__global__ void __launch_bounds__(256) k_assemble_d(size_t nc, int r, const double* Zu, const double* Zv,
-                                                    const double* zw, int zparts, const double* zold,
-                                                    const double* mw, const double* mold, double* du, double* dv) {
-  extern __shared__ double dz[];
-  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+// du = Zu dz + (m_w - m_old)/N_c, dv = Zv dz  (Zu, Zv: N_c x r column-major).
+// Block = AD_I consecutive points x AD_J column groups: group g sums columns j = g, g + AD_J, ...
+// (all loads of a thread independent, coalesced across the AD_I points), then the AD_J partials
+// are added in a fixed tree order -- the result depends on (nc, r) only.
+constexpr int AD_I = 32, AD_J = 8;
+__global__ void __launch_bounds__(AD_I * AD_J) k_assemble_d(size_t nc, int r, const double* Zu, const double* Zv,
+                                                          const double* zw, int zparts, const double* zold,
+                                                          const double* mw, const double* mold, double* du,
+                                                          double* dv) {
+  extern __shared__ double dz[];  // r, then [2][AD_J][AD_I] partials
+  const int tid = threadIdx.y * AD_I + threadIdx.x;
+  for (int j = tid; j < r; j += AD_I * AD_J) {
     double zj = 0.0;  // z_w[j] = sum of its partials, in order
     for (int q = 0; q < zparts; ++q) zj += zw[size_t(j) * zparts + q];
     dz[j] = zold ? __dsub_rn(zj, zold[j]) : zj;
   }
   __syncthreads();
-  const double dm = mold ? __dsub_rn(*mw, *mold) : *mw;
-  const double add = dm / double(nc);
-  GRID_STRIDE(i, nc) {
-    // four independent accumulators per output (loads of four columns in flight), fixed order
-    double su[4] = {0.0, 0.0, 0.0, 0.0}, sv[4] = {0.0, 0.0, 0.0, 0.0};
-    int j = 0;
-    for (; j + 3 < r; j += 4) {
+  double* pu = dz + ((r + 1) & ~1);
+  double* pv = pu + AD_J * AD_I;
+  const size_t i = size_t(blockIdx.x) * AD_I + threadIdx.x;
+  double su0 = 0.0, su1 = 0.0, sv0 = 0.0, sv1 = 0.0;
+  if (i < nc) {
+    int j = threadIdx.y;
+    for (; j + AD_J < r; j += 2 * AD_J) {
+      su0 = fma(Zu[size_t(j) * nc + i], dz[j], su0);
+      sv0 = fma(Zv[size_t(j) * nc + i], dz[j], sv0);
+      su1 = fma(Zu[size_t(j + AD_J) * nc + i], dz[j + AD_J], su1);
+      sv1 = fma(Zv[size_t(j + AD_J) * nc + i], dz[j + AD_J], sv1);
+    }
+    if (j < r) {
+      su0 = fma(Zu[size_t(j) * nc + i], dz[j], su0);
+      sv0 = fma(Zv[size_t(j) * nc + i], dz[j], sv0);
+    }
+  }
+  pu[threadIdx.y * AD_I + threadIdx.x] = su0 + su1;
+  pv[threadIdx.y * AD_I + threadIdx.x] = sv0 + sv1;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < nc) {
+    double a[AD_J], b[AD_J];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        su[q] = fma(Zu[size_t(j + q) * nc + i], dz[j + q], su[q]);
-        sv[q] = fma(Zv[size_t(j + q) * nc + i], dz[j + q], sv[q]);
+    for (int g = 0; g < AD_J; ++g) {
+      a[g] = pu[g * AD_I + threadIdx.x];
+      b[g] = pv[g * AD_I + threadIdx.x];
+    }
+#pragma unroll
+    for (int w = AD_J / 2; w > 0; w >>= 1)
+#pragma unroll
+      for (int g = 0; g < w; ++g) {
+        a[g] += a[g + w];
+        b[g] += b[g + w];
       }
-    }
-    for (; j < r; ++j) {
-      su[0] = fma(Zu[size_t(j) * nc + i], dz[j], su[0]);
-      sv[0] = fma(Zv[size_t(j) * nc + i], dz[j], sv[0]);
-    }
-    du[i] = ((su[0] + su[1]) + (su[2] + su[3])) + add;
-    dv[i] = (sv[0] + sv[1]) + (sv[2] + sv[3]);
+    const double dm = mold ? __dsub_rn(*mw, *mold) : *mw;
+    du[i] = a[0] + dm / double(nc);
+    dv[i] = b[0];
   }
 }
 
@@ -644,7 +668,8 @@ struct Driver {
                   double* du, double* dv) {
     const int r = c.rank;
     if (fused_sweep(c)) {
-      k_assemble_d<<<blocks(ctx, nc), 256, size_t(std::max(r, 1)) * sizeof(double), st()>>>(
+      const size_t smem = (size_t(r + 1) + 2 * AD_J * AD_I) * sizeof(double);
+      k_assemble_d<<<unsigned((nc + AD_I - 1) / AD_I), dim3(AD_I, AD_J), smem, st()>>>(
           nc, r, static_cast<double*>(Zu.ptr), static_cast<double*>(Zv.ptr), zw_, zw_parts, zold_, mw, mold, du,
           dv);
       PTB_LAUNCH_CHECK(ctx);

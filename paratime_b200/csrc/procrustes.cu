@@ -536,6 +536,48 @@ __global__ void __launch_bounds__(256) k_wy_larft(const double* S, const double*
   }
 }
 
+// The same T by recursive doubling instead of the column recurrence (k <= WY_TREE_MAX): for
+// adjacent factored blocks [i0, i0 + b) and [i0 + b, i1),
+//   (I - V1 T1 V1^T)(I - V2 T2 V2^T) = I - [V1 V2] [[T1, -T1 S12 T2], [0, T2]] [V1 V2]^T,
+// so every level b = 1, 2, 4, ... forms all its off-diagonal blocks T12 = -T11 (S12 T22) in
+// parallel (two barriers per level, log2 k levels; tau = 0 needs no special case).  T and the
+// W = S12 T22 scratch live in shared memory.
+constexpr int WY_TREE_MAX = 112;
+__global__ void __launch_bounds__(1024) k_wy_larft_tree(const double* S, const double* tau, int k, double* Tout) {
+  extern __shared__ double tsm[];
+  double* T = tsm;          // k x k, column-major
+  double* W = tsm + k * k;  // S12 T22 at the positions of T12
+  const int kk = k * k;
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+    const int c = e / k, r = e - c * k;
+    T[e] = r == c ? tau[c] : 0.0;
+  }
+  __syncthreads();
+  for (int b = 1; b < k; b *= 2) {
+    const int b2x = 2 * b;
+    for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+      const int c = e / k, r = e - c * k;
+      const int i0 = (r / b2x) * b2x;
+      if (c / b2x * b2x != i0 || r - i0 >= b || c - i0 < b) continue;  // not in this level's T12
+      const int j0 = i0 + b;  // W[r][c] = sum_{l = j0}^{c} S[r][l] T[l][c]  (T22 upper)
+      double acc = 0.0;
+      for (int l = j0; l <= c; ++l) acc = fma(S[size_t(l) * k + r], T[c * k + l], acc);
+      W[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+      const int c = e / k, r = e - c * k;
+      const int i0 = (r / b2x) * b2x;
+      if (c / b2x * b2x != i0 || r - i0 >= b || c - i0 < b) continue;
+      double acc = 0.0;  // T12[r][c] = -sum_{l = r}^{i0 + b - 1} T[r][l] W[l][c]  (T11 upper)
+      for (int l = r; l < i0 + b; ++l) acc = fma(T[l * k + r], W[c * k + l], acc);
+      T[e] = -acc;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) Tout[e] = T[e];
+}
+
 // blocked QR helpers: a panel's unit lower-trapezoidal reflectors (rows c0.., ld lda) into V
 // (same offsets, ld lda), and the upper triangle of the leading n x n block.
 __global__ void k_panel_v(const double* A, int lda, int mp, int w, double* V) {
@@ -999,6 +1041,8 @@ ProcWork::~ProcWork() {
   for (auto& b : buf) b.release();
   for (DeviceBuffer* b : {&QF, &RF, &QG, &RG, &Uh, &Vh, &PQ, &PR, &PU, &SX, &SY, &BA, &BV, &BT, &BR, &BQ2})
     b->release();
+  for (auto& b : TS) b.release();
+  for (auto& b : TX) b.release();
 }
 
 DevCorrector::~DevCorrector() {
@@ -1015,6 +1059,329 @@ void DevCorrector::assign(int rows_, int rank_, const std::vector<double>& s, do
   double* d = static_cast<double*>(Sd.get(std::max<size_t>(1, S.size()) * sizeof(double)));
   if (!S.empty())
     PTB_CUDA_CHECK(cudaMemcpy(d, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+void wy_larft(ptb_context* ctx, cudaStream_t st, const double* S, const double* tau, int k, double* T) {
+  if (k <= WY_TREE_MAX) {
+    const size_t smem = size_t(2) * k * k * sizeof(double);
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_wy_larft_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_wy_larft_tree<<<1, 1024, smem, st>>>(S, tau, k, T);
+  } else {
+    k_wy_larft<<<1, 256, size_t(k) * sizeof(double), st>>>(S, tau, k, T);
+  }
+  PTB_LAUNCH_CHECK(ctx);
+}
+
+// ---- TSQR: tall-skinny QR as a reduction tree (n <= TS_MAXN) ------------------------------
+// Level l splits its m_l rows into nb_l leaves of <= TS_ROWS rows (sizes differ by at most one,
+// so every leaf has >= TS_ROWS / 2 >= n rows); each leaf is an unpivoted Householder QR in one
+// CTA's shared memory (no grid barrier), its n x n R goes into the next level's stack
+// (nb_l n rows).  When the stack fits one leaf, its column-pivoted QR (k_qrcp_small, the
+// reference's keep rule) gives the pivots, keep and R -- column norms are invariant under the
+// leaves' orthogonal factors, so these are A's own pivoted-QR decisions up to rounding, as in
+// the blocked route -- and the thin Q is assembled top-down, each leaf applying its reflectors
+// to its n-row slice of the level above (padded with zeros to the leaf's rows).  Leaves are
+// k_qr_reg<.., TS = true> (below), the down-sweep k_tsqr_apply4.
+constexpr int TS_ROWS = 256, TS_MAXN = 64;
+
+__device__ __forceinline__ int ts_row0(int i, int m, int nb) { return int((long long)i * m / nb); }
+
+// ---- register-resident Householder QR of a small block (one CTA) -------------------------
+// Column k lives in the registers of warp k % QRR_WARPS (slot k / QRR_WARPS); lane l holds rows
+// l + 32 u.  Per step j: every warp picks the same pivot (PIVOT: largest remaining squared norm,
+// first position on ties, positions swapped as dgeqp3 swaps columns -- each warp keeps its own
+// copy of the position table), the pivot's owner forms the reflector (dlarfg: beta, tau, scal)
+// and publishes the column through shared memory, then every warp applies H_j to its own
+// columns from registers and (PIVOT) recomputes their exact squared norms below row j.  Two
+// barriers per step; no shared-memory traffic for the trailing matrix.  Keep rule, outputs and
+// layout as k_qrcp_small (TS = false: pivoted columns in place, R above and beta on the
+// diagonal, scaled reflectors below; TS = true: a TSQR leaf -- reflectors to V, R to the stack).
+constexpr int QRR_THREADS = 512, QRR_WARPS = QRR_THREADS / 32;
+
+struct QrRegArgs {
+  const double* A;  // input columns, ld lda; TS: this leaf's rows start at ts_row0(blockIdx.x)
+  int lda, m, n, nb;
+  int pivot;
+  double drop_tol;
+  double* out;  // !TS: pivoted factor, m x n, ld m
+  double* V;    // TS: reflectors, ld ldv (rows of the leaf)
+  int ldv;
+  double* R;    // TS: stack, ld ldr (leaf i at rows i n)
+  int ldr;
+  double* tau;  // !TS: n; TS: nb x n
+  int* perm;
+  int* keep_out;
+  double* beta_out;
+};
+
+template <int CPW, int RPL, bool PIVOT, bool TS>
+__global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
+  constexpr int NMAX = CPW * QRR_WARPS, MMAX = 32 * RPL;
+  __shared__ double cbuf[MMAX];
+  __shared__ double nrm[2][NMAX];
+  __shared__ double betas[NMAX], scals[NMAX];
+  __shared__ double s_sc[3];
+  __shared__ int posc[PIVOT ? QRR_WARPS : 1][PIVOT ? NMAX : 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = a.n;
+  int r0 = 0, m = a.m;
+  if (TS) {
+    r0 = ts_row0(blockIdx.x, a.m, a.nb);
+    m = ts_row0(blockIdx.x + 1, a.m, a.nb) - r0;
+  }
+  double x[CPW][RPL];
+  int estep[CPW];  // step at which the column was eliminated (-1: not yet)
+#pragma unroll
+  for (int s = 0; s < CPW; ++s) {
+    const int k = warp + QRR_WARPS * s;
+    estep[s] = -1;
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int r = lane + 32 * u;
+      x[s][u] = (k < n && r < m) ? a.A[size_t(k) * a.lda + r0 + r] : 0.0;
+    }
+    if (PIVOT && k < n) {
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) acc = fma(x[s][u], x[s][u], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) nrm[0][k] = acc;
+    }
+  }
+  if (PIVOT)
+    for (int q = lane; q < n; q += 32) posc[warp][q] = q;
+  __syncthreads();
+  const int steps = min(m, n);
+  int keep = steps;
+  for (int j = 0; j < steps; ++j) {
+    const int par = j & 1;
+    int p = j;
+    if (PIVOT) {
+      double best = -1.0;
+      int bpos = n;
+      for (int q = j + lane; q < n; q += 32) {
+        const double v = nrm[par][posc[warp][q]];
+        if (v > best) {
+          best = v;
+          bpos = q;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bpos, o);
+        if (ob > best || (ob == best && oi < bpos)) {
+          best = ob;
+          bpos = oi;
+        }
+      }
+      p = posc[warp][bpos];
+      __syncwarp();
+      if (lane == 0) {
+        posc[warp][bpos] = posc[warp][j];
+        posc[warp][j] = p;
+      }
+      __syncwarp();
+    }
+    if (warp == p % QRR_WARPS) {  // the pivot's owner: dlarfg, publish the column
+#pragma unroll
+      for (int s = 0; s < CPW; ++s) {
+        if (s != p / QRR_WARPS) continue;
+        double xs = 0.0, alc = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int r = lane + 32 * u;
+          if (r > j) xs = fma(x[s][u], x[s][u], xs);
+          if (u == j / 32) alc = x[s][u];
+          cbuf[r] = x[s][u];
+        }
+        xs = warp_sum(xs);
+        const double al = __shfl_sync(0xffffffffu, alc, j & 31);
+        estep[s] = j;
+        if (lane == 0) {
+          const double xnorm = sqrt(xs);
+          double beta, tau, scal;
+          if (xnorm == 0.0) {
+            beta = al;
+            tau = 0.0;
+            scal = 0.0;
+          } else {
+            beta = -copysign(hypot(al, xnorm), al);
+            tau = (beta - al) / beta;
+            scal = 1.0 / (al - beta);
+          }
+          s_sc[0] = beta;
+          s_sc[1] = tau;
+          s_sc[2] = scal;
+        }
+      }
+    }
+    __syncthreads();
+    const double beta = s_sc[0], tau = s_sc[1], scal = s_sc[2];
+    if (fabs(beta) <= a.drop_tol) {  // first pivot at or below the guard: keep = j
+      if (tid == 0 && a.beta_out) a.beta_out[j] = fabs(beta);
+      keep = j;
+#pragma unroll
+      for (int s = 0; s < CPW; ++s)
+        if (estep[s] == j) estep[s] = -1;
+      break;
+    }
+    if (tid == 0) {
+      betas[j] = beta;
+      scals[j] = scal;
+      if (TS) a.tau[size_t(blockIdx.x) * n + j] = tau;
+      else a.tau[j] = tau;
+      if (!TS && a.beta_out) a.beta_out[j] = fabs(beta);
+    }
+    double v[RPL];
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int r = lane + 32 * u;
+      v[u] = r > j ? cbuf[r] * scal : (r == j ? 1.0 : 0.0);
+    }
+    double w[CPW];
+#pragma unroll
+    for (int s = 0; s < CPW; ++s) {
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) acc = fma(v[u], x[s][u], acc);
+      w[s] = acc;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int s = 0; s < CPW; ++s) w[s] += __shfl_xor_sync(0xffffffffu, w[s], o);
+    double nn[CPW];
+#pragma unroll
+    for (int s = 0; s < CPW; ++s) {
+      const int k = warp + QRR_WARPS * s;
+      nn[s] = 0.0;
+      if (k >= n || estep[s] >= 0) continue;  // eliminated columns keep their R entries
+      const double tw = tau * w[s];
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int r = lane + 32 * u;
+        x[s][u] = fma(-tw, v[u], x[s][u]);
+        if (PIVOT && r > j) nn[s] = fma(x[s][u], x[s][u], nn[s]);
+      }
+    }
+    if (PIVOT) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int s = 0; s < CPW; ++s) nn[s] += __shfl_xor_sync(0xffffffffu, nn[s], o);
+      if (lane == 0)
+#pragma unroll
+        for (int s = 0; s < CPW; ++s) {
+          const int k = warp + QRR_WARPS * s;
+          if (k < n) nrm[par ^ 1][k] = nn[s];
+        }
+    }
+    __syncthreads();
+  }
+  // outputs: each warp writes its own columns
+#pragma unroll
+  for (int s = 0; s < CPW; ++s) {
+    const int k = warp + QRR_WARPS * s;
+    if (k >= n) continue;
+    int pos = k;
+    if (PIVOT)
+      for (int q = 0; q < n; ++q)
+        if (posc[warp][q] == k) pos = q;
+    const int e = estep[s];
+    if (TS) {
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int r = lane + 32 * u;
+        if (r >= m) continue;
+        if (r > k) a.V[size_t(k) * a.ldv + r0 + r] = x[s][u] * scals[k];
+        if (r < n) a.R[size_t(k) * a.ldr + size_t(blockIdx.x) * n + r] = r < k ? x[s][u] : (r == k ? betas[k] : 0.0);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int r = lane + 32 * u;
+        if (r >= m) continue;
+        double val = x[s][u];
+        if (e >= 0 && r == e) val = betas[e];
+        else if (e >= 0 && r > e) val = x[s][u] * scals[e];
+        a.out[size_t(pos) * m + r] = val;
+      }
+      if (lane == 0) a.perm[pos] = k;
+    }
+  }
+  if (!TS && tid == 0) *a.keep_out = keep;
+}
+
+// Xout[leaf rows, :] = H_0 ... H_{n-1} [Xin[i n : i n + n, :]; 0] -- one warp per four columns of
+// X held in registers (the reflector is read once for all four), the four dot products reduced
+// together (transposed butterfly: 6 double shuffles instead of 20, then 4 broadcasts)
+__global__ void __launch_bounds__(QRR_THREADS) k_tsqr_apply4(const double* V, int m, int n, int nb, const double* tau,
+                                                             const double* Xin, int ldin, int kq, double* Xout,
+                                                             int ldout) {
+  extern __shared__ double tv[];  // reflectors rows x n (unit diagonal, zeros above) | tau[n]
+  constexpr int PL = TS_ROWS / 32;
+  const int i = blockIdx.x, r0 = ts_row0(i, m, nb), rows = ts_row0(i + 1, m, nb) - r0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* tt = tv + size_t(rows) * n;
+  for (int e = tid; e < rows * n; e += blockDim.x) {
+    const int c = e / rows, r = e - c * rows;
+    tv[e] = r > c ? V[size_t(c) * m + r0 + r] : (r == c ? 1.0 : 0.0);
+  }
+  for (int c = tid; c < n; c += blockDim.x) tt[c] = tau[size_t(i) * n + c];
+  __syncthreads();
+  for (int q0 = 4 * warp; q0 < kq; q0 += 4 * QRR_WARPS) {
+    double y[4][PL];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int u = 0; u < PL; ++u) {
+        const int r = lane + 32 * u;
+        y[c][u] = (r < n && q0 + c < kq) ? Xin[size_t(q0 + c) * ldin + size_t(i) * n + r] : 0.0;
+      }
+    const bool b4 = lane & 16, b3 = lane & 8;
+    for (int j = n - 1; j >= 0; --j) {
+      const double* vj = tv + size_t(j) * rows;
+      double vr[PL];
+#pragma unroll
+      for (int u = 0; u < PL; ++u) {
+        const int r = lane + 32 * u;
+        vr[u] = (r < rows && r >= j) ? vj[r] : 0.0;
+      }
+      double s[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int u = 0; u < PL; ++u) acc = fma(vr[u], y[c][u], acc);
+        s[c] = acc;
+      }
+      // xor 16: keep columns {0,1} (bit 4 clear) or {2,3}
+      const double k0 = b4 ? s[2] : s[0], k1 = b4 ? s[3] : s[1];
+      const double g0 = b4 ? s[0] : s[2], g1 = b4 ? s[1] : s[3];
+      const double t0 = k0 + __shfl_xor_sync(0xffffffffu, g0, 16);
+      const double t1 = k1 + __shfl_xor_sync(0xffffffffu, g1, 16);
+      // xor 8: keep column 2 b4 + b3
+      const double kk = b3 ? t1 : t0, gg = b3 ? t0 : t1;
+      double t = kk + __shfl_xor_sync(0xffffffffu, gg, 8);
+      t += __shfl_xor_sync(0xffffffffu, t, 4);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      const double tj = tt[j];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double tw = tj * __shfl_sync(0xffffffffu, t, 8 * c);
+#pragma unroll
+        for (int u = 0; u < PL; ++u) y[c][u] = fma(-tw, vr[u], y[c][u]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int u = 0; u < PL; ++u) {
+        const int r = lane + 32 * u;
+        if (r < rows && q0 + c < kq) Xout[size_t(q0 + c) * ldout + r0 + r] = y[c][u];
+      }
+  }
 }
 
 // truncated_qr (procrustes.cpp:34-46): Q (m x keep) and R (keep x n, un-pivoted) in
@@ -1040,7 +1407,14 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
     const char* e = std::getenv("PTB_QR_SMALL");
     return !(e && std::atoi(e) == 0);
   }();
-  if (small_env && small_smem <= 200 * 1024) {
+  const int reg = !small_env ? 0 : (m <= 128 && n <= 64) ? 1 : (m <= 256 && n <= 64) ? 2 : (m <= 128 && n <= 128) ? 3 : 0;
+  if (reg) {  // register-resident pivoted QR (one CTA, two barriers per column)
+    QrRegArgs ra{A, m, m, n, 0, 1, drop_tol, A, nullptr, 0, nullptr, 0, tau, perm, keep_d, betas};
+    if (reg == 1) k_qr_reg<4, 4, true, false><<<1, QRR_THREADS, 0, st>>>(ra);
+    else if (reg == 2) k_qr_reg<4, 8, true, false><<<1, QRR_THREADS, 0, st>>>(ra);
+    else k_qr_reg<8, 4, true, false><<<1, QRR_THREADS, 0, st>>>(ra);
+    PTB_LAUNCH_CHECK(ctx);
+  } else if (small_env && small_smem <= 200 * 1024) {
     QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, nullptr, keep_d, betas};
     PTB_CUDA_CHECK(
         cudaFuncSetAttribute(k_qrcp_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(small_smem)));
@@ -1083,8 +1457,7 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
                                                                                                       V, Q);
     PTB_LAUNCH_CHECK(ctx);
     gemm(ctx, true, false, keep, keep, m, 1.0, V, m, V, m, 0.0, S, keep);  // S = V^T V
-    k_wy_larft<<<1, 256, size_t(keep) * sizeof(double), st>>>(S, tau, keep, T);
-    PTB_LAUNCH_CHECK(ctx);
+    wy_larft(ctx, st, S, tau, keep, T);
     gemm(ctx, false, true, keep, keep, keep, 1.0, T, keep, V, m, 0.0, W, keep);  // W = T V1^T
     gemm(ctx, false, false, m, keep, keep, -1.0, V, m, W, keep, 1.0, Q, m);     // Q = E - V W
     k_unpivot_r<<<std::max(1, std::min(256, (keep * n + 255) / 256)), 256, 0, st>>>(A, m, n, keep, perm, R);
@@ -1181,8 +1554,7 @@ int truncated_qr_blocked(ProcWork& w, const double* A_in, int m, int n, double d
     PTB_LAUNCH_CHECK(ctx);
     double* Tp = Tall + size_t(p) * QB * QB;
     gemm(ctx, true, false, wd, wd, mp, 1.0, Vp, m, Vp, m, 0.0, S, wd);  // S = Vp^T Vp
-    k_wy_larft<<<1, 256, size_t(wd) * sizeof(double), st>>>(S, tau + c0, wd, Tp);
-    PTB_LAUNCH_CHECK(ctx);
+    wy_larft(ctx, st, S, tau + c0, wd, Tp);
     if (nr > 0) {  // A_trail -= Vp (Tp^T (Vp^T A_trail))
       double* At = A + size_t(c0 + wd) * m + c0;
       gemm(ctx, true, false, wd, nr, mp, 1.0, Vp, m, At, m, 0.0, W1, wd);
@@ -1215,12 +1587,72 @@ int truncated_qr_blocked(ProcWork& w, const double* A_in, int m, int n, double d
   return kq;
 }
 
+// TSQR route of truncated_qr (see the TSQR note above k_qr_reg): up-sweep of leaf QRs, the pivoted QR of the
+// last stack with the reference's keep rule, then the down-sweep forming Q = Q_0 ... Q_L Q_top.
+int truncated_qr_tsqr(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb,
+                      DeviceBuffer& Rb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  struct Level {
+    int m, nb;
+    double *V, *tau;
+  };
+  std::vector<Level> lv;
+  const double* cur = A_in;
+  int curm = m, ld = m;
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(k_tsqr_apply4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int((size_t(TS_ROWS) * TS_MAXN + TS_MAXN) * sizeof(double))));
+  while (curm > TS_ROWS) {
+    const int L = int(lv.size());
+    if (3 * L + 2 >= int(sizeof(w.TS) / sizeof(w.TS[0]))) fail(PTB_UNSUPPORTED, "truncated_qr: TSQR depth");
+    const int nb = (curm + TS_ROWS - 1) / TS_ROWS;
+    const int rows_max = (curm + nb - 1) / nb;
+    double* V = static_cast<double*>(w.TS[3 * L].get(size_t(curm) * n * sizeof(double)));
+    double* tau = static_cast<double*>(w.TS[3 * L + 1].get(size_t(nb) * n * sizeof(double)));
+    double* S = static_cast<double*>(w.TS[3 * L + 2].get(size_t(nb) * n * n * sizeof(double)));
+    (void)rows_max;
+    QrRegArgs la{cur, ld, curm, n, nb, 0, -1.0, nullptr, V, curm, S, nb * n, tau, nullptr, nullptr, nullptr};
+    k_qr_reg<4, 8, false, true><<<unsigned(nb), QRR_THREADS, 0, st>>>(la);
+    PTB_LAUNCH_CHECK(ctx);
+    lv.push_back(Level{curm, nb, V, tau});
+    cur = S;
+    curm = nb * n;
+    ld = curm;
+  }
+  const int kq = truncated_qr_direct(w, cur, curm, n, drop_tol, w.BQ2, Rb);
+  double* Q = static_cast<double*>(Qb.get(std::max<size_t>(1, size_t(m) * kq) * sizeof(double)));
+  if (kq == 0) return 0;
+  const double* X = static_cast<const double*>(w.BQ2.ptr);
+  int ldx = curm;
+  for (int l = int(lv.size()) - 1; l >= 0; --l) {
+    const Level& L = lv[size_t(l)];
+    double* out = l == 0 ? Q : static_cast<double*>(w.TX[l & 1].get(size_t(L.m) * kq * sizeof(double)));
+    const int rows_max = (L.m + L.nb - 1) / L.nb;
+    k_tsqr_apply4<<<unsigned(L.nb), QRR_THREADS, (size_t(rows_max) * n + n) * sizeof(double), st>>>(
+        L.V, L.m, n, L.nb, L.tau, X, ldx, kq, out, L.m);
+    PTB_LAUNCH_CHECK(ctx);
+    X = out;
+    ldx = L.m;
+  }
+  if (lv.empty())
+    PTB_CUDA_CHECK(cudaMemcpyAsync(Q, X, size_t(m) * kq * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return kq;
+}
+
 int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb, DeviceBuffer& Rb) {
-  static const int env = [] {  // PTB_QR=direct forces the unblocked pivoted kernel
+  // PTB_QR=direct | blocked | tsqr forces a route (tests, diagnostics)
+  static const int env = [] {
     const char* e = std::getenv("PTB_QR");
-    return e && std::string(e) == "direct" ? 1 : 0;
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "direct" ? 1 : v == "blocked" ? 2 : v == "tsqr" ? 3 : 0;
   }();
-  if (env == 0 && n > QB && m >= 8 * n) return truncated_qr_blocked(w, A_in, m, n, drop_tol, Qb, Rb);
+  const bool tall = m >= 8 * n && m > TS_ROWS;
+  if (env == 1) return truncated_qr_direct(w, A_in, m, n, drop_tol, Qb, Rb);
+  if (env == 3 && tall && n <= TS_MAXN) return truncated_qr_tsqr(w, A_in, m, n, drop_tol, Qb, Rb);
+  if (env == 2 && tall && n > 1) return truncated_qr_blocked(w, A_in, m, n, drop_tol, Qb, Rb);
+  if (env == 0 && tall && n <= TS_MAXN && m > 1024) return truncated_qr_tsqr(w, A_in, m, n, drop_tol, Qb, Rb);
+  if (env == 0 && tall && n > QB) return truncated_qr_blocked(w, A_in, m, n, drop_tol, Qb, Rb);
   return truncated_qr_direct(w, A_in, m, n, drop_tol, Qb, Rb);
 }
 

@@ -31,6 +31,7 @@ struct ProcWork {
   DeviceBuffer PQ, PR, PU;  // thin_svd preconditioning: Q, R of the QR and U of R^T
   DeviceBuffer SX, SY;      // spare corrector factors: update_svd writes here, then swaps
   DeviceBuffer BA, BV, BT, BR, BQ2;  // blocked tall QR: work copy, reflectors, tau/T/W, R1, Q2
+  DeviceBuffer TS[24], TX[2];       // TSQR: per level reflectors, tau, R stack; Q down-sweep ping-pong
   explicit ProcWork(ptb_context* c);
   ~ProcWork();
 };

@@ -12,10 +12,20 @@ import paratime_b200 as B
 def mats():
     rng = np.random.default_rng(77)
     out = []
-    for m, n, rank in [(4096, 40, 40), (6000, 64, 50), (20000, 100, 100), (3000, 33, 20), (8192, 96, 96)]:
+    for m, n, rank in [(4096, 40, 40), (6000, 64, 50), (20000, 100, 100), (3000, 33, 20), (8192, 96, 96),
+                       (12288, 32, 29), (49152, 64, 60), (1537, 17, 17)]:
         a = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n))
         a *= np.logspace(0, -6, n)[None, :]  # graded columns: pivoting matters
         out.append(a)
+    # exactly repeated and zero columns, and columns supported on a few rows (zero reflectors
+    # inside TSQR leaves)
+    a = rng.standard_normal((20000, 48))
+    a[:, 5] = a[:, 2]
+    a[:, 11] = 0.0
+    a[:, 20] = 0.0
+    a[:300, 20] = rng.standard_normal(300)
+    a[:, 30] = 2.0 * a[:, 7]
+    out.append(a)
     return out
 
 

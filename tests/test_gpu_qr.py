@@ -1,6 +1,7 @@
-"""truncated_qr (procrustes.cpp:34-46) on tall snapshot-like blocks: the blocked route (unpivoted
-panel QR + WY updates, then the pivoted QR of R1; used for n > 32, m >= 8n) and the direct
-column-pivoted kernel (PTB_QR=direct) must both reproduce the oracle's keep count, an orthonormal
+"""truncated_qr (procrustes.cpp:34-46) on tall snapshot-like blocks: the TSQR route (leaf QRs in
+shared memory, then the pivoted QR of the last stack; n <= 64), the blocked route (unpivoted
+panel QR + WY updates, then the pivoted QR of R1; n > 64), the direct column-pivoted kernel and
+the default choice must all reproduce the oracle's keep count, an orthonormal
 Q and the same product Q R as the oracle's column-pivoted QR."""
 import os
 import subprocess
@@ -16,11 +17,12 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("path", ["blocked", "direct"])
+@pytest.mark.parametrize("path", ["auto", "blocked", "direct", "tsqr"])
 def test_truncated_qr_tall_matches_oracle(tmp_path, path):
     env = dict(os.environ, PYTHONPATH=str(ROOT))
-    if path == "direct":
-        env["PTB_QR"] = "direct"
+    env.pop("PTB_QR", None)
+    if path != "auto":
+        env["PTB_QR"] = path
     out = tmp_path / "qr.npz"
     subprocess.run([sys.executable, str(ROOT / "tests" / "qr_probe.py"), str(out)], check=True, env=env, timeout=600)
     d = np.load(out)
