@@ -203,16 +203,15 @@ ptb_status ptb_truncated_qr(ptb_context* ctx, size_t m, size_t n, const double* 
     require(ctx && keep, "truncated_qr: null argument");
     Dev d(ctx->device);
     std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
-    ProcWork w(ctx);
-    DeviceBuffer qb, rb;
+    ProcWork& w = context_proc_work(ctx);
+    DeviceBuffer& qb = w.QF;  // the workspace's own buffers: no allocation per call
+    DeviceBuffer& rb = w.RF;
     const int k = truncated_qr(w, A, int(m), int(n), drop_tol, qb, rb);
     if (k > 0) {
       PTB_CUDA_CHECK(cudaMemcpyAsync(Q, qb.ptr, m * size_t(k) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
       PTB_CUDA_CHECK(cudaMemcpyAsync(R, rb.ptr, size_t(k) * n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     }
     PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    qb.release();
-    rb.release();
     *keep = size_t(k);
   });
 }
@@ -222,8 +221,9 @@ ptb_status ptb_thin_svd(ptb_context* ctx, size_t p, size_t q, const double* M, d
     require(ctx && S, "thin_svd: null argument");
     Dev d(ctx->device);
     std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
-    ProcWork w(ctx);
-    DeviceBuffer ub, vb;
+    ProcWork& w = context_proc_work(ctx);
+    DeviceBuffer& ub = w.Uh;
+    DeviceBuffer& vb = w.Vh;
     std::vector<double> sigma;
     thin_svd(w, M, int(p), int(q), ub, sigma, vb);
     const size_t k = std::min(p, q);
@@ -232,8 +232,6 @@ ptb_status ptb_thin_svd(ptb_context* ctx, size_t p, size_t q, const double* M, d
       PTB_CUDA_CHECK(cudaMemcpy(V, vb.ptr, q * k * sizeof(double), cudaMemcpyDeviceToDevice));
     }
     for (size_t i = 0; i < k; ++i) S[i] = sigma[i];
-    ub.release();
-    vb.release();
   });
 }
 

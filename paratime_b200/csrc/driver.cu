@@ -156,10 +156,18 @@ int gemv_parts(size_t rows) { return int(std::max<size_t>(1, std::min<size_t>(64
 // (all loads of a thread independent, coalesced across the AD_I points), then the AD_J partials
 // are added in a fixed tree order -- the result depends on (nc, r) only.
 constexpr int AD_I = 32, AD_J = 8;
+// mw: mparts partials of m_w, summed in order (k_state_sum_final's order: bitwise the same m_w).
+// Optional sweep-step tail (f0 non-null): d := NaN where w, coarse_next[n] or fine_next[n] is
+// non-finite (parareal.cpp:323-326), then R(next[n]) = R(fine_next[n]) + d (k_sweep_tail).
+struct SweepTail {
+  const int32_t *f0, *f1, *f2;
+  const double *rfu, *rfv;
+  double *ru, *rv;
+};
 __global__ void __launch_bounds__(AD_I * AD_J) k_assemble_d(size_t nc, int r, const double* Zu, const double* Zv,
                                                           const double* zw, int zparts, const double* zold,
-                                                          const double* mw, const double* mold, double* du,
-                                                          double* dv) {
+                                                          const double* mw, int mparts, const double* mold,
+                                                          double* du, double* dv, const SweepTail tl) {
   extern __shared__ double dz[];  // r, then [2][AD_J][AD_I] partials
   const int tid = threadIdx.y * AD_I + threadIdx.x;
   for (int j = tid; j < r; j += AD_I * AD_J) {
@@ -202,9 +210,19 @@ __global__ void __launch_bounds__(AD_I * AD_J) k_assemble_d(size_t nc, int r, co
         a[g] += a[g + w];
         b[g] += b[g + w];
       }
-    const double dm = mold ? __dsub_rn(*mw, *mold) : *mw;
-    du[i] = a[0] + dm / double(nc);
-    dv[i] = b[0];
+    double m = 0.0;
+    for (int q = 0; q < mparts; ++q) m += mw[q];
+    const double dm = mold ? __dsub_rn(m, *mold) : m;
+    double ou = a[0] + dm / double(nc), ov = b[0];
+    if (tl.f0) {
+      if (*tl.f0 || *tl.f1 || *tl.f2) ou = ov = CUDART_NAN;
+      if (tl.ru) {
+        tl.ru[i] = tl.rfu[i] + ou;
+        tl.rv[i] = tl.rfv[i] + ov;
+      }
+    }
+    du[i] = ou;
+    dv[i] = ov;
   }
 }
 
@@ -243,6 +261,8 @@ DriverCache& driver_cache(ptb_context* ctx) {
   if (!ctx->driver_cache) ctx->driver_cache = std::make_shared<DriverCache>(ctx);
   return *static_cast<DriverCache*>(ctx->driver_cache.get());
 }
+
+ProcWork& context_proc_work(ptb_context* ctx) { return driver_cache(ctx).pw; }
 
 struct Driver {
   ptb_context* ctx;
@@ -665,13 +685,13 @@ struct Driver {
 
   // d (coarse) = Z (z_w - z_old) + (m_w - m_old)/Nc  [u], Zv (z_w - z_old) [udot]
   void assemble_d(const DevCorrector& c, const double* zw_, const double* zold_, const double* mw, const double* mold,
-                  double* du, double* dv) {
+                  double* du, double* dv, int mparts = 1, const SweepTail& tail = SweepTail{}) {
     const int r = c.rank;
     if (fused_sweep(c)) {
       const size_t smem = (size_t(r + 1) + 2 * AD_J * AD_I) * sizeof(double);
       k_assemble_d<<<unsigned((nc + AD_I - 1) / AD_I), dim3(AD_I, AD_J), smem, st()>>>(
-          nc, r, static_cast<double*>(Zu.ptr), static_cast<double*>(Zv.ptr), zw_, zw_parts, zold_, mw, mold, du,
-          dv);
+          nc, r, static_cast<double*>(Zu.ptr), static_cast<double*>(Zv.ptr), zw_, zw_parts, zold_, mw, mparts, mold, du,
+          dv, tail);
       PTB_LAUNCH_CHECK(ctx);
       return;
     }
@@ -716,7 +736,7 @@ struct Driver {
       }
     }
     double* zwp = dalloc<double>(zw, size_t(std::max(c.rank, 1)) * 64);  // r x P partials
-    double* mw = dalloc<double>(mean, std::max<size_t>(N, 1));
+    double* mw = dalloc<double>(mean, std::max<size_t>(N, 64));  // >= 64: sum(u) partials of comp_gemv
     double* ru = static_cast<double*>(rn_u.ptr);
     double* rv = static_cast<double*>(rn_v.ptr);
     // n = 1: next[1] = fine_next[1]  ->  d_1 = 0, R(next[1]) = R(fine_next[1])
@@ -735,6 +755,17 @@ struct Driver {
         k_sub<<<1, 32, 0, st()>>>(1, mw, mo + (n - 1), mw + 1);
         PTB_LAUNCH_CHECK(ctx);
         from_energy_components(ew, cg, 1, cw, rows, mw + 1, cf_dev, du, dv, nc);
+      } else if (fused_sweep(c) && s.scheme != PTB_SPECTRAL) {
+        // one launch for Lambda(w), z_w = Y^T Lambda(w) and sum(u); one for d, the NaN rule and
+        // R(next[n]) = R(fine_next[n]) + d_n
+        const int P = comp_gemv_parts(rows);
+        zw_parts = P;
+        comp_gemv(ew, cg, s.scheme, ru, rv, cf_dev, c.Yp(), rows, c.rank, zwp, P, mw);
+        const bool more = n < N;
+        const SweepTail tail{wfl + n, fl(cf) + (n - 1), fl(ff) + (n - 1), more ? slot(rf_u, n, nc) : nullptr,
+                             more ? slot(rf_v, n, nc) : nullptr, more ? ru : nullptr, more ? rv : nullptr};
+        assemble_d(c, zwp, zo + (n - 1) * size_t(c.rank), mw, mo + (n - 1), du, dv, sweep_mean_parts(int(nc)), tail);
+        continue;
       } else {
         corrected_batch(c, false, 1, ru, rv, nullptr, nullptr, zwp, mw);
         assemble_d(c, zwp, zo + (n - 1) * size_t(c.rank), mw, mo + (n - 1), du, dv);

@@ -167,6 +167,47 @@ __global__ void k_state_sum_final(size_t batch, int P, const double* part, doubl
   }
 }
 
+// The sweep step's z = Y^T Lambda(w) for ONE coarse state without materialising Lambda(w):
+// block (j, p), j < r, reduces rows [p chunk, (p + 1) chunk) of column j of Y against the
+// components evaluated on the fly (fd gradients / momentum of k_components_fd, bitwise the same
+// values; w is L2-resident); blocks (r, p < Psum) are k_state_sum's partials of sum(u) (same
+// partition and order, so mean_u is bitwise energy_components'), one launch for both.
+__global__ void __launch_bounds__(256) k_comp_gemv(const CompArgs a, int r, size_t rows, size_t chunk, const double* Y,
+                                                   size_t ldy, double* z, int Psum, double* mean_part) {
+  const int n = a.n, d = a.G.dim;
+  if (int(blockIdx.x) == r) {  // sum(u) partials
+    if (int(blockIdx.y) >= Psum) return;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int step = Psum * 256;
+    int i = blockIdx.y * 256 + threadIdx.x;
+    for (; i + 3 * step < n; i += 4 * step) {
+      a0 += a.u[i];
+      a1 += a.u[i + step];
+      a2 += a.u[i + 2 * step];
+      a3 += a.u[i + 3 * step];
+    }
+    for (; i < n; i += step) a0 += a.u[i];
+    const double s = block_sum<256>((a0 + a1) + (a2 + a3));
+    if (threadIdx.x == 0) mean_part[blockIdx.y] = s;
+    return;
+  }
+  const double* Yj = Y + size_t(blockIdx.x) * ldy;
+  const size_t r0 = size_t(blockIdx.y) * chunk, r1 = min(rows, r0 + chunk);
+  auto comp = [&](size_t row) {
+    const int ax = int(row / size_t(n)), pt = int(row - size_t(ax) * n);
+    return ax < d ? fd_grad<false>(a.u, nullptr, a.G, a.B, ax, pt) : __ddiv_rn(a.v[pt], a.c[pt]);
+  };
+  double s0 = 0.0, s1 = 0.0;
+  size_t i = r0 + threadIdx.x;
+  for (; i + 256 < r1; i += 512) {
+    s0 += Yj[i] * comp(i);
+    s1 += Yj[i + 256] * comp(i + 256);
+  }
+  if (i < r1) s0 += Yj[i] * comp(i);
+  const double t = block_sum<256>(s0 + s1);
+  if (threadIdx.x == 0) z[size_t(blockIdx.x) * gridDim.y + blockIdx.y] = t;
+}
+
 int state_sum_parts(int n) { return std::max(1, std::min(64, n / 4096)); }
 
 // complex staging for spectral maps
@@ -509,6 +550,23 @@ void energy_components(EnergyWork& w, const ptb_grid& g, int scheme, size_t batc
       PTB_LAUNCH_CHECK(ctx);
     }
   }
+}
+
+int comp_gemv_parts(size_t rows) { return int(std::max<size_t>(1, std::min<size_t>(64, rows / 2048))); }
+int sweep_mean_parts(int n) { return state_sum_parts(n); }
+
+void comp_gemv(EnergyWork& w, const ptb_grid& g, int scheme, const double* u, const double* v, const double* c,
+               const double* Y, size_t ldy, int r, double* z, int P, double* mean_part) {
+  ptb_context* ctx = w.ctx;
+  require(scheme != PTB_SPECTRAL, "comp_gemv: finite-difference schemes only");
+  const Geo G = geo_of(g);
+  const int n = G.ny * G.nx;
+  const size_t rows = size_t(G.dim + 1) * n;
+  const int Psum = state_sum_parts(n);
+  CompArgs a{G, beta_of(scheme), n, u, v, size_t(n), nullptr, c, nullptr, 0};
+  k_comp_gemv<<<dim3(unsigned(r + 1), unsigned(std::max(P, Psum))), 256, 0, ctx->stream>>>(
+      a, r, rows, (rows + P - 1) / P, Y, ldy, z, Psum, mean_part);
+  PTB_LAUNCH_CHECK(ctx);
 }
 
 void from_energy_components(EnergyWork& w, const ptb_grid& g, size_t batch, const double* stacked, size_t ld,

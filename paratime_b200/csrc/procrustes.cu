@@ -744,6 +744,366 @@ __global__ void __launch_bounds__(1024) k_jacobi(JacobiArgs a) {
   for (int k = threadIdx.x; k < c; k += blockDim.x) a.sigma[k] = sv[a.order[k]];
 }
 
+// One-sided Jacobi for matrices that fit one CTA's shared memory (the corrector's H up to ~110
+// columns): the same tournament schedule and stopping rules as k_jacobi, with fewer instructions
+// per pair -- the instruction issue of one SM is what bounds this kernel (ncu: ~600 instructions
+// per pair-round in k_jacobi).  A GS-lane group owns one pair per round (more rows per lane, so the
+// per-pair scalar work is shared by fewer lanes), the pairing advances by conditional subtraction
+// instead of a modulo, the rotation test compares squares (ga^2 > tol^2 al be) instead of
+// forming sqrt(al) sqrt(be), and cos = rsqrt(1 + t^2).
+template <int GS, int RPL>  // r <= GS * RPL (and c <= r), c / 2 * GS <= 512 threads
+__global__ void __launch_bounds__(512) k_jacobi_small(JacobiArgs a) {
+  extern __shared__ double js[];
+  const int r = a.r, c = a.c;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  __shared__ int rotated;
+  __shared__ double colmax;
+  double* A = js;
+  double* V = js + size_t(r) * c;
+  for (int e = tid; e < r * c; e += blockDim.x) A[e] = a.A[e];
+  for (int e = tid; e < c * c; e += blockDim.x) V[e] = (e % (c + 1) == 0) ? 1.0 : 0.0;
+  const int cc = (c % 2 == 0) ? c : c + 1;  // tournament size (dummy column when odd)
+  const int m1 = cc - 1;
+  const double eps = 2.220446049250313e-16;
+  const double tol2 = eps * eps * double(r);
+  const int glane = tid & (GS - 1), pr = tid / GS;  // one pair per group
+  const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1u) << (lane & ~(GS - 1)));
+  auto gsum = [&](double x) {
+#pragma unroll
+    for (int o = GS / 2; o > 0; o >>= 1) x += __shfl_xor_sync(gmask, x, o);
+    return x;
+  };
+  // tournament positions of this group's pair: pos(q) = q == 0 ? 0 : 1 + (q - 1 + round) % (cc - 1)
+  int x1 = pr - 1, x2 = cc - 2 - pr;  // (q - 1) for q = pr and q = cc - 1 - pr, advanced per round
+  if (x1 < 0) x1 += m1;               // pr == 0 stays at position 0 (handled below)
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    if (tid == 0) {
+      rotated = 0;
+      colmax = 0.0;
+    }
+    __syncthreads();
+    for (int k = warp; k < c; k += nwarps) {
+      double sacc = 0.0;
+      for (int q = lane; q < r; q += 32) sacc = fma(A[size_t(k) * r + q], A[size_t(k) * r + q], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&colmax), __double_as_longlong(sacc));
+    }
+    __syncthreads();
+    const double floor2 = eps * eps * colmax;
+    const double floor4 = floor2 * floor2;
+    int y1 = x1, y2 = x2;
+    for (int round = 0; round < m1; ++round) {
+      if (pr < cc / 2) {
+        int i = pr == 0 ? 0 : 1 + y1, j = 1 + y2;
+        if (i > j) {
+          const int t = i;
+          i = j;
+          j = t;
+        }
+        if (j < c) {
+          // the pair's rows in registers: all loads issued together, reused by the rotation
+          double* ai = A + size_t(i) * r;
+          double* aj = A + size_t(j) * r;
+          double x[RPL], y[RPL];
+#pragma unroll
+          for (int t = 0; t < RPL; ++t) {
+            const int k = glane + GS * t;
+            x[t] = k < r ? ai[k] : 0.0;
+            y[t] = k < r ? aj[k] : 0.0;
+          }
+          double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+          for (int t = 0; t < RPL; ++t) {
+            al = fma(x[t], x[t], al);
+            be = fma(y[t], y[t], be);
+            ga = fma(x[t], y[t], ga);
+          }
+          al = gsum(al);
+          be = gsum(be);
+          ga = gsum(ga);
+          const double ab = al * be;
+          if (ga != 0.0 && ga * ga > tol2 * ab && ab > floor4) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+              const int k = glane + GS * u;
+              if (k < r) {
+                ai[k] = fma(cs, x[u], -sn * y[u]);
+                aj[k] = fma(sn, x[u], cs * y[u]);
+              }
+            }
+            double* vi = V + size_t(i) * c;  // V's columns through the same registers
+            double* vj = V + size_t(j) * c;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+              const int k = glane + GS * u;
+              x[u] = k < c ? vi[k] : 0.0;
+              y[u] = k < c ? vj[k] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+              const int k = glane + GS * u;
+              if (k < c) {
+                vi[k] = fma(cs, x[u], -sn * y[u]);
+                vj[k] = fma(sn, x[u], cs * y[u]);
+              }
+            }
+            if (glane == 0) rotated = 1;
+          }
+        }
+      }
+      if (++y1 == m1) y1 = 0;
+      if (++y2 == m1) y2 = 0;
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  double* sv = a.tmp + size_t(r) * c + size_t(c) * c;
+  for (int k = warp; k < c; k += nwarps) {
+    double sacc = 0.0;
+    for (int q = lane; q < r; q += 32) sacc = fma(A[size_t(k) * r + q], A[size_t(k) * r + q], sacc);
+    sacc = warp_sum(sacc);
+    if (lane == 0) sv[k] = sqrt(sacc);
+  }
+  if (tid == 0) sv[c] = double(sweep);  // diagnostics: sweeps used
+  __syncthreads();
+  for (int k = tid; k < c; k += blockDim.x) {
+    int rank = 0;
+    for (int q = 0; q < c; ++q)
+      if (sv[q] > sv[k] || (sv[q] == sv[k] && q < k)) ++rank;
+    a.order[rank] = k;
+  }
+  __syncthreads();
+  for (int e = tid; e < r * c; e += blockDim.x) {
+    const int k = e / r, q = e - k * r;
+    const int src = a.order[k];
+    const double sg = sv[src];
+    a.A[e] = sg > 0.0 ? A[size_t(src) * r + q] / sg : 0.0;
+  }
+  for (int e = tid; e < c * c; e += blockDim.x) {
+    const int k = e / c, q = e - k * c;
+    a.V[e] = V[size_t(a.order[k]) * c + q];
+  }
+  for (int k = tid; k < c; k += blockDim.x) a.sigma[k] = sv[a.order[k]];
+}
+
+// One-sided Jacobi on a thread-block cluster (JC_CS CTAs): the single-SM kernels above are bound
+// by one SM's shared-memory bandwidth -- every round streams all of A and V through it.  Here the
+// ROWS of A and V are split over the cluster (rotations act on columns, so rows are independent):
+// each round every CTA forms its partial (a_i.a_i, a_j.a_j, a_i.a_j) of every pair over its own
+// rows; rank q then reduces the partials of pairs q, q + CS, ... over the cluster (distributed
+// shared memory, fixed rank order) and decides their rotations, and every CTA fetches each
+// pair's rotation from its deciding rank and applies it to its own rows (two cluster barriers per
+// round; pulling every partial into every CTA instead was DSMEM-latency bound).  Same tournament
+// schedule and stopping rules as k_jacobi_small; deterministic.
+constexpr int JC_CS = 8, JC_GS = 8;
+static_assert(JC_GS == JC_CS, "one lane per cluster rank in the partial exchange");
+
+__global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double jc[];
+  const int q = int(cluster.block_rank());
+  const int r = a.r, c = a.c;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int ra0 = q * r / JC_CS, na = (q + 1) * r / JC_CS - ra0;  // own rows of A
+  const int rv0 = q * c / JC_CS, nv = (q + 1) * c / JC_CS - rv0;  // own rows of V
+  const int cc = (c % 2 == 0) ? c : c + 1, m1 = cc - 1, pairs = cc / 2;
+  const int PB = max(3 * pairs, c);
+  // the exchanged partials first: map_shared_rank maps the same offset in every CTA, and the row
+  // counts (hence the A/V tile sizes) differ between CTAs
+  double* part = jc;                // [2][PB]: per-pair partial sums / per-column partial norms
+  double* rot = part + 2 * PB;      // [2][pairs][cs, sn]: decided rotations (cs = 2: none)
+  double* sv = rot + 4 * pairs;     // c
+  int* order = reinterpret_cast<int*>(sv + c);  // c (c / 2 doubles)
+  double* Ao = sv + c + (c + 1) / 2;  // c columns x na rows
+  double* Vo = Ao + size_t(c) * na;   // c columns x nv rows
+  __shared__ int any_rot, nrot;
+  __shared__ double s_colmax;
+  for (int e = tid; e < c * na; e += blockDim.x) {
+    const int k = e / na, t = e - k * na;
+    Ao[e] = a.A[size_t(k) * r + ra0 + t];
+  }
+  for (int e = tid; e < c * nv; e += blockDim.x) {
+    const int k = e / nv, t = e - k * nv;
+    Vo[e] = (rv0 + t == k) ? 1.0 : 0.0;
+  }
+  const double eps = 2.220446049250313e-16;
+  const double tol2 = eps * eps * double(r);
+  const int glane = tid & (JC_GS - 1), pr = tid / JC_GS;
+  const unsigned gmask = ((1u << JC_GS) - 1u) << (lane & ~(JC_GS - 1));
+  auto gsum = [&](double x) {
+#pragma unroll
+    for (int o = JC_GS / 2; o > 0; o >>= 1) x += __shfl_xor_sync(gmask, x, o);
+    return x;
+  };
+  int it = 0;  // parity of the partial-sum buffer, advanced at every exchange
+  // column norms^2 of A over the cluster -> sv (identical in every CTA)
+  auto column_norms2 = [&]() {
+    double* pb = part + (it & 1) * PB;
+    for (int k = warp; k < c; k += nwarps) {
+      double acc = 0.0;
+      for (int t = lane; t < na; t += 32) acc = fma(Ao[size_t(k) * na + t], Ao[size_t(k) * na + t], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) pb[k] = acc;
+    }
+    cluster.sync();
+    for (int k = tid; k < c; k += blockDim.x) {
+      double acc = 0.0;
+      for (int o = 0; o < JC_CS; ++o) acc += cluster.map_shared_rank(pb, o)[k];
+      sv[k] = acc;
+    }
+    ++it;
+    __syncthreads();
+  };
+  int x1 = pr - 1, x2 = cc - 2 - pr;
+  if (x1 < 0) x1 += m1;
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    column_norms2();
+    if (warp == 0) {
+      double mx = 0.0;
+      for (int k = lane; k < c; k += 32) mx = fmax(mx, sv[k]);
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) {
+        s_colmax = mx;
+        any_rot = 0;
+        nrot = 0;
+      }
+    }
+    __syncthreads();
+    const double floor2 = eps * eps * s_colmax;
+    const double floor4 = floor2 * floor2;
+    int y1 = x1, y2 = x2;
+    for (int round = 0; round < m1; ++round) {
+      double* pb = part + (it & 1) * PB;
+      int i = 0, j = 0;
+      bool act = false;
+      if (pr < pairs) {
+        i = pr == 0 ? 0 : 1 + y1;
+        j = 1 + y2;
+        if (i > j) {
+          const int t = i;
+          i = j;
+          j = t;
+        }
+        act = j < c;
+      }
+      double* ai = Ao + size_t(i) * na;
+      double* aj = Ao + size_t(j) * na;
+      if (act) {
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int t = glane; t < na; t += JC_GS) {
+          const double x = ai[t], y = aj[t];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = gsum(al);
+        be = gsum(be);
+        ga = gsum(ga);
+        if (glane == 0) {
+          pb[3 * pr] = al;
+          pb[3 * pr + 1] = be;
+          pb[3 * pr + 2] = ga;
+        }
+      }
+      cluster.sync();
+      // reduce-scatter: rank q reduces the pairs p = q, q + CS, ... over the cluster (fixed rank
+      // order) and decides their rotations; one remote load per rank and value
+      double* rb = rot + (it & 1) * 2 * pairs;
+      for (int p2 = q + JC_CS * warp; p2 < pairs; p2 += JC_CS * nwarps) {
+        // one warp per pair: lane l < CS reads rank l's three partials
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        if (lane < JC_CS) {
+          const double* rp = cluster.map_shared_rank(pb, lane) + 3 * p2;
+          v0 = rp[0];
+          v1 = rp[1];
+          v2 = rp[2];
+        }
+#pragma unroll
+        for (int o = JC_CS / 2; o > 0; o >>= 1) {
+          v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+          v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+          v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+        }
+        if (lane == 0) {
+          const double al = v0, be = v1, ga = v2, ab = al * be;
+          double cs = 2.0, sn = 0.0;  // cs = 2: no rotation
+          if (ga != 0.0 && ga * ga > tol2 * ab && ab > floor4) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            cs = rsqrt(fma(t, t, 1.0));
+            sn = cs * t;
+          }
+          rb[2 * p2] = cs;
+          rb[2 * p2 + 1] = sn;
+        }
+      }
+      cluster.sync();
+      if (act) {
+        // all-gather: the pair's rotation from the rank that decided it
+        const double2 cr = *reinterpret_cast<const double2*>(cluster.map_shared_rank(rb, pr % JC_CS) + 2 * pr);
+        const double cs = cr.x, sn = cr.y;
+        if (cs != 2.0) {
+          for (int u = glane; u < na; u += JC_GS) {
+            const double x = ai[u], y = aj[u];
+            ai[u] = fma(cs, x, -sn * y);
+            aj[u] = fma(sn, x, cs * y);
+          }
+          double* vi = Vo + size_t(i) * nv;
+          double* vj = Vo + size_t(j) * nv;
+          for (int u = glane; u < nv; u += JC_GS) {
+            const double x = vi[u], y = vj[u];
+            vi[u] = fma(cs, x, -sn * y);
+            vj[u] = fma(sn, x, cs * y);
+          }
+          if (glane == 0) {
+            any_rot = 1;
+            atomicAdd(&nrot, 1);
+          }
+        }
+      }
+      ++it;
+      if (++y1 == m1) y1 = 0;
+      if (++y2 == m1) y2 = 0;
+      __syncthreads();
+    }
+    if (q == 0 && tid == 0 && sweep < 16) a.tmp[size_t(r) * c + size_t(c) * c + c + 1 + sweep] = double(nrot);
+    if (!any_rot) break;
+  }
+  column_norms2();
+  for (int k = tid; k < c; k += blockDim.x) sv[k] = sqrt(sv[k]);
+  __syncthreads();
+  for (int k = tid; k < c; k += blockDim.x) {
+    int rank = 0;
+    for (int o = 0; o < c; ++o)
+      if (sv[o] > sv[k] || (sv[o] == sv[k] && o < k)) ++rank;
+    order[rank] = k;
+  }
+  __syncthreads();
+  for (int e = tid; e < c * na; e += blockDim.x) {
+    const int k = e / na, t = e - k * na;
+    const int src = order[k];
+    const double sg = sv[src];
+    a.A[size_t(k) * r + ra0 + t] = sg > 0.0 ? Ao[size_t(src) * na + t] / sg : 0.0;
+  }
+  for (int e = tid; e < c * nv; e += blockDim.x) {
+    const int k = e / nv, t = e - k * nv;
+    a.V[size_t(k) * c + rv0 + t] = Vo[size_t(order[k]) * nv + t];
+  }
+  if (q == 0) {
+    for (int k = tid; k < c; k += blockDim.x) a.sigma[k] = sv[order[k]];
+    if (tid == 0) a.tmp[size_t(r) * c + size_t(c) * c + c] = double(sweep);  // diagnostics
+  }
+  cluster.sync();  // no CTA leaves while another may still read its shared memory
+}
+
 // Multi-CTA one-sided Jacobi for matrices that do not fit one CTA's shared memory: the same
 // tournament schedule and per-pair arithmetic as k_jacobi (warp-strided sums, xor-shuffle
 // reduction, same rotation and stopping rules), so the result is bitwise the one k_jacobi<false>
@@ -1098,6 +1458,36 @@ __device__ __forceinline__ int ts_row0(int i, int m, int nb) { return int((long 
 // diagonal, scaled reflectors below; TS = true: a TSQR leaf -- reflectors to V, R to the stack).
 constexpr int QRR_THREADS = 512, QRR_WARPS = QRR_THREADS / 32;
 
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
+// C per-lane partial sums -> the C warp totals in every lane, by a transposed butterfly: the first
+// log2 C levels exchange half of the values still held (C - 1 double shuffles in all), the rest
+// reduce one value, then the C totals are broadcast -- 10 double shuffles for C = 4 instead of 20.
+// Column c ends in lanes [c 32 / C, (c + 1) 32 / C).  Fixed order: deterministic.
+template <int C>
+__device__ __forceinline__ void warp_allsum(double (&v)[C]) {
+  constexpr int L = ilog2(C);
+  static_assert((1 << L) == C && C <= 32, "power of two");
+  const int lane = threadIdx.x & 31;
+  double t[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) t[c] = v[c];
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const int o = 16 >> l, half = C >> (l + 1);
+    const bool hi = lane & o;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double keep = hi ? t[half + i] : t[i], give = hi ? t[i] : t[half + i];
+      t[i] = keep + __shfl_xor_sync(0xffffffffu, give, o);
+    }
+  }
+#pragma unroll
+  for (int o = 16 >> L; o > 0; o >>= 1) t[0] += __shfl_xor_sync(0xffffffffu, t[0], o);
+#pragma unroll
+  for (int c = 0; c < C; ++c) v[c] = __shfl_sync(0xffffffffu, t[0], c * (32 / C));
+}
+
 struct QrRegArgs {
   const double* A;  // input columns, ld lda; TS: this leaf's rows start at ts_row0(blockIdx.x)
   int lda, m, n, nb;
@@ -1113,6 +1503,21 @@ struct QrRegArgs {
   int* keep_out;
   double* beta_out;
 };
+
+// explicit predicated selects (selp): unlike a ternary over an unrolled slot loop, the front end
+// cannot fold these into a dynamically indexed register array
+__device__ __forceinline__ double selp(bool c, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(r) : "d"(a), "d"(b), "r"(int(c)));
+  return r;
+}
+__device__ __forceinline__ int selp(bool c, int a, int b) {
+  int r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.s32 %0, %1, %2, q;\n\t}"
+      : "=r"(r) : "r"(a), "r"(b), "r"(int(c)));
+  return r;
+}
 
 template <int CPW, int RPL, bool PIVOT, bool TS>
 __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
@@ -1183,36 +1588,38 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
       __syncwarp();
     }
     if (warp == p % QRR_WARPS) {  // the pivot's owner: dlarfg, publish the column
+      // the pivot's slot is dynamic: gather it with explicit selects (an indexed read would move
+      // the whole register tile to local memory)
+      const int sp = p / QRR_WARPS;
+      double xs = 0.0, alc = 0.0;
 #pragma unroll
-      for (int s = 0; s < CPW; ++s) {
-        if (s != p / QRR_WARPS) continue;
-        double xs = 0.0, alc = 0.0;
+      for (int u = 0; u < RPL; ++u) {
+        double c = x[0][u];
 #pragma unroll
-        for (int u = 0; u < RPL; ++u) {
-          const int r = lane + 32 * u;
-          if (r > j) xs = fma(x[s][u], x[s][u], xs);
-          if (u == j / 32) alc = x[s][u];
-          cbuf[r] = x[s][u];
+        for (int s = 1; s < CPW; ++s) c = selp(sp == s, x[s][u], c);
+        const int r = lane + 32 * u;
+        if (r > j) xs = fma(c, c, xs);
+        if (u == j / 32) alc = c;
+        cbuf[r] = c;
+      }
+#pragma unroll
+      for (int s = 0; s < CPW; ++s) estep[s] = selp(sp == s, j, estep[s]);
+      xs = warp_sum(xs);
+      const double al = __shfl_sync(0xffffffffu, alc, j & 31);
+      if (lane == 0) {
+        double beta, tau, scal;
+        if (xs == 0.0) {
+          beta = al;
+          tau = 0.0;
+          scal = 0.0;
+        } else {  // sqrt(al^2 + |x|^2): the entries are far from the double range limits
+          beta = -copysign(sqrt(fma(al, al, xs)), al);
+          tau = (beta - al) / beta;
+          scal = 1.0 / (al - beta);
         }
-        xs = warp_sum(xs);
-        const double al = __shfl_sync(0xffffffffu, alc, j & 31);
-        estep[s] = j;
-        if (lane == 0) {
-          const double xnorm = sqrt(xs);
-          double beta, tau, scal;
-          if (xnorm == 0.0) {
-            beta = al;
-            tau = 0.0;
-            scal = 0.0;
-          } else {
-            beta = -copysign(hypot(al, xnorm), al);
-            tau = (beta - al) / beta;
-            scal = 1.0 / (al - beta);
-          }
-          s_sc[0] = beta;
-          s_sc[1] = tau;
-          s_sc[2] = scal;
-        }
+        s_sc[0] = beta;
+        s_sc[1] = tau;
+        s_sc[2] = scal;
       }
     }
     __syncthreads();
@@ -1221,8 +1628,7 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
       if (tid == 0 && a.beta_out) a.beta_out[j] = fabs(beta);
       keep = j;
 #pragma unroll
-      for (int s = 0; s < CPW; ++s)
-        if (estep[s] == j) estep[s] = -1;
+      for (int s = 0; s < CPW; ++s) estep[s] = selp(estep[s] == j, -1, estep[s]);
       break;
     }
     if (tid == 0) {
@@ -1246,10 +1652,7 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
       for (int u = 0; u < RPL; ++u) acc = fma(v[u], x[s][u], acc);
       w[s] = acc;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int s = 0; s < CPW; ++s) w[s] += __shfl_xor_sync(0xffffffffu, w[s], o);
+    warp_allsum<CPW>(w);
     double nn[CPW];
 #pragma unroll
     for (int s = 0; s < CPW; ++s) {
@@ -1265,10 +1668,7 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
       }
     }
     if (PIVOT) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int s = 0; s < CPW; ++s) nn[s] += __shfl_xor_sync(0xffffffffu, nn[s], o);
+      warp_allsum<CPW>(nn);
       if (lane == 0)
 #pragma unroll
         for (int s = 0; s < CPW; ++s) {
@@ -1466,6 +1866,13 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
   return keep;
 }
 
+size_t jacobi_cluster_smem(int r, int c) {
+  const int pairs = ((c % 2 == 0) ? c : c + 1) / 2;
+  const int na = (r + JC_CS - 1) / JC_CS + 1, nv = (c + JC_CS - 1) / JC_CS + 1;
+  return (size_t(c) * (na + nv) + 2 * size_t(std::max(3 * pairs, c)) + 4 * size_t(pairs) + 2 * size_t(c) + 2) *
+         sizeof(double);
+}
+
 // thin SVD of M (p x q): U (p x k), sigma (k, host), V (q x k), k = min(p, q)
 // One-sided Jacobi of A (r x c, r >= c, column-major, overwritten): A := U (sorted, unit
 // columns), V (c x c), sigma (c, descending) -- the device buffers of JacobiArgs.
@@ -1478,11 +1885,40 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
     const char* e = std::getenv("PTB_JACOBI");
     if (e && std::string(e) == "single") return 1;
     if (e && std::string(e) == "coop") return 2;
+    if (e && std::string(e) == "small") return 3;  // one-CTA shared-memory kernels only
     return 0;
   }();
-  if (smem <= 200 * 1024 && jacobi_env != 2) {
-    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k_jacobi<true><<<1, 1024, smem, st>>>(ja);
+  const int pairs = ((c % 2 == 0) ? c : c + 1) / 2;
+  const size_t csmem = jacobi_cluster_smem(r, c);
+  const bool cluster_ok = jacobi_env == 0 && c >= 24 && pairs * JC_GS <= 1024 && csmem <= 200 * 1024;
+  if (cluster_ok || (smem <= 200 * 1024 && jacobi_env != 2)) {
+    if (cluster_ok) {
+      PTB_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csmem)));
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(JC_CS);
+      cfg.blockDim = dim3(unsigned(std::max(32, (pairs * JC_GS + 31) / 32 * 32)));
+      cfg.dynamicSmemBytes = csmem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = JC_CS;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      PTB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_jacobi_cluster, ja));
+    } else if (r <= 128 && pairs * 8 <= 512) {  // one 8-lane group per pair, <= 16 rows per lane
+      PTB_CUDA_CHECK(
+          cudaFuncSetAttribute(k_jacobi_small<8, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      k_jacobi_small<8, 16><<<1, std::max(32, (pairs * 8 + 31) / 32 * 32), smem, st>>>(ja);
+    } else if (r <= 256 && pairs * 16 <= 512) {
+      PTB_CUDA_CHECK(
+          cudaFuncSetAttribute(k_jacobi_small<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      k_jacobi_small<16, 16><<<1, std::max(32, (pairs * 16 + 31) / 32 * 32), smem, st>>>(ja);
+    } else {
+      PTB_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      k_jacobi<true><<<1, 1024, smem, st>>>(ja);
+    }
     PTB_LAUNCH_CHECK(ctx);
   } else if (jacobi_env == 1) {
     k_jacobi<false><<<1, 1024, 0, st>>>(ja);
@@ -1500,11 +1936,12 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
     PTB_LAUNCH_CHECK(ctx);
   }
   if (HostProf(st).on) {  // diagnostics: sweeps used (written after the singular values)
-    double sweeps = 0.0;
-    PTB_CUDA_CHECK(cudaMemcpyAsync(&sweeps, tmp + size_t(r) * c + size_t(c) * c + c, sizeof(double),
-                                   cudaMemcpyDeviceToHost, st));
+    double d[17] = {};
+    PTB_CUDA_CHECK(cudaMemcpyAsync(d, tmp + size_t(r) * c + size_t(c) * c + c, sizeof(d), cudaMemcpyDeviceToHost, st));
     PTB_CUDA_CHECK(cudaStreamSynchronize(st));
-    std::fprintf(stderr, "[ptb prof] jacobi %d x %d: %g sweeps\n", r, c, sweeps);
+    std::fprintf(stderr, "[ptb prof] jacobi %d x %d: %g sweeps; rotations per sweep (cluster kernel):", r, c, d[0]);
+    for (int k = 1; k < 17 && k <= int(d[0]) + 1; ++k) std::fprintf(stderr, " %g", d[k]);
+    std::fprintf(stderr, "\n");
   }
 }
 
@@ -1697,7 +2134,7 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
     double* V = static_cast<double*>(w.buf[7].get(std::max<size_t>(1, size_t(kq) * kq) * sizeof(double)));
     double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
     int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
-    double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 1) * sizeof(double)));
+    double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 17) * sizeof(double)));
     std::vector<double> s_k(size_t(kq), 0.0);
     if (kq > 0) {
       // Bt = R^T (c x kq): R is kq x c column-major
@@ -1725,7 +2162,7 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
   double* V = static_cast<double*>(w.buf[7].get(size_t(c) * c * sizeof(double)));
   double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
   int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
-  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 1) * sizeof(double)));
+  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 17) * sizeof(double)));
   jacobi_core(w, A, r, c, V, sg, tmp, order);
   PTB_CUDA_CHECK(cudaMemcpyAsync(sigma.data(), sg, size_t(c) * sizeof(double), cudaMemcpyDeviceToHost, st));
   // M = A_sorted diag(s) V^T  (A is r x c = U when !trans; when trans, M^T = A S V^T -> M = V S A^T)

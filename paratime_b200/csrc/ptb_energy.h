@@ -16,6 +16,14 @@ struct EnergyWork {
 void energy_components(EnergyWork& w, const ptb_grid& g, int scheme, size_t batch, const double* u, const double* v,
                        size_t sstride, const int* index, const double* c, double* stacked, size_t ld, double* mean);
 
+// Sweep step of the theta sweep (finite-difference schemes): z[j P + p] = partial p of
+// Y[:, j]^T Lambda(w) (P = comp_gemv_parts(rows) chunks), mean_part[q] = partial q of sum(u)
+// (sweep_mean_parts(n) partials, k_state_sum's) -- one launch, Lambda(w) never stored.
+int comp_gemv_parts(size_t rows);
+int sweep_mean_parts(int n);
+void comp_gemv(EnergyWork& w, const ptb_grid& g, int scheme, const double* u, const double* v, const double* c,
+               const double* Y, size_t ldy, int r, double* z, int P, double* mean_part);
+
 // Lambda-dagger: stacked columns + mean_u -> states (u, v at stride sstride).
 void from_energy_components(EnergyWork& w, const ptb_grid& g, size_t batch, const double* stacked, size_t ld,
                             const double* mean, const double* c, double* u, double* v, size_t sstride);

@@ -25,7 +25,7 @@ def _run(p, q, path, jacobi):
 @pytest.mark.parametrize("shape", [(300, 290), (290, 300), (420, 180)])
 def test_coop_jacobi_matches_single_cta_bitwise(tmp_path, shape):
     p, q = shape
-    a = _run(p, q, tmp_path / "coop.npz", None)
+    a = _run(p, q, tmp_path / "coop.npz", "coop")
     b = _run(p, q, tmp_path / "single.npz", "single")
     for key in ("U", "S", "V"):
         assert np.array_equal(a[key], b[key]), key
@@ -35,3 +35,19 @@ def test_coop_jacobi_matches_single_cta_bitwise(tmp_path, shape):
     assert np.linalg.norm(m - (U * S) @ V.T) <= 1e-12 * np.linalg.norm(m)  # reference pins 1e-12 (planted)
     k = min(p, q)
     assert np.max(np.abs(V.T @ V - np.eye(k))) <= 1e-12
+
+
+@pytest.mark.parametrize("path", ["auto", "small"])
+@pytest.mark.parametrize("shape", [(108, 108), (60, 44), (44, 60), (33, 33), (7, 5), (150, 120), (250, 240)])
+def test_small_and_cluster_jacobi_are_accurate(tmp_path, shape, path):
+    """k_jacobi_cluster (default from 24 columns: rows split over a thread-block cluster) and
+    k_jacobi_small (one CTA's shared memory) on the corrector's H sizes at cfg1-3."""
+    p, q = shape
+    a = _run(p, q, tmp_path / "small.npz", None if path == "auto" else path)
+    m, U, S, V = a["m"], a["U"], a["S"], a["V"]
+    ref = np.linalg.svd(m, compute_uv=False)
+    assert np.max(np.abs(S - ref) / ref[0]) <= 1e-13
+    assert np.linalg.norm(m - (U * S) @ V.T) <= 1e-12 * np.linalg.norm(m)
+    k = min(p, q)
+    assert np.max(np.abs(V.T @ V - np.eye(k))) <= 1e-12
+    assert np.max(np.abs(U.T @ U - np.eye(k))) <= 1e-12
