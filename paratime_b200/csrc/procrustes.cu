@@ -33,6 +33,7 @@
 #include <cmath>
 #include <vector>
 
+#include "ptb_dsmem.h"
 #include "ptb_procrustes.h"
 
 namespace cg = cooperative_groups;
@@ -896,11 +897,11 @@ __global__ void __launch_bounds__(512) k_jacobi_small(JacobiArgs a) {
 // by one SM's shared-memory bandwidth -- every round streams all of A and V through it.  Here the
 // ROWS of A and V are split over the cluster (rotations act on columns, so rows are independent):
 // each round every CTA forms its partial (a_i.a_i, a_j.a_j, a_i.a_j) of every pair over its own
-// rows; rank q then reduces the partials of pairs q, q + CS, ... over the cluster (distributed
-// shared memory, fixed rank order) and decides their rotations, and every CTA fetches each
-// pair's rotation from its deciding rank and applies it to its own rows (two cluster barriers per
-// round; pulling every partial into every CTA instead was DSMEM-latency bound).  Same tournament
-// schedule and stopping rules as k_jacobi_small; deterministic.
+// rows and pushes them into every rank's shared memory with st.async (bytes completed on the
+// receiver's mbarrier: no cluster barrier per round -- a cluster barrier's release waits for the
+// remote stores, ncu: ERRBAR 31 % of stall samples); then every CTA sums the partials of every
+// pair in the same fixed rank order, takes the same decision and applies the rotation to its own
+// rows.  Same tournament schedule and stopping rules as k_jacobi_small; deterministic.
 constexpr int JC_CS = 8, JC_GS = 8;
 static_assert(JC_GS == JC_CS, "one lane per cluster rank in the partial exchange");
 
@@ -913,17 +914,24 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
   const int ra0 = q * r / JC_CS, na = (q + 1) * r / JC_CS - ra0;  // own rows of A
   const int rv0 = q * c / JC_CS, nv = (q + 1) * c / JC_CS - rv0;  // own rows of V
   const int cc = (c % 2 == 0) ? c : c + 1, m1 = cc - 1, pairs = cc / 2;
-  const int PB = max(3 * pairs, c);
-  // the exchanged partials first: map_shared_rank maps the same offset in every CTA, and the row
+  // the exchanged buffers first: map_shared_rank maps the same offset in every CTA, and the row
   // counts (hence the A/V tile sizes) differ between CTAs
-  double* part = jc;                // [2][PB]: per-pair partial sums / per-column partial norms
-  double* rot = part + 2 * PB;      // [2][pairs][cs, sn]: decided rotations (cs = 2: none)
-  double* sv = rot + 4 * pairs;     // c
+  double* gath = jc;                        // [2][CS][pairs][4]: partials pushed by every rank
+  double* cn = gath + 2 * JC_CS * 4 * pairs;  // [2][c]: per-column partial norms
+  double* sv = cn + 2 * c;                  // c
   int* order = reinterpret_cast<int*>(sv + c);  // c (c / 2 doubles)
-  double* Ao = sv + c + (c + 1) / 2;  // c columns x na rows
-  double* Vo = Ao + size_t(c) * na;   // c columns x nv rows
+  double* Ao = sv + c + (c + 1) / 2;        // c columns x na rows
+  double* Vo = Ao + size_t(c) * na;         // c columns x nv rows
   __shared__ int any_rot, nrot;
   __shared__ double s_colmax;
+  __shared__ __align__(8) unsigned long long bars[2];  // one mbarrier per exchange buffer
+  const unsigned bar0 = smem_addr(&bars[0]);
+  const unsigned round_bytes = unsigned(JC_CS * (c / 2) * 4 * sizeof(double));
+  if (tid == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   for (int e = tid; e < c * na; e += blockDim.x) {
     const int k = e / na, t = e - k * na;
     Ao[e] = a.A[size_t(k) * r + ra0 + t];
@@ -941,10 +949,11 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
     for (int o = JC_GS / 2; o > 0; o >>= 1) x += __shfl_xor_sync(gmask, x, o);
     return x;
   };
-  int it = 0;  // parity of the partial-sum buffer, advanced at every exchange
+  int it = 0;  // parity of the column-norm buffers, advanced at every column-norm exchange
+  int ex = 0;  // pair-partial exchanges so far (buffer and mbarrier phase)
   // column norms^2 of A over the cluster -> sv (identical in every CTA)
   auto column_norms2 = [&]() {
-    double* pb = part + (it & 1) * PB;
+    double* pb = cn + (it & 1) * c;
     for (int k = warp; k < c; k += nwarps) {
       double acc = 0.0;
       for (int t = lane; t < na; t += 32) acc = fma(Ao[size_t(k) * na + t], Ao[size_t(k) * na + t], acc);
@@ -962,7 +971,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
   };
   int x1 = pr - 1, x2 = cc - 2 - pr;
   if (x1 < 0) x1 += m1;
-  __syncthreads();
+  cluster.sync();  // mbarriers initialised before any rank sends
   int sweep = 0;
   for (; sweep < a.max_sweeps; ++sweep) {
     column_norms2();
@@ -980,8 +989,13 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
     const double floor2 = eps * eps * s_colmax;
     const double floor4 = floor2 * floor2;
     int y1 = x1, y2 = x2;
-    for (int round = 0; round < m1; ++round) {
-      double* pb = part + (it & 1) * PB;
+    for (int round = 0; round < m1; ++round, ++ex) {
+      // exchange ex: buffer ex & 1, mbarrier phase (ex >> 1) & 1 (no cluster barrier per round:
+      // a rank sends round ex + 2 into this buffer only after receiving this rank's round ex + 1
+      // partials, which are sent after this round's reads)
+      double* gb = gath + (ex & 1) * JC_CS * 4 * pairs;
+      const unsigned bar = bar0 + 8u * unsigned(ex & 1);
+      if (tid == 0) mbar_expect(bar, round_bytes);
       int i = 0, j = 0;
       bool act = false;
       if (pr < pairs) {
@@ -1007,50 +1021,24 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
         al = gsum(al);
         be = gsum(be);
         ga = gsum(ga);
-        if (glane == 0) {
-          pb[3 * pr] = al;
-          pb[3 * pr + 1] = be;
-          pb[3 * pr + 2] = ga;
-        }
+        // all-gather by push: lane l sends this rank's partials into rank l's buffer with
+        // st.async, completing bytes on rank l's mbarrier
+        const unsigned dst = cluster_map(smem_addr(gb + (size_t(q) * pairs + pr) * 4), glane);
+        const unsigned rbar = cluster_map(bar, glane);
+        st_async2(dst, al, be, rbar);
+        st_async2(dst + 16u, ga, 0.0, rbar);
       }
-      cluster.sync();
-      // reduce-scatter: rank q reduces the pairs p = q, q + CS, ... over the cluster (fixed rank
-      // order) and decides their rotations; one remote load per rank and value
-      double* rb = rot + (it & 1) * 2 * pairs;
-      for (int p2 = q + JC_CS * warp; p2 < pairs; p2 += JC_CS * nwarps) {
-        // one warp per pair: lane l < CS reads rank l's three partials
-        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-        if (lane < JC_CS) {
-          const double* rp = cluster.map_shared_rank(pb, lane) + 3 * p2;
-          v0 = rp[0];
-          v1 = rp[1];
-          v2 = rp[2];
-        }
-#pragma unroll
-        for (int o = JC_CS / 2; o > 0; o >>= 1) {
-          v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-          v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-          v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-        }
-        if (lane == 0) {
-          const double al = v0, be = v1, ga = v2, ab = al * be;
-          double cs = 2.0, sn = 0.0;  // cs = 2: no rotation
-          if (ga != 0.0 && ga * ga > tol2 * ab && ab > floor4) {
-            const double zeta = (be - al) / (2.0 * ga);
-            const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-            cs = rsqrt(fma(t, t, 1.0));
-            sn = cs * t;
-          }
-          rb[2 * p2] = cs;
-          rb[2 * p2 + 1] = sn;
-        }
-      }
-      cluster.sync();
+      mbar_wait(bar, unsigned(ex >> 1) & 1u);
       if (act) {
-        // all-gather: the pair's rotation from the rank that decided it
-        const double2 cr = *reinterpret_cast<const double2*>(cluster.map_shared_rank(rb, pr % JC_CS) + 2 * pr);
-        const double cs = cr.x, sn = cr.y;
-        if (cs != 2.0) {
+        // lane o reads rank o's partials (local shared memory); the same fixed tree in every
+        // CTA, so every CTA takes the same decision for every pair
+        const double* sp = gb + (size_t(glane) * pairs + pr) * 4;
+        const double al = gsum(sp[0]), be = gsum(sp[1]), ga = gsum(sp[2]);
+        const double ab = al * be;
+        if (ga != 0.0 && ga * ga > tol2 * ab && ab > floor4) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
           for (int u = glane; u < na; u += JC_GS) {
             const double x = ai[u], y = aj[u];
             ai[u] = fma(cs, x, -sn * y);
@@ -1069,7 +1057,6 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
           }
         }
       }
-      ++it;
       if (++y1 == m1) y1 = 0;
       if (++y2 == m1) y2 = 0;
       __syncthreads();
@@ -1869,8 +1856,7 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
 size_t jacobi_cluster_smem(int r, int c) {
   const int pairs = ((c % 2 == 0) ? c : c + 1) / 2;
   const int na = (r + JC_CS - 1) / JC_CS + 1, nv = (c + JC_CS - 1) / JC_CS + 1;
-  return (size_t(c) * (na + nv) + 2 * size_t(std::max(3 * pairs, c)) + 4 * size_t(pairs) + 2 * size_t(c) + 2) *
-         sizeof(double);
+  return (size_t(c) * (na + nv) + 2 * size_t(JC_CS) * 4 * pairs + 4 * size_t(c) + 2) * sizeof(double);
 }
 
 // thin SVD of M (p x q): U (p x k), sigma (k, host), V (q x k), k = min(p, q)
@@ -1890,7 +1876,9 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
   }();
   const int pairs = ((c % 2 == 0) ? c : c + 1) / 2;
   const size_t csmem = jacobi_cluster_smem(r, c);
-  const bool cluster_ok = jacobi_env == 0 && c >= 24 && pairs * JC_GS <= 1024 && csmem <= 200 * 1024;
+  // measured (scripts/ubench_procrustes.py): the cluster kernel wins from ~100 columns (108: 2.1 vs 2.6 ms),
+  // the one-CTA kernel below (60: 0.65 vs 0.72 ms)
+  const bool cluster_ok = jacobi_env == 0 && c >= 96 && pairs * JC_GS <= 1024 && csmem <= 200 * 1024;
   if (cluster_ok || (smem <= 200 * 1024 && jacobi_env != 2)) {
     if (cluster_ok) {
       PTB_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csmem)));

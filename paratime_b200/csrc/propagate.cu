@@ -42,6 +42,8 @@
 
 #include <cooperative_groups.h>
 
+#include "ptb_dsmem.h"
+
 #include "ptb_internal.h"
 
 namespace ptb {
@@ -230,36 +232,7 @@ __global__ void __launch_bounds__(1024) k_small(const SmallArgs a) {
 // first had to receive this CTA's next-step rows, which it sends only after finishing the
 // reads of this step, so one mbarrier per buffer and no cluster-wide barrier per step.
 
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ unsigned cluster_map(unsigned addr, int rank) {
-  unsigned r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void st_async2(unsigned remote, double a, double b, unsigned remote_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(remote),
-               "d"(a), "d"(b), "r"(remote_bar)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  unsigned done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!done);
-}
+// smem_addr, cluster_map, st_async2, mbar_*: ptb_dsmem.h
 
 // Thread mapping: the CTA's rows are cut into 128-point chunks (nx % 128 == 0, so a chunk
 // lies in one row); warp w owns chunks RW w .. RW w + RW - 1 and in each chunk lane l owns the

@@ -5,6 +5,9 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 
+#include "../paratime_b200/csrc/ptb_dsmem.h"
+using namespace ptb;
+
 namespace cg = cooperative_groups;
 constexpr int ITERS = 4096;
 
@@ -59,6 +62,37 @@ __global__ void k_fp64_chain(long long* out, double seed) {
   if (x + y + z + w + v == -1.0) out[5] = 1;
 }
 
+// st.async ring: every CTA sends 16 bytes to the next rank and waits for its own 16 bytes
+// (mbarrier transaction count), ITERS times; cycles per hop
+__global__ void __cluster_dims__(8, 1, 1) k_st_async_ring(long long* out) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double buf[2][2];
+  __shared__ __align__(8) unsigned long long bars[2];
+  const unsigned bar0 = smem_addr(&bars[0]);
+  if (threadIdx.x == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  cl.sync();
+  const int peer = (cl.block_rank() + 1) % 8;
+  double acc = 0.0;
+  const long long t0 = clock64();
+  for (int i = 0; i < ITERS; ++i) {
+    const unsigned bar = bar0 + 8u * unsigned(i & 1);
+    if (threadIdx.x == 0) {
+      mbar_expect(bar, 16);
+      st_async2(cluster_map(smem_addr(&buf[i & 1][0]), peer), acc, 1.0, cluster_map(bar, peer));
+    }
+    mbar_wait(bar, unsigned(i >> 1) & 1u);
+    acc += buf[i & 1][1];
+    __syncthreads();
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0 && cl.block_rank() == 0) out[0] = (t1 - t0) / ITERS + (acc == -1.0 ? 1 : 0);
+  cl.sync();
+}
+
 int main() {
   long long* d;
   long long h[8] = {};
@@ -67,6 +101,9 @@ int main() {
   cudaMemcpy(h, d, 3 * sizeof(long long), cudaMemcpyDeviceToHost);
   std::printf("cycles/iter: cluster.sync %lld, cluster.sync+DSMEM load %lld, __syncthreads(256) %lld\n", h[0], h[1],
               h[2]);
+  k_st_async_ring<<<8, 256>>>(d);
+  cudaMemcpy(h, d, sizeof(long long), cudaMemcpyDeviceToHost);
+  std::printf("st.async + mbarrier ring hop: %lld cycles\n", h[0]);
   k_fp64_chain<<<1, 32>>>(d, 1.0);
   cudaMemcpy(h, d, 5 * sizeof(long long), cudaMemcpyDeviceToHost);
   std::printf("dependent cycles: ddiv %lld, dsqrt %lld, drsqrt %lld, 64-bit shfl+dfma %lld, dfma %lld\n", h[0], h[1],
