@@ -1390,6 +1390,11 @@ ProcWork::~ProcWork() {
     b->release();
   for (auto& b : TS) b.release();
   for (auto& b : TX) b.release();
+  for (auto& b : TS2) b.release();
+  for (auto& b : TX2) b.release();
+  for (auto& b : PA) b.release();
+  for (auto& b : PB) b.release();
+  BQ2b.release();
 }
 
 DevCorrector::~DevCorrector() {
@@ -1506,8 +1511,11 @@ __device__ __forceinline__ int selp(bool c, int a, int b) {
   return r;
 }
 
+// Two independent matrices per launch (update_svd's F and G): TS: blockIdx.y, else blockIdx.x
+// selects the argument set.
 template <int CPW, int RPL, bool PIVOT, bool TS>
-__global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
+__global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, const QrRegArgs a1) {
+  const QrRegArgs& a = (TS ? blockIdx.y : blockIdx.x) == 0 ? a0 : a1;
   constexpr int NMAX = CPW * QRR_WARPS, MMAX = 32 * RPL;
   __shared__ double cbuf[MMAX];
   __shared__ double nrm[2][NMAX];
@@ -1517,7 +1525,7 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = a.n;
   int r0 = 0, m = a.m;
-  if (TS) {
+  if (TS) {  // leaf blockIdx.x of matrix blockIdx.y
     r0 = ts_row0(blockIdx.x, a.m, a.nb);
     m = ts_row0(blockIdx.x + 1, a.m, a.nb) - r0;
   }
@@ -1702,9 +1710,21 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(QrRegArgs a) {
 // Xout[leaf rows, :] = H_0 ... H_{n-1} [Xin[i n : i n + n, :]; 0] -- one warp per four columns of
 // X held in registers (the reflector is read once for all four), the four dot products reduced
 // together (transposed butterfly: 6 double shuffles instead of 20, then 4 broadcasts)
-__global__ void __launch_bounds__(QRR_THREADS) k_tsqr_apply4(const double* V, int m, int n, int nb, const double* tau,
-                                                             const double* Xin, int ldin, int kq, double* Xout,
-                                                             int ldout) {
+struct TsApply {
+  const double* V;
+  int m, n, nb;
+  const double* tau;
+  const double* Xin;
+  int ldin, kq;
+  double* Xout;
+  int ldout;
+};
+__global__ void __launch_bounds__(QRR_THREADS) k_tsqr_apply4(const TsApply a0, const TsApply a1) {
+  const TsApply& A = blockIdx.y == 0 ? a0 : a1;  // matrix blockIdx.y (F, G)
+  const double* V = A.V;
+  const int m = A.m, n = A.n, nb = A.nb, ldin = A.ldin, kq = A.kq, ldout = A.ldout;
+  const double *tau = A.tau, *Xin = A.Xin;
+  double* Xout = A.Xout;
   extern __shared__ double tv[];  // reflectors rows x n (unit diagonal, zeros above) | tau[n]
   constexpr int PL = TS_ROWS / 32;
   const int i = blockIdx.x, r0 = ts_row0(i, m, nb), rows = ts_row0(i + 1, m, nb) - r0;
@@ -1771,6 +1791,31 @@ __global__ void __launch_bounds__(QRR_THREADS) k_tsqr_apply4(const double* V, in
   }
 }
 
+// thin Q (compact WY: dlarft / dorg2r order) and the un-pivoted R of a factor left in A by the
+// pivoted QR kernels (R above + beta on the diagonal, scaled reflectors below, tau, perm)
+void qr_form(ProcWork& w, const double* A, int m, int n, int keep, const double* tau, const int* perm,
+             DeviceBuffer& Qb, DeviceBuffer& Rb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  double* Q = static_cast<double*>(Qb.get(std::max<size_t>(1, size_t(m) * keep) * sizeof(double)));
+  double* R = static_cast<double*>(Rb.get(std::max<size_t>(1, size_t(keep) * n) * sizeof(double)));
+  if (keep == 0) return;
+  const size_t mk = size_t(m) * keep, kk = size_t(keep) * keep;
+  double* V = static_cast<double*>(w.buf[19].get(mk * sizeof(double)));
+  double* S = static_cast<double*>(w.buf[20].get(3 * kk * sizeof(double)));
+  double* T = S + kk;
+  double* W = T + kk;
+  k_wy_prep<<<unsigned(std::min<size_t>((mk + 255) / 256, size_t(ctx->num_sms) * 16)), 256, 0, st>>>(A, m, keep, V,
+                                                                                                    Q);
+  PTB_LAUNCH_CHECK(ctx);
+  gemm(ctx, true, false, keep, keep, m, 1.0, V, m, V, m, 0.0, S, keep);  // S = V^T V
+  wy_larft(ctx, st, S, tau, keep, T);
+  gemm(ctx, false, true, keep, keep, keep, 1.0, T, keep, V, m, 0.0, W, keep);  // W = T V1^T
+  gemm(ctx, false, false, m, keep, keep, -1.0, V, m, W, keep, 1.0, Q, m);     // Q = E - V W
+  k_unpivot_r<<<std::max(1, std::min(256, (keep * n + 255) / 256)), 256, 0, st>>>(A, m, n, keep, perm, R);
+  PTB_LAUNCH_CHECK(ctx);
+}
+
 // truncated_qr (procrustes.cpp:34-46): Q (m x keep) and R (keep x n, un-pivoted) in
 // caller buffers; A is copied (the input is not modified).  Returns keep.
 int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb,
@@ -1797,9 +1842,9 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
   const int reg = !small_env ? 0 : (m <= 128 && n <= 64) ? 1 : (m <= 256 && n <= 64) ? 2 : (m <= 128 && n <= 128) ? 3 : 0;
   if (reg) {  // register-resident pivoted QR (one CTA, two barriers per column)
     QrRegArgs ra{A, m, m, n, 0, 1, drop_tol, A, nullptr, 0, nullptr, 0, tau, perm, keep_d, betas};
-    if (reg == 1) k_qr_reg<4, 4, true, false><<<1, QRR_THREADS, 0, st>>>(ra);
-    else if (reg == 2) k_qr_reg<4, 8, true, false><<<1, QRR_THREADS, 0, st>>>(ra);
-    else k_qr_reg<8, 4, true, false><<<1, QRR_THREADS, 0, st>>>(ra);
+    if (reg == 1) k_qr_reg<4, 4, true, false><<<1, QRR_THREADS, 0, st>>>(ra, ra);
+    else if (reg == 2) k_qr_reg<4, 8, true, false><<<1, QRR_THREADS, 0, st>>>(ra, ra);
+    else k_qr_reg<8, 4, true, false><<<1, QRR_THREADS, 0, st>>>(ra, ra);
     PTB_LAUNCH_CHECK(ctx);
   } else if (small_env && small_smem <= 200 * 1024) {
     QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, nullptr, keep_d, betas};
@@ -1832,24 +1877,7 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
   int keep = 0;
   PTB_CUDA_CHECK(cudaMemcpyAsync(&keep, keep_d, sizeof(int), cudaMemcpyDeviceToHost, st));
   PTB_CUDA_CHECK(cudaStreamSynchronize(st));
-  double* Q = static_cast<double*>(Qb.get(std::max<size_t>(1, size_t(m) * keep) * sizeof(double)));
-  double* R = static_cast<double*>(Rb.get(std::max<size_t>(1, size_t(keep) * n) * sizeof(double)));
-  if (keep > 0) {
-    const size_t mk = size_t(m) * keep, kk = size_t(keep) * keep;
-    double* V = static_cast<double*>(w.buf[19].get(mk * sizeof(double)));
-    double* S = static_cast<double*>(w.buf[20].get(3 * kk * sizeof(double)));
-    double* T = S + kk;
-    double* W = T + kk;
-    k_wy_prep<<<unsigned(std::min<size_t>((mk + 255) / 256, size_t(ctx->num_sms) * 16)), 256, 0, st>>>(A, m, keep,
-                                                                                                      V, Q);
-    PTB_LAUNCH_CHECK(ctx);
-    gemm(ctx, true, false, keep, keep, m, 1.0, V, m, V, m, 0.0, S, keep);  // S = V^T V
-    wy_larft(ctx, st, S, tau, keep, T);
-    gemm(ctx, false, true, keep, keep, keep, 1.0, T, keep, V, m, 0.0, W, keep);  // W = T V1^T
-    gemm(ctx, false, false, m, keep, keep, -1.0, V, m, W, keep, 1.0, Q, m);     // Q = E - V W
-    k_unpivot_r<<<std::max(1, std::min(256, (keep * n + 255) / 256)), 256, 0, st>>>(A, m, n, keep, perm, R);
-    PTB_LAUNCH_CHECK(ctx);
-  }
+  qr_form(w, A, m, n, keep, tau, perm, Qb, Rb);
   return keep;
 }
 
@@ -2037,7 +2065,7 @@ int truncated_qr_tsqr(ProcWork& w, const double* A_in, int m, int n, double drop
     double* S = static_cast<double*>(w.TS[3 * L + 2].get(size_t(nb) * n * n * sizeof(double)));
     (void)rows_max;
     QrRegArgs la{cur, ld, curm, n, nb, 0, -1.0, nullptr, V, curm, S, nb * n, tau, nullptr, nullptr, nullptr};
-    k_qr_reg<4, 8, false, true><<<unsigned(nb), QRR_THREADS, 0, st>>>(la);
+    k_qr_reg<4, 8, false, true><<<unsigned(nb), QRR_THREADS, 0, st>>>(la, la);
     PTB_LAUNCH_CHECK(ctx);
     lv.push_back(Level{curm, nb, V, tau});
     cur = S;
@@ -2053,8 +2081,8 @@ int truncated_qr_tsqr(ProcWork& w, const double* A_in, int m, int n, double drop
     const Level& L = lv[size_t(l)];
     double* out = l == 0 ? Q : static_cast<double*>(w.TX[l & 1].get(size_t(L.m) * kq * sizeof(double)));
     const int rows_max = (L.m + L.nb - 1) / L.nb;
-    k_tsqr_apply4<<<unsigned(L.nb), QRR_THREADS, (size_t(rows_max) * n + n) * sizeof(double), st>>>(
-        L.V, L.m, n, L.nb, L.tau, X, ldx, kq, out, L.m);
+    const TsApply ap{L.V, L.m, n, L.nb, L.tau, X, ldx, kq, out, L.m};
+    k_tsqr_apply4<<<unsigned(L.nb), QRR_THREADS, (size_t(rows_max) * n + n) * sizeof(double), st>>>(ap, ap);
     PTB_LAUNCH_CHECK(ctx);
     X = out;
     ldx = L.m;
@@ -2064,14 +2092,126 @@ int truncated_qr_tsqr(ProcWork& w, const double* A_in, int m, int n, double drop
   return kq;
 }
 
-int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb, DeviceBuffer& Rb) {
-  // PTB_QR=direct | blocked | tsqr forces a route (tests, diagnostics)
+// PTB_QR=direct | blocked | tsqr forces a route (tests, diagnostics); 0 = automatic
+int qr_route_env() {
   static const int env = [] {
     const char* e = std::getenv("PTB_QR");
     if (!e) return 0;
     const std::string v(e);
     return v == "direct" ? 1 : v == "blocked" ? 2 : v == "tsqr" ? 3 : 0;
   }();
+  return env;
+}
+
+// update_svd's two QRs (F and G: same shape) through the TSQR route together: every leaf level
+// and every down-sweep level is one launch for both matrices, the two pivoted QRs of the last
+// stacks are one launch, and one host synchronisation reads both keep counts.  Each matrix goes
+// through exactly the arithmetic of truncated_qr_tsqr.  Returns false (nothing done) when the
+// shape is not a TSQR shape.
+bool truncated_qr_pair(ProcWork& w, const double* F, const double* G, int m, int n, double tol_f, double tol_g,
+                       DeviceBuffer& QF, DeviceBuffer& RF, DeviceBuffer& QG, DeviceBuffer& RG, int& kf, int& kg) {
+  if (!(m >= 8 * n && m > 1024 && n <= TS_MAXN && n > 0) || qr_route_env() != 0) return false;
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  struct Level {
+    int m, nb;
+    double *V[2], *tau[2];
+  };
+  std::vector<Level> lv;
+  const double* cur[2] = {F, G};
+  int curm = m, ld = m;
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(k_tsqr_apply4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int((size_t(TS_ROWS) * TS_MAXN + TS_MAXN) * sizeof(double))));
+  while (curm > TS_ROWS) {
+    const int L = int(lv.size());
+    if (3 * L + 2 >= int(sizeof(w.TS) / sizeof(w.TS[0]))) fail(PTB_UNSUPPORTED, "truncated_qr: TSQR depth");
+    const int nb = (curm + TS_ROWS - 1) / TS_ROWS;
+    Level lev{curm, nb, {}, {}};
+    QrRegArgs la[2];
+    double* S[2];
+    for (int b = 0; b < 2; ++b) {
+      DeviceBuffer* T = b == 0 ? w.TS : w.TS2;
+      lev.V[b] = static_cast<double*>(T[3 * L].get(size_t(curm) * n * sizeof(double)));
+      lev.tau[b] = static_cast<double*>(T[3 * L + 1].get(size_t(nb) * n * sizeof(double)));
+      S[b] = static_cast<double*>(T[3 * L + 2].get(size_t(nb) * n * n * sizeof(double)));
+      la[b] = QrRegArgs{cur[b], ld, curm, n, nb, 0, -1.0, nullptr, lev.V[b], curm, S[b], nb * n, lev.tau[b],
+                        nullptr, nullptr, nullptr};
+    }
+    k_qr_reg<4, 8, false, true><<<dim3(unsigned(nb), 2), QRR_THREADS, 0, st>>>(la[0], la[1]);
+    PTB_LAUNCH_CHECK(ctx);
+    lv.push_back(lev);
+    cur[0] = S[0];
+    cur[1] = S[1];
+    curm = nb * n;
+    ld = curm;
+  }
+  // pivoted QRs of the two last stacks (curm <= TS_ROWS rows), one launch, one sync
+  double* A[2];
+  double* tau[2];
+  int* perm[2];
+  int* keep_d = static_cast<int*>(w.buf[3].get(2 * sizeof(int)));
+  QrRegArgs ra[2];
+  const double tol[2] = {tol_f, tol_g};
+  for (int b = 0; b < 2; ++b) {
+    DeviceBuffer* P = b == 0 ? w.PA : w.PB;  // [0] factor, [1] tau, [2] perm, [3] |R_jj|
+    A[b] = static_cast<double*>(P[0].get(size_t(curm) * n * sizeof(double)));
+    tau[b] = static_cast<double*>(P[1].get(size_t(n) * sizeof(double)));
+    perm[b] = static_cast<int*>(P[2].get(size_t(n) * sizeof(int)));
+    double* betas = static_cast<double*>(P[3].get(size_t(n) * sizeof(double)));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(A[b], cur[b], size_t(curm) * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    ra[b] = QrRegArgs{A[b], curm, curm, n, 0, 1, tol[b], A[b], nullptr, 0, nullptr, 0, tau[b], perm[b], keep_d + b,
+                      betas};
+  }
+  if (curm <= 128) k_qr_reg<4, 4, true, false><<<2, QRR_THREADS, 0, st>>>(ra[0], ra[1]);
+  else k_qr_reg<4, 8, true, false><<<2, QRR_THREADS, 0, st>>>(ra[0], ra[1]);
+  PTB_LAUNCH_CHECK(ctx);
+  int keep[2] = {0, 0};
+  PTB_CUDA_CHECK(cudaMemcpyAsync(keep, keep_d, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+  DeviceBuffer* Qt[2] = {&w.BQ2, &w.BQ2b};
+  DeviceBuffer* Qo[2] = {&QF, &QG};
+  DeviceBuffer* Ro[2] = {&RF, &RG};
+  for (int b = 0; b < 2; ++b) {
+    qr_form(w, A[b], curm, n, keep[b], tau[b], perm[b], *Qt[b], *Ro[b]);
+    Qo[b]->get(std::max<size_t>(1, size_t(m) * keep[b]) * sizeof(double));
+  }
+  kf = keep[0];
+  kg = keep[1];
+  if (lv.empty()) {
+    for (int b = 0; b < 2; ++b)
+      if (keep[b] > 0)
+        PTB_CUDA_CHECK(cudaMemcpyAsync(Qo[b]->ptr, Qt[b]->ptr, size_t(m) * keep[b] * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st));
+    return true;
+  }
+  const double* X[2] = {static_cast<const double*>(w.BQ2.ptr), static_cast<const double*>(w.BQ2b.ptr)};
+  int ldx = curm;
+  for (int l = int(lv.size()) - 1; l >= 0; --l) {
+    const Level& L = lv[size_t(l)];
+    TsApply ap[2];
+    double* out[2];
+    for (int b = 0; b < 2; ++b) {
+      DeviceBuffer* TX = b == 0 ? w.TX : w.TX2;
+      out[b] = l == 0 ? static_cast<double*>(Qo[b]->ptr)
+                      : static_cast<double*>(TX[l & 1].get(std::max<size_t>(1, size_t(L.m) * keep[b]) *
+                                                           sizeof(double)));
+      ap[b] = TsApply{L.V[b], L.m, n, L.nb, L.tau[b], X[b], ldx, keep[b], out[b], L.m};
+    }
+    const int rows_max = (L.m + L.nb - 1) / L.nb;
+    if (keep[0] > 0 || keep[1] > 0) {
+      k_tsqr_apply4<<<dim3(unsigned(L.nb), 2), QRR_THREADS, (size_t(rows_max) * n + n) * sizeof(double), st>>>(
+          ap[0], ap[1]);
+      PTB_LAUNCH_CHECK(ctx);
+    }
+    X[0] = out[0];
+    X[1] = out[1];
+    ldx = L.m;
+  }
+  return true;
+}
+
+int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb, DeviceBuffer& Rb) {
+  const int env = qr_route_env();
   const bool tall = m >= 8 * n && m > TS_ROWS;
   if (env == 1) return truncated_qr_direct(w, A_in, m, n, drop_tol, Qb, Rb);
   if (env == 3 && tall && n <= TS_MAXN) return truncated_qr_tsqr(w, A_in, m, n, drop_tol, Qb, Rb);
@@ -2241,10 +2381,15 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
   const double fn = std::sqrt(dev_sumsq(ctx, F, size_t(rows) * cols, w.buf[11]));
   const double gn = std::sqrt(dev_sumsq(ctx, G, size_t(rows) * cols, w.buf[11]));
   hp_.mark("update: norms");
-  const int qf = truncated_qr(w, Fr, rows, cols, qr_guard * fn, w.QF, w.RF);
-  hp_.mark("update: qr F");
-  const int qg = truncated_qr(w, Gr, rows, cols, qr_guard * gn, w.QG, w.RG);
-  hp_.mark("update: qr G");
+  int qf = 0, qg = 0;
+  if (truncated_qr_pair(w, Fr, Gr, rows, cols, qr_guard * fn, qr_guard * gn, w.QF, w.RF, w.QG, w.RG, qf, qg)) {
+    hp_.mark("update: qr F+G (batched TSQR)");
+  } else {
+    qf = truncated_qr(w, Fr, rows, cols, qr_guard * fn, w.QF, w.RF);
+    hp_.mark("update: qr F");
+    qg = truncated_qr(w, Gr, rows, cols, qr_guard * gn, w.QG, w.RG);
+    hp_.mark("update: qr G");
+  }
   double* LB = static_cast<double*>(w.buf[17].get(std::max<size_t>(1, size_t(r + qf) * cols) * sizeof(double)));
   double* RB = static_cast<double*>(w.buf[18].get(std::max<size_t>(1, size_t(r + qg) * cols) * sizeof(double)));
   const unsigned nb = unsigned(std::max(1, std::min(1024, ((r + std::max(qf, qg)) * cols + 255) / 256)));

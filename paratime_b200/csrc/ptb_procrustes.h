@@ -32,6 +32,8 @@ struct ProcWork {
   DeviceBuffer SX, SY;      // spare corrector factors: update_svd writes here, then swaps
   DeviceBuffer BA, BV, BT, BR, BQ2;  // blocked tall QR: work copy, reflectors, tau/T/W, R1, Q2
   DeviceBuffer TS[24], TX[2];       // TSQR: per level reflectors, tau, R stack; Q down-sweep ping-pong
+  DeviceBuffer TS2[24], TX2[2], BQ2b;  // the second matrix of a batched (F, G) TSQR
+  DeviceBuffer PA[4], PB[4];        // batched TSQR: the two final pivoted factors, tau, perm, |R_jj|
   explicit ProcWork(ptb_context* c);
   ~ProcWork();
 };
