@@ -768,10 +768,9 @@ __global__ void __launch_bounds__(512) k_jacobi_small(JacobiArgs a) {
   const double eps = 2.220446049250313e-16;
   const double tol2 = eps * eps * double(r);
   const int glane = tid & (GS - 1), pr = tid / GS;  // one pair per group
-  const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1u) << (lane & ~(GS - 1)));
-  auto gsum = [&](double x) {
+  auto gsum = [&](double x) {  // xor offsets < GS stay inside the group; all 32 lanes take part
 #pragma unroll
-    for (int o = GS / 2; o > 0; o >>= 1) x += __shfl_xor_sync(gmask, x, o);
+    for (int o = GS / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
   };
   // tournament positions of this group's pair: pos(q) = q == 0 ? 0 : 1 + (q - 1 + round) % (cc - 1)
@@ -796,66 +795,67 @@ __global__ void __launch_bounds__(512) k_jacobi_small(JacobiArgs a) {
     const double floor4 = floor2 * floor2;
     int y1 = x1, y2 = x2;
     for (int round = 0; round < m1; ++round) {
-      if (pr < cc / 2) {
-        int i = pr == 0 ? 0 : 1 + y1, j = 1 + y2;
-        if (i > j) {
-          const int t = i;
-          i = j;
-          j = t;
-        }
-        if (j < c) {
-          // the pair's rows in registers: all loads issued together, reused by the rotation
-          double* ai = A + size_t(i) * r;
-          double* aj = A + size_t(j) * r;
-          double x[RPL], y[RPL];
+      // every lane of the warp reaches the shuffles (full-warp masks; a per-group partial mask
+      // makes the warp serialise its groups, ncu: BRA.DIV + WARPSYNC on the reductions);
+      // inactive groups compute on zeros and store nothing
+      int i = pr == 0 ? 0 : 1 + y1, j = 1 + y2;
+      if (i > j) {
+        const int t = i;
+        i = j;
+        j = t;
+      }
+      const bool act = pr < cc / 2 && j < c;
+      if (!act) i = j = 0;
+      // the pair's rows in registers: all loads issued together, reused by the rotation
+      double* ai = A + size_t(i) * r;
+      double* aj = A + size_t(j) * r;
+      double x[RPL], y[RPL];
 #pragma unroll
-          for (int t = 0; t < RPL; ++t) {
-            const int k = glane + GS * t;
-            x[t] = k < r ? ai[k] : 0.0;
-            y[t] = k < r ? aj[k] : 0.0;
-          }
-          double al = 0.0, be = 0.0, ga = 0.0;
+      for (int t = 0; t < RPL; ++t) {
+        const int k = glane + GS * t;
+        x[t] = act && k < r ? ai[k] : 0.0;
+        y[t] = act && k < r ? aj[k] : 0.0;
+      }
+      double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-          for (int t = 0; t < RPL; ++t) {
-            al = fma(x[t], x[t], al);
-            be = fma(y[t], y[t], be);
-            ga = fma(x[t], y[t], ga);
-          }
-          al = gsum(al);
-          be = gsum(be);
-          ga = gsum(ga);
-          const double ab = al * be;
-          if (ga != 0.0 && ga * ga > tol2 * ab && ab > floor4) {
-            const double zeta = (be - al) / (2.0 * ga);
-            const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-            const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+      for (int t = 0; t < RPL; ++t) {
+        al = fma(x[t], x[t], al);
+        be = fma(y[t], y[t], be);
+        ga = fma(x[t], y[t], ga);
+      }
+      al = gsum(al);
+      be = gsum(be);
+      ga = gsum(ga);
+      const double ab = al * be;
+      if (act && ga != 0.0 && ga * ga > tol2 * ab && ab > floor4) {
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
 #pragma unroll
-            for (int u = 0; u < RPL; ++u) {
-              const int k = glane + GS * u;
-              if (k < r) {
-                ai[k] = fma(cs, x[u], -sn * y[u]);
-                aj[k] = fma(sn, x[u], cs * y[u]);
-              }
-            }
-            double* vi = V + size_t(i) * c;  // V's columns through the same registers
-            double* vj = V + size_t(j) * c;
-#pragma unroll
-            for (int u = 0; u < RPL; ++u) {
-              const int k = glane + GS * u;
-              x[u] = k < c ? vi[k] : 0.0;
-              y[u] = k < c ? vj[k] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < RPL; ++u) {
-              const int k = glane + GS * u;
-              if (k < c) {
-                vi[k] = fma(cs, x[u], -sn * y[u]);
-                vj[k] = fma(sn, x[u], cs * y[u]);
-              }
-            }
-            if (glane == 0) rotated = 1;
+        for (int u = 0; u < RPL; ++u) {
+          const int k = glane + GS * u;
+          if (k < r) {
+            ai[k] = fma(cs, x[u], -sn * y[u]);
+            aj[k] = fma(sn, x[u], cs * y[u]);
           }
         }
+        double* vi = V + size_t(i) * c;  // V's columns through the same registers
+        double* vj = V + size_t(j) * c;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int k = glane + GS * u;
+          x[u] = k < c ? vi[k] : 0.0;
+          y[u] = k < c ? vj[k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int k = glane + GS * u;
+          if (k < c) {
+            vi[k] = fma(cs, x[u], -sn * y[u]);
+            vj[k] = fma(sn, x[u], cs * y[u]);
+          }
+        }
+        if (glane == 0) rotated = 1;
       }
       if (++y1 == m1) y1 = 0;
       if (++y2 == m1) y2 = 0;
@@ -902,9 +902,9 @@ __global__ void __launch_bounds__(512) k_jacobi_small(JacobiArgs a) {
 // remote stores, ncu: ERRBAR 31 % of stall samples); then every CTA sums the partials of every
 // pair in the same fixed rank order, takes the same decision and applies the rotation to its own
 // rows.  Same tournament schedule and stopping rules as k_jacobi_small; deterministic.
-constexpr int JC_CS = 8, JC_GS = 8;
-static_assert(JC_GS == JC_CS, "one lane per cluster rank in the partial exchange");
+constexpr int JC_CS = 8;
 
+template <int JC_GS>  // lanes per pair
 __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double jc[];
@@ -917,7 +917,8 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
   // the exchanged buffers first: map_shared_rank maps the same offset in every CTA, and the row
   // counts (hence the A/V tile sizes) differ between CTAs
   double* gath = jc;                        // [2][CS][pairs][4]: partials pushed by every rank
-  double* cn = gath + 2 * JC_CS * 4 * pairs;  // [2][c]: per-column partial norms
+  double* stg = gath + 2 * JC_CS * 4 * pairs;  // [2][pairs][4]: this rank's partials, staged
+  double* cn = stg + 2 * 4 * pairs;         // [2][c]: per-column partial norms
   double* sv = cn + 2 * c;                  // c
   int* order = reinterpret_cast<int*>(sv + c);  // c (c / 2 doubles)
   double* Ao = sv + c + (c + 1) / 2;        // c columns x na rows
@@ -926,7 +927,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
   __shared__ double s_colmax;
   __shared__ __align__(8) unsigned long long bars[2];  // one mbarrier per exchange buffer
   const unsigned bar0 = smem_addr(&bars[0]);
-  const unsigned round_bytes = unsigned(JC_CS * (c / 2) * 4 * sizeof(double));
+  const unsigned round_bytes = unsigned(JC_CS * pairs * 4 * sizeof(double));
   if (tid == 0) {
     mbar_init(bar0, 1);
     mbar_init(bar0 + 8, 1);
@@ -943,12 +944,12 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
   const double eps = 2.220446049250313e-16;
   const double tol2 = eps * eps * double(r);
   const int glane = tid & (JC_GS - 1), pr = tid / JC_GS;
-  const unsigned gmask = ((1u << JC_GS) - 1u) << (lane & ~(JC_GS - 1));
-  auto gsum = [&](double x) {
+  auto gsum = [&](double x) {  // xor offsets < GS stay inside the group; all 32 lanes take part
 #pragma unroll
-    for (int o = JC_GS / 2; o > 0; o >>= 1) x += __shfl_xor_sync(gmask, x, o);
+    for (int o = JC_GS / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
   };
+  long long ph[5] = {0, 0, 0, 0, 0};  // diagnostics (rank 0, thread 0 written at the end)
   int it = 0;  // parity of the column-norm buffers, advanced at every column-norm exchange
   int ex = 0;  // pair-partial exchanges so far (buffer and mbarrier phase)
   // column norms^2 of A over the cluster -> sv (identical in every CTA)
@@ -995,6 +996,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
       // partials, which are sent after this round's reads)
       double* gb = gath + (ex & 1) * JC_CS * 4 * pairs;
       const unsigned bar = bar0 + 8u * unsigned(ex & 1);
+      const long long tc0 = clock64();
       if (tid == 0) mbar_expect(bar, round_bytes);
       int i = 0, j = 0;
       bool act = false;
@@ -1010,33 +1012,52 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
       }
       double* ai = Ao + size_t(i) * na;
       double* aj = Ao + size_t(j) * na;
-      if (act) {
-        double al = 0.0, be = 0.0, ga = 0.0;
+      // all lanes reach the shuffles (full-warp masks); inactive groups sum zeros, send nothing
+      double al = 0.0, be = 0.0, ga = 0.0;
+      if (act)
         for (int t = glane; t < na; t += JC_GS) {
           const double x = ai[t], y = aj[t];
           al = fma(x, x, al);
           be = fma(y, y, be);
           ga = fma(x, y, ga);
         }
-        al = gsum(al);
-        be = gsum(be);
-        ga = gsum(ga);
-        // all-gather by push: lane l sends this rank's partials into rank l's buffer with
-        // st.async, completing bytes on rank l's mbarrier
-        const unsigned dst = cluster_map(smem_addr(gb + (size_t(q) * pairs + pr) * 4), glane);
-        const unsigned rbar = cluster_map(bar, glane);
-        st_async2(dst, al, be, rbar);
-        st_async2(dst + 16u, ga, 0.0, rbar);
+      al = gsum(al);
+      be = gsum(be);
+      ga = gsum(ga);
+      // all-gather by push: the partials of all pairs are staged locally, then thread t < CS
+      // sends the block to rank t with ONE bulk copy completing on rank t's mbarrier (per-pair
+      // st.async made every CTA's mbarrier absorb CS x pairs transaction updates per round)
+      double* sg = stg + (ex & 1) * 4 * pairs;
+      if (act && glane == 0) {
+        sg[4 * pr] = al;
+        sg[4 * pr + 1] = be;
+        sg[4 * pr + 2] = ga;
       }
+      __syncthreads();
+      if (tid < JC_CS) {
+        fence_proxy_async_smem();
+        bulk_to_peer(cluster_map(smem_addr(gb + size_t(q) * pairs * 4), tid), smem_addr(sg),
+                     unsigned(pairs * 4 * sizeof(double)), cluster_map(bar, tid));
+      }
+      const long long tc1 = clock64();
       mbar_wait(bar, unsigned(ex >> 1) & 1u);
-      if (act) {
-        // lane o reads rank o's partials (local shared memory); the same fixed tree in every
-        // CTA, so every CTA takes the same decision for every pair
-        const double* sp = gb + (size_t(glane) * pairs + pr) * 4;
-        const double al = gsum(sp[0]), be = gsum(sp[1]), ga = gsum(sp[2]);
-        const double ab = al * be;
-        if (ga != 0.0 && ga * ga > tol2 * ab && ab > floor4) {
-          const double zeta = (be - al) / (2.0 * ga);
+      const long long tc2 = clock64();
+      {
+        // lane l sums ranks l, l + GS, ... (local shared memory), then the group tree: the same
+        // fixed order in every CTA, so every CTA takes the same decision for every pair
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        if (act)
+#pragma unroll
+          for (int o = glane; o < JC_CS; o += JC_GS) {
+            const double* sp = gb + (size_t(o) * pairs + pr) * 4;
+            s0 += sp[0];
+            s1 += sp[1];
+            s2 += sp[2];
+          }
+        const double al2 = gsum(s0), be2 = gsum(s1), ga2 = gsum(s2);
+        const double ab = al2 * be2;
+        if (act && ga2 != 0.0 && ga2 * ga2 > tol2 * ab && ab > floor4) {
+          const double zeta = (be2 - al2) / (2.0 * ga2);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
           const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
           for (int u = glane; u < na; u += JC_GS) {
@@ -1057,9 +1078,16 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
           }
         }
       }
+      const long long tc3 = clock64();
       if (++y1 == m1) y1 = 0;
       if (++y2 == m1) y2 = 0;
       __syncthreads();
+      const long long tc4 = clock64();
+      ph[0] += tc1 - tc0;  // diagnostics: cycles per phase, summed over rounds (registers)
+      ph[1] += tc2 - tc1;
+      ph[2] += tc3 - tc2;
+      ph[3] += tc4 - tc3;
+      ++ph[4];
     }
     if (q == 0 && tid == 0 && sweep < 16) a.tmp[size_t(r) * c + size_t(c) * c + c + 1 + sweep] = double(nrot);
     if (!any_rot) break;
@@ -1086,7 +1114,11 @@ __global__ void __launch_bounds__(1024) k_jacobi_cluster(JacobiArgs a) {
   }
   if (q == 0) {
     for (int k = tid; k < c; k += blockDim.x) a.sigma[k] = sv[order[k]];
-    if (tid == 0) a.tmp[size_t(r) * c + size_t(c) * c + c] = double(sweep);  // diagnostics
+    if (tid == 0) {  // diagnostics
+      double* dg = a.tmp + size_t(r) * c + size_t(c) * c + c;
+      dg[0] = double(sweep);
+      for (int k = 0; k < 5; ++k) dg[17 + k] = double(ph[k]);
+    }
   }
   cluster.sync();  // no CTA leaves while another may still read its shared memory
 }
@@ -1881,10 +1913,11 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
   return keep;
 }
 
+constexpr int JC_GS_DEFAULT = 4;  // measured: 108^2 2.22 ms (GS 4) vs 2.32 (8), 2.31 (2), 2.80 (1)
 size_t jacobi_cluster_smem(int r, int c) {
   const int pairs = ((c % 2 == 0) ? c : c + 1) / 2;
   const int na = (r + JC_CS - 1) / JC_CS + 1, nv = (c + JC_CS - 1) / JC_CS + 1;
-  return (size_t(c) * (na + nv) + 2 * size_t(JC_CS) * 4 * pairs + 4 * size_t(c) + 2) * sizeof(double);
+  return (size_t(c) * (na + nv) + 2 * size_t(JC_CS + 1) * 4 * pairs + 4 * size_t(c) + 4) * sizeof(double);
 }
 
 // thin SVD of M (p x q): U (p x k), sigma (k, host), V (q x k), k = min(p, q)
@@ -1894,6 +1927,7 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
   ptb_context* ctx = w.ctx;
   cudaStream_t st = ctx->stream;
   JacobiArgs ja{A, V, r, c, sg, order, tmp, 40};
+  PTB_CUDA_CHECK(cudaMemsetAsync(tmp + size_t(r) * c + size_t(c) * c + c + 17, 0, 5 * sizeof(double), st));
   const size_t smem = (size_t(r) * c + size_t(c) * c) * sizeof(double);
   static const int jacobi_env = [] {  // PTB_JACOBI=single: one-CTA global-memory kernel; =coop: grid
     const char* e = std::getenv("PTB_JACOBI");
@@ -1906,13 +1940,23 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
   const size_t csmem = jacobi_cluster_smem(r, c);
   // measured (scripts/ubench_procrustes.py): the cluster kernel wins from ~100 columns (108: 2.1 vs 2.6 ms),
   // the one-CTA kernel below (60: 0.65 vs 0.72 ms)
-  const bool cluster_ok = jacobi_env == 0 && c >= 96 && pairs * JC_GS <= 1024 && csmem <= 200 * 1024;
+  const bool cluster_ok = jacobi_env == 0 && c >= 96 && pairs * 8 <= 1024 && csmem <= 200 * 1024;
   if (cluster_ok || (smem <= 200 * 1024 && jacobi_env != 2)) {
     if (cluster_ok) {
-      PTB_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csmem)));
+      static const int gs_env = [] {  // PTB_JACOBI_GS: lanes per pair in the cluster kernel (1, 2, 4, 8)
+        const char* e = std::getenv("PTB_JACOBI_GS");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
+      }();
+      const int gs = gs_env ? gs_env : JC_GS_DEFAULT;
+      const void* kern = gs == 1   ? reinterpret_cast<const void*>(k_jacobi_cluster<1>)
+                         : gs == 2 ? reinterpret_cast<const void*>(k_jacobi_cluster<2>)
+                         : gs == 4 ? reinterpret_cast<const void*>(k_jacobi_cluster<4>)
+                                   : reinterpret_cast<const void*>(k_jacobi_cluster<8>);
+      PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csmem)));
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(JC_CS);
-      cfg.blockDim = dim3(unsigned(std::max(32, (pairs * JC_GS + 31) / 32 * 32)));
+      cfg.blockDim = dim3(unsigned(std::max(32, (pairs * gs + 31) / 32 * 32)));
       cfg.dynamicSmemBytes = csmem;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
@@ -1922,7 +1966,8 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      PTB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_jacobi_cluster, ja));
+      void* args[] = {&ja};
+      PTB_CUDA_CHECK(cudaLaunchKernelExC(&cfg, kern, args));
     } else if (r <= 128 && pairs * 8 <= 512) {  // one 8-lane group per pair, <= 16 rows per lane
       PTB_CUDA_CHECK(
           cudaFuncSetAttribute(k_jacobi_small<8, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1952,8 +1997,11 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
     PTB_LAUNCH_CHECK(ctx);
   }
   if (HostProf(st).on) {  // diagnostics: sweeps used (written after the singular values)
-    double d[17] = {};
+    double d[22] = {};
     PTB_CUDA_CHECK(cudaMemcpyAsync(d, tmp + size_t(r) * c + size_t(c) * c + c, sizeof(d), cudaMemcpyDeviceToHost, st));
+    if (d[21] > 0)
+      std::fprintf(stderr, "[ptb prof] jacobi cluster cycles/round: partials+send %.0f, wait %.0f, decide+rotate %.0f, barrier %.0f\n",
+                   d[17] / d[21], d[18] / d[21], d[19] / d[21], d[20] / d[21]);
     PTB_CUDA_CHECK(cudaStreamSynchronize(st));
     std::fprintf(stderr, "[ptb prof] jacobi %d x %d: %g sweeps; rotations per sweep (cluster kernel):", r, c, d[0]);
     for (int k = 1; k < 17 && k <= int(d[0]) + 1; ++k) std::fprintf(stderr, " %g", d[k]);
@@ -2262,7 +2310,7 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
     double* V = static_cast<double*>(w.buf[7].get(std::max<size_t>(1, size_t(kq) * kq) * sizeof(double)));
     double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
     int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
-    double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 17) * sizeof(double)));
+    double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 22) * sizeof(double)));
     std::vector<double> s_k(size_t(kq), 0.0);
     if (kq > 0) {
       // Bt = R^T (c x kq): R is kq x c column-major
@@ -2290,7 +2338,7 @@ void thin_svd(ProcWork& w, const double* M, int p, int q, DeviceBuffer& Ub, std:
   double* V = static_cast<double*>(w.buf[7].get(size_t(c) * c * sizeof(double)));
   double* sg = static_cast<double*>(w.buf[8].get(size_t(c) * sizeof(double)));
   int* order = static_cast<int*>(w.buf[9].get(size_t(c) * sizeof(int)));
-  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 17) * sizeof(double)));
+  double* tmp = static_cast<double*>(w.buf[10].get((size_t(r) * c + size_t(c) * c + c + 22) * sizeof(double)));
   jacobi_core(w, A, r, c, V, sg, tmp, order);
   PTB_CUDA_CHECK(cudaMemcpyAsync(sigma.data(), sg, size_t(c) * sizeof(double), cudaMemcpyDeviceToHost, st));
   // M = A_sorted diag(s) V^T  (A is r x c = U when !trans; when trans, M^T = A S V^T -> M = V S A^T)

@@ -18,6 +18,21 @@ __device__ __forceinline__ void st_async2(unsigned remote, double a, double b, u
                "d"(a), "d"(b), "r"(remote_bar)
                : "memory");
 }
+// bulk copy of `bytes` (multiple of 16, 16-byte aligned) from this CTA's shared memory to a
+// cluster peer's, completing the bytes on the peer's mbarrier (one transaction instead of
+// bytes / 16 st.async updates of the peer's mbarrier)
+__device__ __forceinline__ void bulk_to_peer(unsigned remote_dst, unsigned local_src, unsigned bytes,
+                                             unsigned remote_bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          remote_dst),
+      "r"(local_src), "r"(bytes), "r"(remote_bar)
+      : "memory");
+}
+// generic-proxy shared-memory writes visible to the async proxy (before a bulk copy reads them)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
 }

@@ -49,9 +49,9 @@ __global__ void k_fp64_chain(long long* out, double seed) {
   for (int i = 0; i < ITERS; ++i) z = rsqrt(z + 1.0);
   t1 = clock64();
   if (threadIdx.x == 0) out[2] = (t1 - t0) / ITERS;
-  double w = 0.5;
+  double w = 0.5 + threadIdx.x;  // lane-dependent: a uniform value lets the compiler drop the shuffle
   t0 = clock64();
-  for (int i = 0; i < ITERS; ++i) w = __shfl_xor_sync(0xffffffffu, w, 1) * 0.999 + 0.001;
+  for (int i = 0; i < ITERS; ++i) w = __shfl_xor_sync(0xffffffffu, w, 1 + (i & 3)) * 0.999 + 0.001;
   t1 = clock64();
   if (threadIdx.x == 0) out[3] = (t1 - t0) / ITERS;
   double v = 0.5;
@@ -60,6 +60,29 @@ __global__ void k_fp64_chain(long long* out, double seed) {
   t1 = clock64();
   if (threadIdx.x == 0) out[4] = (t1 - t0) / ITERS;
   if (x + y + z + w + v == -1.0) out[5] = 1;
+}
+
+// issue cost of one st.async (16 B) to the next rank + mapa, no waiting (ITERS sends, one
+// mbarrier wait for all bytes at the end)
+__global__ void __cluster_dims__(8, 1, 1) k_st_async_issue(long long* out) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double buf[2];
+  __shared__ __align__(8) unsigned long long bar;
+  const unsigned b0 = smem_addr(&bar);
+  if (threadIdx.x == 0) {
+    mbar_init(b0, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  cl.sync();
+  const int peer = (cl.block_rank() + 1) % 8;
+  if (threadIdx.x == 0) mbar_expect(b0, 16u * ITERS);
+  const long long t0 = clock64();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < ITERS; ++i) st_async2(cluster_map(smem_addr(&buf[0]), peer), 1.0, double(i), cluster_map(b0, peer));
+  const long long t1 = clock64();
+  mbar_wait(b0, 0);
+  if (threadIdx.x == 0 && cl.block_rank() == 0) out[0] = (t1 - t0) / ITERS;
+  cl.sync();
 }
 
 // st.async ring: every CTA sends 16 bytes to the next rank and waits for its own 16 bytes
@@ -104,6 +127,9 @@ int main() {
   k_st_async_ring<<<8, 256>>>(d);
   cudaMemcpy(h, d, sizeof(long long), cudaMemcpyDeviceToHost);
   std::printf("st.async + mbarrier ring hop: %lld cycles\n", h[0]);
+  k_st_async_issue<<<8, 32>>>(d);
+  cudaMemcpy(h, d, sizeof(long long), cudaMemcpyDeviceToHost);
+  std::printf("st.async issue (one thread, back to back): %lld cycles each\n", h[0]);
   k_fp64_chain<<<1, 32>>>(d, 1.0);
   cudaMemcpy(h, d, 5 * sizeof(long long), cudaMemcpyDeviceToHost);
   std::printf("dependent cycles: ddiv %lld, dsqrt %lld, drsqrt %lld, 64-bit shfl+dfma %lld, dfma %lld\n", h[0], h[1],
