@@ -186,6 +186,14 @@ ptb_status ptb_speed_model_write(const ptb_grid* grid, const double* c, char* bu
  * malformed input (the reference's ConfigError, message in ptb_last_error()). */
 ptb_status ptb_speed_model_read(const char* text, ptb_grid* grid, double* c, size_t cap, size_t* npoints);
 
+/* run-record CSV schemas of the reference's harness (experiment.cpp:596-628, write_run_files):
+ * which = 0 errors.csv, 1 residuals.csv (header only when plain), 2 summary.csv, for K = iterations
+ * records x couplings values (row-major energy_err, l2_err; per record residual, rank, diverged).
+ * Host only.  Replaces: the reference writes these files only from run_experiment (no API). */
+ptb_status ptb_run_csv(size_t iterations, size_t couplings, const double* energy_err, const double* l2_err,
+                       const double* residual, const int* rank, const int* diverged, int plain, int which, char* buf,
+                       size_t len, size_t* needed);
+
 /* ---- parareal drivers (parareal.hpp:60-79) -------------------------------------------- */
 typedef enum { PTB_PLAIN = 0, PTB_THETA = 1, PTB_CORRECTED_COARSE_ONLY = 2, PTB_OMEGA_IDENTITY = 3 } ptb_variant;
 

@@ -239,6 +239,25 @@ def write_speed_model(grid: Grid, c) -> str:
     return buf.value.decode()
 
 
+def run_csv(energy_err, l2_err, residual, rank, diverged, plain: bool, which: str) -> str:
+    """The reference harness's run-record CSV text (experiment.cpp:596-628): which is "errors",
+    "residuals" or "summary"; energy_err / l2_err are K x (N + 1), the rest length K."""
+    ee = np.ascontiguousarray(energy_err, dtype=np.float64)
+    l2 = np.ascontiguousarray(l2_err, dtype=np.float64)
+    res = np.ascontiguousarray(residual, dtype=np.float64)
+    rk = np.ascontiguousarray(rank, dtype=np.int32)
+    dv = np.ascontiguousarray(diverged, dtype=np.int32)
+    K, N1 = ee.shape
+    w = {"errors": 0, "residuals": 1, "summary": 2}[which]
+    args = (C.c_size_t(K), C.c_size_t(N1), _dp(ee), _dp(l2), _dp(res), rk.ctypes.data_as(C.c_void_p),
+            dv.ctypes.data_as(C.c_void_p), C.c_int(int(plain)), C.c_int(w))
+    need = C.c_size_t()
+    check(lib().ptb_run_csv(*args, None, C.c_size_t(0), C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(lib().ptb_run_csv(*args, buf, C.c_size_t(need.value), C.byref(need)))
+    return buf.value.decode()
+
+
 def read_speed_model(text: str):
     """read_speed_model (experiment.hpp:86): (Grid, c as grid.shape); PtbError(CONFIG) on malformed
     input, as the reference's ConfigError."""

@@ -13,6 +13,7 @@
 #include <functional>
 #include <cstring>
 #include <sstream>
+#include <filesystem>
 #include <fstream>
 #include <cstdio>
 #include <istream>
@@ -25,6 +26,7 @@
 
 #include "paratime/energy_map.hpp"
 #include "paratime/errors.hpp"
+#include "paratime/run_files.hpp"
 #include "paratime/speed_model.hpp"
 #include "paratime/grid.hpp"
 #include "paratime/parareal.hpp"
@@ -834,6 +836,44 @@ SpeedField to_field(SpeedText t) {
 
 }  // namespace
 
+// ---- run-record CSVs (experiment.cpp:596-628) -------------------------------------------
+void write_errors_csv(const ParaRun& run, std::ostream& os) {
+  os << "iteration,coupling,energy_error,l2_error,diverged\n";
+  for (std::size_t k = 0; k < run.iterations.size(); ++k) {
+    const IterationRecord& rec = run.iterations[k];
+    for (std::size_t n = 0; n < rec.energy_err.size(); ++n)
+      os << k << "," << n << "," << fmt17(rec.energy_err[n]) << "," << fmt17(rec.l2_err[n]) << ","
+         << (rec.diverged ? 1 : 0) << "\n";
+  }
+}
+
+void write_residuals_csv(const ParaRun& run, bool plain, std::ostream& os) {
+  os << "iteration,residual,rank\n";
+  if (!plain)
+    for (std::size_t k = 1; k < run.iterations.size(); ++k)
+      os << k << "," << fmt17(run.iterations[k].residual) << "," << run.iterations[k].rank << "\n";
+}
+
+void write_summary_csv(const ParaRun& run, std::ostream& os) {
+  os << "iteration,energy_error,l2_error,diverged\n";
+  for (std::size_t k = 0; k < run.iterations.size(); ++k) {
+    const IterationRecord& rec = run.iterations[k];
+    os << k << "," << fmt17(rec.energy_err.back()) << "," << fmt17(rec.l2_err.back()) << ","
+       << (rec.diverged ? 1 : 0) << "\n";
+  }
+}
+
+void write_run_csv(const ParaRun& run, bool plain, const std::string& dir) {
+  namespace fs = std::filesystem;
+  fs::create_directories(dir);
+  std::ofstream e(fs::path(dir) / "errors.csv");
+  write_errors_csv(run, e);
+  std::ofstream r(fs::path(dir) / "residuals.csv");
+  write_residuals_csv(run, plain, r);
+  std::ofstream s(fs::path(dir) / "summary.csv");
+  write_summary_csv(run, s);
+}
+
 SpeedField read_speed_model(std::istream& is) { return to_field(parse_speed(is)); }
 
 SpeedField ingest_speed_model(const std::string& path) {
@@ -920,5 +960,34 @@ extern "C" ptb_status ptb_speed_model_read(const char* text, ptb_grid* grid, dou
     }
     *npoints = f.c.size();
     if (c && cap >= f.c.size()) std::copy(f.c.begin(), f.c.end(), c);
+  });
+}
+
+// run-record CSV text (experiment.cpp:596-628) of K iterations x (N + 1) couplings given as
+// row-major arrays; which: 0 errors.csv, 1 residuals.csv, 2 summary.csv
+extern "C" ptb_status ptb_run_csv(size_t iterations, size_t couplings, const double* energy_err, const double* l2_err,
+                                  const double* residual, const int* rank, const int* diverged, int plain, int which,
+                                  char* buf, size_t len, size_t* needed) {
+  return host_guarded([&] {
+    if (!energy_err || !l2_err || !residual || !rank || !diverged || !needed)
+      throw std::invalid_argument("run_csv: null argument");
+    if (which < 0 || which > 2) throw std::invalid_argument("run_csv: which must be 0, 1 or 2");
+    paratime::ParaRun run;
+    run.iterations.resize(iterations);
+    for (size_t k = 0; k < iterations; ++k) {
+      paratime::IterationRecord& rec = run.iterations[k];
+      rec.energy_err.assign(energy_err + k * couplings, energy_err + (k + 1) * couplings);
+      rec.l2_err.assign(l2_err + k * couplings, l2_err + (k + 1) * couplings);
+      rec.residual = residual[k];
+      rec.rank = rank[k];
+      rec.diverged = diverged[k] != 0;
+    }
+    std::ostringstream os;
+    if (which == 0) paratime::write_errors_csv(run, os);
+    else if (which == 1) paratime::write_residuals_csv(run, plain != 0, os);
+    else paratime::write_summary_csv(run, os);
+    const std::string t = os.str();
+    *needed = t.size() + 1;
+    if (buf && len >= t.size() + 1) std::memcpy(buf, t.c_str(), t.size() + 1);
   });
 }
