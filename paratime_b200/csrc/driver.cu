@@ -114,15 +114,21 @@ __global__ void k_add_sub(size_t n, const double* x, const double* y, const doub
 }
 
 // u-part of Lambda-dagger(X z, m): u += (m_new - m_old) / Nc  (zero mode of the inverse DFT)
-__device__ __forceinline__ double drv_block_sum256(double x) {
-  __shared__ double red[256];
-  red[threadIdx.x] = x;
+__device__ __forceinline__ double drv_block_sum256(double x) {  // as energy.cu's block_sum<256>
+  __shared__ double red[8];
+  __shared__ double tot;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
   __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
+  if (threadIdx.x < 32) {
+    double y = threadIdx.x < 8 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (threadIdx.x == 0) tot = y;
   }
-  const double r = red[0];
+  __syncthreads();
+  const double r = tot;
   __syncthreads();
   return r;
 }
@@ -293,7 +299,11 @@ struct Driver {
   // per-step sweep products as single fused launches (k_gemv_t1 + k_assemble_d) for small and mid
   // correctors (latency-bound: cfg1-3); cuBLAS GEMVs for large ones (HBM-bound: cfg4)
   bool fused_sweep(const DevCorrector& c) const {
-    return size_t(cg.dim + 1) * nc * size_t(std::max(c.rank, 1)) <= (size_t(4) << 20);
+    static const long long limit = [] {  // PTB_FUSED_SWEEP_MAX: corrector entries (diagnostics)
+      const char* e = std::getenv("PTB_FUSED_SWEEP_MAX");
+      return e ? std::atoll(e) : (4LL << 20);
+    }();
+    return (long long)(size_t(cg.dim + 1) * nc * size_t(std::max(c.rank, 1))) <= limit;
   }
   const double* cf_dev = nullptr;  // coarse speed
 

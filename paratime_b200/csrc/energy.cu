@@ -123,17 +123,26 @@ __global__ void k_momentum(const CompArgs a, size_t batch) {
 }
 
 // deterministic per-state sum: one CTA per state, fixed thread->element map, tree reduce
+// fixed-order block reduction: xor-butterfly inside each warp, then the T/32 warp sums by warp 0
+// (two barriers instead of log2 T); the result is returned to every thread
 template <int T>
 __device__ double block_sum(double x) {
-  __shared__ double red[T];
-  red[threadIdx.x] = x;
+  static_assert(T % 32 == 0 && T <= 1024, "block size");
+  __shared__ double red[T / 32];
+  __shared__ double tot;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
   __syncthreads();
-  for (int s = T / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
+  if (threadIdx.x < 32) {
+    double y = threadIdx.x < T / 32 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (threadIdx.x == 0) tot = y;
   }
-  const double r = red[0];
   __syncthreads();
+  const double r = tot;
+  __syncthreads();  // red / tot are reused by the next call
   return r;
 }
 
