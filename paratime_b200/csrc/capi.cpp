@@ -22,6 +22,14 @@ bool sync_check_enabled() {
   return on;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PTB_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 void* DeviceBuffer::get(size_t need) {
   if (need == 0) need = 8;
   if (need > bytes) {

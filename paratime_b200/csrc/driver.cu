@@ -174,6 +174,8 @@ __global__ void __launch_bounds__(AD_I * AD_J) k_assemble_d(size_t nc, int r, co
                                                           const double* zw, int zparts, const double* zold,
                                                           const double* mw, int mparts, const double* mold,
                                                           double* du, double* dv, const SweepTail tl) {
+  pdl_wait();  // z_w and sum(u) come from k_comp_gemv launched just before
+  pdl_trigger();
   extern __shared__ double dz[];  // r, then [2][AD_J][AD_I] partials
   const int tid = threadIdx.y * AD_I + threadIdx.x;
   for (int j = tid; j < r; j += AD_I * AD_J) {
@@ -699,9 +701,19 @@ struct Driver {
     const int r = c.rank;
     if (fused_sweep(c)) {
       const size_t smem = (size_t(r + 1) + 2 * AD_J * AD_I) * sizeof(double);
-      k_assemble_d<<<unsigned((nc + AD_I - 1) / AD_I), dim3(AD_I, AD_J), smem, st()>>>(
-          nc, r, static_cast<double*>(Zu.ptr), static_cast<double*>(Zv.ptr), zw_, zw_parts, zold_, mw, mparts, mold, du,
-          dv, tail);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned((nc + AD_I - 1) / AD_I));
+      cfg.blockDim = dim3(AD_I, AD_J);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st();
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl_enabled() ? 1 : 0;
+      PTB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_assemble_d, nc, r, static_cast<const double*>(Zu.ptr),
+                                        static_cast<const double*>(Zv.ptr), zw_, zw_parts, zold_, mw, mparts, mold, du,
+                                        dv, tail));
       PTB_LAUNCH_CHECK(ctx);
       return;
     }

@@ -183,6 +183,8 @@ __global__ void k_state_sum_final(size_t batch, int P, const double* part, doubl
 // partition and order, so mean_u is bitwise energy_components'), one launch for both.
 __global__ void __launch_bounds__(256) k_comp_gemv(const CompArgs a, int r, size_t rows, size_t chunk, const double* Y,
                                                    size_t ldy, double* z, int Psum, double* mean_part) {
+  pdl_wait();  // w comes from the coarse propagation launched just before
+  pdl_trigger();
   const int n = a.n, d = a.G.dim;
   if (int(blockIdx.x) == r) {  // sum(u) partials
     if (int(blockIdx.y) >= Psum) return;
@@ -573,8 +575,16 @@ void comp_gemv(EnergyWork& w, const ptb_grid& g, int scheme, const double* u, co
   const size_t rows = size_t(G.dim + 1) * n;
   const int Psum = state_sum_parts(n);
   CompArgs a{G, beta_of(scheme), n, u, v, size_t(n), nullptr, c, nullptr, 0};
-  k_comp_gemv<<<dim3(unsigned(r + 1), unsigned(std::max(P, Psum))), 256, 0, ctx->stream>>>(
-      a, r, rows, (rows + P - 1) / P, Y, ldy, z, Psum, mean_part);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(r + 1), unsigned(std::max(P, Psum)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PTB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_comp_gemv, a, r, rows, (rows + P - 1) / P, Y, ldy, z, Psum, mean_part));
   PTB_LAUNCH_CHECK(ctx);
 }
 

@@ -131,6 +131,8 @@ struct SmallArgs {
 
 template <int PPT, bool EXACT, bool HASY>
 __global__ void __launch_bounds__(1024) k_small(const SmallArgs a) {
+  pdl_wait();  // PDL launches (the theta sweep's coarse steps): the state comes from the previous kernel
+  pdl_trigger();
   extern __shared__ double buf[];  // [2][n]
   const int n = a.n, T = blockDim.x, tid = threadIdx.x;
   const size_t off = static_cast<size_t>(blockIdx.x) * n;
@@ -244,6 +246,8 @@ constexpr int CL_THREADS = 512;  // 4096 points per CTA
 
 template <bool EXACT>
 __global__ void __launch_bounds__(CL_THREADS, 1) k_cluster(const SmallArgs a) {
+  pdl_wait();
+  pdl_trigger();
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double cbuf[];  // [2][R + 2][nx]
   __shared__ alignas(8) unsigned long long bars[2];
@@ -900,7 +904,17 @@ void launch_small(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, int thr
   const size_t smem = 2 * size_t(a.n) * sizeof(double);
   auto kern = k_small<PPT, EXACT, HASY>;
   PTB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  kern<<<static_cast<unsigned>(batch), threads, smem, st>>>(a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(batch));
+  cfg.blockDim = dim3(unsigned(threads));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PTB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
   PTB_LAUNCH_CHECK(ctx);
 }
 
@@ -938,13 +952,15 @@ void launch_cluster(ptb_context* ctx, cudaStream_t st, const SmallArgs& a, int c
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   PTB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
   PTB_LAUNCH_CHECK(ctx);
 }

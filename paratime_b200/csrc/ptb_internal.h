@@ -102,6 +102,25 @@ struct DeviceBuffer {
 
 }  // namespace ptb
 
+namespace ptb {
+// Programmatic dependent launch (sm_90+): a kernel launched with pdl_attr() may start while its
+// predecessor on the stream is still running; it must call pdl_wait() before reading anything the
+// predecessor wrote.  pdl_trigger() lets the successor's blocks be scheduled early (they spin in
+// pdl_wait until this grid has completed and its writes are visible).  Both are no-ops for
+// kernels launched without the attribute.  Used on the latency-bound theta-sweep chain.
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
+bool pdl_enabled();  // PTB_PDL=0 disables the attribute (diagnostics)
+}  // namespace ptb
+
 struct ptb_context {
   int device = 0;
   cudaStream_t stream = nullptr;      // stream all work is issued on
