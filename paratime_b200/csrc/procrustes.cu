@@ -1547,6 +1547,8 @@ __device__ __forceinline__ int selp(bool c, int a, int b) {
 // selects the argument set.
 template <int CPW, int RPL, bool PIVOT, bool TS>
 __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, const QrRegArgs a1) {
+  pdl_wait();  // PDL launches: inputs come from the previous TSQR level
+  pdl_trigger();
   const QrRegArgs& a = (TS ? blockIdx.y : blockIdx.x) == 0 ? a0 : a1;
   constexpr int NMAX = CPW * QRR_WARPS, MMAX = 32 * RPL;
   __shared__ double cbuf[MMAX];
@@ -1752,6 +1754,8 @@ struct TsApply {
   int ldout;
 };
 __global__ void __launch_bounds__(QRR_THREADS) k_tsqr_apply4(const TsApply a0, const TsApply a1) {
+  pdl_wait();  // PDL launches: inputs come from the previous TSQR level
+  pdl_trigger();
   const TsApply& A = blockIdx.y == 0 ? a0 : a1;  // matrix blockIdx.y (F, G)
   const double* V = A.V;
   const int m = A.m, n = A.n, nb = A.nb, ldin = A.ldin, kq = A.kq, ldout = A.ldout;
@@ -1874,9 +1878,9 @@ int truncated_qr_direct(ProcWork& w, const double* A_in, int m, int n, double dr
   const int reg = !small_env ? 0 : (m <= 128 && n <= 64) ? 1 : (m <= 256 && n <= 64) ? 2 : (m <= 128 && n <= 128) ? 3 : 0;
   if (reg) {  // register-resident pivoted QR (one CTA, two barriers per column)
     QrRegArgs ra{A, m, m, n, 0, 1, drop_tol, A, nullptr, 0, nullptr, 0, tau, perm, keep_d, betas};
-    if (reg == 1) k_qr_reg<4, 4, true, false><<<1, QRR_THREADS, 0, st>>>(ra, ra);
-    else if (reg == 2) k_qr_reg<4, 8, true, false><<<1, QRR_THREADS, 0, st>>>(ra, ra);
-    else k_qr_reg<8, 4, true, false><<<1, QRR_THREADS, 0, st>>>(ra, ra);
+    if (reg == 1) launch_pdl(k_qr_reg<4, 4, true, false>, dim3(1), dim3(QRR_THREADS), 0, st, ra, ra);
+    else if (reg == 2) launch_pdl(k_qr_reg<4, 8, true, false>, dim3(1), dim3(QRR_THREADS), 0, st, ra, ra);
+    else launch_pdl(k_qr_reg<8, 4, true, false>, dim3(1), dim3(QRR_THREADS), 0, st, ra, ra);
     PTB_LAUNCH_CHECK(ctx);
   } else if (small_env && small_smem <= 200 * 1024) {
     QrArgs qa{A, m, n, m, 1, drop_tol, tau, perm, nullptr, keep_d, betas};
@@ -2113,7 +2117,7 @@ int truncated_qr_tsqr(ProcWork& w, const double* A_in, int m, int n, double drop
     double* S = static_cast<double*>(w.TS[3 * L + 2].get(size_t(nb) * n * n * sizeof(double)));
     (void)rows_max;
     QrRegArgs la{cur, ld, curm, n, nb, 0, -1.0, nullptr, V, curm, S, nb * n, tau, nullptr, nullptr, nullptr};
-    k_qr_reg<4, 8, false, true><<<unsigned(nb), QRR_THREADS, 0, st>>>(la, la);
+    launch_pdl(k_qr_reg<4, 8, false, true>, dim3(unsigned(nb)), dim3(QRR_THREADS), 0, st, la, la);
     PTB_LAUNCH_CHECK(ctx);
     lv.push_back(Level{curm, nb, V, tau});
     cur = S;
@@ -2130,7 +2134,7 @@ int truncated_qr_tsqr(ProcWork& w, const double* A_in, int m, int n, double drop
     double* out = l == 0 ? Q : static_cast<double*>(w.TX[l & 1].get(size_t(L.m) * kq * sizeof(double)));
     const int rows_max = (L.m + L.nb - 1) / L.nb;
     const TsApply ap{L.V, L.m, n, L.nb, L.tau, X, ldx, kq, out, L.m};
-    k_tsqr_apply4<<<unsigned(L.nb), QRR_THREADS, (size_t(rows_max) * n + n) * sizeof(double), st>>>(ap, ap);
+    launch_pdl(k_tsqr_apply4, dim3(unsigned(L.nb)), dim3(QRR_THREADS), (size_t(rows_max) * n + n) * sizeof(double), st, ap, ap);
     PTB_LAUNCH_CHECK(ctx);
     X = out;
     ldx = L.m;
@@ -2185,7 +2189,7 @@ bool truncated_qr_pair(ProcWork& w, const double* F, const double* G, int m, int
       la[b] = QrRegArgs{cur[b], ld, curm, n, nb, 0, -1.0, nullptr, lev.V[b], curm, S[b], nb * n, lev.tau[b],
                         nullptr, nullptr, nullptr};
     }
-    k_qr_reg<4, 8, false, true><<<dim3(unsigned(nb), 2), QRR_THREADS, 0, st>>>(la[0], la[1]);
+    launch_pdl(k_qr_reg<4, 8, false, true>, dim3(unsigned(nb), 2), dim3(QRR_THREADS), 0, st, la[0], la[1]);
     PTB_LAUNCH_CHECK(ctx);
     lv.push_back(lev);
     cur[0] = S[0];
@@ -2210,8 +2214,8 @@ bool truncated_qr_pair(ProcWork& w, const double* F, const double* G, int m, int
     ra[b] = QrRegArgs{A[b], curm, curm, n, 0, 1, tol[b], A[b], nullptr, 0, nullptr, 0, tau[b], perm[b], keep_d + b,
                       betas};
   }
-  if (curm <= 128) k_qr_reg<4, 4, true, false><<<2, QRR_THREADS, 0, st>>>(ra[0], ra[1]);
-  else k_qr_reg<4, 8, true, false><<<2, QRR_THREADS, 0, st>>>(ra[0], ra[1]);
+  if (curm <= 128) launch_pdl(k_qr_reg<4, 4, true, false>, dim3(2), dim3(QRR_THREADS), 0, st, ra[0], ra[1]);
+  else launch_pdl(k_qr_reg<4, 8, true, false>, dim3(2), dim3(QRR_THREADS), 0, st, ra[0], ra[1]);
   PTB_LAUNCH_CHECK(ctx);
   int keep[2] = {0, 0};
   PTB_CUDA_CHECK(cudaMemcpyAsync(keep, keep_d, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -2247,8 +2251,8 @@ bool truncated_qr_pair(ProcWork& w, const double* F, const double* G, int m, int
     }
     const int rows_max = (L.m + L.nb - 1) / L.nb;
     if (keep[0] > 0 || keep[1] > 0) {
-      k_tsqr_apply4<<<dim3(unsigned(L.nb), 2), QRR_THREADS, (size_t(rows_max) * n + n) * sizeof(double), st>>>(
-          ap[0], ap[1]);
+      launch_pdl(k_tsqr_apply4, dim3(unsigned(L.nb), 2), dim3(QRR_THREADS), (size_t(rows_max) * n + n) * sizeof(double),
+                 st, ap[0], ap[1]);
       PTB_LAUNCH_CHECK(ctx);
     }
     X[0] = out[0];

@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "paratime_b200.h"
@@ -119,6 +120,23 @@ __device__ __forceinline__ void pdl_trigger() {
 #endif
 }
 bool pdl_enabled();  // PTB_PDL=0 disables the attribute (diagnostics)
+
+// launch `kern` with the programmatic-stream-serialization attribute (the kernel must pdl_wait())
+template <typename... Exp, typename... Act>
+void launch_pdl(void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+  if (e != cudaSuccess) fail(PTB_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+}
 }  // namespace ptb
 
 struct ptb_context {
