@@ -1942,9 +1942,13 @@ void jacobi_core(ProcWork& w, double* A, int r, int c, double* V, double* sg, do
   }();
   const int pairs = ((c % 2 == 0) ? c : c + 1) / 2;
   const size_t csmem = jacobi_cluster_smem(r, c);
-  // measured (scripts/ubench_procrustes.py): the cluster kernel wins from ~100 columns (108: 2.1 vs 2.6 ms),
+  // measured (scripts/ubench_procrustes.py): the cluster kernel wins from ~64 columns (108: 2.2 vs 3.1 ms),
   // the one-CTA kernel below (60: 0.65 vs 0.72 ms)
-  const bool cluster_ok = jacobi_env == 0 && c >= 96 && pairs * 8 <= 1024 && csmem <= 200 * 1024;
+  static const int cluster_min = [] {  // PTB_JACOBI_CLUSTER_MIN: smallest c for the cluster kernel
+    const char* e = std::getenv("PTB_JACOBI_CLUSTER_MIN");
+    return e ? std::atoi(e) : 64;  // measured crossover: 60^2 equal, 80^2 1.30 vs 1.50 ms, 95^2 1.80 vs 2.35 ms
+  }();
+  const bool cluster_ok = jacobi_env == 0 && c >= cluster_min && pairs * 8 <= 1024 && csmem <= 200 * 1024;
   if (cluster_ok || (smem <= 200 * 1024 && jacobi_env != 2)) {
     if (cluster_ok) {
       static const int gs_env = [] {  // PTB_JACOBI_GS: lanes per pair in the cluster kernel (1, 2, 4, 8)

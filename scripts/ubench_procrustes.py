@@ -17,7 +17,7 @@ import torch
 import paratime_b200 as B
 
 QR_SHAPES = [(3072, 16), (12288, 32), (49152, 64), (196608, 128)]
-SVD_SHAPES = [(32, 32), (60, 60), (108, 108), (160, 160)]
+SVD_SHAPES = [(32, 32), (60, 60), (80, 80), (95, 95), (108, 108), (160, 160)]
 
 
 def timed(fn, reps=20, warm=3):

@@ -43,7 +43,7 @@ def test_small_and_cluster_jacobi_are_accurate(tmp_path, shape, path):
     """k_jacobi_cluster (default from 24 columns: rows split over a thread-block cluster) and
     k_jacobi_small (one CTA's shared memory) on the corrector's H sizes at cfg1-3."""
     p, q = shape
-    a = _run(p, q, tmp_path / "small.npz", None if path == "auto" else path)  # auto: cluster from 96 columns
+    a = _run(p, q, tmp_path / "small.npz", None if path == "auto" else path)  # auto: cluster from 64 columns
     m, U, S, V = a["m"], a["U"], a["S"], a["V"]
     ref = np.linalg.svd(m, compute_uv=False)
     assert np.max(np.abs(S - ref) / ref[0]) <= 1e-13
