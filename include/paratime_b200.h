@@ -110,6 +110,24 @@ ptb_status ptb_propagate_coupling_host(ptb_propagator* p, const double* u_in, co
  * (nullable, int32[batch]) gets the per-slice divergence flags. */
 ptb_status ptb_propagate_batch_host(ptb_propagator* p, size_t batch, const double* u_in, const double* udot_in,
                                     double* u_out, double* udot_out, int32_t* nonfinite_host, int mode);
+/* ---- absorbing layer (PML) fine propagator: BASELINE.json config 4 (not in the reference) --
+ * The reference propagator is periodic only (propagator.cpp:31-105); SURVEY.md 8(f) rank 4.
+ * State per slice: u, udot and the auxiliary fields px, py (same SoA layout); px, py must be
+ * zero wherever zeta_x = zeta_y = 0.  Scheme: oracle/pml_np.py.  A zero profile reproduces the
+ * periodic FAST propagator bitwise. */
+typedef struct ptb_pml ptb_pml;
+/* quadratic damping profile of `width` cells at both ends of an axis of n cells (host) */
+ptb_status ptb_pml_damping_profile(size_t n, size_t width, double h, double cmax, double reflection,
+                                   double* out_host);
+/* validates like ptb_propagator_create (2D only); zeta_y_host: n[0] values, zeta_x_host: n[1] */
+ptb_status ptb_pml_create(ptb_context* ctx, const ptb_grid* grid, const double* c_host,
+                          const double* zeta_y_host, const double* zeta_x_host, double dt,
+                          size_t steps_per_coupling, ptb_pml** out);
+ptb_status ptb_pml_destroy(ptb_pml* p);
+/* `steps` (0 = steps_per_coupling) steps on `batch` states in place (device pointers);
+ * nonfinite_dev (nullable, int32[batch]) |= 1 where the result is not finite */
+ptb_status ptb_pml_propagate_batch(ptb_pml* p, size_t steps, size_t batch, double* u_dev, double* udot_dev,
+                                   double* px_dev, double* py_dev, int32_t* nonfinite_dev);
 /* laplacian (propagator.cpp:31-58, reference operation order) */
 ptb_status ptb_laplacian_batch(ptb_context* ctx, const ptb_grid* grid, size_t batch,
                                const double* f_dev, double* out_dev);

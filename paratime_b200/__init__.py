@@ -22,7 +22,9 @@ from .api import (  # noqa: F401
     Context,
     Grid,
     PtbError,
+    PmlPropagator,
     Propagator,
+    damping_profile,
     Transfer,
     lib,
     lib_path,

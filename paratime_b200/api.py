@@ -193,6 +193,47 @@ class Propagator:
         return uo, vo
 
 
+class PmlPropagator:
+    """Absorbing-layer fine propagator (config 4; not in the reference, scheme in oracle/pml_np.py).
+
+    State: u, udot, px, py device tensors of shape (batch, ny, nx) or (ny, nx); px, py zero
+    outside the layer.  zeta_y / zeta_x: damping per row / column (damping_profile)."""
+
+    def __init__(self, ctx: Context, grid: Grid, c, zeta_y, zeta_x, dt: float, steps: int):
+        self.ctx, self.grid, self.dt, self.steps = ctx, grid, float(dt), int(steps)
+        dp = C.POINTER(C.c_double)
+        c = np.ascontiguousarray(c, dtype=np.float64).reshape(-1)
+        zy = np.ascontiguousarray(zeta_y, dtype=np.float64).reshape(-1)
+        zx = np.ascontiguousarray(zeta_x, dtype=np.float64).reshape(-1)
+        if c.size != grid.size or grid.dim != 2 or zy.size != grid.n[0] or zx.size != grid.n[1]:
+            raise PtbError(INVALID_ARGUMENT, "PmlConfig: field sizes do not match the 2D grid")
+        h = C.c_void_p()
+        check(lib().ptb_pml_create(ctx.h, C.byref(grid.c()), c.ctypes.data_as(dp), zy.ctypes.data_as(dp),
+                                   zx.ctypes.data_as(dp), C.c_double(dt), C.c_size_t(steps), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ptb_pml_destroy(self.h)
+        except Exception:
+            pass
+
+    def propagate(self, u, udot, px, py, steps: Optional[int] = None, flags=None):
+        batch = u.numel() // self.grid.size
+        check(lib().ptb_pml_propagate_batch(self.h, C.c_size_t(steps or 0), C.c_size_t(batch), _ptr(u), _ptr(udot),
+                                            _ptr(px), _ptr(py), _ptr(flags)))
+        return u, udot, px, py
+
+
+def damping_profile(n: int, width: int, h: float, cmax: float, reflection: float = 1e-4) -> np.ndarray:
+    """ptb_pml_damping_profile (host): quadratic profile on `width` cells at both ends."""
+    out = np.empty(n)
+    check(lib().ptb_pml_damping_profile(C.c_size_t(n), C.c_size_t(width), C.c_double(h), C.c_double(cmax),
+                                        C.c_double(reflection), out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
 class Transfer:
     """GridTransfer (grid.hpp:56-67): restriction and interpolation on the device."""
 

@@ -1,0 +1,147 @@
+"""Absorbing-layer (PML) fine propagator on the B200 against oracle/pml_np.py.
+
+The reference has no PML: the oracle is this build's own specification,
+pinned by tests/test_pml_oracle.py.  Tolerance 1e-12 relative L2 per field (fp64, FMA-contracted
+kernel vs the numpy restatement); a zero profile must reproduce the periodic FAST kernels bitwise."""
+import numpy as np
+import pytest
+
+from oracle import pml_np as M
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paratime_b200 as B
+
+    return B.Context(0)
+
+
+def _case(ny, nx, hy, hx, w, batch, seed, layer_noise=True):
+    rng = np.random.default_rng(seed)
+    c = 0.5 + 0.5 * rng.random((ny, nx))
+    zy = M.damping_profile(ny, w, hy, 1.0, 1e-4)
+    zx = M.damping_profile(nx, w, hx, 1.0, 1e-4)
+    u = rng.standard_normal((batch, ny, nx))
+    v = rng.standard_normal((batch, ny, nx))
+    mask = (zy[:, None] > 0) | (zx[None, :] > 0)
+    px = rng.standard_normal((batch, ny, nx)) * mask if layer_noise else np.zeros((batch, ny, nx))
+    py = rng.standard_normal((batch, ny, nx)) * mask if layer_noise else np.zeros((batch, ny, nx))
+    return c, zy, zx, (u, v, px, py)
+
+
+def _rel(a, b):
+    d = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (d if d > 0 else 1.0))
+
+
+@pytest.mark.parametrize(
+    "ny,nx,w,steps,batch",
+    [
+        (64, 64, 8, 4, 2),      # one pass
+        (64, 64, 8, 9, 2),      # passes 4+4+1 (odd: result copied back from scratch)
+        (96, 80, 6, 7, 3),      # partial tiles, non-square grid
+        (128, 128, 16, 16, 2),  # cfg1-size grid, 4 passes
+        (40, 24, 5, 5, 1),      # grid smaller than the haloed tile (multiple periodic wraps)
+        (256, 192, 32, 12, 1),  # cfg4's 32-cell layer
+    ],
+)
+def test_pml_matches_oracle(ctx, ny, nx, w, steps, batch):
+    import paratime_b200 as B
+
+    hy, hx = 1 / ny, 1 / nx
+    dt = min(hy, hx) / 8
+    c, zy, zx, st = _case(ny, nx, hy, hx, w, batch, seed=ny * 7 + nx)
+    k = M.PmlCoefficients(c, hy, hx, dt, zy, zx)
+    want = M.pml_steps(*st, k, steps)
+    prop = B.PmlPropagator(ctx, B.Grid((ny, nx), (hy, hx)), c, zy, zx, dt, steps)
+    t = [ctx.tensor(a) for a in st]
+    flags = ctx.torch.zeros(batch, dtype=ctx.torch.int32, device="cuda:0")
+    prop.propagate(*t, flags=flags)
+    got = [x.cpu().numpy() for x in t]
+    for name, g, r in zip(("u", "udot", "px", "py"), got, want):
+        assert _rel(g, r) <= TOL, (name, _rel(g, r))
+    assert not flags.cpu().numpy().any()
+
+
+@pytest.mark.parametrize("n,steps", [(128, 64), (256, 8), (100, 13)])
+def test_zero_profile_is_periodic_fast_bitwise(ctx, n, steps):
+    import paratime_b200 as B
+
+    h = 1 / n
+    rng = np.random.default_rng(n)
+    c = 0.5 + 0.5 * rng.random((n, n))
+    u = rng.standard_normal((2, n, n))
+    v = rng.standard_normal((2, n, n))
+    g = B.Grid((n, n), (h, h))
+    pml = B.PmlPropagator(ctx, g, c, np.zeros(n), np.zeros(n), h / 8, steps)
+    per = B.Propagator(ctx, g, c, h / 8, steps)
+    a = [ctx.tensor(u), ctx.tensor(v), ctx.tensor(np.zeros_like(u)), ctx.tensor(np.zeros_like(u))]
+    b = [ctx.tensor(u), ctx.tensor(v)]
+    pml.propagate(*a)
+    per.propagate(*b, mode=B.FAST)
+    assert np.array_equal(a[0].cpu().numpy(), b[0].cpu().numpy())
+    assert np.array_equal(a[1].cpu().numpy(), b[1].cpu().numpy())
+
+
+def test_fused_equals_repeated_single_steps(ctx):
+    import paratime_b200 as B
+
+    n, w, steps = 96, 12, 10
+    h = 1 / n
+    c, zy, zx, st = _case(n, n, h, h, w, 2, seed=5)
+    prop = B.PmlPropagator(ctx, B.Grid((n, n), (h, h)), c, zy, zx, h / 8, steps)
+    a = [ctx.tensor(x) for x in st]
+    b = [ctx.tensor(x) for x in st]
+    prop.propagate(*a)
+    for _ in range(steps):
+        prop.propagate(*b, steps=1)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
+
+
+def test_nonfinite_flag(ctx):
+    import paratime_b200 as B
+
+    n = 64
+    h = 1 / n
+    c, zy, zx, st = _case(n, n, h, h, 8, 3, seed=9)
+    st[0][1, 3, 3] = np.nan
+    prop = B.PmlPropagator(ctx, B.Grid((n, n), (h, h)), c, zy, zx, h / 8, 4)
+    t = [ctx.tensor(a) for a in st]
+    flags = ctx.torch.zeros(3, dtype=ctx.torch.int32, device="cuda:0")
+    prop.propagate(*t, flags=flags)
+    assert flags.cpu().numpy().tolist() == [0, 1, 0]
+
+
+def test_cfl_and_shape_errors(ctx):
+    import paratime_b200 as B
+
+    n = 32
+    g = B.Grid((n, n), (1 / n, 1 / n))
+    with pytest.raises(B.PtbError):
+        B.PmlPropagator(ctx, g, np.ones((n, n)), np.zeros(n), np.zeros(n), 1.0 / n, 4)  # CFL
+    with pytest.raises(B.PtbError):
+        B.PmlPropagator(ctx, g, np.ones((n, n)), -np.ones(n), np.zeros(n), 0.1 / n, 4)  # negative damping
+
+
+def test_pulse_absorbed_on_device(ctx):
+    """cfg4-like: 512^2 with a 32-cell layer, constant speed; the interior energy drops once the
+    pulse has crossed the layer and the run stays finite."""
+    import paratime_b200 as B
+
+    n, w = 512, 32
+    h = 1 / n
+    y, x = np.meshgrid(np.arange(n) / n, np.arange(n) / n, indexing="ij")
+    u0 = np.exp(-2500 * ((x - 0.5) ** 2 + (y - 0.5) ** 2))
+    c = np.ones((n, n))
+    zs = M.damping_profile(n, w, h, 1.0, 1e-4)
+    prop = B.PmlPropagator(ctx, B.Grid((n, n), (h, h)), c, zs, zs, h / 8, 4096)
+    z = np.zeros((n, n))
+    t = [ctx.tensor(u0), ctx.tensor(z), ctx.tensor(z), ctx.tensor(z)]
+    e0 = M.interior_energy(u0, z, c, h, h, w)
+    prop.propagate(*t)  # t = 1: the front has crossed the layer
+    e1 = M.interior_energy(t[0].cpu().numpy(), t[1].cpu().numpy(), c, h, h, w)
+    assert np.isfinite(e1) and e1 < 1e-2 * e0, e1 / e0
