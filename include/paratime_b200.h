@@ -128,6 +128,16 @@ ptb_status ptb_pml_destroy(ptb_pml* p);
  * nonfinite_dev (nullable, int32[batch]) |= 1 where the result is not finite */
 ptb_status ptb_pml_propagate_batch(ptb_pml* p, size_t steps, size_t batch, double* u_dev, double* udot_dev,
                                    double* px_dev, double* py_dev, int32_t* nonfinite_dev);
+/* Plain parareal (Eq. 2, parareal.cpp:201-237) with the absorbing layer: states carry
+ * (u, udot, px, py); fine and coarse are PML propagators on t's fine / coarse grids (the same
+ * coupling interval); iterate 0 is the interpolated serial coarse chain, the sweep runs on the
+ * coarse grid (R(I(d)) = d).  Host outputs (all nullable): rel_err_host[K x (N+1)] relative L2 of
+ * [u; udot] vs the serial fine run, iteration_ms_host[K] device time of each iteration body
+ * (metrics excluded), states_host[4 x (N+1) x N_f] the last iterate, diverged_host = any
+ * non-finite fine stage.  The theta (Procrustes) variant is periodic only. */
+ptb_status ptb_pml_parareal_run(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t n_couplings, int iterations,
+                                const double* u0_host, const double* udot0_host, double* rel_err_host,
+                                double* iteration_ms_host, double* states_host, int32_t* diverged_host);
 /* laplacian (propagator.cpp:31-58, reference operation order) */
 ptb_status ptb_laplacian_batch(ptb_context* ctx, const ptb_grid* grid, size_t batch,
                                const double* f_dev, double* out_dev);

@@ -119,3 +119,48 @@ def interior_energy(u, v, c, hy, hx, width: int):
     e = 0.5 * (gx * gx + gy * gy + (v / c) ** 2) * hx * hy
     w = width
     return float(np.sum(e[..., w:e.shape[-2] - w, w:e.shape[-1] - w]))
+
+
+def plain_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m_c: int, t, N: int, K: int):
+    """Plain parareal (Eq. 2; parareal.cpp:201-237) on the layered state (u, udot, px, py), the
+    way csrc/pml.cu pml_parareal evaluates it: iterate 0 = the interpolated serial coarse chain;
+    per iteration fine_next[n] = F(cur[n-1]), old[n] = C(R cur[n-1]); coarse sweep
+    w_0 = R(init), d_n = C(w_{n-1}) - old[n], w_n = R(fine_next[n]) + d_n; next[n] = fine_next[n] + I(d_n).
+    `t` is an oracle/paratime_np.Transfer.  Returns (iterates per k as lists of 4-tuples,
+    rel. L2 errors of [u; udot] vs the serial fine run [K x (N+1)])."""
+    from oracle import paratime_np as P
+
+    R = lambda s: tuple(P.restrict_field(f, t) for f in s)  # noqa: E731
+    I = lambda s: tuple(P.interpolate_field(f, t) for f in s)  # noqa: E731
+    Fp = lambda s: pml_steps(*s, kf, m_f)  # noqa: E731
+    Cp = lambda s: pml_steps(*s, kc, m_c)  # noqa: E731
+    z = np.zeros_like(u0)
+    init = (u0, v0, z, z)
+    ref = [init]
+    for _ in range(N):
+        ref.append(Fp(ref[-1]))
+    cur = [init]
+    w = R(init)
+    for _ in range(N):
+        w = Cp(w)
+        cur.append(I(w))
+    out, errs = [], []
+    for _ in range(K):
+        fine_next = [None] + [Fp(cur[n - 1]) for n in range(1, N + 1)]
+        old = [None] + [Cp(R(cur[n - 1])) for n in range(1, N + 1)]
+        nxt = [init]
+        w = R(init)
+        for n in range(1, N + 1):
+            g = Cp(w)
+            d = tuple(a - b for a, b in zip(g, old[n]))
+            w = tuple(a + b for a, b in zip(R(fine_next[n]), d))
+            nxt.append(tuple(a + b for a, b in zip(fine_next[n], I(d))))
+        e = []
+        for n in range(N + 1):
+            num = np.sum((nxt[n][0] - ref[n][0]) ** 2 + (nxt[n][1] - ref[n][1]) ** 2)
+            den = np.sum(ref[n][0] ** 2 + ref[n][1] ** 2)
+            e.append(float(np.sqrt(num / den)) if den > 0 else float(np.sqrt(num)))
+        errs.append(e)
+        out.append(nxt)
+        cur = nxt
+    return out, np.array(errs)

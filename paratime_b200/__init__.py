@@ -25,6 +25,7 @@ from .api import (  # noqa: F401
     PmlPropagator,
     Propagator,
     damping_profile,
+    pml_parareal_run,
     Transfer,
     lib,
     lib_path,

@@ -226,6 +226,25 @@ class PmlPropagator:
         return u, udot, px, py
 
 
+def pml_parareal_run(fine: "PmlPropagator", coarse: "PmlPropagator", transfer: "Transfer", n_couplings: int,
+                     iterations: int, u0, udot0, keep_states: bool = False):
+    """ptb_pml_parareal_run: plain parareal with the absorbing layer.  Returns a dict with the
+    relative L2 errors [K x (N+1)], per-iteration device ms, the diverged flag and (optionally)
+    the last iterate as an array [4, N+1, *grid] (u, udot, px, py)."""
+    N, K = int(n_couplings), int(iterations)
+    dp = C.POINTER(C.c_double)
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    v0 = np.ascontiguousarray(udot0, dtype=np.float64)
+    err = np.zeros((max(K, 1), N + 1))
+    ms = np.zeros(max(K, 1))
+    states = np.empty((4, N + 1) + tuple(fine.grid.n)) if keep_states else None
+    div = C.c_int32(0)
+    check(lib().ptb_pml_parareal_run(fine.h, coarse.h, transfer.h, C.c_size_t(N), C.c_int(K), u0.ctypes.data_as(dp),
+                                     v0.ctypes.data_as(dp), err.ctypes.data_as(dp), ms.ctypes.data_as(dp),
+                                     states.ctypes.data_as(dp) if keep_states else None, C.byref(div)))
+    return {"rel_err": err[:K], "iteration_ms": ms[:K], "diverged": bool(div.value), "states": states}
+
+
 def damping_profile(n: int, width: int, h: float, cmax: float, reflection: float = 1e-4) -> np.ndarray:
     """ptb_pml_damping_profile (host): quadratic profile on `width` cells at both ends."""
     out = np.empty(n)

@@ -19,8 +19,9 @@
 // reads new auxiliary neighbours) and by 1 elsewhere; after S steps the central tile is exact.  The carried velocity is the half
 // kick vh (as the FAST kernel), so the drift is pointwise.  Tiles with no layer cell in their
 // halo run the plain FAST step (bitwise the periodic kernels' arithmetic, bfast<true> below);
-// the two tile classes are two launches (LAYER = false / true) so the plain tiles need only the
-// u plane in shared memory (more CTAs per SM).  Out of place (halo reads of other tiles' inputs):
+// the two tile classes (fixed per propagator, listed at create) are two launches (LAYER = false /
+// true): plain tiles need a smaller halo and only the u and coefficient planes in shared memory
+// (two CTAs per SM, so one loads while the other computes).  Out of place (halo reads of other tiles' inputs):
 // passes ping-pong between the caller's buffers and the propagator's scratch.
 #include <algorithm>
 #include <cmath>
@@ -34,7 +35,7 @@ namespace {
 constexpr int PS = 4;           // steps per pass
 constexpr int HL = 2 * PS + 1;  // layer-tile halo: the first half kick costs 1 cell, each step 2
 constexpr int HP = PS + 1;      // plain-tile halo: 1 cell per step + 1
-constexpr int BT = 96;          // plain tiles are BT x BT; layer tiles BT/2 (4 per big tile)
+constexpr int PT = 64;          // output tile (both classes)
 
 struct PmlArgs {
   int ny, nx;
@@ -47,6 +48,7 @@ struct PmlArgs {
   double *uo, *vo, *pxo, *pyo;
   int steps;                                 // steps of this pass (<= PS)
   int32_t* flags;
+  const int2* tiles;                         // (ty0, tx0) of the tiles of this launch's class
 };
 
 template <int T, int H, int NT>
@@ -81,21 +83,9 @@ __device__ __forceinline__ int wrap(int i, int n) {
   return i < 0 ? i + n : i;
 }
 
-// Does big tile (by, bx) have a layer cell within HL cells?  Both launches classify with this
-// one rule, so every tile is processed by exactly one of them.  Called by all threads.
-template <int NT>
-__device__ bool big_tile_has_layer(const PmlArgs& a, int by, int bx) {
-  bool any = false;
-  for (int j = threadIdx.x; j < BT + 2 * HL; j += NT) {
-    any |= a.zx[wrap(bx * BT - HL + j, a.nx)] > 0.0;
-    any |= a.zy[wrap(by * BT - HL + j, a.ny)] > 0.0;
-  }
-  return __syncthreads_or(any) != 0;
-}
-
 template <bool LAYER, int NT>
-__global__ void __launch_bounds__(NT, 1) k_pml(const PmlArgs a) {
-  constexpr int T = LAYER ? BT / 2 : BT, H = LAYER ? HL : HP;
+__global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
+  constexpr int T = PT, H = LAYER ? HL : HP;
   using G = Geo<T, H, NT>;
   constexpr int E = G::E, NPT = G::NPT;
   extern __shared__ double sm[];
@@ -112,11 +102,9 @@ __global__ void __launch_bounds__(NT, 1) k_pml(const PmlArgs a) {
   int* colg = reinterpret_cast<int*>(zxs + (LAYER ? 6 * E : 0));  // E: global column
   int* rowg = colg + E;                                             // E: global row offset
 
-  const int tid = threadIdx.x, b = blockIdx.z;
-  const int ty0 = blockIdx.y * T, tx0 = blockIdx.x * T;
-  if (ty0 >= a.ny || tx0 >= a.nx) return;
-  const int by = LAYER ? blockIdx.y / 2 : blockIdx.y, bx = LAYER ? blockIdx.x / 2 : blockIdx.x;
-  if (big_tile_has_layer<NT>(a, by, bx) != LAYER) return;  // the other launch owns this tile
+  const int tid = threadIdx.x, b = blockIdx.y;
+  const int2 t0 = a.tiles[blockIdx.x];
+  const int ty0 = t0.x, tx0 = t0.y;
 
   for (int j = tid; j < E; j += NT) {
     const int gx = wrap(tx0 - H + j, a.nx), gy = wrap(ty0 - H + j, a.ny);
@@ -255,11 +243,11 @@ __global__ void __launch_bounds__(NT, 1) k_pml(const PmlArgs a) {
   }
 }
 
-constexpr int kPlainThreads = 512, kLayerThreads = 512;
+constexpr int kPlainThreads = 256, kLayerThreads = 512;
 
 template <bool LAYER>
 size_t pml_smem() {
-  using G = Geo<LAYER ? BT / 2 : BT, LAYER ? HL : HP, LAYER ? kLayerThreads : kPlainThreads>;
+  using G = Geo<PT, LAYER ? HL : HP, LAYER ? kLayerThreads : kPlainThreads>;
   return size_t(G::PLANE) * (LAYER ? 3 : 2) * sizeof(double) + (LAYER ? 6 * G::E * sizeof(double) : 0) +
          2 * G::E * sizeof(int);
 }
@@ -286,6 +274,8 @@ struct ptb_pml {
   double* coef = nullptr;  // kx (n) | zx ax qx (nx) | zy ay qy (ny)
   ptb::DeviceBuffer scratch;  // 4 fields x batch (ping-pong partner; phi planes zeroed once)
   size_t scratch_batch = 0;
+  int2* tiles = nullptr;       // plain tiles, then layer tiles (PT x PT, classified at create)
+  int nplain = 0, nlayer = 0;
 };
 
 namespace ptb {
@@ -330,9 +320,7 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
                                         int(pml_smem<true>())));
     attr = true;
   }
-  // plain launch: big tiles; layer launch: the four half-size tiles of every big tile
-  const dim3 gplain((nx + BT - 1) / BT, (ny + BT - 1) / BT, unsigned(batch));
-  const dim3 glayer(2 * gplain.x, 2 * gplain.y, unsigned(batch));
+  require(batch <= 65535, "pml propagate: at most 65535 slices per call");
   int cur = 0;
   for (size_t done = 0; done < steps;) {
     const int ns = int(std::min<size_t>(PS, steps - done));
@@ -347,15 +335,194 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     a.pyo = bufs[1 - cur][3];
     a.steps = ns;
     a.flags = done == steps ? flags : nullptr;
-    k_pml<false, kPlainThreads><<<gplain, kPlainThreads, pml_smem<false>(), st>>>(a);
-    PTB_LAUNCH_CHECK(ctx);
-    k_pml<true, kLayerThreads><<<glayer, kLayerThreads, pml_smem<true>(), st>>>(a);
-    PTB_LAUNCH_CHECK(ctx);
+    if (p->nplain) {
+      a.tiles = p->tiles;
+      k_pml<false, kPlainThreads><<<dim3(p->nplain, unsigned(batch)), kPlainThreads, pml_smem<false>(), st>>>(a);
+      PTB_LAUNCH_CHECK(ctx);
+    }
+    if (p->nlayer) {
+      a.tiles = p->tiles + p->nplain;
+      k_pml<true, kLayerThreads><<<dim3(p->nlayer, unsigned(batch)), kLayerThreads, pml_smem<true>(), st>>>(a);
+      PTB_LAUNCH_CHECK(ctx);
+    }
     cur = 1 - cur;
   }
   if (cur == 1)  // odd number of passes: the result is in the scratch
     for (int f = 0; f < 4; ++f)
       PTB_CUDA_CHECK(cudaMemcpyAsync(bufs[0][f], bufs[1][f], fb, cudaMemcpyDeviceToDevice, st));
+}
+
+
+// ---------------------------------------------------------------- plain parareal with the layer
+namespace {
+
+__global__ void k_sweep_diff(size_t n, const double* g, const double* old, const double* rf, double* d, double* w) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const double di = g[i] - old[i];
+    d[i] = di;
+    w[i] = rf[i] + di;
+  }
+}
+__global__ void k_add_into(size_t n, double* x, const double* y) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    x[i] = x[i] + y[i];
+}
+// per slice (one block each, fixed-order reduction): out[2b] = sum (a-b)^2, out[2b+1] = sum b^2 over [u; udot]
+__global__ void __launch_bounds__(512) k_err_sums(size_t n, const double* au, const double* av, const double* bu,
+                                                  const double* bv, double* out) {
+  const size_t o = size_t(blockIdx.x) * n;
+  double e = 0.0, r = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += 512) {
+    const double du = au[o + i] - bu[o + i], dv = av[o + i] - bv[o + i];
+    e += du * du + dv * dv;
+    r += bu[o + i] * bu[o + i] + bv[o + i] * bv[o + i];
+  }
+  __shared__ double se[512], sr[512];
+  se[threadIdx.x] = e;
+  sr[threadIdx.x] = r;
+  __syncthreads();
+  for (int k = 256; k > 0; k >>= 1) {
+    if (int(threadIdx.x) < k) {
+      se[threadIdx.x] += se[threadIdx.x + k];
+      sr[threadIdx.x] += sr[threadIdx.x + k];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[2 * blockIdx.x] = se[0];
+    out[2 * blockIdx.x + 1] = sr[0];
+  }
+}
+
+unsigned ew_blocks(ptb_context* ctx, size_t n) {
+  return unsigned(std::max<size_t>(1, std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 8)));
+}
+
+// a set of (N+1) states of 4 fields each: field f of state s at base + (f*(N+1) + s)*n
+struct States {
+  double* base = nullptr;
+  size_t n = 0, count = 0;
+  double* f(int field, size_t s = 0) const { return base + (size_t(field) * count + s) * n; }
+};
+
+}  // namespace
+
+void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t N, int K, const double* u0, const double* v0,
+                  double* err_out, double* ms_out, double* states_out, int32_t* diverged_out) {
+  ptb_context* ctx = fine->ctx;
+  cudaStream_t st = ctx->stream;
+  const size_t nf = fine->n, nc = coarse->n;
+  auto same = [](const ptb_grid& a, const ptb_grid& b) {
+    return a.dim == b.dim && a.n[0] == b.n[0] && a.n[1] == b.n[1] && a.h[0] == b.h[0] && a.h[1] == b.h[1];
+  };
+  require(same(fine->grid, t->fine) && same(coarse->grid, t->coarse), "pml parareal: grids do not match the transfer");
+  const double tf = fine->dt * double(fine->steps), tc = coarse->dt * double(coarse->steps);
+  require(std::fabs(tf - tc) <= 1e-12 * std::max(tf, tc), "CouplingSchedule: fine and coarse couplings differ");
+  require(N >= 1 && K >= 0, "pml parareal: need N >= 1 couplings and K >= 0 iterations");
+  // device state: cur, next, reference ((N+1) fine states x 4 fields) + coarse work
+  DeviceBuffer bcur, bnext, bref, bc, bflag, bsum, bchunk;
+  States cur{static_cast<double*>(bcur.get(4 * (N + 1) * nf * sizeof(double))), nf, N + 1};
+  States nxt{static_cast<double*>(bnext.get(4 * (N + 1) * nf * sizeof(double))), nf, N + 1};
+  States ref{static_cast<double*>(bref.get(4 * (N + 1) * nf * sizeof(double))), nf, N + 1};
+  // coarse: old (N), rf = R(fine_next) (N), d (N), w (1), g (1)
+  double* cw = static_cast<double*>(bc.get(4 * (3 * N + 2) * nc * sizeof(double)));
+  States cold{cw, nc, N}, crf{cw + 4 * N * nc, nc, N}, cd{cw + 8 * N * nc, nc, N};
+  States cwv{cw + 12 * N * nc, nc, 1}, cg{cw + 12 * N * nc + 4 * nc, nc, 1};
+  int32_t* flags = static_cast<int32_t*>(bflag.get((N + 1) * sizeof(int32_t)));
+  double* sums = static_cast<double*>(bsum.get(2 * (N + 1) * sizeof(double)));
+  const size_t chunk = std::min<size_t>(N, 8);
+  double* fchunk = static_cast<double*>(bchunk.get(chunk * nf * sizeof(double)));
+  auto cpy = [&](double* dst, const double* src, size_t count) {
+    PTB_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  };
+  // initial state: u0, v0, px = py = 0
+  for (States* S : {&cur, &ref}) {
+    PTB_CUDA_CHECK(cudaMemcpyAsync(S->f(0), u0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(S->f(1), v0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
+    PTB_CUDA_CHECK(cudaMemsetAsync(S->f(2), 0, nf * sizeof(double), st));
+    PTB_CUDA_CHECK(cudaMemsetAsync(S->f(3), 0, nf * sizeof(double), st));
+  }
+  PTB_CUDA_CHECK(cudaMemsetAsync(flags, 0, (N + 1) * sizeof(int32_t), st));
+  // serial fine reference (parareal.cpp:190-199)
+  for (size_t n = 1; n <= N; ++n) {
+    for (int f = 0; f < 4; ++f) cpy(ref.f(f, n), ref.f(f, n - 1), nf);
+    pml_propagate(fine, fine->steps, 1, ref.f(0, n), ref.f(1, n), ref.f(2, n), ref.f(3, n), nullptr);
+  }
+  // iterate 0: the serial coarse chain, interpolated (parareal.cpp:139-145)
+  for (int f = 0; f < 4; ++f) restrict_fields(t, 1, cur.f(f, 0), cwv.f(f));
+  for (size_t n = 1; n <= N; ++n) {
+    pml_propagate(coarse, coarse->steps, 1, cwv.f(0), cwv.f(1), cwv.f(2), cwv.f(3), nullptr);
+    for (int f = 0; f < 4; ++f) interpolate_fields(t, 1, cwv.f(f), cur.f(f, n));
+  }
+  cudaEvent_t e0, e1;
+  PTB_CUDA_CHECK(cudaEventCreate(&e0));
+  PTB_CUDA_CHECK(cudaEventCreate(&e1));
+  std::vector<double> hs(2 * (N + 1));
+  for (int k = 1; k <= K; ++k) {
+    PTB_CUDA_CHECK(cudaEventRecord(e0, st));
+    // parallel stage: next[n] = F(cur[n-1]), old[n] = C(R cur[n-1]) for n = 1..N
+    for (int f = 0; f < 4; ++f) {
+      cpy(nxt.f(f, 1), cur.f(f, 0), N * nf);
+      restrict_fields(t, N, cur.f(f, 0), cold.f(f));
+    }
+    pml_propagate(fine, fine->steps, N, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), flags + 1);
+    pml_propagate(coarse, coarse->steps, N, cold.f(0), cold.f(1), cold.f(2), cold.f(3), nullptr);
+    for (int f = 0; f < 4; ++f) restrict_fields(t, N, nxt.f(f, 1), crf.f(f));
+    // sequential sweep on the coarse grid: w_0 = R(next[0]); g = C(w_{n-1}); d_n = g - old[n];
+    // w_n = R(fine_next[n]) + d_n  (= R(next[n]): R(I(d)) = d at the coarse nodes)
+    for (int f = 0; f < 4; ++f) {
+      cpy(nxt.f(f, 0), cur.f(f, 0), nf);
+      restrict_fields(t, 1, nxt.f(f, 0), cwv.f(f));
+    }
+    for (size_t n = 1; n <= N; ++n) {
+      for (int f = 0; f < 4; ++f) cpy(cg.f(f), cwv.f(f), nc);
+      pml_propagate(coarse, coarse->steps, 1, cg.f(0), cg.f(1), cg.f(2), cg.f(3), nullptr);
+      for (int f = 0; f < 4; ++f) {
+        k_sweep_diff<<<ew_blocks(ctx, nc), 256, 0, st>>>(nc, cg.f(f), cold.f(f, n - 1), crf.f(f, n - 1),
+                                                         cd.f(f, n - 1), cwv.f(f));
+        PTB_LAUNCH_CHECK(ctx);
+      }
+    }
+    // next[n] = fine_next[n] + I(d_n), in chunks of slices
+    for (int f = 0; f < 4; ++f)
+      for (size_t a = 0; a < N; a += chunk) {
+        const size_t m = std::min(chunk, N - a);
+        interpolate_fields(t, m, cd.f(f, a), fchunk);
+        k_add_into<<<ew_blocks(ctx, m * nf), 256, 0, st>>>(m * nf, nxt.f(f, 1 + a), fchunk);
+        PTB_LAUNCH_CHECK(ctx);
+      }
+    PTB_CUDA_CHECK(cudaEventRecord(e1, st));
+    // metric (outside the timed body): relative L2 over [u; udot] vs the serial fine reference
+    if (err_out) {
+      k_err_sums<<<unsigned(N + 1), 512, 0, st>>>(nf, nxt.f(0), nxt.f(1), ref.f(0), ref.f(1), sums);
+      PTB_LAUNCH_CHECK(ctx);
+      PTB_CUDA_CHECK(cudaMemcpyAsync(hs.data(), sums, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (ms_out) {
+      float ms = 0.f;
+      PTB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+      ms_out[k - 1] = ms;
+    }
+    if (err_out)
+      for (size_t n = 0; n <= N; ++n)
+        err_out[size_t(k - 1) * (N + 1) + n] = hs[2 * n + 1] > 0 ? std::sqrt(hs[2 * n] / hs[2 * n + 1]) : std::sqrt(hs[2 * n]);
+    std::swap(cur, nxt);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (diverged_out) {
+    std::vector<int32_t> hf(N + 1);
+    PTB_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, (N + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+    int32_t any = 0;
+    for (auto x : hf) any |= x;
+    *diverged_out = any;
+  }
+  if (states_out) {  // the last iterate, [field][state][point] with fields u, udot, px, py
+    PTB_CUDA_CHECK(cudaMemcpyAsync(states_out, cur.base, 4 * (N + 1) * nf * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
 }
 
 }  // namespace ptb
@@ -433,6 +600,25 @@ ptb_status ptb_pml_create(ptb_context* ctx, const ptb_grid* grid, const double* 
     }
     PTB_CUDA_CHECK(cudaMalloc(&p->coef, h.size() * sizeof(double)));
     PTB_CUDA_CHECK(cudaMemcpy(p->coef, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+    // tile classes: a tile is a layer tile when a damped row or column lies within HL cells of
+    // it (the halo the layer kernel reads); the plain kernel's smaller halo then sees none
+    std::vector<int2> plain, layer;
+    auto damped = [](const double* z, long n, long lo, long hi) {
+      for (long i = lo; i < hi; ++i)
+        if (z[((i % n) + n) % n] > 0.0) return true;
+      return false;
+    };
+    for (long ty = 0; ty < long(ny); ty += PT)
+      for (long tx = 0; tx < long(nx); tx += PT) {
+        const bool l = damped(zeta_y_host, long(ny), ty - HL, ty + PT + HL) ||
+                       damped(zeta_x_host, long(nx), tx - HL, tx + PT + HL);
+        (l ? layer : plain).push_back(make_int2(int(ty), int(tx)));
+      }
+    p->nplain = int(plain.size());
+    p->nlayer = int(layer.size());
+    plain.insert(plain.end(), layer.begin(), layer.end());
+    PTB_CUDA_CHECK(cudaMalloc(&p->tiles, plain.size() * sizeof(int2)));
+    PTB_CUDA_CHECK(cudaMemcpy(p->tiles, plain.data(), plain.size() * sizeof(int2), cudaMemcpyHostToDevice));
     *out = p;
   });
 }
@@ -442,6 +628,7 @@ ptb_status ptb_pml_destroy(ptb_pml* p) {
     if (!p) return;
     DevGuard g(p->ctx->device);
     cudaFree(p->coef);
+    cudaFree(p->tiles);
     delete p;
   });
 }
@@ -453,6 +640,19 @@ ptb_status ptb_pml_propagate_batch(ptb_pml* p, size_t steps, size_t batch, doubl
     DevGuard g(p->ctx->device);
     std::lock_guard<std::recursive_mutex> lock(p->ctx->mutex);
     pml_propagate(p, steps ? steps : p->steps, batch, u_dev, udot_dev, px_dev, py_dev, nonfinite_dev);
+  });
+}
+
+ptb_status ptb_pml_parareal_run(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t n_couplings, int iterations,
+                                const double* u0_host, const double* udot0_host, double* rel_err_host,
+                                double* iteration_ms_host, double* states_host, int32_t* diverged_host) {
+  return guarded([&] {
+    require(fine && coarse && t && u0_host && udot0_host, "pml parareal: null argument");
+    require(fine->ctx == coarse->ctx && t->ctx == fine->ctx, "pml parareal: objects of different contexts");
+    DevGuard g(fine->ctx->device);
+    std::lock_guard<std::recursive_mutex> lock(fine->ctx->mutex);
+    pml_parareal(fine, coarse, t, n_couplings, iterations, u0_host, udot0_host, rel_err_host, iteration_ms_host,
+                 states_host, diverged_host);
   });
 }
 

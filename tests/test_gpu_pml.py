@@ -145,3 +145,33 @@ def test_pulse_absorbed_on_device(ctx):
     prop.propagate(*t)  # t = 1: the front has crossed the layer
     e1 = M.interior_energy(t[0].cpu().numpy(), t[1].cpu().numpy(), c, h, h, w)
     assert np.isfinite(e1) and e1 < 1e-2 * e0, e1 / e0
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_pml_plain_parareal_matches_oracle(ctx, kind):
+    """Iterates of the device driver vs oracle/pml_np.plain_parareal (1e-10 relative per field,
+    the north star's iterate tolerance) and bitwise exactness of the converged slices."""
+    import paratime_b200 as B
+    from tests.test_pml_oracle import _small_parareal
+
+    s = _small_parareal(kind)
+    its, err = M.plain_parareal(s["u0"], np.zeros_like(s["u0"]), s["kf"], s["mf"], s["kc"], s["mc"], s["t"],
+                                s["N"], s["K"])
+    nf, nc, W = s["nf"], s["nc"], s["W"]
+    gf, gc = B.Grid((nf, nf), (1 / nf, 1 / nf)), B.Grid((nc, nc), (1 / nc, 1 / nc))
+    zf = M.damping_profile(nf, W, 1 / nf, 1.0)
+    zc = M.damping_profile(nc, W // 4, 1 / nc, 1.0)
+    fine = B.PmlPropagator(ctx, gf, s["c"], zf, zf, s["dtf"], s["mf"])
+    coarse = B.PmlPropagator(ctx, gc, s["cc"], zc, zc, s["dtc"], s["mc"])
+    tr = B.Transfer(ctx, gc, gf, kind)
+    r = B.pml_parareal_run(fine, coarse, tr, s["N"], s["K"], s["u0"], np.zeros_like(s["u0"]), keep_states=True)
+    assert not r["diverged"]
+    last = its[-1]
+    for f in range(4):
+        want = np.stack([last[n][f] for n in range(s["N"] + 1)])
+        got = r["states"][f]
+        assert _rel(got, want) <= 1e-10, (f, _rel(got, want))
+    for k in range(s["K"]):
+        assert np.all(r["rel_err"][k, : k + 2] == 0.0), r["rel_err"][k]  # exact slices, bitwise
+    np.testing.assert_allclose(r["rel_err"][:, s["K"] + 1:], err[:, s["K"] + 1:], rtol=1e-8)
+    assert np.all(r["iteration_ms"] > 0)

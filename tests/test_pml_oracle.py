@@ -95,3 +95,31 @@ def test_host_profile_matches_oracle_bitwise():
         pytest.skip("library not built")
     for n, w, h, cmax, R in [(2048, 32, 1 / 2048, 1.0, 1e-4), (256, 4, 1 / 256, 1.0, 1e-4), (100, 7, 0.013, 0.8, 1e-6)]:
         assert np.array_equal(B.damping_profile(n, w, h, cmax, R), M.damping_profile(n, w, h, cmax, R))
+
+
+def _small_parareal(kind=0, N=6, K=3):
+    nf, nc, W = 64, 16, 8
+    hf, hc = 1 / nf, 1 / nc
+    rng = np.random.default_rng(11)
+    c = 0.7 + 0.3 * rng.random((nf, nf))
+    cc = np.ascontiguousarray(c[::4, ::4])
+    dtf, mf = hf / 8, 16
+    dtc, mc = hc / 4, 2  # the same coupling interval 1/32
+    kf = M.PmlCoefficients(c, hf, hf, dtf, M.damping_profile(nf, W, hf, 1.0), M.damping_profile(nf, W, hf, 1.0))
+    kc = M.PmlCoefficients(cc, hc, hc, dtc, M.damping_profile(nc, W // 4, hc, 1.0),
+                           M.damping_profile(nc, W // 4, hc, 1.0))
+    t = P.Transfer(P.Grid((nc, nc), (hc, hc)), P.Grid((nf, nf), (hf, hf)), kind)
+    u0 = _pulse(nf, w=300.0, x0=0.45, y0=0.55)
+    return dict(nf=nf, nc=nc, c=c, cc=cc, dtf=dtf, mf=mf, dtc=dtc, mc=mc, kf=kf, kc=kc, t=t, u0=u0, N=N, K=K, W=W)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_plain_parareal_oracle_exactness_and_convergence(kind):
+    s = _small_parareal(kind)
+    its, err = M.plain_parareal(s["u0"], np.zeros_like(s["u0"]), s["kf"], s["mf"], s["kc"], s["mc"], s["t"],
+                                s["N"], s["K"])
+    for k in range(s["K"]):
+        assert np.all(err[k, : k + 2] == 0.0), err[k]  # slices n <= k+1 are exact (parareal.cpp exactness)
+    assert np.all(np.isfinite(err))
+    if kind == 0:  # plain parareal need not converge for waves (the paper's motivation); here it does
+        assert np.max(err[-1]) < np.max(err[0])
