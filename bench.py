@@ -204,6 +204,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the cfg5 grid sweep")
     ap.add_argument("--no-parareal", action="store_true", help="skip the s/iteration measurement")
+    ap.add_argument("--no-pml", action="store_true", help="skip the cfg4 absorbing-layer section")
     args = ap.parse_args()
 
     rank, world, local = dist_env()
@@ -334,6 +335,8 @@ def main():
                 line["cpu_baseline_parareal"] = cpu_parareal_iteration(2)
         if not args.no_sweep:
             line["cfg5_sweep"] = sweep(B, ctx, mode, tflops_peak, hbm_peak)
+        if not args.no_pml:
+            line["cfg4_pml"] = pml_section(B, ctx, tflops_peak, hbm_peak)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -505,6 +508,53 @@ def sweep(B, ctx, mode, tflops_peak, hbm_peak):
                     "frac_binding": max(f_fp64 or 0.0, f_hbm)})
         del u, v, prop
     return out
+
+def pml_section(B, ctx, tflops_peak, hbm_peak):
+    """BASELINE.json config 4 WITH its 32-cell absorbing layer (workloads.cfg4_pml; not in the
+    reference).  (1) fine-stage throughput of the layered propagator on the
+    per-GPU share of cfg4 at 8 GPUs (16 slices x 128 steps, 2048^2), device-resident, CUDA events;
+    binding roofline with 40 B per point per 4-step pass (10 B/update) and 17 flops/update;
+    (2) s/iteration of plain parareal (ptb_pml_parareal_run, N = 128, K = 8, one GPU)."""
+    import torch
+
+    from workloads import cfg4_pml
+
+    spec, c, cc, u0, v0, (zf, zc) = cfg4_pml()
+    nf, nc = spec["fine_n"][0], spec["coarse_n"][0]
+    gf = B.Grid((nf, nf), (1.0 / nf, 1.0 / nf))
+    gc = B.Grid((nc, nc), (1.0 / nc, 1.0 / nc))
+    fine = B.PmlPropagator(ctx, gf, c, zf, zf, spec["dt_fine"], spec["m_fine"])
+    coarse = B.PmlPropagator(ctx, gc, cc, zc, zc, spec["dt_coarse"], spec["m_coarse"])
+    batch = 16
+    t = [torch.zeros((batch, nf, nf), dtype=torch.float64, device="cuda") for _ in range(4)]
+    t[0].copy_(torch.as_tensor(u0, device="cuda").expand(batch, nf, nf))
+    for _ in range(3):
+        fine.propagate(*t)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        fine.propagate(*t)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ups = batch * nf * nf * spec["m_fine"] / (ms * 1e-3)
+    del t
+    torch.cuda.empty_cache()
+    f_hbm = ups * 10.0 / (hbm_peak * 1e9)
+    f_fp64 = ups * FLOPS_PER_UPDATE / (tflops_peak * 1e12) if tflops_peak else None
+    tr = B.Transfer(ctx, gc, gf, spec["interp"])
+    r = B.pml_parareal_run(fine, coarse, tr, spec["n_couplings"], spec["iterations"], u0, v0)
+    its = [float(x) for x in r["iteration_ms"]]
+    return {"workload": "cfg4 + 32-cell absorbing layer (fine 2048^2 / coarse 256^2, layered-faulted medium)",
+            "fine_stage": {"batch": batch, "steps": spec["m_fine"], "ms": round(ms, 3), "updates_per_s": ups,
+                           "frac_hbm": f_hbm, "frac_fp64": f_fp64, "frac_binding": max(f_hbm, f_fp64 or 0.0),
+                           "kernel": "k_pml<plain> 64x64 tiles (halo 5) + k_pml<layer> (halo 9), 4 steps per pass"},
+            "plain_parareal": {"N": spec["n_couplings"], "K": spec["iterations"],
+                               "s_per_iteration": float(np.median(its)) / 1e3, "iteration_ms": [round(x, 2) for x in its],
+                               "max_err_last_rel_init": float(np.max(r["rel_err"][-1])), "diverged": r["diverged"]}}
+
 
 if __name__ == "__main__":
     main()

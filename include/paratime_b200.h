@@ -131,8 +131,8 @@ ptb_status ptb_pml_propagate_batch(ptb_pml* p, size_t steps, size_t batch, doubl
 /* Plain parareal (Eq. 2, parareal.cpp:201-237) with the absorbing layer: states carry
  * (u, udot, px, py); fine and coarse are PML propagators on t's fine / coarse grids (the same
  * coupling interval); iterate 0 is the interpolated serial coarse chain, the sweep runs on the
- * coarse grid (R(I(d)) = d).  Host outputs (all nullable): rel_err_host[K x (N+1)] relative L2 of
- * [u; udot] vs the serial fine run, iteration_ms_host[K] device time of each iteration body
+ * coarse grid (R(I(d)) = d).  Host outputs (all nullable): rel_err_host[K x (N+1)] L2 distance of
+ * [u; udot] to the serial fine run relative to the initial state's norm (the layer drains energy), iteration_ms_host[K] device time of each iteration body
  * (metrics excluded), states_host[4 x (N+1) x N_f] the last iterate, diverged_host = any
  * non-finite fine stage.  The theta (Procrustes) variant is periodic only. */
 ptb_status ptb_pml_parareal_run(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t n_couplings, int iterations,

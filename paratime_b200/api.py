@@ -229,7 +229,7 @@ class PmlPropagator:
 def pml_parareal_run(fine: "PmlPropagator", coarse: "PmlPropagator", transfer: "Transfer", n_couplings: int,
                      iterations: int, u0, udot0, keep_states: bool = False):
     """ptb_pml_parareal_run: plain parareal with the absorbing layer.  Returns a dict with the
-    relative L2 errors [K x (N+1)], per-iteration device ms, the diverged flag and (optionally)
+    L2 distances to the serial fine run relative to the initial state [K x (N+1)], per-iteration device ms, the diverged flag and (optionally)
     the last iterate as an array [4, N+1, *grid] (u, udot, px, py)."""
     N, K = int(n_couplings), int(iterations)
     dp = C.POINTER(C.c_double)

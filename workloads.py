@@ -115,6 +115,23 @@ def cfg4(tol=1e-4, **kw):
     return _spec(nf, nc, 128, 8, 128, 8, tol, **kw), c, cc, u0, np.zeros_like(u0)
 
 
+def cfg4_pml(reflection=1e-4, profile=None):
+    """cfg4 with BASELINE.json's 32-cell absorbing layer on all sides (fine 2048^2: 32 cells; coarse
+    256^2: the same physical width, 4 cells), quadratic damping profile with amplitude
+    1.5 cmax ln(1/R)/L, R = 1e-4, cmax = max fine c for both grids.  Returns
+    (spec, c_fine, c_coarse, u0, udot0, (zeta_fine, zeta_coarse)); the profiles are per axis (the
+    same for rows and columns).  The reference has no layer: this runs plain
+    parareal through ptb_pml_parareal_run; theta-parareal stays periodic."""
+    if profile is None:  # the C ABI's host profile (bitwise equal to oracle/pml_np.damping_profile)
+        from paratime_b200 import damping_profile as profile
+    spec, c, cc, u0, v0 = cfg4()
+    nf, nc = spec["fine_n"][0], spec["coarse_n"][0]
+    cmax = float(c.max())
+    zf = profile(nf, 32, 1.0 / nf, cmax, reflection)
+    zc = profile(nc, 4, 1.0 / nc, cmax, reflection)
+    return spec, c, cc, u0, v0, (zf, zc)
+
+
 def cfg5_medium(n, seed=SEED + 5):
     """c = 0.75 + 0.25 S/max|S|, S = sum of 8 sinusoids of integer wavenumbers 1..4."""
     rng = np.random.default_rng(seed)
