@@ -79,6 +79,13 @@ __device__ __forceinline__ double force_layer(double fb, double kx, double gx, d
   return __dadd_rn(fb, __dmul_rn(kx, __dadd_rn(__dmul_rn(gx, __dsub_rn(pxe, pxw)), __dmul_rn(gy, __dsub_rn(pyn, pys)))));
 }
 
+// 8-byte global -> shared asynchronous copy (LDGSTS)
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 __device__ __forceinline__ int wrap(int i, int n) {
   i %= n;
   return i < 0 ? i + n : i;
@@ -136,31 +143,33 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
   const size_t base = size_t(b) * a.n;
   double hv[NPT];                  // v on load, then the carried half kick vh, then v at the end
   double kr[LAYER ? NPT : 1];      // layer tiles: kx in registers (plain tiles: the ks plane)
+  // shared planes filled with cp.async (all copies in flight together), v and k into registers
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     const int e = tid + i * NT;
-    double u = 0.0, v = 0.0, k = 0.0, px = 0.0, py = 0.0;
+    double v = 0.0, k = 0.0;
     if (e < G::EXT) {
       const int ey = e / E, ex = e - ey * E;
       const size_t g = size_t(rowg[ey]) + colg[ex];
-      u = a.ui[base + g];
+      cp_async8(&us[e], a.ui + base + g);
       v = a.vi[base + g];
       k = a.kx[g];
       if constexpr (LAYER) {
-        px = a.pxi[base + g];
-        py = a.pyi[base + g];
+        cp_async8(&pxs[e], a.pxi + base + g);
+        cp_async8(&pys[e], a.pyi + base + g);
       }
+    } else {
+      us[e] = 0.0;
+      if constexpr (LAYER) pxs[e] = pys[e] = 0.0;
     }
-    us[e] = u;
     hv[i] = v;
     if constexpr (LAYER) {
       kr[i] = k;
-      pxs[e] = px;
-      pys[e] = py;
     } else {
       ks[e] = k;
     }
   }
+  cp_async_wait_all();
   __syncthreads();
 
   // Every stage runs over all padded points without branches: rim and pad values are garbage
@@ -276,15 +285,20 @@ __global__ void __launch_bounds__(256, 2) k_pml_plain(const PmlArgs a) {
   __syncthreads();
   const size_t base = size_t(blockIdx.y) * a.n;
   double u[PR], hv[PR];
+  // u and the coefficient go global -> shared with cp.async (no register round trip, so all 40
+  // copies of a thread are in flight together; ncu: a register-staged kx store per row
+  // serialised the loads), the velocity straight into registers
 #pragma unroll
   for (int r = 0; r < PR; ++r) {
     const size_t g = size_t(rowg[r0 + r]) + colg[c];
-    u[r] = a.ui[base + g];
+    cp_async8(&us[(r0 + r) * EX + c], a.ui + base + g);
+    cp_async8(&ks[(r0 + r) * EX + c], a.kx + g);
     hv[r] = a.vi[base + g];
-    ks[(r0 + r) * EX + c] = a.kx[g];
-    us[(r0 + r) * EX + c] = u[r];
   }
+  cp_async_wait_all();
   __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PR; ++r) u[r] = us[(r0 + r) * EX + c];
   auto force = [&](int r, const double* uu) {
     const int e = (r0 + r) * EX + c;
     const double un = r < PR - 1 ? uu[r + 1] : us[e + EX];
