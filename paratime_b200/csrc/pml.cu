@@ -187,9 +187,10 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
   for (int i = 0; i < NPT; ++i) {
     const int e = tid + i * NT;
     const double f = force(e, kr[LAYER ? i : 0]);
-    if constexpr (LAYER)
-      hv[i] = kick_layer(hv[i], f, us[e], zxs[col(e)], zys[row(e)], a.hd);
-    else
+    if constexpr (LAYER) {
+      const double zx = zxs[col(e)], zy = zys[row(e)];
+      hv[i] = (zx != 0.0 || zy != 0.0) ? kick_layer(hv[i], f, us[e], zx, zy, a.hd) : __dadd_rn(hv[i], f);
+    } else
       hv[i] = hv[i] + f;
   }
   for (int s = 0; s < a.steps; ++s) {
@@ -206,10 +207,12 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
         const int e = tid + i * NT;
         const int ex = col(e), ey = row(e);
         const double zx = zxs[ex], zy = zys[ey];
-        pxs[e] = __dadd_rn(__dmul_rn(axs[ex], pxs[e]),
-                           __dmul_rn(__dmul_rn(__dsub_rn(zy, zx), qxs[ex]), __dsub_rn(us[e + 1], us[e - 1])));
-        pys[e] = __dadd_rn(__dmul_rn(ays[ey], pys[e]),
-                           __dmul_rn(__dmul_rn(__dsub_rn(zx, zy), qys[ey]), __dsub_rn(us[e + E], us[e - E])));
+        if (zx != 0.0 || zy != 0.0) {  // undamped points: px' = 1 * px + 0 * (...) = px
+          pxs[e] = __dadd_rn(__dmul_rn(axs[ex], pxs[e]),
+                             __dmul_rn(__dmul_rn(__dsub_rn(zy, zx), qxs[ex]), __dsub_rn(us[e + 1], us[e - 1])));
+          pys[e] = __dadd_rn(__dmul_rn(ays[ey], pys[e]),
+                             __dmul_rn(__dmul_rn(__dsub_rn(zx, zy), qys[ey]), __dsub_rn(us[e + E], us[e - E])));
+        }
       }
       __syncthreads();
     }
@@ -220,10 +223,15 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
       const double f = force(e, kr[LAYER ? i : 0]);
       if constexpr (LAYER) {
         const double zx = zxs[col(e)], zy = zys[row(e)];
-        const double pi = __dmul_rn(zy, zx), sg = __dadd_rn(zy, zx);
-        const double inv = __ddiv_rn(1.0, __dadd_rn(1.0, __dmul_rn(a.hd, sg)));
-        const double v1 = __dmul_rn(__dadd_rn(hv[i], __dsub_rn(f, __dmul_rn(a.hd, __dmul_rn(pi, us[e])))), inv);
-        hv[i] = last ? v1 : kick_layer(v1, f, us[e], zx, zy, a.hd);
+        if (zx != 0.0 || zy != 0.0) {
+          const double pi = __dmul_rn(zy, zx), sg = __dadd_rn(zy, zx);
+          const double inv = __ddiv_rn(1.0, __dadd_rn(1.0, __dmul_rn(a.hd, sg)));
+          const double v1 = __dmul_rn(__dadd_rn(hv[i], __dsub_rn(f, __dmul_rn(a.hd, __dmul_rn(pi, us[e])))), inv);
+          hv[i] = last ? v1 : kick_layer(v1, f, us[e], zx, zy, a.hd);
+        } else {  // the same values for finite fields: pi = sg = 0, inv = 1
+          const double v1 = __dadd_rn(hv[i], f);
+          hv[i] = last ? v1 : __dadd_rn(v1, f);
+        }
       } else {
         const double v1 = hv[i] + f;
         hv[i] = last ? v1 : v1 + f;
