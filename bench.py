@@ -550,7 +550,7 @@ def pml_section(B, ctx, tflops_peak, hbm_peak):
     return {"workload": "cfg4 + 32-cell absorbing layer (fine 2048^2 / coarse 256^2, layered-faulted medium)",
             "fine_stage": {"batch": batch, "steps": spec["m_fine"], "ms": round(ms, 3), "updates_per_s": ups,
                            "frac_hbm": f_hbm, "frac_fp64": f_fp64, "frac_binding": max(f_hbm, f_fp64 or 0.0),
-                           "kernel": "k_pml<plain> 64x64 tiles (halo 5) + k_pml<layer> (halo 9), 4 steps per pass"},
+                           "kernel": "k_pml_plain 70x54 register-column tiles (halo 5) + k_pml<layer> (halo 9), 4 steps per pass"},
             "plain_parareal": {"N": spec["n_couplings"], "K": spec["iterations"],
                                "s_per_iteration": float(np.median(its)) / 1e3, "iteration_ms": [round(x, 2) for x in its],
                                "max_err_last_rel_init": float(np.max(r["rel_err"][-1])), "diverged": r["diverged"]}}

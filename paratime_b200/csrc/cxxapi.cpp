@@ -30,6 +30,7 @@
 #include "paratime/speed_model.hpp"
 #include "paratime/grid.hpp"
 #include "paratime/parareal.hpp"
+#include "paratime/pml.hpp"
 #include "paratime/procrustes.hpp"
 #include "paratime/propagator.hpp"
 #include "paratime_b200.h"
@@ -991,3 +992,86 @@ extern "C" ptb_status ptb_run_csv(size_t iterations, size_t couplings, const dou
     if (buf && len >= t.size() + 1) std::memcpy(buf, t.c_str(), t.size() + 1);
   });
 }
+
+// ------------------------------------------------------------------ absorbing layer (pml.hpp)
+namespace paratime {
+
+PmlState::PmlState(WaveState w) : wave(std::move(w)), px(wave.grid.size(), 0.0), py(wave.grid.size(), 0.0) {}
+
+PmlState::PmlState(WaveState w, std::vector<double> px_in, std::vector<double> py_in)
+    : wave(std::move(w)), px(std::move(px_in)), py(std::move(py_in)) {
+  if (px.size() != wave.grid.size() || py.size() != wave.grid.size())
+    throw std::invalid_argument("PmlState: auxiliary field size does not match grid");
+}
+
+bool PmlState::finite() const { return wave.finite() && all_finite(px) && all_finite(py); }
+
+std::vector<double> pml_damping_profile(std::size_t n, std::size_t width, double h, double cmax, double reflection) {
+  std::vector<double> z(n);
+  check(ptb_pml_damping_profile(n, width, h, cmax, reflection, z.data()));
+  return z;
+}
+
+struct PmlConfig::Device {
+  ptb_pml* h = nullptr;
+  ~Device() {
+    if (h) ptb_pml_destroy(h);
+  }
+};
+
+PmlConfig::PmlConfig(Grid g, SpeedField s, std::vector<double> zy, std::vector<double> zx, double dt_in,
+                     std::size_t steps)
+    : grid(std::move(g)), speed(std::move(s)), zeta_y(std::move(zy)), zeta_x(std::move(zx)), dt(dt_in),
+      steps_per_coupling(steps) {
+  check_same_grid(grid, speed.grid, "PmlConfig");
+  if (grid.dim() != 2) throw std::invalid_argument("PmlConfig: the absorbing layer is two-dimensional");
+  if (zeta_y.size() != grid.points(0) || zeta_x.size() != grid.points(1))
+    throw std::invalid_argument("PmlConfig: one damping value per row and per column");
+  auto d = std::make_shared<Device>();
+  const ptb_grid cg = cgrid(grid);
+  check(ptb_pml_create(ctx(), &cg, speed.c.data(), zeta_y.data(), zeta_x.data(), dt, steps_per_coupling, &d->h));
+  device_ = std::move(d);
+}
+
+void pml_propagate_coupling_batch(std::span<PmlState> states, const PmlConfig& cfg, std::vector<bool>* diverged) {
+  const size_t n = cfg.grid.size(), b = states.size();
+  if (diverged) diverged->assign(b, false);
+  if (b == 0) return;
+  for (const PmlState& s : states) {
+    check_same_grid(s.wave.grid, cfg.grid, "pml_propagate_coupling");
+    if (s.px.size() != n || s.py.size() != n) throw std::invalid_argument("PmlState: auxiliary field size");
+  }
+  DBuf f(4 * b * n);
+  for (size_t i = 0; i < b; ++i) {
+    f.up(states[i].wave.u.data(), n, (0 * b + i) * n);
+    f.up(states[i].wave.udot.data(), n, (1 * b + i) * n);
+    f.up(states[i].px.data(), n, (2 * b + i) * n);
+    f.up(states[i].py.data(), n, (3 * b + i) * n);
+  }
+  void* fl = nullptr;
+  check(ptb_device_alloc(ctx(), b * sizeof(int32_t), &fl));
+  std::unique_ptr<void, std::function<void(void*)>> guard(fl, [](void* q) { ptb_device_free(ctx(), q); });
+  std::vector<int32_t> zeros(b, 0), flags(b, 0);
+  check(ptb_memcpy_h2d(ctx(), fl, zeros.data(), b * sizeof(int32_t)));
+  check(ptb_pml_propagate_batch(cfg.device_->h, 0, b, f.p, f.p + b * n, f.p + 2 * b * n, f.p + 3 * b * n,
+                                static_cast<int32_t*>(fl)));
+  check(ptb_memcpy_d2h(ctx(), flags.data(), fl, b * sizeof(int32_t)));
+  for (size_t i = 0; i < b; ++i) {
+    states[i].wave.u = f.down(n, (0 * b + i) * n);
+    states[i].wave.udot = f.down(n, (1 * b + i) * n);
+    states[i].px = f.down(n, (2 * b + i) * n);
+    states[i].py = f.down(n, (3 * b + i) * n);
+    if (diverged) (*diverged)[i] = flags[i] != 0;
+  }
+}
+
+PmlState pml_propagate_coupling(const PmlState& state, const PmlConfig& cfg) {
+  PmlState out = state;
+  std::vector<bool> div;
+  pml_propagate_coupling_batch(std::span<PmlState>(&out, 1), cfg, &div);
+  if (div[0]) throw PropagationDiverged("pml_propagate_coupling: non-finite state after coupling");
+  return out;
+}
+
+}  // namespace paratime
+

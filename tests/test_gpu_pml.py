@@ -175,3 +175,17 @@ def test_pml_plain_parareal_matches_oracle(ctx, kind):
         assert np.all(r["rel_err"][k, : k + 2] == 0.0), r["rel_err"][k]  # exact slices, bitwise
     np.testing.assert_allclose(r["rel_err"][:, s["K"] + 1:], err[:, s["K"] + 1:], rtol=1e-8)
     assert np.all(r["iteration_ms"] > 0)
+
+
+def test_cxx_api_suite():
+    """tests/refsuite/test_pml.cpp: the C++ drop-in extension (include/paratime/pml.hpp) in the
+    reference's doctest style, built in the development container."""
+    import subprocess
+    from pathlib import Path
+
+    exe = Path(__file__).resolve().parent / "refsuite" / "_bin" / "test_pml"
+    if not exe.exists():
+        pytest.skip(f"{exe} not built")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "failed checks: 0" in r.stdout
