@@ -53,4 +53,12 @@ PmlState pml_propagate_coupling(const PmlState& state, const PmlConfig& cfg);
 void pml_propagate_coupling_batch(std::span<PmlState> states, const PmlConfig& cfg,
                                   std::vector<bool>* diverged = nullptr);
 
+/// Plain parareal (parareal.cpp:201-237, Eq. 2) on the layered state: fine and coarse layered
+/// propagators on transfer's fine / coarse grids with the same coupling interval; iterate 0 is
+/// the interpolated serial coarse chain.  Returns the last iterate (n_couplings + 1 states);
+/// errors[k][n] (optional) = ||[u; udot] - serial fine||_2 / ||initial [u; udot]||_2.
+std::vector<PmlState> pml_plain_parareal(const WaveState& init, const PmlConfig& fine, const PmlConfig& coarse,
+                                         const GridTransfer& transfer, std::size_t n_couplings, int iterations,
+                                         std::vector<std::vector<double>>* errors = nullptr);
+
 }  // namespace paratime

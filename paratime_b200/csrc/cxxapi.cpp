@@ -1073,5 +1073,34 @@ PmlState pml_propagate_coupling(const PmlState& state, const PmlConfig& cfg) {
   return out;
 }
 
+std::vector<PmlState> pml_plain_parareal(const WaveState& init, const PmlConfig& fine, const PmlConfig& coarse,
+                                         const GridTransfer& transfer, std::size_t n_couplings, int iterations,
+                                         std::vector<std::vector<double>>* errors) {
+  check_same_grid(init.grid, fine.grid, "pml_plain_parareal");
+  check_same_grid(transfer.fine, fine.grid, "pml_plain_parareal");
+  check_same_grid(transfer.coarse, coarse.grid, "pml_plain_parareal");
+  const size_t n = fine.grid.size(), N = n_couplings;
+  const int K = std::max(iterations, 0);
+  std::vector<double> err(size_t(std::max(K, 1)) * (N + 1)), states(4 * (N + 1) * n);
+  int32_t div = 0;
+  check(ptb_pml_parareal_run(fine.device_->h, coarse.device_->h, transfer_of(transfer), N, K, init.u.data(),
+                             init.udot.data(), err.data(), nullptr, states.data(), &div));
+  if (errors) {
+    errors->assign(size_t(K), std::vector<double>(N + 1));
+    for (int k = 0; k < K; ++k)
+      std::copy(err.begin() + long(k) * long(N + 1), err.begin() + long(k + 1) * long(N + 1), (*errors)[size_t(k)].begin());
+  }
+  std::vector<PmlState> out;
+  out.reserve(N + 1);
+  for (size_t s = 0; s <= N; ++s) {
+    auto field = [&](int f) {
+      const auto b = states.begin() + long((size_t(f) * (N + 1) + s) * n);
+      return std::vector<double>(b, b + long(n));
+    };
+    out.emplace_back(WaveState(fine.grid, field(0), field(1)), field(2), field(3));
+  }
+  return out;
+}
+
 }  // namespace paratime
 

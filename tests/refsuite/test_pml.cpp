@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "paratime/errors.hpp"
+#include "paratime/parareal.hpp"
 #include "paratime/grid.hpp"
 #include "paratime/pml.hpp"
 #include "paratime/propagator.hpp"
@@ -91,4 +92,21 @@ TEST_CASE("errors follow PropagatorConfig") {
   WaveState w = pulse(g);
   w.u[5] = std::numeric_limits<double>::infinity();
   CHECK_THROWS_AS(pml_propagate_coupling(PmlState(w), cfg), PropagationDiverged);
+}
+
+TEST_CASE("plain parareal with the layer: converged slices are exact") {
+  const Grid fg = grid2(64), cg = grid2(16);
+  const SpeedField fs(fg, std::vector<double>(fg.size(), 1.0)), cs(cg, std::vector<double>(cg.size(), 1.0));
+  const auto zf = pml_damping_profile(64, 8, 1.0 / 64, 1.0), zc = pml_damping_profile(16, 2, 1.0 / 16, 1.0);
+  const PmlConfig fine(fg, fs, zf, zf, 1.0 / 512, 16), coarse(cg, cs, zc, zc, 1.0 / 64, 2);
+  const GridTransfer t(cg, fg, InterpKind::fourier);
+  std::vector<std::vector<double>> err;
+  const auto it = pml_plain_parareal(pulse(fg), fine, coarse, t, 6, 3, &err);
+  REQUIRE(it.size() == 7);
+  REQUIRE(err.size() == 3);
+  for (int k = 0; k < 3; ++k)
+    for (int n = 0; n <= k + 1; ++n) CHECK(err[size_t(k)][size_t(n)] == 0.0);
+  // the first iterate's slice 1 is one fine coupling of the initial state
+  const PmlState f1 = pml_propagate_coupling(PmlState(pulse(fg)), fine);
+  CHECK(it[1].wave.u == f1.wave.u);
 }
