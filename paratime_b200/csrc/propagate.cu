@@ -1110,14 +1110,16 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
       const int nrb = (ny + rb - 1) / rb;
       const size_t ctas = size_t(strips) * nrb * batch;
       const size_t slots = size_t(ctx->num_sms) * occ;
-      const double rounds = std::ceil(double(ctas) / slots);
-      // per-SM time of one round ~ resident warps x rows / throughput; the kernel is
+      // time of one round on its busiest SM ~ rows x max(warps, 8) / 8: the kernel is
       // latency-bound below 8 warps per SM (ncu: W=160, 5 warps/SM, runs ~1.6x slower per
-      // warp-row than 2 x W=128), so throughput scales with min(1, warps / 8)
-      const double warps = double(occ) * (W / 32.0);
-      const double resident = double(std::min(ctas, slots)) / ctx->num_sms * (W / 32.0);
-      const double eff = std::min(1.0, std::min(warps, resident) / 8.0);
-      double cost = rounds * warps * (rb + 2.0 * S) / eff;
+      // warp-row than 2 x W=128), throughput-bound above.  Full rounds hold `occ` CTAs per SM;
+      // a partial last round ceil(rest / SMs) on its busiest SM (idle SMs cost nothing).
+      const auto round_time = [&](size_t ctas_per_sm) {
+        return (rb + 2.0 * S) * std::max(1.0, double(ctas_per_sm) * (W / 32.0) / 8.0);
+      };
+      const size_t full_rounds = ctas / slots, rest = ctas - full_rounds * slots;
+      double cost = double(full_rounds) * round_time(size_t(occ)) +
+                    (rest ? round_time((rest + ctx->num_sms - 1) / ctx->num_sms) : 0.0);
       if (full && full_env == 2) cost *= 1e-6;  // PTB_WAVE_FULL=2 (tests): prefer full-row strips
       if (cost < best_cost) {
         best_cost = cost;
