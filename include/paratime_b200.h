@@ -138,6 +138,13 @@ ptb_status ptb_pml_propagate_batch(ptb_pml* p, size_t steps, size_t batch, doubl
 ptb_status ptb_pml_parareal_run(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t n_couplings, int iterations,
                                 const double* u0_host, const double* udot0_host, double* rel_err_host,
                                 double* iteration_ms_host, double* states_host, int32_t* diverged_host);
+/* the same with slices block-sharded over the ranks of `comm` (one all-gather of the coarse payload
+ * per iteration, the last own fine state to the next rank); every rank gets the full error table,
+ * states_host is filled for the rank's own states only.  Bitwise independent of the world size. */
+ptb_status ptb_pml_parareal_run_sharded(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, ptb_comm* comm,
+                                        size_t n_couplings, int iterations, const double* u0_host,
+                                        const double* udot0_host, double* rel_err_host, double* iteration_ms_host,
+                                        double* states_host, int32_t* diverged_host);
 /* laplacian (propagator.cpp:31-58, reference operation order) */
 ptb_status ptb_laplacian_batch(ptb_context* ctx, const ptb_grid* grid, size_t batch,
                                const double* f_dev, double* out_dev);

@@ -227,7 +227,7 @@ class PmlPropagator:
 
 
 def pml_parareal_run(fine: "PmlPropagator", coarse: "PmlPropagator", transfer: "Transfer", n_couplings: int,
-                     iterations: int, u0, udot0, keep_states: bool = False):
+                     iterations: int, u0, udot0, keep_states: bool = False, comm: "Comm" = None):
     """ptb_pml_parareal_run: plain parareal with the absorbing layer.  Returns a dict with the
     L2 distances to the serial fine run relative to the initial state [K x (N+1)], per-iteration device ms, the diverged flag and (optionally)
     the last iterate as an array [4, N+1, *grid] (u, udot, px, py)."""
@@ -239,9 +239,14 @@ def pml_parareal_run(fine: "PmlPropagator", coarse: "PmlPropagator", transfer: "
     ms = np.zeros(max(K, 1))
     states = np.empty((4, N + 1) + tuple(fine.grid.n)) if keep_states else None
     div = C.c_int32(0)
-    check(lib().ptb_pml_parareal_run(fine.h, coarse.h, transfer.h, C.c_size_t(N), C.c_int(K), u0.ctypes.data_as(dp),
-                                     v0.ctypes.data_as(dp), err.ctypes.data_as(dp), ms.ctypes.data_as(dp),
-                                     states.ctypes.data_as(dp) if keep_states else None, C.byref(div)))
+    out = (err.ctypes.data_as(dp), ms.ctypes.data_as(dp), states.ctypes.data_as(dp) if keep_states else None,
+           C.byref(div))
+    if comm is None:
+        check(lib().ptb_pml_parareal_run(fine.h, coarse.h, transfer.h, C.c_size_t(N), C.c_int(K),
+                                         u0.ctypes.data_as(dp), v0.ctypes.data_as(dp), *out))
+    else:  # slices sharded over the ranks of `comm`; states filled for the own slices only
+        check(lib().ptb_pml_parareal_run_sharded(fine.h, coarse.h, transfer.h, comm.h, C.c_size_t(N), C.c_int(K),
+                                                 u0.ctypes.data_as(dp), v0.ctypes.data_as(dp), *out))
     return {"rel_err": err[:K], "iteration_ms": ms[:K], "diverged": bool(div.value), "states": states}
 
 

@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "ptb_comm.h"
 #include "ptb_internal.h"
 
 namespace ptb {
@@ -517,8 +518,14 @@ struct States {
 
 }  // namespace
 
-void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t N, int K, const double* u0, const double* v0,
-                  double* err_out, double* ms_out, double* states_out, int32_t* diverged_out) {
+// Slices block-sharded over the ranks of `comm` (null: one GPU), as the periodic driver
+// (driver.cu): rank r owns couplings n in [a, b) and the fine states a-1 .. b-1; per iteration one
+// all-gather of the coarse payload (C(R cur[n-1]) and R(fine_next[n]), 4 fields each) feeds the
+// replicated, deterministic coarse sweep, and the last own state goes to rank r+1.  Results are
+// bitwise independent of the world size.
+void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* comm, size_t N, int K,
+                  const double* u0, const double* v0, double* err_out, double* ms_out, double* states_out,
+                  int32_t* diverged_out) {
   ptb_context* ctx = fine->ctx;
   cudaStream_t st = ctx->stream;
   const size_t nf = fine->n, nc = coarse->n;
@@ -529,61 +536,97 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t N, int
   const double tf = fine->dt * double(fine->steps), tc = coarse->dt * double(coarse->steps);
   require(std::fabs(tf - tc) <= 1e-12 * std::max(tf, tc), "CouplingSchedule: fine and coarse couplings differ");
   require(N >= 1 && K >= 0, "pml parareal: need N >= 1 couplings and K >= 0 iterations");
-  // device state: cur, next, reference ((N+1) fine states x 4 fields) + coarse work
-  DeviceBuffer bcur, bnext, bref, bc, bflag, bsum, bchunk;
-  States cur{static_cast<double*>(bcur.get(4 * (N + 1) * nf * sizeof(double))), nf, N + 1};
-  States nxt{static_cast<double*>(bnext.get(4 * (N + 1) * nf * sizeof(double))), nf, N + 1};
-  States ref{static_cast<double*>(bref.get(4 * (N + 1) * nf * sizeof(double))), nf, N + 1};
-  // coarse: old (N), rf = R(fine_next) (N), d (N), w (1), g (1)
-  double* cw = static_cast<double*>(bc.get(4 * (3 * N + 2) * nc * sizeof(double)));
-  States cold{cw, nc, N}, crf{cw + 4 * N * nc, nc, N}, cd{cw + 8 * N * nc, nc, N};
-  States cwv{cw + 12 * N * nc, nc, 1}, cg{cw + 12 * N * nc + 4 * nc, nc, 1};
-  int32_t* flags = static_cast<int32_t*>(bflag.get((N + 1) * sizeof(int32_t)));
-  double* sums = static_cast<double*>(bsum.get(2 * (N + 1) * sizeof(double)));
-  const size_t chunk = std::min<size_t>(N, 8);
-  double* fchunk = static_cast<double*>(bchunk.get(chunk * nf * sizeof(double)));
+  const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
+  const size_t chunk = (N + size_t(world) - 1) / size_t(world);
+  const size_t a = std::min(N + 1, 1 + size_t(rank) * chunk), b = std::min(N + 1, a + chunk), L = b - a;
+  const size_t P = size_t(world) * chunk;  // padded global coarse slots (slot n-1 <-> coupling n)
+  // device state: own fine states a-1 .. b-1 (local 0 .. L), the init state, coarse work
+  DeviceBuffer bcur, bnext, bref, bini, bc, bflag, bsum, bchunk, bpay, ball, bgs;
+  States cur{static_cast<double*>(bcur.get(4 * (L + 1) * nf * sizeof(double))), nf, L + 1};
+  States nxt{static_cast<double*>(bnext.get(4 * (L + 1) * nf * sizeof(double))), nf, L + 1};
+  States ref{static_cast<double*>(bref.get(4 * (L + 1) * nf * sizeof(double))), nf, L + 1};
+  States ini{static_cast<double*>(bini.get(4 * 2 * nf * sizeof(double))), nf, 2};  // init + a work state
+  double* cw = static_cast<double*>(bc.get(4 * (3 * P + 2) * nc * sizeof(double)));
+  States cold{cw, nc, P}, crf{cw + 4 * P * nc, nc, P}, cd{cw + 8 * P * nc, nc, P};
+  States cwv{cw + 12 * P * nc, nc, 1}, cg{cw + 12 * P * nc + 4 * nc, nc, 1};
+  int32_t* flags = static_cast<int32_t*>(bflag.get((L + 1) * sizeof(int32_t)));
+  double* sums = static_cast<double*>(bsum.get(2 * (chunk + 2) * sizeof(double)));
+  const size_t ichunk = std::max<size_t>(1, std::min<size_t>(L, 8));
+  double* fchunk = static_cast<double*>(bchunk.get(ichunk * nf * sizeof(double)));
   auto cpy = [&](double* dst, const double* src, size_t count) {
-    PTB_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (count) PTB_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
   };
-  // initial state: u0, v0, px = py = 0
-  for (States* S : {&cur, &ref}) {
-    PTB_CUDA_CHECK(cudaMemcpyAsync(S->f(0), u0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
-    PTB_CUDA_CHECK(cudaMemcpyAsync(S->f(1), v0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
-    PTB_CUDA_CHECK(cudaMemsetAsync(S->f(2), 0, nf * sizeof(double), st));
-    PTB_CUDA_CHECK(cudaMemsetAsync(S->f(3), 0, nf * sizeof(double), st));
+  auto cpy_state = [&](const States& D, size_t ds, const States& S, size_t ss) {
+    for (int f = 0; f < 4; ++f) cpy(D.f(f, ds), S.f(f, ss), D.n);
+  };
+  PTB_CUDA_CHECK(cudaMemcpyAsync(ini.f(0), u0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
+  PTB_CUDA_CHECK(cudaMemcpyAsync(ini.f(1), v0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
+  PTB_CUDA_CHECK(cudaMemsetAsync(ini.f(2), 0, 2 * nf * sizeof(double), st));  // px, py of state 0
+  PTB_CUDA_CHECK(cudaMemsetAsync(ini.f(3), 0, 2 * nf * sizeof(double), st));
+  PTB_CUDA_CHECK(cudaMemsetAsync(flags, 0, (L + 1) * sizeof(int32_t), st));
+  PTB_CUDA_CHECK(cudaMemsetAsync(cw, 0, 4 * (3 * P + 2) * nc * sizeof(double), st));
+  // serial fine reference (parareal.cpp:190-199): the chain up to b-1, own states kept
+  cpy_state(ini, 1, ini, 0);
+  for (size_t n = 0; n < b; ++n) {
+    if (n > 0) pml_propagate(fine, fine->steps, 1, ini.f(0, 1), ini.f(1, 1), ini.f(2, 1), ini.f(3, 1), nullptr);
+    if (n + 1 >= a) cpy_state(ref, n + 1 - a, ini, 1);
   }
-  PTB_CUDA_CHECK(cudaMemsetAsync(flags, 0, (N + 1) * sizeof(int32_t), st));
-  // serial fine reference (parareal.cpp:190-199)
-  for (size_t n = 1; n <= N; ++n) {
-    for (int f = 0; f < 4; ++f) cpy(ref.f(f, n), ref.f(f, n - 1), nf);
-    pml_propagate(fine, fine->steps, 1, ref.f(0, n), ref.f(1, n), ref.f(2, n), ref.f(3, n), nullptr);
-  }
-  // iterate 0: the serial coarse chain, interpolated (parareal.cpp:139-145)
-  for (int f = 0; f < 4; ++f) restrict_fields(t, 1, cur.f(f, 0), cwv.f(f));
-  for (size_t n = 1; n <= N; ++n) {
+  // iterate 0: the serial coarse chain, interpolated (parareal.cpp:139-145), own states
+  for (int f = 0; f < 4; ++f) restrict_fields(t, 1, ini.f(f, 0), cwv.f(f));
+  if (a == 1) cpy_state(cur, 0, ini, 0);
+  for (size_t n = 1; n < b; ++n) {
     pml_propagate(coarse, coarse->steps, 1, cwv.f(0), cwv.f(1), cwv.f(2), cwv.f(3), nullptr);
-    for (int f = 0; f < 4; ++f) interpolate_fields(t, 1, cwv.f(f), cur.f(f, n));
+    if (n + 1 >= a)
+      for (int f = 0; f < 4; ++f) interpolate_fields(t, 1, cwv.f(f), cur.f(f, n + 1 - a));
   }
+  // init norm (errors are relative to it)
+  k_err_sums<<<1, 512, 0, st>>>(nf, ini.f(0), ini.f(1), ini.f(0), ini.f(1), sums);
+  PTB_LAUNCH_CHECK(ctx);
+  double init_sums[2];
+  PTB_CUDA_CHECK(cudaMemcpyAsync(init_sums, sums, sizeof(init_sums), cudaMemcpyDeviceToHost, st));
+  PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+  const double init_norm2 = init_sums[1];
+
   cudaEvent_t e0, e1;
   PTB_CUDA_CHECK(cudaEventCreate(&e0));
   PTB_CUDA_CHECK(cudaEventCreate(&e1));
-  std::vector<double> hs(2 * (N + 1));
+  const size_t per = 8 * chunk * nc;  // payload doubles per rank: cold and crf, 4 fields each
+  double* own = static_cast<double*>(bpay.get(per * sizeof(double)));
+  double* all = static_cast<double*>(ball.get(per * size_t(world) * sizeof(double)));
+  std::vector<double> hs(2 * (chunk + 1) * size_t(world));
+  double* gsums = static_cast<double*>(bgs.get(hs.size() * sizeof(double)));
   for (int k = 1; k <= K; ++k) {
     PTB_CUDA_CHECK(cudaEventRecord(e0, st));
-    // parallel stage: next[n] = F(cur[n-1]), old[n] = C(R cur[n-1]) for n = 1..N
-    for (int f = 0; f < 4; ++f) {
-      cpy(nxt.f(f, 1), cur.f(f, 0), N * nf);
-      restrict_fields(t, N, cur.f(f, 0), cold.f(f));
+    // parallel stage on the own couplings: next[n] = F(cur[n-1]), old[n] = C(R cur[n-1])
+    if (L) {
+      for (int f = 0; f < 4; ++f) {
+        cpy(nxt.f(f, 1), cur.f(f, 0), L * nf);
+        restrict_fields(t, L, cur.f(f, 0), cold.f(f, a - 1));
+      }
+      pml_propagate(fine, fine->steps, L, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), flags + 1);
+      pml_propagate(coarse, coarse->steps, L, cold.f(0, a - 1), cold.f(1, a - 1), cold.f(2, a - 1), cold.f(3, a - 1),
+                    nullptr);
+      for (int f = 0; f < 4; ++f) restrict_fields(t, L, nxt.f(f, 1), crf.f(f, a - 1));
     }
-    pml_propagate(fine, fine->steps, N, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), flags + 1);
-    pml_propagate(coarse, coarse->steps, N, cold.f(0), cold.f(1), cold.f(2), cold.f(3), nullptr);
-    for (int f = 0; f < 4; ++f) restrict_fields(t, N, nxt.f(f, 1), crf.f(f));
-    // sequential sweep on the coarse grid: w_0 = R(next[0]); g = C(w_{n-1}); d_n = g - old[n];
-    // w_n = R(fine_next[n]) + d_n  (= R(next[n]): R(I(d)) = d at the coarse nodes)
-    for (int f = 0; f < 4; ++f) {
-      cpy(nxt.f(f, 0), cur.f(f, 0), nf);
-      restrict_fields(t, 1, nxt.f(f, 0), cwv.f(f));
+    if (world > 1) {  // one all-gather of the coarse payload
+      for (int f = 0; f < 4; ++f) {
+        cpy(own + size_t(f) * chunk * nc, cold.f(f, a - 1), L * nc);
+        cpy(own + size_t(4 + f) * chunk * nc, crf.f(f, a - 1), L * nc);
+      }
+      comm->allgather(own, all, per * sizeof(double), st);
+      for (int r = 0; r < world; ++r) {
+        const size_t ra = 1 + size_t(r) * chunk;
+        if (ra > N || r == rank) continue;
+        const size_t rl = std::min(N + 1, ra + chunk) - ra;
+        for (int f = 0; f < 4; ++f) {
+          cpy(cold.f(f, ra - 1), all + size_t(r) * per + size_t(f) * chunk * nc, rl * nc);
+          cpy(crf.f(f, ra - 1), all + size_t(r) * per + size_t(4 + f) * chunk * nc, rl * nc);
+        }
+      }
     }
+    // replicated sequential sweep on the coarse grid: w_0 = R(init); g = C(w_{n-1});
+    // d_n = g - old[n]; w_n = R(fine_next[n]) + d_n  (= R(next[n]): R(I(d)) = d at the coarse nodes)
+    for (int f = 0; f < 4; ++f) restrict_fields(t, 1, ini.f(f, 0), cwv.f(f));
     for (size_t n = 1; n <= N; ++n) {
       for (int f = 0; f < 4; ++f) cpy(cg.f(f), cwv.f(f), nc);
       pml_propagate(coarse, coarse->steps, 1, cg.f(0), cg.f(1), cg.f(2), cg.f(3), nullptr);
@@ -593,20 +636,33 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t N, int
         PTB_LAUNCH_CHECK(ctx);
       }
     }
-    // next[n] = fine_next[n] + I(d_n), in chunks of slices
+    // own combine: next[n] = fine_next[n] + I(d_n), in chunks of slices
     for (int f = 0; f < 4; ++f)
-      for (size_t a = 0; a < N; a += chunk) {
-        const size_t m = std::min(chunk, N - a);
-        interpolate_fields(t, m, cd.f(f, a), fchunk);
-        k_add_into<<<ew_blocks(ctx, m * nf), 256, 0, st>>>(m * nf, nxt.f(f, 1 + a), fchunk);
+      for (size_t c0 = 0; c0 < L; c0 += ichunk) {
+        const size_t m = std::min(ichunk, L - c0);
+        interpolate_fields(t, m, cd.f(f, a - 1 + c0), fchunk);
+        k_add_into<<<ew_blocks(ctx, m * nf), 256, 0, st>>>(m * nf, nxt.f(f, 1 + c0), fchunk);
         PTB_LAUNCH_CHECK(ctx);
       }
+    // state a-1: the initial state on rank 0, the previous rank's last state elsewhere
+    if (a == 1) cpy_state(nxt, 0, ini, 0);
+    if (world > 1) {
+      const bool has_next = rank + 1 < world && b <= N && L > 0, has_prev = rank > 0 && a <= N;
+      for (int f = 0; f < 4; ++f)
+        comm->shift_right(nxt.f(f, L), nf * sizeof(double), has_next, nxt.f(f, 0), nf * sizeof(double), has_prev, st);
+    }
     PTB_CUDA_CHECK(cudaEventRecord(e1, st));
-    // metric (outside the timed body): relative L2 over [u; udot] vs the serial fine reference
+    // metric (outside the timed body): L2 distance of [u; udot] to the serial fine run
     if (err_out) {
-      k_err_sums<<<unsigned(N + 1), 512, 0, st>>>(nf, nxt.f(0), nxt.f(1), ref.f(0), ref.f(1), sums);
+      PTB_CUDA_CHECK(cudaMemsetAsync(sums, 0, 2 * (chunk + 1) * sizeof(double), st));
+      k_err_sums<<<unsigned(L + 1), 512, 0, st>>>(nf, nxt.f(0), nxt.f(1), ref.f(0), ref.f(1), sums);
       PTB_LAUNCH_CHECK(ctx);
-      PTB_CUDA_CHECK(cudaMemcpyAsync(hs.data(), sums, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (world > 1) {
+        comm->allgather(sums, gsums, 2 * (chunk + 1) * sizeof(double), st);
+        PTB_CUDA_CHECK(cudaMemcpyAsync(hs.data(), gsums, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      } else {
+        PTB_CUDA_CHECK(cudaMemcpyAsync(hs.data(), sums, 2 * (L + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+      }
     }
     PTB_CUDA_CHECK(cudaStreamSynchronize(st));
     if (ms_out) {
@@ -614,23 +670,37 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t N, int
       PTB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
       ms_out[k - 1] = ms;
     }
-    if (err_out)  // relative to the initial state's norm: the layer drains the reference towards 0
-      for (size_t n = 0; n <= N; ++n)
-        err_out[size_t(k - 1) * (N + 1) + n] = hs[1] > 0 ? std::sqrt(hs[2 * n] / hs[1]) : std::sqrt(hs[2 * n]);
+    if (err_out)
+      for (size_t n = 0; n <= N; ++n) {  // state n from the rank owning coupling n (state 0: rank 0)
+        const size_t r = n == 0 ? 0 : (n - 1) / chunk, local = n == 0 ? 0 : n - (1 + r * chunk) + 1;
+        const double* h = hs.data() + 2 * (r * (chunk + 1) + local);
+        err_out[size_t(k - 1) * (N + 1) + n] = init_norm2 > 0 ? std::sqrt(h[0] / init_norm2) : std::sqrt(h[0]);
+      }
     std::swap(cur, nxt);
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (diverged_out) {
-    std::vector<int32_t> hf(N + 1);
-    PTB_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, (N + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> hf(L + 1);
+    PTB_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, (L + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     PTB_CUDA_CHECK(cudaStreamSynchronize(st));
     int32_t any = 0;
     for (auto x : hf) any |= x;
+    if (world > 1) {  // any rank
+      int32_t* d = reinterpret_cast<int32_t*>(sums);
+      std::vector<int32_t> gv(static_cast<size_t>(world));
+      PTB_CUDA_CHECK(cudaMemcpyAsync(d, &any, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      comm->allgather(d, gsums, sizeof(int32_t), st);
+      PTB_CUDA_CHECK(cudaMemcpyAsync(gv.data(), gsums, gv.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+      for (auto x : gv) any |= x;
+    }
     *diverged_out = any;
   }
-  if (states_out) {  // the last iterate, [field][state][point] with fields u, udot, px, py
-    PTB_CUDA_CHECK(cudaMemcpyAsync(states_out, cur.base, 4 * (N + 1) * nf * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (states_out) {  // the last iterate, [field][state][point]: own states a-1 .. b-1 (all on one GPU)
+    for (int f = 0; f < 4; ++f)
+      PTB_CUDA_CHECK(cudaMemcpyAsync(states_out + (size_t(f) * (N + 1) + (a - 1)) * nf, cur.f(f, 0),
+                                     (L + 1) * nf * sizeof(double), cudaMemcpyDeviceToHost, st));
     PTB_CUDA_CHECK(cudaStreamSynchronize(st));
   }
 }
@@ -761,8 +831,22 @@ ptb_status ptb_pml_parareal_run(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t,
     require(fine->ctx == coarse->ctx && t->ctx == fine->ctx, "pml parareal: objects of different contexts");
     DevGuard g(fine->ctx->device);
     std::lock_guard<std::recursive_mutex> lock(fine->ctx->mutex);
-    pml_parareal(fine, coarse, t, n_couplings, iterations, u0_host, udot0_host, rel_err_host, iteration_ms_host,
-                 states_host, diverged_host);
+    pml_parareal(fine, coarse, t, nullptr, n_couplings, iterations, u0_host, udot0_host, rel_err_host,
+                 iteration_ms_host, states_host, diverged_host);
+  });
+}
+
+ptb_status ptb_pml_parareal_run_sharded(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, ptb_comm* comm,
+                                        size_t n_couplings, int iterations, const double* u0_host,
+                                        const double* udot0_host, double* rel_err_host, double* iteration_ms_host,
+                                        double* states_host, int32_t* diverged_host) {
+  return guarded([&] {
+    require(fine && coarse && t && u0_host && udot0_host, "pml parareal: null argument");
+    require(fine->ctx == coarse->ctx && t->ctx == fine->ctx, "pml parareal: objects of different contexts");
+    DevGuard g(fine->ctx->device);
+    std::lock_guard<std::recursive_mutex> lock(fine->ctx->mutex);
+    pml_parareal(fine, coarse, t, comm_of(comm), n_couplings, iterations, u0_host, udot0_host, rel_err_host,
+                 iteration_ms_host, states_host, diverged_host);
   });
 }
 

@@ -189,3 +189,52 @@ def test_cxx_api_suite():
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "failed checks: 0" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pml_parareal_sharded_equals_single_gpu(world):
+    """The slice-sharded layered driver (loopback communicator: in-process ranks on cuda:0, the same
+    C++ all-gather / boundary-shift code as NCCL) is bitwise equal to one GPU."""
+    import threading
+
+    import paratime_b200 as B
+    from tests.test_pml_oracle import _small_parareal
+
+    s = _small_parareal(0, N=7, K=3)
+    nf, nc, W = s["nf"], s["nc"], s["W"]
+    gf, gc = B.Grid((nf, nf), (1 / nf, 1 / nf)), B.Grid((nc, nc), (1 / nc, 1 / nc))
+    zf = M.damping_profile(nf, W, 1 / nf, 1.0)
+    zc = M.damping_profile(nc, W // 4, 1 / nc, 1.0)
+    v0 = np.zeros_like(s["u0"])
+
+    def objects(c):
+        return (B.PmlPropagator(c, gf, s["c"], zf, zf, s["dtf"], s["mf"]),
+                B.PmlPropagator(c, gc, s["cc"], zc, zc, s["dtc"], s["mc"]), B.Transfer(c, gc, gf, 0))
+
+    c1 = B.Context(0)
+    single = B.pml_parareal_run(*objects(c1), s["N"], s["K"], s["u0"], v0, keep_states=True)
+    group = B.api.LoopbackGroup(world)
+    ctxs = [B.Context(0) for _ in range(world)]
+    objs = [objects(c) for c in ctxs]
+    comms = [group.comm(ctxs[r], r) for r in range(world)]
+    out, err = [None] * world, []
+
+    def work(r):
+        try:
+            out[r] = B.pml_parareal_run(*objs[r], s["N"], s["K"], s["u0"], v0, keep_states=True, comm=comms[r])
+        except Exception as e:  # pragma: no cover
+            err.append(e)
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not err, err
+    N = s["N"]
+    chunk = -(-N // world)
+    for r, o in enumerate(out):
+        assert np.array_equal(o["rel_err"], single["rel_err"])
+        a = 1 + r * chunk
+        b = min(N + 1, a + chunk)
+        assert np.array_equal(o["states"][:, a - 1:b], single["states"][:, a - 1:b])
