@@ -317,6 +317,10 @@ def main():
     if not args.no_parareal:
         parareal = guarded_section(lambda: parareal_iteration_times(B, ctx, rank, world, dist))
 
+    pml = None
+    if not args.no_pml:
+        pml = guarded_section(lambda: pml_section(B, ctx, tflops_peak, hbm_peak, rank, world, dist))
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "grid-pt updates/s", "n_gpus": world, "steps": args.steps,
@@ -335,8 +339,8 @@ def main():
                 line["cpu_baseline_parareal"] = cpu_parareal_iteration(2)
         if not args.no_sweep:
             line["cfg5_sweep"] = sweep(B, ctx, mode, tflops_peak, hbm_peak)
-        if not args.no_pml:
-            line["cfg4_pml"] = pml_section(B, ctx, tflops_peak, hbm_peak)
+        if pml is not None:
+            line["cfg4_pml"] = pml
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -509,12 +513,13 @@ def sweep(B, ctx, mode, tflops_peak, hbm_peak):
         del u, v, prop
     return out
 
-def pml_section(B, ctx, tflops_peak, hbm_peak):
+def pml_section(B, ctx, tflops_peak, hbm_peak, rank=0, world=1, dist=None):
     """BASELINE.json config 4 WITH its 32-cell absorbing layer (workloads.cfg4_pml; not in the
     reference).  (1) fine-stage throughput of the layered propagator on the
     per-GPU share of cfg4 at 8 GPUs (16 slices x 128 steps, 2048^2), device-resident, CUDA events;
     binding roofline with 40 B per point per 4-step pass (10 B/update) and 17 flops/update;
-    (2) s/iteration of plain parareal (ptb_pml_parareal_run, N = 128, K = 8, one GPU)."""
+    (2) s/iteration of plain parareal (N = 128, K = 8; slices sharded over the ranks with
+    ptb_pml_parareal_run_sharded when world > 1, max over ranks)."""
     import torch
 
     from workloads import cfg4_pml
@@ -545,13 +550,26 @@ def pml_section(B, ctx, tflops_peak, hbm_peak):
     f_hbm = ups * 10.0 / (hbm_peak * 1e9)
     f_fp64 = ups * FLOPS_PER_UPDATE / (tflops_peak * 1e12) if tflops_peak else None
     tr = B.Transfer(ctx, gc, gf, spec["interp"])
-    r = B.pml_parareal_run(fine, coarse, tr, spec["n_couplings"], spec["iterations"], u0, v0)
-    its = [float(x) for x in r["iteration_ms"]]
+    comm = None
+    if world > 1:
+        def bcast(raw):
+            obj = [raw]
+            dist.broadcast_object_list(obj, src=0)
+            return obj[0]
+
+        comm = B.api.Comm(ctx, rank, world, broadcast=bcast)
+    r = B.pml_parareal_run(fine, coarse, tr, spec["n_couplings"], spec["iterations"], u0, v0, comm=comm)
+    its = np.asarray(r["iteration_ms"], dtype=np.float64)
+    if world > 1:  # device time of each iteration, max over ranks
+        t_it = torch.as_tensor(its, device="cuda")
+        dist.all_reduce(t_it, op=dist.ReduceOp.MAX)
+        its = t_it.cpu().numpy()
+    its = [float(x) for x in its]
     return {"workload": "cfg4 + 32-cell absorbing layer (fine 2048^2 / coarse 256^2, layered-faulted medium)",
-            "fine_stage": {"batch": batch, "steps": spec["m_fine"], "ms": round(ms, 3), "updates_per_s": ups,
+            "fine_stage": {"per_gpu": True, "batch": batch, "steps": spec["m_fine"], "ms": round(ms, 3), "updates_per_s": ups,
                            "frac_hbm": f_hbm, "frac_fp64": f_fp64, "frac_binding": max(f_hbm, f_fp64 or 0.0),
                            "kernel": "k_pml_plain 70x54 register-column tiles (halo 5) + k_pml<layer> (halo 9), 4 steps per pass"},
-            "plain_parareal": {"N": spec["n_couplings"], "K": spec["iterations"],
+            "plain_parareal": {"N": spec["n_couplings"], "K": spec["iterations"], "ranks": world,
                                "s_per_iteration": float(np.median(its)) / 1e3, "iteration_ms": [round(x, 2) for x in its],
                                "max_err_last_rel_init": float(np.max(r["rel_err"][-1])), "diverged": r["diverged"]}}
 

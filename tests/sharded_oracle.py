@@ -108,3 +108,61 @@ def _shift(states, a, b, init):
     else:
         states[0] = init
     return states
+
+
+def pml_plain_sharded(u0, v0, kf, m_f, kc, m_c, t, N, K):
+    """The decomposition of csrc/pml.cu pml_parareal with slices block-sharded over the gloo ranks
+    (numpy, test infrastructure): own fine and coarse stages, one all-gather of the coarse payload
+    (C(R cur[n-1]) and R(fine_next[n])), the replicated coarse sweep, the own fine combine and the
+    last own state sent to the next rank.  Returns {global n: state} of the own states per iteration."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import paratime_np as P
+    from oracle import pml_np as M
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    chunk = -(-N // world)
+    a = min(N + 1, 1 + rank * chunk)
+    b = min(N + 1, a + chunk)
+    R = lambda s: tuple(P.restrict_field(f, t) for f in s)  # noqa: E731
+    I = lambda s: tuple(P.interpolate_field(f, t) for f in s)  # noqa: E731
+    Fp = lambda s: M.pml_steps(*s, kf, m_f)  # noqa: E731
+    Cp = lambda s: M.pml_steps(*s, kc, m_c)  # noqa: E731
+    z = np.zeros_like(u0)
+    init = (u0, v0, z, z)
+    cur, w = {}, R(init)
+    if a == 1:
+        cur[0] = init
+    for n in range(1, b):
+        w = Cp(w)
+        if n >= a - 1:
+            cur[n] = I(w)
+    hist = []
+    for _ in range(K):
+        fine_next = {n: Fp(cur[n - 1]) for n in range(a, b)}
+        payload = {n: (Cp(R(cur[n - 1])), R(fine_next[n])) for n in range(a, b)}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, payload)
+        allp = {}
+        for g in gathered:
+            allp.update(g)
+        w, d = R(init), {}
+        for n in range(1, N + 1):
+            g = Cp(w)
+            old, rf = allp[n]
+            d[n] = tuple(x - y for x, y in zip(g, old))
+            w = tuple(x + y for x, y in zip(rf, d[n]))
+        nxt = {n: tuple(x + y for x, y in zip(fine_next[n], I(d[n]))) for n in range(a, b)}
+        if a == 1:
+            nxt[0] = init
+        # boundary: the last own state to the next rank
+        if rank + 1 < world and b <= N:
+            dist.send(torch.from_numpy(np.stack(nxt[b - 1])), dst=rank + 1)
+        if rank > 0 and a <= N:
+            buf = torch.empty((4,) + u0.shape, dtype=torch.float64)
+            dist.recv(buf, src=rank - 1)
+            nxt[a - 1] = tuple(buf.numpy()[f].copy() for f in range(4))
+        hist.append(nxt)
+        cur = nxt
+    return hist
