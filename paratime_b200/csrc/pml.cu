@@ -12,18 +12,20 @@
 // row-major fields as everywhere else).  px, py must be zero wherever zx = zy = 0 (they stay
 // zero there); the kernel never touches them on tiles without layer cells.
 //
-// Kernel k_pml<LAYER>: overlapped temporal tiling.  A CTA owns a TY x TX output tile of one slice
-// and loads it with a halo of H = 2S+1 cells (periodic wrap, so any grid size works) into shared
-// memory, then runs up to S steps on chip: the initial half kick shrinks the valid region by one
-// cell, each step by 2 more in the layer (the auxiliary update reads new u neighbours, the force
-// reads new auxiliary neighbours) and by 1 elsewhere; after S steps the central tile is exact.  The carried velocity is the half
-// kick vh (as the FAST kernel), so the drift is pointwise.  Tiles with no layer cell in their
-// halo run the plain FAST step (bitwise the periodic kernels' arithmetic, bfast<true> below);
-// the two tile classes (fixed per propagator, listed at create) are two launches (LAYER = false /
-// true): plain tiles need a smaller halo and only the u and coefficient planes in shared memory
-// (two CTAs per SM, so one loads while the other computes).  Out of place (halo reads of other tiles' inputs):
-// passes ping-pong between the caller's buffers and the propagator's scratch.
+// Overlapped temporal tiling, 4 steps per pass, 70 x 54 output tiles in two classes fixed per
+// propagator (host tile lists built at create):
+//   k_pml<true> (layer tiles: damping within 9 cells) — the tile plus a halo of H = 2S+1 cells
+//     (periodic wrap, so any grid size works) in shared memory (u, px, py planes): the initial half
+//     kick shrinks the valid region by one cell, each step by 2 more (the auxiliary update reads
+//     new u neighbours, the force reads new auxiliary neighbours); after S steps the central tile
+//     is exact.  Branch-free stages over the padded box; undamped points take the plain arithmetic.
+//   k_pml_plain (all other tiles) — halo S+1, the periodic FAST step on register columns (below),
+//     bitwise the periodic kernels' arithmetic (bfast<true>); two CTAs per SM.
+// The carried velocity is the half kick vh (as the FAST kernel), so the drift is pointwise.  Out
+// of place (halo reads of other tiles' inputs): passes ping-pong between the caller's buffers and
+// the propagator's scratch.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 
@@ -423,13 +425,15 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
   a.zy = a.qx + nx;
   a.ay = a.zy + ny;
   a.qy = a.ay + ny;
-  static bool attr = false;
-  if (!attr) {
+  // the dynamic shared-memory opt-in is per device
+  static std::atomic<uint64_t> attr_done{0};
+  const uint64_t bit = uint64_t(1) << (ctx->device & 63);
+  if (!(attr_done.load() & bit)) {
     PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml_plain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(pml_plain_smem())));
     PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(pml_smem<true>())));
-    attr = true;
+    attr_done.fetch_or(bit);
   }
   require(batch <= 65535, "pml propagate: at most 65535 slices per call");
   int cur = 0;
