@@ -276,8 +276,7 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
 // instead of 8 for the generic kernel.  Same arithmetic as k_pml<false> and the periodic kernels.
 constexpr int PR = 20;
 __global__ void __launch_bounds__(256, 2) k_pml_plain(const PmlArgs a) {
-  using G = Geo<PTY, PTX, HP, 256>;
-  constexpr int EX = G::EX, EY = G::EY, H = HP, PAD = EX + 1, PLANE = EY * EX + 2 * PAD;
+  constexpr int EX = PTX + 2 * HP, EY = PTY + 2 * HP, H = HP, PAD = EX + 1, PLANE = EY * EX + 2 * PAD;
   static_assert(EX == 64 && EY == 4 * PR, "plain tile geometry");
   extern __shared__ double sm[];
   double* us = sm + PAD;
@@ -352,8 +351,8 @@ __global__ void __launch_bounds__(256, 2) k_pml_plain(const PmlArgs a) {
   }
 }
 size_t pml_plain_smem() {
-  using G = Geo<PTY, PTX, HP, 256>;
-  return size_t(2 * (G::EY * G::EX + 2 * (G::EX + 1))) * sizeof(double) + (G::EX + G::EY) * sizeof(int);
+  constexpr int EX = PTX + 2 * HP, EY = PTY + 2 * HP;
+  return size_t(2 * (EY * EX + 2 * (EX + 1))) * sizeof(double) + (EX + EY) * sizeof(int);
 }
 
 constexpr int kPlainThreads = 256, kLayerThreads = 512;
