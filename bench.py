@@ -27,7 +27,7 @@ from pathlib import Path
 
 import numpy as np
 
-from workloads import cfg5_medium, cfg5_pulses
+from workloads import cfg5_medium, cfg5_pulses, cfg5_pulses_device
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -36,31 +36,6 @@ METRIC = "fine-propagator fp64 grid-pt updates/s"
 ITER_CONFIGS = (1, 2, 3, 4)  # BASELINE configs timed for seconds per parareal iteration
 FLOPS_PER_UPDATE = 17  # Laplacian 9, x c^2 1, u-update 4, udot-update 3
 STEPS_PER_COUPLING = 64
-
-
-def medium(n: int, seed: int) -> np.ndarray:
-    """cfg5 medium: c = 0.75 + 0.25 S/max|S|, S = sum of 8 sinusoids, wavenumbers 1..4."""
-    rng = np.random.default_rng(seed)
-    y, x = np.meshgrid(np.arange(n) / n, np.arange(n) / n, indexing="ij")
-    s = np.zeros((n, n))
-    for _ in range(8):
-        ky, kx = rng.integers(1, 5, 2)
-        s += rng.uniform(0.2, 1.0) * np.sin(2 * np.pi * (ky * y + kx * x) + rng.uniform(0, 2 * np.pi))
-    return 0.75 + 0.25 * s / np.max(np.abs(s))
-
-
-def pulses(n: int, batch: int, seed: int) -> np.ndarray:
-    """cfg5 initial states: exp(-w |x - x0|^2), x0 ~ U[0,1)^2 (periodic distance), w ~ U[200, 2000]."""
-    rng = np.random.default_rng(seed)
-    ax = np.arange(n) / n
-    out = np.empty((batch, n, n))
-    for b in range(batch):
-        y0, x0 = rng.random(2)
-        w = rng.uniform(200, 2000)
-        dy = np.minimum(np.abs(ax - y0), 1 - np.abs(ax - y0))[:, None]
-        dx = np.minimum(np.abs(ax - x0), 1 - np.abs(ax - x0))[None, :]
-        out[b] = np.exp(-w * (dy * dy + dx * dx))
-    return out
 
 
 class ClockSampler:
@@ -135,9 +110,9 @@ def run_reference(args, rank, world):
     cores = os.cpu_count() or 1
     sample_slices = cores  # one slice per std::thread worker (parareal.cpp:25-47 partition)
     g = Grid((n, n), (1.0 / n, 1.0 / n))
-    c = medium(n, 7)
+    c = cfg5_medium(n)
     dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
-    u0 = pulses(n, sample_slices, 11)
+    u0 = cfg5_pulses(n, sample_slices)
     v0 = np.zeros_like(u0)
     steps = max(1, args.ref_steps)
     times = []
@@ -164,47 +139,23 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(n, steps=8):
-    """Same as the reference arm, small and quick, for the `cpu_baseline` key (rank 0, N=1)."""
-    try:
-        from oracle import refbind
-        from oracle.paratime_np import Grid
-
-        if not refbind.LIB_PATH.exists():
-            return None
-        cores = os.cpu_count() or 1
-        g = Grid((n, n), (1.0 / n, 1.0 / n))
-        c = medium(n, 7)
-        dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
-        u0 = pulses(n, cores, 11)
-        v0 = np.zeros_like(u0)
-        refbind.propagate(u0[:1], v0[:1], c, g, dt, 1, workers=1)  # warm
-        t0 = time.perf_counter()
-        refbind.propagate(u0, v0, c, g, dt, steps, workers=cores)
-        dt_s = time.perf_counter() - t0
-        return {"value": cores * n * n * steps / dt_s, "unit": "grid-pt updates/s", "cores": cores,
-                "kind": "reference",
-                "sample": f"{cores} slices of {n}^2 x {steps} steps through the reference's propagate_coupling "
-                          f"(oracle/_ref, propagator.cpp verbatim) on std::thread x{cores}"}
-    except Exception as e:  # pragma: no cover
-        return {"value": None, "error": str(e)}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--grid", type=int, default=2048)
-    ap.add_argument("--batch", type=int, default=64, help="slices per GPU")
+    ap.add_argument("--grid", type=int, default=4096)
+    ap.add_argument("--batch", type=int, default=512, help="slices per GPU")
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
     ap.add_argument("--ref-steps", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-batch", type=int, default=128, help="slices per e2e call (host-pinned state)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the cfg5 grid sweep")
     ap.add_argument("--no-parareal", action="store_true", help="skip the s/iteration measurement")
     ap.add_argument("--no-pml", action="store_true", help="skip the cfg4 absorbing-layer section")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference legs (parity check too)")
     args = ap.parse_args()
 
     rank, world, local = dist_env()
@@ -226,15 +177,24 @@ def main():
     n, batch = args.grid, args.batch
     mode = B.FAST if args.mode == "fast" else B.EXACT
     ctx = B.Context(local)
-    c = medium(n, 7)
+    c = cfg5_medium(n)
     dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
     grid = B.Grid((n, n), (1.0 / n, 1.0 / n))
     prop = B.Propagator(ctx, grid, c, dt, STEPS_PER_COUPLING)
-    # each rank owns its own contiguous block of slices (seeded by global slice index)
-    u_host = pulses(n, batch, 1000 + rank)
-    u = torch.as_tensor(u_host, device=f"cuda:{local}")
+    # each rank owns its own contiguous block of slices, seeded by rank; generated on the device
+    # (a 4096^2 x 512 batch is 69 GB per field)
+    seed = 20261019 + 50 + 1000 * rank
+    u = torch.empty((batch, n, n), dtype=torch.float64, device=f"cuda:{local}")
+    cfg5_pulses_device(n, batch, u, seed)
     v = torch.zeros_like(u)
     stream = torch.cuda.current_stream()
+    eb = min(args.e2e_batch, batch)
+    e2e_host = None
+    if not args.no_e2e:  # pinned host copies of the first e2e slices (inputs of the e2e leg)
+        e2e_host = (u[:eb].cpu().pin_memory(), torch.zeros((eb, n, n), dtype=torch.float64).pin_memory())
+    cpu_leg = rank == 0 and world == 1 and not args.no_cpu
+    check_idx = parity_slices(batch, os.cpu_count() or 1) if cpu_leg else []
+    u_check0 = u[check_idx].cpu().numpy() if cpu_leg else None
 
     def step():
         prop.propagate(u, v, mode=mode)
@@ -265,14 +225,25 @@ def main():
     ms_per_step = ms / args.steps
     finite = bool(torch.isfinite(u).all().item() and torch.isfinite(v).all().item())
 
+    # parity of the timed kernel plan: one more step of the SAME batch from regenerated inputs;
+    # the checked slices go to the reference's propagate_coupling (cpu_baseline leg below)
+    u_check1 = None
+    if cpu_leg:
+        cfg5_pulses_device(n, batch, u, seed)
+        v.zero_()
+        step()
+        torch.cuda.synchronize()
+        u_check1 = (u[check_idx].cpu().numpy(), v[check_idx].cpu().numpy())
+
     # roofline: live fp64 FMA peak on this GPU; dominant kernel = the wavefront K1 pass
     tflops_peak, _ = probe_fp64(ctx)
     per_launch_ms = ms / max(launches, 1)
     launches_per_step = launches / args.steps
     steps_per_launch = STEPS_PER_COUPLING / launches_per_step
-    flops_per_launch = batch * n * n * steps_per_launch * FLOPS_PER_UPDATE
+    slices_per_launch = batch * steps_per_launch / STEPS_PER_COUPLING  # chunked batches: fewer per launch
+    flops_per_launch = slices_per_launch * n * n * steps_per_launch * FLOPS_PER_UPDATE
     achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
-    hbm_bytes_per_launch = batch * n * n * 40.0  # read u, udot, coef; write u, udot (8 B each)
+    hbm_bytes_per_launch = slices_per_launch * n * n * 40.0  # read u, udot, coef; write u, udot (8 B each)
     plan = prop.plan(batch, mode)
     traffic = ncu_traffic(n, batch, args.mode, plan)
 
@@ -297,7 +268,10 @@ def main():
     roofline = {"bound": binding, "achieved": main_["achieved"], "peak": main_["peak"], "unit": main_["unit"],
                 "frac": main_["frac"], "traffic": traffic and traffic["dram_bytes_per_launch"],
                 "traffic_source": traffic and traffic["source"], "kernel": plan, "per_launch_ms": per_launch_ms,
-                "steps_per_launch": steps_per_launch, "fp64": fp64, "hbm": hbm}
+                "steps_per_launch": steps_per_launch, "slices_per_launch": slices_per_launch, "fp64": fp64,
+                "hbm": hbm}
+    del u, v
+    torch.cuda.empty_cache()
 
     def guarded_section(fn):
         """Secondary measurements never cost the headline line: at N > 1 a failure in the
@@ -310,9 +284,9 @@ def main():
             return {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
     e2e = None
-    if not args.no_e2e:
-        e2e = guarded_section(lambda: measure_e2e(B, prop, u_host, mode, args.e2e_steps, local, dist, world))
-    del u, v
+    if e2e_host is not None:
+        e2e = guarded_section(lambda: measure_e2e(B, prop, e2e_host, mode, args.e2e_steps, local, dist, world))
+        del e2e_host
     parareal = None
     if not args.no_parareal:
         parareal = guarded_section(lambda: parareal_iteration_times(B, ctx, rank, world, dist))
@@ -331,12 +305,18 @@ def main():
             "roofline": roofline,
             "clocks": clocks.summary(),
             "e2e": e2e,
-            "parareal": parareal,
         }
-        if world == 1:
-            line["cpu_baseline"] = cpu_baseline_sample(n)
+        if parareal is not None:  # compact top-level keys (the driver keeps the line's head)
+            for k, r in parareal.items():
+                line[f"s_per_iteration_{k}"] = round(r["s_per_iteration"], 6)
+        if cpu_leg:
+            base, par = cpu_baseline_and_parity(n, c, dt, check_idx, u_check0, u_check1)
+            line["parity"] = par
+            line["cpu_baseline"] = base
             if parareal is not None:
-                line["cpu_baseline_parareal"] = cpu_parareal_iteration(2)
+                line["cpu_baseline_parareal"] = {k: cpu_parareal_iteration(k) for k in ("cfg1", "cfg2", "cfg3", "cfg4r")}
+                line["cpu_host"] = host_cpu_model()
+        line["parareal"] = parareal
         if not args.no_sweep:
             line["cfg5_sweep"] = sweep(B, ctx, mode, tflops_peak, hbm_peak)
         if pml is not None:
@@ -344,6 +324,52 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def parity_slices(batch, cores):
+    """Slices checked against the reference (first, last, evenly spread; one per host core)."""
+    k = max(2, min(batch, cores))
+    return sorted({int(round(i * (batch - 1) / (k - 1))) for i in range(k)})
+
+
+def cpu_baseline_and_parity(n, c, dt, idx, u0, got):
+    """The reference's propagate_coupling (oracle/_ref, propagator.cpp verbatim; parareal.cpp:25-47
+    thread partition) on the checked slices of the headline batch: timed on all host cores (the
+    `cpu_baseline`), and its outputs compared with the device's for the SAME slices under the
+    SAME launch plan as the timed region (north star: <= 1e-12 relative L2 over [u; udot])."""
+    from oracle import refbind
+    from oracle.paratime_np import Grid
+
+    if not refbind.LIB_PATH.exists():
+        return {"value": None, "error": "oracle/_ref not built"}, {"checked": False}
+    cores = os.cpu_count() or 1
+    g = Grid((n, n), (1.0 / n, 1.0 / n))
+    v0 = np.zeros_like(u0)
+    t0 = time.perf_counter()
+    ru, rv, div = refbind.propagate(u0, v0, c, g, dt, STEPS_PER_COUPLING, workers=cores)
+    el = time.perf_counter() - t0
+    rel = []
+    for b in range(len(idx)):
+        num = np.concatenate([got[0][b].ravel() - ru[b].ravel(), got[1][b].ravel() - rv[b].ravel()])
+        den = np.concatenate([ru[b].ravel(), rv[b].ravel()])
+        rel.append(float(np.linalg.norm(num) / np.linalg.norm(den)))
+    base = {"value": len(idx) * n * n * STEPS_PER_COUPLING / el, "unit": "grid-pt updates/s", "cores": cores,
+            "kind": "reference",
+            "sample": f"{len(idx)} slices of the headline batch ({n}^2 x {STEPS_PER_COUPLING} steps each) through the "
+                      f"reference's propagate_coupling (oracle/_ref, propagator.cpp verbatim) on std::thread x{cores}"}
+    par = {"checked": True, "slices": idx, "max_rel_l2": max(rel), "tol": 1e-12, "ok": max(rel) <= 1e-12,
+           "against": "oracle/_ref propagate_coupling, same inputs, device run under the timed plan"}
+    return base, par
+
+
+def host_cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.lower().startswith("model name"):
+                return {"model": line.split(":", 1)[1].strip(), "cores": os.cpu_count()}
+    except OSError:
+        pass
+    return {"model": None, "cores": os.cpu_count()}
 
 
 def ncu_traffic(n, batch, mode, plan):
@@ -390,16 +416,19 @@ def parareal_iteration_times(B, ctx, rank, world, dist, cfgs=ITER_CONFIGS):
     return out
 
 
-def cpu_parareal_iteration(cfg=2):
+def cpu_parareal_iteration(cfg="cfg2"):
     """The reference's theta_parareal (oracle/_ref: parareal.cpp verbatim, Procrustes on LAPACK)
-    on the host cores for one BASELINE config: (wall - serial fine reference) / K."""
+    on the host cores for one BASELINE config: (wall - serial fine reference) / K.  "cfg4r" is
+    config 4's first 16 couplings (workloads.cfg4_subset, K = 2): the full config 4 would take
+    ~15 min per iteration here; its per-iteration cost is reported scaled by 128/16 (the fine
+    stage, snapshots and sweep are linear in N)."""
     try:
         import workloads as W
         from oracle import refbind
 
         if not refbind.LIB_PATH.exists():
             return None
-        spec, cf, cc, u0, v0 = W.CONFIGS[cfg]()
+        spec, cf, cc, u0, v0 = W.cfg4_subset() if cfg == "cfg4r" else W.CONFIGS[int(cfg[3:])]()
         cores = os.cpu_count() or 1
         rs = refbind.RunSpec()
         rs.dim = 2
@@ -420,10 +449,13 @@ def cpu_parareal_iteration(cfg=2):
         ref_s = time.perf_counter() - t0
         r = refbind.parareal_run(rs, cf, cc, u0, v0)
         wall = r["wall_ms"] / 1e3
-        return {"value": (wall - ref_s) / spec["iterations"], "unit": "s/iteration", "cores": cores,
-                "kind": "reference", "config": f"cfg{cfg}",
-                "sample": f"theta_parareal on cfg{cfg} (K={spec['iterations']}, N={spec['n_couplings']}), "
-                          f"wall {wall:.2f} s minus serial fine reference {ref_s:.2f} s, std::thread x{cores}"}
+        out = {"value": (wall - ref_s) / spec["iterations"], "unit": "s/iteration", "cores": cores,
+               "kind": "reference", "config": cfg,
+               "sample": f"theta_parareal on {cfg} (K={spec['iterations']}, N={spec['n_couplings']}), "
+                         f"wall {wall:.2f} s minus serial fine reference {ref_s:.2f} s, std::thread x{cores}"}
+        if cfg == "cfg4r":
+            out["cfg4_estimate_s_per_iteration"] = out["value"] * 128 / spec["n_couplings"]
+        return out
     except Exception as e:  # pragma: no cover
         return {"value": None, "error": str(e)}
 
@@ -438,25 +470,23 @@ def probe_fp64(ctx):
     return tf.value, ms.value
 
 
-def measure_e2e(B, prop, u_host, mode, steps, local, dist, world):
-    """Same metric through the C-ABI host-buffer call: H2D inputs, K1, D2H results per step."""
+def measure_e2e(B, prop, host, mode, steps, local, dist, world):
+    """Same metric through the C-ABI host-buffer call (ptb_propagate_batch_host): every step
+    copies the slices' state host->device, propagates, and copies it back device->host, in
+    place in the pinned host buffers (the call pipelines chunks over three streams)."""
     import ctypes
 
     import torch
 
-    batch = u_host.shape[0]
-    n = u_host.shape[1]
-    uh = torch.from_numpy(u_host).pin_memory()
-    vh = torch.zeros_like(uh).pin_memory()
-    ou = torch.empty_like(uh).pin_memory()
-    ov = torch.empty_like(uh).pin_memory()
+    uh, vh = host
+    batch, n = uh.shape[0], uh.shape[1]
     flags = np.zeros(batch, dtype=np.int32)
     dp = ctypes.POINTER(ctypes.c_double)
 
     def call():
         B.api.check(B.lib().ptb_propagate_batch_host(
             prop.h, ctypes.c_size_t(batch), ctypes.cast(uh.data_ptr(), dp), ctypes.cast(vh.data_ptr(), dp),
-            ctypes.cast(ou.data_ptr(), dp), ctypes.cast(ov.data_ptr(), dp),
+            ctypes.cast(uh.data_ptr(), dp), ctypes.cast(vh.data_ptr(), dp),
             flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.c_int(mode)))
 
     call()
@@ -474,7 +504,8 @@ def measure_e2e(B, prop, u_host, mode, steps, local, dist, world):
     value = world * batch * n * n * STEPS_PER_COUPLING * steps / el
     return {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": int(2 * uh.numel() * 8),
             "d2h_bytes_per_step": int(2 * uh.numel() * 8 + batch * 4), "ms_per_step": el / steps * 1e3,
-            "api": "ptb_propagate_batch_host (pinned host buffers, 3-stream chunked copies)"}
+            "slices_per_call": batch, "grid": n,
+            "api": "ptb_propagate_batch_host (pinned host buffers, in place; 3-stream chunked copies)"}
 
 
 def sweep(B, ctx, mode, tflops_peak, hbm_peak):

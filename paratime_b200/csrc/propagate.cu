@@ -1185,6 +1185,15 @@ void wave_pass(ptb_context* ctx, cudaStream_t st, int S, const StepParams& p, si
   }
 }
 
+// slices per ping-pong chunk of the context scratch (see wave_propagate)
+size_t scratch_chunk(size_t n, size_t batch) {
+  static const size_t cap = [] {
+    const char* e = std::getenv("PTB_SCRATCH_MIB");
+    return (e && std::atoll(e) > 0 ? size_t(std::atoll(e)) : size_t(16384)) << 20;
+  }();
+  return std::min(batch, std::max<size_t>(1, cap / (2 * n * sizeof(double))));
+}
+
 template <bool EXACT>
 void wave_propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double* v, int32_t* flags,
                     const LaunchSlot& slot) {
@@ -1198,22 +1207,33 @@ void wave_propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, d
   while (rem >= 8) { passes.push_back(8); rem -= 8; }
   for (int s : {4, 2, 1})
     if (rem >= size_t(s)) { passes.push_back(s); rem -= size_t(s); }
-  double* su = slot.su ? slot.su : static_cast<double*>(ctx->scratch[0].get(batch * n * sizeof(double)));
-  double* sv = slot.sv ? slot.sv : static_cast<double*>(ctx->scratch[1].get(batch * n * sizeof(double)));
-  const double *ci = u, *cvi = v;
-  for (size_t k = 0; k < passes.size(); ++k) {
-    const bool to_scratch = (k % 2) == 0;
-    double* uo = to_scratch ? su : u;
-    double* vo = to_scratch ? sv : v;
-    wave_pass<EXACT>(ctx, slot.stream, passes[k], p, batch, ci, cvi, uo, vo, coef,
-                     k + 1 == passes.size() ? flags : nullptr);
-    ci = uo;
-    cvi = vo;
-  }
-  if (ci != u) {
-    const size_t total = batch * n;
-    k_copy2<<<grid_for(ctx, total, 256), 256, 0, slot.stream>>>(total, su, sv, u, v);
-    PTB_LAUNCH_CHECK(ctx);
+  // The context scratch holds at most `chunk` slices (PTB_SCRATCH_MIB, default 16 GiB for the
+  // pair): larger batches run the whole coupling chunk by chunk, each chunk ping-ponging between
+  // its own slices and the shared scratch, so a batch can use ~all of HBM for its state (cfg5
+  // 4096^2 x 512 slices: 137 GB of state + 17 GB of scratch).  A slice's arithmetic does not
+  // depend on the plan, so chunking never changes results.
+  const size_t chunk = slot.su ? batch : scratch_chunk(n, batch);
+  double* su = slot.su ? slot.su : static_cast<double*>(ctx->scratch[0].get(chunk * n * sizeof(double)));
+  double* sv = slot.sv ? slot.sv : static_cast<double*>(ctx->scratch[1].get(chunk * n * sizeof(double)));
+  for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+    const size_t nb = std::min(chunk, batch - b0);
+    double* hu = u + b0 * n;
+    double* hv = v + b0 * n;
+    const double *ci = hu, *cvi = hv;
+    for (size_t k = 0; k < passes.size(); ++k) {
+      const bool to_scratch = (k % 2) == 0;
+      double* uo = to_scratch ? su : hu;
+      double* vo = to_scratch ? sv : hv;
+      wave_pass<EXACT>(ctx, slot.stream, passes[k], p, nb, ci, cvi, uo, vo, coef,
+                       k + 1 == passes.size() && flags ? flags + b0 : nullptr);
+      ci = uo;
+      cvi = vo;
+    }
+    if (ci != hu) {
+      const size_t total = nb * n;
+      k_copy2<<<grid_for(ctx, total, 256), 256, 0, slot.stream>>>(total, su, sv, hu, hv);
+      PTB_LAUNCH_CHECK(ctx);
+    }
   }
 }
 
@@ -1289,6 +1309,8 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
     return std::string("k_cluster<") + m + "> x1 launch, cluster of " + std::to_string(cs) + " CTAs x " +
            std::to_string(CL_THREADS) + " threads per slice";
   if (p.dim != 2) return std::string("k_stream_drift/kick<") + m + "> 2 launches per step";
+  const size_t full_batch = batch;
+  batch = scratch_chunk(pr->n, batch);
   std::string out;
   size_t rem = steps;
   int passes = 0;
@@ -1306,7 +1328,8 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
         case 2: pl = plan_wave2<2>(pr->ctx, p.ny, p.nx, batch); break;
         default: pl = plan_wave2<1>(pr->ctx, p.ny, p.nx, batch); break;
       }
-      d = "k_wave2<" + std::to_string(S) + "," + std::to_string(pl.W) + ">" + (pl.full ? " full-row" : "");
+      d = "k_wave2<" + std::to_string(S) + "," + std::to_string(pl.W) + ">" + (pl.full ? " full-row" : "") +
+          ((wave2_variant(p, pl.full) & 2) ? " ry1" : "");
       d += " grid " + std::to_string(batch) + "x" + std::to_string(pl.strips) + "x" + std::to_string(pl.nrb);
     } else {
       const WavePlan pl = plan_wave(pr->ctx, p.ny, p.nx, S, batch);
@@ -1316,6 +1339,9 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
     out += (out.empty() ? "" : " + ") + std::to_string(k) + " x " + d;
   }
   if (passes % 2) out += " + k_copy2";
+  if (batch < full_batch)
+    out = "(" + out + ") per chunk of " + std::to_string(batch) + " slices x " +
+          std::to_string((full_batch + batch - 1) / batch);
   return out;
 }
 

@@ -158,4 +158,44 @@ def cfg5_pulses(n, batch, seed=SEED + 50):
     return out
 
 
+def cfg4_subset(n_couplings=16, iterations=2, tol=1e-4):
+    """BASELINE config 4 (periodic, 2048^2 / 256^2, m_F = 128, m_C = 8) over its first
+    `n_couplings` coupling intervals (T = n_couplings / 128, same dt_com and inputs): small enough
+    for the CPU reference (parity tests, the CPU s/iteration sample), and 3 N_c x r = 196608 x r
+    > 4M corrector entries, so the device sweep takes its large-corrector branch as the full
+    config does."""
+    spec, cf, cc, u0, v0 = cfg4(tol=tol)
+    spec = dict(spec)
+    spec["n_couplings"] = n_couplings
+    spec["T"] = n_couplings * spec["dt_com"]
+    spec["iterations"] = iterations
+    return spec, cf, cc, u0, v0
+
+
 CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4}
+
+
+def cfg5_pulse_params(batch, seed=SEED + 50):
+    """(y0, x0, w) per slice for cfg5_pulses_device (same draws, same order as cfg5_pulses)."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((batch, 3))
+    for b in range(batch):
+        out[b, :2] = rng.random(2)
+        out[b, 2] = rng.uniform(200, 2000)
+    return out
+
+
+def cfg5_pulses_device(n, batch, out, seed=SEED + 50):
+    """cfg5 initial states written straight into the device tensor `out` (batch, n, n), for
+    batches too large to stage on the host (4096^2 x 512 slices = 69 GB per field):
+    exp(-w dy^2) * exp(-w dx^2) with periodic distances.  Deterministic (same bits on every
+    call), so a parity check can regenerate the inputs and hand the same slices to the
+    reference."""
+    import torch
+
+    ax = torch.arange(n, dtype=torch.float64, device=out.device) / n
+    for b, (y0, x0, w) in enumerate(cfg5_pulse_params(batch, seed)):
+        dy = torch.minimum((ax - y0).abs(), 1 - (ax - y0).abs())
+        dx = torch.minimum((ax - x0).abs(), 1 - (ax - x0).abs())
+        torch.outer(torch.exp(-w * dy * dy), torch.exp(-w * dx * dx), out=out[b])
+    return out
