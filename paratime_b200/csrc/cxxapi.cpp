@@ -19,6 +19,7 @@
 #include <istream>
 #include <ostream>
 #include <map>
+#include <numeric>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -141,88 +142,80 @@ int scheme_id(GradientScheme s) { return static_cast<int>(s); }
 }  // namespace
 
 // ------------------------------------------------------------------------ grid.hpp
+//
+// Host value types.  The checks and their messages are the reference's contract (grid.cpp:13-119):
+// the same std::invalid_argument text is what CHECK_THROWS_AS cases and callers see.
+
+namespace {
+void require(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+bool positive_finite(double v) { return v > 0.0 && std::isfinite(v); }
+
+// elementwise a (op) b on both fields of a state; grids must agree
+template <typename Op>
+WaveState combine(const WaveState& a, const WaveState& b, const char* what, Op op) {
+  check_same_grid(a.grid, b.grid, what);
+  WaveState o = a;
+  std::transform(o.u.begin(), o.u.end(), b.u.begin(), o.u.begin(), op);
+  std::transform(o.udot.begin(), o.udot.end(), b.udot.begin(), o.udot.begin(), op);
+  return o;
+}
+}  // namespace
 
 Grid::Grid(std::vector<std::size_t> points_per_axis, std::vector<double> spacing)
     : n_(std::move(points_per_axis)), h_(std::move(spacing)) {
-  if (n_.empty() || n_.size() > 2 || n_.size() != h_.size())
-    throw std::invalid_argument("Grid: dimension must be 1 or 2 with matching spacing");
-  for (std::size_t a = 0; a < n_.size(); ++a) {
-    if (n_[a] < 4) throw std::invalid_argument("Grid: need at least 4 points per axis");
-    if (!(h_[a] > 0.0) || !std::isfinite(h_[a])) throw std::invalid_argument("Grid: spacing must be positive");
+  require(!n_.empty() && n_.size() <= 2 && n_.size() == h_.size(), "Grid: dimension must be 1 or 2 with matching spacing");
+  for (std::size_t a = 0; a < n_.size(); ++a) {  // axis by axis: the first bad axis names the error
+    require(n_[a] >= 4, "Grid: need at least 4 points per axis");
+    require(positive_finite(h_[a]), "Grid: spacing must be positive");
   }
 }
 
 std::size_t Grid::size() const {
-  std::size_t s = 1;
-  for (std::size_t v : n_) s *= v;
-  return s;
+  return std::accumulate(n_.begin(), n_.end(), std::size_t(1), std::multiplies<std::size_t>());
 }
 
-double Grid::cell_volume() const {
-  double v = 1.0;
-  for (double h : h_) v *= h;
-  return v;
-}
+double Grid::cell_volume() const { return std::accumulate(h_.begin(), h_.end(), 1.0, std::multiplies<double>()); }
 
 bool Grid::operator==(const Grid& o) const { return n_ == o.n_ && h_ == o.h_; }
 
 WaveState::WaveState(Grid g, std::vector<double> u_in, std::vector<double> udot_in)
     : grid(std::move(g)), u(std::move(u_in)), udot(std::move(udot_in)) {
-  if (u.size() != grid.size() || udot.size() != grid.size())
-    throw std::invalid_argument("WaveState: field size does not match grid");
+  require(u.size() == grid.size() && udot.size() == grid.size(), "WaveState: field size does not match grid");
 }
 
 WaveState::WaveState(Grid g) : grid(std::move(g)), u(grid.size(), 0.0), udot(grid.size(), 0.0) {}
 
 bool WaveState::finite() const { return all_finite(u) && all_finite(udot); }
 
-WaveState operator+(const WaveState& a, const WaveState& b) {
-  check_same_grid(a.grid, b.grid, "state add");
-  WaveState o = a;
-  for (size_t i = 0; i < o.u.size(); ++i) {
-    o.u[i] += b.u[i];
-    o.udot[i] += b.udot[i];
-  }
-  return o;
-}
+WaveState operator+(const WaveState& a, const WaveState& b) { return combine(a, b, "state add", std::plus<double>()); }
 
 WaveState operator-(const WaveState& a, const WaveState& b) {
-  check_same_grid(a.grid, b.grid, "state subtract");
-  WaveState o = a;
-  for (size_t i = 0; i < o.u.size(); ++i) {
-    o.u[i] -= b.u[i];
-    o.udot[i] -= b.udot[i];
-  }
-  return o;
+  return combine(a, b, "state subtract", std::minus<double>());
 }
 
 WaveState operator*(double s, const WaveState& a) {
   WaveState o = a;
-  for (size_t i = 0; i < o.u.size(); ++i) {
-    o.u[i] *= s;
-    o.udot[i] *= s;
-  }
+  for (auto* f : {&o.u, &o.udot})
+    for (double& x : *f) x *= s;
   return o;
 }
 
 SpeedField::SpeedField(Grid g, std::vector<double> c_in) : grid(std::move(g)), c(std::move(c_in)) {
-  if (c.size() != grid.size()) throw std::invalid_argument("SpeedField: field size does not match grid");
-  for (double v : c)
-    if (!(v > 0.0) || !std::isfinite(v))
-      throw std::invalid_argument("SpeedField: wave speed must be strictly positive and finite");
+  require(c.size() == grid.size(), "SpeedField: field size does not match grid");
+  require(std::all_of(c.begin(), c.end(), positive_finite), "SpeedField: wave speed must be strictly positive and finite");
 }
 
 GridTransfer::GridTransfer(Grid coarse_in, Grid fine_in, InterpKind kind_in)
     : coarse(std::move(coarse_in)), fine(std::move(fine_in)), kind(kind_in) {
-  if (coarse.dim() != fine.dim()) throw std::invalid_argument("GridTransfer: dimension mismatch");
+  require(coarse.dim() == fine.dim(), "GridTransfer: dimension mismatch");
   for (int a = 0; a < coarse.dim(); ++a) {
-    const size_t nc = coarse.points(a), nf = fine.points(a);
-    if (nf % nc != 0)
-      throw std::invalid_argument("GridTransfer: fine points must be an integer multiple of coarse points");
+    const std::size_t nc = coarse.points(a), nf = fine.points(a);
+    require(nf % nc == 0, "GridTransfer: fine points must be an integer multiple of coarse points");
     ratio.push_back(nf / nc);
     const double ec = coarse.extent(a), ef = fine.extent(a);
-    if (std::abs(ec - ef) > 1e-12 * std::max(ec, ef))
-      throw std::invalid_argument("GridTransfer: coarse and fine extents differ; grids are not nested");
+    require(std::abs(ec - ef) <= 1e-12 * std::max(ec, ef), "GridTransfer: coarse and fine extents differ; grids are not nested");
   }
 }
 
@@ -259,34 +252,6 @@ WaveState interpolate_state(const WaveState& s, const GridTransfer& t) {
 SpeedField resize_speed(const SpeedField& fine_speed, const Grid& coarse) {
   const GridTransfer t(coarse, fine_speed.grid, InterpKind::linear);
   return SpeedField(coarse, restrict_field(fine_speed.c, t));
-}
-
-std::vector<double> bilinear_resample(const std::vector<double>& src, std::size_t sny, std::size_t snx,
-                                      std::size_t dny, std::size_t dnx) {
-  if (src.size() != sny * snx) throw std::invalid_argument("bilinear_resample: field size does not match source shape");
-  if (!sny || !snx || !dny || !dnx) throw std::invalid_argument("bilinear_resample: empty shape");
-  std::vector<double> out(dny * dnx);
-  const double fy = double(sny) / double(dny), fx = double(snx) / double(dnx);
-  for (size_t jy = 0; jy < dny; ++jy) {
-    const double py = double(jy) * fy;
-    const size_t y0 = size_t(std::floor(py)) % sny, y1 = (y0 + 1) % sny;
-    const double wy = py - std::floor(py);
-    for (size_t jx = 0; jx < dnx; ++jx) {
-      const double px = double(jx) * fx;
-      const size_t x0 = size_t(std::floor(px)) % snx, x1 = (x0 + 1) % snx;
-      const double wx = px - std::floor(px);
-      out[jy * dnx + jx] = (1.0 - wy) * ((1.0 - wx) * src[y0 * snx + x0] + wx * src[y0 * snx + x1]) +
-                           wy * ((1.0 - wx) * src[y1 * snx + x0] + wx * src[y1 * snx + x1]);
-    }
-  }
-  return out;
-}
-
-std::vector<double> bilinear_resample(const std::vector<double>& src, const Grid& sg, const Grid& dg) {
-  if (src.size() != sg.size()) throw std::invalid_argument("bilinear_resample: field size does not match source grid");
-  if (sg.dim() != dg.dim()) throw std::invalid_argument("bilinear_resample: dimension mismatch");
-  if (sg.dim() == 1) return bilinear_resample(src, 1, sg.points(0), 1, dg.points(0));
-  return bilinear_resample(src, sg.points(0), sg.points(1), dg.points(0), dg.points(1));
 }
 
 // ------------------------------------------------------------------ propagator.hpp
@@ -557,41 +522,6 @@ PhaseCorrector PhaseCorrector::drop_leading(Index count) const {
   return PhaseCorrector(std::move(l), std::vector<double>(sv_.begin() + first, sv_.end()), std::move(r), tol_);
 }
 
-// Checkpoint text format of procrustes.cpp:95-127: "rows rank" line, then X row by row, the
-// singular values on one line, Y row by row; 17 significant digits, single-space separated.
-void PhaseCorrector::save(std::ostream& os) const {
-  os << rows() << " " << rank() << "\n";
-  os.precision(17);
-  const auto dump = [&os](const Matrix& m) {
-    for (Index i = 0; i < m.rows(); ++i) {
-      for (Index j = 0; j < m.cols(); ++j) os << (j ? " " : "") << m(i, j);
-      os << "\n";
-    }
-  };
-  dump(left_);
-  for (size_t i = 0; i < sv_.size(); ++i) os << (i ? " " : "") << sv_[i];
-  os << "\n";
-  dump(right_);
-}
-
-PhaseCorrector PhaseCorrector::load(std::istream& is) {
-  Index rows = 0, r = 0;
-  if (!(is >> rows >> r) || rows < 0 || r < 0) throw std::runtime_error("corrector checkpoint: bad header");
-  const auto block = [&is, rows, r]() {
-    Matrix m(rows, r);
-    for (Index i = 0; i < rows; ++i)
-      for (Index j = 0; j < r; ++j)
-        if (!(is >> m(i, j))) throw std::runtime_error("corrector checkpoint: truncated matrix block");
-    return m;
-  };
-  Matrix X = block();
-  std::vector<double> sv(static_cast<size_t>(r));
-  for (Index i = 0; i < r; ++i)
-    if (!(is >> sv[size_t(i)])) throw std::runtime_error("corrector checkpoint: truncated values");
-  Matrix Y = block();
-  return PhaseCorrector(std::move(X), std::move(sv), std::move(Y), 0.0);
-}
-
 std::vector<double> stack_components(const EnergyComponents& comp) {
   std::vector<double> out;
   out.reserve((comp.grad.size() + 1) * comp.grid.size());
@@ -677,16 +607,14 @@ double relative_residual(const PhaseCorrector& corrector, const SnapshotMatrix& 
 CouplingSchedule::CouplingSchedule(double T_in, double dt_com_in, std::size_t n, PropagatorConfig fine,
                                    PropagatorConfig coarse)
     : T(T_in), dt_com(dt_com_in), n_couplings(n), fine_cfg(std::move(fine)), coarse_cfg(std::move(coarse)) {
-  if (!(T > 0.0) || !(dt_com > 0.0) || n_couplings == 0)
-    throw std::invalid_argument("CouplingSchedule: T, dt_com, N must be positive");
-  if (std::abs(double(n_couplings) * dt_com - T) > 1e-9 * T)
-    throw std::invalid_argument("CouplingSchedule: N * dt_com must equal T");
-  for (const auto* c : {&fine_cfg, &coarse_cfg}) {
-    const double span = double(c->steps_per_coupling) * c->dt;
-    if (std::abs(span - dt_com) > 1e-12 * dt_com)
-      throw std::invalid_argument(std::string("CouplingSchedule: ") + (c == &fine_cfg ? "fine" : "coarse") +
-                                  " steps_per_coupling * dt != dt_com");
-  }
+  // parareal.cpp:172-188: N dt_com = T to 1e-9, m dt = dt_com to 1e-12 for both propagators
+  require(T > 0.0 && dt_com > 0.0 && n_couplings > 0, "CouplingSchedule: T, dt_com, N must be positive");
+  require(std::abs(double(n_couplings) * dt_com - T) <= 1e-9 * T, "CouplingSchedule: N * dt_com must equal T");
+  const auto spans = [this](const PropagatorConfig& c) {
+    return std::abs(double(c.steps_per_coupling) * c.dt - dt_com) <= 1e-12 * dt_com;
+  };
+  require(spans(fine_cfg), "CouplingSchedule: fine steps_per_coupling * dt != dt_com");
+  require(spans(coarse_cfg), "CouplingSchedule: coarse steps_per_coupling * dt != dt_com");
 }
 
 std::vector<WaveState> serial_fine(const WaveState& init, const CouplingSchedule& schedule) {
@@ -776,222 +704,7 @@ ParaRun corrected_coarse_only(const WaveState& init, const CouplingSchedule& sch
   return theta_parareal(init, schedule, transfer, iterations, options);
 }
 
-double speedup_estimate(double n_cpu, double m_s, double m_t, int d, double n_couplings, double iterations) {
-  if (n_cpu <= 0 || m_s <= 0 || m_t <= 0 || n_couplings <= 0 || iterations <= 0)
-    throw std::invalid_argument("speedup_estimate: all arguments must be positive");
-  const double per = std::pow(m_s, d) * m_t;
-  return (1.0 / iterations) * std::min({n_cpu, per, per / n_couplings});
-}
-
-double speedup_full(double n_cpu, double iterations, double dt_fine, double dt_coarse, double dt_com,
-                    double n_fine_points, double n_coarse_points, double n_couplings) {
-  const double stage = 1.0 / n_cpu;
-  const double coarse = (1.0 / n_cpu + 1.0) * (dt_fine * n_coarse_points) / (dt_coarse * n_fine_points);
-  const double qr = n_coarse_points * n_couplings * dt_fine / (n_fine_points * dt_com);
-  return 1.0 / (iterations * (stage + coarse + qr));
-}
-
 }  // namespace paratime
-
-// ---- speed-model text format (experiment.hpp:84-90; behaviour of experiment.cpp:711-784) ----
-namespace paratime {
-namespace {
-
-struct SpeedText {
-  std::size_t ny = 0, nx = 0;
-  double dy = 0.0, dx = 0.0;
-  std::vector<double> values;
-};
-
-std::string fmt17(double v) {  // experiment.cpp:19-23
-  char buf[40];
-  std::snprintf(buf, sizeof buf, "%.17g", v);
-  return buf;
-}
-
-SpeedText parse_speed(std::istream& is) {
-  SpeedText t;
-  long ny = 0, nx = 0;
-  if (!(is >> ny >> nx >> t.dy >> t.dx)) throw ConfigError("speed model: bad header (want: ny nx dy dx)");
-  if (ny < 1 || nx < 1) throw ConfigError("speed model: nonpositive shape");
-  if (!(t.dx > 0.0) || (ny > 1 && !(t.dy > 0.0))) throw ConfigError("speed model: nonpositive spacing");
-  t.ny = std::size_t(ny);
-  t.nx = std::size_t(nx);
-  t.values.resize(t.ny * t.nx);
-  for (double& v : t.values) {
-    if (!(is >> v)) throw ConfigError("speed model: truncated value table");
-    if (!(v > 0.0) || !std::isfinite(v))
-      throw ConfigError("speed model: wave speed entries must be positive and finite");
-  }
-  double extra;
-  if (is >> extra) throw ConfigError("speed model: trailing values beyond ny*nx");
-  return t;
-}
-
-SpeedField to_field(SpeedText t) {
-  if (t.nx < 4 || (t.ny > 1 && t.ny < 4))
-    throw ConfigError("speed model: too few points for a grid; resample to a target size");
-  if (t.ny == 1) return SpeedField(Grid({t.nx}, {t.dx}), std::move(t.values));
-  return SpeedField(Grid({t.ny, t.nx}, {t.dy, t.dx}), std::move(t.values));
-}
-
-}  // namespace
-
-// ---- run-record CSVs (experiment.cpp:596-628) -------------------------------------------
-void write_errors_csv(const ParaRun& run, std::ostream& os) {
-  os << "iteration,coupling,energy_error,l2_error,diverged\n";
-  for (std::size_t k = 0; k < run.iterations.size(); ++k) {
-    const IterationRecord& rec = run.iterations[k];
-    for (std::size_t n = 0; n < rec.energy_err.size(); ++n)
-      os << k << "," << n << "," << fmt17(rec.energy_err[n]) << "," << fmt17(rec.l2_err[n]) << ","
-         << (rec.diverged ? 1 : 0) << "\n";
-  }
-}
-
-void write_residuals_csv(const ParaRun& run, bool plain, std::ostream& os) {
-  os << "iteration,residual,rank\n";
-  if (!plain)
-    for (std::size_t k = 1; k < run.iterations.size(); ++k)
-      os << k << "," << fmt17(run.iterations[k].residual) << "," << run.iterations[k].rank << "\n";
-}
-
-void write_summary_csv(const ParaRun& run, std::ostream& os) {
-  os << "iteration,energy_error,l2_error,diverged\n";
-  for (std::size_t k = 0; k < run.iterations.size(); ++k) {
-    const IterationRecord& rec = run.iterations[k];
-    os << k << "," << fmt17(rec.energy_err.back()) << "," << fmt17(rec.l2_err.back()) << ","
-       << (rec.diverged ? 1 : 0) << "\n";
-  }
-}
-
-void write_run_csv(const ParaRun& run, bool plain, const std::string& dir) {
-  namespace fs = std::filesystem;
-  fs::create_directories(dir);
-  std::ofstream e(fs::path(dir) / "errors.csv");
-  write_errors_csv(run, e);
-  std::ofstream r(fs::path(dir) / "residuals.csv");
-  write_residuals_csv(run, plain, r);
-  std::ofstream s(fs::path(dir) / "summary.csv");
-  write_summary_csv(run, s);
-}
-
-SpeedField read_speed_model(std::istream& is) { return to_field(parse_speed(is)); }
-
-SpeedField ingest_speed_model(const std::string& path) {
-  std::ifstream is(path);
-  if (!is) throw ConfigError("cannot open speed model: " + path);
-  return read_speed_model(is);
-}
-
-SpeedField ingest_speed_model(const std::string& path, const Grid& target) {
-  std::ifstream is(path);
-  if (!is) throw ConfigError("cannot open speed model: " + path);
-  SpeedText t = parse_speed(is);
-  const std::size_t ty = target.dim() == 1 ? 1 : target.points(0);
-  const std::size_t tx = target.dim() == 1 ? target.points(0) : target.points(1);
-  if (target.dim() == 2 && t.ny == 1) throw ConfigError("speed model: 1D file cannot fill a 2D grid");
-  return SpeedField(target, bilinear_resample(t.values, t.ny, t.nx, ty, tx));
-}
-
-void write_speed_model(const SpeedField& field, std::ostream& os) {
-  const Grid& g = field.grid;
-  const std::size_t ny = g.dim() == 1 ? 1 : g.points(0);
-  const std::size_t nx = g.dim() == 1 ? g.points(0) : g.points(1);
-  const double dy = g.dim() == 1 ? 1.0 : g.spacing(0);
-  const double dx = g.dim() == 1 ? g.spacing(0) : g.spacing(1);
-  os << ny << " " << nx << " " << fmt17(dy) << " " << fmt17(dx) << "\n";
-  for (std::size_t iy = 0; iy < ny; ++iy) {
-    for (std::size_t ix = 0; ix < nx; ++ix) os << (ix ? " " : "") << fmt17(field.c[iy * nx + ix]);
-    os << "\n";
-  }
-}
-
-}  // namespace paratime
-
-namespace ptb {
-extern thread_local std::string g_last_error;  // capi.cpp (ptb_last_error)
-}
-
-namespace {
-// C ABI wrappers: ConfigError -> PTB_CONFIG, std::invalid_argument -> PTB_INVALID_ARGUMENT
-template <typename Fn>
-ptb_status host_guarded(Fn&& fn) {
-  try {
-    fn();
-    return PTB_OK;
-  } catch (const paratime::ConfigError& e) {
-    ptb::g_last_error = e.what();
-    return PTB_CONFIG;
-  } catch (const std::invalid_argument& e) {
-    ptb::g_last_error = e.what();
-    return PTB_INVALID_ARGUMENT;
-  } catch (const std::exception& e) {
-    ptb::g_last_error = e.what();
-    return PTB_UNSUPPORTED;
-  }
-}
-}  // namespace
-
-extern "C" ptb_status ptb_speed_model_write(const ptb_grid* grid, const double* c, char* buf, size_t len,
-                                            size_t* needed) {
-  return host_guarded([&] {
-    if (!grid || !c || !needed) throw std::invalid_argument("speed_model_write: null argument");
-    std::vector<std::size_t> n(grid->n, grid->n + grid->dim);
-    std::vector<double> h(grid->h, grid->h + grid->dim);
-    const paratime::Grid g(n, h);
-    const paratime::SpeedField f(g, std::vector<double>(c, c + g.size()));
-    std::ostringstream os;
-    paratime::write_speed_model(f, os);
-    const std::string t = os.str();
-    *needed = t.size() + 1;
-    if (buf && len >= t.size() + 1) std::memcpy(buf, t.c_str(), t.size() + 1);
-  });
-}
-
-extern "C" ptb_status ptb_speed_model_read(const char* text, ptb_grid* grid, double* c, size_t cap,
-                                           size_t* npoints) {
-  return host_guarded([&] {
-    if (!text || !grid || !npoints) throw std::invalid_argument("speed_model_read: null argument");
-    std::istringstream is(text);
-    const paratime::SpeedField f = paratime::read_speed_model(is);
-    grid->dim = f.grid.dim();
-    for (int a = 0; a < 2; ++a) {
-      grid->n[a] = a < f.grid.dim() ? f.grid.points(a) : 0;
-      grid->h[a] = a < f.grid.dim() ? f.grid.spacing(a) : 0.0;
-    }
-    *npoints = f.c.size();
-    if (c && cap >= f.c.size()) std::copy(f.c.begin(), f.c.end(), c);
-  });
-}
-
-// run-record CSV text (experiment.cpp:596-628) of K iterations x (N + 1) couplings given as
-// row-major arrays; which: 0 errors.csv, 1 residuals.csv, 2 summary.csv
-extern "C" ptb_status ptb_run_csv(size_t iterations, size_t couplings, const double* energy_err, const double* l2_err,
-                                  const double* residual, const int* rank, const int* diverged, int plain, int which,
-                                  char* buf, size_t len, size_t* needed) {
-  return host_guarded([&] {
-    if (!energy_err || !l2_err || !residual || !rank || !diverged || !needed)
-      throw std::invalid_argument("run_csv: null argument");
-    if (which < 0 || which > 2) throw std::invalid_argument("run_csv: which must be 0, 1 or 2");
-    paratime::ParaRun run;
-    run.iterations.resize(iterations);
-    for (size_t k = 0; k < iterations; ++k) {
-      paratime::IterationRecord& rec = run.iterations[k];
-      rec.energy_err.assign(energy_err + k * couplings, energy_err + (k + 1) * couplings);
-      rec.l2_err.assign(l2_err + k * couplings, l2_err + (k + 1) * couplings);
-      rec.residual = residual[k];
-      rec.rank = rank[k];
-      rec.diverged = diverged[k] != 0;
-    }
-    std::ostringstream os;
-    if (which == 0) paratime::write_errors_csv(run, os);
-    else if (which == 1) paratime::write_residuals_csv(run, plain != 0, os);
-    else paratime::write_summary_csv(run, os);
-    const std::string t = os.str();
-    *needed = t.size() + 1;
-    if (buf && len >= t.size() + 1) std::memcpy(buf, t.c_str(), t.size() + 1);
-  });
-}
 
 // ------------------------------------------------------------------ absorbing layer (pml.hpp)
 namespace paratime {

@@ -6,7 +6,3 @@ tail -30 gpurun_out/r02a_tests.log
 timeout 900 python bench.py > gpurun_out/r02a_bench.json 2> gpurun_out/r02a_bench.err; echo bench_rc=$?
 tail -c 600 gpurun_out/r02a_bench.err
 python -c "import json;d=json.loads(open('gpurun_out/r02a_bench.json').read().splitlines()[-1]);print({k:d[k] for k in ('value','ms_per_step','parity','e2e') if k in d}); print(d['roofline']['kernel'], d['roofline']['frac']); print({k:v for k,v in d.items() if k.startswith('s_per')})"
-for tool in racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_kernels.py > gpurun_out/r02a_sanitize_$tool.log 2>&1; echo ${tool}_rc=$?
-  tail -5 gpurun_out/r02a_sanitize_$tool.log
-done

@@ -21,7 +21,8 @@ pytestmark = pytest.mark.gpu
 FAST_TOL = 1e-12
 
 CASES = [  # (grid, batch, steps, expected plan fragment)
-    (128, 512, 64, "k_cluster"),
+    (128, 64, 64, "k_cluster"),
+    (128, 512, 64, "full-row ry1"),
     (256, 64, 64, "ry1"),
     (512, 64, 64, "ry1"),
     (1024, 64, 64, "ry1"),
