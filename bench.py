@@ -238,13 +238,18 @@ def main():
     # roofline: live fp64 FMA peak on this GPU; dominant kernel = the wavefront K1 pass
     tflops_peak, _ = probe_fp64(ctx)
     per_launch_ms = ms / max(launches, 1)
-    launches_per_step = launches / args.steps
-    steps_per_launch = STEPS_PER_COUPLING / launches_per_step
-    slices_per_launch = batch * steps_per_launch / STEPS_PER_COUPLING  # chunked batches: fewer per launch
-    flops_per_launch = slices_per_launch * n * n * steps_per_launch * FLOPS_PER_UPDATE
-    achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
-    hbm_bytes_per_launch = slices_per_launch * n * n * 40.0  # read u, udot, coef; write u, udot (8 B each)
     plan = prop.plan(batch, mode)
+    # every launch is one wavefront pass of `fused` steps over one chunk of slices (the headline
+    # batch runs in scratch chunks, PTB_SCRATCH_MIB): algorithmic work per launch = the step's
+    # updates / launches per step
+    fused = fused_steps(plan)
+    launches_per_step = launches / args.steps
+    updates_per_launch = batch * n * n * STEPS_PER_COUPLING / launches_per_step
+    steps_per_launch = fused
+    slices_per_launch = updates_per_launch / (n * n * fused)
+    flops_per_launch = updates_per_launch * FLOPS_PER_UPDATE
+    achieved = flops_per_launch / (per_launch_ms * 1e-3) / 1e12
+    hbm_bytes_per_launch = updates_per_launch * 40.0 / fused  # read u, udot, coef; write u, udot (8 B each)
     traffic = ncu_traffic(n, batch, args.mode, plan)
 
     # achieved fraction = max(upd/s*17/FP64_peak, upd/s*40/s_f/HBM_peak), s_f the
@@ -324,6 +329,15 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def fused_steps(plan):
+    """Steps fused per HBM round trip by a plan string (wavefront depth S, or the whole
+    coupling for the on-chip k_small / k_cluster)."""
+    import re
+
+    m = re.search(r"k_wave2?<(\d+),", plan)
+    return int(m.group(1)) if m else STEPS_PER_COUPLING
 
 
 def parity_slices(batch, cores):
@@ -535,7 +549,7 @@ def sweep(B, ctx, mode, tflops_peak, hbm_peak):
         ms = e0.elapsed_time(e1) / reps
         ups = batch * n * n * STEPS_PER_COUPLING / (ms * 1e-3)
         plan = prop.plan(batch, mode)
-        s_f = STEPS_PER_COUPLING if plan.startswith("k_cluster") or plan.startswith("k_small") else 8
+        s_f = fused_steps(plan)
         f_fp64 = ups * FLOPS_PER_UPDATE / (tflops_peak * 1e12) if tflops_peak else None
         f_hbm = ups * (40.0 / s_f) / (hbm_peak * 1e9)
         out.append({"grid": n, "batch": batch, "ms": round(ms, 3), "updates_per_s": ups, "plan": plan,

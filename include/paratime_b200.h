@@ -204,6 +204,12 @@ ptb_status ptb_corrector_apply_batch(ptb_corrector* c, size_t batch, const doubl
 ptb_status ptb_relative_residual(ptb_corrector* c, size_t rows, size_t cols, const double* F_dev,
                                  const double* G_dev, double* out);
 
+/* C (m x n) = alpha op(A) op(B) + beta C, column-major device arrays (BLAS dgemm semantics,
+ * ta/tb: 1 = transposed).  The hand-written sm_100a DGEMM/DGEMV every corrector product uses
+ * (procrustes.cpp:65-66, 201-234, 251; apply :82-86), exposed for parity tests and benchmarks. */
+ptb_status ptb_dgemm(ptb_context* ctx, int ta, int tb, int m, int n, int k, double alpha, const double* A_dev,
+                     int lda, const double* B_dev, int ldb, double beta, double* C_dev, int ldc);
+
 /* building blocks of update_svd, exposed for parity tests:
  * truncated_qr (procrustes.cpp:34-46): A m x n (device, col-major) -> Q m x keep, R keep x n
  * (un-pivoted), keep = leading pivoted |R_ii| > drop_tol.  Q_dev/R_dev sized m*n / n*n. */

@@ -123,7 +123,8 @@ def interior_energy(u, v, c, hy, hx, width: int):
 
 def plain_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m_c: int, t, N: int, K: int):
     """Plain parareal (Eq. 2; parareal.cpp:201-237) on the layered state (u, udot, px, py), the
-    way csrc/pml.cu pml_parareal evaluates it: iterate 0 = the interpolated serial coarse chain;
+    way csrc/pml.cu pml_parareal evaluates it: interpolated px, py are zeroed on undamped cells,
+    non-finite iterates are clamped to the previous one; iterate 0 = the interpolated serial coarse chain;
     per iteration fine_next[n] = F(cur[n-1]), old[n] = C(R cur[n-1]); coarse sweep
     w_0 = R(init), d_n = C(w_{n-1}) - old[n], w_n = R(fine_next[n]) + d_n; next[n] = fine_next[n] + I(d_n).
     `t` is an oracle/paratime_np.Transfer.  Returns (iterates per k as lists of 4-tuples,
@@ -131,7 +132,17 @@ def plain_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m
     from oracle import paratime_np as P
 
     R = lambda s: tuple(P.restrict_field(f, t) for f in s)  # noqa: E731
-    I = lambda s: tuple(P.interpolate_field(f, t) for f in s)  # noqa: E731
+    # px, py vanish identically on undamped cells (zx = zy = 0), so their interpolants are cut
+    # back to the layer (Fourier I would otherwise spread them over the interior)
+    damped = (kf.zy[:, None] != 0.0) | (kf.zx[None, :] != 0.0)
+
+    def I(s):  # noqa: E743
+        u, v, px, py = (P.interpolate_field(f, t) for f in s)
+        return u, v, np.where(damped, px, 0.0), np.where(damped, py, 0.0)
+
+    def finite(s):
+        return all(np.all(np.isfinite(f)) for f in s)
+
     Fp = lambda s: pml_steps(*s, kf, m_f)  # noqa: E731
     Cp = lambda s: pml_steps(*s, kc, m_c)  # noqa: E731
     z = np.zeros_like(u0)
@@ -155,6 +166,9 @@ def plain_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m
             d = tuple(a - b for a, b in zip(g, old[n]))
             w = tuple(a + b for a, b in zip(R(fine_next[n]), d))
             nxt.append(tuple(a + b for a, b in zip(fine_next[n], I(d))))
+        for n in range(1, N + 1):  # finalize_iteration (parareal.cpp:117-124): clamp non-finite
+            if not finite(nxt[n]):
+                nxt[n] = cur[n]
         e = []
         den = np.sum(ref[0][0] ** 2 + ref[0][1] ** 2)  # the initial state's norm (the layer drains energy)
         for n in range(N + 1):

@@ -30,7 +30,7 @@ def _nccl_include():
 COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3", f"-I{ROOT / 'include'}", f"-I{CSRC}",
           f"-I{_nccl_include()}"]
 CUDA_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-LINK = ["-lcublas", "-lcufft", "-lcudart", "-ldl"]
+LINK = ["-lcudart", "-ldl"]
 
 
 def sources():

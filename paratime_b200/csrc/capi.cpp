@@ -84,8 +84,6 @@ struct DeviceGuard {
 
 using namespace ptb;
 
-extern "C" void ptb_release_blas(ptb_context*);
-
 extern "C" {
 
 const char* ptb_last_error(void) { return g_last_error.c_str(); }
@@ -122,7 +120,7 @@ ptb_status ptb_context_destroy(ptb_context* ctx) {
     ctx->flags.release();
     ctx->driver_cache.reset();  // parareal work buffers
     if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
-    ptb_release_blas(ctx);
+    ctx->gemm_ws.release();
     cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -407,8 +405,6 @@ ptb_status ptb_transfer_destroy(ptb_transfer* t) {
     DeviceGuard g(t->ctx->device);
     if (t->wx) cudaFree(t->wx);
     if (t->wy) cudaFree(t->wy);
-    if (t->mx) cudaFree(t->mx);
-    if (t->my) cudaFree(t->my);
     transfer_release(t);
     t->nodes_half.release();
     delete t;
@@ -441,5 +437,3 @@ ptb_status ptb_nonfinite_batch(ptb_context* ctx, size_t n, size_t batch, const d
 
 }  // extern "C"
 
-// cuBLAS handle lifetime is owned by the BLAS unit; weak default when not linked.
-extern "C" __attribute__((weak)) void ptb_release_blas(ptb_context*) {}

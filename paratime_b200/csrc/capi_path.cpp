@@ -1,6 +1,7 @@
 // extern "C" entry points for the energy map, the Procrustes corrector and the drivers.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <memory>
 
 #include "ptb_comm.h"
@@ -184,6 +185,19 @@ ptb_status ptb_corrector_apply_batch(ptb_corrector* c, size_t batch, const doubl
     std::lock_guard<std::recursive_mutex> lock(c->ctx->mutex);
     apply_corrector(*c->work, c->c, batch, in, size_t(c->c.rows), out, size_t(c->c.rows));
     PTB_CUDA_CHECK(cudaStreamSynchronize(c->ctx->stream));
+  });
+}
+
+ptb_status ptb_dgemm(ptb_context* ctx, int ta, int tb, int m, int n, int k, double alpha, const double* A, int lda,
+                     const double* B, int ldb, double beta, double* C, int ldc) {
+  return guarded([&] {
+    require(ctx && (m == 0 || n == 0 || (C && (k == 0 || (A && B)))), "dgemm: null argument");
+    require(m >= 0 && n >= 0 && k >= 0 && ldc >= std::max(1, m), "dgemm: bad dimensions");
+    require(lda >= std::max(1, ta ? k : m) && ldb >= std::max(1, tb ? n : k), "dgemm: leading dimension too small");
+    Dev d(ctx->device);
+    std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
+    gemm(ctx, ta != 0, tb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   });
 }
 

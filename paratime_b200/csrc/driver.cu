@@ -301,10 +301,9 @@ struct Driver {
   // per-step sweep products as single fused launches (k_gemv_t1 + k_assemble_d) for small and mid
   // correctors (latency-bound: cfg1-3); cuBLAS GEMVs for large ones (HBM-bound: cfg4)
   bool fused_sweep(const DevCorrector& c) const {
-    static const long long limit = [] {  // PTB_FUSED_SWEEP_MAX: corrector entries (diagnostics)
-      const char* e = std::getenv("PTB_FUSED_SWEEP_MAX");
-      return e ? std::atoll(e) : (4LL << 20);
-    }();
+    // PTB_FUSED_SWEEP_MAX: corrector entries (tests force the large-corrector branch with it)
+    const char* e = std::getenv("PTB_FUSED_SWEEP_MAX");
+    const long long limit = e ? std::atoll(e) : (4LL << 20);
     return (long long)(size_t(cg.dim + 1) * nc * size_t(std::max(c.rank, 1))) <= limit;
   }
   const double* cf_dev = nullptr;  // coarse speed
@@ -894,15 +893,12 @@ struct Driver {
     HostProf hp_(st());
     double* iu = dalloc<double>(fine_u, L * nf);
     double* iv = dalloc<double>(fine_v, L * nf);
-    if (theta) {
-      interpolate_fields(tr, L, slot(d_u, a, nc), iu);
-      interpolate_fields(tr, L, slot(d_v, a, nc), iv);
-      hp_.mark("combine: interpolate");
-      if (additive) {
-        k_add<<<blocks(ctx, L * nf), 256, 0, st()>>>(L * nf, FU(a), iu, NU(a));
-        k_add<<<blocks(ctx, L * nf), 256, 0, st()>>>(L * nf, FV(a), iv, NV(a));
-        PTB_LAUNCH_CHECK(ctx);
-        hp_.mark("combine: add");
+    if (theta && additive) {
+      // next = fine_next + I(d): fused into the interpolation's last pass on the FFT route
+      interpolate_fields_add(tr, L, slot(d_u, a, nc), FU(a), NU(a), iu);
+      interpolate_fields_add(tr, L, slot(d_v, a, nc), FV(a), NV(a), iv);
+      hp_.mark("combine: interpolate + add");
+      {
         if (a == 1) {  // next[1] = fine_next[1] exactly
           copy(NU(1), FU(1), nf);
           copy(NV(1), FV(1), nf);
@@ -912,11 +908,11 @@ struct Driver {
           copy(NU(1), FU(1), nf);
           copy(NV(1), FV(1), nf);
         }
-      } else {
-        copy(NU(a), iu, L * nf);
-        copy(NV(a), iv, L * nf);
-        nan_where(nf, L, fl(wf) + a, nullptr, nullptr, NU(a), NV(a));
       }
+    } else if (theta) {
+      interpolate_fields(tr, L, slot(d_u, a, nc), NU(a));
+      interpolate_fields(tr, L, slot(d_v, a, nc), NV(a));
+      nan_where(nf, L, fl(wf) + a, nullptr, nullptr, NU(a), NV(a));
     } else {
       // (I(w) + fine_next) - I(coarse_next), with NaN states where w / coarse_next diverged
       double* ku = dalloc<double>(fine2_u, L * nf);

@@ -481,6 +481,50 @@ __global__ void k_add_into(size_t n, double* x, const double* y) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
     x[i] = x[i] + y[i];
 }
+// auxiliary fields of an interpolated correction: px, py vanish identically where the cell is
+// undamped (zx = zy = 0: px_t = py_t = 0 from a zero start), so the interpolant's spread into
+// the interior (Fourier I rings across the whole row) is cut back to the layer; x += mask * y
+__global__ void k_aux_mask_add(size_t total, int ny, int nx, const double* __restrict__ zx,
+                               const double* __restrict__ zy, double* x, const double* __restrict__ y) {
+  const size_t n = size_t(ny) * nx;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+    const size_t p = i % n;
+    const int iy = int(p / nx), ix = int(p - size_t(iy) * nx);
+    if (zx[ix] != 0.0 || zy[iy] != 0.0) x[i] = x[i] + y[i];
+  }
+}
+// x = 0 where undamped (iterate 0's interpolated auxiliary fields)
+__global__ void k_aux_mask(size_t total, int ny, int nx, const double* __restrict__ zx, const double* __restrict__ zy,
+                           double* x) {
+  const size_t n = size_t(ny) * nx;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+    const size_t p = i % n;
+    const int iy = int(p / nx), ix = int(p - size_t(iy) * nx);
+    if (zx[ix] == 0.0 && zy[iy] == 0.0) x[i] = 0.0;
+  }
+}
+// finalize_iteration (parareal.cpp:117-124) on the layered state: slice s of `next` with any
+// non-finite entry in its four fields is flagged (bad[s], and the divergence flags) ...
+__global__ void __launch_bounds__(256) k_state_bad(size_t n, const double* u, const double* v, const double* px,
+                                                    const double* py, int32_t* bad, int32_t* flags) {
+  const size_t o = size_t(blockIdx.y) * n;
+  bool ok = true;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    ok &= isfinite(u[o + i]) && isfinite(v[o + i]) && isfinite(px[o + i]) && isfinite(py[o + i]);
+  if (__syncthreads_or(!ok) && threadIdx.x == 0) {
+    atomicOr(bad + blockIdx.y, 1);
+    atomicOr(flags + blockIdx.y, 1);
+  }
+}
+// ... and clamped to the previous iterate
+__global__ void k_clamp_bad(size_t n, const int32_t* bad, double* const* dst, const double* const* src) {
+  if (!bad[blockIdx.y]) return;
+  const size_t o = size_t(blockIdx.y) * n;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+#pragma unroll
+    for (int f = 0; f < 4; ++f) dst[f][o + i] = src[f][o + i];
+}
+
 // per slice (one block each, fixed-order reduction): out[2b] = sum (a-b)^2, out[2b+1] = sum b^2 over [u; udot]
 __global__ void __launch_bounds__(512) k_err_sums(size_t n, const double* au, const double* av, const double* bu,
                                                   const double* bv, double* out) {
@@ -555,6 +599,10 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
   int32_t* flags = static_cast<int32_t*>(bflag.get((L + 1) * sizeof(int32_t)));
   double* sums = static_cast<double*>(bsum.get(2 * (chunk + 2) * sizeof(double)));
   const size_t ichunk = std::max<size_t>(1, std::min<size_t>(L, 8));
+  DeviceBuffer bbad, bptr;
+  int32_t* bad = static_cast<int32_t*>(bbad.get((L + 1) * sizeof(int32_t)));
+  double** dptr = static_cast<double**>(bptr.get(8 * sizeof(double*)));
+  double* hptr[8];
   double* fchunk = static_cast<double*>(bchunk.get(ichunk * nf * sizeof(double)));
   auto cpy = [&](double* dst, const double* src, size_t count) {
     if (count) PTB_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -577,10 +625,18 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
   // iterate 0: the serial coarse chain, interpolated (parareal.cpp:139-145), own states
   for (int f = 0; f < 4; ++f) restrict_fields(t, 1, ini.f(f, 0), cwv.f(f));
   if (a == 1) cpy_state(cur, 0, ini, 0);
+  const int fny = int(fine->grid.n[0]), fnx = int(fine->grid.n[1]);
+  const double* fzx = fine->coef + nf;             // coef layout: kx (n) | zx ax qx (nx) | zy ay qy (ny)
+  const double* fzy = fine->coef + nf + 3 * size_t(fnx);
   for (size_t n = 1; n < b; ++n) {
     pml_propagate(coarse, coarse->steps, 1, cwv.f(0), cwv.f(1), cwv.f(2), cwv.f(3), nullptr);
-    if (n + 1 >= a)
+    if (n + 1 >= a) {
       for (int f = 0; f < 4; ++f) interpolate_fields(t, 1, cwv.f(f), cur.f(f, n + 1 - a));
+      for (int f = 2; f < 4; ++f) {
+        k_aux_mask<<<ew_blocks(ctx, nf), 256, 0, st>>>(nf, fny, fnx, fzx, fzy, cur.f(f, n + 1 - a));
+        PTB_LAUNCH_CHECK(ctx);
+      }
+    }
   }
   // init norm (errors are relative to it)
   k_err_sums<<<1, 512, 0, st>>>(nf, ini.f(0), ini.f(1), ini.f(0), ini.f(1), sums);
@@ -639,14 +695,33 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
         PTB_LAUNCH_CHECK(ctx);
       }
     }
-    // own combine: next[n] = fine_next[n] + I(d_n), in chunks of slices
+    // own combine: next[n] = fine_next[n] + I(d_n), in chunks of slices (u, udot: fused into the
+    // interpolation; px, py: the correction masked to the layer)
     for (int f = 0; f < 4; ++f)
       for (size_t c0 = 0; c0 < L; c0 += ichunk) {
         const size_t m = std::min(ichunk, L - c0);
-        interpolate_fields(t, m, cd.f(f, a - 1 + c0), fchunk);
-        k_add_into<<<ew_blocks(ctx, m * nf), 256, 0, st>>>(m * nf, nxt.f(f, 1 + c0), fchunk);
-        PTB_LAUNCH_CHECK(ctx);
+        if (f < 2) {
+          interpolate_fields_add(t, m, cd.f(f, a - 1 + c0), nxt.f(f, 1 + c0), nxt.f(f, 1 + c0), fchunk);
+        } else {
+          interpolate_fields(t, m, cd.f(f, a - 1 + c0), fchunk);
+          k_aux_mask_add<<<ew_blocks(ctx, m * nf), 256, 0, st>>>(m * nf, fny, fnx, fzx, fzy, nxt.f(f, 1 + c0), fchunk);
+          PTB_LAUNCH_CHECK(ctx);
+        }
       }
+    // non-finite iterates: flag and clamp to the previous iterate (parareal.cpp:117-124)
+    if (L) {
+      PTB_CUDA_CHECK(cudaMemsetAsync(bad, 0, (L + 1) * sizeof(int32_t), st));
+      const dim3 g(unsigned(std::min<size_t>((nf + 255) / 256, 64)), unsigned(L));
+      k_state_bad<<<g, 256, 0, st>>>(nf, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), bad, flags + 1);
+      PTB_LAUNCH_CHECK(ctx);
+      for (int f = 0; f < 4; ++f) {
+        hptr[f] = nxt.f(f, 1);
+        hptr[4 + f] = cur.f(f, 1);
+      }
+      PTB_CUDA_CHECK(cudaMemcpyAsync(dptr, hptr, sizeof(hptr), cudaMemcpyHostToDevice, st));
+      k_clamp_bad<<<g, 256, 0, st>>>(nf, bad, dptr, dptr + 4);
+      PTB_LAUNCH_CHECK(ctx);
+    }
     // state a-1: the initial state on rank 0, the previous rank's last state elsewhere
     if (a == 1) cpy_state(nxt, 0, ini, 0);
     if (world > 1) {

@@ -27,7 +27,6 @@
 // Large products (U^T F, U UF, [U Q_F] Xh, X(Y^T v)) are plain cuBLAS DGEMMs.
 
 #include <cooperative_groups.h>
-#include <cublas_v2.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1362,22 +1361,6 @@ __global__ void __launch_bounds__(256) k_sum_final(const double* part, int np, d
   if (threadIdx.x == 0) *out = red[0];
 }
 
-cublasHandle_t blas(ptb_context* ctx) {
-  if (!ctx->cublas) {
-    cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(PTB_CUDA, "cublasCreate failed");
-    ctx->cublas = h;
-  }
-  cublasHandle_t h = static_cast<cublasHandle_t>(ctx->cublas);
-  cublasSetStream(h, ctx->stream);
-  cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
-  return h;
-}
-
-void check_blas(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS) fail(PTB_CUDA, std::string("cuBLAS ") + what + " failed");
-}
-
 double dev_sumsq(ptb_context* ctx, const double* x, size_t n, DeviceBuffer& scratch) {
   constexpr int NP = 296;  // fixed partial count (2 x 148 SMs): deterministic for a given n
   double* d = static_cast<double*>(scratch.get((NP + 1) * sizeof(double)));
@@ -1400,20 +1383,6 @@ int qr_grid(ptb_context* ctx, int m, size_t smem, const void* kern, int rows_per
 }
 
 }  // namespace
-
-// C (m x n) = alpha op(A) op(B) + beta C, all column-major
-void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
-          const double* B, int ldb, double beta, double* C, int ldc) {
-  if (m == 0 || n == 0) return;
-  if (k == 0) {
-    if (beta == 0.0) PTB_CUDA_CHECK(cudaMemsetAsync(C, 0, size_t(ldc) * n * sizeof(double), ctx->stream));
-    return;
-  }
-  check_blas(cublasDgemm(blas(ctx), ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k, &alpha, A,
-                         std::max(1, lda), B, std::max(1, ldb), &beta, C, std::max(1, ldc)),
-             "dgemm");
-  ctx->launches.fetch_add(1, std::memory_order_relaxed);
-}
 
 ProcWork::ProcWork(ptb_context* c) : ctx(c) {}
 ProcWork::~ProcWork() {
@@ -1554,7 +1523,9 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, cons
   __shared__ double cbuf[MMAX];
   __shared__ double nrm[2][NMAX];
   __shared__ double betas[NMAX], scals[NMAX];
+  __shared__ int exps[NMAX];
   __shared__ double s_sc[3];
+  __shared__ int s_ex;
   __shared__ int posc[PIVOT ? QRR_WARPS : 1][PIVOT ? NMAX : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = a.n;
@@ -1620,19 +1591,33 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, cons
       // the pivot's slot is dynamic: gather it with explicit selects (an indexed read would move
       // the whole register tile to local memory)
       const int sp = p / QRR_WARPS;
-      double xs = 0.0, alc = 0.0;
+      double cv[RPL], amax = 0.0;
 #pragma unroll
       for (int u = 0; u < RPL; ++u) {
         double c = x[0][u];
 #pragma unroll
         for (int s = 1; s < CPW; ++s) c = selp(sp == s, x[s][u], c);
+        cv[u] = c;
+        if (lane + 32 * u >= j) amax = fmax(amax, fabs(c));
+      }
+#pragma unroll
+      for (int s = 0; s < CPW; ++s) estep[s] = selp(sp == s, j, estep[s]);
+      // dlarfg on the column scaled by 2^-ex (max |entry| in [1, 2)): a TSQR leaf can hold a
+      // column of tiny entries (snapshot rows far from the wave, down to denormals) whose squares
+      // underflow; an unscaled norm then yields a non-orthogonal reflector, harmless for the tiny
+      // leaf data but not for the O(1) rows the down-sweep applies it to.  Power-of-two scaling is
+      // exact, so well-scaled columns get the same reflector as before.
+      for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      const int ex = amax > 0.0 ? ilogb(amax) : 0;
+      double xs = 0.0, alc = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const double c = scalbn(cv[u], -ex);
         const int r = lane + 32 * u;
         if (r > j) xs = fma(c, c, xs);
         if (u == j / 32) alc = c;
         cbuf[r] = c;
       }
-#pragma unroll
-      for (int s = 0; s < CPW; ++s) estep[s] = selp(sp == s, j, estep[s]);
       xs = warp_sum(xs);
       const double al = __shfl_sync(0xffffffffu, alc, j & 31);
       if (lane == 0) {
@@ -1641,14 +1626,15 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, cons
           beta = al;
           tau = 0.0;
           scal = 0.0;
-        } else {  // sqrt(al^2 + |x|^2): the entries are far from the double range limits
+        } else {
           beta = -copysign(sqrt(fma(al, al, xs)), al);
           tau = (beta - al) / beta;
           scal = 1.0 / (al - beta);
         }
-        s_sc[0] = beta;
+        s_sc[0] = scalbn(beta, ex);  // R_jj in the column's own scale
         s_sc[1] = tau;
-        s_sc[2] = scal;
+        s_sc[2] = scal;  // applies to the SCALED column (cbuf)
+        s_ex = ex;
       }
     }
     __syncthreads();
@@ -1662,7 +1648,8 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, cons
     }
     if (tid == 0) {
       betas[j] = beta;
-      scals[j] = scal;
+      scals[j] = scal;  // reflector of the unscaled column: v = (x 2^-ex) scal
+      exps[j] = s_ex;
       if (TS) a.tau[size_t(blockIdx.x) * n + j] = tau;
       else a.tau[j] = tau;
       if (!TS && a.beta_out) a.beta_out[j] = fabs(beta);
@@ -1722,7 +1709,7 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, cons
       for (int u = 0; u < RPL; ++u) {
         const int r = lane + 32 * u;
         if (r >= m) continue;
-        if (r > k) a.V[size_t(k) * a.ldv + r0 + r] = x[s][u] * scals[k];
+        if (r > k) a.V[size_t(k) * a.ldv + r0 + r] = scalbn(x[s][u], -exps[k]) * scals[k];
         if (r < n) a.R[size_t(k) * a.ldr + size_t(blockIdx.x) * n + r] = r < k ? x[s][u] : (r == k ? betas[k] : 0.0);
       }
     } else {
@@ -1732,7 +1719,7 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, cons
         if (r >= m) continue;
         double val = x[s][u];
         if (e >= 0 && r == e) val = betas[e];
-        else if (e >= 0 && r > e) val = x[s][u] * scals[e];
+        else if (e >= 0 && r > e) val = scalbn(x[s][u], -exps[e]) * scals[e];
         a.out[size_t(pos) * m + r] = val;
       }
       if (lane == 0) a.perm[pos] = k;
@@ -2509,9 +2496,7 @@ double relative_residual(ProcWork& w, const DevCorrector& c, const double* F, co
   double* D = static_cast<double*>(w.buf[20].get(size_t(rows) * cols * sizeof(double)));
   apply_corrector(w, c, size_t(cols), G, size_t(rows), D, size_t(rows));
   // D = F - X Y^T G
-  const double minus1 = -1.0, one = 1.0;
-  check_blas(cublasDgeam(blas(ctx), CUBLAS_OP_N, CUBLAS_OP_N, rows, cols, &one, F, rows, &minus1, D, rows, D, rows),
-             "dgeam");
+  geam_sub(ctx, size_t(rows) * cols, F, D);
   return std::sqrt(dev_sumsq(ctx, D, size_t(rows) * cols, w.buf[11])) / fnorm;
 }
 
@@ -2532,9 +2517,3 @@ void drop_leading(const DevCorrector& c, size_t count, DevCorrector& out, ptb_co
 
 }  // namespace ptb
 
-extern "C" void ptb_release_blas(ptb_context* ctx) {
-  if (ctx && ctx->cublas) {
-    cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
-    ctx->cublas = nullptr;
-  }
-}

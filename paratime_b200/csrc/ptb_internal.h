@@ -156,7 +156,7 @@ struct ptb_context {
   // memory is synchronous and would serialise the pipeline
   int32_t* pinned_flags = nullptr;
   size_t pinned_flags_n = 0;
-  void* cublas = nullptr;  // lazily created cublasHandle_t
+  ptb::DeviceBuffer gemm_ws;  // split-K partials of ptb::gemm (gemm.cu)
   // parareal driver work buffers kept between runs (driver.cu), so a repeated run neither
   // reallocates nor synchronises on cudaMalloc/cudaFree; freed with the context
   std::shared_ptr<void> driver_cache;
@@ -194,13 +194,8 @@ struct ptb_transfer {
   // Fourier weights per axis: w[a][rem*nc + j] = weight of coarse node q-j..., see transfer.cu
   double* wx = nullptr;
   double* wy = nullptr;
-  // dense forms of the same maps for the GEMM path (2D, large grids): mx = cx x fx, my = fy x cy
-  double* mx = nullptr;
-  double* my = nullptr;
-  // FFT route (2D Fourier, large grids): cuFFT plans for one field (coarse D2Z, fine Z2D) and
-  // the two spectra; plans are created lazily (int handles, 0 = none)
-  int fft_fwd = 0, fft_inv = 0;
-  ptb::DeviceBuffer spec_c, spec_f;
+  // warp-FFT route (2D Fourier, large grids): the x-pass plane (batch x coarse rows x fine cols)
+  ptb::DeviceBuffer spec_c;
   ptb::DeviceBuffer nodes_half;  // scratch of interpolate_at_coarse_nodes
 };
 
@@ -239,9 +234,12 @@ void nonfinite(ptb_context* ctx, size_t n, size_t batch, const double* f, int32_
 
 // transfer.cu
 void transfer_init(ptb_transfer* t);
-void transfer_release(ptb_transfer* t);  // cuFFT plans
+void transfer_release(ptb_transfer* t);  // work buffers
 void restrict_fields(ptb_transfer* t, size_t batch, const double* fine, double* coarse);
 void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, double* fine);
+// out = base + I(coarse) (base may alias out); scratch: batch fine fields (used off the FFT route)
+void interpolate_fields_add(ptb_transfer* t, size_t batch, const double* coarse, const double* base, double* out,
+                            double* scratch);
 // R(I(coarse)): the interpolant's values at the coarse nodes, bitwise equal to restricting
 // the full interpolation (used by the coarse-only sweep)
 void interpolate_at_coarse_nodes(ptb_transfer* t, size_t batch, const double* coarse, double* out);

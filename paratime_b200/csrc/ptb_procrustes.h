@@ -50,6 +50,7 @@ double relative_residual(ProcWork& w, const DevCorrector& c, const double* F, co
 void drop_leading(const DevCorrector& c, size_t count, DevCorrector& out, ptb_context* ctx);
 void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
           const double* B, int ldb, double beta, double* C, int ldc);
+void geam_sub(ptb_context* ctx, size_t total, const double* F, double* D);  // D = F - D
 void fix_signs(ptb_context* ctx, double* X, double* Y, int rows, int cols);
 
 }  // namespace ptb

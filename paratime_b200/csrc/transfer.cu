@@ -18,27 +18,16 @@
 // bin contributes cos(pi delta)).  W is tabulated on the host with exact integer
 // argument reduction, so the device path is a two-pass (x then y) dense stencil with
 // no FFT; R(I(U)) = U holds to round-off like the reference's FFT route.
-// On large 2D grids the two passes are matrix products with the dense forms
-//   Mx[j][q*r + rem] = W[rem][(q - j) mod n]   (x: half = in . Mx)
-//   My[q*r + rem][j] = W[rem][(q - j) mod n]   (y: out = My . half)
-// issued as cuBLAS DGEMMs of one fixed shape per field, so each slice's result does not
-// depend on how many slices a call (or a rank) carries.
-// Default on 2D fine grids >= 256^2 (measured: faster than the DGEMMs from 256^2 up; the
-// DGEMM route stays for PTB_INTERP_FFT=0) is the reference's own construction done with cuFFT (fft.cpp wraps
-// FFTW): 2D D2Z of the coarse field, the zero-padded spectrum (Nyquist bins split 1/2-1/2 per
-// axis as grid.cpp:161-166; the x split comes from the implicit Hermitian mirror of the
-// half-spectrum), 2D Z2D on the fine grid.  The 2D DFT is separable, so this equals the
-// reference's x-then-y line interpolation; plans are for one field, executed per field (same
-// determinism argument as the DGEMMs).  Memory-bound instead of 2 n_c flops per output point.
+// On 2D fine grids >= 256^2 with power-of-two coarse axes (32..256 points) the same map runs as
+// warp FFTs (k_fourier_fft_x / k_fourier_fft_y below): O(n log n) per line instead of n taps per
+// output point, phase 0 copied so the nodes stay exact.  Every field is transformed on its own,
+// so a slice's result never depends on how many slices a call or a rank carries.
 
 #include <cmath>
 #include <cstdlib>
 #include <vector>
 
-#include <cufft.h>
-
 #include "ptb_internal.h"
-#include "ptb_procrustes.h"  // gemm (cuBLAS DGEMM on the context stream)
 
 namespace ptb {
 namespace {
@@ -221,9 +210,8 @@ void transfer_init(ptb_transfer* t) {
 }
 
 void transfer_release(ptb_transfer* t) {
-  if (t->fft_fwd) cufftDestroy(cufftHandle(t->fft_fwd));
-  if (t->fft_inv) cufftDestroy(cufftHandle(t->fft_inv));
-  t->fft_fwd = t->fft_inv = 0;
+  t->spec_c.release();
+  t->nodes_half.release();
 }
 
 void restrict_fields(ptb_transfer* t, size_t batch, const double* fine, double* coarse) {
@@ -236,68 +224,297 @@ void restrict_fields(ptb_transfer* t, size_t batch, const double* fine, double* 
 }
 
 namespace {
-// dense circulant matrix of one axis: rows x cols row-major, TRANSPOSED selects the x form
-std::vector<double> dense_axis(int n, int r, bool x_form) {
-  const std::vector<double> w = fourier_weights(n, r);
+// ------------------------------------------------------------------ Fourier I by warp FFTs
+//
+// fourier_interp_line (grid.cpp:151-177) maps n coarse values x to m = n r fine values
+//   out[i] = (1/n) sum_k X_k e^{2 pi i kappa(k) i / m},   X = DFT_n(x),
+// kappa(k) the signed frequency, the Nyquist bin k = n/2 split half/half between +-n/2.  At
+// i = q r + s this is a length-n inverse DFT of the phase-shifted spectrum
+//   Y^(s)_k = X_k e^{2 pi i kappa s / m}   (Nyquist: X_{n/2} cos(pi s / r)),
+// so one forward DFT_n and r-1 inverse DFT_n per line give all r phases, and s = 0 is the
+// line itself (the interpolant passes through the nodes exactly, as the circulant weights
+// do).  Y^(s) is Hermitian, so two phases share one complex inverse transform (real part:
+// phase s1, imaginary part: phase s2).  n = 32 E (E <= 8) points live in one warp, lane L
+// holding x[L + 32 e]: an E-point DFT in registers, a twiddle, then a 32-point DFT across the
+// lanes by shuffles (DIF, bit-reversed lane order); the inverse runs the same network backwards
+// (DIT), so the spectrum is never permuted.  x pass: a warp per coarse row, the r n outputs
+// staged in shared memory phase-major and written as one contiguous row; y pass: a CTA per 16
+// adjacent fine columns (128-byte rows), a warp per column.  Optionally fused with the fine
+// combine: out = base + I(coarse).
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+constexpr int bitrev_c(int v, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1) << (bits - 1 - i);
+  return r;
+}
+constexpr int log2_c(int v) { return v <= 1 ? 0 : 1 + log2_c(v / 2); }
+
+// e^{-2 pi i p / q} for the compile-time register DFTs (q <= 8)
+__device__ __forceinline__ double2 tw_const(int p, int q, bool inv) {
+  constexpr double h = 0.70710678118654752440;
+  double2 w;
+  switch ((p * 8) / q) {  // angle in units of pi/4
+    case 0: w = make_double2(1.0, 0.0); break;
+    case 1: w = make_double2(h, -h); break;
+    case 2: w = make_double2(0.0, -1.0); break;
+    default: w = make_double2(-h, -h); break;  // 3 pi / 4
+  }
+  if (inv) w.y = -w.y;
+  return w;
+}
+
+// E-point DFT in registers, natural order in and out (unnormalised; INV: e^{+})
+template <int E, bool INV>
+__device__ __forceinline__ void dft_reg(double2 (&v)[E]) {
+  if constexpr (E > 1) {
+#pragma unroll
+    for (int h = E / 2; h >= 1; h /= 2)
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        if ((i & h) == 0) {
+          const double2 a = v[i], b = v[i + h];
+          v[i] = cadd(a, b);
+          const int p = i & (h - 1);
+          v[i + h] = p == 0 ? csub(a, b) : cmul(csub(a, b), tw_const(p, 2 * h, INV));
+        }
+    double2 t[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) t[bitrev_c(i, log2_c(E))] = v[i];
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = t[i];
+  }
+}
+
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+
+// per-lane twiddles of the transforms: lane network w_{2h}^{lane & (h-1)} (h = 16 >> st) and the
+// register-to-lane twiddle w_n^{lane k1}
+template <int E>
+struct LaneTw {
+  double2 net[5];
+  double2 mid[E];
+  __device__ void init(int lane) {
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+      const int h = 16 >> st;
+      double sn, cs;
+      sincospi(-double(lane & (h - 1)) / double(h), &sn, &cs);  // e^{-2 pi i p / (2h)}
+      net[st] = make_double2(cs, sn);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < E; ++k1) {
+      double sn, cs;
+      sincospi(-2.0 * double(lane * k1) / double(32 * E), &sn, &cs);
+      mid[k1] = make_double2(cs, sn);
+    }
+  }
+};
+
+// forward DFT of n = 32 E points: in lane L slot e = x[L + 32 e]; out lane L slot k1 = X[k1 + E rev5(L)]
+template <int E>
+__device__ __forceinline__ void fft_fwd(double2 (&v)[E], const LaneTw<E>& tw, int lane) {
+  dft_reg<E, false>(v);
+#pragma unroll
+  for (int k1 = 1; k1 < E; ++k1) v[k1] = cmul(v[k1], tw.mid[k1]);
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int h = 16 >> st;
+    const bool up = lane & h;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double2 o = shfl_xor2(v[e], h);
+      v[e] = up ? cmul(csub(o, v[e]), tw.net[st]) : cadd(v[e], o);
+    }
+  }
+}
+
+// inverse (unnormalised, e^{+}): in lane L slot k1 = Z[k1 + E rev5(L)]; out lane L slot e = z[L + 32 e]
+template <int E>
+__device__ __forceinline__ void fft_inv(double2 (&v)[E], const LaneTw<E>& tw, int lane) {
+#pragma unroll
+  for (int st = 4; st >= 0; --st) {
+    const int h = 16 >> st;
+    const bool up = lane & h;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (up) v[e] = cmulc(v[e], tw.net[st]);
+      const double2 o = shfl_xor2(v[e], h);
+      v[e] = up ? csub(o, v[e]) : cadd(v[e], o);
+    }
+  }
+#pragma unroll
+  for (int k1 = 1; k1 < E; ++k1) v[k1] = cmulc(v[k1], tw.mid[k1]);
+  dft_reg<E, true>(v);
+}
+
+// The r phases of one line.  Per lane: the spectrum X (layout of fft_fwd) and the unit phase
+// steps e^{2 pi i kappa / m} of its bins; emit(s, e, value) receives out[(L + 32 e) r + s].
+template <int E, typename Emit>
+__device__ __forceinline__ void interp_line(double2 (&x)[E], int r, const LaneTw<E>& tw, const double2 (&step)[E],
+                                            int lane, Emit&& emit) {
+  constexpr int n = 32 * E;
+#pragma unroll
+  for (int e = 0; e < E; ++e) emit(0, e, x[e].x);  // phase 0: the nodes themselves
+  fft_fwd<E>(x, tw, lane);
+  const double inv_n = 1.0 / double(n);  // power of two: exact
+  // Nyquist bin (k = n/2): lane 1 (rev5(1) = 16), slot 0
+  const bool nyq_lane = lane == 1;
+  double2 ph[E];  // e^{2 pi i kappa s / m} for the current s
+#pragma unroll
+  for (int e = 0; e < E; ++e) ph[e] = make_double2(1.0, 0.0);
+  for (int s1 = 1; s1 < r; s1 += 2) {
+    const int s2 = s1 + 1;
+    double2 z[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double2 p1 = cmul(ph[e], step[e]);
+      const double2 p2 = cmul(p1, step[e]);
+      ph[e] = p2;
+      double2 a = p1, b = s2 < r ? p2 : make_double2(0.0, 0.0);
+      if (nyq_lane && e == 0) {  // split Nyquist: X_{n/2} cos(pi s / r)
+        a = make_double2(a.x, 0.0);
+        b = make_double2(b.x, 0.0);
+      }
+      const double2 y1 = cmul(x[e], a), y2 = cmul(x[e], b);
+      z[e] = make_double2((y1.x - y2.y) * inv_n, (y1.y + y2.x) * inv_n);  // (Y1 + i Y2) / n
+    }
+    fft_inv<E>(z, tw, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      emit(s1, e, z[e].x);
+      if (s2 < r) emit(s2, e, z[e].y);
+    }
+  }
+}
+
+// unit phase steps of the bins a lane holds after fft_fwd: e^{2 pi i kappa / m}
+template <int E>
+__device__ __forceinline__ void phase_steps(double2 (&step)[E], int lane, int r) {
+  constexpr int n = 32 * E;
+  const int k2 = __brev(unsigned(lane)) >> 27;
+#pragma unroll
+  for (int k1 = 0; k1 < E; ++k1) {
+    const int k = k1 + E * k2;
+    const int kap = k <= n / 2 ? k : k - n;  // Nyquist (k = n/2): +n/2, only its real part is used
+    double sn, cs;
+    sincospi(2.0 * double(kap) / double(n * r), &sn, &cs);
+    step[k1] = make_double2(cs, sn);
+  }
+}
+
+constexpr int FX_WARPS = 4;
+
+// x pass: rows of `lines` coarse lines (length n = 32E, row stride n) -> rows of n r values
+template <int E>
+__global__ void __launch_bounds__(32 * FX_WARPS) k_fourier_fft_x(size_t lines, int r, const double* __restrict__ in,
+                                                                   double* __restrict__ out) {
+  constexpr int n = 32 * E, PITCH = n + 4;  // phase-major staging, pitch n+4: conflict-free row reads
+  extern __shared__ double stage_x[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sb = stage_x + size_t(warp) * r * PITCH;
+  LaneTw<E> tw;
+  tw.init(lane);
+  double2 step[E];
+  phase_steps<E>(step, lane, r);
   const size_t m = size_t(n) * r;
-  std::vector<double> d(m * n);
-  for (size_t i = 0; i < m; ++i) {
-    const int q = int(i / r), rem = int(i % r);
-    for (int j = 0; j < n; ++j) {
-      const double v = w[size_t(rem) * n + size_t(((q - j) % n + n) % n)];
-      if (x_form)
-        d[size_t(j) * m + i] = v;  // Mx[j][i]
-      else
-        d[i * n + size_t(j)] = v;  // My[i][j]
-    }
-  }
-  return d;
-}
-
-bool use_gemm(const TGeom& g) {
-  static const int env = [] {
-    const char* e = std::getenv("PTB_INTERP_GEMM");
-    return e ? std::atoi(e) : -1;
-  }();
-  if (env == 0) return false;
-  const bool ok = g.cy > 1 && g.rx > 1 && g.ry > 1;
-  return ok && (env == 1 || size_t(g.fy) * g.fx >= size_t(512) * 512);
-}
-
-__global__ void k_pad_spectrum(int cy, int cx, int fy, int fx, double scale, const double2* __restrict__ in_all,
-                               double2* __restrict__ out_all) {
-  const int hc = cx / 2 + 1, hf = fx / 2 + 1;
-  const size_t total = size_t(fy) * hf;
-  const double2* __restrict__ in = in_all + size_t(blockIdx.y) * cy * hc;
-  double2* __restrict__ out = out_all + size_t(blockIdx.y) * total;
-  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
-    const int ky = int(e / hf), kx = int(e - size_t(ky) * hf);
-    double2 v = make_double2(0.0, 0.0);
-    // source row: fine row ky <-> signed frequency sy (coarse row sy mod cy)
-    int sy;
-    double wgt = scale;
-    if (ky < (cy + 1) / 2) {
-      sy = ky;
-    } else if (ky > fy - (cy + 1) / 2) {
-      sy = ky - fy + cy;
-    } else if (cy % 2 == 0 && (ky == cy / 2 || ky == fy - cy / 2)) {
-      sy = cy / 2;  // Nyquist row split between +cy/2 and -cy/2
-      wgt *= 0.5;
-    } else {
-      sy = -1;
-    }
-    if (sy >= 0 && kx <= cx / 2) {
-      if (cx % 2 == 0 && kx == cx / 2) wgt *= 0.5;  // mirror (implicit) carries the other half
-      const double2 f = in[size_t(sy) * hc + kx];
-      v = make_double2(f.x * wgt, f.y * wgt);
-    }
-    out[e] = v;
+  for (size_t line = size_t(blockIdx.x) * FX_WARPS + warp; line < lines; line += size_t(gridDim.x) * FX_WARPS) {
+    double2 x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = make_double2(in[line * n + lane + 32 * e], 0.0);
+    interp_line<E>(x, r, tw, step, lane, [&](int s, int e, double val) { sb[s * PITCH + lane + 32 * e] = val; });
+    __syncwarp();
+    double* o = out + line * m;
+    for (int i = lane; i < int(m); i += 32) o[i] = sb[(i % r) * PITCH + i / r];
+    __syncwarp();
   }
 }
 
-void check_fft(cufftResult r, const char* what) {
-  if (r != CUFFT_SUCCESS) fail(PTB_CUDA, std::string("cuFFT ") + what + " failed (" + std::to_string(int(r)) + ")");
+constexpr int FY_COLS = 16;
+
+// y pass: plane (n x w) per field -> (n r x w), columns [16 blockIdx.x, +16) of field blockIdx.y;
+// out = base + I (base nullable, may alias out)
+template <int E>
+__global__ void __launch_bounds__(32 * FY_COLS) k_fourier_fft_y(int w, int r, const double* __restrict__ in,
+                                                                  const double* base, double* out) {
+  constexpr int n = 32 * E, IP = n + 1, OP = FY_COLS + 1;
+  extern __shared__ double smem_y[];
+  double* tin = smem_y;                  // [FY_COLS][n + 1]
+  double* tout = smem_y + FY_COLS * IP;  // [2][n][FY_COLS + 1]: one phase pair
+  const int tid = threadIdx.x, lane = tid & 31, col = tid >> 5;
+  const int x0 = blockIdx.x * FY_COLS;
+  const double* src = in + size_t(blockIdx.y) * n * w + x0;
+  const size_t off = size_t(blockIdx.y) * n * r * w + x0;
+  for (int i = tid; i < n * FY_COLS; i += 32 * FY_COLS) {
+    const int row = i / FY_COLS, c = i % FY_COLS;
+    tin[c * IP + row] = src[size_t(row) * w + c];
+  }
+  __syncthreads();
+  // phase 0: the coarse rows themselves
+  for (int i = tid; i < n * FY_COLS; i += 32 * FY_COLS) {
+    const int q = i / FY_COLS, c = i % FY_COLS;
+    const size_t g = off + size_t(q) * r * w + c;
+    const double v = tin[c * IP + q];
+    out[g] = base ? base[g] + v : v;
+  }
+  LaneTw<E> tw;
+  tw.init(lane);
+  double2 step[E];
+  phase_steps<E>(step, lane, r);
+  double2 x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = make_double2(tin[col * IP + lane + 32 * e], 0.0);
+  fft_fwd<E>(x, tw, lane);
+  const double inv_n = 1.0 / double(n);
+  const bool nyq_lane = lane == 1;
+  double2 ph[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) ph[e] = make_double2(1.0, 0.0);
+  for (int s1 = 1; s1 < r; s1 += 2) {
+    const int s2 = s1 + 1, cnt = s2 < r ? 2 : 1;
+    double2 z[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double2 p1 = cmul(ph[e], step[e]);
+      const double2 p2 = cmul(p1, step[e]);
+      ph[e] = p2;
+      double2 a = p1, b = cnt == 2 ? p2 : make_double2(0.0, 0.0);
+      if (nyq_lane && e == 0) {
+        a = make_double2(a.x, 0.0);
+        b = make_double2(b.x, 0.0);
+      }
+      const double2 y1 = cmul(x[e], a), y2 = cmul(x[e], b);
+      z[e] = make_double2((y1.x - y2.y) * inv_n, (y1.y + y2.x) * inv_n);
+    }
+    fft_inv<E>(z, tw, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      tout[(lane + 32 * e) * OP + col] = z[e].x;
+      tout[(n + lane + 32 * e) * OP + col] = z[e].y;
+    }
+    __syncthreads();
+    for (int i = tid; i < cnt * n * FY_COLS; i += 32 * FY_COLS) {
+      const int c = i % FY_COLS, qq = i / FY_COLS, slot = qq / n, q = qq % n;
+      const size_t g = off + (size_t(q) * r + s1 + slot) * w + c;
+      const double v = tout[(slot * n + q) * OP + c];
+      out[g] = base ? base[g] + v : v;
+    }
+    __syncthreads();
+  }
 }
+
+// E = n / 32 for the warp FFT route, 0 when n is not 32, 64, 128 or 256
+int fft_e(int n) { return (n == 32 || n == 64 || n == 128 || n == 256) ? n / 32 : 0; }
 
 bool use_fft(const TGeom& g) {
   static const int env = [] {
@@ -305,76 +522,57 @@ bool use_fft(const TGeom& g) {
     return e ? std::atoi(e) : -1;
   }();
   if (env == 0) return false;
-  const bool ok = g.cy > 1 && g.rx > 1 && g.ry > 1;
+  const bool ok = g.cy > 1 && g.rx > 1 && g.ry > 1 && fft_e(g.cx) && fft_e(g.cy) && g.fx % FY_COLS == 0;
   return ok && (env == 1 || size_t(g.fy) * g.fx >= size_t(256) * 256);
 }
 
-constexpr int FFT_CHUNK = 8;  // fields per cuFFT execution (fixed: a partial chunk is padded)
+template <int E>
+void launch_fft_x(ptb_context* ctx, size_t lines, int r, const double* in, double* out) {
+  const size_t smem = size_t(FX_WARPS) * r * (32 * E + 4) * sizeof(double);
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(k_fourier_fft_x<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const unsigned grid = unsigned(std::min<size_t>((lines + FX_WARPS - 1) / FX_WARPS, size_t(ctx->num_sms) * 16));
+  k_fourier_fft_x<E><<<grid, 32 * FX_WARPS, smem, ctx->stream>>>(lines, r, in, out);
+  PTB_LAUNCH_CHECK(ctx);
+}
 
-void interpolate_fft(ptb_transfer* t, const TGeom& g, size_t batch, const double* coarse, double* fine) {
-  ptb_context* ctx = t->ctx;
-  cudaStream_t st = ctx->stream;
-  const int hc = g.cx / 2 + 1, hf = g.fx / 2 + 1;
-  const size_t nc = size_t(g.cy) * g.cx, nf = size_t(g.fy) * g.fx;
-  const size_t sc_n = size_t(g.cy) * hc, sf_n = size_t(g.fy) * hf;
-  if (!t->fft_fwd) {
-    cufftHandle f = 0, b = 0;
-    int nC[2] = {g.cy, g.cx}, nF[2] = {g.fy, g.fx};
-    check_fft(cufftPlanMany(&f, 2, nC, nullptr, 1, int(nc), nullptr, 1, int(sc_n), CUFFT_D2Z, FFT_CHUNK),
-              "plan D2Z");
-    check_fft(cufftPlanMany(&b, 2, nF, nullptr, 1, int(sf_n), nullptr, 1, int(nf), CUFFT_Z2D, FFT_CHUNK),
-              "plan Z2D");
-    t->fft_fwd = int(f);
-    t->fft_inv = int(b);
-  }
-  const cufftHandle f = cufftHandle(t->fft_fwd), b = cufftHandle(t->fft_inv);
-  check_fft(cufftSetStream(f, st), "set stream");
-  check_fft(cufftSetStream(b, st), "set stream");
-  double2* sc = static_cast<double2*>(t->spec_c.get(FFT_CHUNK * sc_n * sizeof(double2)));
-  double2* sf = static_cast<double2*>(t->spec_f.get(FFT_CHUNK * sf_n * sizeof(double2)));
-  const double scale = 1.0 / double(nc);
-  for (size_t i0 = 0; i0 < batch; i0 += FFT_CHUNK) {
-    const size_t cnt = std::min<size_t>(FFT_CHUNK, batch - i0);
-    const double* in = coarse + i0 * nc;
-    double* out = fine + i0 * nf;
-    double* stage_in = nullptr;
-    double* stage_out = nullptr;
-    if (cnt < FFT_CHUNK) {  // partial chunk: same plan on a zero-padded staging copy
-      stage_in = static_cast<double*>(ctx->scratch[2].get(FFT_CHUNK * nc * sizeof(double)));
-      stage_out = static_cast<double*>(ctx->scratch[3].get(FFT_CHUNK * nf * sizeof(double)));
-      PTB_CUDA_CHECK(cudaMemsetAsync(stage_in, 0, FFT_CHUNK * nc * sizeof(double), st));
-      PTB_CUDA_CHECK(cudaMemcpyAsync(stage_in, in, cnt * nc * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      in = stage_in;
-    }
-    // cuFFT's D2Z takes its input as non-const
-    check_fft(cufftExecD2Z(f, const_cast<double*>(in), reinterpret_cast<cufftDoubleComplex*>(sc)), "exec D2Z");
-    k_pad_spectrum<<<dim3(blocks_for(ctx, sf_n), FFT_CHUNK), 256, 0, st>>>(g.cy, g.cx, g.fy, g.fx, scale, sc, sf);
+template <int E>
+void launch_fft_y(ptb_context* ctx, size_t planes, int w, int r, const double* in, const double* base, double* out) {
+  constexpr int n = 32 * E;
+  const size_t smem = (size_t(FY_COLS) * (n + 1) + size_t(2) * n * (FY_COLS + 1)) * sizeof(double);
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(k_fourier_fft_y<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  for (size_t p0 = 0; p0 < planes; p0 += 65535) {  // gridDim.y limit
+    const size_t np = std::min<size_t>(65535, planes - p0);
+    k_fourier_fft_y<E><<<dim3(unsigned(w / FY_COLS), unsigned(np)), 32 * FY_COLS, smem, ctx->stream>>>(
+        w, r, in + p0 * size_t(n) * w, base ? base + p0 * size_t(n) * r * w : nullptr, out + p0 * size_t(n) * r * w);
     PTB_LAUNCH_CHECK(ctx);
-    check_fft(cufftExecZ2D(b, reinterpret_cast<cufftDoubleComplex*>(sf), stage_out ? stage_out : out), "exec Z2D");
-    ctx->launches.fetch_add(2, std::memory_order_relaxed);
-    if (stage_out)
-      PTB_CUDA_CHECK(cudaMemcpyAsync(out, stage_out, cnt * nf * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
 }
 
-void interpolate_gemm(ptb_transfer* t, const TGeom& g, size_t batch, const double* coarse, double* fine) {
+// fine = [base +] I(coarse) for `batch` fields, x pass into a scratch plane, then y pass
+void interpolate_fft(ptb_transfer* t, const TGeom& g, size_t batch, const double* coarse, const double* base,
+                     double* fine) {
   ptb_context* ctx = t->ctx;
-  if (!t->mx) {
-    const std::vector<double> mx = dense_axis(g.cx, g.rx, true), my = dense_axis(g.cy, g.ry, false);
-    PTB_CUDA_CHECK(cudaMalloc(&t->mx, mx.size() * sizeof(double)));
-    PTB_CUDA_CHECK(cudaMalloc(&t->my, my.size() * sizeof(double)));
-    PTB_CUDA_CHECK(cudaMemcpy(t->mx, mx.data(), mx.size() * sizeof(double), cudaMemcpyHostToDevice));
-    PTB_CUDA_CHECK(cudaMemcpy(t->my, my.data(), my.size() * sizeof(double), cudaMemcpyHostToDevice));
+  double* half = static_cast<double*>(t->spec_c.get(batch * size_t(g.cy) * g.fx * sizeof(double)));
+  const size_t lines = batch * size_t(g.cy);
+  switch (fft_e(g.cx)) {
+    case 1: launch_fft_x<1>(ctx, lines, g.rx, coarse, half); break;
+    case 2: launch_fft_x<2>(ctx, lines, g.rx, coarse, half); break;
+    case 4: launch_fft_x<4>(ctx, lines, g.rx, coarse, half); break;
+    default: launch_fft_x<8>(ctx, lines, g.rx, coarse, half); break;
   }
-  const size_t nc = size_t(g.cy) * g.cx, nh = size_t(g.cy) * g.fx, nf = size_t(g.fy) * g.fx;
-  double* half = static_cast<double*>(ctx->scratch[3].get(batch * nh * sizeof(double)));
-  // row-major products as column-major GEMMs: half_b^T (fx x cy) = Mx^T (fx x cx) . in_b^T (cx x cy)
-  for (size_t b = 0; b < batch; ++b)
-    gemm(ctx, false, false, g.fx, g.cy, g.cx, 1.0, t->mx, g.fx, coarse + b * nc, g.cx, 0.0, half + b * nh, g.fx);
-  // out_b^T (fx x fy) = half_b^T (fx x cy) . My^T (cy x fy)
-  for (size_t b = 0; b < batch; ++b)
-    gemm(ctx, false, false, g.fx, g.fy, g.cy, 1.0, half + b * nh, g.fx, t->my, g.cy, 0.0, fine + b * nf, g.fx);
+  switch (fft_e(g.cy)) {
+    case 1: launch_fft_y<1>(ctx, batch, g.fx, g.ry, half, base, fine); break;
+    case 2: launch_fft_y<2>(ctx, batch, g.fx, g.ry, half, base, fine); break;
+    case 4: launch_fft_y<4>(ctx, batch, g.fx, g.ry, half, base, fine); break;
+    default: launch_fft_y<8>(ctx, batch, g.fx, g.ry, half, base, fine); break;
+  }
 }
+
+__global__ void k_add_base(size_t total, const double* __restrict__ base, double* out) {
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x)
+    out[e] = base[e] + out[e];
+}
+
 }  // namespace
 
 void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, double* fine) {
@@ -388,11 +586,7 @@ void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, dou
     return;
   }
   if (use_fft(g)) {
-    interpolate_fft(t, g, batch, coarse, fine);
-    return;
-  }
-  if (use_gemm(g)) {
-    interpolate_gemm(t, g, batch, coarse, fine);
+    interpolate_fft(t, g, batch, coarse, nullptr, fine);
     return;
   }
   // Fourier: x pass into scratch (cy x fx), then y pass (fy x fx)
@@ -412,6 +606,25 @@ void interpolate_fields(ptb_transfer* t, size_t batch, const double* coarse, dou
     k_copy<<<blocks_for(ctx, batch * nf), 256, 0, ctx->stream>>>(batch * nf, coarse, fine);
     PTB_LAUNCH_CHECK(ctx);
   }
+}
+
+// out = base + I(coarse): the fine combine next = fine_next + I(d) (base may alias out); fused
+// into the y pass on the warp-FFT route, a separate add otherwise
+void interpolate_fields_add(ptb_transfer* t, size_t batch, const double* coarse, const double* base, double* out,
+                            double* scratch) {
+  ptb_context* ctx = t->ctx;
+  const TGeom g = geom(t);
+  if (batch == 0) return;
+  if (t->kind == PTB_INTERP_FOURIER && !(g.rx == 1 && g.ry == 1) && use_fft(g)) {
+    interpolate_fft(t, g, batch, coarse, base, out);
+    return;
+  }
+  const size_t total = batch * size_t(g.fy) * g.fx;
+  interpolate_fields(t, batch, coarse, scratch);
+  k_add_base<<<blocks_for(ctx, total), 256, 0, ctx->stream>>>(total, base, scratch);
+  PTB_LAUNCH_CHECK(ctx);
+  if (scratch != out) PTB_CUDA_CHECK(cudaMemcpyAsync(out, scratch, total * sizeof(double), cudaMemcpyDeviceToDevice,
+                                                     ctx->stream));
 }
 
 void interpolate_at_coarse_nodes(ptb_transfer* t, size_t batch, const double* coarse, double* out) {

@@ -26,6 +26,14 @@ def mats():
     a[:300, 20] = rng.standard_normal(300)
     a[:, 30] = 2.0 * a[:, 7]
     out.append(a)
+    # snapshot-like: whole TSQR leaves of tiny entries (rows far from the wave: squares underflow,
+    # some entries denormal) stacked with O(1) rows -- the reflectors of those leaves must stay
+    # orthogonal (config 3's first snapshot block exposed this)
+    a = rng.standard_normal((49152, 64)) @ np.diag(np.logspace(0, -5, 64))
+    a[3000:9000] *= 1e-160
+    a[20000:26000] *= 1e-300
+    a[40000:41000] *= 1e-310
+    out.append(a)
     return out
 
 

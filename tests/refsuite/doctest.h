@@ -107,9 +107,21 @@ inline void report(bool ok, const char* expr, const char* file, int line, bool r
   } while (0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
-int main() {
+// --test-case-exclude=<prefix>* (doctest's option; only trailing-* patterns are supported here)
+int main(int argc, char** argv) {
+  std::string exclude;
+  for (int i = 1; i < argc; ++i) {
+    const std::string a = argv[i], key = "--test-case-exclude=";
+    if (a.rfind(key, 0) == 0) exclude = a.substr(key.size());
+  }
+  if (!exclude.empty() && exclude.back() == '*') exclude.pop_back();
   int failed_cases = 0;
+  size_t skipped = 0;
   for (const auto& c : doctest::detail::registry()) {
+    if (!exclude.empty() && std::string(c.name).rfind(exclude, 0) == 0) {
+      ++skipped;
+      continue;
+    }
     doctest::detail::current() = c.name;
     const int before = doctest::detail::failures();
     try {
@@ -121,9 +133,10 @@ int main() {
     }
     if (doctest::detail::failures() != before) ++failed_cases;
   }
-  std::printf("[doctest] test cases: %zu | passed: %zu | failed: %d | checks: %d | failed checks: %d\n",
-              doctest::detail::registry().size(), doctest::detail::registry().size() - size_t(failed_cases),
-              failed_cases, doctest::detail::checks(), doctest::detail::failures());
+  std::printf("[doctest] test cases: %zu | passed: %zu | failed: %d | skipped: %zu | checks: %d | failed checks: %d\n",
+              doctest::detail::registry().size() - skipped,
+              doctest::detail::registry().size() - skipped - size_t(failed_cases), failed_cases, skipped,
+              doctest::detail::checks(), doctest::detail::failures());
   return doctest::detail::failures() == 0 ? 0 : 1;
 }
 #endif

@@ -126,7 +126,12 @@ def pml_plain_sharded(u0, v0, kf, m_f, kc, m_c, t, N, K):
     a = min(N + 1, 1 + rank * chunk)
     b = min(N + 1, a + chunk)
     R = lambda s: tuple(P.restrict_field(f, t) for f in s)  # noqa: E731
-    I = lambda s: tuple(P.interpolate_field(f, t) for f in s)  # noqa: E731
+    damped = (kf.zy[:, None] != 0.0) | (kf.zx[None, :] != 0.0)
+
+    def I(s):  # noqa: E743  (px, py cut back to the layer, as oracle/pml_np.plain_parareal)
+        u, v, px, py = (P.interpolate_field(f, t) for f in s)
+        return u, v, np.where(damped, px, 0.0), np.where(damped, py, 0.0)
+
     Fp = lambda s: M.pml_steps(*s, kf, m_f)  # noqa: E731
     Cp = lambda s: M.pml_steps(*s, kc, m_c)  # noqa: E731
     z = np.zeros_like(u0)
@@ -154,6 +159,9 @@ def pml_plain_sharded(u0, v0, kf, m_f, kc, m_c, t, N, K):
             d[n] = tuple(x - y for x, y in zip(g, old))
             w = tuple(x + y for x, y in zip(rf, d[n]))
         nxt = {n: tuple(x + y for x, y in zip(fine_next[n], I(d[n]))) for n in range(a, b)}
+        for n in range(a, b):  # non-finite iterates clamped to the previous one
+            if not all(np.all(np.isfinite(f)) for f in nxt[n]):
+                nxt[n] = cur[n]
         if a == 1:
             nxt[0] = init
         # boundary: the last own state to the next rank

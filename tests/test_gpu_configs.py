@@ -35,11 +35,12 @@ def _check(ref, spec, cf, cc, u0, v0):
     assert list(gpu["rank"]) == list(want["rank"]), (gpu["rank"], want["rank"])
     assert list(gpu["diverged"]) == list(want["diverged"])
     ee, l2 = T.iterate_distance(ref, gpu["states"], want["states"], cf, T.fine_grid(spec), spec["metric_scheme"])
+    print("iterate energy distance per k", ee.max(axis=1), "l2", l2.max(axis=1))
+    assert ee.max() <= ITERATE_TOL, (ee.max(axis=1), ee.argmax())
+    assert l2.max() <= L2_TOL, l2.max(axis=1)
     # the per-iteration error tables against the serial fine run agree as well
     np.testing.assert_allclose(gpu["energy_err"], want["energy_err"], rtol=1e-7, atol=1e-13)
     np.testing.assert_allclose(gpu["l2_err"], want["l2_err"], rtol=1e-7, atol=1e-13)
-    assert ee.max() <= ITERATE_TOL, (ee.max(axis=1), ee.argmax())
-    assert l2.max() <= L2_TOL, l2.max(axis=1)
     return gpu, want, ee
 
 
@@ -53,12 +54,14 @@ def test_config3_theta_iterates_match_reference(ref):
     _check(ref, *W.cfg3())
 
 
-def test_config4_reduced_theta_iterates_match_reference(ref):
+def test_config4_reduced_theta_iterates_match_reference(ref, monkeypatch):
     """BASELINE config 4 (periodic) over its first 16 couplings, K = 2: the full 2048^2 / 256^2
-    schedule (m_F = 128, m_C = 8, sigma = 4 smoothing), and a corrector of 196608 x r > 4M
-    entries, i.e. the device sweep's large-corrector branch that the full config runs."""
+    schedule (m_F = 128, m_C = 8, sigma = 4 smoothing).  The sweep's large-corrector branch
+    (the one the full config's 196608 x ~1000 corrector takes) is forced by lowering its
+    threshold below this run's 196608 x r entries."""
+    monkeypatch.setenv("PTB_FUSED_SWEEP_MAX", "1000000")
     gpu, want, ee = _check(ref, *T.reduced_cfg4())
-    assert gpu["rank"][-1] * 3 * 256 * 256 > 4_000_000
+    assert gpu["rank"][-1] * 3 * 256 * 256 > 1_000_000
 
 
 def test_config1_plain_and_theta_default_tol(ref):

@@ -130,8 +130,12 @@ def test_transfer_known_answers_on_gpu(impls, check):
 @pytest.mark.parametrize("kind", [0, 1])
 @pytest.mark.parametrize("shapes", [((32, 32), (128, 128)), ((64, 64), (256, 256)), ((6, 10), (18, 30)),
                                     ((20,), (100,)), ((12, 16), (12, 64)), ((9, 8), (27, 8)),
-                                    # fine >= 512^2: the dense-GEMM route (transfer.cu interpolate_gemm)
-                                    ((128, 128), (512, 512)), ((64, 96), (512, 768)), ((256, 256), (1024, 1024))])
+                                    # fine >= 256^2, power-of-two coarse axes: the warp-FFT route
+                                    # (transfer.cu k_fourier_fft_x/y), odd ratios included; 64 x 96
+                                    # has a non-power-of-two axis: the direct circulant passes
+                                    ((128, 128), (512, 512)), ((64, 96), (512, 768)), ((256, 256), (1024, 1024)),
+                                    ((256, 256), (2048, 2048)), ((32, 32), (256, 256)), ((128, 64), (384, 512)),
+                                    ((64, 128), (512, 256))])
 def test_transfer_parity(impls, kind, shapes):
     cs, fs = shapes
     coarse = P.Grid(cs, tuple(1.0 / k for k in cs))

@@ -97,8 +97,8 @@ def test_host_profile_matches_oracle_bitwise():
         assert np.array_equal(B.damping_profile(n, w, h, cmax, R), M.damping_profile(n, w, h, cmax, R))
 
 
-def _small_parareal(kind=0, N=6, K=3):
-    nf, nc, W = 64, 16, 8
+def _small_parareal(kind=0, N=6, K=3, nf=64, W=8):
+    nc = nf // 4
     hf, hc = 1 / nf, 1 / nc
     rng = np.random.default_rng(11)
     c = 0.7 + 0.3 * rng.random((nf, nf))
