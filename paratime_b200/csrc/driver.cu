@@ -234,6 +234,78 @@ __global__ void __launch_bounds__(AD_I * AD_J) k_assemble_d(size_t nc, int r, co
   }
 }
 
+// Row-sharded sweep products of a large corrector (3 N_c x r, cfg4): the rows of Y are cut into
+// SWEEP_BLOCKS fixed blocks; block b belongs to rank b % world.  part[b][j] = Y[rows_b, j] . x[rows_b]
+// (fixed-order tree per block), then z[j] = sum_b part[b][j] in block order on every rank: the
+// value does not depend on the world size.
+constexpr int SWEEP_BLOCKS = 8;
+__global__ void __launch_bounds__(256) k_zt_blocks(size_t rows, size_t bl, const double* __restrict__ Y, size_t ld,
+                                                   const double* __restrict__ x, int r, int rank, int world,
+                                                   double* __restrict__ part) {
+  const int j = blockIdx.x, b = blockIdx.y;
+  if (b % world != rank) return;
+  const size_t r0 = size_t(b) * bl, r1 = min(rows, r0 + bl);
+  const double* col = Y + size_t(j) * ld;
+  double s = 0.0;
+  for (size_t i = r0 + threadIdx.x; i < r1; i += 256) s = fma(col[i], x[i], s);
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[size_t(b) * r + j] = t;
+  }
+}
+// z[j] = sum_b part_of_owner(b)[b][j]; `all` holds world copies of the [SWEEP_BLOCKS][r] array
+__global__ void k_zt_sum(int r, int world, const double* __restrict__ all, double* z) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < SWEEP_BLOCKS; ++b) s += all[(size_t(b % world) * SWEEP_BLOCKS + b) * r + j];
+    z[j] = s;
+  }
+}
+// d rows [i0, i1) of both blocks: seg = [du rows | dv rows] of this rank, sg rows each
+__global__ void k_zd_rows(int i0, int i1, int sg, int r, const double* __restrict__ Zu, const double* __restrict__ Zv,
+                          size_t ld, const double* __restrict__ dz, double* seg) {
+  extern __shared__ double dzs[];
+  for (int k = threadIdx.x; k < r; k += blockDim.x) dzs[k] = dz[k];
+  __syncthreads();
+  const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
+  double su = 0.0, sv = 0.0;  // sequential in k (fixed order), loads issued 8 columns ahead
+  int k = 0;
+  for (; k + 8 <= r; k += 8) {
+    double tu[8], tv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      tu[q] = Zu[i + size_t(k + q) * ld];
+      tv[q] = Zv[i + size_t(k + q) * ld];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      su = fma(tu[q], dzs[k + q], su);
+      sv = fma(tv[q], dzs[k + q], sv);
+    }
+  }
+  for (; k < r; ++k) {
+    su = fma(Zu[i + size_t(k) * ld], dzs[k], su);
+    sv = fma(Zv[i + size_t(k) * ld], dzs[k], sv);
+  }
+  seg[i - i0] = su;
+  seg[sg + i - i0] = sv;
+}
+// gathered segments (world x [du sg | dv sg]) -> du, dv (n rows)
+__global__ void k_zd_unpack(size_t n, int sg, const double* __restrict__ all, double* du, double* dv) {
+  GRID_STRIDE(i, n) {
+    const size_t rr = i / size_t(sg), o = i - rr * size_t(sg);
+    du[i] = all[rr * 2 * size_t(sg) + o];
+    dv[i] = all[rr * 2 * size_t(sg) + sg + o];
+  }
+}
+
 __global__ void k_add_mean(size_t n, const double* mnew, const double* mold, double* u) {
   const double dm = mold ? __dsub_rn(*mnew, *mold) : *mnew;
   const double v = dm / double(n);
@@ -256,7 +328,7 @@ __global__ void k_or_flags(int32_t* out, const int32_t* a, const int32_t* b, con
 }  // namespace
 
 // Work buffers reused by successive runs on one context (ptb_context::driver_cache).
-constexpr int kDriverBuffers = 56;
+constexpr int kDriverBuffers = 64;
 struct DriverCache {
   EnergyWork ew;
   ProcWork pw;
@@ -295,6 +367,7 @@ struct Driver {
   DeviceBuffer ff, cf, wf, bad, sflags, sums_own, sums_all, own_sc, all_sc;
   DeviceBuffer rn_u, rn_v, ri_u, ri_v, init_u, init_v, init_cu, init_cv;
   DeviceBuffer comp, mean, comp_old, mean_old, zold, zw, Zu, Zv, Fm, Gm, idx, tmpc;
+  DeviceBuffer zpart, zpart_all, dseg, dseg_all;  // row-sharded large-corrector sweep
   std::vector<int32_t> ref_bad;
   int zw_parts = 1;  // partials per z_w entry written by corrected_batch (batch 1)
 
@@ -313,7 +386,8 @@ struct Driver {
             &rf_u, &rf_v, &kn_u, &kn_v, &d_u, &d_v, &w_u, &w_v, &rik_u, &rik_v, &own_pay, &all_pay,
             &ff, &cf, &wf, &bad, &sflags, &sums_own, &sums_all, &own_sc, &all_sc,
             &rn_u, &rn_v, &ri_u, &ri_v, &init_u, &init_v, &init_cu, &init_cv,
-            &comp, &mean, &comp_old, &mean_old, &zold, &zw, &Zu, &Zv, &Fm, &Gm, &idx, &tmpc};
+            &comp, &mean, &comp_old, &mean_old, &zold, &zw, &Zu, &Zv, &Fm, &Gm, &idx, &tmpc,
+            &zpart, &zpart_all, &dseg, &dseg_all};
   }
 
   Driver(ptb_context* c, const Comm* cm, const ptb_run_spec& spec)
@@ -679,11 +753,50 @@ struct Driver {
       k_gemv_t1<<<dim3(unsigned(c.rank), unsigned(P)), 256, 0, st()>>>(rows, (rows + P - 1) / P, c.Yp(), rows, cp,
                                                                        zout);
       PTB_LAUNCH_CHECK(ctx);
+    } else if (batch == 1) {  // large corrector: the row-sharded product (bitwise the same at any world)
+      zw_parts = 1;
+      sharded_zt(c, cp, zout);
     } else {
-      if (batch == 1) zw_parts = 1;
       gemm(ctx, true, false, c.rank, int(batch), int(rows), 1.0, c.Yp(), int(rows), cp, int(rows), 0.0, zout,
            c.rank);
     }
+  }
+
+  // z = Y^T x for a large corrector, rows split over the ranks in SWEEP_BLOCKS fixed blocks
+  void sharded_zt(const DevCorrector& c, const double* x, double* z) {
+    const size_t rows = size_t(cg.dim + 1) * nc;
+    const int r = c.rank, W = comm->world;
+    const size_t bl = (rows + SWEEP_BLOCKS - 1) / SWEEP_BLOCKS, arr = size_t(SWEEP_BLOCKS) * r;
+    double* part = dalloc<double>(zpart, arr);
+    k_zt_blocks<<<dim3(unsigned(r), SWEEP_BLOCKS), 256, 0, st()>>>(rows, bl, c.Yp(), rows, x, r, comm->rank, W, part);
+    PTB_LAUNCH_CHECK(ctx);
+    const double* all = part;
+    if (W > 1) {
+      double* g = dalloc<double>(zpart_all, arr * size_t(W));
+      comm->allgather(part, g, arr * sizeof(double), st());
+      all = g;
+    }
+    k_zt_sum<<<unsigned((r + 255) / 256), 256, 0, st()>>>(r, W, all, z);
+    PTB_LAUNCH_CHECK(ctx);
+  }
+
+  // du = Zu dz, dv = Zv dz for a large corrector: each rank its own row segment, one all-gather
+  void sharded_zd(int r, const double* dz, double* du, double* dv) {
+    const int W = comm->world, sg = int((nc + size_t(W) - 1) / size_t(W));
+    const int i0 = std::min(int(nc), comm->rank * sg), i1 = std::min(int(nc), i0 + sg);
+    double* seg = dalloc<double>(dseg, 2 * size_t(sg));
+    if (i1 > i0)
+      k_zd_rows<<<unsigned((i1 - i0 + 255) / 256), 256, size_t(r) * sizeof(double), st()>>>(
+          i0, i1, sg, r, static_cast<const double*>(Zu.ptr), static_cast<const double*>(Zv.ptr), nc, dz, seg);
+    PTB_LAUNCH_CHECK(ctx);
+    const double* all = seg;
+    if (W > 1) {
+      double* g = dalloc<double>(dseg_all, 2 * size_t(sg) * size_t(W));
+      comm->allgather(seg, g, 2 * size_t(sg) * sizeof(double), st());
+      all = g;
+    }
+    k_zd_unpack<<<blocks(ctx, nc), 256, 0, st()>>>(nc, sg, all, du, dv);
+    PTB_LAUNCH_CHECK(ctx);
   }
 
   // ---- sweeps (coarse, replicated) --------------------------------------------------------
@@ -716,7 +829,8 @@ struct Driver {
       PTB_LAUNCH_CHECK(ctx);
       return;
     }
-    // large corrector (cfg4: 3 N_c x r = 30 M entries): cuBLAS GEMVs stream Zu, Zv faster
+    // large corrector (cfg4: 3 N_c x r up to ~200 M entries): HBM-bound GEMVs, rows sharded
+    // over the ranks (each streams 1/world of Zu, Zv), d all-gathered
     double* dz = dalloc<double>(tmpc, std::max(r, 1));
     if (r > 0) {
       if (zold_) {
@@ -725,8 +839,7 @@ struct Driver {
       } else {
         copy(dz, zw_, size_t(r));
       }
-      gemm(ctx, false, false, int(nc), 1, r, 1.0, static_cast<double*>(Zu.ptr), int(nc), dz, r, 0.0, du, int(nc));
-      gemm(ctx, false, false, int(nc), 1, r, 1.0, static_cast<double*>(Zv.ptr), int(nc), dz, r, 0.0, dv, int(nc));
+      sharded_zd(r, dz, du, dv);
     } else {
       PTB_CUDA_CHECK(cudaMemsetAsync(du, 0, nc * sizeof(double), st()));
       PTB_CUDA_CHECK(cudaMemsetAsync(dv, 0, nc * sizeof(double), st()));

@@ -388,7 +388,11 @@ __global__ void __launch_bounds__(256) k_pair_sums2d(Geo G, Beta B, const double
   const double* VB = vb + pr * sb;
   const int nx = G.nx, ny = G.ny;
   double sd = 0.0, sr = 0.0, ld = 0.0, lr = 0.0;
-  for (int r = blockIdx.x; r < ny; r += gridDim.x) {
+  // a contiguous band of rows per block: the y-neighbour rows of row r were rows of the band's
+  // previous iterations, so they come from this SM's L1 instead of L2
+  const int band = (ny + int(gridDim.x) - 1) / int(gridDim.x);
+  const int r_end = min(ny, (int(blockIdx.x) + 1) * band);
+  for (int r = int(blockIdx.x) * band; r < r_end; ++r) {
     int rp[4], rm[4];
 #pragma unroll
     for (int j = 1; j <= 4; ++j) {

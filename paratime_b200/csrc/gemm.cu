@@ -15,9 +15,9 @@
 // (sm80 d884) kernels on the corrector's shapes.
 //
 // Kernels
-//   k_dgemm<TA, TB>  64 x 64 CTA tile, BK = 16, 256 threads, 4 x 4 outputs per thread
-//                    (rows {2ty, 2ty+1, 32+2ty, 33+2ty}, columns likewise from tx: every
-//                    LDS.128 of a quarter warp is 128 contiguous bytes), global loads staged in
+//   k_dgemm<TA, TB>  128 x 64 CTA tile, BK = 16, 256 threads, 8 x 4 outputs per thread
+//                    (rows 32p + 2ty + {0,1}, columns 32q + 2tx + {0,1}: every LDS.128 of a
+//                    quarter warp is 128 contiguous bytes or a broadcast), global loads staged in
 //                    registers one k-tile ahead (double-buffered shared memory, one barrier per
 //                    k-tile).  Split-K over blockIdx.z for the corrector's tall-skinny
 //                    products (k = 3 N_c up to 196608, m, n <= ~1100): partial tiles go to a
@@ -36,8 +36,10 @@
 namespace ptb {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, GT = 256;
+constexpr int BM = 128, BN = 64, BK = 16, GT = 256;
 constexpr int LDS_A = BM + 2, LDS_B = BN + 2;  // padded rows, 16-byte aligned
+constexpr int AL = BM * BK / GT, BL = BN * BK / GT;  // staged global loads per thread: 8 of A, 4 of B
+constexpr size_t GEMM_SMEM = size_t(2) * BK * (LDS_A + LDS_B) * sizeof(double);  // 49 KB: dynamic
 
 struct GemmArgs {
   int m, n, k;
@@ -52,78 +54,85 @@ struct GemmArgs {
   double* ws;  // split-K partials [z][n][m] (null: write C)
 };
 
-// op(A) tile (BM x BK) of k-tile k0 into registers: 4 values per thread
+// op(A) tile (BM x BK) of k-tile k0 into registers.  !TA: A(i, kk) = A[i + kk lda], a warp reads
+// 32 consecutive rows; TA: op(A)(i, kk) = A[kk + i lda], a half warp reads 16 consecutive k.  One
+// base pointer per thread, constant strides; bounds checks only on edge tiles.
 template <bool TA>
-__device__ __forceinline__ void load_a(const GemmArgs& a, int i0, int k0, int kend, double (&r)[4]) {
+__device__ __forceinline__ void load_a(const GemmArgs& a, int i0, int k0, int kend, double (&r)[AL]) {
   const int t = threadIdx.x;
+  const int ib = TA ? t / BK : t % BM, kb = TA ? t % BK : t / BM;  // element j: (ib + di j, kb + dk j)
+  constexpr int di = TA ? GT / BK : 0, dk = TA ? 0 : GT / BM;
+  const size_t lda = size_t(a.lda);
+  const double* p = TA ? a.A + (k0 + kb) + size_t(i0 + ib) * lda : a.A + (i0 + ib) + size_t(k0 + kb) * lda;
+  const size_t step = TA ? size_t(di) * lda : size_t(dk) * lda;
+  if (i0 + BM <= a.m && k0 + BK <= kend) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    int i, kk;
-    if (!TA) {  // A(i, kk) = A[i + kk lda]: a warp reads 32 consecutive rows
-      i = t % BM;
-      kk = t / BM + 4 * j;
-    } else {  // op(A)(i, kk) = A[kk + i lda]: a warp reads 2 x 16 consecutive k
-      kk = t % BK;
-      i = t / BK + 16 * j;
-    }
-    const int gi = i0 + i, gk = k0 + kk;
-    r[j] = (gi < a.m && gk < kend) ? (TA ? a.A[gk + size_t(gi) * a.lda] : a.A[gi + size_t(gk) * a.lda]) : 0.0;
+    for (int j = 0; j < AL; ++j) r[j] = p[j * step];
+  } else {
+#pragma unroll
+    for (int j = 0; j < AL; ++j)
+      r[j] = (i0 + ib + di * j < a.m && k0 + kb + dk * j < kend) ? p[j * step] : 0.0;
   }
 }
 template <bool TA>
-__device__ __forceinline__ void store_a(double* As, const double (&r)[4]) {
+__device__ __forceinline__ void store_a(double* As, const double (&r)[AL]) {
   const int t = threadIdx.x;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int i = TA ? t / BK + 16 * j : t % BM, kk = TA ? t % BK : t / BM + 4 * j;
+  for (int j = 0; j < AL; ++j) {
+    const int i = TA ? t / BK + (GT / BK) * j : t % BM, kk = TA ? t % BK : t / BM + (GT / BM) * j;
     As[kk * LDS_A + i] = r[j];
   }
 }
-// op(B) tile (BK x BN)
+// op(B) tile (BK x BN).  TB: op(B)(kk, c) = B[c + kk ldb], contiguous in c; else B(kk, c) =
+// B[kk + c ldb], contiguous in kk
 template <bool TB>
-__device__ __forceinline__ void load_b(const GemmArgs& a, int j0, int k0, int kend, double (&r)[4]) {
+__device__ __forceinline__ void load_b(const GemmArgs& a, int j0, int k0, int kend, double (&r)[BL]) {
   const int t = threadIdx.x;
+  const int cb = TB ? t % BN : t / BK, kb = TB ? t / BN : t % BK;
+  constexpr int dc = TB ? 0 : GT / BK, dk = TB ? GT / BN : 0;
+  const size_t ldb = size_t(a.ldb);
+  const double* p = TB ? a.B + (j0 + cb) + size_t(k0 + kb) * ldb : a.B + (k0 + kb) + size_t(j0 + cb) * ldb;
+  const size_t step = TB ? size_t(dk) * ldb : size_t(dc) * ldb;
+  if (j0 + BN <= a.n && k0 + BK <= kend) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    int c, kk;
-    if (TB) {  // op(B)(kk, c) = B[c + kk ldb]: contiguous in c
-      c = t % BN;
-      kk = t / BN + 4 * j;
-    } else {  // B(kk, c) = B[kk + c ldb]: contiguous in kk
-      kk = t % BK;
-      c = t / BK + 16 * j;
-    }
-    const int gc = j0 + c, gk = k0 + kk;
-    r[j] = (gc < a.n && gk < kend) ? (TB ? a.B[gc + size_t(gk) * a.ldb] : a.B[gk + size_t(gc) * a.ldb]) : 0.0;
+    for (int j = 0; j < BL; ++j) r[j] = p[j * step];
+  } else {
+#pragma unroll
+    for (int j = 0; j < BL; ++j)
+      r[j] = (j0 + cb + dc * j < a.n && k0 + kb + dk * j < kend) ? p[j * step] : 0.0;
   }
 }
 template <bool TB>
-__device__ __forceinline__ void store_b(double* Bs, const double (&r)[4]) {
+__device__ __forceinline__ void store_b(double* Bs, const double (&r)[BL]) {
   const int t = threadIdx.x;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int c = TB ? t % BN : t / BK + 16 * j, kk = TB ? t / BN + 4 * j : t % BK;
+  for (int j = 0; j < BL; ++j) {
+    const int c = TB ? t % BN : t / BK + (GT / BK) * j, kk = TB ? t / BN + (GT / BN) * j : t % BK;
     Bs[kk * LDS_B + c] = r[j];
   }
 }
 
+// thread (tx, ty) = (t % 16, t / 16) owns rows 32 p + 2 ty + h (p < 4) and columns 32 q + 2 tx + h
+// (q < 2), h in {0, 1}: 8 x 4 accumulators; per k step 4 + 2 LDS.128, the A ones shared by the
+// 16 lanes of a row group (broadcast), the B ones 128 contiguous bytes per quarter warp
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(GT) k_dgemm(const GemmArgs a) {
-  __shared__ __align__(16) double As[2][BK * LDS_A];
-  __shared__ __align__(16) double Bs[2][BK * LDS_B];
+__global__ void __launch_bounds__(GT, 1) k_dgemm(const GemmArgs a) {
+  extern __shared__ __align__(16) double gsm[];  // A stages [2][BK][LDS_A], then B stages [2][BK][LDS_B]
+  double* const Asm = gsm;
+  double* const Bsm = gsm + 2 * BK * LDS_A;
   const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
   const int kbeg = blockIdx.z * a.kchunk, kend = min(a.k, kbeg + a.kchunk);
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  double acc[4][4];
+  double acc[8][4];
 #pragma unroll
-  for (int p = 0; p < 4; ++p)
+  for (int p = 0; p < 8; ++p)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
-  double ra[4], rb[4];
+  double ra[AL], rb[BL];
   load_a<TA>(a, i0, kbeg, kend, ra);
   load_b<TB>(a, j0, kbeg, kend, rb);
-  store_a<TA>(As[0], ra);
-  store_b<TB>(Bs[0], rb);
+  store_a<TA>(Asm, ra);
+  store_b<TB>(Bsm, rb);
   __syncthreads();
   int buf = 0;
   for (int k0 = kbeg; k0 < kend; k0 += BK) {
@@ -132,34 +141,42 @@ __global__ void __launch_bounds__(GT) k_dgemm(const GemmArgs a) {
       load_a<TA>(a, i0, k0 + BK, kend, ra);
       load_b<TB>(a, j0, k0 + BK, kend, rb);
     }
-    const double* as = As[buf];
-    const double* bs = Bs[buf];
+    const double* as = Asm + buf * (BK * LDS_A);
+    const double* bs = Bsm + buf * (BK * LDS_B);
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      const double2 a0 = *reinterpret_cast<const double2*>(as + kk * LDS_A + 2 * ty);
-      const double2 a1 = *reinterpret_cast<const double2*>(as + kk * LDS_A + 32 + 2 * ty);
-      const double2 b0 = *reinterpret_cast<const double2*>(bs + kk * LDS_B + 2 * tx);
-      const double2 b1 = *reinterpret_cast<const double2*>(bs + kk * LDS_B + 32 + 2 * tx);
-      const double av[4] = {a0.x, a0.y, a1.x, a1.y}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
+      double av[8], bv[4];
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
+      for (int p = 0; p < 4; ++p) {
+        const double2 t2 = *reinterpret_cast<const double2*>(as + kk * LDS_A + 32 * p + 2 * ty);
+        av[2 * p] = t2.x;
+        av[2 * p + 1] = t2.y;
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double2 t2 = *reinterpret_cast<const double2*>(bs + kk * LDS_B + 32 * q + 2 * tx);
+        bv[2 * q] = t2.x;
+        bv[2 * q + 1] = t2.y;
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[p][q] = fma(av[p], bv[q], acc[p][q]);
     }
     if (more) {
-      store_a<TA>(As[buf ^ 1], ra);
-      store_b<TB>(Bs[buf ^ 1], rb);
+      store_a<TA>(Asm + (buf ^ 1) * (BK * LDS_A), ra);
+      store_b<TB>(Bsm + (buf ^ 1) * (BK * LDS_B), rb);
     }
     __syncthreads();
     buf ^= 1;
   }
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int i = i0 + (p < 2 ? 2 * ty + p : 32 + 2 * ty + p - 2);
+  for (int p = 0; p < 8; ++p) {
+    const int i = i0 + 32 * (p / 2) + 2 * ty + (p & 1);
     if (i >= a.m) continue;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int j = j0 + (q < 2 ? 2 * tx + q : 32 + 2 * tx + q - 2);
+      const int j = j0 + 32 * (q / 2) + 2 * tx + (q & 1);
       if (j >= a.n) continue;
       if (a.ws) {
         a.ws[(size_t(blockIdx.z) * a.n + j) * a.m + i] = acc[p][q];
@@ -192,14 +209,18 @@ __global__ void k_gemv_n(int m, int k, double alpha, const double* __restrict__ 
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
-  double s0 = 0.0, s1 = 0.0;  // two chains: even / odd columns (more loads in flight)
+  // one sequential chain per row (a fixed order), loads issued 8 columns ahead of the FMAs
+  double s = 0.0;
+  const double* a = A + i;
   int j = 0;
-  for (; j + 1 < k; j += 2) {
-    s0 = fma(A[i + size_t(j) * lda], xs[j], s0);
-    s1 = fma(A[i + size_t(j + 1) * lda], xs[j + 1], s1);
+  for (; j + 8 <= k; j += 8) {
+    double t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = a[size_t(j + q) * lda];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = fma(t[q], xs[j + q], s);
   }
-  if (j < k) s0 = fma(A[i + size_t(j) * lda], xs[j], s0);
-  const double s = s0 + s1;
+  for (; j < k; ++j) s = fma(a[size_t(j) * lda], xs[j], s);
   y[i] = beta == 0.0 ? alpha * s : alpha * s + beta * y[i];
 }
 
@@ -276,10 +297,19 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
   GemmArgs a{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, nullptr};
   if (splits > 1) a.ws = workspace(ctx, size_t(splits) * m * n);
   const dim3 grid{unsigned(tm), unsigned(tn), unsigned(splits)};
-  if (!ta && !tb) k_dgemm<false, false><<<grid, GT, 0, st>>>(a);
-  else if (ta && !tb) k_dgemm<true, false><<<grid, GT, 0, st>>>(a);
-  else if (!ta && tb) k_dgemm<false, true><<<grid, GT, 0, st>>>(a);
-  else k_dgemm<true, true><<<grid, GT, 0, st>>>(a);
+  static const bool attrs = [] {
+    for (const void* f : {reinterpret_cast<const void*>(k_dgemm<false, false>),
+                          reinterpret_cast<const void*>(k_dgemm<true, false>),
+                          reinterpret_cast<const void*>(k_dgemm<false, true>),
+                          reinterpret_cast<const void*>(k_dgemm<true, true>)})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GEMM_SMEM));
+    return true;
+  }();
+  (void)attrs;
+  if (!ta && !tb) k_dgemm<false, false><<<grid, GT, GEMM_SMEM, st>>>(a);
+  else if (ta && !tb) k_dgemm<true, false><<<grid, GT, GEMM_SMEM, st>>>(a);
+  else if (!ta && tb) k_dgemm<false, true><<<grid, GT, GEMM_SMEM, st>>>(a);
+  else k_dgemm<true, true><<<grid, GT, GEMM_SMEM, st>>>(a);
   PTB_LAUNCH_CHECK(ctx);
   if (splits > 1) {
     k_splitk_reduce<<<ew_grid(ctx, size_t(m) * n), 256, 0, st>>>(m, n, splits, a.ws, alpha, beta, C, ldc);

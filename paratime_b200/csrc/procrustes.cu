@@ -1591,34 +1591,45 @@ __global__ void __launch_bounds__(QRR_THREADS) k_qr_reg(const QrRegArgs a0, cons
       // the pivot's slot is dynamic: gather it with explicit selects (an indexed read would move
       // the whole register tile to local memory)
       const int sp = p / QRR_WARPS;
-      double cv[RPL], amax = 0.0;
+      double cv[RPL], xs = 0.0;
 #pragma unroll
       for (int u = 0; u < RPL; ++u) {
         double c = x[0][u];
 #pragma unroll
         for (int s = 1; s < CPW; ++s) c = selp(sp == s, x[s][u], c);
         cv[u] = c;
-        if (lane + 32 * u >= j) amax = fmax(amax, fabs(c));
+        if (lane + 32 * u > j) xs = fma(c, c, xs);
       }
 #pragma unroll
       for (int s = 0; s < CPW; ++s) estep[s] = selp(sp == s, j, estep[s]);
-      // dlarfg on the column scaled by 2^-ex (max |entry| in [1, 2)): a TSQR leaf can hold a
-      // column of tiny entries (snapshot rows far from the wave, down to denormals) whose squares
-      // underflow; an unscaled norm then yields a non-orthogonal reflector, harmless for the tiny
-      // leaf data but not for the O(1) rows the down-sweep applies it to.  Power-of-two scaling is
-      // exact, so well-scaled columns get the same reflector as before.
-      for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      const int ex = amax > 0.0 ? ilogb(amax) : 0;
-      double xs = 0.0, alc = 0.0;
+      xs = warp_sum(xs);
+      // dlarfg on the column scaled by 2^-ex (max |entry| in [1, 2)) when its squares may have
+      // underflowed: a TSQR leaf can hold a column of tiny entries (snapshot rows far from the
+      // wave, down to denormals); an unscaled norm then yields a non-orthogonal reflector,
+      // harmless for the tiny leaf data but not for the O(1) rows the down-sweep applies it to.
+      // Above 2^-600 every underflowed square is below 2^-200 of the norm: no scaling (ex = 0).
+      int ex = 0;
+      if (xs < 0x1p-600) {  // warp-uniform (xs is the warp total)
+        double amax = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u)
+          if (lane + 32 * u >= j) amax = fmax(amax, fabs(cv[u]));
+        for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        ex = amax > 0.0 ? ilogb(amax) : 0;
+        xs = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          cv[u] = scalbn(cv[u], -ex);
+          if (lane + 32 * u > j) xs = fma(cv[u], cv[u], xs);
+        }
+        xs = warp_sum(xs);
+      }
+      double alc = 0.0;
 #pragma unroll
       for (int u = 0; u < RPL; ++u) {
-        const double c = scalbn(cv[u], -ex);
-        const int r = lane + 32 * u;
-        if (r > j) xs = fma(c, c, xs);
-        if (u == j / 32) alc = c;
-        cbuf[r] = c;
+        if (u == j / 32) alc = cv[u];
+        cbuf[lane + 32 * u] = cv[u];
       }
-      xs = warp_sum(xs);
       const double al = __shfl_sync(0xffffffffu, alc, j & 31);
       if (lane == 0) {
         double beta, tau, scal;

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(32 * FX_WARPS) k_fourier_fft_x(size_t lines, i
   }
 }
 
-constexpr int FY_COLS = 16;
+constexpr int FY_COLS = 8;  // columns (= warps) per CTA: 64-byte row segments, <= 255 registers
 
 // y pass: plane (n x w) per field -> (n r x w), columns [16 blockIdx.x, +16) of field blockIdx.y;
 // out = base + I (base nullable, may alias out)
@@ -460,12 +460,20 @@ __global__ void __launch_bounds__(32 * FY_COLS) k_fourier_fft_y(int w, int r, co
     tin[c * IP + row] = src[size_t(row) * w + c];
   }
   __syncthreads();
-  // phase 0: the coarse rows themselves
-  for (int i = tid; i < n * FY_COLS; i += 32 * FY_COLS) {
-    const int q = i / FY_COLS, c = i % FY_COLS;
-    const size_t g = off + size_t(q) * r * w + c;
-    const double v = tin[c * IP + q];
-    out[g] = base ? base[g] + v : v;
+  // phase 0: the coarse rows themselves (loads first, as below)
+  {
+    constexpr int PER = n / 32;
+    double bv[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int i = tid + e * 32 * FY_COLS, q = i / FY_COLS, c = i % FY_COLS;
+      bv[e] = base ? base[off + size_t(q) * r * w + c] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int i = tid + e * 32 * FY_COLS, q = i / FY_COLS, c = i % FY_COLS;
+      out[off + size_t(q) * r * w + c] = bv[e] + tin[c * IP + q];
+    }
   }
   LaneTw<E> tw;
   tw.init(lane);
@@ -503,11 +511,19 @@ __global__ void __launch_bounds__(32 * FY_COLS) k_fourier_fft_y(int w, int r, co
       tout[(n + lane + 32 * e) * OP + col] = z[e].y;
     }
     __syncthreads();
-    for (int i = tid; i < cnt * n * FY_COLS; i += 32 * FY_COLS) {
-      const int c = i % FY_COLS, qq = i / FY_COLS, slot = qq / n, q = qq % n;
-      const size_t g = off + (size_t(q) * r + s1 + slot) * w + c;
-      const double v = tout[(slot * n + q) * OP + c];
-      out[g] = base ? base[g] + v : v;
+    // all base loads of this thread first, then the stores (base may alias out: without the
+    // split each store would wait for the next load)
+    constexpr int PER = 2 * n * FY_COLS / (32 * FY_COLS);  // = 2n/32 elements per thread
+    double bv[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int i = tid + e * 32 * FY_COLS, c = i % FY_COLS, qq = i / FY_COLS, slot = qq / n, q = qq % n;
+      bv[e] = (base && slot < cnt) ? base[off + (size_t(q) * r + s1 + slot) * w + c] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int i = tid + e * 32 * FY_COLS, c = i % FY_COLS, qq = i / FY_COLS, slot = qq / n, q = qq % n;
+      if (slot < cnt) out[off + (size_t(q) * r + s1 + slot) * w + c] = bv[e] + tout[(slot * n + q) * OP + c];
     }
     __syncthreads();
   }

@@ -2,13 +2,13 @@ import math, os, sys, json
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import torch
 import paratime_b200 as B
-from bench import medium, pulses
+from workloads import cfg5_medium, cfg5_pulses
 ctx = B.Context(0)
 for n, batch in [(1024, 64), (256, 64), (512, 64)]:
-    c = medium(n, 7)
+    c = cfg5_medium(n)
     dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
     prop = B.Propagator(ctx, B.Grid((n, n), (1.0 / n, 1.0 / n)), c, dt, 64)
-    u = torch.as_tensor(pulses(n, batch, 5), device="cuda")
+    u = torch.as_tensor(cfg5_pulses(n, batch), device="cuda")
     v = torch.zeros_like(u)
     res = []
     for w in (0, 64, 96, 128, 192, 256):

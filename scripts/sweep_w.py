@@ -3,16 +3,16 @@ import math, os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paratime_b200 as B
-from bench import medium, pulses
+from workloads import cfg5_medium, cfg5_pulses
 ctx = B.Context(0)
 cases = [(128, 64), (128, 512), (256, 64), (512, 64), (512, 256), (1024, 64), (2048, 64), (4096, 16), (4096, 64)]
 if len(sys.argv) > 1:
     cases = [tuple(int(x) for x in a.split("x")) for a in sys.argv[1:]]
 for n, batch in cases:
-    c = medium(n, 7)
+    c = cfg5_medium(n)
     dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
     prop = B.Propagator(ctx, B.Grid((n, n), (1.0 / n, 1.0 / n)), c, dt, 64)
-    u = torch.as_tensor(pulses(n, batch, 5), device="cuda")
+    u = torch.as_tensor(cfg5_pulses(n, batch), device="cuda")
     v = torch.zeros_like(u)
     row = {}
     for w in (0, 64, 96, 128, 160, 192, 256):

@@ -1,18 +1,67 @@
-"""cuBLAS DGEMM throughput (torch float64 matmul) at the interpolation / Procrustes shapes."""
-import torch
+"""The hand-written DGEMM (ptb_dgemm, csrc/gemm.cu: DFMA register tiles) against cuBLAS's
+DMMA kernels (torch float64 matmul, measurement only) on the corrector's shapes.
+
+Shapes (column-major BLAS view, rows = 3 N_c of config 4 = 196608, r ~ 150, N = 128):
+  TN  U^T F            m=r   n=N    k=rows   (split-K)
+  NN  F - U (U^T F)    m=rows n=N   k=r
+  NN  [U Q_F] Xh       m=rows n=r   k=r+N
+  NT  H = L R^T        m=r+N n=r+N  k=N
+  TN  S = V^T V        m=32  n=32   k=rows
+Prints one JSON line per shape: ms and TFLOP/s for both."""
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paratime_b200 as B  # noqa: E402
+
 torch.backends.cuda.matmul.allow_tf32 = False
-for (m, k, n, reps) in [(2048, 256, 2048, 50), (256, 256, 2048, 200), (512, 128, 512, 200), (4096, 4096, 4096, 5),
-                        (196608, 300, 300, 5), (300, 196608, 300, 5)]:
-    a = torch.randn(m, k, dtype=torch.float64, device="cuda")
-    b = torch.randn(k, n, dtype=torch.float64, device="cuda")
-    for _ in range(3):
-        c = a @ b
+ctx = B.Context(0)
+rows = int(sys.argv[1]) if len(sys.argv) > 1 else 196608
+SHAPES = [("U^T F", 1, 0, 150, 128, rows), ("F - U(U^T F)", 0, 0, rows, 128, 150),
+          ("[U Q_F] Xh", 0, 0, rows, 150, 278), ("H = L R^T", 0, 1, 278, 278, 128), ("V^T V", 1, 0, 32, 32, rows)]
+
+
+def timed(fn, reps):
+    fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        c = a @ b
+        fn()
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    print(f"{m}x{k} @ {k}x{n}: {ms*1e3:.1f} us  {2*m*n*k/ms/1e9:.2f} TFLOP/s")
+    return e0.elapsed_time(e1) / reps
+
+
+for name, ta, tb, m, n, k in SHAPES:
+    A = torch.randn((m, k) if ta else (k, m), dtype=torch.float64, device="cuda")  # row-major of the col-major
+    Bm = torch.randn((k, n) if tb else (n, k), dtype=torch.float64, device="cuda")
+    C = torch.zeros((n, m), dtype=torch.float64, device="cuda")
+    lda, ldb = (k if ta else m), (n if tb else k)
+    dp = ctypes.c_void_p
+
+    def ours():
+        B.api.check(B.lib().ptb_dgemm(ctx.h, ta, tb, m, n, k, ctypes.c_double(1.0), dp(A.data_ptr()), lda,
+                                      dp(Bm.data_ptr()), ldb, ctypes.c_double(0.0), dp(C.data_ptr()), m))
+
+    # a column-major X (r x c) is the row-major torch tensor (c x r): X = tensor^T
+    Acm = A.t()
+    opA = Acm.t() if ta else Acm
+    Bcm = Bm.t()
+    opB = Bcm.t() if tb else Bcm
+
+    def cublas():
+        torch.matmul(opA, opB)
+
+    reps = 5 if m * n * k > 1e9 else 50
+    t_o = timed(ours, reps)
+    t_c = timed(cublas, reps)
+    fl = 2.0 * m * n * k
+    print(json.dumps({"shape": name, "m": m, "n": n, "k": k, "ours_ms": round(t_o, 4),
+                      "ours_tflops": round(fl / t_o / 1e9, 2), "cublas_dmma_ms": round(t_c, 4),
+                      "cublas_tflops": round(fl / t_c / 1e9, 2)}), flush=True)

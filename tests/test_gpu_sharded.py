@@ -41,8 +41,12 @@ def _run_world(world, spec, cf, cc, u0, v0):
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-@pytest.mark.parametrize("variant", [1, 0])
-def test_sharded_equals_single_gpu(world, variant):
+@pytest.mark.parametrize("variant,large", [(1, False), (0, False), (1, True)])
+def test_sharded_equals_single_gpu(world, variant, large, monkeypatch):
+    """large: the sweep's large-corrector branch (config 4's), whose GEMVs are row-sharded over
+    the ranks (fixed row blocks, fixed-order sums): still bitwise the one-GPU result."""
+    if large:
+        monkeypatch.setenv("PTB_FUSED_SWEEP_MAX", "0")
     spec, cf, cc, u0, v0 = W.cfg1(tol=1e-8)
     spec = dict(spec, variant=variant, iterations=3)
     single = _run_world(1, spec, cf, cc, u0, v0)[0]
