@@ -12,7 +12,10 @@
  *   - a batch of B states is slice-major SoA: u[b*N + i], udot[b*N + i], N = grid size;
  *   - "_dev" pointers are device (HBM) addresses on the context's device, "_host"
  *     pointers are host memory (pinned or pageable);
- *   - every call is stream-ordered on the context stream; *_host calls synchronise.
+ *   - every call is stream-ordered on the context stream.  Calls whose outputs are all
+ *     device memory return without waiting for the GPU (like a CUDA library call: compose
+ *     them freely, ptb_context_synchronize before reading results on the host); calls with
+ *     host outputs (*_host, keep counts, residuals, ranks) complete before they return.
  * Errors: a ptb_status is returned and a thread-local message is kept
  * (ptb_last_error).  The C++ layer rethrows the reference's exception types:
  *   PTB_INVALID_ARGUMENT -> std::invalid_argument, PTB_DIVERGED -> PropagationDiverged,
@@ -134,7 +137,7 @@ ptb_status ptb_pml_propagate_batch(ptb_pml* p, size_t steps, size_t batch, doubl
  * coarse grid (R(I(d)) = d).  Host outputs (all nullable): rel_err_host[K x (N+1)] L2 distance of
  * [u; udot] to the serial fine run relative to the initial state's norm (the layer drains energy), iteration_ms_host[K] device time of each iteration body
  * (metrics excluded), states_host[4 x (N+1) x N_f] the last iterate, diverged_host = any
- * non-finite fine stage.  The theta (Procrustes) variant is periodic only. */
+ * non-finite fine stage.  The theta (Procrustes) coupling: ptb_pml_theta_run below. */
 ptb_status ptb_pml_parareal_run(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, size_t n_couplings, int iterations,
                                 const double* u0_host, const double* udot0_host, double* rel_err_host,
                                 double* iteration_ms_host, double* states_host, int32_t* diverged_host);
@@ -145,6 +148,17 @@ ptb_status ptb_pml_parareal_run_sharded(ptb_pml* fine, ptb_pml* coarse, ptb_tran
                                         size_t n_couplings, int iterations, const double* u0_host,
                                         const double* udot0_host, double* rel_err_host, double* iteration_ms_host,
                                         double* states_host, int32_t* diverged_host);
+/* Theta parareal (the data-driven Procrustes coupling, parareal.cpp:255-350) with the absorbing
+ * layer — this build's extension (the reference defines the coupling on the periodic (u, udot)
+ * state only, energy_map.cpp:137-214; scheme: oracle/pml_np.py theta_parareal).  The corrector is
+ * fitted on Lambda of the (u, udot) snapshots (coarse speed of `coarse`, gradient `scheme`,
+ * truncation `tol`); the sweep corrects (u, udot) through Lambda-dagger Omega Lambda and the
+ * auxiliary fields additively.  comm nullable (one GPU).  Outputs as ptb_pml_parareal_run plus
+ * ranks_host[K] (corrector rank) and residual_host[K] (relative_residual of the fit), nullable. */
+ptb_status ptb_pml_theta_run(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, ptb_comm* comm, size_t n_couplings,
+                             int iterations, double tol, int scheme, const double* u0_host, const double* udot0_host,
+                             double* rel_err_host, double* iteration_ms_host, double* states_host,
+                             int32_t* ranks_host, double* residual_host, int32_t* diverged_host);
 /* laplacian (propagator.cpp:31-58, reference operation order) */
 ptb_status ptb_laplacian_batch(ptb_context* ctx, const ptb_grid* grid, size_t batch,
                                const double* f_dev, double* out_dev);

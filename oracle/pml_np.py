@@ -178,3 +178,93 @@ def plain_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m
         out.append(nxt)
         cur = nxt
     return out, np.array(errs)
+
+
+def theta_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m_c: int, t, N: int, K: int,
+                   c_coarse, tol: float = 1e-4, scheme: int = 0):
+    """Theta-parareal (the data-driven Procrustes coupling, parareal.cpp:255-350) on the layered
+    state (u, udot, px, py) — this build's extension, the way csrc/pml.cu pml_parareal(theta)
+    evaluates it.  The reference defines the coupling on (u, udot) only (energy_map.cpp:137-214);
+    with the layer:
+      * snapshots F = Lambda(R fine_next[n]), G = Lambda(C(R cur[n-1])) of the (u, udot) part over
+        slices whose four fields are finite; corrector = update_svd(corrector, F, G, tol);
+      * the sweep corrects (u, udot) with Lambda-dagger Omega Lambda (corrected_coarse_state,
+        parareal.cpp:245-253) and the auxiliary fields (px, py) additively as plain parareal:
+        d = (corr(w) - corr(old[n]))_{u,udot} ++ (w - old[n])_{px,py},  w = C(w_{n-1});
+        n = 1 takes fine_next[1] (both terms cancel exactly, as in parareal.cpp:315-318);
+        w_n = R(fine_next[n]) + d (as the plain sweep), next[n] = fine_next[n] + I(d) with the
+        auxiliary part masked to the layer; a non-finite w, old[n] or fine_next[n] gives a NaN
+        state (parareal.cpp:323-326);
+      * finalize: non-finite iterates clamped to the previous one.
+    Returns (iterates per k, L2 distances of [u; udot] to the serial fine run relative to the
+    initial state's norm [K x (N+1)], corrector ranks per k)."""
+    from oracle import paratime_np as P
+
+    R = lambda s: tuple(P.restrict_field(f, t) for f in s)  # noqa: E731
+    damped = (kf.zy[:, None] != 0.0) | (kf.zx[None, :] != 0.0)
+
+    def I(s):  # noqa: E743
+        u, v, px, py = (P.interpolate_field(f, t) for f in s)
+        return u, v, np.where(damped, px, 0.0), np.where(damped, py, 0.0)
+
+    def finite(s):
+        return all(np.all(np.isfinite(f)) for f in s)
+
+    Fp = lambda s: pml_steps(*s, kf, m_f)  # noqa: E731
+    Cp = lambda s: pml_steps(*s, kc, m_c)  # noqa: E731
+    z = np.zeros_like(u0)
+    init = (u0, v0, z, z)
+    ref = [init]
+    for _ in range(N):
+        ref.append(Fp(ref[-1]))
+    cur = [init]
+    w = R(init)
+    for _ in range(N):
+        w = Cp(w)
+        cur.append(I(w))
+    corr = P.empty_corrector()
+    nan = np.full_like(u0, np.nan)
+    out, errs, ranks = [], [], []
+    den = np.sum(init[0] ** 2 + init[1] ** 2)
+    for _ in range(K):
+        fine_next = [None] + [Fp(cur[n - 1]) for n in range(1, N + 1)]
+        old = [None] + [Cp(R(cur[n - 1])) for n in range(1, N + 1)]
+        keep = [n for n in range(1, N + 1) if finite(fine_next[n]) and finite(old[n])]
+        if keep:
+            F, G = P.assemble_snapshots([fine_next[n][:2] for n in keep], [old[n][:2] for n in keep], t,
+                                        c_coarse, scheme)
+            corr = P.update_svd(corr, F, G, tol)
+        ranks.append(corr.rank)
+
+        def corrected(s):
+            return P._corrected_coarse_state(s[:2], corr, c_coarse, t.coarse, scheme, False)
+
+        nxt = [init]
+        w = R(init)
+        for n in range(1, N + 1):
+            g = Cp(w)
+            if n == 1:
+                d = tuple(np.zeros_like(f) for f in g)
+            elif not (finite(g) and finite(old[n]) and finite(fine_next[n])):
+                d = tuple(np.full_like(f, np.nan) for f in g)
+            else:
+                cn, co = corrected(g), corrected(old[n])
+                d = (cn[0] - co[0], cn[1] - co[1], g[2] - old[n][2], g[3] - old[n][3])
+            w = tuple(a + b for a, b in zip(R(fine_next[n]), d))
+            if n == 1:
+                nxt.append(fine_next[1])
+            elif not np.all(np.isfinite(d[0])):
+                nxt.append((nan, nan, nan, nan))
+            else:
+                nxt.append(tuple(a + b for a, b in zip(fine_next[n], I(d))))
+        for n in range(1, N + 1):
+            if not finite(nxt[n]):
+                nxt[n] = cur[n]
+        e = []
+        for n in range(N + 1):
+            num = np.sum((nxt[n][0] - ref[n][0]) ** 2 + (nxt[n][1] - ref[n][1]) ** 2)
+            e.append(float(np.sqrt(num / den)) if den > 0 else float(np.sqrt(num)))
+        errs.append(e)
+        out.append(nxt)
+        cur = nxt
+    return out, np.array(errs), ranks

@@ -26,6 +26,7 @@ from .api import (  # noqa: F401
     Propagator,
     damping_profile,
     pml_parareal_run,
+    pml_theta_run,
     Transfer,
     lib,
     lib_path,

@@ -7,6 +7,7 @@ torch ops are stream-ordered.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from pathlib import Path
 from typing import Optional, Sequence, Tuple
@@ -34,16 +35,18 @@ class _Grid(C.Structure):
 
 
 def lib_path() -> Path:
-    return LIB
+    # PTB_LIB: an alternate build of the same library (A/B measurements of kernel variants only)
+    return Path(os.environ["PTB_LIB"]) if os.environ.get("PTB_LIB") else LIB
 
 
 def lib():
     """Load the CUDA library; raises (no fallback) when it has not been built."""
     global _lib
     if _lib is None:
-        if not LIB.exists():
-            raise ImportError(f"{LIB} is missing — build it with `python -m paratime_b200.build`")
-        _lib = C.CDLL(str(LIB))
+        path = lib_path()
+        if not path.exists():
+            raise ImportError(f"{path} is missing — build it with `python -m paratime_b200.build`")
+        _lib = C.CDLL(str(path))
         _lib.ptb_last_error.restype = C.c_char_p
         _lib.ptb_version.restype = C.c_char_p
         _lib.ptb_context_stream.restype = C.c_void_p
@@ -220,7 +223,18 @@ class PmlPropagator:
             pass
 
     def propagate(self, u, udot, px, py, steps: Optional[int] = None, flags=None):
-        batch = u.numel() // self.grid.size
+        import torch
+
+        n = self.grid.size
+        batch = u.numel() // n
+        dev = torch.device("cuda", self.ctx.device)
+        for name, t in (("u", u), ("udot", udot), ("px", px), ("py", py)):
+            if (t.dtype != torch.float64 or not t.is_contiguous() or t.device != dev
+                    or t.numel() != batch * n or batch == 0):
+                raise PtbError(INVALID_ARGUMENT, f"pml propagate: {name} must be a contiguous float64 tensor of "
+                               f"batch x {n} values on {dev}")
+        if flags is not None and (flags.dtype != torch.int32 or flags.numel() < batch or flags.device != dev):
+            raise PtbError(INVALID_ARGUMENT, "pml propagate: flags must be int32[batch] on the context's device")
         check(lib().ptb_pml_propagate_batch(self.h, C.c_size_t(steps or 0), C.c_size_t(batch), _ptr(u), _ptr(udot),
                                             _ptr(px), _ptr(py), _ptr(flags)))
         return u, udot, px, py
@@ -235,6 +249,8 @@ def pml_parareal_run(fine: "PmlPropagator", coarse: "PmlPropagator", transfer: "
     dp = C.POINTER(C.c_double)
     u0 = np.ascontiguousarray(u0, dtype=np.float64)
     v0 = np.ascontiguousarray(udot0, dtype=np.float64)
+    if u0.size != fine.grid.size or v0.size != fine.grid.size:
+        raise PtbError(INVALID_ARGUMENT, "pml_parareal_run: initial state does not match the fine grid")
     err = np.zeros((max(K, 1), N + 1))
     ms = np.zeros(max(K, 1))
     states = np.empty((4, N + 1) + tuple(fine.grid.n)) if keep_states else None
@@ -248,6 +264,33 @@ def pml_parareal_run(fine: "PmlPropagator", coarse: "PmlPropagator", transfer: "
         check(lib().ptb_pml_parareal_run_sharded(fine.h, coarse.h, transfer.h, comm.h, C.c_size_t(N), C.c_int(K),
                                                  u0.ctypes.data_as(dp), v0.ctypes.data_as(dp), *out))
     return {"rel_err": err[:K], "iteration_ms": ms[:K], "diverged": bool(div.value), "states": states}
+
+
+def pml_theta_run(fine: "PmlPropagator", coarse: "PmlPropagator", transfer: "Transfer", n_couplings: int,
+                  iterations: int, u0, udot0, tol: float = 1e-4, scheme: int = 0, keep_states: bool = False,
+                  comm: "Comm" = None):
+    """ptb_pml_theta_run: theta (Procrustes) parareal with the absorbing layer (oracle/pml_np.py
+    theta_parareal).  Returns pml_parareal_run's dict plus per-iteration corrector "rank" and "residual"."""
+    N, K = int(n_couplings), int(iterations)
+    dp = C.POINTER(C.c_double)
+    n_f = int(np.prod(fine.grid.n))
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    v0 = np.ascontiguousarray(udot0, dtype=np.float64)
+    if u0.size != n_f or v0.size != n_f:
+        raise PtbError(INVALID_ARGUMENT, "pml_theta_run: initial state does not match the fine grid")
+    err = np.zeros((max(K, 1), N + 1))
+    ms = np.zeros(max(K, 1))
+    ranks = np.zeros(max(K, 1), dtype=np.int32)
+    res = np.zeros(max(K, 1))
+    states = np.empty((4, N + 1) + tuple(fine.grid.n)) if keep_states else None
+    div = C.c_int32(0)
+    check(lib().ptb_pml_theta_run(fine.h, coarse.h, transfer.h, comm.h if comm is not None else None,
+                                  C.c_size_t(N), C.c_int(K), C.c_double(tol), C.c_int(scheme),
+                                  u0.ctypes.data_as(dp), v0.ctypes.data_as(dp), err.ctypes.data_as(dp),
+                                  ms.ctypes.data_as(dp), states.ctypes.data_as(dp) if keep_states else None,
+                                  ranks.ctypes.data_as(C.POINTER(C.c_int32)), res.ctypes.data_as(dp), C.byref(div)))
+    return {"rel_err": err[:K], "iteration_ms": ms[:K], "diverged": bool(div.value), "states": states,
+            "rank": ranks[:K], "residual": res[:K]}
 
 
 def damping_profile(n: int, width: int, h: float, cmax: float, reflection: float = 1e-4) -> np.ndarray:

@@ -42,9 +42,8 @@ ptb_status ptb_energy_components_batch(ptb_context* ctx, const ptb_grid* grid, c
     require(scheme >= PTB_FD2 && scheme <= PTB_SPECTRAL, "unknown gradient scheme");
     Dev d(ctx->device);
     std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
-    EnergyWork w(ctx);
+    EnergyWork& w = context_energy_work(ctx);  // cached: no allocation (and no implicit sync) per call
     energy_components(w, *grid, scheme, batch, u, v, grid_size(*grid), nullptr, c, stacked, ld, mean);
-    PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -56,9 +55,8 @@ ptb_status ptb_from_energy_components_batch(ptb_context* ctx, const ptb_grid* gr
     validate_grid(*grid);
     Dev d(ctx->device);
     std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
-    EnergyWork w(ctx);
+    EnergyWork& w = context_energy_work(ctx);  // cached: no allocation (and no implicit sync) per call
     from_energy_components(w, *grid, batch, stacked, ld, mean, c, u, v, grid_size(*grid));
-    PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -70,10 +68,9 @@ ptb_status ptb_energy_sums_batch(ptb_context* ctx, const ptb_grid* grid, const d
     validate_grid(*grid);
     Dev d(ctx->device);
     std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
-    EnergyWork w(ctx);
+    EnergyWork& w = context_energy_work(ctx);  // cached: no allocation (and no implicit sync) per call
     const size_t n = grid_size(*grid);
     pair_energy_sums(w, *grid, scheme, batch, ua, va, n, ub, vb, n, c, sums4);
-    PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -184,7 +181,6 @@ ptb_status ptb_corrector_apply_batch(ptb_corrector* c, size_t batch, const doubl
     Dev d(c->ctx->device);
     std::lock_guard<std::recursive_mutex> lock(c->ctx->mutex);
     apply_corrector(*c->work, c->c, batch, in, size_t(c->c.rows), out, size_t(c->c.rows));
-    PTB_CUDA_CHECK(cudaStreamSynchronize(c->ctx->stream));
   });
 }
 
@@ -197,7 +193,6 @@ ptb_status ptb_dgemm(ptb_context* ctx, int ta, int tb, int m, int n, int k, doub
     Dev d(ctx->device);
     std::lock_guard<std::recursive_mutex> lock(ctx->mutex);
     gemm(ctx, ta != 0, tb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-    PTB_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   });
 }
 

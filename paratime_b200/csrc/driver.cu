@@ -343,6 +343,7 @@ DriverCache& driver_cache(ptb_context* ctx) {
 }
 
 ProcWork& context_proc_work(ptb_context* ctx) { return driver_cache(ctx).pw; }
+EnergyWork& context_energy_work(ptb_context* ctx) { return driver_cache(ctx).ew; }
 
 struct Driver {
   ptb_context* ctx;

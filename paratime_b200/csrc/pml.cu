@@ -28,9 +28,13 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <limits>
 
 #include "ptb_comm.h"
+#include "ptb_driver.h"
+#include "ptb_energy.h"
 #include "ptb_internal.h"
+#include "ptb_procrustes.h"
 
 namespace ptb {
 namespace {
@@ -384,6 +388,7 @@ struct ptb_pml {
   size_t n = 0, steps = 0;
   double dt = 0, hd = 0, ry = 0, cc = 0, gx = 0, gy = 0;
   double* coef = nullptr;  // kx (n) | zx ax qx (nx) | zy ay qy (ny)
+  double* speed = nullptr;  // c (n): the energy map of the theta coupling
   ptb::DeviceBuffer scratch;  // 4 fields x batch (ping-pong partner; phi planes zeroed once)
   size_t scratch_batch = 0;
   int2* tiles = nullptr;       // plain tiles, then layer tiles (PT x PT, classified at create)
@@ -552,6 +557,41 @@ __global__ void __launch_bounds__(512) k_err_sums(size_t n, const double* au, co
   }
 }
 
+// theta coupling, one sweep step's tail on the layered coarse state (one launch): the (u, udot)
+// part d = Z dz + (m_w - m_old)/N_c (dl: Z dz as [du; dv], null when the corrector is empty), the
+// auxiliary part d = g - old[n] (plain correction); d := NaN when g, old[n] or fine_next[n] is
+// non-finite (parareal.cpp:323-326); then w = R(fine_next[n]) + d for all four fields (the next
+// step's R(next[n]), R(I(d)) = d at the coarse nodes).  g and w share storage (read before write).
+struct Fields4 {
+  double* f[4];
+};
+__global__ void k_theta_tail(size_t nc, const double* __restrict__ dl, const double* __restrict__ mw,
+                             const double* __restrict__ mold, const int32_t* gbad, const int32_t* obad,
+                             const int32_t* fbad, Fields4 g, Fields4 old, Fields4 rf, Fields4 d) {
+  const bool nan = *gbad || *obad || *fbad;
+  const double dm = (*mw - *mold) / double(nc);
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nc; i += size_t(gridDim.x) * blockDim.x) {
+    double di[4];
+    di[0] = (dl ? dl[i] : 0.0) + dm;
+    di[1] = dl ? dl[nc + i] : 0.0;
+    di[2] = g.f[2][i] - old.f[2][i];
+    di[3] = g.f[3][i] - old.f[3][i];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double x = nan ? __longlong_as_double(0x7ff8000000000000LL) : di[f];
+      d.f[f][i] = x;
+      g.f[f][i] = rf.f[f][i] + x;
+    }
+  }
+}
+__global__ void k_sub_small(int n, const double* a, const double* b, double* out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = a[i] - b[i];
+}
+__global__ void k_or_flags(size_t n, const int32_t* src, int32_t* dst) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    dst[i] |= src[i];
+}
+
 unsigned ew_blocks(ptb_context* ctx, size_t n) {
   return unsigned(std::max<size_t>(1, std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 8)));
 }
@@ -570,9 +610,20 @@ struct States {
 // all-gather of the coarse payload (C(R cur[n-1]) and R(fine_next[n]), 4 fields each) feeds the
 // replicated, deterministic coarse sweep, and the last own state goes to rank r+1.  Results are
 // bitwise independent of the world size.
+// th (nullable): the theta (Procrustes) coupling instead of plain parareal — oracle/pml_np.py
+// theta_parareal: (u, udot) corrected through Lambda-dagger Omega Lambda with the coarse speed, the
+// auxiliary fields additively; the corrector is fitted on the (u, udot) snapshots of the slices
+// whose four fields are finite.
+struct PmlTheta {
+  double tol = 1e-4;
+  int scheme = PTB_FD2;
+  int* ranks = nullptr;        // [K] corrector rank per iteration (nullable)
+  double* residual = nullptr;  // [K] relative_residual of the fit (nullable)
+};
+
 void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* comm, size_t N, int K,
                   const double* u0, const double* v0, double* err_out, double* ms_out, double* states_out,
-                  int32_t* diverged_out) {
+                  int32_t* diverged_out, const PmlTheta* th = nullptr) {
   ptb_context* ctx = fine->ctx;
   cudaStream_t st = ctx->stream;
   const size_t nf = fine->n, nc = coarse->n;
@@ -597,6 +648,34 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
   States cold{cw, nc, P}, crf{cw + 4 * P * nc, nc, P}, cd{cw + 8 * P * nc, nc, P};
   States cwv{cw + 12 * P * nc, nc, 1}, cg{cw + 12 * P * nc + 4 * nc, nc, 1};
   int32_t* flags = static_cast<int32_t*>(bflag.get((L + 1) * sizeof(int32_t)));
+  // theta: per-iteration stage flags (own fine, own coarse), their global copies, the corrector
+  const bool theta = th != nullptr;
+  const size_t rows = 3 * nc;  // stacked (c dx u, c dy u, udot) on the coarse grid
+  DeviceBuffer bsf, bgf, bth, bZ, bidx, bsw;
+  int32_t *ffl = nullptr, *cfl = nullptr, *gff = nullptr, *gcf = nullptr, *swf = nullptr;
+  double *Fm = nullptr, *Gm = nullptr, *cmp = nullptr, *zold = nullptr, *mold = nullptr, *zw = nullptr,
+         *mw = nullptr, *dl = nullptr, *dz = nullptr;
+  int* idx_d = nullptr;
+  DevCorrector corr;
+  EnergyWork ew(ctx);
+  if (theta) {
+    check_tol(th->tol);
+    require(th->scheme >= PTB_FD2 && th->scheme <= PTB_SPECTRAL, "pml theta: unknown gradient scheme");
+    ffl = static_cast<int32_t*>(bsf.get(2 * (chunk + 1) * sizeof(int32_t)));
+    cfl = ffl + chunk + 1;
+    gff = static_cast<int32_t*>(bgf.get(2 * P * sizeof(int32_t)));
+    gcf = gff + P;
+    swf = static_cast<int32_t*>(bsw.get((N + 1) * sizeof(int32_t)));
+    double* w = static_cast<double*>(bth.get((3 * rows * N + 4 * N + 2) * sizeof(double)));
+    Fm = w;
+    Gm = Fm + rows * N;
+    cmp = Gm + rows * N;   // Lambda of the old terms (rows x (N-1)), then of w (batch 1)
+    mold = cmp + rows * N;  // N
+    mw = mold + N;          // 1 (+1 pad)
+    idx_d = static_cast<int*>(bidx.get(N * sizeof(int)));
+    require(ctx->num_sms > 0, "pml theta: context");
+  }
+  const double* ccs = coarse->speed;
   double* sums = static_cast<double*>(bsum.get(2 * (chunk + 2) * sizeof(double)));
   const size_t ichunk = std::max<size_t>(1, std::min<size_t>(L, 8));
   DeviceBuffer bbad, bptr;
@@ -650,10 +729,75 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
   PTB_CUDA_CHECK(cudaEventCreate(&e0));
   PTB_CUDA_CHECK(cudaEventCreate(&e1));
   const size_t per = 8 * chunk * nc;  // payload doubles per rank: cold and crf, 4 fields each
-  double* own = static_cast<double*>(bpay.get(per * sizeof(double)));
-  double* all = static_cast<double*>(ball.get(per * size_t(world) * sizeof(double)));
+  const size_t per_b = per * sizeof(double) + (theta ? 2 * chunk * sizeof(int32_t) + 8 : 0);  // + flags
+  double* own = static_cast<double*>(bpay.get(per_b));
+  double* all = static_cast<double*>(ball.get(per_b * size_t(world)));
   std::vector<double> hs(2 * (chunk + 1) * size_t(world));
   double* gsums = static_cast<double*>(bgs.get(hs.size() * sizeof(double)));
+  ProcWork* pw = theta ? &context_proc_work(ctx) : nullptr;
+  const ptb_grid& cgr = coarse->grid;
+  // theta: fit the corrector on this iteration's snapshots, then the replicated coarse sweep -> cd
+  auto theta_iteration = [&](int k) {
+    std::vector<int32_t> hf(2 * N);
+    PTB_CUDA_CHECK(cudaMemcpyAsync(hf.data(), gff, N * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PTB_CUDA_CHECK(cudaMemcpyAsync(hf.data() + N, gcf, N * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+    std::vector<int> keep;
+    for (size_t n = 1; n <= N; ++n)
+      if (!hf[n - 1] && !hf[N + n - 1]) keep.push_back(int(n - 1));
+    double res = std::numeric_limits<double>::quiet_NaN();
+    if (!keep.empty()) {  // assemble_snapshots (procrustes.cpp:158-175) on the (u, udot) part
+      const int cols = int(keep.size());
+      PTB_CUDA_CHECK(cudaMemcpyAsync(idx_d, keep.data(), keep.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      energy_components(ew, cgr, th->scheme, size_t(cols), crf.f(0), crf.f(1), nc, idx_d, ccs, Fm, rows, nullptr);
+      energy_components(ew, cgr, th->scheme, size_t(cols), cold.f(0), cold.f(1), nc, idx_d, ccs, Gm, rows, nullptr);
+      update_svd(*pw, corr, Fm, Gm, int(rows), cols, th->tol);
+      if (th->residual) res = relative_residual(*pw, corr, Fm, Gm, int(rows), cols);
+    }
+    if (th->ranks) th->ranks[k - 1] = corr.rank;
+    if (th->residual) th->residual[k - 1] = res;
+    const int r = corr.rank;
+    // Z = Lambda-dagger(X, 0) as one (2 N_c x r) matrix [Zu; Zv]; z_old = Y^T Lambda(old[n]), n >= 2
+    if (r > 0) {
+      dl = static_cast<double*>(bZ.get((2 * nc * size_t(r) + 2 * nc + size_t(r) * (N + 2)) * sizeof(double)));
+      double* Z = dl + 2 * nc;
+      zold = Z + 2 * nc * size_t(r);
+      zw = zold + size_t(r) * N;
+      dz = zw + r;
+      PTB_CUDA_CHECK(cudaMemsetAsync(zw, 0, size_t(r) * sizeof(double), st));
+      from_energy_components(ew, cgr, size_t(r), corr.Xp(), rows, zw, ccs, Z, Z + nc, 2 * nc);
+      if (N >= 2) {
+        energy_components(ew, cgr, th->scheme, N - 1, cold.f(0, 1), cold.f(1, 1), nc, nullptr, ccs, cmp, rows, mold + 1);
+        gemm(ctx, true, false, r, int(N - 1), int(rows), 1.0, corr.Yp(), int(rows), cmp, int(rows), 0.0, zold, r);
+      }
+    } else if (N >= 2) {
+      energy_components(ew, cgr, th->scheme, N - 1, cold.f(0, 1), cold.f(1, 1), nc, nullptr, ccs, cmp, rows, mold + 1);
+    }
+    const double* Z = r > 0 ? dl + 2 * nc : nullptr;
+    PTB_CUDA_CHECK(cudaMemsetAsync(swf, 0, (N + 1) * sizeof(int32_t), st));
+    // n = 1: next[1] = fine_next[1] (both corrected terms cancel, parareal.cpp:315-318): d_1 = 0
+    for (int f = 0; f < 4; ++f) {
+      PTB_CUDA_CHECK(cudaMemsetAsync(cd.f(f, 0), 0, nc * sizeof(double), st));
+      cpy(cwv.f(f), crf.f(f, 0), nc);
+    }
+    Fields4 G{{cwv.f(0), cwv.f(1), cwv.f(2), cwv.f(3)}};
+    for (size_t n = 2; n <= N; ++n) {
+      pml_propagate(coarse, coarse->steps, 1, cwv.f(0), cwv.f(1), cwv.f(2), cwv.f(3), swf + n);  // g = C(w)
+      energy_components(ew, cgr, th->scheme, 1, cwv.f(0), cwv.f(1), nc, nullptr, ccs, cmp, rows, mw);
+      if (r > 0) {
+        gemm(ctx, true, false, r, 1, int(rows), 1.0, corr.Yp(), int(rows), cmp, int(rows), 0.0, zw, r);
+        k_sub_small<<<1, 256, 0, st>>>(r, zw, zold + (n - 2) * size_t(r), dz);
+        PTB_LAUNCH_CHECK(ctx);
+        gemm(ctx, false, false, int(2 * nc), 1, r, 1.0, Z, int(2 * nc), dz, r, 0.0, dl, int(2 * nc));
+      }
+      Fields4 O{{cold.f(0, n - 1), cold.f(1, n - 1), cold.f(2, n - 1), cold.f(3, n - 1)}};
+      Fields4 RF{{crf.f(0, n - 1), crf.f(1, n - 1), crf.f(2, n - 1), crf.f(3, n - 1)}};
+      Fields4 D{{cd.f(0, n - 1), cd.f(1, n - 1), cd.f(2, n - 1), cd.f(3, n - 1)}};
+      k_theta_tail<<<ew_blocks(ctx, nc), 256, 0, st>>>(nc, r > 0 ? dl : nullptr, mw, mold + (n - 1), swf + n,
+                                                      gcf + (n - 1), gff + (n - 1), G, O, RF, D);
+      PTB_LAUNCH_CHECK(ctx);
+    }
+  };
   for (int k = 1; k <= K; ++k) {
     PTB_CUDA_CHECK(cudaEventRecord(e0, st));
     // parallel stage on the own couplings: next[n] = F(cur[n-1]), old[n] = C(R cur[n-1])
@@ -662,27 +806,52 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
         cpy(nxt.f(f, 1), cur.f(f, 0), L * nf);
         restrict_fields(t, L, cur.f(f, 0), cold.f(f, a - 1));
       }
-      pml_propagate(fine, fine->steps, L, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), flags + 1);
+      if (theta) {
+        PTB_CUDA_CHECK(cudaMemsetAsync(ffl, 0, 2 * (chunk + 1) * sizeof(int32_t), st));
+        pml_propagate(fine, fine->steps, L, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), ffl);
+        k_or_flags<<<1, 256, 0, st>>>(L, ffl, flags + 1);
+        PTB_LAUNCH_CHECK(ctx);
+      } else {
+        pml_propagate(fine, fine->steps, L, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), flags + 1);
+      }
       pml_propagate(coarse, coarse->steps, L, cold.f(0, a - 1), cold.f(1, a - 1), cold.f(2, a - 1), cold.f(3, a - 1),
-                    nullptr);
+                    theta ? cfl : nullptr);
       for (int f = 0; f < 4; ++f) restrict_fields(t, L, nxt.f(f, 1), crf.f(f, a - 1));
     }
-    if (world > 1) {  // one all-gather of the coarse payload
+    if (world > 1) {  // one all-gather of the coarse payload (theta: and the stage flags)
       for (int f = 0; f < 4; ++f) {
         cpy(own + size_t(f) * chunk * nc, cold.f(f, a - 1), L * nc);
         cpy(own + size_t(4 + f) * chunk * nc, crf.f(f, a - 1), L * nc);
       }
-      comm->allgather(own, all, per * sizeof(double), st);
+      if (theta && L) {  // two int32 rows of `chunk` after the fields (per_b counts them)
+        int32_t* of = reinterpret_cast<int32_t*>(own + per);
+        PTB_CUDA_CHECK(cudaMemcpyAsync(of, ffl, L * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        PTB_CUDA_CHECK(cudaMemcpyAsync(of + chunk, cfl, L * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      }
+      comm->allgather(own, all, per_b, st);
       for (int r = 0; r < world; ++r) {
         const size_t ra = 1 + size_t(r) * chunk;
-        if (ra > N || r == rank) continue;
+        if (ra > N) continue;
         const size_t rl = std::min(N + 1, ra + chunk) - ra;
+        const double* src = reinterpret_cast<const double*>(reinterpret_cast<const char*>(all) + size_t(r) * per_b);
+        if (theta) {
+          const int32_t* rf_ = reinterpret_cast<const int32_t*>(src + per);
+          PTB_CUDA_CHECK(cudaMemcpyAsync(gff + (ra - 1), rf_, rl * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+          PTB_CUDA_CHECK(cudaMemcpyAsync(gcf + (ra - 1), rf_ + chunk, rl * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        }
+        if (r == rank) continue;
         for (int f = 0; f < 4; ++f) {
-          cpy(cold.f(f, ra - 1), all + size_t(r) * per + size_t(f) * chunk * nc, rl * nc);
-          cpy(crf.f(f, ra - 1), all + size_t(r) * per + size_t(4 + f) * chunk * nc, rl * nc);
+          cpy(cold.f(f, ra - 1), src + size_t(f) * chunk * nc, rl * nc);
+          cpy(crf.f(f, ra - 1), src + size_t(4 + f) * chunk * nc, rl * nc);
         }
       }
+    } else if (theta && L) {
+      PTB_CUDA_CHECK(cudaMemcpyAsync(gff, ffl, L * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      PTB_CUDA_CHECK(cudaMemcpyAsync(gcf, cfl, L * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     }
+    if (theta) {
+      theta_iteration(k);
+    } else {
     // replicated sequential sweep on the coarse grid: w_0 = R(init); g = C(w_{n-1});
     // d_n = g - old[n]; w_n = R(fine_next[n]) + d_n  (= R(next[n]): R(I(d)) = d at the coarse nodes)
     for (int f = 0; f < 4; ++f) restrict_fields(t, 1, ini.f(f, 0), cwv.f(f));
@@ -694,6 +863,7 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
                                                          cd.f(f, n - 1), cwv.f(f));
         PTB_LAUNCH_CHECK(ctx);
       }
+    }
     }
     // own combine: next[n] = fine_next[n] + I(d_n), in chunks of slices (u, udot: fused into the
     // interpolation; px, py: the correction masked to the layer)
@@ -856,6 +1026,8 @@ ptb_status ptb_pml_create(ptb_context* ctx, const ptb_grid* grid, const double* 
       zy[ny + i] = (1.0 - p->hd * z) / (1.0 + p->hd * z);
       zy[2 * ny + i] = dt / (2.0 * hy * (1.0 + p->hd * z));
     }
+    PTB_CUDA_CHECK(cudaMalloc(&p->speed, n * sizeof(double)));
+    PTB_CUDA_CHECK(cudaMemcpy(p->speed, c_host, n * sizeof(double), cudaMemcpyHostToDevice));
     PTB_CUDA_CHECK(cudaMalloc(&p->coef, h.size() * sizeof(double)));
     PTB_CUDA_CHECK(cudaMemcpy(p->coef, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
     // tile classes: a tile is a layer tile when a damped row or column lies within HL cells of
@@ -886,6 +1058,7 @@ ptb_status ptb_pml_destroy(ptb_pml* p) {
     if (!p) return;
     DevGuard g(p->ctx->device);
     cudaFree(p->coef);
+    cudaFree(p->speed);
     cudaFree(p->tiles);
     delete p;
   });
@@ -925,6 +1098,25 @@ ptb_status ptb_pml_parareal_run_sharded(ptb_pml* fine, ptb_pml* coarse, ptb_tran
     std::lock_guard<std::recursive_mutex> lock(fine->ctx->mutex);
     pml_parareal(fine, coarse, t, comm_of(comm), n_couplings, iterations, u0_host, udot0_host, rel_err_host,
                  iteration_ms_host, states_host, diverged_host);
+  });
+}
+
+ptb_status ptb_pml_theta_run(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, ptb_comm* comm, size_t n_couplings,
+                             int iterations, double tol, int scheme, const double* u0_host, const double* udot0_host,
+                             double* rel_err_host, double* iteration_ms_host, double* states_host, int32_t* ranks_host,
+                             double* residual_host, int32_t* diverged_host) {
+  return guarded([&] {
+    require(fine && coarse && t && u0_host && udot0_host, "pml parareal: null argument");
+    require(fine->ctx == coarse->ctx && t->ctx == fine->ctx, "pml parareal: objects of different contexts");
+    DevGuard g(fine->ctx->device);
+    std::lock_guard<std::recursive_mutex> lock(fine->ctx->mutex);
+    PmlTheta th;
+    th.tol = tol;
+    th.scheme = scheme;
+    th.ranks = ranks_host;
+    th.residual = residual_host;
+    pml_parareal(fine, coarse, t, comm_of(comm), n_couplings, iterations, u0_host, udot0_host, rel_err_host,
+                 iteration_ms_host, states_host, diverged_host, &th);
   });
 }
 

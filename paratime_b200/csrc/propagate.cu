@@ -46,6 +46,10 @@
 
 #include "ptb_internal.h"
 
+#ifndef PTB_WAVE2_CPASYNC  // 1: round-1 per-thread cp.async ring in k_wave2 (A/B builds only)
+#define PTB_WAVE2_CPASYNC 0
+#endif
+
 namespace ptb {
 
 namespace cg = cooperative_groups;
@@ -821,7 +825,8 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     o += nx;
     if (o >= npts) o -= npts;
   };
-  auto issue = [&](int slot) {
+#if PTB_WAVE2_CPASYNC
+  auto issue = [&](int slot, int) {
     double2* d = ring + (slot * 3) * T + j;
     cp_async16(d, U + ou);
     cp_async16(d + T, V + ov);
@@ -830,8 +835,48 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     adv(ou);
     adv(ov);
   };
+#else
+  // Level-0 rows arrive by bulk copies (the TMA engine, cp.async.bulk): one thread moves the
+  // strip's u, udot and coefficient row segments (2W contiguous doubles each, split where the
+  // strip wraps the periodic x boundary) into the ring slot and they complete on the slot's
+  // mbarrier.  Every thread then waits on the barrier's phase and reads its pair: no per-thread
+  // LDGSTS through the LSU, which the edge exchange saturates (profiles/r01_k1_full.md).
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RING * 3 * T);
+  const int gx0 = FULL ? 0 : ((x0 - HXE) % nx + nx) % nx;  // first column of the strip
+  int ru = 0, rv = 0;                                       // next u row / udot,coef row (thread 0)
+  if (j == 0) {
+    ru = ((ystart + 1) % ny + ny) % ny;
+    rv = ((ystart) % ny + ny) % ny;
 #pragma unroll
-  for (int s0 = 0; s0 < RING - 1; ++s0) issue(s0);
+    for (int s0 = 0; s0 < RING; ++s0) mbar_init(smem_addr(&bars[s0]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto copy_row = [&](double* dst, const double* row, unsigned bar) {
+    int col = gx0, rem = 2 * T;
+    while (rem > 0) {
+      const int len = min(rem, nx - col);
+      bulk_from_global(smem_addr(dst), row + col, unsigned(len) * 8u, bar);
+      dst += len;
+      rem -= len;
+      col = 0;
+    }
+  };
+  auto issue = [&](int slot, int iter) {
+    if (j == 0 && iter < n_iter) {
+      const unsigned bar = smem_addr(&bars[slot]);
+      mbar_expect(bar, unsigned(3 * 2 * T) * 8u);
+      double* d = reinterpret_cast<double*>(ring + (slot * 3) * T);
+      copy_row(d, U + size_t(ru) * nx, bar);
+      copy_row(d + 2 * T, V + size_t(rv) * nx, bar);
+      copy_row(d + 4 * T, K + size_t(rv) * nx, bar);
+      if (++ru == ny) ru = 0;
+      if (++rv == ny) rv = 0;
+    }
+  };
+#endif
+#pragma unroll
+  for (int s0 = 0; s0 < RING - 1; ++s0) issue(s0, s0);
   __syncthreads();
   bool ok = true;
   const int last_out = nrows + 2 * S;
@@ -839,10 +884,14 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
 #pragma unroll
     for (int k = 0; k < UNROLL; ++k) {
       const int i = i0 + k;
+#if PTB_WAVE2_CPASYNC
       cp_async_wait<RING - 2>();
+#else
+      mbar_wait(smem_addr(&bars[k]), unsigned(i0 / UNROLL) & 1u);
+#endif
       const double2* src = ring + ((k % RING) * 3) * T + j;
       const double2 uu0 = src[0], v0 = src[T], k0 = src[2 * T];
-      issue((k + RING - 1) % RING);
+      issue((k + RING - 1) % RING, i + RING - 1);
       double2 out_u, out_v;
       if (k & 1)
         wave2_iter<S, W, 1, RY1>(eL, eR, offl, offr, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
@@ -857,7 +906,9 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
       __syncthreads();
     }
   }
+#if PTB_WAVE2_CPASYNC
   cp_async_wait<0>();
+#endif
   if (a.flags) {
     const int bad = __syncthreads_or(!ok);
     if (bad && j == 0) atomicOr(&a.flags[blockIdx.x], 1);
@@ -1043,7 +1094,8 @@ void launch_wave(ptb_context* ctx, cudaStream_t st, const WavePlan& pl, WaveArgs
 
 // k_wave2: W threads cover 2W columns; useful width even; occupancy from the runtime.
 size_t wave2_smem(int S, int W) {
-  return (size_t(4) * (S + 1) * (W + 2) + size_t(6) * 3 * 2 * W) * sizeof(double);
+  // edges [L,R][2 parity][S+1][W+2], ring [6][3][2W], 6 ring mbarriers
+  return (size_t(4) * (S + 1) * (W + 2) + size_t(6) * 3 * 2 * W) * sizeof(double) + 6 * sizeof(uint64_t);
 }
 
 // strip widths (threads) k_wave2 is instantiated for; each thread covers 2 columns

@@ -29,6 +29,13 @@ __device__ __forceinline__ void bulk_to_peer(unsigned remote_dst, unsigned local
       "r"(local_src), "r"(bytes), "r"(remote_bar)
       : "memory");
 }
+// bulk copy of `bytes` (multiple of 16, both addresses 16-byte aligned) from global memory into
+// this CTA's shared memory, completing the bytes on the CTA's mbarrier
+__device__ __forceinline__ void bulk_from_global(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 // generic-proxy shared-memory writes visible to the async proxy (before a bulk copy reads them)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

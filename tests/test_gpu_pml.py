@@ -240,3 +240,84 @@ def test_pml_parareal_sharded_equals_single_gpu(world):
         a = 1 + r * chunk
         b = min(N + 1, a + chunk)
         assert np.array_equal(o["states"][:, a - 1:b], single["states"][:, a - 1:b])
+
+
+@pytest.mark.parametrize("kind,nf,width", [(0, 64, 8), (1, 64, 8), (0, 256, 32)])
+def test_pml_theta_parareal_matches_oracle(ctx, kind, nf, width):
+    """Theta (Procrustes) parareal with the absorbing layer (ptb_pml_theta_run) vs
+    oracle/pml_np.theta_parareal: corrector ranks equal, iterates within 1e-10 relative per field
+    (the north star's iterate tolerance; tol 1e-4 as the periodic config tests), converged slices exact."""
+    import paratime_b200 as B
+    from tests.test_pml_oracle import _small_parareal
+
+    s = _small_parareal(kind, N=5 if nf > 64 else 7, K=3, nf=nf, W=width)
+    v0 = np.zeros_like(s["u0"])
+    its, err, ranks = M.theta_parareal(s["u0"], v0, s["kf"], s["mf"], s["kc"], s["mc"], s["t"], s["N"], s["K"],
+                                       s["cc"], tol=1e-4)
+    nf, nc, W = s["nf"], s["nc"], s["W"]
+    gf, gc = B.Grid((nf, nf), (1 / nf, 1 / nf)), B.Grid((nc, nc), (1 / nc, 1 / nc))
+    zf = M.damping_profile(nf, W, 1 / nf, 1.0)
+    zc = M.damping_profile(nc, W // 4, 1 / nc, 1.0)
+    fine = B.PmlPropagator(ctx, gf, s["c"], zf, zf, s["dtf"], s["mf"])
+    coarse = B.PmlPropagator(ctx, gc, s["cc"], zc, zc, s["dtc"], s["mc"])
+    tr = B.Transfer(ctx, gc, gf, kind)
+    r = B.pml_theta_run(fine, coarse, tr, s["N"], s["K"], s["u0"], v0, tol=1e-4, keep_states=True)
+    assert not r["diverged"]
+    assert list(r["rank"]) == list(ranks), (r["rank"], ranks)
+    last = its[-1]
+    for f in range(4):
+        want = np.stack([last[n][f] for n in range(s["N"] + 1)])
+        got = r["states"][f]
+        assert _rel(got, want) <= 1e-10, (f, _rel(got, want))
+    for k in range(s["K"]):
+        assert np.all(r["rel_err"][k, : k + 2] == 0.0), r["rel_err"][k]
+    np.testing.assert_allclose(r["rel_err"][:, s["K"] + 1:], err[:, s["K"] + 1:], rtol=1e-7)
+    assert np.all(r["residual"] >= 0) and np.all(r["iteration_ms"] > 0)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pml_theta_sharded_equals_single_gpu(world):
+    """Theta with the layer, slices sharded over loopback ranks: bitwise equal to one GPU (the stage
+    flags travel with the coarse payload; the corrector fit and the sweep are replicated)."""
+    import threading
+
+    import paratime_b200 as B
+    from tests.test_pml_oracle import _small_parareal
+
+    s = _small_parareal(0, N=7, K=3)
+    nf, nc, W = s["nf"], s["nc"], s["W"]
+    gf, gc = B.Grid((nf, nf), (1 / nf, 1 / nf)), B.Grid((nc, nc), (1 / nc, 1 / nc))
+    zf = M.damping_profile(nf, W, 1 / nf, 1.0)
+    zc = M.damping_profile(nc, W // 4, 1 / nc, 1.0)
+    v0 = np.zeros_like(s["u0"])
+
+    def objects(c):
+        return (B.PmlPropagator(c, gf, s["c"], zf, zf, s["dtf"], s["mf"]),
+                B.PmlPropagator(c, gc, s["cc"], zc, zc, s["dtc"], s["mc"]), B.Transfer(c, gc, gf, 0))
+
+    single = B.pml_theta_run(*objects(B.Context(0)), s["N"], s["K"], s["u0"], v0, keep_states=True)
+    group = B.api.LoopbackGroup(world)
+    ctxs = [B.Context(0) for _ in range(world)]
+    objs = [objects(c) for c in ctxs]
+    comms = [group.comm(ctxs[r], r) for r in range(world)]
+    out, errs = [None] * world, []
+
+    def work(r):
+        try:
+            out[r] = B.pml_theta_run(*objs[r], s["N"], s["K"], s["u0"], v0, keep_states=True, comm=comms[r])
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    chunk = -(-s["N"] // world)
+    for r, o in enumerate(out):
+        assert np.array_equal(o["rel_err"], single["rel_err"])
+        assert list(o["rank"]) == list(single["rank"])
+        a = 1 + r * chunk
+        b = min(s["N"] + 1, a + chunk)
+        assert np.array_equal(o["states"][:, a - 1:b], single["states"][:, a - 1:b])

@@ -123,3 +123,40 @@ def test_plain_parareal_oracle_exactness_and_convergence(kind):
     assert np.all(np.isfinite(err))
     if kind == 0:  # plain parareal need not converge for waves (the paper's motivation); here it does
         assert np.max(err[-1]) < np.max(err[0])
+
+
+def test_theta_parareal_zero_profile_is_the_periodic_theta_oracle():
+    """With no layer the layered theta coupling IS the reference's theta_engine (parareal.cpp:255-350):
+    oracle/pml_np.theta_parareal on a zero profile equals oracle/paratime_np.theta_parareal (pinned
+    to the compiled reference in tests/test_oracle_pin.py) to the theta path's round-off floor."""
+    s = _small_parareal(0, N=6, K=3, W=8)
+    nf, nc = s["nf"], s["nc"]
+    hf, hc = 1 / nf, 1 / nc
+    z_f, z_c = np.zeros(nf), np.zeros(nc)
+    kf = M.PmlCoefficients(s["c"], hf, hf, s["dtf"], z_f, z_f)
+    kc = M.PmlCoefficients(s["cc"], hc, hc, s["dtc"], z_c, z_c)
+    v0 = np.zeros_like(s["u0"])
+    its, err, ranks = M.theta_parareal(s["u0"], v0, kf, s["mf"], kc, s["mc"], s["t"], s["N"], s["K"], s["cc"], tol=1e-4)
+    sch = P.Schedule(T=s["N"] * s["dtf"] * s["mf"], dt_com=s["dtf"] * s["mf"], n=s["N"], fine_grid=s["t"].fine,
+                     c_fine=s["c"], dt_fine=s["dtf"], m_fine=s["mf"], coarse_grid=s["t"].coarse, c_coarse=s["cc"],
+                     dt_coarse=s["dtc"], m_coarse=s["mc"])
+    run = P.theta_parareal((s["u0"], v0), sch, s["t"], s["K"], tol=1e-4)
+    for k in range(s["K"]):
+        assert run.iterations[k + 1].rank == ranks[k]
+        for n in range(s["N"] + 1):
+            want = np.concatenate([run.iterations[k + 1].states[n][0].ravel(), run.iterations[k + 1].states[n][1].ravel()])
+            got = np.concatenate([its[k][n][0].ravel(), its[k][n][1].ravel()])
+            assert np.linalg.norm(got - want) <= 1e-10 * max(np.linalg.norm(want), 1e-300), (k, n)
+            assert not its[k][n][2].any() and not its[k][n][3].any()
+
+
+def test_theta_parareal_layer_exactness_and_stability():
+    """With the layer: slices n <= k+1 are exact after iteration k (the parareal exactness property),
+    and where plain parareal's iterates grow the theta coupling keeps them bounded."""
+    s = _small_parareal(0, N=8, K=4, W=8)
+    v0 = np.zeros_like(s["u0"])
+    _, et, ranks = M.theta_parareal(s["u0"], v0, s["kf"], s["mf"], s["kc"], s["mc"], s["t"], s["N"], s["K"], s["cc"])
+    for k in range(s["K"]):
+        assert np.all(et[k, : k + 2] == 0.0), et[k]
+    assert np.all(np.isfinite(et)) and all(r > 0 for r in ranks)
+    assert list(ranks) == sorted(ranks)  # the corrector accumulates snapshots
