@@ -29,6 +29,8 @@
 //   k_geam_sub       D = F - D (relative_residual, procrustes.cpp:251).
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "ptb_internal.h"
 #include "ptb_procrustes.h"
@@ -188,6 +190,111 @@ __global__ void __launch_bounds__(GT, 1) k_dgemm(const GemmArgs a) {
   }
 }
 
+// ---- the fp64 tensor-core variant (DMMA, mma.sync m8n8k4 f64) ----------------------------------
+// Same CTA tile (128 x 64, BK = 16, split-K, register-staged double-buffered shared memory) and the
+// same global->shared staging as k_dgemm; 8 warps in a 4 x 2 grid, each a 32 x 32 block = 4 x 4
+// m8n8k4 tiles (32 accumulator doubles per lane).  Per 4-deep k step a warp loads 4 A and 4 B
+// fragments (LDS.64: lane l holds A(8p + l/4, kk + l%4) / B(kk + l%4, 8q + l/4)) and issues 16
+// DMMA.  Row strides of 136 / 72 doubles (= 8 mod 16) put the four k rows of a fragment load on
+// disjoint bank halves: two wavefronts per LDS.64, the minimum for 256 bytes.  Each output is one
+// fixed-order accumulation over k (the DMMA's internal order), independent of the launch shape.
+constexpr int MLDS_A = BM + 8, MLDS_B = BN + 8;
+constexpr size_t MMA_SMEM = size_t(2) * BK * (MLDS_A + MLDS_B) * sizeof(double);
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <bool TA>
+__device__ __forceinline__ void store_a_m(double* As, const double (&r)[AL]) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < AL; ++j) {
+    const int i = TA ? t / BK + (GT / BK) * j : t % BM, kk = TA ? t % BK : t / BM + (GT / BM) * j;
+    As[kk * MLDS_A + i] = r[j];
+  }
+}
+template <bool TB>
+__device__ __forceinline__ void store_b_m(double* Bs, const double (&r)[BL]) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < BL; ++j) {
+    const int c = TB ? t % BN : t / BK + (GT / BK) * j, kk = TB ? t / BN + (GT / BN) * j : t % BK;
+    Bs[kk * MLDS_B + c] = r[j];
+  }
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GT, 2) k_dgemm_mma(const GemmArgs a) {
+  extern __shared__ __align__(16) double gsm[];
+  double* const Asm = gsm;
+  double* const Bsm = gsm + 2 * BK * MLDS_A;
+  const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
+  const int kbeg = blockIdx.z * a.kchunk, kend = min(a.k, kbeg + a.kchunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;  // the warp's 32 x 32 block
+  const int fr = lane >> 2, fk = lane & 3;                 // fragment row (or column) / k index
+  double acc[4][4][2];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[p][q][0] = acc[p][q][1] = 0.0;
+  double ra[AL], rb[BL];
+  load_a<TA>(a, i0, kbeg, kend, ra);
+  load_b<TB>(a, j0, kbeg, kend, rb);
+  store_a_m<TA>(Asm, ra);
+  store_b_m<TB>(Bsm, rb);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = kbeg; k0 < kend; k0 += BK) {
+    const bool more = k0 + BK < kend;
+    if (more) {
+      load_a<TA>(a, i0, k0 + BK, kend, ra);
+      load_b<TB>(a, j0, k0 + BK, kend, rb);
+    }
+    const double* as = Asm + buf * (BK * MLDS_A) + fk * MLDS_A + wm + fr;
+    const double* bs = Bsm + buf * (BK * MLDS_B) + fk * MLDS_B + wn + fr;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) af[p] = as[kk * MLDS_A + 8 * p];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bf[q] = bs[kk * MLDS_B + 8 * q];
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dmma884(acc[p][q], af[p], bf[q]);
+    }
+    if (more) {
+      store_a_m<TA>(Asm + (buf ^ 1) * (BK * MLDS_A), ra);
+      store_b_m<TB>(Bsm + (buf ^ 1) * (BK * MLDS_B), rb);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int i = i0 + wm + 8 * p + fr;
+    if (i >= a.m) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = j0 + wn + 8 * q + 2 * fk + h;
+        if (j >= a.n) continue;
+        if (a.ws) {
+          a.ws[(size_t(blockIdx.z) * a.n + j) * a.m + i] = acc[p][q][h];
+        } else {
+          double* c = a.C + i + size_t(j) * a.ldc;
+          *c = a.beta == 0.0 ? a.alpha * acc[p][q][h] : a.alpha * acc[p][q][h] + a.beta * *c;
+        }
+      }
+  }
+}
+
 // C = alpha sum_z ws[z] + beta C, partials summed in split order (deterministic)
 __global__ void k_splitk_reduce(int m, int n, int splits, const double* __restrict__ ws, double alpha, double beta,
                                 double* C, int ldc) {
@@ -253,6 +360,12 @@ unsigned ew_grid(ptb_context* ctx, size_t total) {
   return unsigned(std::min<size_t>((total + 255) / 256, size_t(ctx->num_sms) * 8));
 }
 
+// PTB_DGEMM=dfma|dmma selects the kernel family (A/B measurements); default: DMMA
+bool use_dmma() {
+  const char* e = std::getenv("PTB_DGEMM");  // read per call: tests switch it with monkeypatch
+  return !(e && std::string(e) == "dfma");
+}
+
 double* workspace(ptb_context* ctx, size_t doubles) {
   return static_cast<double*>(ctx->gemm_ws.get(std::max<size_t>(1, doubles) * sizeof(double)));
 }
@@ -303,10 +416,20 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
                           reinterpret_cast<const void*>(k_dgemm<false, true>),
                           reinterpret_cast<const void*>(k_dgemm<true, true>)})
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GEMM_SMEM));
+    for (const void* f : {reinterpret_cast<const void*>(k_dgemm_mma<false, false>),
+                          reinterpret_cast<const void*>(k_dgemm_mma<true, false>),
+                          reinterpret_cast<const void*>(k_dgemm_mma<false, true>),
+                          reinterpret_cast<const void*>(k_dgemm_mma<true, true>)})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(MMA_SMEM));
     return true;
   }();
   (void)attrs;
-  if (!ta && !tb) k_dgemm<false, false><<<grid, GT, GEMM_SMEM, st>>>(a);
+  if (use_dmma()) {
+    if (!ta && !tb) k_dgemm_mma<false, false><<<grid, GT, MMA_SMEM, st>>>(a);
+    else if (ta && !tb) k_dgemm_mma<true, false><<<grid, GT, MMA_SMEM, st>>>(a);
+    else if (!ta && tb) k_dgemm_mma<false, true><<<grid, GT, MMA_SMEM, st>>>(a);
+    else k_dgemm_mma<true, true><<<grid, GT, MMA_SMEM, st>>>(a);
+  } else if (!ta && !tb) k_dgemm<false, false><<<grid, GT, GEMM_SMEM, st>>>(a);
   else if (ta && !tb) k_dgemm<true, false><<<grid, GT, GEMM_SMEM, st>>>(a);
   else if (!ta && tb) k_dgemm<false, true><<<grid, GT, GEMM_SMEM, st>>>(a);
   else k_dgemm<true, true><<<grid, GT, GEMM_SMEM, st>>>(a);

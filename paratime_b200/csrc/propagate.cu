@@ -46,8 +46,12 @@
 
 #include "ptb_internal.h"
 
-#ifndef PTB_WAVE2_CPASYNC  // 1: round-1 per-thread cp.async ring in k_wave2 (A/B builds only)
-#define PTB_WAVE2_CPASYNC 0
+// k_wave2's level-0 ring (A/B builds; see DESIGN.md 3.1 for the measurements):
+//   0: per-thread 16-byte cp.async (LDGSTS, L1-allocating .ca)   1: the same with .cg (L2 only)
+//   2: bulk copies (cp.async.bulk, TMA engine) of the CTA's rows by one thread, one mbarrier per slot
+//   3: bulk copies of each warp's 64-column segment by its lane 0, one mbarrier per slot and warp
+#ifndef PTB_WAVE2_RING
+#define PTB_WAVE2_RING 0
 #endif
 
 namespace ptb {
@@ -673,10 +677,17 @@ __global__ void __launch_bounds__(512) k_wave(const WaveArgs a) {
 // stores.  Requires even nx (pairs never straddle the periodic wrap); the strip halo is the
 // even HXE = S + 2 columns per side.  Arithmetic identical to k_wave/k_small FAST.
 
+template <bool CG = false>
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+  if constexpr (CG)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
+// bulk-copy issuers per CTA for k_wave2's ring variants 2 (one) and 3 (one per warp)
+template <int RINGV, int T>
+constexpr int RING_ISSUERS = RINGV == 3 ? T / 32 : 1;
 
 template <int S, int W, int PAR, bool RY1>
 __device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __restrict__ eR, const int offl,
@@ -825,35 +836,40 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     o += nx;
     if (o >= npts) o -= npts;
   };
-#if PTB_WAVE2_CPASYNC
+#if PTB_WAVE2_RING <= 1
   auto issue = [&](int slot, int) {
     double2* d = ring + (slot * 3) * T + j;
-    cp_async16(d, U + ou);
-    cp_async16(d + T, V + ov);
-    cp_async16(d + 2 * T, K + ov);
+    cp_async16<PTB_WAVE2_RING == 1>(d, U + ou);
+    cp_async16<PTB_WAVE2_RING == 1>(d + T, V + ov);
+    cp_async16<PTB_WAVE2_RING == 1>(d + 2 * T, K + ov);
     cp_async_commit();
     adv(ou);
     adv(ov);
   };
 #else
-  // Level-0 rows arrive by bulk copies (the TMA engine, cp.async.bulk): one thread moves the
-  // strip's u, udot and coefficient row segments (2W contiguous doubles each, split where the
-  // strip wraps the periodic x boundary) into the ring slot and they complete on the slot's
-  // mbarrier.  Every thread then waits on the barrier's phase and reads its pair: no per-thread
-  // LDGSTS through the LSU, which the edge exchange saturates (profiles/r01_k1_full.md).
+  // Level-0 rows arrive by bulk copies (the TMA engine, cp.async.bulk) that complete on an
+  // mbarrier; every thread waits on the barrier's phase and reads its pair from the slot.
+  //   RING 2: one thread moves the CTA's three row segments (2W doubles each, split where the strip
+  //           wraps the periodic x boundary), one barrier per slot;
+  //   RING 3: lane 0 of each warp moves the warp's 64-column segments, one barrier per slot and warp
+  //           (no cross-warp dependency: a warp only waits for its own bytes).
+  constexpr int NW = RING_ISSUERS<PTB_WAVE2_RING, T>;
+  constexpr int SEG = 2 * T / NW;  // doubles per issuer and row
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RING * 3 * T);
-  const int gx0 = FULL ? 0 : ((x0 - HXE) % nx + nx) % nx;  // first column of the strip
-  int ru = 0, rv = 0;                                       // next u row / udot,coef row (thread 0)
-  if (j == 0) {
+  const int wid = PTB_WAVE2_RING == 3 ? (j >> 5) : 0;
+  const bool issuer = PTB_WAVE2_RING == 3 ? (j & 31) == 0 : j == 0;
+  const int gx0 = ((FULL ? 0 : ((x0 - HXE) % nx + nx) % nx) + SEG * wid) % nx;  // first column of the segment
+  int ru = 0, rv = 0;  // next u row / udot,coef row (issuers)
+  if (issuer) {
     ru = ((ystart + 1) % ny + ny) % ny;
     rv = ((ystart) % ny + ny) % ny;
 #pragma unroll
-    for (int s0 = 0; s0 < RING; ++s0) mbar_init(smem_addr(&bars[s0]), 1);
+    for (int s0 = 0; s0 < RING; ++s0) mbar_init(smem_addr(&bars[s0 * NW + wid]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   auto copy_row = [&](double* dst, const double* row, unsigned bar) {
-    int col = gx0, rem = 2 * T;
+    int col = gx0, rem = SEG;
     while (rem > 0) {
       const int len = min(rem, nx - col);
       bulk_from_global(smem_addr(dst), row + col, unsigned(len) * 8u, bar);
@@ -863,10 +879,10 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     }
   };
   auto issue = [&](int slot, int iter) {
-    if (j == 0 && iter < n_iter) {
-      const unsigned bar = smem_addr(&bars[slot]);
-      mbar_expect(bar, unsigned(3 * 2 * T) * 8u);
-      double* d = reinterpret_cast<double*>(ring + (slot * 3) * T);
+    if (issuer && iter < n_iter) {
+      const unsigned bar = smem_addr(&bars[slot * NW + wid]);
+      mbar_expect(bar, unsigned(3 * SEG) * 8u);
+      double* d = reinterpret_cast<double*>(ring + (slot * 3) * T) + SEG * wid;
       copy_row(d, U + size_t(ru) * nx, bar);
       copy_row(d + 2 * T, V + size_t(rv) * nx, bar);
       copy_row(d + 4 * T, K + size_t(rv) * nx, bar);
@@ -884,10 +900,10 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
 #pragma unroll
     for (int k = 0; k < UNROLL; ++k) {
       const int i = i0 + k;
-#if PTB_WAVE2_CPASYNC
+#if PTB_WAVE2_RING <= 1
       cp_async_wait<RING - 2>();
 #else
-      mbar_wait(smem_addr(&bars[k]), unsigned(i0 / UNROLL) & 1u);
+      mbar_wait(smem_addr(&bars[k * NW + wid]), unsigned(i0 / UNROLL) & 1u);
 #endif
       const double2* src = ring + ((k % RING) * 3) * T + j;
       const double2 uu0 = src[0], v0 = src[T], k0 = src[2 * T];
@@ -906,7 +922,7 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
       __syncthreads();
     }
   }
-#if PTB_WAVE2_CPASYNC
+#if PTB_WAVE2_RING <= 1
   cp_async_wait<0>();
 #endif
   if (a.flags) {
@@ -1094,8 +1110,9 @@ void launch_wave(ptb_context* ctx, cudaStream_t st, const WavePlan& pl, WaveArgs
 
 // k_wave2: W threads cover 2W columns; useful width even; occupancy from the runtime.
 size_t wave2_smem(int S, int W) {
-  // edges [L,R][2 parity][S+1][W+2], ring [6][3][2W], 6 ring mbarriers
-  return (size_t(4) * (S + 1) * (W + 2) + size_t(6) * 3 * 2 * W) * sizeof(double) + 6 * sizeof(uint64_t);
+  // edges [L,R][2 parity][S+1][W+2], ring [6][3][2W], ring mbarriers (bulk variants)
+  return (size_t(4) * (S + 1) * (W + 2) + size_t(6) * 3 * 2 * W) * sizeof(double) +
+         (PTB_WAVE2_RING >= 2 ? size_t(6) * (W / 32 + 1) * sizeof(uint64_t) : 0);
 }
 
 // strip widths (threads) k_wave2 is instantiated for; each thread covers 2 columns

@@ -1,8 +1,8 @@
 # round-2 call M: bulk-copy k_wave2 ring + theta with the absorbing layer (parity), A/B vs the
 # cp.async ring on the cfg5 sweep, hand-written DGEMM vs cuBLAS DMMA on the corrector shapes
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_gpu_pml.py tests/test_gpu_bench_plans.py tests/test_gpu_propagator.py tests/test_gpu_fullrow.py -q -x -rf > gpurun_out/r02m_tests.log 2>&1; echo tests_rc=$?
-tail -6 gpurun_out/r02m_tests.log
+timeout 1500 python -m pytest tests/test_gpu_pml.py tests/test_gpu_bench_plans.py tests/test_gpu_propagator.py tests/test_gpu_fullrow.py -q -x -rf --durations=25 > gpurun_out/r02m_tests.log 2>&1; echo tests_rc=$?
+tail -40 gpurun_out/r02m_tests.log
 for v in bulk cpasync; do
   if [ $v = cpasync ]; then export PTB_LIB=$PWD/paratime_b200/_ab/libparatime_b200_cpasync.so; fi
   timeout 900 python bench.py --no-parareal --no-pml --no-cpu --no-e2e --steps 5 > gpurun_out/r02m_bench_$v.json 2> gpurun_out/r02m_bench_$v.err; echo bench_$v=$?

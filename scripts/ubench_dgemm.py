@@ -1,4 +1,4 @@
-"""The hand-written DGEMM (ptb_dgemm, csrc/gemm.cu: DFMA register tiles) against cuBLAS's
+"""The hand-written DGEMM (ptb_dgemm, csrc/gemm.cu: DMMA tiles and DFMA register tiles) against cuBLAS's
 DMMA kernels (torch float64 matmul, measurement only) on the corrector's shapes.
 
 Shapes (column-major BLAS view, rows = 3 N_c of config 4 = 196608, r ~ 150, N = 128):
@@ -59,9 +59,14 @@ for name, ta, tb, m, n, k in SHAPES:
         torch.matmul(opA, opB)
 
     reps = 5 if m * n * k > 1e9 else 50
+    os.environ["PTB_DGEMM"] = "dmma"
     t_o = timed(ours, reps)
+    os.environ["PTB_DGEMM"] = "dfma"
+    t_f = timed(ours, reps)
+    os.environ.pop("PTB_DGEMM")
     t_c = timed(cublas, reps)
     fl = 2.0 * m * n * k
-    print(json.dumps({"shape": name, "m": m, "n": n, "k": k, "ours_ms": round(t_o, 4),
-                      "ours_tflops": round(fl / t_o / 1e9, 2), "cublas_dmma_ms": round(t_c, 4),
+    print(json.dumps({"shape": name, "m": m, "n": n, "k": k, "ours_dmma_ms": round(t_o, 4),
+                      "ours_dmma_tflops": round(fl / t_o / 1e9, 2), "ours_dfma_ms": round(t_f, 4),
+                      "ours_dfma_tflops": round(fl / t_f / 1e9, 2), "cublas_dmma_ms": round(t_c, 4),
                       "cublas_tflops": round(fl / t_c / 1e9, 2)}), flush=True)

@@ -1,4 +1,4 @@
-"""The hand-written DGEMM / DGEMV (csrc/gemm.cu) against numpy on the corrector's shapes.
+"""The hand-written DGEMM / DGEMV (csrc/gemm.cu, DMMA and DFMA families) against numpy on the corrector's shapes.
 
 Every Eigen product of the reference's Procrustes step (procrustes.cpp:65-66, 201-234, 251) and
 PhaseCorrector::apply (:82-86) runs through it: tall-skinny transposed products with split-K
@@ -53,9 +53,12 @@ def _run(ta, tb, m, n, k, alpha, beta, pad, seed):
     return got[:, :m].T, want, k
 
 
+@pytest.mark.parametrize("family", ["dmma", "dfma"])
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("alpha,beta", [(1.0, 0.0), (-1.0, 1.0), (0.5, -2.0)])
-def test_dgemm_matches_numpy(shape, alpha, beta):
+def test_dgemm_matches_numpy(shape, alpha, beta, family, monkeypatch):
+    """Both kernel families: k_dgemm_mma (fp64 tensor cores, the default) and k_dgemm (DFMA)."""
+    monkeypatch.setenv("PTB_DGEMM", family)
     got, want, k = _run(*shape, alpha, beta, pad=3, seed=sum(shape))
     scale = np.sqrt(max(k, 1)) * (abs(alpha) + abs(beta)) * 4
     assert np.max(np.abs(got - want)) <= 1e-15 * scale * max(1.0, np.max(np.abs(want))) + 1e-300

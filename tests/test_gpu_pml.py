@@ -269,8 +269,9 @@ def test_pml_theta_parareal_matches_oracle(ctx, kind, nf, width):
         want = np.stack([last[n][f] for n in range(s["N"] + 1)])
         got = r["states"][f]
         assert _rel(got, want) <= 1e-10, (f, _rel(got, want))
-    for k in range(s["K"]):
-        assert np.all(r["rel_err"][k, : k + 2] == 0.0), r["rel_err"][k]
+    for k in range(s["K"]):  # converged slices: exact up to the sweep's round-off (corrected(old[n]) is a
+        # batched product, corrected(w) a per-step one; test_gpu_path.py applies the same bound)
+        assert np.all(r["rel_err"][k, : k + 2] <= 1e-12), r["rel_err"][k]
     np.testing.assert_allclose(r["rel_err"][:, s["K"] + 1:], err[:, s["K"] + 1:], rtol=1e-7)
     assert np.all(r["residual"] >= 0) and np.all(r["iteration_ms"] > 0)
 
