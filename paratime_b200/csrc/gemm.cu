@@ -54,6 +54,7 @@ struct GemmArgs {
   double alpha, beta;
   int kchunk;  // k-range per blockIdx.z
   double* ws;  // split-K partials [z][n][m] (null: write C)
+  int tc = 0;  // 1: the kernel computes C^T (m x n here = C's n x m): element (i, j) goes to C[j + i ldc]
 };
 
 // op(A) tile (BM x BK) of k-tile k0 into registers.  !TA: A(i, kk) = A[i + kk lda], a warp reads
@@ -207,13 +208,54 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Staging for the DMMA kernel.  Where op(A) / op(B) is contiguous along k in memory (TA, !TB) a
+// warp covers 8 rows x 4 consecutive k (one 32-byte sector per row) instead of 2 rows x 16 k: the
+// shared-memory store of a fixed k-row then hits 8 consecutive addresses in each of 4 k-rows, whose
+// bank halves alternate (row stride 8 mod 16 doubles) -- 2 wavefronts per STS.64 instead of 8.
+// Where op(A) / op(B) is contiguous along m / n the layout of load_a / load_b is kept.
+template <bool TA>
+__device__ __forceinline__ void load_a_m(const GemmArgs& a, int i0, int k0, int kend, double (&r)[AL]) {
+  if constexpr (!TA) {
+    load_a<false>(a, i0, k0, kend, r);
+  } else {
+    const int t = threadIdx.x, kb = t % 4, ib = t / 4;  // element j: (ib + 64 (j & 1), kb + 4 (j >> 1))
+    const size_t lda = size_t(a.lda);
+    const double* p = a.A + (k0 + kb) + size_t(i0 + ib) * lda;
+    if (i0 + BM <= a.m && k0 + BK <= kend) {
+#pragma unroll
+      for (int j = 0; j < AL; ++j) r[j] = p[4 * (j >> 1) + size_t(64 * (j & 1)) * lda];
+    } else {
+#pragma unroll
+      for (int j = 0; j < AL; ++j)
+        r[j] = (i0 + ib + 64 * (j & 1) < a.m && k0 + kb + 4 * (j >> 1) < kend)
+                   ? p[4 * (j >> 1) + size_t(64 * (j & 1)) * lda]
+                   : 0.0;
+    }
+  }
+}
 template <bool TA>
 __device__ __forceinline__ void store_a_m(double* As, const double (&r)[AL]) {
   const int t = threadIdx.x;
 #pragma unroll
   for (int j = 0; j < AL; ++j) {
-    const int i = TA ? t / BK + (GT / BK) * j : t % BM, kk = TA ? t % BK : t / BM + (GT / BM) * j;
+    const int i = TA ? t / 4 + 64 * (j & 1) : t % BM, kk = TA ? t % 4 + 4 * (j >> 1) : t / BM + (GT / BM) * j;
     As[kk * MLDS_A + i] = r[j];
+  }
+}
+template <bool TB>
+__device__ __forceinline__ void load_b_m(const GemmArgs& a, int j0, int k0, int kend, double (&r)[BL]) {
+  if constexpr (TB) {
+    load_b<true>(a, j0, k0, kend, r);
+  } else {
+    const int t = threadIdx.x, kb = t % 4, cb = t / 4;  // element j: (kb + 4 j, cb)
+    const double* p = a.B + (k0 + kb) + size_t(j0 + cb) * size_t(a.ldb);
+    if (j0 + BN <= a.n && k0 + BK <= kend) {
+#pragma unroll
+      for (int j = 0; j < BL; ++j) r[j] = p[4 * j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < BL; ++j) r[j] = (j0 + cb < a.n && k0 + kb + 4 * j < kend) ? p[4 * j] : 0.0;
+    }
   }
 }
 template <bool TB>
@@ -221,7 +263,7 @@ __device__ __forceinline__ void store_b_m(double* Bs, const double (&r)[BL]) {
   const int t = threadIdx.x;
 #pragma unroll
   for (int j = 0; j < BL; ++j) {
-    const int c = TB ? t % BN : t / BK + (GT / BK) * j, kk = TB ? t / BN + (GT / BN) * j : t % BK;
+    const int c = TB ? t % BN : t / 4, kk = TB ? t / BN + (GT / BN) * j : t % 4 + 4 * j;
     Bs[kk * MLDS_B + c] = r[j];
   }
 }
@@ -242,8 +284,8 @@ __global__ void __launch_bounds__(GT, 2) k_dgemm_mma(const GemmArgs a) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[p][q][0] = acc[p][q][1] = 0.0;
   double ra[AL], rb[BL];
-  load_a<TA>(a, i0, kbeg, kend, ra);
-  load_b<TB>(a, j0, kbeg, kend, rb);
+  load_a_m<TA>(a, i0, kbeg, kend, ra);
+  load_b_m<TB>(a, j0, kbeg, kend, rb);
   store_a_m<TA>(Asm, ra);
   store_b_m<TB>(Bsm, rb);
   __syncthreads();
@@ -251,8 +293,8 @@ __global__ void __launch_bounds__(GT, 2) k_dgemm_mma(const GemmArgs a) {
   for (int k0 = kbeg; k0 < kend; k0 += BK) {
     const bool more = k0 + BK < kend;
     if (more) {
-      load_a<TA>(a, i0, k0 + BK, kend, ra);
-      load_b<TB>(a, j0, k0 + BK, kend, rb);
+      load_a_m<TA>(a, i0, k0 + BK, kend, ra);
+      load_b_m<TB>(a, j0, k0 + BK, kend, rb);
     }
     const double* as = Asm + buf * (BK * MLDS_A) + fk * MLDS_A + wm + fr;
     const double* bs = Bsm + buf * (BK * MLDS_B) + fk * MLDS_B + wn + fr;
@@ -288,7 +330,7 @@ __global__ void __launch_bounds__(GT, 2) k_dgemm_mma(const GemmArgs a) {
         if (a.ws) {
           a.ws[(size_t(blockIdx.z) * a.n + j) * a.m + i] = acc[p][q][h];
         } else {
-          double* c = a.C + i + size_t(j) * a.ldc;
+          double* c = a.tc ? a.C + j + size_t(i) * a.ldc : a.C + i + size_t(j) * a.ldc;
           *c = a.beta == 0.0 ? a.alpha * acc[p][q][h] : a.alpha * acc[p][q][h] + a.beta * *c;
         }
       }
@@ -297,13 +339,13 @@ __global__ void __launch_bounds__(GT, 2) k_dgemm_mma(const GemmArgs a) {
 
 // C = alpha sum_z ws[z] + beta C, partials summed in split order (deterministic)
 __global__ void k_splitk_reduce(int m, int n, int splits, const double* __restrict__ ws, double alpha, double beta,
-                                double* C, int ldc) {
+                                double* C, int ldc, int tc = 0) {
   const size_t total = size_t(m) * n;
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += ws[size_t(z) * total + e];
     const size_t i = e % m, j = e / m;
-    double* c = C + i + j * ldc;
+    double* c = tc ? C + j + i * ldc : C + i + j * ldc;
     *c = beta == 0.0 ? alpha * s : alpha * s + beta * *c;
   }
 }
@@ -372,6 +414,9 @@ double* workspace(ptb_context* ctx, size_t doubles) {
 
 }  // namespace
 
+void gemm_core(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
+               const double* B, int ldb, double beta, double* C, int ldc, int tc);
+
 // C (m x n) = alpha op(A) op(B) + beta C, all column-major (BLAS dgemm semantics)
 void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
           const double* B, int ldb, double beta, double* C, int ldc) {
@@ -400,6 +445,26 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
     PTB_LAUNCH_CHECK(ctx);
     return;
   }
+  // DMMA: a short m that the 128-row tile would pad badly (the corrector's U^T F, r x N') is
+  // computed as C^T = op(B)^T op(A)^T with a transposed store when that pads less
+  if (use_dmma() && m <= 1024 && n <= 1024) {
+    const auto padded = [](int rows, int cols) { return size_t((rows + BM - 1) / BM * BM) * ((cols + BN - 1) / BN * BN); };
+    if (padded(n, m) < padded(m, n)) {
+      std::swap(m, n);
+      std::swap(A, B);
+      std::swap(lda, ldb);
+      std::swap(ta, tb);
+      ta = !ta;
+      tb = !tb;
+      return gemm_core(ctx, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, 1);
+    }
+  }
+  return gemm_core(ctx, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+}
+
+void gemm_core(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
+               const double* B, int ldb, double beta, double* C, int ldc, int tc) {
+  cudaStream_t st = ctx->stream;
   const int tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN, tiles = tm * tn;
   // split K so the grid covers >= 2 CTAs per SM, keeping >= 4 k-tiles per split
   int splits = 1;
@@ -407,7 +472,7 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
   if (tiles < want) splits = std::min({(want + tiles - 1) / tiles, (k + 4 * BK - 1) / (4 * BK), 128});
   int kchunk = ((k + splits - 1) / splits + BK - 1) / BK * BK;
   splits = (k + kchunk - 1) / kchunk;
-  GemmArgs a{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, nullptr};
+  GemmArgs a{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, nullptr, tc};
   if (splits > 1) a.ws = workspace(ctx, size_t(splits) * m * n);
   const dim3 grid{unsigned(tm), unsigned(tn), unsigned(splits)};
   static const bool attrs = [] {
@@ -435,7 +500,7 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
   else k_dgemm<true, true><<<grid, GT, GEMM_SMEM, st>>>(a);
   PTB_LAUNCH_CHECK(ctx);
   if (splits > 1) {
-    k_splitk_reduce<<<ew_grid(ctx, size_t(m) * n), 256, 0, st>>>(m, n, splits, a.ws, alpha, beta, C, ldc);
+    k_splitk_reduce<<<ew_grid(ctx, size_t(m) * n), 256, 0, st>>>(m, n, splits, a.ws, alpha, beta, C, ldc, tc);
     PTB_LAUNCH_CHECK(ctx);
   }
 }

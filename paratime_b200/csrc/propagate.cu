@@ -50,6 +50,7 @@
 //   0: per-thread 16-byte cp.async (LDGSTS, L1-allocating .ca)   1: the same with .cg (L2 only)
 //   2: bulk copies (cp.async.bulk, TMA engine) of the CTA's rows by one thread, one mbarrier per slot
 //   3: bulk copies of each warp's 64-column segment by its lane 0, one mbarrier per slot and warp
+//   4, 5: no ring: 16-byte loads straight into registers 2 (4) or 3 (5) rows ahead
 #ifndef PTB_WAVE2_RING
 #define PTB_WAVE2_RING 0
 #endif
@@ -685,6 +686,12 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
+// 16-byte streaming load (read-only path, no L1 allocation)
+__device__ __forceinline__ double2 ldg_stream2(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
 // bulk-copy issuers per CTA for k_wave2's ring variants 2 (one) and 3 (one per warp)
 template <int RINGV, int T>
 constexpr int RING_ISSUERS = RINGV == 3 ? T / 32 : 1;
@@ -846,6 +853,17 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     adv(ou);
     adv(ov);
   };
+#elif PTB_WAVE2_RING >= 4
+  // level-0 inputs straight into registers, PD rows ahead (no shared-memory ring)
+  constexpr int PD = PTB_WAVE2_RING - 2;
+  double2 pu[PD], pv[PD], pk[PD];
+  auto issue = [&](int slot, int) {
+    pu[slot] = ldg_stream2(U + ou);
+    pv[slot] = ldg_stream2(V + ov);
+    pk[slot] = ldg_stream2(K + ov);
+    adv(ou);
+    adv(ov);
+  };
 #else
   // Level-0 rows arrive by bulk copies (the TMA engine, cp.async.bulk) that complete on an
   // mbarrier; every thread waits on the barrier's phase and reads its pair from the slot.
@@ -891,8 +909,13 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     }
   };
 #endif
+#if PTB_WAVE2_RING >= 4
+#pragma unroll
+  for (int s0 = 0; s0 < PD; ++s0) issue(s0, s0);
+#else
 #pragma unroll
   for (int s0 = 0; s0 < RING - 1; ++s0) issue(s0, s0);
+#endif
   __syncthreads();
   bool ok = true;
   const int last_out = nrows + 2 * S;
@@ -900,6 +923,10 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
 #pragma unroll
     for (int k = 0; k < UNROLL; ++k) {
       const int i = i0 + k;
+#if PTB_WAVE2_RING >= 4
+      const double2 uu0 = pu[k % PD], v0 = pv[k % PD], k0 = pk[k % PD];
+      issue(k % PD, i + PD);
+#else
 #if PTB_WAVE2_RING <= 1
       cp_async_wait<RING - 2>();
 #else
@@ -908,6 +935,7 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
       const double2* src = ring + ((k % RING) * 3) * T + j;
       const double2 uu0 = src[0], v0 = src[T], k0 = src[2 * T];
       issue((k + RING - 1) % RING, i + RING - 1);
+#endif
       double2 out_u, out_v;
       if (k & 1)
         wave2_iter<S, W, 1, RY1>(eL, eR, offl, offr, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);

@@ -22,6 +22,9 @@ SHAPES = [  # (ta, tb, m, n, k)
     (0, 0, 65536, 1, 150),     # Z dz (GEMV)
     (1, 0, 150, 1, 196608),    # Y^T v (GEMV^T)
     (1, 0, 1, 1, 5),
+    (0, 1, 150, 100, 64),      # short m: DMMA computes C^T with a transposed store
+    (0, 0, 200, 60, 300),
+    (1, 1, 150, 90, 77),
     (0, 0, 7, 3, 0),           # k = 0: C = beta C
 ]
 
