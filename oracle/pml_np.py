@@ -181,7 +181,7 @@ def plain_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m
 
 
 def theta_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m_c: int, t, N: int, K: int,
-                   c_coarse, tol: float = 1e-4, scheme: int = 0):
+                   c_coarse, tol: float = 1e-4, scheme: int = 0, aux: str = "none"):
     """Theta-parareal (the data-driven Procrustes coupling, parareal.cpp:255-350) on the layered
     state (u, udot, px, py) — this build's extension, the way csrc/pml.cu pml_parareal(theta)
     evaluates it.  The reference defines the coupling on (u, udot) only (energy_map.cpp:137-214);
@@ -189,8 +189,12 @@ def theta_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m
       * snapshots F = Lambda(R fine_next[n]), G = Lambda(C(R cur[n-1])) of the (u, udot) part over
         slices whose four fields are finite; corrector = update_svd(corrector, F, G, tol);
       * the sweep corrects (u, udot) with Lambda-dagger Omega Lambda (corrected_coarse_state,
-        parareal.cpp:245-253) and the auxiliary fields (px, py) additively as plain parareal:
-        d = (corr(w) - corr(old[n]))_{u,udot} ++ (w - old[n])_{px,py},  w = C(w_{n-1});
+        parareal.cpp:245-253); the auxiliary fields (px, py) are not corrected (aux="none", the
+        default: next[n]'s are fine_next[n]'s):
+        d = (corr(w) - corr(old[n]))_{u,udot} ++ (0, 0),  w = C(w_{n-1});
+        aux="plain" corrects them additively as plain parareal, d_p = (w - old[n])_p — measured
+        unstable (scripts/pml_theta_explore.py: the iterates grow from iteration ~5 while the
+        corrector rank collapses, as plain parareal does on the whole state; DESIGN.md 3.7);
         n = 1 takes fine_next[1] (both terms cancel exactly, as in parareal.cpp:315-318);
         w_n = R(fine_next[n]) + d (as the plain sweep), next[n] = fine_next[n] + I(d) with the
         auxiliary part masked to the layer; a non-finite w, old[n] or fine_next[n] gives a NaN
@@ -249,7 +253,10 @@ def theta_parareal(u0, v0, kf: PmlCoefficients, m_f: int, kc: PmlCoefficients, m
                 d = tuple(np.full_like(f, np.nan) for f in g)
             else:
                 cn, co = corrected(g), corrected(old[n])
-                d = (cn[0] - co[0], cn[1] - co[1], g[2] - old[n][2], g[3] - old[n][3])
+                if aux == "plain":
+                    d = (cn[0] - co[0], cn[1] - co[1], g[2] - old[n][2], g[3] - old[n][3])
+                else:  # "none": the auxiliary fields take fine_next's as they are
+                    d = (cn[0] - co[0], cn[1] - co[1], np.zeros_like(g[2]), np.zeros_like(g[3]))
             w = tuple(a + b for a, b in zip(R(fine_next[n]), d))
             if n == 1:
                 nxt.append(fine_next[1])

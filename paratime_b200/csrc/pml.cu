@@ -27,7 +27,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <cstdint>
 #include <limits>
 
 #include "ptb_comm.h"
@@ -393,9 +395,19 @@ struct ptb_pml {
   size_t scratch_batch = 0;
   int2* tiles = nullptr;       // plain tiles, then layer tiles (PT x PT, classified at create)
   int nplain = 0, nlayer = 0;
+  // the plain tiles as one rectangle (rows [ry0, ry0 + rny), columns [rx0, rx0 + rnx)) when they
+  // form one: the interior then runs the periodic wavefront kernel (k_wave2) instead of k_pml_plain
+  int ry0 = 0, rny = 0, rx0 = 0, rnx = 0;
+  ptb::StepParams prm{};
 };
 
 namespace ptb {
+
+// PTB_PML_WAVE=0: interior tiles through k_pml_plain (A/B measurements, tests)
+bool pml_wave_enabled() {
+  const char* e = std::getenv("PTB_PML_WAVE");
+  return !(e && std::atoi(e) == 0);
+}
 
 void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v, double* px, double* py,
                    int32_t* flags) {
@@ -454,7 +466,12 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     a.pyo = bufs[1 - cur][3];
     a.steps = ns;
     a.flags = done == steps ? flags : nullptr;
-    if (p->nplain) {
+    if (p->nplain && p->rnx && (ns == 4 || ns == 2 || ns == 1) && pml_wave_enabled()) {
+      // the undamped interior: the periodic FAST wavefront kernel on the plain-tile rectangle
+      // (bitwise k_pml_plain's arithmetic; its S-step cone stays in undamped cells, px = py = 0)
+      wave_rect_fast(ctx, st, ns, p->prm, batch, a.ui, a.vi, a.uo, a.vo, a.kx, a.flags, p->ry0, p->rny, p->rx0,
+                     p->rnx);
+    } else if (p->nplain) {
       a.tiles = p->tiles;
       k_pml_plain<<<dim3(p->nplain, unsigned(batch)), 256, pml_plain_smem(), st>>>(a);
       PTB_LAUNCH_CHECK(ctx);
@@ -558,24 +575,25 @@ __global__ void __launch_bounds__(512) k_err_sums(size_t n, const double* au, co
 }
 
 // theta coupling, one sweep step's tail on the layered coarse state (one launch): the (u, udot)
-// part d = Z dz + (m_w - m_old)/N_c (dl: Z dz as [du; dv], null when the corrector is empty), the
-// auxiliary part d = g - old[n] (plain correction); d := NaN when g, old[n] or fine_next[n] is
-// non-finite (parareal.cpp:323-326); then w = R(fine_next[n]) + d for all four fields (the next
-// step's R(next[n]), R(I(d)) = d at the coarse nodes).  g and w share storage (read before write).
+// part d = Z dz + (m_w - m_old)/N_c (dl: Z dz as [du; dv], null when the corrector is empty); the
+// auxiliary fields are not corrected (d = 0: next[n]'s px, py are fine_next[n]'s — correcting them
+// additively, as plain parareal does, is unstable: DESIGN.md 3.7); d := NaN when g, old[n] or
+// fine_next[n] is non-finite (parareal.cpp:323-326); then w = R(fine_next[n]) + d for all four
+// fields (the next step's R(next[n]), R(I(d)) = d at the coarse nodes).  g and w share storage.
 struct Fields4 {
   double* f[4];
 };
 __global__ void k_theta_tail(size_t nc, const double* __restrict__ dl, const double* __restrict__ mw,
                              const double* __restrict__ mold, const int32_t* gbad, const int32_t* obad,
-                             const int32_t* fbad, Fields4 g, Fields4 old, Fields4 rf, Fields4 d) {
+                             const int32_t* fbad, Fields4 g, Fields4 rf, Fields4 d) {
   const bool nan = *gbad || *obad || *fbad;
   const double dm = (*mw - *mold) / double(nc);
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nc; i += size_t(gridDim.x) * blockDim.x) {
     double di[4];
     di[0] = (dl ? dl[i] : 0.0) + dm;
     di[1] = dl ? dl[nc + i] : 0.0;
-    di[2] = g.f[2][i] - old.f[2][i];
-    di[3] = g.f[3][i] - old.f[3][i];
+    di[2] = 0.0;
+    di[3] = 0.0;
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       const double x = nan ? __longlong_as_double(0x7ff8000000000000LL) : di[f];
@@ -790,11 +808,10 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
         PTB_LAUNCH_CHECK(ctx);
         gemm(ctx, false, false, int(2 * nc), 1, r, 1.0, Z, int(2 * nc), dz, r, 0.0, dl, int(2 * nc));
       }
-      Fields4 O{{cold.f(0, n - 1), cold.f(1, n - 1), cold.f(2, n - 1), cold.f(3, n - 1)}};
       Fields4 RF{{crf.f(0, n - 1), crf.f(1, n - 1), crf.f(2, n - 1), crf.f(3, n - 1)}};
       Fields4 D{{cd.f(0, n - 1), cd.f(1, n - 1), cd.f(2, n - 1), cd.f(3, n - 1)}};
       k_theta_tail<<<ew_blocks(ctx, nc), 256, 0, st>>>(nc, r > 0 ? dl : nullptr, mw, mold + (n - 1), swf + n,
-                                                      gcf + (n - 1), gff + (n - 1), G, O, RF, D);
+                                                      gcf + (n - 1), gff + (n - 1), G, RF, D);
       PTB_LAUNCH_CHECK(ctx);
     }
   };
@@ -1046,6 +1063,32 @@ ptb_status ptb_pml_create(ptb_context* ctx, const ptb_grid* grid, const double* 
       }
     p->nplain = int(plain.size());
     p->nlayer = int(layer.size());
+    if (!plain.empty()) {  // do the plain tiles tile a rectangle?
+      int y0 = INT32_MAX, y1 = 0, x0 = INT32_MAX, x1 = 0;
+      for (const int2& t : plain) {
+        y0 = std::min(y0, t.x);
+        y1 = std::max(y1, std::min(t.x + PTY, int(ny)));
+        x0 = std::min(x0, t.y);
+        x1 = std::max(x1, std::min(t.y + PTX, int(nx)));
+      }
+      const size_t rows = size_t((y1 - y0 + PTY - 1) / PTY), cols = size_t((x1 - x0 + PTX - 1) / PTX);
+      if (rows * cols == plain.size() && nx % 2 == 0 && x0 % 2 == 0 && (x1 - x0) % 2 == 0) {
+        p->ry0 = y0;
+        p->rny = y1 - y0;
+        p->rx0 = x0;
+        p->rnx = x1 - x0;
+      }
+    }
+    p->prm.dim = 2;
+    p->prm.ny = int(ny);
+    p->prm.nx = int(nx);
+    p->prm.ihx2 = ihx2;
+    p->prm.ihy2 = ihy2;
+    p->prm.dt = dt;
+    p->prm.hd = p->hd;
+    p->prm.hdt2 = 0.5 * dt * dt;
+    p->prm.ry = p->ry;
+    p->prm.cc = p->cc;
     plain.insert(plain.end(), layer.begin(), layer.end());
     PTB_CUDA_CHECK(cudaMalloc(&p->tiles, plain.size() * sizeof(int2)));
     PTB_CUDA_CHECK(cudaMemcpy(p->tiles, plain.data(), plain.size() * sizeof(int2), cudaMemcpyHostToDevice));

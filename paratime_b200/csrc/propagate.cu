@@ -483,6 +483,9 @@ struct WaveArgs {
   int rb;                           // output rows per row block
   int32_t* flags;                   // nonfinite flags (nullable)
   int full = 0;                     // k_wave2: the strip is the whole periodic row (2W == nx)
+  // k_wave2 output rectangle (rows [ry0, ry0 + rny), columns [rx0, rx0 + rnx)); inputs are read
+  // with the periodic wrap of the whole ny x nx slice.  Default (rnx = 0): the whole slice.
+  int ry0 = 0, rny = 0, rx0 = 0, rnx = 0;
 };
 
 // One iteration of the wavefront: level 0 loads row r0 = ystart+i (+ look-ahead row), levels
@@ -797,15 +800,16 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
   const int offr = FULL && j == W - 1 ? -(W - 1) : 1;
   const int nx = a.p.nx, ny = a.p.ny;
   const int npts = nx * ny;
-  const int x0 = blockIdx.y * a.wu;  // even
+  const int rnx = a.rnx ? a.rnx : nx, rny = a.rnx ? a.rny : ny;  // output rectangle
+  const int x0 = a.rx0 + blockIdx.y * a.wu;  // even
   int gx = (x0 - HXE + 2 * j) % nx;
   if (gx < 0) gx += nx;
-  const int Y0 = blockIdx.z * a.rb;
-  const int nrows = min(a.rb, ny - Y0);
+  const int Y0 = a.ry0 + blockIdx.z * a.rb;
+  const int nrows = min(a.rb, a.ry0 + rny - Y0);
   const int ystart = Y0 - S;
   const int n_iter = ((nrows + 2 * S + UNROLL - 1) / UNROLL) * UNROLL;
   const int oc = 2 * j - HXE;  // output column offset of col 0 within the strip
-  const bool col_out = oc >= 0 && 2 * j + 1 < 2 * T - HXE && oc < a.wu && x0 + oc < nx;
+  const bool col_out = oc >= 0 && 2 * j + 1 < 2 * T - HXE && oc < a.wu && x0 + oc < a.rx0 + rnx;
   const size_t off = static_cast<size_t>(blockIdx.x) * a.stride;
   const double* __restrict__ U = a.u_in + off;
   const double* __restrict__ V = a.v_in + off;
@@ -1177,7 +1181,7 @@ inline int wave2_variant(const StepParams& p, int full) {
 }
 
 template <int S>
-WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
+WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch, bool no_full = false) {
   const int HXE = (S + 3) & ~1;
   WavePlan best{};
   double best_cost = 1e300;
@@ -1190,7 +1194,7 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
   for (int W : kWave2Widths)
    for (int full = 0; full < 2; ++full) {
     if (forceW && W != forceW) continue;
-    if (full && (nx != 2 * W || !full_env)) continue;
+    if (full && (nx != 2 * W || !full_env || no_full)) continue;
     const int wu_max = full ? nx : (2 * W - 2 * HXE) & ~1;
     if (wu_max < 16) continue;
     int occ = 0;
@@ -1236,7 +1240,10 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch) {
 
 template <int S>
 void launch_wave2(ptb_context* ctx, cudaStream_t st, WaveArgs a, size_t batch) {
-  const WavePlan pl = plan_wave2<S>(ctx, a.p.ny, a.p.nx, batch);
+  // a rectangle narrower than the row is covered by haloed strips (full-row needs rnx == nx)
+  const bool rect = a.rnx != 0;
+  const WavePlan pl = plan_wave2<S>(ctx, rect ? a.rny : a.p.ny, rect ? a.rnx : a.p.nx, batch,
+                                    rect && a.rnx != a.p.nx);
   const size_t smem = wave2_smem(S, pl.W);
   a.wu = pl.wu;
   a.rb = pl.rb;
@@ -1361,6 +1368,29 @@ void stream_propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u,
 }
 
 }  // namespace
+
+// FAST steps on the rectangle [y0, y0 + rny) x [x0, x0 + rnx) of every slice (out of place; points
+// outside the rectangle are neither computed nor written).  The caller guarantees that the S-step
+// dependency cone of the rectangle lies where the periodic FAST step is the right one (the
+// absorbing-layer propagator's undamped interior).  S in {1, 2, 4, 8}, even nx.
+void wave_rect_fast(ptb_context* ctx, cudaStream_t st, int S, const StepParams& p, size_t batch, const double* ui,
+                    const double* vi, double* uo, double* vo, const double* kx, int32_t* flags, int y0, int rny,
+                    int x0, int rnx) {
+  require(p.nx % 2 == 0 && x0 % 2 == 0 && rnx % 2 == 0 && rnx > 0 && rny > 0, "wave rect: bad rectangle");
+  WaveArgs a{p, ui, vi, uo, vo, kx, size_t(p.ny) * p.nx, 0, 0, flags};
+  a.ry0 = y0;
+  a.rny = rny;
+  a.rx0 = x0;
+  a.rnx = rnx;
+  switch (S) {
+    case 1: launch_wave2<1>(ctx, st, a, batch); return;
+    case 2: launch_wave2<2>(ctx, st, a, batch); return;
+    case 4: launch_wave2<4>(ctx, st, a, batch); return;
+    case 8: launch_wave2<8>(ctx, st, a, batch); return;
+    default: fail(PTB_UNSUPPORTED, "wave rect: depth");
+  }
+}
+
 
 void propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double* v, int32_t* flags, int mode,
                const LaunchSlot* slot_in) {

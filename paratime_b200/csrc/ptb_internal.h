@@ -230,6 +230,9 @@ std::string describe_plan(ptb_propagator* p, size_t steps, size_t batch, int mod
 void propagate(ptb_propagator* p, size_t steps, size_t batch, double* u, double* v, int32_t* flags,
                int mode, const LaunchSlot* slot = nullptr);
 void laplacian(ptb_context* ctx, const ptb_grid& g, size_t batch, const double* f, double* out);
+void wave_rect_fast(ptb_context* ctx, cudaStream_t st, int S, const StepParams& p, size_t batch, const double* ui,
+                    const double* vi, double* uo, double* vo, const double* kx, int32_t* flags, int y0, int rny,
+                    int x0, int rnx);
 void nonfinite(ptb_context* ctx, size_t n, size_t batch, const double* f, int32_t* flags);
 
 // transfer.cu

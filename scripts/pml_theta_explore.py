@@ -32,7 +32,11 @@ kf = M.PmlCoefficients(c, 1 / nf, 1 / nf, dtf, zf, zf)
 kc = M.PmlCoefficients(cc, 1 / nc, 1 / nc, dtc, zc, zc)
 t = P.Transfer(P.grid2(nc, nc, 1 / nc, 1 / nc), P.grid2(nf, nf, 1 / nf, 1 / nf), 0)
 print(f"fine {nf}^2 layer {wf}, coarse {nc}^2, N={N} K={K} m_f={mf} m_c={mc} tol={tol}", flush=True)
-_, ep = M.plain_parareal(u0, v0, kf, mf, kc, mc, t, N, K)
-print("plain max err per k:", " ".join(f"{e:.2e}" for e in ep.max(axis=1)), flush=True)
-_, et, ranks = M.theta_parareal(u0, v0, kf, mf, kc, mc, t, N, K, cc, tol=tol)
-print("theta max err per k:", " ".join(f"{e:.2e}" for e in et.max(axis=1)), "ranks", ranks, flush=True)
+variants = sys.argv[7].split(",") if len(sys.argv) > 7 else ["plain", "theta:plain", "theta:none"]
+for var in variants:
+    if var == "plain":
+        _, e = M.plain_parareal(u0, v0, kf, mf, kc, mc, t, N, K)
+        ranks = None
+    else:
+        _, e, ranks = M.theta_parareal(u0, v0, kf, mf, kc, mc, t, N, K, cc, tol=tol, aux=var.split(":")[1])
+    print(f"{var:12s} max err per k:", " ".join(f"{x:.2e}" for x in e.max(axis=1)), "ranks", ranks, flush=True)

@@ -322,3 +322,25 @@ def test_pml_theta_sharded_equals_single_gpu(world):
         a = 1 + r * chunk
         b = min(s["N"] + 1, a + chunk)
         assert np.array_equal(o["states"][:, a - 1:b], single["states"][:, a - 1:b])
+
+
+@pytest.mark.parametrize("n,w,steps", [(256, 32, 12), (512, 32, 10), (384, 16, 8)])
+def test_interior_wavefront_equals_plain_tiles_bitwise(ctx, n, w, steps, monkeypatch):
+    """The undamped interior runs the periodic wavefront kernel (k_wave2 on the plain-tile
+    rectangle) instead of k_pml_plain: the same FAST arithmetic, so the layered propagation is
+    bitwise unchanged (steps not a multiple of 4 take a 2- or 1-step pass)."""
+    import paratime_b200 as B
+
+    c, zy, zx, state = _case(n, n, 1 / n, 1 / n, w, 2, seed=n + w)
+    prop = B.PmlPropagator(ctx, B.Grid((n, n), (1 / n, 1 / n)), c, zy, zx, 0.5 / n / np.sqrt(2), steps)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PTB_PML_WAVE", mode)
+        t = [ctx.tensor(a) for a in state]
+        prop.propagate(*t)
+        out[mode] = [x.cpu().numpy() for x in t]
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
+    want = M.pml_steps(*(s_[0] for s_ in state), M.PmlCoefficients(c, 1 / n, 1 / n, 0.5 / n / np.sqrt(2), zy, zx), steps)
+    for got, ref in zip(out["1"], want):
+        assert _rel(got[0], ref) <= TOL
