@@ -120,8 +120,8 @@ def cfg4_pml(reflection=1e-4, profile=None):
     256^2: the same physical width, 4 cells), quadratic damping profile with amplitude
     1.5 cmax ln(1/R)/L, R = 1e-4, cmax = max fine c for both grids.  Returns
     (spec, c_fine, c_coarse, u0, udot0, (zeta_fine, zeta_coarse)); the profiles are per axis (the
-    same for rows and columns).  The reference has no layer: this runs plain
-    parareal through ptb_pml_parareal_run; theta-parareal stays periodic."""
+    same for rows and columns).  The reference has no layer: this runs
+    theta-parareal with the layer through ptb_pml_theta_run."""
     if profile is None:  # the C ABI's host profile (bitwise equal to oracle/pml_np.damping_profile)
         from paratime_b200 import damping_profile as profile
     spec, c, cc, u0, v0 = cfg4()
