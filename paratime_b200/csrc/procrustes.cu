@@ -2146,13 +2146,78 @@ int truncated_qr_tsqr(ProcWork& w, const double* A_in, int m, int n, double drop
   return kq;
 }
 
+// R (k1 + k2) x (n1 + n2), column-major: [R1 C; 0 R2] with C = C1 + C2 (the two Gram-Schmidt passes)
+__global__ void k_assemble_r2(int k1, int k2, int n1, int n2, const double* R1, const double* C1, const double* C2,
+                              const double* R2, double* R) {
+  const int rows = k1 + k2, cols = n1 + n2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int j = e / rows, i = e - j * rows;
+    double x = 0.0;
+    if (j < n1) {
+      if (i < k1) x = R1[size_t(j) * k1 + i];
+    } else if (i < k1) {
+      x = C1[size_t(j - n1) * k1 + i] + C2[size_t(j - n1) * k1 + i];
+    } else {
+      x = R2[size_t(j - n1) * k2 + (i - k1)];
+    }
+    R[e] = x;
+  }
+}
+
+// Tall blocks of TS_MAXN < n <= 2 TS_MAXN columns (config 4's update_svd: 196608 x 128): the first
+// 64 columns through the TSQR route, the rest projected off its Q by block Gram-Schmidt applied
+// twice (BCGS2: orthogonal to working precision), their TSQR, then the column-pivoted QR of the
+// assembled R = [R1 C; 0 R2].  A = [Q1 Q2] R with [Q1 Q2] orthonormal, so the pivoting and keep
+// decisions are those of A's own column-pivoted QR (procrustes.cpp:34-46) up to rounding, as for
+// the TSQR route; Q = [Q1 Q2] Q_R.  Replaces the blocked route (one grid barrier per column).
+int truncated_qr_2panel(ProcWork& w, const double* A_in, int m, int n, double drop_tol, DeviceBuffer& Qb,
+                        DeviceBuffer& Rb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  const int n1 = TS_MAXN, n2 = n - n1;
+  const int k1 = truncated_qr_tsqr(w, A_in, m, n1, 0.0, w.TP[0], w.TP[1]);
+  const double* Q1 = static_cast<const double*>(w.TP[0].ptr);
+  double* A2 = static_cast<double*>(w.TP[2].get(size_t(m) * n2 * sizeof(double)));
+  PTB_CUDA_CHECK(cudaMemcpyAsync(A2, A_in + size_t(n1) * m, size_t(m) * n2 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 st));
+  double* C = static_cast<double*>(w.TP[3].get(std::max<size_t>(1, 2 * size_t(k1) * n2) * sizeof(double)));
+  if (k1 > 0) {
+    for (int pass = 0; pass < 2; ++pass) {
+      double* Cp = C + size_t(pass) * k1 * n2;
+      gemm(ctx, true, false, k1, n2, m, 1.0, Q1, m, A2, m, 0.0, Cp, k1);
+      gemm(ctx, false, false, m, n2, k1, -1.0, Q1, m, Cp, k1, 1.0, A2, m);
+    }
+  }
+  const int k2 = truncated_qr_tsqr(w, A2, m, n2, 0.0, w.TP[4], w.TP[5]);
+  const int kk = k1 + k2;
+  double* R = static_cast<double*>(w.TP[6].get(std::max<size_t>(1, size_t(kk) * n) * sizeof(double)));
+  if (kk == 0) {
+    Qb.get(8);
+    Rb.get(8);
+    return 0;
+  }
+  k_assemble_r2<<<unsigned(std::max(1, std::min(1024, (kk * n + 255) / 256))), 256, 0, st>>>(
+      k1, k2, n1, n2, static_cast<const double*>(w.TP[1].ptr), C, C + size_t(k1) * n2,
+      static_cast<const double*>(w.TP[5].ptr), R);
+  PTB_LAUNCH_CHECK(ctx);
+  const int kq = truncated_qr_direct(w, R, kk, n, drop_tol, w.BQ2, Rb);
+  double* Q = static_cast<double*>(Qb.get(std::max<size_t>(1, size_t(m) * kq) * sizeof(double)));
+  if (kq == 0) return 0;
+  const double* QR = static_cast<const double*>(w.BQ2.ptr);  // kk x kq
+  if (k1 > 0) gemm(ctx, false, false, m, kq, k1, 1.0, Q1, m, QR, kk, 0.0, Q, m);
+  if (k2 > 0)
+    gemm(ctx, false, false, m, kq, k2, 1.0, static_cast<const double*>(w.TP[4].ptr), m, QR + k1, kk,
+         k1 > 0 ? 1.0 : 0.0, Q, m);
+  return kq;
+}
+
 // PTB_QR=direct | blocked | tsqr forces a route (tests, diagnostics); 0 = automatic
 int qr_route_env() {
   static const int env = [] {
     const char* e = std::getenv("PTB_QR");
     if (!e) return 0;
     const std::string v(e);
-    return v == "direct" ? 1 : v == "blocked" ? 2 : v == "tsqr" ? 3 : 0;
+    return v == "direct" ? 1 : v == "blocked" ? 2 : v == "tsqr" ? 3 : v == "panel2" ? 4 : 0;
   }();
   return env;
 }
@@ -2271,6 +2336,8 @@ int truncated_qr(ProcWork& w, const double* A_in, int m, int n, double drop_tol,
   if (env == 3 && tall && n <= TS_MAXN) return truncated_qr_tsqr(w, A_in, m, n, drop_tol, Qb, Rb);
   if (env == 2 && tall && n > 1) return truncated_qr_blocked(w, A_in, m, n, drop_tol, Qb, Rb);
   if (env == 0 && tall && n <= TS_MAXN && m > 1024) return truncated_qr_tsqr(w, A_in, m, n, drop_tol, Qb, Rb);
+  if ((env == 0 || env == 4) && tall && n > TS_MAXN && n <= 2 * TS_MAXN && m > 1024)
+    return truncated_qr_2panel(w, A_in, m, n, drop_tol, Qb, Rb);
   if (env == 0 && tall && n > QB) return truncated_qr_blocked(w, A_in, m, n, drop_tol, Qb, Rb);
   return truncated_qr_direct(w, A_in, m, n, drop_tol, Qb, Rb);
 }

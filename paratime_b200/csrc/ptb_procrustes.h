@@ -34,6 +34,7 @@ struct ProcWork {
   DeviceBuffer TS[24], TX[2];       // TSQR: per level reflectors, tau, R stack; Q down-sweep ping-pong
   DeviceBuffer TS2[24], TX2[2], BQ2b;  // the second matrix of a batched (F, G) TSQR
   DeviceBuffer PA[4], PB[4];        // batched TSQR: the two final pivoted factors, tau, perm, |R_jj|
+  DeviceBuffer TP[8];               // two-panel TSQR: Q1, R1, A2, C, Q2, R2, the assembled R
   explicit ProcWork(ptb_context* c);
   ~ProcWork();
 };

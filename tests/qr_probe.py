@@ -13,7 +13,8 @@ def mats():
     rng = np.random.default_rng(77)
     out = []
     for m, n, rank in [(4096, 40, 40), (6000, 64, 50), (20000, 100, 100), (3000, 33, 20), (8192, 96, 96),
-                       (12288, 32, 29), (49152, 64, 60), (1537, 17, 17)]:
+                       (12288, 32, 29), (49152, 64, 60), (1537, 17, 17),
+                       (30000, 128, 90), (16384, 72, 72), (20000, 100, 50)]:  # two-panel route, rank-deficient panels
         a = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n))
         a *= np.logspace(0, -6, n)[None, :]  # graded columns: pivoting matters
         out.append(a)

@@ -1,6 +1,8 @@
 """truncated_qr (procrustes.cpp:34-46) on tall snapshot-like blocks: the TSQR route (leaf QRs in
-shared memory, then the pivoted QR of the last stack; n <= 64), the blocked route (unpivoted
-panel QR + WY updates, then the pivoted QR of R1; n > 64), the direct column-pivoted kernel and
+shared memory, then the pivoted QR of the last stack; n <= 64), the two-panel route (two TSQR
+panels with block Gram-Schmidt between them, then the pivoted QR of the assembled R; 64 < n <=
+128, the default there), the blocked route (unpivoted panel QR + WY updates, then the pivoted QR
+of R1), the direct column-pivoted kernel and
 the default choice must all reproduce the oracle's keep count, an orthonormal
 Q and the same product Q R as the oracle's column-pivoted QR."""
 import os
@@ -17,7 +19,7 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("path", ["auto", "blocked", "direct", "tsqr"])
+@pytest.mark.parametrize("path", ["auto", "blocked", "direct", "tsqr", "panel2"])
 def test_truncated_qr_tall_matches_oracle(tmp_path, path):
     env = dict(os.environ, PYTHONPATH=str(ROOT))
     env.pop("PTB_QR", None)
