@@ -17,6 +17,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cstdlib>
+
 #include "ptb_energy.h"
 #include "ptb_fft.h"
 
@@ -445,6 +447,107 @@ __global__ void __launch_bounds__(256) k_pair_sums2d(Geo G, Beta B, const double
   }
 }
 
+// Streaming variant for wide 2D grids (nx % 256 == 0): block = a 256-column strip x a band of rows
+// of one pair; each thread owns one column and marches down the band with the (2M+1)-row windows
+// of u_a and u_b in registers, so every u value is loaded once (the y-neighbours come from the
+// window, the x-neighbours from a shared row of the band's current row, halo columns of the
+// neighbouring strips loaded by the edge threads).  Per-point arithmetic is k_pair_sums2d's (same
+// rounding: the x-term differences u_a - u_b are formed before they are shared); only the grouping
+// of the partial sums differs (fixed: thread, then block, then k_pair_final in block order).
+constexpr int PS_T = 256;
+template <int M>
+__global__ void __launch_bounds__(PS_T) k_pair_sums_stream(Geo G, Beta B, int bands, const double* ua,
+                                                          const double* va, size_t sa, const double* ub,
+                                                          const double* vb, size_t sb, const double* c, double* part,
+                                                          int32_t* nonfinite) {
+  __shared__ double sdif[2][PS_T + 2 * M], sref[2][PS_T + 2 * M];
+  const int nx = G.nx, ny = G.ny, strips = nx / PS_T;
+  const int strip = int(blockIdx.x) % strips, band = int(blockIdx.x) / strips;
+  const size_t pr = blockIdx.y;
+  const double* UA = ua + pr * sa;
+  const double* VA = va + pr * sa;
+  const double* UB = ub + pr * sb;
+  const double* VB = vb + pr * sb;
+  const int t = threadIdx.x, x = strip * PS_T + t;
+  const int rows = (ny + bands - 1) / bands, r0 = band * rows, r1 = min(ny, r0 + rows);
+  // halo columns: thread t < 2M loads column x_h of the left (t < M) or right halo
+  const int hx = t < M ? (strip * PS_T - M + t + nx) % nx : ((strip + 1) * PS_T + (t - M)) % nx;
+  const int hslot = t < M ? t : PS_T + t;
+  double wa[2 * M + 1], wb[2 * M + 1];
+#pragma unroll
+  for (int k = 0; k < 2 * M; ++k) {  // rows r0 - M .. r0 + M - 1
+    const size_t o = size_t((r0 - M + k + ny) % ny) * nx + x;
+    wa[k] = UA[o];
+    wb[k] = UB[o];
+  }
+  double sd = 0.0, sr = 0.0, ld = 0.0, lr = 0.0;
+  bool ok = true;
+  int buf = 0;
+  for (int r = r0; r < r1; ++r) {
+    {
+      const size_t o = size_t((r + M) % ny) * nx + x;
+      wa[2 * M] = UA[o];
+      wb[2 * M] = UB[o];
+    }
+    const size_t p = size_t(r) * nx + x;
+    sdif[buf][M + t] = __dsub_rn(wa[M], wb[M]);
+    sref[buf][M + t] = wb[M];
+    if (t < 2 * M) {
+      const size_t ho = size_t(r) * nx + hx;
+      sdif[buf][hslot] = __dsub_rn(UA[ho], UB[ho]);
+      sref[buf][hslot] = UB[ho];
+    }
+    const double cp = c[p], vbp = VB[p], vap = VA[p];
+    // axis 0 (y) from the windows
+    double ady = 0.0, ary = 0.0;
+#pragma unroll
+    for (int j = 1; j <= M; ++j) {
+      ady = __dadd_rn(ady, __dmul_rn(B.b[j - 1], __dsub_rn(__dsub_rn(wa[M + j], wb[M + j]),
+                                                            __dsub_rn(wa[M - j], wb[M - j]))));
+      ary = __dadd_rn(ary, __dmul_rn(B.b[j - 1], __dsub_rn(wb[M + j], wb[M - j])));
+    }
+    const double gdy = __dmul_rn(ady, G.ih[0]), gry = __dmul_rn(ary, G.ih[0]);
+    sd += gdy * gdy;
+    sr += gry * gry;
+    __syncthreads();  // the shared row (and its halo) of this r complete
+    double adx = 0.0, arx = 0.0;
+#pragma unroll
+    for (int j = 1; j <= M; ++j) {
+      adx = __dadd_rn(adx, __dmul_rn(B.b[j - 1], __dsub_rn(sdif[buf][M + t + j], sdif[buf][M + t - j])));
+      arx = __dadd_rn(arx, __dmul_rn(B.b[j - 1], __dsub_rn(sref[buf][M + t + j], sref[buf][M + t - j])));
+    }
+    const double gdx = __dmul_rn(adx, G.ih[1]), grx = __dmul_rn(arx, G.ih[1]);
+    sd += gdx * gdx;
+    sr += grx * grx;
+    ok &= isfinite(wa[M]) && isfinite(vap);
+    const double md = __ddiv_rn(__dsub_rn(vap, vbp), cp);
+    const double mr = __ddiv_rn(vbp, cp);
+    sd += md * md;
+    sr += mr * mr;
+    const double du = __dsub_rn(wa[M], wb[M]);
+    ld += du * du;
+    lr += wb[M] * wb[M];
+#pragma unroll
+    for (int k = 0; k < 2 * M; ++k) {
+      wa[k] = wa[k + 1];
+      wb[k] = wb[k + 1];
+    }
+    buf ^= 1;  // the other shared row next: its previous readers passed this row's barrier
+  }
+  if (nonfinite && __syncthreads_or(!ok) && threadIdx.x == 0) atomicOr(&nonfinite[pr], 1);
+  sd = block_sum<256>(sd);
+  sr = block_sum<256>(sr);
+  ld = block_sum<256>(ld);
+  lr = block_sum<256>(lr);
+  if (threadIdx.x == 0) {
+    double* o = part + (pr * gridDim.x + blockIdx.x) * 4;
+    o[0] = sd;
+    o[1] = sr;
+    o[2] = ld;
+    o[3] = lr;
+  }
+}
+
 __global__ void k_pair_final(size_t pairs, int nb, const double* part, double* out) {
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < pairs * 4; e += size_t(gridDim.x) * blockDim.x) {
     const size_t pr = e / 4, q = e % 4;
@@ -629,6 +732,12 @@ __global__ void k_nonfinite_states(int n, const double* u, const double* v, size
   if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicOr(&flags[b], 1);
 }
 
+// PTB_PAIR_STREAM=0: the row-per-block kernel (A/B measurements, tests)
+bool pair_stream_enabled() {
+  const char* e = std::getenv("PTB_PAIR_STREAM");
+  return !(e && std::atoi(e) == 0);
+}
+
 void pair_energy_sums(EnergyWork& w, const ptb_grid& g, int scheme, size_t batch, const double* ua, const double* va,
                       size_t sa, const double* ub, const double* vb, size_t sb, const double* c, double* out4,
                       int32_t* nonfinite_a) {
@@ -637,6 +746,23 @@ void pair_energy_sums(EnergyWork& w, const ptb_grid& g, int scheme, size_t batch
   if (batch == 0) return;
   const Geo G = geo_of(g);
   const int n = G.ny * G.nx;
+  if (scheme != PTB_SPECTRAL && G.dim == 2 && G.nx % PS_T == 0 && G.ny >= 64 && pair_stream_enabled()) {
+    const int strips = G.nx / PS_T, bands = std::max(1, std::min(G.ny / 32, 64 / strips));
+    const int nb = strips * bands;
+    double* part = static_cast<double*>(w.buf[7].get(batch * nb * 4 * sizeof(double)));
+    const dim3 grid{unsigned(nb), unsigned(batch)};
+    const Beta bt = beta_of(scheme);
+    switch (bt.m) {
+      case 1: k_pair_sums_stream<1><<<grid, PS_T, 0, st>>>(G, bt, bands, ua, va, sa, ub, vb, sb, c, part, nonfinite_a); break;
+      case 2: k_pair_sums_stream<2><<<grid, PS_T, 0, st>>>(G, bt, bands, ua, va, sa, ub, vb, sb, c, part, nonfinite_a); break;
+      case 3: k_pair_sums_stream<3><<<grid, PS_T, 0, st>>>(G, bt, bands, ua, va, sa, ub, vb, sb, c, part, nonfinite_a); break;
+      default: k_pair_sums_stream<4><<<grid, PS_T, 0, st>>>(G, bt, bands, ua, va, sa, ub, vb, sb, c, part, nonfinite_a); break;
+    }
+    PTB_LAUNCH_CHECK(ctx);
+    k_pair_final<<<nblk(ctx, batch * 4), 256, 0, st>>>(batch, nb, part, out4);
+    PTB_LAUNCH_CHECK(ctx);
+    return;
+  }
   if (scheme != PTB_SPECTRAL) {
     const int nb = std::max(1, std::min(PAIR_BLOCKS, (n + 255) / 256));
     double* part = static_cast<double*>(w.buf[7].get(batch * nb * 4 * sizeof(double)));

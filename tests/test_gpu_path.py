@@ -251,3 +251,23 @@ def test_one_dimensional_preset_matches_reference(ref):
             worst = max(worst, P.energy_error((a[0], a[1]), (b[0], b[1]), cf, fg, 0))
     assert list(gpu["rank"]) == list(r["rank"])
     assert worst <= ITERATE_TOL, worst
+
+
+@pytest.mark.parametrize("shape", [(256, 256), (128, 512), (512, 256)])
+@pytest.mark.parametrize("scheme", [0, 1, 2, 3])
+def test_streaming_pair_sums_match_row_kernel(impl, shape, scheme, monkeypatch):
+    """k_pair_sums_stream (column windows in registers, the default on nx % 256 == 0) against the
+    row-per-block k_pair_sums2d and the oracle: the same per-point arithmetic, only the grouping
+    of the partial sums differs."""
+    g = P.Grid(shape, (1.0 / shape[0], 1.0 / shape[1]))
+    rng = np.random.default_rng(11)
+    a = (rng.uniform(-1, 1, g.shape), rng.uniform(-1, 1, g.shape))
+    b = (rng.uniform(-1, 1, g.shape), rng.uniform(-1, 1, g.shape))
+    c = 0.5 + rng.random(g.shape)
+    got = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PTB_PAIR_STREAM", mode)
+        got[mode] = impl.energy_error(a, b, c, g, scheme)
+    want = P.energy_error(a, b, c, g, scheme)
+    assert got["1"] == pytest.approx(want, rel=1e-13)
+    assert got["1"] == pytest.approx(got["0"], rel=1e-13)
