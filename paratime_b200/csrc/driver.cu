@@ -242,6 +242,8 @@ constexpr int SWEEP_BLOCKS = 8;
 __global__ void __launch_bounds__(256) k_zt_blocks(size_t rows, size_t bl, const double* __restrict__ Y, size_t ld,
                                                    const double* __restrict__ x, int r, int rank, int world,
                                                    double* __restrict__ part) {
+  pdl_wait();  // x (Lambda(w)) comes from the launch just before
+  pdl_trigger();
   const int j = blockIdx.x, b = blockIdx.y;
   if (b % world != rank) return;
   const size_t r0 = size_t(b) * bl, r1 = min(rows, r0 + bl);
@@ -297,6 +299,55 @@ __global__ void k_zd_rows(int i0, int i1, int sg, int r, const double* __restric
   seg[i - i0] = su;
   seg[sg + i - i0] = sv;
 }
+// One GPU, large corrector: the whole sweep-step tail in one launch — z_w = sum of the
+// SWEEP_BLOCKS partials in block order (k_zt_sum), dz = z_w - z_old (k_sub), d = Z dz row by row
+// (k_zd_rows' sequential order), the zero mode (m_w - m_old)/N_c (k_add_mean), the NaN rule and
+// R(next[n]) = R(fine_next[n]) + d (k_sweep_tail): the same operations in the same order as the
+// multi-rank path, so results stay bitwise independent of the world size.
+__global__ void k_zd_fused(int n, int r, const double* __restrict__ Zu, const double* __restrict__ Zv, size_t ld,
+                           const double* __restrict__ part, const double* __restrict__ zold, const double* mw,
+                           const double* mold, double* du, double* dv, const SweepTail tl) {
+  pdl_wait();  // the partials come from k_zt_blocks launched just before
+  pdl_trigger();
+  extern __shared__ double dzs[];
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    double z = 0.0;
+    for (int b = 0; b < SWEEP_BLOCKS; ++b) z += part[size_t(b) * r + j];
+    dzs[j] = zold ? __dsub_rn(z, zold[j]) : z;
+  }
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double su = 0.0, sv = 0.0;
+  int k = 0;
+  for (; k + 8 <= r; k += 8) {
+    double tu[8], tv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      tu[q] = Zu[i + size_t(k + q) * ld];
+      tv[q] = Zv[i + size_t(k + q) * ld];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      su = fma(tu[q], dzs[k + q], su);
+      sv = fma(tv[q], dzs[k + q], sv);
+    }
+  }
+  for (; k < r; ++k) {
+    su = fma(Zu[i + size_t(k) * ld], dzs[k], su);
+    sv = fma(Zv[i + size_t(k) * ld], dzs[k], sv);
+  }
+  const double dm = mold ? __dsub_rn(*mw, *mold) : *mw;
+  su += dm / double(n);
+  if (tl.f0 && (*tl.f0 || *tl.f1 || *tl.f2)) su = sv = CUDART_NAN;
+  du[i] = su;
+  dv[i] = sv;
+  if (tl.ru) {
+    tl.ru[i] = tl.rfu[i] + su;
+    tl.rv[i] = tl.rfv[i] + sv;
+  }
+}
+
 // gathered segments (world x [du sg | dv sg]) -> du, dv (n rows)
 __global__ void k_zd_unpack(size_t n, int sg, const double* __restrict__ all, double* du, double* dv) {
   GRID_STRIDE(i, n) {
@@ -900,6 +951,26 @@ struct Driver {
         const SweepTail tail{wfl + n, fl(cf) + (n - 1), fl(ff) + (n - 1), more ? slot(rf_u, n, nc) : nullptr,
                              more ? slot(rf_v, n, nc) : nullptr, more ? ru : nullptr, more ? rv : nullptr};
         assemble_d(c, zwp, zo + (n - 1) * size_t(c.rank), mw, mo + (n - 1), du, dv, sweep_mean_parts(int(nc)), tail);
+        continue;
+      } else if (comm->world == 1 && s.scheme != PTB_SPECTRAL) {
+        // one GPU, large corrector: Lambda(w) and sum(u); the row-block partials of z_w; one launch
+        // for the rest of the step (k_zd_fused: bitwise the multi-rank path's operations)
+        double* cp = dalloc<double>(comp, rows);
+        energy_components(ew, cg, s.scheme, 1, ru, rv, nc, nullptr, cf_dev, cp, rows, mw);
+        const int r = c.rank;
+        double* part = dalloc<double>(zpart, size_t(SWEEP_BLOCKS) * std::max(r, 1));
+        if (r > 0)
+          launch_pdl(k_zt_blocks, dim3(unsigned(r), SWEEP_BLOCKS), dim3(256), 0, st(), rows,
+                     (rows + SWEEP_BLOCKS - 1) / SWEEP_BLOCKS, c.Yp(), rows, static_cast<const double*>(cp), r, 0, 1,
+                     part);
+        const bool more = n < N;
+        const SweepTail tail{wfl + n, fl(cf) + (n - 1), fl(ff) + (n - 1), more ? slot(rf_u, n, nc) : nullptr,
+                             more ? slot(rf_v, n, nc) : nullptr, more ? ru : nullptr, more ? rv : nullptr};
+        launch_pdl(k_zd_fused, dim3(unsigned((nc + 255) / 256)), dim3(256), size_t(std::max(r, 1)) * sizeof(double),
+                   st(), int(nc), r, static_cast<const double*>(Zu.ptr), static_cast<const double*>(Zv.ptr), nc,
+                   static_cast<const double*>(part), static_cast<const double*>(zo + (n - 1) * size_t(r)),
+                   static_cast<const double*>(mw), static_cast<const double*>(mo + (n - 1)), du, dv, tail);
+        PTB_LAUNCH_CHECK(ctx);
         continue;
       } else {
         corrected_batch(c, false, 1, ru, rv, nullptr, nullptr, zwp, mw);
