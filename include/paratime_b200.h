@@ -171,6 +171,10 @@ ptb_status ptb_transfer_destroy(ptb_transfer* t);
 ptb_status ptb_restrict_batch(ptb_transfer* t, size_t batch, const double* fine_dev, double* coarse_dev);
 /* interpolate_field (trigonometric with split Nyquist, or periodic linear) */
 ptb_status ptb_interpolate_batch(ptb_transfer* t, size_t batch, const double* coarse_dev, double* fine_dev);
+/* out = base + I(coarse) for `batch` fields (the parareal combine next = fine_next + I(d));
+ * base and out may alias */
+ptb_status ptb_interpolate_add_batch(ptb_transfer* t, size_t batch, const double* coarse_dev, const double* base_dev,
+                                     double* out_dev);
 /* finite check of `batch` fields of n values each; flags_dev[b] |= 1 when any is non-finite */
 ptb_status ptb_nonfinite_batch(ptb_context* ctx, size_t n, size_t batch, const double* f_dev,
                                int32_t* flags_dev);

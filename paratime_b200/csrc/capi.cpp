@@ -428,6 +428,22 @@ ptb_status ptb_interpolate_batch(ptb_transfer* t, size_t batch, const double* co
   });
 }
 
+ptb_status ptb_interpolate_add_batch(ptb_transfer* t, size_t batch, const double* coarse, const double* base,
+                                     double* out) {
+  return guarded([&] {
+    require(t && (batch == 0 || (coarse && base && out)), "interpolate_add: null argument");
+    DeviceGuard g(t->ctx->device);
+    std::lock_guard<std::recursive_mutex> lock(t->ctx->mutex);
+    DeviceBuffer& work = t->add_work;
+    const size_t nf = grid_size(t->fine);
+    double* w = static_cast<double*>(work.get(std::max<size_t>(1, std::min<size_t>(batch, 8)) * nf * sizeof(double)));
+    for (size_t b0 = 0; b0 < batch; b0 += 8) {
+      const size_t m = std::min<size_t>(8, batch - b0);
+      interpolate_fields_add(t, m, coarse + b0 * grid_size(t->coarse), base + b0 * nf, out + b0 * nf, w);
+    }
+  });
+}
+
 ptb_status ptb_nonfinite_batch(ptb_context* ctx, size_t n, size_t batch, const double* f, int32_t* flags) {
   return guarded([&] {
     DeviceGuard g(ctx->device);

@@ -197,6 +197,7 @@ struct ptb_transfer {
   // warp-FFT route (2D Fourier, large grids): the x-pass plane (batch x coarse rows x fine cols)
   ptb::DeviceBuffer spec_c;
   ptb::DeviceBuffer nodes_half;  // scratch of interpolate_at_coarse_nodes
+  ptb::DeviceBuffer add_work;    // scratch of ptb_interpolate_add_batch (direct routes)
 };
 
 namespace ptb {

@@ -24,6 +24,7 @@
 // so a slice's result never depends on how many slices a call or a rank carries.
 
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 #include <vector>
 
@@ -442,22 +443,44 @@ __global__ void __launch_bounds__(32 * FX_WARPS) k_fourier_fft_x(size_t lines, i
 
 constexpr int FY_COLS = 8;  // columns (= warps) per CTA: 64-byte row segments, <= 255 registers
 
+__device__ __forceinline__ void cp_async16_y(double* smem_dst, const double* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_y() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_y() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // y pass: plane (n x w) per field -> (n r x w), columns [16 blockIdx.x, +16) of field blockIdx.y;
 // out = base + I (base nullable, may alias out)
 template <int E>
 __global__ void __launch_bounds__(32 * FY_COLS) k_fourier_fft_y(int w, int r, const double* __restrict__ in,
                                                                   const double* base, double* out) {
   constexpr int n = 32 * E, IP = n + 1, OP = FY_COLS + 1;
-  extern __shared__ double smem_y[];
+  extern __shared__ __align__(16) double smem_y[];
   double* tin = smem_y;                  // [FY_COLS][n + 1]
   double* tout = smem_y + FY_COLS * IP;  // [2][n][FY_COLS + 1]: one phase pair
+  double* bsm = tout + 2 * n * OP + 1;   // [2 buffers][2 phases][n][FY_COLS]: base rows (16-byte aligned)
+  bsm += (reinterpret_cast<uintptr_t>(bsm) & 15) ? 1 : 0;
   const int tid = threadIdx.x, lane = tid & 31, col = tid >> 5;
   const int x0 = blockIdx.x * FY_COLS;
   const double* src = in + size_t(blockIdx.y) * n * w + x0;
   const size_t off = size_t(blockIdx.y) * n * r * w + x0;
-  for (int i = tid; i < n * FY_COLS; i += 32 * FY_COLS) {
-    const int row = i / FY_COLS, c = i % FY_COLS;
-    tin[c * IP + row] = src[size_t(row) * w + c];
+  {  // the plane's coarse columns: all loads of a thread in flight together, then the stores
+    constexpr int PER = n / 32;  // = n * FY_COLS / (32 * FY_COLS)
+    double t[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int i = tid + e * 32 * FY_COLS;
+      t[e] = src[size_t(i / FY_COLS) * w + i % FY_COLS];
+    }
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int i = tid + e * 32 * FY_COLS;
+      tin[(i % FY_COLS) * IP + i / FY_COLS] = t[e];
+    }
   }
   __syncthreads();
   // phase 0: the coarse rows themselves (loads first, as below)
@@ -475,6 +498,17 @@ __global__ void __launch_bounds__(32 * FY_COLS) k_fourier_fft_y(int w, int r, co
       out[off + size_t(q) * r * w + c] = bv[e] + tin[c * IP + q];
     }
   }
+  // base rows q r + s1 + {0, 1} (8 columns each) of a phase pair -> bsm[b], 16-byte cp.async
+  auto prefetch = [&](int b, int s1) {
+    double* d = bsm + b * (2 * n * FY_COLS);
+    for (int k = tid; k < n * FY_COLS; k += 32 * FY_COLS) {  // 2n rows x 4 chunks
+      const int qq = k / (FY_COLS / 2), ch = k % (FY_COLS / 2), slot = qq / n, q = qq % n;
+      if (s1 + slot < r) cp_async16_y(d + qq * FY_COLS + 2 * ch, base + off + (size_t(q) * r + s1 + slot) * w + 2 * ch);
+    }
+  };
+  int buf = 0;
+  if (base && r > 1) prefetch(0, 1);
+  cp_async_commit_y();
   LaneTw<E> tw;
   tw.init(lane);
   double2 step[E];
@@ -510,22 +544,21 @@ __global__ void __launch_bounds__(32 * FY_COLS) k_fourier_fft_y(int w, int r, co
       tout[(lane + 32 * e) * OP + col] = z[e].x;
       tout[(n + lane + 32 * e) * OP + col] = z[e].y;
     }
-    __syncthreads();
-    // all base loads of this thread first, then the stores (base may alias out: without the
-    // split each store would wait for the next load)
+    // the next phase pair's base rows start moving while this pair's are added and stored
+    if (base && s1 + 2 < r) prefetch(buf ^ 1, s1 + 2);
+    cp_async_commit_y();
+    cp_async_wait_y<1>();
+    __syncthreads();  // tout and this pair's base rows complete
     constexpr int PER = 2 * n * FY_COLS / (32 * FY_COLS);  // = 2n/32 elements per thread
-    double bv[PER];
+    const double* bs = bsm + buf * (2 * n * FY_COLS);
 #pragma unroll
     for (int e = 0; e < PER; ++e) {
       const int i = tid + e * 32 * FY_COLS, c = i % FY_COLS, qq = i / FY_COLS, slot = qq / n, q = qq % n;
-      bv[e] = (base && slot < cnt) ? base[off + (size_t(q) * r + s1 + slot) * w + c] : 0.0;
-    }
-#pragma unroll
-    for (int e = 0; e < PER; ++e) {
-      const int i = tid + e * 32 * FY_COLS, c = i % FY_COLS, qq = i / FY_COLS, slot = qq / n, q = qq % n;
-      if (slot < cnt) out[off + (size_t(q) * r + s1 + slot) * w + c] = bv[e] + tout[(slot * n + q) * OP + c];
+      if (slot < cnt)
+        out[off + (size_t(q) * r + s1 + slot) * w + c] = (base ? bs[qq * FY_COLS + c] : 0.0) + tout[(slot * n + q) * OP + c];
     }
     __syncthreads();
+    buf ^= 1;
   }
 }
 
@@ -554,7 +587,8 @@ void launch_fft_x(ptb_context* ctx, size_t lines, int r, const double* in, doubl
 template <int E>
 void launch_fft_y(ptb_context* ctx, size_t planes, int w, int r, const double* in, const double* base, double* out) {
   constexpr int n = 32 * E;
-  const size_t smem = (size_t(FY_COLS) * (n + 1) + size_t(2) * n * (FY_COLS + 1)) * sizeof(double);
+  const size_t smem =
+      (size_t(FY_COLS) * (n + 1) + size_t(2) * n * (FY_COLS + 1) + 2 + size_t(2) * 2 * n * FY_COLS) * sizeof(double);
   PTB_CUDA_CHECK(cudaFuncSetAttribute(k_fourier_fft_y<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   for (size_t p0 = 0; p0 < planes; p0 += 65535) {  // gridDim.y limit
     const size_t np = std::min<size_t>(65535, planes - p0);
