@@ -100,10 +100,10 @@ __device__ __forceinline__ int wrap(int i, int n) {
   return i < 0 ? i + n : i;
 }
 
-template <bool LAYER, int NT>
+template <bool LAYER, int NT, int TY = PTY, int TX = PTX>
 __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
   constexpr int H = LAYER ? HL : HP;
-  using G = Geo<PTY, PTX, H, NT>;
+  using G = Geo<TY, TX, H, NT>;
   constexpr int E = G::EX, EY = G::EY, NPT = G::NPT;
   extern __shared__ double sm[];
   double* us = sm + G::PAD;
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
     if (e < G::EXT) {
       const int ey = e / E, ex = e - ey * E;
       const int oy = ey - H, ox = ex - H;
-      if (oy >= 0 && oy < PTY && ox >= 0 && ox < PTX && ty0 + oy < a.ny && tx0 + ox < a.nx) {
+      if (oy >= 0 && oy < TY && ox >= 0 && ox < TX && ty0 + oy < a.ny && tx0 + ox < a.nx) {
         const size_t g = base + size_t(ty0 + oy) * a.nx + (tx0 + ox);
         a.uo[g] = us[e];
         a.vo[g] = hv[i];
@@ -363,9 +363,15 @@ size_t pml_plain_smem() {
 
 constexpr int kPlainThreads = 256, kLayerThreads = 512;
 
-template <bool LAYER>
+// frame mode (a standard layer: damped bands at both ends of each axis, undamped interior): the
+// interior rectangle runs k_wave2, the four bands run the layer kernel on band-shaped tiles —
+// FB rows x PTX columns (top and bottom), PTY rows x FB columns (left and right)
+constexpr int FB = 40;
+constexpr int FRAME_MARGIN = PS + 2;  // interior rectangle starts this far from the last damped cell
+
+template <bool LAYER, int TY = PTY, int TX = PTX>
 size_t pml_smem() {
-  using G = Geo<PTY, PTX, LAYER ? HL : HP, LAYER ? kLayerThreads : kPlainThreads>;
+  using G = Geo<TY, TX, LAYER ? HL : HP, LAYER ? kLayerThreads : kPlainThreads>;
   return size_t(G::PLANE) * (LAYER ? 3 : 2) * sizeof(double) + (LAYER ? 3 * (G::EX + G::EY) * sizeof(double) : 0) +
          (G::EX + G::EY) * sizeof(int);
 }
@@ -399,6 +405,9 @@ struct ptb_pml {
   // form one: the interior then runs the periodic wavefront kernel (k_wave2) instead of k_pml_plain
   int ry0 = 0, rny = 0, rx0 = 0, rnx = 0;
   ptb::StepParams prm{};
+  // frame mode: interior rectangle and the band tiles (top/bottom FB x PTX, then left/right PTY x FB)
+  int frame = 0, fy0 = 0, fny = 0, fx0 = 0, fnx = 0, ntb = 0, nlr = 0;
+  int2* ftiles = nullptr;
 };
 
 namespace ptb {
@@ -406,6 +415,11 @@ namespace ptb {
 // PTB_PML_WAVE=0: interior tiles through k_pml_plain (A/B measurements, tests)
 bool pml_wave_enabled() {
   const char* e = std::getenv("PTB_PML_WAVE");
+  return !(e && std::atoi(e) == 0);
+}
+// PTB_PML_FRAME=0: the 70 x 54 tile classes instead of the frame (A/B measurements, tests)
+bool pml_frame_enabled() {
+  const char* e = std::getenv("PTB_PML_FRAME");
   return !(e && std::atoi(e) == 0);
 }
 
@@ -449,6 +463,10 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
                                         int(pml_plain_smem())));
     PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(pml_smem<true>())));
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, FB, PTX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(pml_smem<true, FB, PTX>())));
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, PTY, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(pml_smem<true, PTY, FB>())));
     attr_done.fetch_or(bit);
   }
   require(batch <= 65535, "pml propagate: at most 65535 slices per call");
@@ -466,6 +484,21 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     a.pyo = bufs[1 - cur][3];
     a.steps = ns;
     a.flags = done == steps ? flags : nullptr;
+    if (p->frame && (ns == 4 || ns == 2 || ns == 1) && pml_wave_enabled() && pml_frame_enabled()) {
+      // frame mode: the interior rectangle through k_wave2, the bands through band-shaped layer tiles
+      wave_rect_fast(ctx, st, ns, p->prm, batch, a.ui, a.vi, a.uo, a.vo, a.kx, a.flags, p->fy0, p->fny, p->fx0,
+                     p->fnx);
+      a.tiles = p->ftiles;
+      k_pml<true, kLayerThreads, FB, PTX><<<dim3(p->ntb, unsigned(batch)), kLayerThreads, pml_smem<true, FB, PTX>(),
+                                            st>>>(a);
+      PTB_LAUNCH_CHECK(ctx);
+      a.tiles = p->ftiles + p->ntb;
+      k_pml<true, kLayerThreads, PTY, FB><<<dim3(p->nlr, unsigned(batch)), kLayerThreads, pml_smem<true, PTY, FB>(),
+                                            st>>>(a);
+      PTB_LAUNCH_CHECK(ctx);
+      cur = 1 - cur;
+      continue;
+    }
     if (p->nplain && p->rnx && (ns == 4 || ns == 2 || ns == 1) && pml_wave_enabled()) {
       // the undamped interior: the periodic FAST wavefront kernel on the plain-tile rectangle
       // (bitwise k_pml_plain's arithmetic; its S-step cone stays in undamped cells, px = py = 0)
@@ -1079,6 +1112,45 @@ ptb_status ptb_pml_create(ptb_context* ctx, const ptb_grid* grid, const double* 
         p->rnx = x1 - x0;
       }
     }
+    {  // frame mode: damped cells only in bands [0, lo) and [n - hi, n) of each axis
+      auto bands = [](const double* z, long n, long& lo, long& hi) {
+        lo = 0;
+        while (lo < n && z[lo] > 0.0) ++lo;
+        hi = 0;
+        while (hi < n - lo && z[n - 1 - hi] > 0.0) ++hi;
+        for (long i = lo; i < n - hi; ++i)
+          if (z[i] > 0.0) return false;  // damping inside: not a layer
+        return true;
+      };
+      long ylo, yhi, xlo, xhi;
+      if (bands(zeta_y_host, long(ny), ylo, yhi) && bands(zeta_x_host, long(nx), xlo, xhi)) {
+        const long m = FRAME_MARGIN;
+        const long y0 = ylo + m, y1 = long(ny) - yhi - m;
+        const long x0 = (xlo + m + 1) & ~1L, x1 = (long(nx) - xhi - m) & ~1L;
+        const bool fits = y0 <= FB && long(ny) - y1 <= FB && x0 <= FB && long(nx) - x1 <= FB;
+        if (fits && nx % 2 == 0 && y1 - y0 >= 4 * FB && x1 - x0 >= 4 * FB) {
+          std::vector<int2> ft;
+          for (long tx = 0; tx < long(nx); tx += PTX) {  // top and bottom bands, FB rows
+            ft.push_back(make_int2(0, int(tx)));
+            ft.push_back(make_int2(int(ny) - FB, int(tx)));
+          }
+          const int ntb = int(ft.size());
+          for (long ty = y0; ty < y1; ty += PTY) {  // left and right bands between them, FB columns
+            ft.push_back(make_int2(int(ty), 0));
+            ft.push_back(make_int2(int(ty), int(nx) - FB));
+          }
+          p->frame = 1;
+          p->fy0 = int(y0);
+          p->fny = int(y1 - y0);
+          p->fx0 = int(x0);
+          p->fnx = int(x1 - x0);
+          p->ntb = ntb;
+          p->nlr = int(ft.size()) - ntb;
+          PTB_CUDA_CHECK(cudaMalloc(&p->ftiles, ft.size() * sizeof(int2)));
+          PTB_CUDA_CHECK(cudaMemcpy(p->ftiles, ft.data(), ft.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        }
+      }
+    }
     p->prm.dim = 2;
     p->prm.ny = int(ny);
     p->prm.nx = int(nx);
@@ -1103,6 +1175,7 @@ ptb_status ptb_pml_destroy(ptb_pml* p) {
     cudaFree(p->coef);
     cudaFree(p->speed);
     cudaFree(p->tiles);
+    cudaFree(p->ftiles);
     delete p;
   });
 }

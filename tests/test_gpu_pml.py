@@ -326,21 +326,26 @@ def test_pml_theta_sharded_equals_single_gpu(world):
 
 @pytest.mark.parametrize("n,w,steps", [(256, 32, 12), (512, 32, 10), (384, 16, 8)])
 def test_interior_wavefront_equals_plain_tiles_bitwise(ctx, n, w, steps, monkeypatch):
-    """The undamped interior runs the periodic wavefront kernel (k_wave2 on the plain-tile
-    rectangle) instead of k_pml_plain: the same FAST arithmetic, so the layered propagation is
-    bitwise unchanged (steps not a multiple of 4 take a 2- or 1-step pass)."""
+    """The undamped interior runs the periodic wavefront kernel (k_wave2 on the interior
+    rectangle) and the layer band-shaped tiles (frame mode), or k_wave2 on the plain-tile rectangle
+    with 70 x 54 layer tiles, or k_pml_plain + layer tiles: the same arithmetic per point, so the
+    layered propagation is bitwise the same in all three (steps not a multiple of 4 take a 2- or
+    1-step pass)."""
     import paratime_b200 as B
 
     c, zy, zx, state = _case(n, n, 1 / n, 1 / n, w, 2, seed=n + w)
     prop = B.PmlPropagator(ctx, B.Grid((n, n), (1 / n, 1 / n)), c, zy, zx, 0.5 / n / np.sqrt(2), steps)
     out = {}
-    for mode in ("1", "0"):
-        monkeypatch.setenv("PTB_PML_WAVE", mode)
+    for mode, wave, frame in (("frame", "1", "1"), ("tiles+wave", "1", "0"), ("tiles", "0", "0")):
+        monkeypatch.setenv("PTB_PML_WAVE", wave)
+        monkeypatch.setenv("PTB_PML_FRAME", frame)
         t = [ctx.tensor(a) for a in state]
         prop.propagate(*t)
         out[mode] = [x.cpu().numpy() for x in t]
-    for a, b in zip(out["1"], out["0"]):
-        assert np.array_equal(a, b)
+    for other in ("tiles+wave", "tiles"):
+        for a, b in zip(out["frame"], out[other]):
+            assert np.array_equal(a, b), other
+    out["1"] = out["frame"]
     want = M.pml_steps(*(s_[0] for s_ in state), M.PmlCoefficients(c, 1 / n, 1 / n, 0.5 / n / np.sqrt(2), zy, zx), steps)
     for got, ref in zip(out["1"], want):
         assert _rel(got[0], ref) <= TOL
