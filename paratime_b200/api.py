@@ -112,6 +112,12 @@ class Context:
         s = self.torch.cuda.current_stream(self.device).cuda_stream
         check(lib().ptb_context_set_stream(self.h, C.c_void_p(s)))
 
+    def use_own_stream(self):
+        """Issue this context's work on its own stream instead of torch's current one (in-process
+        loopback ranks: each rank's work stays in its own stream, as in one-process-per-GPU runs)."""
+        check(lib().ptb_context_use_own_stream(self.h))
+        return self
+
     def launches(self) -> int:
         return int(lib().ptb_context_launches(self.h))
 

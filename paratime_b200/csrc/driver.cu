@@ -1204,7 +1204,9 @@ struct Driver {
             res = nrm[0] > 0.0 ? std::sqrt(nrm[1]) / std::sqrt(nrm[0]) : 0.0;
           } else {
             HostProf hp_(st());
+            pw.comm = comm;  // the factor update's tall products and QRs are row-sharded over the ranks
             update_svd(pw, corr, Fp, Gp, int(rows), cols, s.tol);
+            pw.comm = nullptr;
             hp_.mark("driver: update_svd total");
             if (s.remove_leading > 0) {
               drop_leading(corr, size_t(s.remove_leading), dropped, ctx);

@@ -29,6 +29,7 @@
 //   k_geam_sub       D = F - D (relative_residual, procrustes.cpp:251).
 
 #include <algorithm>
+#include <functional>
 #include <cstdlib>
 #include <string>
 
@@ -55,6 +56,7 @@ struct GemmArgs {
   int kchunk;  // k-range per blockIdx.z
   double* ws;  // split-K partials [z][n][m] (null: write C)
   int tc = 0;  // 1: the kernel computes C^T (m x n here = C's n x m): element (i, j) goes to C[j + i ldc]
+  int zbase = 0;  // k-range of split z starts at (z + zbase) kchunk (row-slab products)
 };
 
 // op(A) tile (BM x BK) of k-tile k0 into registers.  !TA: A(i, kk) = A[i + kk lda], a warp reads
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(GT, 1) k_dgemm(const GemmArgs a) {
   double* const Asm = gsm;
   double* const Bsm = gsm + 2 * BK * LDS_A;
   const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
-  const int kbeg = blockIdx.z * a.kchunk, kend = min(a.k, kbeg + a.kchunk);
+  const int kbeg = (int(blockIdx.z) + a.zbase) * a.kchunk, kend = min(a.k, kbeg + a.kchunk);
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   double acc[8][4];
 #pragma unroll
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(GT, 2) k_dgemm_mma(const GemmArgs a) {
   double* const Asm = gsm;
   double* const Bsm = gsm + 2 * BK * MLDS_A;
   const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
-  const int kbeg = blockIdx.z * a.kchunk, kend = min(a.k, kbeg + a.kchunk);
+  const int kbeg = (int(blockIdx.z) + a.zbase) * a.kchunk, kend = min(a.k, kbeg + a.kchunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;  // the warp's 32 x 32 block
   const int fr = lane >> 2, fk = lane & 3;                 // fragment row (or column) / k index
@@ -415,7 +417,7 @@ double* workspace(ptb_context* ctx, size_t doubles) {
 }  // namespace
 
 void gemm_core(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
-               const double* B, int ldb, double beta, double* C, int ldc, int tc);
+               const double* B, int ldb, double beta, double* C, int ldc, int tc, int max_splits = 128);
 
 // C (m x n) = alpha op(A) op(B) + beta C, all column-major (BLAS dgemm semantics)
 void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
@@ -463,13 +465,13 @@ void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha,
 }
 
 void gemm_core(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
-               const double* B, int ldb, double beta, double* C, int ldc, int tc) {
+               const double* B, int ldb, double beta, double* C, int ldc, int tc, int max_splits) {
   cudaStream_t st = ctx->stream;
   const int tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN, tiles = tm * tn;
   // split K so the grid covers >= 2 CTAs per SM, keeping >= 4 k-tiles per split
   int splits = 1;
   const int want = 2 * ctx->num_sms;
-  if (tiles < want) splits = std::min({(want + tiles - 1) / tiles, (k + 4 * BK - 1) / (4 * BK), 128});
+  if (tiles < want) splits = std::min({(want + tiles - 1) / tiles, (k + 4 * BK - 1) / (4 * BK), max_splits});
   int kchunk = ((k + splits - 1) / splits + BK - 1) / BK * BK;
   splits = (k + kchunk - 1) / kchunk;
   GemmArgs a{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, kchunk, nullptr, tc};
@@ -503,6 +505,59 @@ void gemm_core(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double a
     k_splitk_reduce<<<ew_grid(ctx, size_t(m) * n), 256, 0, st>>>(m, n, splits, a.ws, alpha, beta, C, ldc, tc);
     PTB_LAUNCH_CHECK(ctx);
   }
+}
+
+// Row-local product for row-sharded matrices: C = alpha A B + beta C on a range of rows, never
+// split over k, so every output row has the same value whatever range (rank) computes it.
+void gemm_rows(ptb_context* ctx, int m, int n, int k, double alpha, const double* A, int lda, const double* B, int ldb,
+               double beta, double* C, int ldc) {
+  if (m == 0 || n == 0) return;
+  if (k == 0 || n == 1) {  // the general entry handles these shapes (no split over rows either way)
+    gemm(ctx, false, false, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    return;
+  }
+  gemm_core(ctx, false, false, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, 0, 1);
+}
+
+// Row-slab reduction C (m x n) = A^T B over `rows` = P slabs of `slab` rows (A: rows x m, B: rows x n,
+// column-major).  This process computes the partials of slabs [z0, z0 + nz) (k-split z of the DMMA
+// kernel = one slab) into ws_own (nz x n x m), `gather` assembles all P partials in slab order into
+// ws_all (it may be ws_own itself when nz == P), and they are summed in slab order: the value is
+// the same whichever process computed which slabs.  A short m is computed as C^T exactly as gemm().
+void gemm_tn_slabs(ptb_context* ctx, int m, int n, const double* A, int lda, const double* B, int ldb, double* C,
+                   int ldc, int P, int slab, int z0, int nz, double* ws_own, double* ws_all,
+                   const std::function<void()>& gather) {
+  cudaStream_t st = ctx->stream;
+  int tc = 0;
+  if (use_dmma() && m <= 1024 && n <= 1024) {
+    const auto padded = [](int rows, int cols) { return size_t((rows + BM - 1) / BM * BM) * ((cols + BN - 1) / BN * BN); };
+    if (padded(n, m) < padded(m, n)) {
+      std::swap(m, n);
+      std::swap(A, B);
+      std::swap(lda, ldb);
+      tc = 1;
+    }
+  }
+  static const bool attrs = [] {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(k_dgemm_mma<true, false>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(MMA_SMEM));
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(k_dgemm<true, false>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(GEMM_SMEM));
+    return true;
+  }();
+  (void)attrs;
+  if (nz > 0) {
+    GemmArgs a{m, n, P * slab, A, lda, B, ldb, C, ldc, 1.0, 0.0, slab, ws_own, tc, z0};
+    const dim3 grid{unsigned((m + BM - 1) / BM), unsigned((n + BN - 1) / BN), unsigned(nz)};
+    if (use_dmma())
+      k_dgemm_mma<true, false><<<grid, GT, MMA_SMEM, st>>>(a);
+    else
+      k_dgemm<true, false><<<grid, GT, GEMM_SMEM, st>>>(a);
+    PTB_LAUNCH_CHECK(ctx);
+  }
+  gather();
+  k_splitk_reduce<<<ew_grid(ctx, size_t(m) * n), 256, 0, st>>>(m, n, P, ws_all, 1.0, 0.0, C, ldc, tc);
+  PTB_LAUNCH_CHECK(ctx);
 }
 
 // D = F - D, rows x cols contiguous (relative_residual)

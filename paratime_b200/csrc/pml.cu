@@ -802,7 +802,9 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
       PTB_CUDA_CHECK(cudaMemcpyAsync(idx_d, keep.data(), keep.size() * sizeof(int), cudaMemcpyHostToDevice, st));
       energy_components(ew, cgr, th->scheme, size_t(cols), crf.f(0), crf.f(1), nc, idx_d, ccs, Fm, rows, nullptr);
       energy_components(ew, cgr, th->scheme, size_t(cols), cold.f(0), cold.f(1), nc, idx_d, ccs, Gm, rows, nullptr);
+      pw->comm = comm;
       update_svd(*pw, corr, Fm, Gm, int(rows), cols, th->tol);
+      pw->comm = nullptr;
       if (th->residual) res = relative_residual(*pw, corr, Fm, Gm, int(rows), cols);
     }
     if (th->ranks) th->ranks[k - 1] = corr.rank;

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "ptb_dsmem.h"
+#include "ptb_comm.h"
 #include "ptb_procrustes.h"
 
 namespace cg = cooperative_groups;
@@ -2475,6 +2476,288 @@ void solve_from_scratch(ProcWork& w, DevCorrector& out, const double* F, const d
 }
 
 // procrustes.cpp:188-237; `c` is updated in place.
+// ---- row-sharded update_svd -------------------------------------------------------------------
+// The corrector's tall matrices (3 N_c rows) are cut into SLABS fixed slabs of whole TSQR leaves;
+// with W ranks, rank q owns the contiguous slabs [q SLABS/W, (q+1) SLABS/W).  The products over rows
+// (U^T F, V^T G, the panels' Gram-Schmidt projections) are per-slab partials gathered and summed in
+// slab order; row-local products (projections, rotations) are never split over k; the TSQR leaves
+// of a slab are factored by its owner and the stack of all leaves' R is gathered and reduced by
+// every rank (truncated_qr_tsqr on the stack: exactly the unsharded TSQR's levels above the
+// leaves).  So every value is the same at any W, W = 1 included; the new factors' own rows are
+// gathered, fix_signs and everything small (H, its SVD) are replicated.
+constexpr int SLABS = 48;
+struct RowPart {
+  int W, rank, rows, own, r0;  // own rows [r0, r0 + own)
+};
+
+bool row_shard(int rows, int cols, const Comm* comm, RowPart& rp) {
+  const int W = comm ? comm->world : 1;
+  static const bool env = [] {
+    const char* e = std::getenv("PTB_ROW_SHARD");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!env || rows % (SLABS * TS_ROWS) != 0 || SLABS % W != 0 || cols < 1 || cols > 2 * TS_MAXN || rows < 8 * cols)
+    return false;
+  const int rank = comm ? comm->rank : 0;
+  rp = RowPart{W, rank, rows, rows / W, rank * (rows / W)};
+  return true;
+}
+
+// full[(q own + i) + j rows] = g[q own cols + i + j own]: the ranks' row blocks into one matrix
+__global__ void k_repack_rows(int W, int own, int cols, const double* __restrict__ g, double* __restrict__ full) {
+  const size_t rows = size_t(W) * own, total = rows * size_t(cols);
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t j = e / rows, i = e - j * rows, q = i / size_t(own), li = i - q * size_t(own);
+    full[e] = g[q * size_t(own) * cols + li + j * size_t(own)];
+  }
+}
+
+// every rank's own block (own x cols, ld own) -> full (rows x cols, ld rows) on every rank
+void gather_rows(ProcWork& w, const RowPart& rp, const double* own, int cols, double* full, DeviceBuffer& tmp) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  if (cols == 0) return;
+  if (rp.W == 1) {
+    if (own != full)
+      PTB_CUDA_CHECK(cudaMemcpyAsync(full, own, size_t(rp.rows) * cols * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  double* g = static_cast<double*>(tmp.get(size_t(rp.rows) * cols * sizeof(double)));
+  w.comm->allgather(own, g, size_t(rp.own) * cols * sizeof(double), st);
+  const size_t total = size_t(rp.rows) * cols;
+  k_repack_rows<<<unsigned(std::min<size_t>((total + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0, st>>>(
+      rp.W, rp.own, cols, g, full);
+  PTB_LAUNCH_CHECK(ctx);
+}
+
+// C (m x n) = A^T B over the slabs: A, B full (every rank holds all rows: z offset = own slabs) or
+// own (rows from the own slabs' first row: offset 0)
+void slab_tn(ProcWork& w, const RowPart& rp, bool full, int m, int n, const double* A, int lda, const double* B, int ldb,
+             double* C) {
+  ptb_context* ctx = w.ctx;
+  if (m == 0 || n == 0) return;
+  const int per = SLABS / rp.W, slab = rp.rows / SLABS;
+  double* own = static_cast<double*>(w.SH[6].get(size_t(per) * m * n * sizeof(double)));
+  double* all = rp.W == 1 ? own : static_cast<double*>(w.SH[7].get(size_t(SLABS) * m * n * sizeof(double)));
+  gemm_tn_slabs(ctx, m, n, A, lda, B, ldb, C, m, SLABS, slab, full ? rp.rank * per : 0, per, own, all, [&] {
+    if (rp.W > 1) w.comm->allgather(own, all, size_t(per) * m * n * sizeof(double), ctx->stream);
+  });
+}
+
+// truncated_qr (procrustes.cpp:34-46) of a row-sharded tall block through the TSQR route: this
+// rank's leaves, the gathered stack of all leaves' R reduced by truncated_qr_tsqr (the unsharded
+// TSQR above its first level), then this rank's leaves applied to the stack's Q -> the own rows of
+// Q (own x kq, ld own).  R and kq are the same on every rank.
+int tsqr_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, double drop_tol, DeviceBuffer& Qo,
+              DeviceBuffer& Rb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  const int nbo = rp.own / TS_ROWS, nbt = rp.rows / TS_ROWS;
+  double* V = static_cast<double*>(w.SH[0].get(size_t(rp.own) * n * sizeof(double)));
+  double* tau = static_cast<double*>(w.SH[1].get(size_t(nbo) * n * sizeof(double)));
+  double* So = static_cast<double*>(w.SH[2].get(size_t(nbo) * n * n * sizeof(double)));
+  QrRegArgs la{A, lda, rp.own, n, nbo, 0, -1.0, nullptr, V, rp.own, So, nbo * n, tau, nullptr, nullptr, nullptr};
+  launch_pdl(k_qr_reg<4, 8, false, true>, dim3(unsigned(nbo)), dim3(QRR_THREADS), 0, st, la, la);
+  PTB_LAUNCH_CHECK(ctx);
+  double* S = So;
+  if (rp.W > 1) {
+    S = static_cast<double*>(w.SH[3].get(size_t(nbt) * n * n * sizeof(double)));
+    RowPart sp{rp.W, rp.rank, nbt * n, nbo * n, rp.rank * nbo * n};  // the stack: rows = leaves x n
+    gather_rows(w, sp, So, n, S, w.SH[4]);
+  }
+  const int kq = truncated_qr_tsqr(w, S, nbt * n, n, drop_tol, w.SH[5], Rb);  // Q of the stack: (nbt n) x kq
+  double* Q = static_cast<double*>(Qo.get(std::max<size_t>(1, size_t(rp.own) * kq) * sizeof(double)));
+  if (kq == 0) return 0;
+  PTB_CUDA_CHECK(cudaFuncSetAttribute(k_tsqr_apply4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int((size_t(TS_ROWS) * TS_MAXN + TS_MAXN) * sizeof(double))));
+  const int leaf0 = rp.r0 / TS_ROWS;
+  const TsApply ap{V, rp.own, n, nbo, tau, static_cast<const double*>(w.SH[5].ptr) + size_t(leaf0) * n, nbt * n, kq, Q,
+                   rp.own};
+  launch_pdl(k_tsqr_apply4, dim3(unsigned(nbo), 1), dim3(QRR_THREADS), (size_t(TS_ROWS) * n + n) * sizeof(double), st,
+             ap, ap);
+  PTB_LAUNCH_CHECK(ctx);
+  return kq;
+}
+
+// F and G together (update_svd's two QRs, the same shape): every leaf launch and every down-sweep
+// launch covers both matrices, the stacks go through truncated_qr_pair (one launch per level, one
+// host sync for both keep counts) — each matrix gets exactly tsqr_rows' arithmetic.
+void tsqr_rows_pair(ProcWork& w, const RowPart& rp, const double* Af, const double* Ag, int lda, int n, double tol_f,
+                    double tol_g, DeviceBuffer& Qf, DeviceBuffer& Rf, DeviceBuffer& Qg, DeviceBuffer& Rg, int& kf,
+                    int& kg) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  const int nbo = rp.own / TS_ROWS, nbt = rp.rows / TS_ROWS;
+  DeviceBuffer* B[2] = {w.SH, w.SG};
+  const double* A[2] = {Af, Ag};
+  double *V[2], *tau[2], *So[2], *S[2];
+  QrRegArgs la[2];
+  for (int b = 0; b < 2; ++b) {
+    V[b] = static_cast<double*>(B[b][0].get(size_t(rp.own) * n * sizeof(double)));
+    tau[b] = static_cast<double*>(B[b][1].get(size_t(nbo) * n * sizeof(double)));
+    So[b] = static_cast<double*>(B[b][2].get(size_t(nbo) * n * n * sizeof(double)));
+    la[b] = QrRegArgs{A[b], lda, rp.own, n, nbo, 0, -1.0, nullptr, V[b], rp.own, So[b], nbo * n, tau[b], nullptr,
+                      nullptr, nullptr};
+  }
+  launch_pdl(k_qr_reg<4, 8, false, true>, dim3(unsigned(nbo), 2), dim3(QRR_THREADS), 0, st, la[0], la[1]);
+  PTB_LAUNCH_CHECK(ctx);
+  for (int b = 0; b < 2; ++b) {
+    S[b] = So[b];
+    if (rp.W > 1) {
+      S[b] = static_cast<double*>(B[b][3].get(size_t(nbt) * n * n * sizeof(double)));
+      RowPart sp{rp.W, rp.rank, nbt * n, nbo * n, rp.rank * nbo * n};
+      gather_rows(w, sp, So[b], n, S[b], B[b][4]);
+    }
+  }
+  int k[2] = {0, 0};
+  if (!truncated_qr_pair(w, S[0], S[1], nbt * n, n, tol_f, tol_g, w.SH[5], Rf, w.SG[5], Rg, k[0], k[1])) {
+    k[0] = truncated_qr_tsqr(w, S[0], nbt * n, n, tol_f, w.SH[5], Rf);
+    k[1] = truncated_qr_tsqr(w, S[1], nbt * n, n, tol_g, w.SG[5], Rg);
+  }
+  DeviceBuffer* Qo[2] = {&Qf, &Qg};
+  TsApply ap[2];
+  const int leaf0 = rp.r0 / TS_ROWS;
+  for (int b = 0; b < 2; ++b) {
+    double* Q = static_cast<double*>(Qo[b]->get(std::max<size_t>(1, size_t(rp.own) * k[b]) * sizeof(double)));
+    ap[b] = TsApply{V[b], rp.own, n, nbo, tau[b], static_cast<const double*>(B[b][5].ptr) + size_t(leaf0) * n,
+                    nbt * n, k[b], Q, rp.own};
+  }
+  if (k[0] > 0 || k[1] > 0) {
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_tsqr_apply4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int((size_t(TS_ROWS) * TS_MAXN + TS_MAXN) * sizeof(double))));
+    launch_pdl(k_tsqr_apply4, dim3(unsigned(nbo), 2), dim3(QRR_THREADS), (size_t(TS_ROWS) * n + n) * sizeof(double),
+               st, ap[0], ap[1]);
+    PTB_LAUNCH_CHECK(ctx);
+  }
+  kf = k[0];
+  kg = k[1];
+}
+
+// the two-panel route (truncated_qr_2panel) on a row-sharded block: both panels through tsqr_rows,
+// the Gram-Schmidt projections over the slabs
+int qr2_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, double drop_tol, DeviceBuffer& Qo,
+             DeviceBuffer& Rb) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  const int n1 = TS_MAXN, n2 = n - n1, own = rp.own;
+  const int k1 = tsqr_rows(w, rp, A, lda, n1, 0.0, w.TP[0], w.TP[1]);
+  const double* Q1 = static_cast<const double*>(w.TP[0].ptr);
+  double* A2 = static_cast<double*>(w.TP[2].get(size_t(own) * n2 * sizeof(double)));
+  PTB_CUDA_CHECK(cudaMemcpy2DAsync(A2, size_t(own) * sizeof(double), A + size_t(n1) * lda, size_t(lda) * sizeof(double),
+                                   size_t(own) * sizeof(double), n2, cudaMemcpyDeviceToDevice, st));
+  double* C = static_cast<double*>(w.TP[3].get(std::max<size_t>(1, 2 * size_t(k1) * n2) * sizeof(double)));
+  if (k1 > 0) {
+    for (int pass = 0; pass < 2; ++pass) {
+      double* Cp = C + size_t(pass) * k1 * n2;
+      slab_tn(w, rp, false, k1, n2, Q1, own, A2, own, Cp);
+      gemm_rows(ctx, own, n2, k1, -1.0, Q1, own, Cp, k1, 1.0, A2, own);
+    }
+  }
+  const int k2 = tsqr_rows(w, rp, A2, own, n2, 0.0, w.TP[4], w.TP[5]);
+  const int kk = k1 + k2;
+  double* R = static_cast<double*>(w.TP[6].get(std::max<size_t>(1, size_t(kk) * n) * sizeof(double)));
+  if (kk == 0) {
+    Qo.get(8);
+    Rb.get(8);
+    return 0;
+  }
+  k_assemble_r2<<<unsigned(std::max(1, std::min(1024, (kk * n + 255) / 256))), 256, 0, st>>>(
+      k1, k2, n1, n2, static_cast<const double*>(w.TP[1].ptr), C, C + size_t(k1) * n2,
+      static_cast<const double*>(w.TP[5].ptr), R);
+  PTB_LAUNCH_CHECK(ctx);
+  const int kq = truncated_qr_direct(w, R, kk, n, drop_tol, w.BQ2, Rb);
+  double* Q = static_cast<double*>(Qo.get(std::max<size_t>(1, size_t(own) * kq) * sizeof(double)));
+  if (kq == 0) return 0;
+  const double* QR = static_cast<const double*>(w.BQ2.ptr);
+  if (k1 > 0) gemm_rows(ctx, own, kq, k1, 1.0, Q1, own, QR, kk, 0.0, Q, own);
+  if (k2 > 0)
+    gemm_rows(ctx, own, kq, k2, 1.0, static_cast<const double*>(w.TP[4].ptr), own, QR + k1, kk, k1 > 0 ? 1.0 : 0.0, Q,
+              own);
+  return kq;
+}
+
+int qr_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, double drop_tol, DeviceBuffer& Qo,
+            DeviceBuffer& Rb) {
+  return n <= TS_MAXN ? tsqr_rows(w, rp, A, lda, n, drop_tol, Qo, Rb) : qr2_rows(w, rp, A, lda, n, drop_tol, Qo, Rb);
+}
+
+void update_svd_rows(ProcWork& w, DevCorrector& c, const double* F, const double* G, int rows, int cols, double tol,
+                     const RowPart& rp) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  HostProf hp_(st);
+  const int r = c.rank, own = rp.own;
+  const double* U = c.Xp();
+  const double* V = c.Yp();
+  double* UF = static_cast<double*>(w.buf[13].get(std::max<size_t>(1, size_t(r) * cols) * sizeof(double)));
+  double* VG = static_cast<double*>(w.buf[14].get(std::max<size_t>(1, size_t(r) * cols) * sizeof(double)));
+  slab_tn(w, rp, true, r, cols, U, rows, F, rows, UF);
+  slab_tn(w, rp, true, r, cols, V, rows, G, rows, VG);
+  // own rows of the projections F - U (U^T F), G - V (V^T G)
+  double* Fr = static_cast<double*>(w.buf[15].get(size_t(own) * cols * sizeof(double)));
+  double* Gr = static_cast<double*>(w.buf[16].get(size_t(own) * cols * sizeof(double)));
+  PTB_CUDA_CHECK(cudaMemcpy2DAsync(Fr, size_t(own) * sizeof(double), F + rp.r0, size_t(rows) * sizeof(double),
+                                   size_t(own) * sizeof(double), cols, cudaMemcpyDeviceToDevice, st));
+  PTB_CUDA_CHECK(cudaMemcpy2DAsync(Gr, size_t(own) * sizeof(double), G + rp.r0, size_t(rows) * sizeof(double),
+                                   size_t(own) * sizeof(double), cols, cudaMemcpyDeviceToDevice, st));
+  if (r > 0) {
+    gemm_rows(ctx, own, cols, r, -1.0, U + rp.r0, rows, UF, r, 1.0, Fr, own);
+    gemm_rows(ctx, own, cols, r, -1.0, V + rp.r0, rows, VG, r, 1.0, Gr, own);
+  }
+  hp_.mark("update(rows): projections");
+  const double qr_guard = 1e-14;
+  const double fn = std::sqrt(dev_sumsq(ctx, F, size_t(rows) * cols, w.buf[11]));  // F, G are replicated
+  const double gn = std::sqrt(dev_sumsq(ctx, G, size_t(rows) * cols, w.buf[11]));
+  int qf = 0, qg = 0;
+  if (cols <= TS_MAXN) {
+    tsqr_rows_pair(w, rp, Fr, Gr, own, cols, qr_guard * fn, qr_guard * gn, w.QF, w.RF, w.QG, w.RG, qf, qg);
+  } else {
+    qf = qr_rows(w, rp, Fr, own, cols, qr_guard * fn, w.QF, w.RF);
+    qg = qr_rows(w, rp, Gr, own, cols, qr_guard * gn, w.QG, w.RG);
+  }
+  hp_.mark("update(rows): qr F, G");
+  double* LB = static_cast<double*>(w.buf[17].get(std::max<size_t>(1, size_t(r + qf) * cols) * sizeof(double)));
+  double* RB = static_cast<double*>(w.buf[18].get(std::max<size_t>(1, size_t(r + qg) * cols) * sizeof(double)));
+  const unsigned nb = unsigned(std::max(1, std::min(1024, ((r + std::max(qf, qg)) * cols + 255) / 256)));
+  k_stack_rows<<<nb, 256, 0, st>>>(UF, r, static_cast<double*>(w.RF.ptr), qf, cols, LB);
+  PTB_LAUNCH_CHECK(ctx);
+  k_stack_rows<<<nb, 256, 0, st>>>(VG, r, static_cast<double*>(w.RG.ptr), qg, cols, RB);
+  PTB_LAUNCH_CHECK(ctx);
+  const int hp = r + qf, hq = r + qg;
+  double* H = static_cast<double*>(w.buf[12].get(size_t(hp) * hq * sizeof(double)));
+  gemm(ctx, false, true, hp, hq, cols, 1.0, LB, hp, RB, hq, 0.0, H, hp);
+  k_add_diag<<<1, 256, 0, st>>>(H, hp, static_cast<const double*>(c.Sd.ptr), r);
+  PTB_LAUNCH_CHECK(ctx);
+  std::vector<double> sigma;
+  thin_svd(w, H, hp, hq, w.Uh, sigma, w.Vh);
+  hp_.mark("update(rows): H + svd");
+  const int keep = truncate_count(sigma, tol);
+  double* X = static_cast<double*>(w.SX.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
+  double* Y = static_cast<double*>(w.SY.get(std::max<size_t>(1, size_t(rows) * keep) * sizeof(double)));
+  const double* Uh = static_cast<double*>(w.Uh.ptr);
+  const double* Vh = static_cast<double*>(w.Vh.ptr);
+  // own rows of the new factors, then every rank's rows gathered
+  double* Xo = rp.W == 1 ? X : static_cast<double*>(w.SH[8].get(std::max<size_t>(1, size_t(own) * keep) * sizeof(double)));
+  double* Yo = rp.W == 1 ? Y : static_cast<double*>(w.SH[9].get(std::max<size_t>(1, size_t(own) * keep) * sizeof(double)));
+  if (keep > 0) {
+    if (r > 0) {
+      gemm_rows(ctx, own, keep, r, 1.0, U + rp.r0, rows, Uh, hp, 0.0, Xo, own);
+      gemm_rows(ctx, own, keep, r, 1.0, V + rp.r0, rows, Vh, hq, 0.0, Yo, own);
+    }
+    if (qf > 0) gemm_rows(ctx, own, keep, qf, 1.0, static_cast<double*>(w.QF.ptr), own, Uh + r, hp, r > 0 ? 1.0 : 0.0, Xo, own);
+    if (qg > 0) gemm_rows(ctx, own, keep, qg, 1.0, static_cast<double*>(w.QG.ptr), own, Vh + r, hq, r > 0 ? 1.0 : 0.0, Yo, own);
+    gather_rows(w, rp, Xo, keep, X, w.SH[10]);
+    gather_rows(w, rp, Yo, keep, Y, w.SH[11]);
+  }
+  hp_.mark("update(rows): rotate + gather");
+  fix_signs(ctx, X, Y, rows, keep);
+  sigma.resize(size_t(keep));
+  PTB_CUDA_CHECK(cudaStreamSynchronize(st));
+  std::swap(c.X, w.SX);
+  std::swap(c.Y, w.SY);
+  c.assign(rows, keep, sigma, tol);
+}
+
 void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, int rows, int cols, double tol) {
   check_tol(tol);
   ptb_context* ctx = w.ctx;
@@ -2483,6 +2766,10 @@ void update_svd(ProcWork& w, DevCorrector& c, const double* F, const double* G, 
     return;
   }
   require(rows == c.rows, "update_svd: block rows do not match corrector");
+  if (RowPart rp{}; row_shard(rows, cols, w.comm, rp)) {
+    update_svd_rows(w, c, F, G, rows, cols, tol, rp);
+    return;
+  }
   HostProf hp_(ctx->stream);
   const int r = c.rank;
   const double* U = c.Xp();

@@ -1,4 +1,5 @@
 #pragma once
+#include <functional>
 #include <vector>
 
 #include "ptb_internal.h"
@@ -35,6 +36,11 @@ struct ProcWork {
   DeviceBuffer TS2[24], TX2[2], BQ2b;  // the second matrix of a batched (F, G) TSQR
   DeviceBuffer PA[4], PB[4];        // batched TSQR: the two final pivoted factors, tau, perm, |R_jj|
   DeviceBuffer TP[8];               // two-panel TSQR: Q1, R1, A2, C, Q2, R2, the assembled R
+  DeviceBuffer SH[12];              // row-sharded update_svd: level-0 leaves, stacks, slab partials, gathers
+  DeviceBuffer SG[6];               // the second matrix (G) of the row-sharded pair TSQR
+  // the ranks the corrector's rows are sharded over (update_svd; null: one process).  Set by the
+  // parareal driver around its update_svd call.
+  const struct Comm* comm = nullptr;
   explicit ProcWork(ptb_context* c);
   ~ProcWork();
 };
@@ -52,6 +58,13 @@ void drop_leading(const DevCorrector& c, size_t count, DevCorrector& out, ptb_co
 void gemm(ptb_context* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int lda,
           const double* B, int ldb, double beta, double* C, int ldc);
 void geam_sub(ptb_context* ctx, size_t total, const double* F, double* D);  // D = F - D
+// row-sharded corrector products (gemm.cu): row-local C = alpha A B + beta C (never split over k),
+// and A^T B over fixed row slabs with the partials of slabs [z0, z0 + nz) computed here
+void gemm_rows(ptb_context* ctx, int m, int n, int k, double alpha, const double* A, int lda, const double* B, int ldb,
+               double beta, double* C, int ldc);
+void gemm_tn_slabs(ptb_context* ctx, int m, int n, const double* A, int lda, const double* B, int ldb, double* C,
+                   int ldc, int P, int slab, int z0, int nz, double* ws_own, double* ws_all,
+                   const std::function<void()>& gather);
 void fix_signs(ptb_context* ctx, double* X, double* Y, int rows, int cols);
 
 }  // namespace ptb

@@ -216,7 +216,7 @@ def test_pml_parareal_sharded_equals_single_gpu(world):
     c1 = B.Context(0)
     single = B.pml_parareal_run(*objects(c1), s["N"], s["K"], s["u0"], v0, keep_states=True)
     group = B.api.LoopbackGroup(world)
-    ctxs = [B.Context(0) for _ in range(world)]
+    ctxs = [B.Context(0).use_own_stream() for _ in range(world)]  # a stream per rank
     objs = [objects(c) for c in ctxs]
     comms = [group.comm(ctxs[r], r) for r in range(world)]
     out, err = [None] * world, []
@@ -298,7 +298,7 @@ def test_pml_theta_sharded_equals_single_gpu(world):
 
     single = B.pml_theta_run(*objects(B.Context(0)), s["N"], s["K"], s["u0"], v0, keep_states=True)
     group = B.api.LoopbackGroup(world)
-    ctxs = [B.Context(0) for _ in range(world)]
+    ctxs = [B.Context(0).use_own_stream() for _ in range(world)]  # a stream per rank
     objs = [objects(c) for c in ctxs]
     comms = [group.comm(ctxs[r], r) for r in range(world)]
     out, errs = [None] * world, []

@@ -19,7 +19,7 @@ def _run_world(world, spec, cf, cc, u0, v0):
     import paratime_b200 as B
 
     group = B.api.LoopbackGroup(world)
-    ctxs = [B.Context(0) for _ in range(world)]
+    ctxs = [B.Context(0).use_own_stream() for _ in range(world)]  # a stream per rank
     comms = [group.comm(ctxs[r], r) for r in range(world)]
     out = [None] * world
     err = []
@@ -31,12 +31,15 @@ def _run_world(world, spec, cf, cc, u0, v0):
         except Exception as e:  # pragma: no cover
             err.append(e)
 
-    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    # daemon threads joined with a timeout: a rank that fails leaves the others waiting at the
+    # loopback barrier, and the failure must surface instead of hanging the suite
+    ts = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
     for t in ts:
         t.start()
     for t in ts:
-        t.join()
+        t.join(timeout=600)
     assert not err, err
+    assert all(not t.is_alive() for t in ts), "a rank did not finish (loopback barrier)"
     return out
 
 
@@ -57,6 +60,29 @@ def test_sharded_equals_single_gpu(world, variant, large, monkeypatch):
         assert np.array_equal(o["energy_err"], single["energy_err"])
         assert np.array_equal(o["l2_err"], single["l2_err"])
         assert list(o["rank"]) == list(single["rank"])
+        np.testing.assert_array_equal(o["residual"][1:], single["residual"][1:])
+        a = 1 + r * chunk
+        b = min(N + 1, a + chunk)
+        lo = 0 if r == 0 else a
+        assert np.array_equal(o["states"][:, lo:b], single["states"][:, lo:b])
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_row_sharded_procrustes_equals_single_gpu(world):
+    """Config 2 (3 N_c = 12288 rows = 48 slabs of one TSQR leaf): update_svd runs row-sharded —
+    the U^T F / V^T G partials per fixed slab gathered and summed in slab order, each rank's TSQR
+    leaves factored by it and the leaves' R stack gathered, the new factors' own rows gathered.
+    Iterates, error tables, ranks and residuals bitwise equal to one GPU; the one-GPU run takes the
+    same slab path (tests/test_gpu_configs.py pins it to the reference at 1e-10)."""
+    spec, cf, cc, u0, v0 = W.cfg2()
+    spec = dict(spec, iterations=3)
+    single = _run_world(1, spec, cf, cc, u0, v0)[0]
+    outs = _run_world(world, spec, cf, cc, u0, v0)
+    N = spec["n_couplings"]
+    chunk = -(-N // world)
+    for r, o in enumerate(outs):
+        assert list(o["rank"]) == list(single["rank"])
+        assert np.array_equal(o["energy_err"], single["energy_err"])
         np.testing.assert_array_equal(o["residual"][1:], single["residual"][1:])
         a = 1 + r * chunk
         b = min(N + 1, a + chunk)
