@@ -174,3 +174,69 @@ def pml_plain_sharded(u0, v0, kf, m_f, kc, m_c, t, N, K):
         hist.append(nxt)
         cur = nxt
     return hist
+
+
+# ---------------------------------------------------------------- row-sharded update_svd
+# The decomposition of paratime_b200/csrc/procrustes.cu `update_svd_rows` restated on numpy: the
+# tall matrices' rows are cut into SLABS fixed slabs of whole TSQR leaves, rank q owns the
+# contiguous slabs [q SLABS/W, (q+1) SLABS/W).  Products over rows are per-slab partials gathered
+# and summed in slab order; projections and rotations are row-local; each rank factors its own
+# leaves, the stack of all leaves' R is gathered and reduced by every rank; the new factors' rows
+# are gathered.  Everything small (H, its SVD, fix_signs) is replicated.
+
+SLABS = 4
+
+
+def _slab_tn(A_own, B_own, per):
+    """A^T B over all rows: own slabs' partials -> all-gather -> summed in slab order."""
+    slab = A_own.shape[0] // per
+    parts = [A_own[s * slab:(s + 1) * slab].T @ B_own[s * slab:(s + 1) * slab] for s in range(per)]
+    acc = None
+    for ranks_parts in _allgather(parts):  # rank order == slab order (contiguous ownership)
+        for p in ranks_parts:
+            acc = p.copy() if acc is None else acc + p
+    return acc
+
+
+def _tsqr_rows(A_own, leaf_rows, drop_tol):
+    """truncated_qr of the row-sharded block: own leaves, gathered R stack, own rows of Q."""
+    n = A_own.shape[1]
+    nbo = A_own.shape[0] // leaf_rows
+    Ql, Rl = [], []
+    for b in range(nbo):
+        q, r = np.linalg.qr(A_own[b * leaf_rows:(b + 1) * leaf_rows])
+        Ql.append(q)
+        Rl.append(r)
+    stacks = _allgather(np.vstack(Rl))
+    S = np.vstack(stacks)
+    Qs, R = P.truncated_qr(S, drop_tol)  # the pivoted decision is taken on the stack, replicated
+    leaf0 = sum(s.shape[0] for s in stacks[:dist.get_rank()]) // n
+    Q = np.vstack([Ql[b] @ Qs[(leaf0 + b) * n:(leaf0 + b + 1) * n] for b in range(nbo)])
+    return Q, R
+
+
+def update_svd_row_sharded(corr: P.Corrector, F, G, tol, leaf_rows):
+    """procrustes.cpp:188-237 with the rows of U, V, F, G sharded over the ranks."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    rows = F.shape[0]
+    assert rows % (SLABS * leaf_rows) == 0 and SLABS % world == 0
+    per, own = SLABS // world, rows // world
+    sl = slice(rank * own, (rank + 1) * own)
+    U, V, Fo, Go = corr.X[sl], corr.Y[sl], F[sl], G[sl]
+    r = corr.rank
+    UF = _slab_tn(U, Fo, per)
+    VG = _slab_tn(V, Go, per)
+    fn = np.sqrt(sum(_allgather(float(np.sum(Fo * Fo)))))
+    gn = np.sqrt(sum(_allgather(float(np.sum(Go * Go)))))
+    QF, RF = _tsqr_rows(Fo - U @ UF, leaf_rows, 1e-14 * fn)
+    QG, RG = _tsqr_rows(Go - V @ VG, leaf_rows, 1e-14 * gn)
+    H = np.vstack([UF, RF]) @ np.vstack([VG, RG]).T
+    H[np.arange(r), np.arange(r)] += corr.S
+    Uh, sigma, Vh = P._thin_svd(H)
+    keep = P._truncate(sigma, tol)
+    Xo = np.hstack([U, QF]) @ Uh[:, :keep]
+    Yo = np.hstack([V, QG]) @ Vh[:, :keep]
+    X = np.vstack(_allgather(Xo))
+    Y = np.vstack(_allgather(Yo))
+    P.fix_signs(X, Y)
+    return P.Corrector(X, sigma[:keep].copy(), Y, tol)
