@@ -54,11 +54,6 @@
 #ifndef PTB_WAVE2_RING
 #define PTB_WAVE2_RING 0
 #endif
-// full-row strips of at least this many threads take the bulk-copy ring (variant 2) instead:
-// 512^2 x 64 (W = 256) 7.0 -> 7.7e11 updates/s; narrower full-row strips and haloed strips lose
-#ifndef PTB_WAVE2_BULK_FROM
-#define PTB_WAVE2_BULK_FROM 256
-#endif
 
 namespace ptb {
 
@@ -852,284 +847,6 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     o += nx;
     if (o >= npts) o -= npts;
   };
-  // ring variant of this instantiation (see the top of the file): the bulk-copy ring pays on wide
-  // full-row strips only (one aligned copy per row for 8 warps), cp.async everywhere else
-  constexpr int RINGV = (FULL && W >= PTB_WAVE2_BULK_FROM && PTB_WAVE2_RING <= 1) ? 2 : PTB_WAVE2_RING;
-  constexpr bool R_ASYNC = RINGV <= 1, R_REGS = RINGV >= 4, R_BULK = !R_ASYNC && !R_REGS;
-  // R_REGS: level-0 inputs straight into registers, PD rows ahead (no shared-memory ring)
-  constexpr int PD = R_REGS ? RINGV - 2 : 1;
-  [[maybe_unused]] double2 pu[PD], pv[PD], pk[PD];
-  // R_BULK: level-0 rows arrive by bulk copies (the TMA engine, cp.async.bulk) that complete on an
-  // mbarrier; every thread waits on the barrier's phase and reads its pair from the slot.
-  //   RING 2: one thread moves the CTA's three row segments (2W doubles each, split where the strip
-  //           wraps the periodic x boundary), one barrier per slot;
-  //   RING 3: lane 0 of each warp moves the warp's 64-column segments, one barrier per slot and warp
-  //           (no cross-warp dependency: a warp only waits for its own bytes).
-  constexpr int NW = RING_ISSUERS<RINGV, T>;
-  constexpr int SEG = 2 * T / NW;  // doubles per issuer and row
-  [[maybe_unused]] uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RING * 3 * T);
-  [[maybe_unused]] const int wid = RINGV == 3 ? (j >> 5) : 0;
-  [[maybe_unused]] const bool issuer = RINGV == 3 ? (j & 31) == 0 : j == 0;
-  // first column of the issuer's segment
-  [[maybe_unused]] const int gx0 = ((FULL ? 0 : ((x0 - HXE) % nx + nx) % nx) + SEG * wid) % nx;
-  [[maybe_unused]] int ru = 0, rv = 0;  // next u row / udot,coef row (issuers)
-  if constexpr (R_BULK) {
-    if (issuer) {
-      ru = ((ystart + 1) % ny + ny) % ny;
-      rv = ((ystart) % ny + ny) % ny;
-#pragma unroll
-      for (int s0 = 0; s0 < RING; ++s0) mbar_init(smem_addr(&bars[s0 * NW + wid]), 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-  }
-  auto copy_row = [&](double* dst, const double* row, unsigned bar) {
-    int col = gx0, rem = SEG;
-    while (rem > 0) {
-      const int len = min(rem, nx - col);
-      bulk_from_global(smem_addr(dst), row + col, unsigned(len) * 8u, bar);
-      dst += len;
-      rem -= len;
-      col = 0;
-    }
-  };
-  auto issue = [&](int slot, int iter) {
-    if constexpr (R_ASYNC) {
-      double2* d = ring + (slot * 3) * T + j;
-      cp_async16<RINGV == 1>(d, U + ou);
-      cp_async16<RINGV == 1>(d + T, V + ov);
-      cp_async16<RINGV == 1>(d + 2 * T, K + ov);
-      cp_async_commit();
-      adv(ou);
-      adv(ov);
-    } else if constexpr (R_REGS) {
-      pu[slot] = ldg_stream2(U + ou);
-      pv[slot] = ldg_stream2(V + ov);
-      pk[slot] = ldg_stream2(K + ov);
-      adv(ou);
-      adv(ov);
-    } else {
-      if (issuer && iter < n_iter) {
-        const unsigned bar = smem_addr(&bars[slot * NW + wid]);
-        mbar_expect(bar, unsigned(3 * SEG) * 8u);
-        double* d = reinterpret_cast<double*>(ring + (slot * 3) * T) + SEG * wid;
-        copy_row(d, U + size_t(ru) * nx, bar);
-        copy_row(d + 2 * T, V + size_t(rv) * nx, bar);
-        copy_row(d + 4 * T, K + size_t(rv) * nx, bar);
-        if (++ru == ny) ru = 0;
-        if (++rv == ny) rv = 0;
-      }
-    }
-  };
-#pragma unroll
-  for (int s0 = 0; s0 < (R_REGS ? PD : RING - 1); ++s0) issue(s0, s0);
-  __syncthreads();
-  bool ok = true;
-  const int last_out = nrows + 2 * S;  // outputs are iterations [2S, nrows+2S)
-  for (int i0 = 0; i0 < n_iter; i0 += UNROLL) {
-#pragma unroll
-    for (int k = 0; k < UNROLL; ++k) {
-      const int i = i0 + k;
-      cp_async_wait<RING - 2>();
-      const double* src = ring + ((k % RING) * 3) * W + j;
-      const double uu0 = src[0], v0 = src[W], k0 = src[2 * W];
-      issue((k + RING - 1) % RING);
-      double out_u, out_v;
-      if (k & 1)
-        wave_iter<S, EXACT, 1>(sbase, sstride_par, p, ulo, uce, vin, kin, ain, uu0, v0, k0, out_u, out_v);
-      else
-        wave_iter<S, EXACT, 0>(sbase, sstride_par, p, ulo, uce, vin, kin, ain, uu0, v0, k0, out_u, out_v);
-      if (col_out && i >= 2 * S && i < last_out) {
-        UO[oo] = out_u;
-        VO[oo] = out_v;
-        ok &= finite2(out_u, out_v);
-      }
-      adv(oo);
-      __syncthreads();
-    }
-  }
-  cp_async_wait<0>();
-  if (a.flags) {
-    const int bad = __syncthreads_or(!ok);
-    if (bad && j == 0) atomicOr(&a.flags[blockIdx.x], 1);
-  }
-}
-
-// ------------------------------------------------------------------ k_wave2 (FAST, 2 columns/thread)
-//
-// Same wavefront as k_wave, but every thread owns the column PAIR (2j, 2j+1): the x-neighbours
-// inside the pair stay in registers and only the pair's edge values go through shared memory
-// (separate left-edge / right-edge rows, conflict-free 8-byte accesses), halving crossbar
-// traffic per update.  Level-0 inputs stream as 16-byte cp.async pairs, outputs are 16-byte
-// stores.  Requires even nx (pairs never straddle the periodic wrap); the strip halo is the
-// even HXE = S + 2 columns per side.  Arithmetic identical to k_wave/k_small FAST.
-
-template <bool CG = false>
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  if constexpr (CG)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
-}
-// 16-byte streaming load (read-only path, no L1 allocation)
-__device__ __forceinline__ double2 ldg_stream2(const double* p) {
-  double2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(r.x), "=d"(r.y) : "l"(p));
-  return r;
-}
-// bulk-copy issuers per CTA for k_wave2's ring variants 2 (one) and 3 (one per warp)
-template <int RINGV, int T>
-constexpr int RING_ISSUERS = RINGV == 3 ? T / 32 : 1;
-
-template <int S, int W, int PAR, bool RY1>
-__device__ __forceinline__ void wave2_iter(double* __restrict__ eL, double* __restrict__ eR, const int offl,
-                                           const int offr,
-                                           const StepParams& p, double (&ulo)[S + 1][2], double (&uce)[S + 1][2],
-                                           double (&vin)[S + 1][2], double (&kin)[S + 1][2], const double2 uu0,
-                                           const double2 v0, const double2 k0, double2& out_u, double2& out_v) {
-  // edge rows: eL/eR + parity*pstride + level*lstride + j (+1 padding)
-  constexpr int lstride = W + 2, pstride = (S + 1) * lstride;
-  const double* __restrict__ rL = eL + PAR * pstride;
-  const double* __restrict__ rR = eR + PAR * pstride;
-  double* __restrict__ wL = eL + (PAR ^ 1) * pstride;
-  double* __restrict__ wR = eR + (PAR ^ 1) * pstride;
-  double nl[S + 1], nr[S + 1];  // left neighbour of col 0, right neighbour of col 1, per level
-#pragma unroll
-  for (int t = 0; t <= S; ++t) {
-    nl[t] = rR[t * lstride + offl];
-    nr[t] = rL[t * lstride + offr];
-  }
-  double up0, up1, cv0, cv1, ck0, ck1;
-  {
-    const double uc0 = uce[0][0], uc1 = uce[0][1];
-    wL[0] = uu0.x;
-    wR[0] = uu0.y;
-    const double vh0 = v0.x + bfast2<RY1>(uc0, nl[0], uc1, uu0.x, ulo[0][0], k0.x, p);
-    const double vh1 = v0.y + bfast2<RY1>(uc1, uc0, nr[0], uu0.y, ulo[0][1], k0.y, p);
-    up0 = fma(p.dt, vh0, uc0);
-    up1 = fma(p.dt, vh1, uc1);
-    cv0 = vh0;
-    cv1 = vh1;
-    ck0 = k0.x;
-    ck1 = k0.y;
-    wL[lstride] = up0;
-    wR[lstride] = up1;
-    ulo[0][0] = uc0;
-    ulo[0][1] = uc1;
-    uce[0][0] = uu0.x;
-    uce[0][1] = uu0.y;
-  }
-  // parts of b independent of the level below: b = fma(K ry, uu, K (cc uc + ry ud + (ul + ur)))
-  double q0[S + 1], q1[S + 1];
-#pragma unroll
-  for (int t = 1; t <= S; ++t) {
-    if (RY1) {
-      q0[t] = kin[t][0] * fma(p.cc, uce[t][0], ulo[t][0] + (nl[t] + uce[t][1]));
-      q1[t] = kin[t][1] * fma(p.cc, uce[t][1], ulo[t][1] + (uce[t][0] + nr[t]));
-    } else {
-      q0[t] = kin[t][0] * fma(p.cc, uce[t][0], fma(p.ry, ulo[t][0], nl[t] + uce[t][1]));
-      q1[t] = kin[t][1] * fma(p.cc, uce[t][1], fma(p.ry, ulo[t][1], uce[t][0] + nr[t]));
-    }
-  }
-#pragma unroll
-  for (int t = 1; t <= S; ++t) {
-    const double vp0 = vin[t][0], vp1 = vin[t][1], k0t = kin[t][0], k1t = kin[t][1];
-    vin[t][0] = cv0;
-    vin[t][1] = cv1;
-    kin[t][0] = ck0;
-    kin[t][1] = ck1;
-    const double uu_0 = up0, uu_1 = up1;
-    const double uc0 = uce[t][0], uc1 = uce[t][1];
-    const double b0 = fma(RY1 ? k0t : k0t * p.ry, uu_0, q0[t]);
-    const double b1 = fma(RY1 ? k1t : k1t * p.ry, uu_1, q1[t]);
-    if (t < S) {
-      const double vh0 = (vp0 + b0) + b0;
-      const double vh1 = (vp1 + b1) + b1;
-      up0 = fma(p.dt, vh0, uc0);
-      up1 = fma(p.dt, vh1, uc1);
-      cv0 = vh0;
-      cv1 = vh1;
-      ck0 = k0t;
-      ck1 = k1t;
-      wL[(t + 1) * lstride] = up0;
-      wR[(t + 1) * lstride] = up1;
-    } else {
-      out_u = make_double2(uc0, uc1);
-      out_v = make_double2(vp0 + b0, vp1 + b1);
-    }
-    ulo[t][0] = uc0;
-    ulo[t][1] = uc1;
-    uce[t][0] = uu_0;
-    uce[t][1] = uu_1;
-  }
-}
-
-// VAR: bit 0 = FULL (one strip spans the periodic row), bit 1 = RY1 (hy == hx)
-template <int S, int W, int VAR>
-__global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
-  constexpr bool FULL = VAR & 1, RY1 = (VAR & 2) != 0;
-  // even halo >= S + 1 (16-byte aligned pairs); none when the strip is the whole periodic row
-  constexpr int HXE = FULL ? 0 : (S + 3) & ~1;
-  constexpr int NL = S + 1;
-  constexpr int UNROLL = 6, RING = 6;
-  extern __shared__ double sm[];
-  constexpr int T = W;
-  const int j = threadIdx.x;
-  // x-neighbour offsets into the edge rows: the left neighbour of column 2j is thread j-1's
-  // right edge, the right neighbour of column 2j+1 thread j+1's left edge; a full-width strip
-  // wraps them inside the CTA (thread 0 <-> thread W-1) instead of through halo columns
-  const int offl = FULL && j == 0 ? W - 1 : -1;
-  const int offr = FULL && j == W - 1 ? -(W - 1) : 1;
-  const int nx = a.p.nx, ny = a.p.ny;
-  const int npts = nx * ny;
-  const int rnx = a.rnx ? a.rnx : nx, rny = a.rnx ? a.rny : ny;  // output rectangle
-  const int x0 = a.rx0 + blockIdx.y * a.wu;  // even
-  int gx = (x0 - HXE + 2 * j) % nx;
-  if (gx < 0) gx += nx;
-  const int Y0 = a.ry0 + blockIdx.z * a.rb;
-  const int nrows = min(a.rb, a.ry0 + rny - Y0);
-  const int ystart = Y0 - S;
-  const int n_iter = ((nrows + 2 * S + UNROLL - 1) / UNROLL) * UNROLL;
-  const int oc = 2 * j - HXE;  // output column offset of col 0 within the strip
-  const bool col_out = oc >= 0 && 2 * j + 1 < 2 * T - HXE && oc < a.wu && x0 + oc < a.rx0 + rnx;
-  const size_t off = static_cast<size_t>(blockIdx.x) * a.stride;
-  const double* __restrict__ U = a.u_in + off;
-  const double* __restrict__ V = a.v_in + off;
-  double* __restrict__ UO = a.u_out + off;
-  double* __restrict__ VO = a.v_out + off;
-  const double* __restrict__ K = a.coef;
-  const StepParams p = a.p;
-  // shared: edges [2 parity][NL][T+2] for L and R, then ring [RING][3][T] double2
-  constexpr int pstride = NL * (T + 2);
-  double* eL = sm + 1 + j;  // +1: pad so j-1 >= 0
-  double* eR = sm + 2 * pstride + 1 + j;
-  double2* ring = reinterpret_cast<double2*>(sm + 4 * pstride);
-  auto wrap = [&](int y) -> int {
-    int r = y % ny;
-    if (r < 0) r += ny;
-    return r * nx + gx;
-  };
-  double ulo[NL][2], uce[NL][2], vin[NL][2], kin[NL][2];
-#pragma unroll
-  for (int t = 0; t < NL; ++t)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) ulo[t][c] = uce[t][c] = vin[t][c] = kin[t][c] = 0.0;
-  {
-    const double2 lo = *reinterpret_cast<const double2*>(U + wrap(ystart - 1));
-    const double2 ce = *reinterpret_cast<const double2*>(U + wrap(ystart));
-    ulo[0][0] = lo.x;
-    ulo[0][1] = lo.y;
-    uce[0][0] = ce.x;
-    uce[0][1] = ce.y;
-    eL[0] = ce.x;  // parity 0, level 0
-    eR[0] = ce.y;
-  }
-  int ou = wrap(ystart + 1), ov = wrap(ystart), oo = wrap(ystart - S);
-  auto adv = [npts, nx](int& o) {
-    o += nx;
-    if (o >= npts) o -= npts;
-  };
 #if PTB_WAVE2_RING <= 1
   auto issue = [&](int slot, int) {
     double2* d = ring + (slot * 3) * T + j;
@@ -1210,19 +927,19 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
 #pragma unroll
     for (int k = 0; k < UNROLL; ++k) {
       const int i = i0 + k;
-      double2 uu0, v0, k0;
-      if constexpr (R_REGS) {
-        uu0 = pu[k % PD], v0 = pv[k % PD], k0 = pk[k % PD];
-        issue(k % PD, i + PD);
-      } else {
-        if constexpr (R_ASYNC)
-          cp_async_wait<RING - 2>();
-        else
-          mbar_wait(smem_addr(&bars[k * NW + wid]), unsigned(i0 / UNROLL) & 1u);
-        const double2* src = ring + ((k % RING) * 3) * T + j;
-        uu0 = src[0], v0 = src[T], k0 = src[2 * T];
-        issue((k + RING - 1) % RING, i + RING - 1);
-      }
+#if PTB_WAVE2_RING >= 4
+      const double2 uu0 = pu[k % PD], v0 = pv[k % PD], k0 = pk[k % PD];
+      issue(k % PD, i + PD);
+#else
+#if PTB_WAVE2_RING <= 1
+      cp_async_wait<RING - 2>();
+#else
+      mbar_wait(smem_addr(&bars[k * NW + wid]), unsigned(i0 / UNROLL) & 1u);
+#endif
+      const double2* src = ring + ((k % RING) * 3) * T + j;
+      const double2 uu0 = src[0], v0 = src[T], k0 = src[2 * T];
+      issue((k + RING - 1) % RING, i + RING - 1);
+#endif
       double2 out_u, out_v;
       if (k & 1)
         wave2_iter<S, W, 1, RY1>(eL, eR, offl, offr, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
@@ -1237,7 +954,9 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
       __syncthreads();
     }
   }
-  if constexpr (R_ASYNC) cp_async_wait<0>();
+#if PTB_WAVE2_RING <= 1
+  cp_async_wait<0>();
+#endif
   if (a.flags) {
     const int bad = __syncthreads_or(!ok);
     if (bad && j == 0) atomicOr(&a.flags[blockIdx.x], 1);
@@ -1425,7 +1144,7 @@ void launch_wave(ptb_context* ctx, cudaStream_t st, const WavePlan& pl, WaveArgs
 size_t wave2_smem(int S, int W) {
   // edges [L,R][2 parity][S+1][W+2], ring [6][3][2W], ring mbarriers (bulk variants)
   return (size_t(4) * (S + 1) * (W + 2) + size_t(6) * 3 * 2 * W) * sizeof(double) +
-         size_t(6) * (W / 32 + 1) * sizeof(uint64_t);
+         (PTB_WAVE2_RING >= 2 ? size_t(6) * (W / 32 + 1) * sizeof(uint64_t) : 0);
 }
 
 // strip widths (threads) k_wave2 is instantiated for; each thread covers 2 columns
