@@ -117,6 +117,9 @@ ptb_status ptb_context_destroy(ptb_context* ctx) {
       for (auto& b : slot) b.release();
     for (auto& st : ctx->aux)
       if (st) cudaStreamDestroy(st);
+    if (ctx->lane) cudaStreamDestroy(ctx->lane);
+    if (ctx->lane_fork) cudaEventDestroy(ctx->lane_fork);
+    if (ctx->lane_join) cudaEventDestroy(ctx->lane_join);
     ctx->flags.release();
     ctx->driver_cache.reset();  // parareal work buffers
     if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);

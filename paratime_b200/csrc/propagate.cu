@@ -54,6 +54,11 @@
 #ifndef PTB_WAVE2_RING
 #define PTB_WAVE2_RING 0
 #endif
+// full-row strips of at least this many threads take the bulk-copy ring (variant 2) instead:
+// 512^2 x 64 (W = 256) 7.0 -> 7.7e11 updates/s; narrower full-row strips and haloed strips lose
+#ifndef PTB_WAVE2_BULK_FROM
+#define PTB_WAVE2_BULK_FROM 256
+#endif
 
 namespace ptb {
 
@@ -847,50 +852,38 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
     o += nx;
     if (o >= npts) o -= npts;
   };
-#if PTB_WAVE2_RING <= 1
-  auto issue = [&](int slot, int) {
-    double2* d = ring + (slot * 3) * T + j;
-    cp_async16<PTB_WAVE2_RING == 1>(d, U + ou);
-    cp_async16<PTB_WAVE2_RING == 1>(d + T, V + ov);
-    cp_async16<PTB_WAVE2_RING == 1>(d + 2 * T, K + ov);
-    cp_async_commit();
-    adv(ou);
-    adv(ov);
-  };
-#elif PTB_WAVE2_RING >= 4
-  // level-0 inputs straight into registers, PD rows ahead (no shared-memory ring)
-  constexpr int PD = PTB_WAVE2_RING - 2;
-  double2 pu[PD], pv[PD], pk[PD];
-  auto issue = [&](int slot, int) {
-    pu[slot] = ldg_stream2(U + ou);
-    pv[slot] = ldg_stream2(V + ov);
-    pk[slot] = ldg_stream2(K + ov);
-    adv(ou);
-    adv(ov);
-  };
-#else
-  // Level-0 rows arrive by bulk copies (the TMA engine, cp.async.bulk) that complete on an
+  // ring variant of this instantiation (see the top of the file): the bulk-copy ring pays on wide
+  // full-row strips only (one aligned copy per row for 8 warps), cp.async everywhere else
+  constexpr int RINGV = (FULL && W >= PTB_WAVE2_BULK_FROM && PTB_WAVE2_RING <= 1) ? 2 : PTB_WAVE2_RING;
+  constexpr bool R_ASYNC = RINGV <= 1, R_REGS = RINGV >= 4, R_BULK = !R_ASYNC && !R_REGS;
+  // R_REGS: level-0 inputs straight into registers, PD rows ahead (no shared-memory ring)
+  constexpr int PD = R_REGS ? RINGV - 2 : 1;
+  [[maybe_unused]] double2 pu[PD], pv[PD], pk[PD];
+  // R_BULK: level-0 rows arrive by bulk copies (the TMA engine, cp.async.bulk) that complete on an
   // mbarrier; every thread waits on the barrier's phase and reads its pair from the slot.
   //   RING 2: one thread moves the CTA's three row segments (2W doubles each, split where the strip
   //           wraps the periodic x boundary), one barrier per slot;
   //   RING 3: lane 0 of each warp moves the warp's 64-column segments, one barrier per slot and warp
   //           (no cross-warp dependency: a warp only waits for its own bytes).
-  constexpr int NW = RING_ISSUERS<PTB_WAVE2_RING, T>;
+  constexpr int NW = RING_ISSUERS<RINGV, T>;
   constexpr int SEG = 2 * T / NW;  // doubles per issuer and row
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RING * 3 * T);
-  const int wid = PTB_WAVE2_RING == 3 ? (j >> 5) : 0;
-  const bool issuer = PTB_WAVE2_RING == 3 ? (j & 31) == 0 : j == 0;
-  const int gx0 = ((FULL ? 0 : ((x0 - HXE) % nx + nx) % nx) + SEG * wid) % nx;  // first column of the segment
-  int ru = 0, rv = 0;  // next u row / udot,coef row (issuers)
-  if (issuer) {
-    ru = ((ystart + 1) % ny + ny) % ny;
-    rv = ((ystart) % ny + ny) % ny;
+  [[maybe_unused]] uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RING * 3 * T);
+  [[maybe_unused]] const int wid = RINGV == 3 ? (j >> 5) : 0;
+  [[maybe_unused]] const bool issuer = RINGV == 3 ? (j & 31) == 0 : j == 0;
+  // first column of the issuer's segment
+  [[maybe_unused]] const int gx0 = ((FULL ? 0 : ((x0 - HXE) % nx + nx) % nx) + SEG * wid) % nx;
+  [[maybe_unused]] int ru = 0, rv = 0;  // next u row / udot,coef row (issuers)
+  if constexpr (R_BULK) {
+    if (issuer) {
+      ru = ((ystart + 1) % ny + ny) % ny;
+      rv = ((ystart) % ny + ny) % ny;
 #pragma unroll
-    for (int s0 = 0; s0 < RING; ++s0) mbar_init(smem_addr(&bars[s0 * NW + wid]), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      for (int s0 = 0; s0 < RING; ++s0) mbar_init(smem_addr(&bars[s0 * NW + wid]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  auto copy_row = [&](double* dst, const double* row, unsigned bar) {
+  [[maybe_unused]] auto copy_row = [&](double* dst, const double* row, unsigned bar) {
     int col = gx0, rem = SEG;
     while (rem > 0) {
       const int len = min(rem, nx - col);
@@ -900,26 +893,36 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
       col = 0;
     }
   };
-  auto issue = [&](int slot, int iter) {
-    if (issuer && iter < n_iter) {
-      const unsigned bar = smem_addr(&bars[slot * NW + wid]);
-      mbar_expect(bar, unsigned(3 * SEG) * 8u);
-      double* d = reinterpret_cast<double*>(ring + (slot * 3) * T) + SEG * wid;
-      copy_row(d, U + size_t(ru) * nx, bar);
-      copy_row(d + 2 * T, V + size_t(rv) * nx, bar);
-      copy_row(d + 4 * T, K + size_t(rv) * nx, bar);
-      if (++ru == ny) ru = 0;
-      if (++rv == ny) rv = 0;
+  auto issue = [&](int slot, [[maybe_unused]] int iter) {
+    if constexpr (R_ASYNC) {
+      double2* d = ring + (slot * 3) * T + j;
+      cp_async16<RINGV == 1>(d, U + ou);
+      cp_async16<RINGV == 1>(d + T, V + ov);
+      cp_async16<RINGV == 1>(d + 2 * T, K + ov);
+      cp_async_commit();
+      adv(ou);
+      adv(ov);
+    } else if constexpr (R_REGS) {
+      pu[slot] = ldg_stream2(U + ou);
+      pv[slot] = ldg_stream2(V + ov);
+      pk[slot] = ldg_stream2(K + ov);
+      adv(ou);
+      adv(ov);
+    } else {
+      if (issuer && iter < n_iter) {
+        const unsigned bar = smem_addr(&bars[slot * NW + wid]);
+        mbar_expect(bar, unsigned(3 * SEG) * 8u);
+        double* d = reinterpret_cast<double*>(ring + (slot * 3) * T) + SEG * wid;
+        copy_row(d, U + size_t(ru) * nx, bar);
+        copy_row(d + 2 * T, V + size_t(rv) * nx, bar);
+        copy_row(d + 4 * T, K + size_t(rv) * nx, bar);
+        if (++ru == ny) ru = 0;
+        if (++rv == ny) rv = 0;
+      }
     }
   };
-#endif
-#if PTB_WAVE2_RING >= 4
 #pragma unroll
-  for (int s0 = 0; s0 < PD; ++s0) issue(s0, s0);
-#else
-#pragma unroll
-  for (int s0 = 0; s0 < RING - 1; ++s0) issue(s0, s0);
-#endif
+  for (int s0 = 0; s0 < (R_REGS ? PD : RING - 1); ++s0) issue(s0, s0);
   __syncthreads();
   bool ok = true;
   const int last_out = nrows + 2 * S;
@@ -927,19 +930,19 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
 #pragma unroll
     for (int k = 0; k < UNROLL; ++k) {
       const int i = i0 + k;
-#if PTB_WAVE2_RING >= 4
-      const double2 uu0 = pu[k % PD], v0 = pv[k % PD], k0 = pk[k % PD];
-      issue(k % PD, i + PD);
-#else
-#if PTB_WAVE2_RING <= 1
-      cp_async_wait<RING - 2>();
-#else
-      mbar_wait(smem_addr(&bars[k * NW + wid]), unsigned(i0 / UNROLL) & 1u);
-#endif
-      const double2* src = ring + ((k % RING) * 3) * T + j;
-      const double2 uu0 = src[0], v0 = src[T], k0 = src[2 * T];
-      issue((k + RING - 1) % RING, i + RING - 1);
-#endif
+      double2 uu0, v0, k0;
+      if constexpr (R_REGS) {
+        uu0 = pu[k % PD], v0 = pv[k % PD], k0 = pk[k % PD];
+        issue(k % PD, i + PD);
+      } else {
+        if constexpr (R_ASYNC)
+          cp_async_wait<RING - 2>();
+        else
+          mbar_wait(smem_addr(&bars[k * NW + wid]), unsigned(i0 / UNROLL) & 1u);
+        const double2* src = ring + ((k % RING) * 3) * T + j;
+        uu0 = src[0], v0 = src[T], k0 = src[2 * T];
+        issue((k + RING - 1) % RING, i + RING - 1);
+      }
       double2 out_u, out_v;
       if (k & 1)
         wave2_iter<S, W, 1, RY1>(eL, eR, offl, offr, p, ulo, uce, vin, kin, uu0, v0, k0, out_u, out_v);
@@ -954,9 +957,7 @@ __global__ void __launch_bounds__(W, 1) k_wave2(const WaveArgs a) {
       __syncthreads();
     }
   }
-#if PTB_WAVE2_RING <= 1
-  cp_async_wait<0>();
-#endif
+  if constexpr (R_ASYNC) cp_async_wait<0>();
   if (a.flags) {
     const int bad = __syncthreads_or(!ok);
     if (bad && j == 0) atomicOr(&a.flags[blockIdx.x], 1);
@@ -1144,7 +1145,7 @@ void launch_wave(ptb_context* ctx, cudaStream_t st, const WavePlan& pl, WaveArgs
 size_t wave2_smem(int S, int W) {
   // edges [L,R][2 parity][S+1][W+2], ring [6][3][2W], ring mbarriers (bulk variants)
   return (size_t(4) * (S + 1) * (W + 2) + size_t(6) * 3 * 2 * W) * sizeof(double) +
-         (PTB_WAVE2_RING >= 2 ? size_t(6) * (W / 32 + 1) * sizeof(uint64_t) : 0);
+         size_t(6) * (W / 32 + 1) * sizeof(uint64_t);
 }
 
 // strip widths (threads) k_wave2 is instantiated for; each thread covers 2 columns
@@ -1289,6 +1290,24 @@ void wave_pass(ptb_context* ctx, cudaStream_t st, int S, const StepParams& p, si
   }
 }
 
+// two-lane chunk loop of wave_propagate: PTB_LANES=0 turns it off, PTB_LANE_MIN_POINTS sets the
+// smallest batch x grid size that takes it (default 2^22 points:
+// 256^2 x 64 slices +10 %, 512^2 / 1024^2 x 64 +4 %, 2048^2 x 64..128 +3 %, 4096^2 x 512 +1 %)
+bool lanes_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PTB_LANES");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+size_t lane_min_points() {
+  static const size_t v = [] {
+    const char* e = std::getenv("PTB_LANE_MIN_POINTS");
+    return e && std::atoll(e) > 0 ? size_t(std::atoll(e)) : size_t(1) << 22;
+  }();
+  return v;
+}
+
 // slices per ping-pong chunk of the context scratch (see wave_propagate)
 size_t scratch_chunk(size_t n, size_t batch) {
   static const size_t cap = [] {
@@ -1296,6 +1315,14 @@ size_t scratch_chunk(size_t n, size_t batch) {
     return (e && std::atoll(e) > 0 ? size_t(std::atoll(e)) : size_t(16384)) << 20;
   }();
   return std::min(batch, std::max<size_t>(1, cap / (2 * n * sizeof(double))));
+}
+
+// slices per launch of wave_propagate on the context scratch, and whether the chunks alternate
+// between two lanes (each lane owns half of the scratch)
+size_t lane_chunk(size_t n, size_t batch, bool& lanes) {
+  const size_t chunk0 = scratch_chunk(n, batch);
+  lanes = lanes_enabled() && batch >= 4 && batch * n >= lane_min_points();
+  return lanes ? std::max<size_t>(1, std::min((batch + 1) / 2, chunk0 / 2)) : chunk0;
 }
 
 template <bool EXACT>
@@ -1316,28 +1343,54 @@ void wave_propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, d
   // its own slices and the shared scratch, so a batch can use ~all of HBM for its state (cfg5
   // 4096^2 x 512 slices: 137 GB of state + 17 GB of scratch).  A slice's arithmetic does not
   // depend on the plan, so chunking never changes results.
-  const size_t chunk = slot.su ? batch : scratch_chunk(n, batch);
-  double* su = slot.su ? slot.su : static_cast<double*>(ctx->scratch[0].get(chunk * n * sizeof(double)));
-  double* sv = slot.sv ? slot.sv : static_cast<double*>(ctx->scratch[1].get(chunk * n * sizeof(double)));
-  for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+  // Two lanes: with the context scratch and enough work, alternate chunks run on the caller's
+  // stream and on the context's lane stream, each lane ping-ponging into its own half of the
+  // scratch.  A pass is a few rounds of long-running CTAs (4096^2: ~3 ms each), so a single
+  // in-order stream idles SMs through every pass's last partial round; the other lane's CTAs fill
+  // them (fork/join by events: the caller's stream still orders the whole call).
+  bool lanes = false;
+  const size_t chunk = slot.su ? batch : lane_chunk(n, batch, lanes);
+  const size_t lane_stride = chunk * n;
+  double* su = slot.su ? slot.su : static_cast<double*>(ctx->scratch[0].get((lanes ? 2 : 1) * lane_stride * sizeof(double)));
+  double* sv = slot.sv ? slot.sv : static_cast<double*>(ctx->scratch[1].get((lanes ? 2 : 1) * lane_stride * sizeof(double)));
+  cudaStream_t st[2] = {slot.stream, slot.stream};
+  if (lanes) {
+    if (!ctx->lane) {
+      PTB_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->lane, cudaStreamNonBlocking));
+      PTB_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_fork, cudaEventDisableTiming));
+      PTB_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_join, cudaEventDisableTiming));
+    }
+    st[1] = ctx->lane;
+    PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_fork, slot.stream));
+    PTB_CUDA_CHECK(cudaStreamWaitEvent(ctx->lane, ctx->lane_fork, 0));
+  }
+  size_t ci_ = 0;
+  for (size_t b0 = 0; b0 < batch; b0 += chunk, ++ci_) {
     const size_t nb = std::min(chunk, batch - b0);
+    const int lane = lanes ? int(ci_ & 1) : 0;
+    double* lu = su + lane * lane_stride;
+    double* lv = sv + lane * lane_stride;
     double* hu = u + b0 * n;
     double* hv = v + b0 * n;
     const double *ci = hu, *cvi = hv;
     for (size_t k = 0; k < passes.size(); ++k) {
       const bool to_scratch = (k % 2) == 0;
-      double* uo = to_scratch ? su : hu;
-      double* vo = to_scratch ? sv : hv;
-      wave_pass<EXACT>(ctx, slot.stream, passes[k], p, nb, ci, cvi, uo, vo, coef,
+      double* uo = to_scratch ? lu : hu;
+      double* vo = to_scratch ? lv : hv;
+      wave_pass<EXACT>(ctx, st[lane], passes[k], p, nb, ci, cvi, uo, vo, coef,
                        k + 1 == passes.size() && flags ? flags + b0 : nullptr);
       ci = uo;
       cvi = vo;
     }
     if (ci != hu) {
       const size_t total = nb * n;
-      k_copy2<<<grid_for(ctx, total, 256), 256, 0, slot.stream>>>(total, su, sv, hu, hv);
+      k_copy2<<<grid_for(ctx, total, 256), 256, 0, st[lane]>>>(total, lu, lv, hu, hv);
       PTB_LAUNCH_CHECK(ctx);
     }
+  }
+  if (lanes) {
+    PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_join, ctx->lane));
+    PTB_CUDA_CHECK(cudaStreamWaitEvent(slot.stream, ctx->lane_join, 0));
   }
 }
 
@@ -1437,7 +1490,8 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
            std::to_string(CL_THREADS) + " threads per slice";
   if (p.dim != 2) return std::string("k_stream_drift/kick<") + m + "> 2 launches per step";
   const size_t full_batch = batch;
-  batch = scratch_chunk(pr->n, batch);
+  bool lanes = false;
+  batch = lane_chunk(pr->n, batch, lanes);
   std::string out;
   size_t rem = steps;
   int passes = 0;
@@ -1468,7 +1522,7 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
   if (passes % 2) out += " + k_copy2";
   if (batch < full_batch)
     out = "(" + out + ") per chunk of " + std::to_string(batch) + " slices x " +
-          std::to_string((full_batch + batch - 1) / batch);
+          std::to_string((full_batch + batch - 1) / batch) + (lanes ? " on two lanes" : "");
   return out;
 }
 

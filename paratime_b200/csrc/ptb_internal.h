@@ -151,6 +151,11 @@ struct ptb_context {
   // host-batch pipeline: three streams/slots so the H2D of chunk i+1, the propagation of chunk i
   // and the D2H of chunk i-1 overlap (separate copy engines for the two directions)
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+  // second lane of the wavefront propagator's chunk loop (propagate.cu wave_propagate): alternate
+  // chunks run on `stream` and `lane`, so one chunk's last partial round of CTAs overlaps the
+  // other's next pass; forked from / joined to `stream` with these events
+  cudaStream_t lane = nullptr;
+  cudaEvent_t lane_fork = nullptr, lane_join = nullptr;
   ptb::DeviceBuffer slotbuf[3][5];  // per pipeline slot: u, v, su, sv, flags
   // pinned staging for the per-slice flags of the host-batch call: a D2H copy into pageable
   // memory is synchronous and would serialise the pipeline
