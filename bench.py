@@ -524,13 +524,14 @@ def measure_e2e(B, prop, host, mode, steps, local, dist, world):
 
 def sweep(B, ctx, mode, tflops_peak, hbm_peak):
     """cfg5 grid sweep (the >= 60 % target is judged on every cfg5 grid at batch >= 64):
-    device-resident, FAST, 64 steps per slice, batch 64.  Per grid: updates/s, the launch plan,
+    device-resident, FAST, 64 steps per slice, batch 64 (and 512 on the grids below 2048^2).  Per grid: updates/s, the launch plan,
     and the binding-roofline fraction max(upd/s*17/FP64, upd/s*(40/s_f)/HBM) with s_f the steps
     fused per HBM round trip of the plan (64 for the on-chip k_cluster, 8 per wavefront pass)."""
     import torch
 
     out = []
-    for n, batch in ((128, 64), (128, 512), (256, 64), (512, 64), (1024, 64), (2048, 64), (4096, 64)):
+    for n, batch in ((128, 64), (128, 512), (256, 64), (512, 64), (512, 512), (1024, 64), (1024, 512), (2048, 64),
+                     (4096, 64)):
         c = cfg5_medium(n)
         dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
         prop = B.Propagator(ctx, B.Grid((n, n), (1.0 / n, 1.0 / n)), c, dt, STEPS_PER_COUPLING)

@@ -491,6 +491,7 @@ struct WaveArgs {
   // k_wave2 output rectangle (rows [ry0, ry0 + rny), columns [rx0, rx0 + rnx)); inputs are read
   // with the periodic wrap of the whole ny x nx slice.  Default (rnx = 0): the whole slice.
   int ry0 = 0, rny = 0, rx0 = 0, rnx = 0;
+  int lanes = 0;  // host-side planning hint: launched from the two-lane chunk loop
 };
 
 // One iteration of the wavefront: level 0 loads row r0 = ystart+i (+ look-ahead row), levels
@@ -1182,10 +1183,11 @@ inline int wave2_variant(const StepParams& p, int full) {
 }
 
 template <int S>
-WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch, bool no_full = false) {
+WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch, bool no_full = false, bool lanes = false) {
   const int HXE = (S + 3) & ~1;
   WavePlan best{};
   double best_cost = 1e300;
+  size_t best_slots = 0;
   int forceW = 0;
   if (const char* e = std::getenv("PTB_WAVE_W"); e && std::atoi(e) > 0) forceW = std::atoi(e);
   static const int full_env = [] {
@@ -1226,11 +1228,26 @@ WavePlan plan_wave2(ptb_context* ctx, int ny, int nx, size_t batch, bool no_full
       if (cost < best_cost) {
         best_cost = cost;
         best = WavePlan{W, wu, strips, rb, nrb, full};
+        best_slots = slots;
       }
       if (rb <= 1) break;
     }
   }
   if (best.W == 0) fail(PTB_UNSUPPORTED, "k_wave2: no feasible strip width");
+  // Two-lane chunk loop (wave_propagate): the other lane's CTAs fill a pass's partial last round, so
+  // the rounds need no balancing by extra row blocks — each costs 2S warm-up rows.  Keep the strip
+  // width and take the fewest row blocks that still give the launch ~one full round of CTAs
+  // (measured, scripts/sweep_div.py: 1024^2 x 64 0.74 -> 0.80e12, 512^2 x 512 0.86 -> 0.94e12).
+  if (lanes) {
+    for (int div = 1; div <= best.nrb; ++div) {
+      const int rb = (ny + div - 1) / div, nrb = (ny + rb - 1) / rb;
+      if (size_t(best.strips) * nrb * batch * 20 >= best_slots * 17 || nrb >= best.nrb) {
+        best.rb = rb;
+        best.nrb = nrb;
+        break;
+      }
+    }
+  }
   if (const char* e = std::getenv("PTB_WAVE_DIV"); e && std::atoi(e) > 0) {
     const int div = std::atoi(e);
     best.rb = (ny + div - 1) / div;
@@ -1244,7 +1261,7 @@ void launch_wave2(ptb_context* ctx, cudaStream_t st, WaveArgs a, size_t batch) {
   // a rectangle narrower than the row is covered by haloed strips (full-row needs rnx == nx)
   const bool rect = a.rnx != 0;
   const WavePlan pl = plan_wave2<S>(ctx, rect ? a.rny : a.p.ny, rect ? a.rnx : a.p.nx, batch,
-                                    rect && a.rnx != a.p.nx);
+                                    rect && a.rnx != a.p.nx, a.lanes != 0);
   const size_t smem = wave2_smem(S, pl.W);
   a.wu = pl.wu;
   a.rb = pl.rb;
@@ -1267,8 +1284,9 @@ bool use_wave2(const StepParams& p) {
 
 template <bool EXACT>
 void wave_pass(ptb_context* ctx, cudaStream_t st, int S, const StepParams& p, size_t batch, const double* ui,
-               const double* vi, double* uo, double* vo, const double* coef, int32_t* flags) {
+               const double* vi, double* uo, double* vo, const double* coef, int32_t* flags, bool lanes) {
   WaveArgs a{p, ui, vi, uo, vo, coef, size_t(p.ny) * p.nx, 0, 0, flags};
+  a.lanes = lanes ? 1 : 0;
   if constexpr (!EXACT) {
     if (use_wave2(p)) {
       switch (S) {
@@ -1378,7 +1396,7 @@ void wave_propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, d
       double* uo = to_scratch ? lu : hu;
       double* vo = to_scratch ? lv : hv;
       wave_pass<EXACT>(ctx, st[lane], passes[k], p, nb, ci, cvi, uo, vo, coef,
-                       k + 1 == passes.size() && flags ? flags + b0 : nullptr);
+                       k + 1 == passes.size() && flags ? flags + b0 : nullptr, lanes);
       ci = uo;
       cvi = vo;
     }
@@ -1504,10 +1522,10 @@ std::string describe_plan(ptb_propagator* pr, size_t steps, size_t batch, int mo
     if (!exact && use_wave2(p)) {
       WavePlan pl;
       switch (S) {
-        case 8: pl = plan_wave2<8>(pr->ctx, p.ny, p.nx, batch); break;
-        case 4: pl = plan_wave2<4>(pr->ctx, p.ny, p.nx, batch); break;
-        case 2: pl = plan_wave2<2>(pr->ctx, p.ny, p.nx, batch); break;
-        default: pl = plan_wave2<1>(pr->ctx, p.ny, p.nx, batch); break;
+        case 8: pl = plan_wave2<8>(pr->ctx, p.ny, p.nx, batch, false, lanes); break;
+        case 4: pl = plan_wave2<4>(pr->ctx, p.ny, p.nx, batch, false, lanes); break;
+        case 2: pl = plan_wave2<2>(pr->ctx, p.ny, p.nx, batch, false, lanes); break;
+        default: pl = plan_wave2<1>(pr->ctx, p.ny, p.nx, batch, false, lanes); break;
       }
       d = "k_wave2<" + std::to_string(S) + "," + std::to_string(pl.W) + ">" + (pl.full ? " full-row" : "") +
           ((wave2_variant(p, pl.full) & 2) ? " ry1" : "");

@@ -4,7 +4,8 @@ import torch
 import paratime_b200 as B
 from workloads import cfg5_medium, cfg5_pulses
 ctx = B.Context(0)
-for n, batch in [(1024, 64), (256, 64), (512, 64)]:
+cases = [tuple(int(x) for x in a.split('x')) for a in sys.argv[1:]] or [(1024, 64), (256, 64), (512, 64)]
+for n, batch in cases:
     c = cfg5_medium(n)
     dt = 0.9 * (1.0 / n) / (math.sqrt(2.0) * float(c.max()))
     prop = B.Propagator(ctx, B.Grid((n, n), (1.0 / n, 1.0 / n)), c, dt, 64)
@@ -30,4 +31,7 @@ for n, batch in [(1024, 64), (256, 64), (512, 64)]:
                 pass
     os.environ["PTB_WAVE_W"] = "0"; os.environ["PTB_WAVE_DIV"] = "0"
     res.sort(reverse=True)
+    if os.environ.get("SWEEP_ALL"):
+        for r in res:
+            print("   ", r[0], r[1], r[2], r[3][:60], flush=True)
     print(n, batch, "auto:", [r for r in res if r[1] == 0 and r[2] == 0][:1], "best:", res[:4], flush=True)
