@@ -110,7 +110,10 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
   double* pxs = sm + G::PLANE + G::PAD;      // LAYER: px; plain: the coefficient kx
   double* pys = sm + 2 * G::PLANE + G::PAD;  // LAYER only
   double* ks = pxs;
-  double* zxs = sm + (LAYER ? 3 : 2) * G::PLANE;  // EX each: zx ax qx; EY each: zy ay qy (LAYER only)
+  // LAYER only: 1 / (1 + hd (zy + zx)) per point, formed once per pass (the same correctly rounded
+  // quotient the second half kick would form at every step)
+  [[maybe_unused]] double* ivs = sm + 3 * G::PLANE;
+  double* zxs = sm + (LAYER ? 4 : 2) * G::PLANE;  // EX each: zx ax qx; EY each: zy ay qy (LAYER only)
   double* axs = zxs + E;
   double* qxs = axs + E;
   double* zys = qxs + E;
@@ -191,6 +194,14 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
   };
   auto col = [](int e) { return e % E; };
   auto row = [](int e) { return min(e / E, EY - 1); };
+  if constexpr (LAYER) {
+#pragma unroll 1
+    for (int i = 0; i < NPT; ++i) {
+      const int e = tid + i * NT;
+      const double sg = __dadd_rn(zys[row(e)], zxs[col(e)]);
+      ivs[e] = __ddiv_rn(1.0, __dadd_rn(1.0, __dmul_rn(a.hd, sg)));
+    }
+  }
 
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
@@ -233,9 +244,8 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
       if constexpr (LAYER) {
         const double zx = zxs[col(e)], zy = zys[row(e)];
         if (zx != 0.0 || zy != 0.0) {
-          const double pi = __dmul_rn(zy, zx), sg = __dadd_rn(zy, zx);
-          const double inv = __ddiv_rn(1.0, __dadd_rn(1.0, __dmul_rn(a.hd, sg)));
-          const double v1 = __dmul_rn(__dadd_rn(hv[i], __dsub_rn(f, __dmul_rn(a.hd, __dmul_rn(pi, us[e])))), inv);
+          const double pi = __dmul_rn(zy, zx);
+          const double v1 = __dmul_rn(__dadd_rn(hv[i], __dsub_rn(f, __dmul_rn(a.hd, __dmul_rn(pi, us[e])))), ivs[e]);
           hv[i] = last ? v1 : kick_layer(v1, f, us[e], zx, zy, a.hd);
         } else {  // the same values for finite fields: pi = sg = 0, inv = 1
           const double v1 = __dadd_rn(hv[i], f);
@@ -372,7 +382,7 @@ constexpr int FRAME_MARGIN = PS + 2;  // interior rectangle starts this far from
 template <bool LAYER, int TY = PTY, int TX = PTX>
 size_t pml_smem() {
   using G = Geo<TY, TX, LAYER ? HL : HP, LAYER ? kLayerThreads : kPlainThreads>;
-  return size_t(G::PLANE) * (LAYER ? 3 : 2) * sizeof(double) + (LAYER ? 3 * (G::EX + G::EY) * sizeof(double) : 0) +
+  return size_t(G::PLANE) * (LAYER ? 4 : 2) * sizeof(double) + (LAYER ? 3 * (G::EX + G::EY) * sizeof(double) : 0) +
          (G::EX + G::EY) * sizeof(int);
 }
 
@@ -470,6 +480,17 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     attr_done.fetch_or(bit);
   }
   require(batch <= 65535, "pml propagate: at most 65535 slices per call");
+  // PTB_PML_LANES=0: every launch of a pass on the one stream (A/B measurements)
+  static const bool lanes_env = [] {
+    const char* e = std::getenv("PTB_PML_LANES");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool lanes = lanes_env && p->frame;
+  if (lanes && !ctx->lane) {
+    PTB_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->lane, cudaStreamNonBlocking));
+    PTB_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_fork, cudaEventDisableTiming));
+    PTB_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_join, cudaEventDisableTiming));
+  }
   int cur = 0;
   for (size_t done = 0; done < steps;) {
     const int ns = int(std::min<size_t>(PS, steps - done));
@@ -486,16 +507,29 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     a.flags = done == steps ? flags : nullptr;
     if (p->frame && (ns == 4 || ns == 2 || ns == 1) && pml_wave_enabled() && pml_frame_enabled()) {
       // frame mode: the interior rectangle through k_wave2, the bands through band-shaped layer tiles
-      wave_rect_fast(ctx, st, ns, p->prm, batch, a.ui, a.vi, a.uo, a.vo, a.kx, a.flags, p->fy0, p->fny, p->fx0,
-                     p->fnx);
+      // The three launches of a pass read the same input and write disjoint parts of the output:
+      // the band tiles (one latency-bound CTA per SM) go to the context's lane stream and overlap the
+      // interior's wavefront CTAs (fork/join by events, so `st` still orders the passes).
+      cudaStream_t bs = st;
+      if (lanes) {
+        PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_fork, st));
+        PTB_CUDA_CHECK(cudaStreamWaitEvent(ctx->lane, ctx->lane_fork, 0));
+        bs = ctx->lane;
+      }
       a.tiles = p->ftiles;
       k_pml<true, kLayerThreads, FB, PTX><<<dim3(p->ntb, unsigned(batch)), kLayerThreads, pml_smem<true, FB, PTX>(),
-                                            st>>>(a);
+                                            bs>>>(a);
       PTB_LAUNCH_CHECK(ctx);
       a.tiles = p->ftiles + p->ntb;
       k_pml<true, kLayerThreads, PTY, FB><<<dim3(p->nlr, unsigned(batch)), kLayerThreads, pml_smem<true, PTY, FB>(),
-                                            st>>>(a);
+                                            bs>>>(a);
       PTB_LAUNCH_CHECK(ctx);
+      wave_rect_fast(ctx, st, ns, p->prm, batch, a.ui, a.vi, a.uo, a.vo, a.kx, a.flags, p->fy0, p->fny, p->fx0,
+                     p->fnx);
+      if (lanes) {
+        PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_join, ctx->lane));
+        PTB_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->lane_join, 0));
+      }
       cur = 1 - cur;
       continue;
     }
