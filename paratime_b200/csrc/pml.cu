@@ -378,6 +378,13 @@ constexpr int kPlainThreads = 256, kLayerThreads = 512;
 // FB rows x PTX columns (top and bottom), PTY rows x FB columns (left and right)
 constexpr int FB = 40;
 constexpr int FRAME_MARGIN = PS + 2;  // interior rectangle starts this far from the last damped cell
+// super-pass (2 PS steps): the interior runs ONE 2 PS-step wavefront launch on the rectangle
+// SUPER_MARGIN cells from the damped bands, the bands two PS-step passes — pass A on bands FBA wide
+// into a third buffer set (its outputs feed pass B's halo), pass B on bands FBB wide into the
+// output.  Tile heights keep the ext box within 10 points per thread.
+constexpr int SUPER_MARGIN = 2 * PS + 2;
+constexpr int FBB = 32 + SUPER_MARGIN, FBA = FBB + HL;  // 42, 51 (layers up to 32 cells)
+constexpr int PTYA = 54, PTYB = 60;                     // left/right tile heights of pass A / pass B
 
 template <bool LAYER, int TY = PTY, int TX = PTX>
 size_t pml_smem() {
@@ -418,6 +425,12 @@ struct ptb_pml {
   // frame mode: interior rectangle and the band tiles (top/bottom FB x PTX, then left/right PTY x FB)
   int frame = 0, fy0 = 0, fny = 0, fx0 = 0, fnx = 0, ntb = 0, nlr = 0;
   int2* ftiles = nullptr;
+  // super-pass geometry (see SUPER_MARGIN): interior rectangle, pass-A and pass-B band tiles
+  // (top/bottom then left/right in each list), and the buffer set pass A writes
+  int super = 0, sy0 = 0, sny = 0, sx0 = 0, snx = 0, natb = 0, nalr = 0, nbtb = 0, nblr = 0;
+  int2* stiles = nullptr;  // pass A tiles, then pass B tiles
+  ptb::DeviceBuffer mid;
+  size_t mid_batch = 0;
 };
 
 namespace ptb {
@@ -430,6 +443,12 @@ bool pml_wave_enabled() {
 // PTB_PML_FRAME=0: the 70 x 54 tile classes instead of the frame (A/B measurements, tests)
 bool pml_frame_enabled() {
   const char* e = std::getenv("PTB_PML_FRAME");
+  return !(e && std::atoi(e) == 0);
+}
+
+// PTB_PML_SUPER=0: PS-step passes only (A/B measurements, tests)
+bool pml_super_enabled() {
+  const char* e = std::getenv("PTB_PML_SUPER");
   return !(e && std::atoi(e) == 0);
 }
 
@@ -477,6 +496,14 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
                                         int(pml_smem<true, FB, PTX>())));
     PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, PTY, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(pml_smem<true, PTY, FB>())));
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, FBA, PTX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(pml_smem<true, FBA, PTX>())));
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, FBB, PTX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(pml_smem<true, FBB, PTX>())));
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, PTYA, FBA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(pml_smem<true, PTYA, FBA>())));
+    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, PTYB, FBB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(pml_smem<true, PTYB, FBB>())));
     attr_done.fetch_or(bit);
   }
   require(batch <= 65535, "pml propagate: at most 65535 slices per call");
@@ -491,8 +518,67 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     PTB_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_fork, cudaEventDisableTiming));
     PTB_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_join, cudaEventDisableTiming));
   }
+  const bool super = p->super && steps >= size_t(2 * PS) && pml_wave_enabled() && pml_frame_enabled() &&
+                     pml_super_enabled();
+  double* mid[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (super) {
+    if (p->mid_batch < batch) {
+      p->mid.get(4 * fb);
+      p->mid_batch = batch;
+    }
+    double* m = static_cast<double*>(p->mid.ptr);
+    const size_t mb = p->mid_batch * n;
+    for (int f = 0; f < 4; ++f) mid[f] = m + f * mb;
+  }
   int cur = 0;
   for (size_t done = 0; done < steps;) {
+    if (super && steps - done >= size_t(2 * PS)) {
+      // One super-pass = 2 PS steps.  Band pass A (PS steps, bands FBA wide) reads the input and writes
+      // the third buffer set; band pass B (PS steps, bands FBB wide) reads that — its halo ends where
+      // pass A's outputs end — and writes the output; the interior rectangle advances 2 PS steps in
+      // one wavefront launch (its cone stays SUPER_MARGIN - 2 PS cells away from damped cells).  The
+      // band passes go to the lane stream, the interior to the caller's.
+      done += 2 * PS;
+      a.flags = done == steps ? flags : nullptr;
+      a.steps = PS;
+      cudaStream_t bs = st;
+      if (lanes) {
+        PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_fork, st));
+        PTB_CUDA_CHECK(cudaStreamWaitEvent(ctx->lane, ctx->lane_fork, 0));
+        bs = ctx->lane;
+      }
+      PmlArgs pa = a;
+      pa.flags = nullptr;
+      pa.ui = bufs[cur][0], pa.vi = bufs[cur][1], pa.pxi = bufs[cur][2], pa.pyi = bufs[cur][3];
+      pa.uo = mid[0], pa.vo = mid[1], pa.pxo = mid[2], pa.pyo = mid[3];
+      pa.tiles = p->stiles;
+      k_pml<true, kLayerThreads, FBA, PTX><<<dim3(p->natb, unsigned(batch)), kLayerThreads,
+                                             pml_smem<true, FBA, PTX>(), bs>>>(pa);
+      PTB_LAUNCH_CHECK(ctx);
+      pa.tiles = p->stiles + p->natb;
+      k_pml<true, kLayerThreads, PTYA, FBA><<<dim3(p->nalr, unsigned(batch)), kLayerThreads,
+                                              pml_smem<true, PTYA, FBA>(), bs>>>(pa);
+      PTB_LAUNCH_CHECK(ctx);
+      PmlArgs pb = a;
+      pb.ui = mid[0], pb.vi = mid[1], pb.pxi = mid[2], pb.pyi = mid[3];
+      pb.uo = bufs[1 - cur][0], pb.vo = bufs[1 - cur][1], pb.pxo = bufs[1 - cur][2], pb.pyo = bufs[1 - cur][3];
+      pb.tiles = p->stiles + p->natb + p->nalr;
+      k_pml<true, kLayerThreads, FBB, PTX><<<dim3(p->nbtb, unsigned(batch)), kLayerThreads,
+                                             pml_smem<true, FBB, PTX>(), bs>>>(pb);
+      PTB_LAUNCH_CHECK(ctx);
+      pb.tiles = p->stiles + p->natb + p->nalr + p->nbtb;
+      k_pml<true, kLayerThreads, PTYB, FBB><<<dim3(p->nblr, unsigned(batch)), kLayerThreads,
+                                              pml_smem<true, PTYB, FBB>(), bs>>>(pb);
+      PTB_LAUNCH_CHECK(ctx);
+      wave_rect_fast(ctx, st, 2 * PS, p->prm, batch, bufs[cur][0], bufs[cur][1], bufs[1 - cur][0], bufs[1 - cur][1],
+                     a.kx, a.flags, p->sy0, p->sny, p->sx0, p->snx);
+      if (lanes) {
+        PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_join, ctx->lane));
+        PTB_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->lane_join, 0));
+      }
+      cur = 1 - cur;
+      continue;
+    }
     const int ns = int(std::min<size_t>(PS, steps - done));
     done += ns;
     a.ui = bufs[cur][0];
@@ -1175,6 +1261,35 @@ ptb_status ptb_pml_create(ptb_context* ctx, const ptb_grid* grid, const double* 
             ft.push_back(make_int2(int(ty), 0));
             ft.push_back(make_int2(int(ty), int(nx) - FB));
           }
+          // the super-pass needs the wider margin and the band tiles of both passes
+          const long sy0 = ylo + SUPER_MARGIN, sy1 = long(ny) - yhi - SUPER_MARGIN;
+          const long sx0 = (xlo + SUPER_MARGIN + 1) & ~1L, sx1 = (long(nx) - xhi - SUPER_MARGIN) & ~1L;
+          if (sy0 <= FBB && long(ny) - sy1 <= FBB && sx0 <= FBB && long(nx) - sx1 <= FBB && sy1 - sy0 >= 4 * FBA &&
+              sx1 - sx0 >= 4 * FBA) {
+            std::vector<int2> stl;
+            auto band_tiles = [&](int fbw, int pty, int& ntb_out, int& nlr_out) {
+              const size_t before = stl.size();
+              for (long tx = 0; tx < long(nx); tx += PTX) {
+                stl.push_back(make_int2(0, int(tx)));
+                stl.push_back(make_int2(int(ny) - fbw, int(tx)));
+              }
+              ntb_out = int(stl.size() - before);
+              for (long ty = fbw; ty < long(ny) - fbw; ty += pty) {
+                stl.push_back(make_int2(int(ty), 0));
+                stl.push_back(make_int2(int(ty), int(nx) - fbw));
+              }
+              nlr_out = int(stl.size() - before) - ntb_out;
+            };
+            band_tiles(FBA, PTYA, p->natb, p->nalr);
+            band_tiles(FBB, PTYB, p->nbtb, p->nblr);
+            p->super = 1;
+            p->sy0 = int(sy0);
+            p->sny = int(sy1 - sy0);
+            p->sx0 = int(sx0);
+            p->snx = int(sx1 - sx0);
+            PTB_CUDA_CHECK(cudaMalloc(&p->stiles, stl.size() * sizeof(int2)));
+            PTB_CUDA_CHECK(cudaMemcpy(p->stiles, stl.data(), stl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+          }
           p->frame = 1;
           p->fy0 = int(y0);
           p->fny = int(y1 - y0);
@@ -1212,6 +1327,7 @@ ptb_status ptb_pml_destroy(ptb_pml* p) {
     cudaFree(p->speed);
     cudaFree(p->tiles);
     cudaFree(p->ftiles);
+    cudaFree(p->stiles);
     delete p;
   });
 }

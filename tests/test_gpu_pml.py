@@ -324,6 +324,32 @@ def test_pml_theta_sharded_equals_single_gpu(world):
         assert np.array_equal(o["states"][:, a - 1:b], single["states"][:, a - 1:b])
 
 
+@pytest.mark.parametrize("ny,nx,w,steps,batch", [(512, 512, 32, 8, 2), (512, 512, 32, 20, 1), (640, 448, 24, 13, 3),
+                                                 (448, 704, 32, 16, 2)])
+def test_super_pass_equals_short_passes_bitwise(ctx, ny, nx, w, steps, batch, monkeypatch):
+    """Super-pass (the interior advances 8 steps in one wavefront launch; the bands run two 4-step
+    passes, the first on wider bands into a third buffer set) against 4-step passes only: the same
+    arithmetic per point, so the layered propagation is bitwise the same (a remainder of the steps
+    takes the 4/2/1-step passes), and both match the oracle."""
+    import paratime_b200 as B
+
+    hy, hx = 1 / ny, 1 / nx
+    c, zy, zx, state = _case(ny, nx, hy, hx, w, batch, seed=ny + nx + steps)
+    dt = 0.5 * min(hy, hx) / np.sqrt(2)
+    prop = B.PmlPropagator(ctx, B.Grid((ny, nx), (hy, hx)), c, zy, zx, dt, steps)
+    out = {}
+    for sup in ("1", "0"):
+        monkeypatch.setenv("PTB_PML_SUPER", sup)
+        t = [ctx.tensor(a) for a in state]
+        prop.propagate(*t)
+        out[sup] = [x.cpu().numpy() for x in t]
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
+    want = M.pml_steps(*(s_[:1] for s_ in state), M.PmlCoefficients(c, hy, hx, dt, zy, zx), steps)
+    for got, ref in zip(out["1"], want):
+        assert _rel(got[:1], ref) <= TOL
+
+
 @pytest.mark.parametrize("n,w,steps", [(256, 32, 12), (512, 32, 10), (384, 16, 8)])
 def test_interior_wavefront_equals_plain_tiles_bitwise(ctx, n, w, steps, monkeypatch):
     """The undamped interior runs the periodic wavefront kernel (k_wave2 on the interior
