@@ -563,7 +563,9 @@ def pml_section(B, ctx, tflops_peak, hbm_peak, rank=0, world=1, dist=None):
     """BASELINE.json config 4 WITH its 32-cell absorbing layer (workloads.cfg4_pml; not in the
     reference).  (1) fine-stage throughput of the layered propagator on the
     per-GPU share of cfg4 at 8 GPUs (16 slices x 128 steps, 2048^2), device-resident, CUDA events;
-    binding roofline with 40 B per point per 4-step pass (10 B/update) and 17 flops/update;
+    binding roofline from the super-pass traffic (interior 40 B per point per 8 steps, band frame
+    2 x 72 B per point per 8 steps: ~6 B/update; the round-1/2 figure at 10 B/update beside it) and
+    17 flops/update;
     (2) s/iteration of theta parareal with the layer (ptb_pml_theta_run: N = 128, K = 8, tol 1e-4;
     slices sharded over the ranks when world > 1, max over ranks).  Plain parareal is not reported:
     its iterates grow without bound on this hyperbolic problem."""
@@ -594,7 +596,13 @@ def pml_section(B, ctx, tflops_peak, hbm_peak, rank=0, world=1, dist=None):
     ups = batch * nf * nf * spec["m_fine"] / (ms * 1e-3)
     del t
     torch.cuda.empty_cache()
-    f_hbm = ups * 10.0 / (hbm_peak * 1e9)
+    # algorithmic HBM bytes per update under the super-pass: the interior rectangle (SUPER_MARGIN = 10
+    # cells from the damped bands) moves 40 B per point per 8 fused steps, the band frame 72 B per
+    # point (u, udot, px, py read + write, coefficient read) in each of its two 4-step passes
+    layer = int(np.count_nonzero(np.asarray(zf) > 0)) // 2
+    fi = ((nf - 2 * (layer + 10)) / nf) ** 2
+    bytes_per_update = fi * 40.0 / 8.0 + (1.0 - fi) * 2 * 72.0 / 8.0
+    f_hbm = ups * bytes_per_update / (hbm_peak * 1e9)
     f_fp64 = ups * FLOPS_PER_UPDATE / (tflops_peak * 1e12) if tflops_peak else None
     tr = B.Transfer(ctx, gc, gf, spec["interp"])
     comm = None
@@ -616,7 +624,10 @@ def pml_section(B, ctx, tflops_peak, hbm_peak, rank=0, world=1, dist=None):
     return {"workload": "cfg4 + 32-cell absorbing layer (fine 2048^2 / coarse 256^2, layered-faulted medium)",
             "fine_stage": {"per_gpu": True, "batch": batch, "steps": spec["m_fine"], "ms": round(ms, 3), "updates_per_s": ups,
                            "frac_hbm": f_hbm, "frac_fp64": f_fp64, "frac_binding": max(f_hbm, f_fp64 or 0.0),
-                           "kernel": "k_pml_plain 70x54 register-column tiles (halo 5) + k_pml<layer> (halo 9), 4 steps per pass"},
+                           "bytes_per_update": bytes_per_update,
+                           "frac_hbm_at_10B_per_update": ups * 10.0 / (hbm_peak * 1e9),
+                           "kernel": "super-pass of 8 steps: k_wave2<8> on the interior rectangle + k_pml<layer> band "
+                                     "tiles (halo 9) in two 4-step passes (51- and 42-cell bands)"},
             "theta_parareal": {"N": spec["n_couplings"], "K": spec["iterations"], "tol": spec["tol"], "ranks": world,
                                "s_per_iteration": float(np.median(its)) / 1e3, "iteration_ms": [round(x, 2) for x in its],
                                "corrector_rank": [int(x) for x in r["rank"]],
