@@ -2633,6 +2633,12 @@ void tsqr_rows_pair(ProcWork& w, const RowPart& rp, const double* Af, const doub
   kg = k[1];
 }
 
+// PTB_QR2_PAIR=0: F and G through qr2_rows one after the other (A/B tests)
+bool qr2_pair_enabled() {
+  const char* e = std::getenv("PTB_QR2_PAIR");
+  return !(e && std::atoi(e) == 0);
+}
+
 // the two-panel route (truncated_qr_2panel) on a row-sharded block: both panels through tsqr_rows,
 // the Gram-Schmidt projections over the slabs
 int qr2_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, double drop_tol, DeviceBuffer& Qo,
@@ -2640,7 +2646,9 @@ int qr2_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, do
   ptb_context* ctx = w.ctx;
   cudaStream_t st = ctx->stream;
   const int n1 = TS_MAXN, n2 = n - n1, own = rp.own;
+  HostProf hp_(st);
   const int k1 = tsqr_rows(w, rp, A, lda, n1, 0.0, w.TP[0], w.TP[1]);
+  hp_.mark("qr2: panel 1 tsqr");
   const double* Q1 = static_cast<const double*>(w.TP[0].ptr);
   double* A2 = static_cast<double*>(w.TP[2].get(size_t(own) * n2 * sizeof(double)));
   PTB_CUDA_CHECK(cudaMemcpy2DAsync(A2, size_t(own) * sizeof(double), A + size_t(n1) * lda, size_t(lda) * sizeof(double),
@@ -2653,7 +2661,9 @@ int qr2_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, do
       gemm_rows(ctx, own, n2, k1, -1.0, Q1, own, Cp, k1, 1.0, A2, own);
     }
   }
+  hp_.mark("qr2: block Gram-Schmidt x2");
   const int k2 = tsqr_rows(w, rp, A2, own, n2, 0.0, w.TP[4], w.TP[5]);
+  hp_.mark("qr2: panel 2 tsqr");
   const int kk = k1 + k2;
   double* R = static_cast<double*>(w.TP[6].get(std::max<size_t>(1, size_t(kk) * n) * sizeof(double)));
   if (kk == 0) {
@@ -2666,6 +2676,7 @@ int qr2_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, do
       static_cast<const double*>(w.TP[5].ptr), R);
   PTB_LAUNCH_CHECK(ctx);
   const int kq = truncated_qr_direct(w, R, kk, n, drop_tol, w.BQ2, Rb);
+  hp_.mark("qr2: R assemble + pivoted qr");
   double* Q = static_cast<double*>(Qo.get(std::max<size_t>(1, size_t(own) * kq) * sizeof(double)));
   if (kq == 0) return 0;
   const double* QR = static_cast<const double*>(w.BQ2.ptr);
@@ -2673,7 +2684,72 @@ int qr2_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, do
   if (k2 > 0)
     gemm_rows(ctx, own, kq, k2, 1.0, static_cast<const double*>(w.TP[4].ptr), own, QR + k1, kk, k1 > 0 ? 1.0 : 0.0, Q,
               own);
+  hp_.mark("qr2: Q = [Q1 Q2] QR");
   return kq;
+}
+
+// F and G together through the two-panel route: both panels' TSQRs run as pairs (tsqr_rows_pair:
+// every leaf, stack level and down-sweep launch covers both matrices, one host sync per keep-count
+// pair), the Gram-Schmidt products, the R assembly + pivoted QR and the Q products per matrix —
+// each matrix gets exactly qr2_rows' arithmetic.
+void qr2_rows_pair(ProcWork& w, const RowPart& rp, const double* Af, const double* Ag, int lda, int n, double tol_f,
+                   double tol_g, DeviceBuffer& Qf, DeviceBuffer& Rf, DeviceBuffer& Qg, DeviceBuffer& Rg, int& kf,
+                   int& kg) {
+  ptb_context* ctx = w.ctx;
+  cudaStream_t st = ctx->stream;
+  const int n1 = TS_MAXN, n2 = n - n1, own = rp.own;
+  HostProf hp_(st);
+  DeviceBuffer* T[2] = {w.TP, w.TPg};
+  const double* A[2] = {Af, Ag};
+  const double tol[2] = {tol_f, tol_g};
+  DeviceBuffer* Qo[2] = {&Qf, &Qg};
+  DeviceBuffer* Ro[2] = {&Rf, &Rg};
+  int k1[2] = {0, 0}, k2[2] = {0, 0}, kq[2] = {0, 0};
+  tsqr_rows_pair(w, rp, A[0], A[1], lda, n1, 0.0, 0.0, T[0][0], T[0][1], T[1][0], T[1][1], k1[0], k1[1]);
+  hp_.mark("qr2 pair: panel 1 tsqr");
+  double *A2[2], *C[2];
+  for (int b = 0; b < 2; ++b) {
+    const double* Q1 = static_cast<const double*>(T[b][0].ptr);
+    A2[b] = static_cast<double*>(T[b][2].get(size_t(own) * n2 * sizeof(double)));
+    PTB_CUDA_CHECK(cudaMemcpy2DAsync(A2[b], size_t(own) * sizeof(double), A[b] + size_t(n1) * lda,
+                                     size_t(lda) * sizeof(double), size_t(own) * sizeof(double), n2,
+                                     cudaMemcpyDeviceToDevice, st));
+    C[b] = static_cast<double*>(T[b][3].get(std::max<size_t>(1, 2 * size_t(k1[b]) * n2) * sizeof(double)));
+    if (k1[b] > 0) {
+      for (int pass = 0; pass < 2; ++pass) {
+        double* Cp = C[b] + size_t(pass) * k1[b] * n2;
+        slab_tn(w, rp, false, k1[b], n2, Q1, own, A2[b], own, Cp);
+        gemm_rows(ctx, own, n2, k1[b], -1.0, Q1, own, Cp, k1[b], 1.0, A2[b], own);
+      }
+    }
+  }
+  hp_.mark("qr2 pair: block Gram-Schmidt x2");
+  tsqr_rows_pair(w, rp, A2[0], A2[1], own, n2, 0.0, 0.0, T[0][4], T[0][5], T[1][4], T[1][5], k2[0], k2[1]);
+  hp_.mark("qr2 pair: panel 2 tsqr");
+  for (int b = 0; b < 2; ++b) {
+    const int kk = k1[b] + k2[b];
+    if (kk == 0) {
+      Qo[b]->get(8);
+      Ro[b]->get(8);
+      continue;
+    }
+    double* R = static_cast<double*>(T[b][6].get(std::max<size_t>(1, size_t(kk) * n) * sizeof(double)));
+    k_assemble_r2<<<unsigned(std::max(1, std::min(1024, (kk * n + 255) / 256))), 256, 0, st>>>(
+        k1[b], k2[b], n1, n2, static_cast<const double*>(T[b][1].ptr), C[b], C[b] + size_t(k1[b]) * n2,
+        static_cast<const double*>(T[b][5].ptr), R);
+    PTB_LAUNCH_CHECK(ctx);
+    kq[b] = truncated_qr_direct(w, R, kk, n, tol[b], w.BQ2, *Ro[b]);
+    double* Q = static_cast<double*>(Qo[b]->get(std::max<size_t>(1, size_t(own) * kq[b]) * sizeof(double)));
+    if (kq[b] == 0) continue;
+    const double* QR = static_cast<const double*>(w.BQ2.ptr);
+    if (k1[b] > 0) gemm_rows(ctx, own, kq[b], k1[b], 1.0, static_cast<const double*>(T[b][0].ptr), own, QR, kk, 0.0, Q, own);
+    if (k2[b] > 0)
+      gemm_rows(ctx, own, kq[b], k2[b], 1.0, static_cast<const double*>(T[b][4].ptr), own, QR + k1[b], kk,
+                k1[b] > 0 ? 1.0 : 0.0, Q, own);
+  }
+  hp_.mark("qr2 pair: R, pivoted qr, Q");
+  kf = kq[0];
+  kg = kq[1];
 }
 
 int qr_rows(ProcWork& w, const RowPart& rp, const double* A, int lda, int n, double drop_tol, DeviceBuffer& Qo,
@@ -2711,6 +2787,8 @@ void update_svd_rows(ProcWork& w, DevCorrector& c, const double* F, const double
   int qf = 0, qg = 0;
   if (cols <= TS_MAXN) {
     tsqr_rows_pair(w, rp, Fr, Gr, own, cols, qr_guard * fn, qr_guard * gn, w.QF, w.RF, w.QG, w.RG, qf, qg);
+  } else if (qr2_pair_enabled()) {
+    qr2_rows_pair(w, rp, Fr, Gr, own, cols, qr_guard * fn, qr_guard * gn, w.QF, w.RF, w.QG, w.RG, qf, qg);
   } else {
     qf = qr_rows(w, rp, Fr, own, cols, qr_guard * fn, w.QF, w.RF);
     qg = qr_rows(w, rp, Gr, own, cols, qr_guard * gn, w.QG, w.RG);

@@ -36,6 +36,7 @@ struct ProcWork {
   DeviceBuffer TS2[24], TX2[2], BQ2b;  // the second matrix of a batched (F, G) TSQR
   DeviceBuffer PA[4], PB[4];        // batched TSQR: the two final pivoted factors, tau, perm, |R_jj|
   DeviceBuffer TP[8];               // two-panel TSQR: Q1, R1, A2, C, Q2, R2, the assembled R
+  DeviceBuffer TPg[8];              // the second matrix (G) of the row-sharded two-panel pair
   DeviceBuffer SH[12];              // row-sharded update_svd: level-0 leaves, stacks, slab partials, gathers
   DeviceBuffer SG[6];               // the second matrix (G) of the row-sharded pair TSQR
   // the ranks the corrector's rows are sharded over (update_svd; null: one process).  Set by the

@@ -40,3 +40,50 @@ def test_truncated_qr_tall_matches_oracle(tmp_path, path):
         if k == a.shape[1]:
             assert np.linalg.norm(q @ r - a) <= 1e-12 * scale, t
         t += 1
+
+
+@pytest.mark.gpu
+def test_two_panel_pair_equals_sequential_bitwise(monkeypatch):
+    """update_svd on the row-slab path with 64 < columns <= 128 (config 4's N = 128 snapshots): F and
+    G go through the two-panel TSQR route as a pair (shared leaf / stack / down-sweep launches) or
+    one after the other (PTB_QR2_PAIR=0) — the same arithmetic per matrix, so the factors are
+    bitwise equal; and they match the oracle's update_svd."""
+    import paratime_b200 as B
+    from oracle import paratime_np as P
+
+    rng = np.random.default_rng(4242)
+    rows, cols = 12288, 96  # 48 slabs of one 256-row TSQR leaf
+    ctx = B.Context(0)
+    out = {}
+    base = rng.standard_normal((rows, 24))
+    blocks = []
+    for k in range(3):
+        F = base @ rng.standard_normal((24, cols)) + 1e-3 * rng.standard_normal((rows, cols))
+        G = F + 1e-2 * rng.standard_normal((rows, cols))
+        blocks.append((F, G))
+    for pair in ("1", "0"):
+        monkeypatch.setenv("PTB_QR2_PAIR", pair)
+        c = B.api.Corrector(ctx)
+        for F, G in blocks:
+            c.update(ctx.tensor(np.ascontiguousarray(F.T)), ctx.tensor(np.ascontiguousarray(G.T)), 1e-8)
+        out[pair] = c.factors()
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
+    co = P.empty_corrector()
+    for F, G in blocks:
+        co = P.update_svd(co, F, G, 1e-8)
+    X, S, Y = out["1"]
+    assert len(S) == co.rank
+    assert np.max(np.abs(S - co.S)) <= 1e-10 * co.S[0]
+    # Omega = X Y^T (procrustes.cpp:82-86) as an operator: individual vectors of clustered singular
+    # values are not comparable, the product is
+    V = rng.standard_normal((rows, 4))
+    want = co.X @ (co.Y.T @ V)
+    got = X @ (Y.T @ V)
+    assert np.linalg.norm(got - want) <= 1e-6 * np.linalg.norm(want)  # noise-level directions are kept (tol 1e-8)
+    F, G = blocks[-1]
+    c = B.api.Corrector(ctx)
+    for Fb, Gb in blocks:
+        c.update(ctx.tensor(np.ascontiguousarray(Fb.T)), ctx.tensor(np.ascontiguousarray(Gb.T)), 1e-8)
+    res = c.residual(ctx.tensor(np.ascontiguousarray(F.T)), ctx.tensor(np.ascontiguousarray(G.T)))
+    assert res == pytest.approx(P.relative_residual(co, F, G), rel=1e-6)
