@@ -58,11 +58,12 @@ struct PmlArgs {
   int steps;                                 // steps of this pass (<= PS)
   int32_t* flags;
   const int2* tiles;                         // (ty0, tx0) of the tiles of this launch's class
+  int ylim, xlim;                            // outputs only on rows < ylim, columns < xlim (0: the grid's)
 };
 
-template <int TY, int TX, int H, int NT>
+template <int TY, int TX, int H, int NT, int HY0 = H, int HY1 = H, int HX0 = H, int HX1 = H>
 struct Geo {
-  static constexpr int EY = TY + 2 * H, EX = TX + 2 * H, EXT = EY * EX, NPT = (EXT + NT - 1) / NT;
+  static constexpr int EY = TY + HY0 + HY1, EX = TX + HX0 + HX1, EXT = EY * EX, NPT = (EXT + NT - 1) / NT;
   static constexpr int EXTP = NPT * NT;
   static constexpr int PAD = EX + 1;           // stencil reads of padded points stay in bounds
   static constexpr int PLANE = EXTP + 2 * PAD;
@@ -100,10 +101,15 @@ __device__ __forceinline__ int wrap(int i, int n) {
   return i < 0 ? i + n : i;
 }
 
-template <bool LAYER, int NT, int TY = PTY, int TX = PTX>
+// HY0/HY1/HX0/HX1 (default: the class halo H on every side): halo rows before / after the tile and
+// halo columns before / after it.  A side whose rim cells are all undamped — no damping within the
+// halo and the margin behind it — needs only the plain halo HP there: garbage moves one cell per
+// step through undamped cells (their px, py are never updated), two through damped ones.
+template <bool LAYER, int NT, int TY = PTY, int TX = PTX, int HY0 = -1, int HY1 = -1, int HX0 = -1, int HX1 = -1>
 __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
   constexpr int H = LAYER ? HL : HP;
-  using G = Geo<TY, TX, H, NT>;
+  constexpr int hy0 = HY0 < 0 ? H : HY0, hy1 = HY1 < 0 ? H : HY1, hx0 = HX0 < 0 ? H : HX0, hx1 = HX1 < 0 ? H : HX1;
+  using G = Geo<TY, TX, H, NT, hy0, hy1, hx0, hx1>;
   constexpr int E = G::EX, EY = G::EY, NPT = G::NPT;
   extern __shared__ double sm[];
   double* us = sm + G::PAD;
@@ -127,7 +133,7 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
   const int ty0 = t0.x, tx0 = t0.y;
 
   for (int j = tid; j < E; j += NT) {
-    const int gx = wrap(tx0 - H + j, a.nx);
+    const int gx = wrap(tx0 - hx0 + j, a.nx);
     colg[j] = gx;
     if constexpr (LAYER) {
       zxs[j] = a.zx[gx];
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
     }
   }
   for (int j = tid; j < EY; j += NT) {
-    const int gy = wrap(ty0 - H + j, a.ny);
+    const int gy = wrap(ty0 - hy0 + j, a.ny);
     rowg[j] = gy * a.nx;
     if constexpr (LAYER) {
       zys[j] = a.zy[gy];
@@ -259,14 +265,15 @@ __global__ void __launch_bounds__(NT, LAYER ? 1 : 2) k_pml(const PmlArgs a) {
   }
 
   // store the central tile
+  const int ylim = a.ylim ? a.ylim : a.ny, xlim = a.xlim ? a.xlim : a.nx;
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     const int e = tid + i * NT;
     if (e < G::EXT) {
       const int ey = e / E, ex = e - ey * E;
-      const int oy = ey - H, ox = ex - H;
-      if (oy >= 0 && oy < TY && ox >= 0 && ox < TX && ty0 + oy < a.ny && tx0 + ox < a.nx) {
+      const int oy = ey - hy0, ox = ex - hx0;
+      if (oy >= 0 && oy < TY && ox >= 0 && ox < TX && ty0 + oy < ylim && tx0 + ox < xlim) {
         const size_t g = base + size_t(ty0 + oy) * a.nx + (tx0 + ox);
         a.uo[g] = us[e];
         a.vo[g] = hv[i];
@@ -379,19 +386,58 @@ constexpr int kPlainThreads = 256, kLayerThreads = 512;
 constexpr int FB = 40;
 constexpr int FRAME_MARGIN = PS + 2;  // interior rectangle starts this far from the last damped cell
 // super-pass (2 PS steps): the interior runs ONE 2 PS-step wavefront launch on the rectangle
-// SUPER_MARGIN cells from the damped bands, the bands two PS-step passes — pass A on bands FBA wide
-// into a third buffer set (its outputs feed pass B's halo), pass B on bands FBB wide into the
-// output.  Tile heights keep the ext box within 10 points per thread.
+// SUPER_MARGIN cells from the damped bands, the bands two PS-step passes — pass A into a third
+// buffer set (its outputs feed pass B's halo), pass B into the output.  Pass B covers bands FBB
+// wide.  Band tile classes of a pass:
+//   corner tiles (the band ends, where the cells beyond the band's inner edge are damped by the
+//     crossing band): the layer halo HL on every side; pass A's are FBA = FBB + HL wide and
+//     two tiles long, so pass B's corner tiles (one tile long) find all their inputs;
+//   mid tiles (top/bottom between the corners) and left/right tiles: the cells beyond the inner
+//     edge are undamped for SUPER_MARGIN + HP cells, so the plain halo HP suffices there (k_pml's
+//     HY0..HX1); pass A's are FBM = FBB + HP wide.  Their tile lengths fill 10 points per thread.
 constexpr int SUPER_MARGIN = 2 * PS + 2;
-constexpr int FBB = 32 + SUPER_MARGIN, FBA = FBB + HL;  // 42, 51 (layers up to 32 cells)
-constexpr int PTYA = 54, PTYB = 60;                     // left/right tile heights of pass A / pass B
+constexpr int FBB = 32 + SUPER_MARGIN, FBA = FBB + HL, FBM = FBB + HP;  // 42, 51, 47 (layers up to 32 cells)
+constexpr int LA = 64, LB = 72;                                         // mid / left-right tile lengths, pass A / B
+constexpr int XCA = 2 * PTX, XCB = PTX;                                 // corner-class extent along the band
 
-template <bool LAYER, int TY = PTY, int TX = PTX>
+template <bool LAYER, int TY = PTY, int TX = PTX, int HY0 = -1, int HY1 = -1, int HX0 = -1, int HX1 = -1>
 size_t pml_smem() {
-  using G = Geo<TY, TX, LAYER ? HL : HP, LAYER ? kLayerThreads : kPlainThreads>;
+  constexpr int H = LAYER ? HL : HP;
+  using G = Geo<TY, TX, H, LAYER ? kLayerThreads : kPlainThreads, (HY0 < 0 ? H : HY0), (HY1 < 0 ? H : HY1),
+                (HX0 < 0 ? H : HX0), (HX1 < 0 ? H : HX1)>;
   return size_t(G::PLANE) * (LAYER ? 4 : 2) * sizeof(double) + (LAYER ? 3 * (G::EX + G::EY) * sizeof(double) : 0) +
          (G::EX + G::EY) * sizeof(int);
 }
+
+// the super-pass band kernels (fixed instantiations; BandLaunch::kern indexes this table)
+struct BandKernel {
+  const void* fn;
+  size_t smem;
+};
+template <int TY, int TX, int HY0 = -1, int HY1 = -1, int HX0 = -1, int HX1 = -1>
+BandKernel band_kernel() {
+  return {reinterpret_cast<const void*>(k_pml<true, kLayerThreads, TY, TX, HY0, HY1, HX0, HX1>),
+          pml_smem<true, TY, TX, HY0, HY1, HX0, HX1>()};
+}
+enum { BK_A_CORNER, BK_A_TOP, BK_A_BOT, BK_A_LEFT, BK_A_RIGHT, BK_B_CORNER, BK_B_TOP, BK_B_BOT, BK_B_LEFT, BK_B_RIGHT, BK_COUNT };
+const BandKernel* band_kernels() {
+  static const BandKernel k[BK_COUNT] = {
+      band_kernel<FBA, PTX>(),
+      band_kernel<FBM, LA, HL, HP, HL, HL>(),  // top: the inner side is below
+      band_kernel<FBM, LA, HP, HL, HL, HL>(),  // bottom: above
+      band_kernel<LA, FBM, HL, HL, HL, HP>(),  // left: to the right
+      band_kernel<LA, FBM, HL, HL, HP, HL>(),  // right: to the left
+      band_kernel<FBB, PTX>(),
+      band_kernel<FBB, LB, HL, HP, HL, HL>(),
+      band_kernel<FBB, LB, HP, HL, HL, HL>(),
+      band_kernel<LB, FBB, HL, HL, HL, HP>(),
+      band_kernel<LB, FBB, HL, HL, HP, HL>(),
+  };
+  return k;
+}
+struct BandLaunch {
+  int kern, first, count, ylim, xlim;  // kernel, tile range in ptb_pml::stiles, output clips (0: none)
+};
 
 struct DevGuard {
   int prev = -1;
@@ -427,8 +473,14 @@ struct ptb_pml {
   int2* ftiles = nullptr;
   // super-pass geometry (see SUPER_MARGIN): interior rectangle, pass-A and pass-B band tiles
   // (top/bottom then left/right in each list), and the buffer set pass A writes
-  int super = 0, sy0 = 0, sny = 0, sx0 = 0, snx = 0, natb = 0, nalr = 0, nbtb = 0, nblr = 0;
-  int2* stiles = nullptr;  // pass A tiles, then pass B tiles
+  int super = 0, sy0 = 0, sny = 0, sx0 = 0, snx = 0;
+  int2* stiles = nullptr;                       // the band tiles of both passes
+  std::vector<ptb::BandLaunch> pass_a, pass_b;  // band launches of pass A / pass B
+  // a pass's band launches are independent one-CTA-per-SM kernels: each class on its own stream, so
+  // one class's last partial round overlaps the next class's first
+  static constexpr int NBS = 5;
+  cudaStream_t bstream[NBS] = {};
+  cudaEvent_t bfork = nullptr, bev[NBS] = {};
   ptb::DeviceBuffer mid;
   size_t mid_batch = 0;
 };
@@ -496,14 +548,9 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
                                         int(pml_smem<true, FB, PTX>())));
     PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, PTY, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(pml_smem<true, PTY, FB>())));
-    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, FBA, PTX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(pml_smem<true, FBA, PTX>())));
-    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, FBB, PTX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(pml_smem<true, FBB, PTX>())));
-    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, PTYA, FBA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(pml_smem<true, PTYA, FBA>())));
-    PTB_CUDA_CHECK(cudaFuncSetAttribute(k_pml<true, kLayerThreads, PTYB, FBB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(pml_smem<true, PTYB, FBB>())));
+    for (int i = 0; i < BK_COUNT; ++i)
+      PTB_CUDA_CHECK(cudaFuncSetAttribute(band_kernels()[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(band_kernels()[i].smem)));
     attr_done.fetch_or(bit);
   }
   require(batch <= 65535, "pml propagate: at most 65535 slices per call");
@@ -541,41 +588,58 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
       done += 2 * PS;
       a.flags = done == steps ? flags : nullptr;
       a.steps = PS;
-      cudaStream_t bs = st;
+      constexpr int NBS = ptb_pml::NBS;
+      if (lanes && !p->bfork) {
+        PTB_CUDA_CHECK(cudaEventCreateWithFlags(&p->bfork, cudaEventDisableTiming));
+        for (int i = 0; i < NBS; ++i) {
+          PTB_CUDA_CHECK(cudaStreamCreateWithFlags(&p->bstream[i], cudaStreamNonBlocking));
+          PTB_CUDA_CHECK(cudaEventCreateWithFlags(&p->bev[i], cudaEventDisableTiming));
+        }
+      }
       if (lanes) {
-        PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_fork, st));
-        PTB_CUDA_CHECK(cudaStreamWaitEvent(ctx->lane, ctx->lane_fork, 0));
-        bs = ctx->lane;
+        PTB_CUDA_CHECK(cudaEventRecord(p->bfork, st));
+        for (int i = 0; i < NBS; ++i) PTB_CUDA_CHECK(cudaStreamWaitEvent(p->bstream[i], p->bfork, 0));
       }
       PmlArgs pa = a;
       pa.flags = nullptr;
       pa.ui = bufs[cur][0], pa.vi = bufs[cur][1], pa.pxi = bufs[cur][2], pa.pyi = bufs[cur][3];
       pa.uo = mid[0], pa.vo = mid[1], pa.pxo = mid[2], pa.pyo = mid[3];
-      pa.tiles = p->stiles;
-      k_pml<true, kLayerThreads, FBA, PTX><<<dim3(p->natb, unsigned(batch)), kLayerThreads,
-                                             pml_smem<true, FBA, PTX>(), bs>>>(pa);
-      PTB_LAUNCH_CHECK(ctx);
-      pa.tiles = p->stiles + p->natb;
-      k_pml<true, kLayerThreads, PTYA, FBA><<<dim3(p->nalr, unsigned(batch)), kLayerThreads,
-                                              pml_smem<true, PTYA, FBA>(), bs>>>(pa);
-      PTB_LAUNCH_CHECK(ctx);
       PmlArgs pb = a;
       pb.ui = mid[0], pb.vi = mid[1], pb.pxi = mid[2], pb.pyi = mid[3];
       pb.uo = bufs[1 - cur][0], pb.vo = bufs[1 - cur][1], pb.pxo = bufs[1 - cur][2], pb.pyo = bufs[1 - cur][3];
-      pb.tiles = p->stiles + p->natb + p->nalr;
-      k_pml<true, kLayerThreads, FBB, PTX><<<dim3(p->nbtb, unsigned(batch)), kLayerThreads,
-                                             pml_smem<true, FBB, PTX>(), bs>>>(pb);
-      PTB_LAUNCH_CHECK(ctx);
-      pb.tiles = p->stiles + p->natb + p->nalr + p->nbtb;
-      k_pml<true, kLayerThreads, PTYB, FBB><<<dim3(p->nblr, unsigned(batch)), kLayerThreads,
-                                              pml_smem<true, PTYB, FBB>(), bs>>>(pb);
-      PTB_LAUNCH_CHECK(ctx);
+      auto run = [&](const std::vector<BandLaunch>& pass, PmlArgs& args) {
+        for (size_t i = 0; i < pass.size(); ++i) {
+          const BandLaunch& bl = pass[i];
+          if (bl.count == 0) continue;
+          args.tiles = p->stiles + bl.first;
+          args.ylim = bl.ylim;
+          args.xlim = bl.xlim;
+          void* kargs[] = {&args};
+          const BandKernel& bk = band_kernels()[bl.kern];
+          PTB_CUDA_CHECK(cudaLaunchKernel(bk.fn, dim3(unsigned(bl.count), unsigned(batch)), dim3(kLayerThreads), kargs,
+                                          bk.smem, lanes ? p->bstream[i % NBS] : st));
+          PTB_LAUNCH_CHECK(ctx);
+        }
+      };
+      // every band stream sees all of the pass's launches before the next pass / the join
+      auto barrier = [&](bool join) {
+        if (!lanes) return;
+        for (int i = 0; i < NBS; ++i) PTB_CUDA_CHECK(cudaEventRecord(p->bev[i], p->bstream[i]));
+        for (int i = 0; i < NBS; ++i) {
+          if (join) {
+            PTB_CUDA_CHECK(cudaStreamWaitEvent(st, p->bev[i], 0));
+          } else {
+            for (int j = 0; j < NBS; ++j)
+              if (j != i) PTB_CUDA_CHECK(cudaStreamWaitEvent(p->bstream[j], p->bev[i], 0));
+          }
+        }
+      };
+      run(p->pass_a, pa);
+      barrier(false);
+      run(p->pass_b, pb);
       wave_rect_fast(ctx, st, 2 * PS, p->prm, batch, bufs[cur][0], bufs[cur][1], bufs[1 - cur][0], bufs[1 - cur][1],
                      a.kx, a.flags, p->sy0, p->sny, p->sx0, p->snx);
-      if (lanes) {
-        PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_join, ctx->lane));
-        PTB_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->lane_join, 0));
-      }
+      barrier(true);
       cur = 1 - cur;
       continue;
     }
@@ -1265,23 +1329,35 @@ ptb_status ptb_pml_create(ptb_context* ctx, const ptb_grid* grid, const double* 
           const long sy0 = ylo + SUPER_MARGIN, sy1 = long(ny) - yhi - SUPER_MARGIN;
           const long sx0 = (xlo + SUPER_MARGIN + 1) & ~1L, sx1 = (long(nx) - xhi - SUPER_MARGIN) & ~1L;
           if (sy0 <= FBB && long(ny) - sy1 <= FBB && sx0 <= FBB && long(nx) - sx1 <= FBB && sy1 - sy0 >= 4 * FBA &&
-              sx1 - sx0 >= 4 * FBA) {
+              sx1 - sx0 >= 4 * FBA && long(nx) >= 2 * XCA + LA && long(ny) >= 2 * FBA + LA) {
             std::vector<int2> stl;
-            auto band_tiles = [&](int fbw, int pty, int& ntb_out, int& nlr_out) {
-              const size_t before = stl.size();
-              for (long tx = 0; tx < long(nx); tx += PTX) {
-                stl.push_back(make_int2(0, int(tx)));
-                stl.push_back(make_int2(int(ny) - fbw, int(tx)));
-              }
-              ntb_out = int(stl.size() - before);
-              for (long ty = fbw; ty < long(ny) - fbw; ty += pty) {
-                stl.push_back(make_int2(int(ty), 0));
-                stl.push_back(make_int2(int(ty), int(nx) - fbw));
-              }
-              nlr_out = int(stl.size() - before) - ntb_out;
+            // one pass: corner tiles at both ends of the top and bottom bands (wc wide, xc long), mid
+            // tiles between them (wm wide, len long, clipped at nx - xc), left/right tiles between the
+            // bands' corner rows (wm wide, len long, clipped at ny - wc)
+            auto pass_tiles = [&](std::vector<ptb::BandLaunch>& pass, int kbase, int wc, int wm, int xc, int len) {
+              const int NX = int(nx), NY = int(ny);
+              int first = int(stl.size());
+              for (int tx = 0; tx < xc; tx += PTX)
+                for (int x : {tx, NX - xc + tx}) {
+                  stl.push_back(make_int2(0, x));
+                  stl.push_back(make_int2(NY - wc, x));
+                }
+              pass.push_back({kbase + 0, first, int(stl.size()) - first, 0, 0});
+              first = int(stl.size());
+              for (int tx = xc; tx < NX - xc; tx += len) stl.push_back(make_int2(0, tx));
+              pass.push_back({kbase + 1, first, int(stl.size()) - first, 0, NX - xc});
+              first = int(stl.size());
+              for (int tx = xc; tx < NX - xc; tx += len) stl.push_back(make_int2(NY - wm, tx));
+              pass.push_back({kbase + 2, first, int(stl.size()) - first, 0, NX - xc});
+              first = int(stl.size());
+              for (int ty = wc; ty < NY - wc; ty += len) stl.push_back(make_int2(ty, 0));
+              pass.push_back({kbase + 3, first, int(stl.size()) - first, NY - wc, 0});
+              first = int(stl.size());
+              for (int ty = wc; ty < NY - wc; ty += len) stl.push_back(make_int2(ty, NX - wm));
+              pass.push_back({kbase + 4, first, int(stl.size()) - first, NY - wc, 0});
             };
-            band_tiles(FBA, PTYA, p->natb, p->nalr);
-            band_tiles(FBB, PTYB, p->nbtb, p->nblr);
+            pass_tiles(p->pass_a, ptb::BK_A_CORNER, FBA, FBM, XCA, LA);
+            pass_tiles(p->pass_b, ptb::BK_B_CORNER, FBB, FBB, XCB, LB);
             p->super = 1;
             p->sy0 = int(sy0);
             p->sny = int(sy1 - sy0);
@@ -1328,6 +1404,11 @@ ptb_status ptb_pml_destroy(ptb_pml* p) {
     cudaFree(p->tiles);
     cudaFree(p->ftiles);
     cudaFree(p->stiles);
+    if (p->bfork) cudaEventDestroy(p->bfork);
+    for (int i = 0; i < ptb_pml::NBS; ++i) {
+      if (p->bstream[i]) cudaStreamDestroy(p->bstream[i]);
+      if (p->bev[i]) cudaEventDestroy(p->bev[i]);
+    }
     delete p;
   });
 }
