@@ -627,7 +627,7 @@ def pml_section(B, ctx, tflops_peak, hbm_peak, rank=0, world=1, dist=None):
                            "bytes_per_update": bytes_per_update,
                            "frac_hbm_at_10B_per_update": ups * 10.0 / (hbm_peak * 1e9),
                            "kernel": "super-pass of 8 steps: k_wave2<8> on the interior rectangle + k_pml<layer> band "
-                                     "tiles (halo 9) in two 4-step passes (51- and 42-cell bands)"},
+                                     "tiles in two 4-step passes (47/51- and 42-cell bands, halo 9 / 5 on undamped inner sides)"},
             "theta_parareal": {"N": spec["n_couplings"], "K": spec["iterations"], "tol": spec["tol"], "ranks": world,
                                "s_per_iteration": float(np.median(its)) / 1e3, "iteration_ms": [round(x, 2) for x in its],
                                "corrector_rank": [int(x) for x in r["rank"]],
