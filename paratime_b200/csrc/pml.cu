@@ -560,11 +560,6 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     return !(e && std::atoi(e) == 0);
   }();
   const bool lanes = lanes_env && p->frame;
-  if (lanes && !ctx->lane) {
-    PTB_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->lane, cudaStreamNonBlocking));
-    PTB_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_fork, cudaEventDisableTiming));
-    PTB_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_join, cudaEventDisableTiming));
-  }
   const bool super = p->super && steps >= size_t(2 * PS) && pml_wave_enabled() && pml_frame_enabled() &&
                      pml_super_enabled();
   double* mid[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -577,6 +572,14 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     const size_t mb = p->mid_batch * n;
     for (int f = 0; f < 4; ++f) mid[f] = m + f * mb;
   }
+  constexpr int NBS = ptb_pml::NBS;
+  if (lanes && !p->bfork) {
+    PTB_CUDA_CHECK(cudaEventCreateWithFlags(&p->bfork, cudaEventDisableTiming));
+    for (int i = 0; i < NBS; ++i) {
+      PTB_CUDA_CHECK(cudaStreamCreateWithFlags(&p->bstream[i], cudaStreamNonBlocking));
+      PTB_CUDA_CHECK(cudaEventCreateWithFlags(&p->bev[i], cudaEventDisableTiming));
+    }
+  }
   int cur = 0;
   for (size_t done = 0; done < steps;) {
     if (super && steps - done >= size_t(2 * PS)) {
@@ -588,14 +591,6 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
       done += 2 * PS;
       a.flags = done == steps ? flags : nullptr;
       a.steps = PS;
-      constexpr int NBS = ptb_pml::NBS;
-      if (lanes && !p->bfork) {
-        PTB_CUDA_CHECK(cudaEventCreateWithFlags(&p->bfork, cudaEventDisableTiming));
-        for (int i = 0; i < NBS; ++i) {
-          PTB_CUDA_CHECK(cudaStreamCreateWithFlags(&p->bstream[i], cudaStreamNonBlocking));
-          PTB_CUDA_CHECK(cudaEventCreateWithFlags(&p->bev[i], cudaEventDisableTiming));
-        }
-      }
       if (lanes) {
         PTB_CUDA_CHECK(cudaEventRecord(p->bfork, st));
         for (int i = 0; i < NBS; ++i) PTB_CUDA_CHECK(cudaStreamWaitEvent(p->bstream[i], p->bfork, 0));
@@ -660,25 +655,31 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
       // The three launches of a pass read the same input and write disjoint parts of the output:
       // the band tiles (one latency-bound CTA per SM) go to the context's lane stream and overlap the
       // interior's wavefront CTAs (fork/join by events, so `st` still orders the passes).
-      cudaStream_t bs = st;
+      // band tiles: top/bottom and left/right on their own streams (independent one-CTA-per-SM
+      // kernels; on a small grid each is one CTA latency long), the interior on the caller's
+      cudaStream_t bs0 = st, bs1 = st;
       if (lanes) {
-        PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_fork, st));
-        PTB_CUDA_CHECK(cudaStreamWaitEvent(ctx->lane, ctx->lane_fork, 0));
-        bs = ctx->lane;
+        PTB_CUDA_CHECK(cudaEventRecord(p->bfork, st));
+        PTB_CUDA_CHECK(cudaStreamWaitEvent(p->bstream[0], p->bfork, 0));
+        PTB_CUDA_CHECK(cudaStreamWaitEvent(p->bstream[1], p->bfork, 0));
+        bs0 = p->bstream[0];
+        bs1 = p->bstream[1];
       }
       a.tiles = p->ftiles;
       k_pml<true, kLayerThreads, FB, PTX><<<dim3(p->ntb, unsigned(batch)), kLayerThreads, pml_smem<true, FB, PTX>(),
-                                            bs>>>(a);
+                                            bs0>>>(a);
       PTB_LAUNCH_CHECK(ctx);
       a.tiles = p->ftiles + p->ntb;
       k_pml<true, kLayerThreads, PTY, FB><<<dim3(p->nlr, unsigned(batch)), kLayerThreads, pml_smem<true, PTY, FB>(),
-                                            bs>>>(a);
+                                            bs1>>>(a);
       PTB_LAUNCH_CHECK(ctx);
       wave_rect_fast(ctx, st, ns, p->prm, batch, a.ui, a.vi, a.uo, a.vo, a.kx, a.flags, p->fy0, p->fny, p->fx0,
                      p->fnx);
       if (lanes) {
-        PTB_CUDA_CHECK(cudaEventRecord(ctx->lane_join, ctx->lane));
-        PTB_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->lane_join, 0));
+        for (int i = 0; i < 2; ++i) {
+          PTB_CUDA_CHECK(cudaEventRecord(p->bev[i], p->bstream[i]));
+          PTB_CUDA_CHECK(cudaStreamWaitEvent(st, p->bev[i], 0));
+        }
       }
       cur = 1 - cur;
       continue;
@@ -972,6 +973,7 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
   ProcWork* pw = theta ? &context_proc_work(ctx) : nullptr;
   const ptb_grid& cgr = coarse->grid;
   // theta: fit the corrector on this iteration's snapshots, then the replicated coarse sweep -> cd
+  HostProf* hp_it = nullptr;  // the running iteration's PTB_PROF timeline
   auto theta_iteration = [&](int k) {
     std::vector<int32_t> hf(2 * N);
     PTB_CUDA_CHECK(cudaMemcpyAsync(hf.data(), gff, N * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -1011,6 +1013,7 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
       energy_components(ew, cgr, th->scheme, N - 1, cold.f(0, 1), cold.f(1, 1), nc, nullptr, ccs, cmp, rows, mold + 1);
     }
     const double* Z = r > 0 ? dl + 2 * nc : nullptr;
+    if (hp_it) hp_it->mark("pml theta:  fit, Z, old terms");
     PTB_CUDA_CHECK(cudaMemsetAsync(swf, 0, (N + 1) * sizeof(int32_t), st));
     // n = 1: next[1] = fine_next[1] (both corrected terms cancel, parareal.cpp:315-318): d_1 = 0
     for (int f = 0; f < 4; ++f) {
@@ -1035,6 +1038,8 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
     }
   };
   for (int k = 1; k <= K; ++k) {
+    HostProf hp_(st);
+    hp_it = &hp_;
     PTB_CUDA_CHECK(cudaEventRecord(e0, st));
     // parallel stage on the own couplings: next[n] = F(cur[n-1]), old[n] = C(R cur[n-1])
     if (L) {
@@ -1054,6 +1059,7 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
                     theta ? cfl : nullptr);
       for (int f = 0; f < 4; ++f) restrict_fields(t, L, nxt.f(f, 1), crf.f(f, a - 1));
     }
+    hp_.mark("pml theta: parallel stage");
     if (world > 1) {  // one all-gather of the coarse payload (theta: and the stage flags)
       for (int f = 0; f < 4; ++f) {
         cpy(own + size_t(f) * chunk * nc, cold.f(f, a - 1), L * nc);
@@ -1101,9 +1107,12 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
       }
     }
     }
+    hp_.mark("pml theta: fit + sweep");
     // own combine: next[n] = fine_next[n] + I(d_n), in chunks of slices (u, udot: fused into the
     // interpolation; px, py: the correction masked to the layer)
-    for (int f = 0; f < 4; ++f)
+    // (theta leaves px, py uncorrected: their d is zero — or NaN together with d_u, d_udot on a
+    // flagged coupling, which the clamp below catches through u — so only u, udot are combined)
+    for (int f = 0; f < (theta ? 2 : 4); ++f)
       for (size_t c0 = 0; c0 < L; c0 += ichunk) {
         const size_t m = std::min(ichunk, L - c0);
         if (f < 2) {
@@ -1114,6 +1123,7 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
           PTB_LAUNCH_CHECK(ctx);
         }
       }
+    hp_.mark("pml theta: combine");
     // non-finite iterates: flag and clamp to the previous iterate (parareal.cpp:117-124)
     if (L) {
       PTB_CUDA_CHECK(cudaMemsetAsync(bad, 0, (L + 1) * sizeof(int32_t), st));
@@ -1135,6 +1145,7 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
       for (int f = 0; f < 4; ++f)
         comm->shift_right(nxt.f(f, L), nf * sizeof(double), has_next, nxt.f(f, 0), nf * sizeof(double), has_prev, st);
     }
+    hp_.mark("pml theta: flags + clamp");
     PTB_CUDA_CHECK(cudaEventRecord(e1, st));
     // metric (outside the timed body): L2 distance of [u; udot] to the serial fine run
     if (err_out) {
