@@ -504,8 +504,11 @@ bool pml_super_enabled() {
   return !(e && std::atoi(e) == 0);
 }
 
+// `src` (optional): the input state (u, udot, px, py); the result still goes to u, v, px, py, whose
+// px, py must then already be zero off the layer (the interior kernels never write them).  Saves
+// the caller a copy of the whole state when it keeps the input.
 void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v, double* px, double* py,
-                   int32_t* flags) {
+                   int32_t* flags, const double* const* src = nullptr) {
   ptb_context* ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   if (batch == 0 || steps == 0) return;
@@ -581,6 +584,7 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     }
   }
   int cur = 0;
+  bool first = true;  // the first pass reads `src` when given
   for (size_t done = 0; done < steps;) {
     if (super && steps - done >= size_t(2 * PS)) {
       // One super-pass = 2 PS steps.  Band pass A (PS steps, bands FBA wide) reads the input and writes
@@ -595,9 +599,12 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
         PTB_CUDA_CHECK(cudaEventRecord(p->bfork, st));
         for (int i = 0; i < NBS; ++i) PTB_CUDA_CHECK(cudaStreamWaitEvent(p->bstream[i], p->bfork, 0));
       }
+      const double* in[4];
+      for (int f = 0; f < 4; ++f) in[f] = (first && src) ? src[f] : bufs[cur][f];
+      first = false;
       PmlArgs pa = a;
       pa.flags = nullptr;
-      pa.ui = bufs[cur][0], pa.vi = bufs[cur][1], pa.pxi = bufs[cur][2], pa.pyi = bufs[cur][3];
+      pa.ui = in[0], pa.vi = in[1], pa.pxi = in[2], pa.pyi = in[3];
       pa.uo = mid[0], pa.vo = mid[1], pa.pxo = mid[2], pa.pyo = mid[3];
       PmlArgs pb = a;
       pb.ui = mid[0], pb.vi = mid[1], pb.pxi = mid[2], pb.pyi = mid[3];
@@ -632,7 +639,7 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
       run(p->pass_a, pa);
       barrier(false);
       run(p->pass_b, pb);
-      wave_rect_fast(ctx, st, 2 * PS, p->prm, batch, bufs[cur][0], bufs[cur][1], bufs[1 - cur][0], bufs[1 - cur][1],
+      wave_rect_fast(ctx, st, 2 * PS, p->prm, batch, in[0], in[1], bufs[1 - cur][0], bufs[1 - cur][1],
                      a.kx, a.flags, p->sy0, p->sny, p->sx0, p->snx);
       barrier(true);
       cur = 1 - cur;
@@ -640,10 +647,11 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     }
     const int ns = int(std::min<size_t>(PS, steps - done));
     done += ns;
-    a.ui = bufs[cur][0];
-    a.vi = bufs[cur][1];
-    a.pxi = bufs[cur][2];
-    a.pyi = bufs[cur][3];
+    a.ui = (first && src) ? src[0] : bufs[cur][0];
+    a.vi = (first && src) ? src[1] : bufs[cur][1];
+    a.pxi = (first && src) ? src[2] : bufs[cur][2];
+    a.pyi = (first && src) ? src[3] : bufs[cur][3];
+    first = false;
     a.uo = bufs[1 - cur][0];
     a.vo = bufs[1 - cur][1];
     a.pxo = bufs[1 - cur][2];
@@ -652,10 +660,8 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
     a.flags = done == steps ? flags : nullptr;
     if (p->frame && (ns == 4 || ns == 2 || ns == 1) && pml_wave_enabled() && pml_frame_enabled()) {
       // frame mode: the interior rectangle through k_wave2, the bands through band-shaped layer tiles
-      // The three launches of a pass read the same input and write disjoint parts of the output:
-      // the band tiles (one latency-bound CTA per SM) go to the context's lane stream and overlap the
-      // interior's wavefront CTAs (fork/join by events, so `st` still orders the passes).
-      // band tiles: top/bottom and left/right on their own streams (independent one-CTA-per-SM
+      // The three launches of a pass read the same input and write disjoint parts of the output.
+      // Band tiles: top/bottom and left/right on their own streams (independent one-CTA-per-SM
       // kernels; on a small grid each is one CTA latency long), the interior on the caller's
       cudaStream_t bs0 = st, bs1 = st;
       if (lanes) {
@@ -1037,23 +1043,24 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
       PTB_LAUNCH_CHECK(ctx);
     }
   };
+  for (int f = 2; f < 4; ++f) PTB_CUDA_CHECK(cudaMemsetAsync(nxt.f(f, 0), 0, (L + 1) * nf * sizeof(double), st));
   for (int k = 1; k <= K; ++k) {
     HostProf hp_(st);
     hp_it = &hp_;
     PTB_CUDA_CHECK(cudaEventRecord(e0, st));
     // parallel stage on the own couplings: next[n] = F(cur[n-1]), old[n] = C(R cur[n-1])
     if (L) {
-      for (int f = 0; f < 4; ++f) {
-        cpy(nxt.f(f, 1), cur.f(f, 0), L * nf);
-        restrict_fields(t, L, cur.f(f, 0), cold.f(f, a - 1));
-      }
+      for (int f = 0; f < 4; ++f) restrict_fields(t, L, cur.f(f, 0), cold.f(f, a - 1));
+      // next[n] = F(cur[n-1]) straight from cur into nxt (no copy of the state; nxt's px, py are
+      // zero off the layer: zeroed before the first iteration, valid iterates afterwards)
+      const double* fsrc[4] = {cur.f(0, 0), cur.f(1, 0), cur.f(2, 0), cur.f(3, 0)};
       if (theta) {
         PTB_CUDA_CHECK(cudaMemsetAsync(ffl, 0, 2 * (chunk + 1) * sizeof(int32_t), st));
-        pml_propagate(fine, fine->steps, L, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), ffl);
+        pml_propagate(fine, fine->steps, L, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), ffl, fsrc);
         k_or_flags<<<1, 256, 0, st>>>(L, ffl, flags + 1);
         PTB_LAUNCH_CHECK(ctx);
       } else {
-        pml_propagate(fine, fine->steps, L, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), flags + 1);
+        pml_propagate(fine, fine->steps, L, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), flags + 1, fsrc);
       }
       pml_propagate(coarse, coarse->steps, L, cold.f(0, a - 1), cold.f(1, a - 1), cold.f(2, a - 1), cold.f(3, a - 1),
                     theta ? cfl : nullptr);
