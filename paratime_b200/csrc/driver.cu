@@ -758,12 +758,15 @@ struct Driver {
   // parallel stage on own slices: fine_next[n] = F(cur[n-1]), coarse_next[n] = C(R cur[n-1])
   void parallel_stage() {
     if (!L) return;
-    copy(FU(a), CU(a - 1), L * nf);
-    copy(FV(a), CV(a - 1), L * nf);
     int32_t* ffo = fl(ff) + (a - 1);
     int32_t* cfo = fl(cf) + (a - 1);
     PTB_CUDA_CHECK(cudaMemsetAsync(ffo, 0, L * sizeof(int32_t), st()));
-    propagate(pf, pf->steps, L, FU(a), FV(a), ffo, s.mode);
+    // fine_next[n] = F(cur[n-1]) read straight from cur (the wavefront path's first pass; no copy)
+    LaunchSlot fs;
+    fs.stream = st();
+    fs.src_u = CU(a - 1);
+    fs.src_v = CV(a - 1);
+    propagate(pf, pf->steps, L, FU(a), FV(a), ffo, s.mode, &fs);
     nan_where(nf, L, ffo, nullptr, nullptr, FU(a), FV(a));
     restrict_fields(tr, L, CU(a - 1), slot(kn_u, a, nc));
     restrict_fields(tr, L, CV(a - 1), slot(kn_v, a, nc));

@@ -1390,7 +1390,8 @@ void wave_propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, d
     double* lv = sv + lane * lane_stride;
     double* hu = u + b0 * n;
     double* hv = v + b0 * n;
-    const double *ci = hu, *cvi = hv;
+    const double* ci = slot.src_u ? slot.src_u + b0 * n : hu;
+    const double* cvi = slot.src_u ? slot.src_v + b0 * n : hv;
     for (size_t k = 0; k < passes.size(); ++k) {
       const bool to_scratch = (k % 2) == 0;
       double* uo = to_scratch ? lu : hu;
@@ -1473,6 +1474,13 @@ void propagate(ptb_propagator* pr, size_t steps, size_t batch, double* u, double
   const bool exact = mode == PTB_MODE_EXACT;
   const StepParams& p = pr->prm;
   const size_t n = pr->n;
+  if (slot.src_u && !(n > 4096 && !cluster_size(p, n, batch) && p.dim == 2)) {
+    // every family but the wavefront works in place: copy the source state first
+    const size_t total = batch * n;
+    k_copy2<<<grid_for(ctx, total, 256), 256, 0, slot.stream>>>(total, slot.src_u, slot.src_v, u, v);
+    PTB_LAUNCH_CHECK(ctx);
+    slot.src_u = slot.src_v = nullptr;
+  }
   if (n <= 4096) {
     SmallArgs a{p, int(n), int(steps), u, v, exact ? pr->c2 : pr->kx, flags};
     const cudaStream_t st = slot.stream;

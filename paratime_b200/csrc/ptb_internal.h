@@ -228,6 +228,10 @@ struct LaunchSlot {
   cudaStream_t stream = nullptr;
   double* su = nullptr;
   double* sv = nullptr;
+  // optional input state: propagate() then reads (src_u, src_v) and writes (u, v) — the wavefront
+  // path's first pass reads the source directly, the other kernel families copy it first
+  const double* src_u = nullptr;
+  const double* src_v = nullptr;
 };
 
 // propagate.cu
