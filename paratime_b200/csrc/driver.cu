@@ -84,15 +84,14 @@ __global__ void k_sweep_tail(size_t n, const int32_t* f0, const int32_t* f1, con
   }
 }
 
-__global__ void k_nan_where(size_t n, size_t batch, const int32_t* f0, const int32_t* f1, const int32_t* f2,
-                            double* u, double* v) {
-  GRID_STRIDE(e, n * batch) {
-    const size_t b = e / n;
-    const bool bad = (f0 && f0[b]) || (f1 && f1[b]) || (f2 && f2[b]);
-    if (bad) {
-      u[e] = CUDART_NAN;
-      if (v) v[e] = CUDART_NAN;
-    }
+// slice blockIdx.y: a clean slice's CTAs leave at once (the flags are almost always clean)
+__global__ void k_nan_where(size_t n, const int32_t* f0, const int32_t* f1, const int32_t* f2, double* u, double* v) {
+  const size_t b = blockIdx.y;
+  const bool bad = (f0 && f0[b]) || (f1 && f1[b]) || (f2 && f2[b]);
+  if (!bad) return;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    u[b * n + i] = CUDART_NAN;
+    if (v) v[b * n + i] = CUDART_NAN;
   }
 }
 
@@ -473,7 +472,12 @@ struct Driver {
   void nan_where(size_t n, size_t batch, const int32_t* f0, const int32_t* f1, const int32_t* f2, double* u,
                  double* v) {
     if (!n || !batch) return;
-    k_nan_where<<<blocks(ctx, n * batch), 256, 0, st()>>>(n, batch, f0, f1, f2, u, v);
+    for (size_t b0 = 0; b0 < batch; b0 += 65535) {  // grid.y limit
+      const size_t nb = std::min<size_t>(65535, batch - b0);
+      const unsigned gx = unsigned(std::min<size_t>((n + 255) / 256, 64));
+      k_nan_where<<<dim3(gx, unsigned(nb)), 256, 0, st()>>>(n, f0 ? f0 + b0 : nullptr, f1 ? f1 + b0 : nullptr,
+                                                         f2 ? f2 + b0 : nullptr, u + b0 * n, v ? v + b0 * n : nullptr);
+    }
     PTB_LAUNCH_CHECK(ctx);
   }
   template <typename T>
