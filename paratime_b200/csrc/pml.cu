@@ -751,12 +751,20 @@ __global__ void k_aux_mask(size_t total, int ny, int nx, const double* __restric
 }
 // finalize_iteration (parareal.cpp:117-124) on the layered state: slice s of `next` with any
 // non-finite entry in its four fields is flagged (bad[s], and the divergence flags) ...
+// (px, py null: their finiteness is known already — `known_bad`, the fine stage's flag of the slice,
+// whose px, py the iterate carries unchanged)
 __global__ void __launch_bounds__(256) k_state_bad(size_t n, const double* u, const double* v, const double* px,
-                                                    const double* py, int32_t* bad, int32_t* flags) {
+                                                    const double* py, const int32_t* known_bad, int32_t* bad,
+                                                    int32_t* flags) {
   const size_t o = size_t(blockIdx.y) * n;
-  bool ok = true;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
-    ok &= isfinite(u[o + i]) && isfinite(v[o + i]) && isfinite(px[o + i]) && isfinite(py[o + i]);
+  bool ok = !(known_bad && known_bad[blockIdx.y]);
+  if (px) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+      ok &= isfinite(u[o + i]) && isfinite(v[o + i]) && isfinite(px[o + i]) && isfinite(py[o + i]);
+  } else {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+      ok &= isfinite(u[o + i]) && isfinite(v[o + i]);
+  }
   if (__syncthreads_or(!ok) && threadIdx.x == 0) {
     atomicOr(bad + blockIdx.y, 1);
     atomicOr(flags + blockIdx.y, 1);
@@ -1135,7 +1143,10 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
     if (L) {
       PTB_CUDA_CHECK(cudaMemsetAsync(bad, 0, (L + 1) * sizeof(int32_t), st));
       const dim3 g(unsigned(std::min<size_t>((nf + 255) / 256, 64)), unsigned(L));
-      k_state_bad<<<g, 256, 0, st>>>(nf, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), bad, flags + 1);
+      if (theta)  // px, py are fine_next's, checked by the fine stage (ffl)
+        k_state_bad<<<g, 256, 0, st>>>(nf, nxt.f(0, 1), nxt.f(1, 1), nullptr, nullptr, ffl, bad, flags + 1);
+      else
+        k_state_bad<<<g, 256, 0, st>>>(nf, nxt.f(0, 1), nxt.f(1, 1), nxt.f(2, 1), nxt.f(3, 1), nullptr, bad, flags + 1);
       PTB_LAUNCH_CHECK(ctx);
       for (int f = 0; f < 4; ++f) {
         hptr[f] = nxt.f(f, 1);
