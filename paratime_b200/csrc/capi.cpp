@@ -1,6 +1,7 @@
 // extern "C" boundary of libparatime_b200 (declared in include/paratime_b200.h).
 // Every entry point converts exceptions to a ptb_status plus a thread-local message.
 
+#include <chrono>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -40,6 +41,9 @@ void* DeviceBuffer::get(size_t need) {
     size_t want = need;
     if (bytes) want = std::max(need, 2 * bytes);
     want = (want + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+    static const bool prof = std::getenv("PTB_PROF") != nullptr;  // diagnostics: slow (re)allocations
+    const auto t0 = std::chrono::steady_clock::now();
+    const size_t old = bytes;
     if (ptr) PTB_CUDA_CHECK(cudaFree(ptr));
     ptr = nullptr;
     if (cudaMalloc(&ptr, want) != cudaSuccess) {  // fall back to the exact size under pressure
@@ -48,6 +52,12 @@ void* DeviceBuffer::get(size_t need) {
       PTB_CUDA_CHECK(cudaMalloc(&ptr, want));
     }
     bytes = want;
+    if (prof) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > 2.0)
+        std::fprintf(stderr, "[ptb prof] DeviceBuffer %zu -> %zu MiB: cudaFree + cudaMalloc %.1f ms\n", old >> 20,
+                     want >> 20, ms);
+    }
   }
   return ptr;
 }

@@ -504,6 +504,23 @@ bool pml_super_enabled() {
   return !(e && std::atoi(e) == 0);
 }
 
+// Size the propagator's ping-pong scratch (and the super-pass's third buffer set) for `batch` slices
+// now, so that a later, larger batch does not reallocate them inside a timed region (a cudaFree +
+// cudaMalloc pair of this size synchronises the device and was measured at 2-700 ms).
+void pml_reserve(ptb_pml* p, size_t batch) {
+  if (batch == 0) return;
+  const size_t fb = batch * p->n * sizeof(double);
+  if (p->scratch_batch < batch) {
+    double* s = static_cast<double*>(p->scratch.get(4 * fb));
+    PTB_CUDA_CHECK(cudaMemsetAsync(s, 0, 4 * fb, p->ctx->stream));  // phi planes: zero off the layer, for good
+    p->scratch_batch = batch;
+  }
+  if (p->super && p->mid_batch < batch) {
+    p->mid.get(4 * fb);
+    p->mid_batch = batch;
+  }
+}
+
 // `src` (optional): the input state (u, udot, px, py); the result still goes to u, v, px, py, whose
 // px, py must then already be zero off the layer (the interior kernels never write them).  Saves
 // the caller a copy of the whole state when it keeps the input.
@@ -514,11 +531,7 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
   if (batch == 0 || steps == 0) return;
   const int ny = int(p->grid.n[0]), nx = int(p->grid.n[1]);
   const size_t n = p->n, fb = batch * n * sizeof(double);
-  if (p->scratch_batch < batch) {
-    double* s = static_cast<double*>(p->scratch.get(4 * fb));
-    PTB_CUDA_CHECK(cudaMemsetAsync(s, 0, 4 * fb, st));  // phi planes: zero off the layer, for good
-    p->scratch_batch = batch;
-  }
+  pml_reserve(p, batch);
   double* s = static_cast<double*>(p->scratch.ptr);
   const size_t sb = p->scratch_batch * n;
   double* bufs[2][4] = {{u, v, px, py}, {s, s + sb, s + 2 * sb, s + 3 * sb}};
@@ -567,10 +580,6 @@ void pml_propagate(ptb_pml* p, size_t steps, size_t batch, double* u, double* v,
                      pml_super_enabled();
   double* mid[4] = {nullptr, nullptr, nullptr, nullptr};
   if (super) {
-    if (p->mid_batch < batch) {
-      p->mid.get(4 * fb);
-      p->mid_batch = batch;
-    }
     double* m = static_cast<double*>(p->mid.ptr);
     const size_t mb = p->mid_batch * n;
     for (int f = 0; f < 4; ++f) mid[f] = m + f * mb;
@@ -924,6 +933,15 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
     mw = mold + N;          // 1 (+1 pad)
     idx_d = static_cast<int*>(bidx.get(N * sizeof(int)));
     require(ctx->num_sms > 0, "pml theta: context");
+    {  // the rank-sized buffers for a corrector of up to 2 N columns now: their growth inside an
+       // iteration is a cudaFree + cudaMalloc pair each (device synchronisation, measured 2-700 ms);
+       // a larger rank still grows them geometrically
+      const size_t rcap = std::min<size_t>(rows, 2 * N);
+      ProcWork& w0 = context_proc_work(ctx);
+      for (DeviceBuffer* bf : {&corr.X, &corr.Y, &w0.SX, &w0.SY}) bf->get(rows * rcap * sizeof(double));
+      bZ.get((2 * nc * rcap + 2 * nc + rcap * (N + 2)) * sizeof(double));
+      for (int i = 1; i <= 3; ++i) ew.buf[i].get(nc * rcap * 2 * sizeof(double));  // Lambda-dagger of X (complex planes)
+    }
   }
   const double* ccs = coarse->speed;
   double* sums = static_cast<double*>(bsum.get(2 * (chunk + 2) * sizeof(double)));
@@ -945,6 +963,8 @@ void pml_parareal(ptb_pml* fine, ptb_pml* coarse, ptb_transfer* t, const Comm* c
   PTB_CUDA_CHECK(cudaMemsetAsync(ini.f(3), 0, 2 * nf * sizeof(double), st));
   PTB_CUDA_CHECK(cudaMemsetAsync(flags, 0, (L + 1) * sizeof(int32_t), st));
   PTB_CUDA_CHECK(cudaMemsetAsync(cw, 0, 4 * (3 * P + 2) * nc * sizeof(double), st));
+  pml_reserve(fine, L);  // the batched stages' buffers now, not inside the first iteration
+  pml_reserve(coarse, L);
   // serial fine reference (parareal.cpp:190-199): the chain up to b-1, own states kept
   cpy_state(ini, 1, ini, 0);
   for (size_t n = 0; n < b; ++n) {
