@@ -1176,6 +1176,16 @@ struct Driver {
     double* Fp = dalloc<double>(Fm, rows * N);
     double* Gp = dalloc<double>(Gm, rows * N);
     int* idx_d = dalloc<int>(idx, N);
+    if (theta) {
+      // the rank-sized buffers for a corrector of up to 2 N columns now: inside an iteration their
+      // growth is a cudaFree + cudaMalloc pair each, which synchronises the device and was measured
+      // at 2-700 ms; a larger rank still grows them geometrically
+      const size_t rcap = std::min<size_t>(rows, 2 * N);
+      for (DeviceBuffer* bf : {&corr.X, &corr.Y, &pw.SX, &pw.SY}) bf->get(rows * rcap * sizeof(double));
+      dalloc<double>(Zu, nc * rcap);
+      dalloc<double>(Zv, nc * rcap);
+      for (int i = 1; i <= 3; ++i) ew.buf[i].get(nc * rcap * 2 * sizeof(double));  // Lambda-dagger planes
+    }
     DevCorrector dropped;
     for (int k = 1; k <= K; ++k) {
       PTB_CUDA_CHECK(cudaEventRecord(ev[0], st()));
